@@ -1,0 +1,455 @@
+"""CPU oracle for the Inf-MLLM streaming-decode hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is the *checker*, never the product.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl
+reference`` legs may import it.  The shipped path (``paper_2409_09086_b200``)
+never imports anything under ``oracle/`` and fails loudly when its CUDA
+library is missing.
+
+It restates, in NumPy float32, the reference package ``streamkv``
+(``/root/reference/pkg/src/streamkv``) for exactly the functions on the hot
+path.  Every function cites the reference file:line it
+follows.  The float32 operation sequence is kept identical to the reference
+(same NumPy/BLAS calls on the same memory layout) so that, fed the same
+inputs, the oracle reproduces the reference bit-for-bit; this is *pinned* by
+``tests/test_oracle_golden.py`` against fixtures produced by running the
+reference itself (``tests/golden/make_golden.py``).
+
+Two things the reference does not have are expressed with reference
+arithmetic, exactly as SURVEY.md 8a "divergences" prescribes:
+
+* GQA: key/value heads are repeated ``Hq // Hkv`` times before the per-head
+  attention loop (mathematically identical to grouped attention).
+* bf16 inputs: callers pass bf16-rounded values upcast to float32.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+F32 = np.float32
+I64 = np.int64
+
+
+# --------------------------------------------------------------------------
+# policy configuration / decision types
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class PolicyConfig:
+    """Mirror of ``streamkv.policies.PolicyConfig`` (policies.py:28-59)."""
+
+    recent_len: int = 32
+    relevant_budget: int = 2016
+    bias: float = 0.1
+    sink_count: int = 4
+    head_agg: str = "mean"
+
+    def __post_init__(self):  # policies.py:45-55
+        if self.recent_len < 1:
+            raise ValueError("recent_len must be >= 1")
+        if self.relevant_budget < 0:
+            raise ValueError("relevant_budget must be >= 0")
+        if self.bias < 0:
+            raise ValueError("bias must be >= 0")
+        if self.sink_count < 0:
+            raise ValueError("sink_count must be >= 0")
+        if self.head_agg not in ("mean", "max"):
+            raise ValueError(f"unknown head_agg {self.head_agg!r}")
+
+    @property
+    def budget(self) -> int:  # policies.py:57-59
+        return self.recent_len + self.relevant_budget
+
+
+@dataclass(frozen=True)
+class Decision:
+    """relevant / recent / kept index sets (policies.py:62-84)."""
+
+    relevant: np.ndarray
+    recent: np.ndarray
+    kept: np.ndarray
+
+    @staticmethod
+    def everything(n: int, recent_len: int) -> "Decision":  # policies.py:76-84
+        k = min(recent_len, n)
+        return Decision(
+            relevant=np.arange(0, n - k, dtype=I64),
+            recent=np.arange(n - k, n, dtype=I64),
+            kept=np.arange(n, dtype=I64),
+        )
+
+
+# --------------------------------------------------------------------------
+# rolling relevance window
+# --------------------------------------------------------------------------
+
+
+class RowWindow:
+    """Rolling list of the last ``capacity`` head-aggregated rows.
+
+    Follows ``AttentionWindow`` (policies.py:87-127): push drops the oldest
+    row beyond capacity (107-115); rows may not shrink between evictions
+    (111-112); ``remap`` keeps, per row, the kept indices that row covers
+    (117-124).
+    """
+
+    def __init__(self, capacity: int):
+        if capacity < 1:
+            raise ValueError("window capacity must be >= 1")
+        self.capacity = capacity
+        self.rows: List[np.ndarray] = []
+
+    def __len__(self) -> int:
+        return len(self.rows)
+
+    def push(self, row) -> None:
+        r = np.asarray(row, dtype=F32)
+        if r.ndim != 1 or r.size == 0:
+            raise ValueError("row must be a non-empty vector")
+        if self.rows and r.size < self.rows[-1].size:
+            raise ValueError("row column count may not shrink between evictions")
+        self.rows.append(r)
+        while len(self.rows) > self.capacity:
+            self.rows.pop(0)
+
+    def remap(self, kept) -> None:
+        idx = np.asarray(kept, dtype=I64)
+        self.rows = [row[idx[idx < row.size]] for row in self.rows]
+
+    def clear(self) -> None:
+        self.rows = []
+
+
+# --------------------------------------------------------------------------
+# Algorithm-1 selection pieces (bit-exact float32 contract)
+# --------------------------------------------------------------------------
+
+
+def window_scores(window: RowWindow, n: int, l: int) -> np.ndarray:
+    """policies.py:130-147: oldest->newest f32 column sums, then / f32(m)."""
+    if len(window) == 0:
+        raise ValueError("attention window is empty")
+    if n <= l:
+        raise ValueError(f"no scorable columns: n={n} <= l={l}")
+    cols = n - l
+    total = np.zeros(cols, dtype=F32)
+    for row in window.rows:
+        upto = min(row.size, cols)
+        total[:upto] += row[:upto]
+    return total / F32(len(window))
+
+
+def age_bias(n: int, l: int, b: float) -> np.ndarray:
+    """policies.py:150-162: d = f32(b)/f32(cols); bias[c] = (-d) * f32(cols-1-c)."""
+    if n <= l:
+        raise ValueError(f"no scorable columns: n={n} <= l={l}")
+    if b < 0:
+        raise ValueError("bias must be >= 0")
+    cols = n - l
+    step = F32(b) / F32(cols)
+    ages = np.arange(cols - 1, -1, -1, dtype=F32)
+    return (-step) * ages
+
+
+def top_k_newer(scores, k: int) -> np.ndarray:
+    """policies.py:165-181: k largest, ties toward the larger index, ascending."""
+    s = np.asarray(scores, dtype=F32)
+    if k < 0:
+        raise ValueError("k must be >= 0")
+    if k == 0:
+        return np.empty(0, dtype=I64)
+    if k >= s.size:
+        return np.arange(s.size, dtype=I64)
+    idx = np.arange(s.size, dtype=I64)
+    order = np.lexsort((-idx, -s))  # primary: score desc; secondary: index desc
+    return np.sort(order[:k])
+
+
+def biased_scores(window: RowWindow, n: int, cfg: PolicyConfig) -> np.ndarray:
+    """The array Algorithm 1 ranks (policies.py:196-197)."""
+    return window_scores(window, n, cfg.recent_len) + age_bias(n, cfg.recent_len, cfg.bias)
+
+
+def saddle_decide(window: RowWindow, n: int, cfg: PolicyConfig) -> Decision:
+    """``inf_mllm_decide`` (policies.py:184-201)."""
+    if len(window) == 0:
+        raise ValueError("attention window is empty")
+    l, r = cfg.recent_len, cfg.relevant_budget
+    if n <= r + l:
+        return Decision.everything(n, l)
+    relevant = top_k_newer(biased_scores(window, n, cfg), r)
+    recent = np.arange(n - l, n, dtype=I64)
+    return Decision(relevant=relevant, recent=recent, kept=np.concatenate([relevant, recent]))
+
+
+def head_mean(per_head: np.ndarray, how: str = "mean") -> np.ndarray:
+    """``aggregate_heads`` (policies.py:259-265)."""
+    if how == "mean":
+        return per_head.mean(axis=0, dtype=F32)
+    if how == "max":
+        return per_head.max(axis=0)
+    raise ValueError(f"unknown head aggregation {how!r}")
+
+
+# --------------------------------------------------------------------------
+# single-query attention
+# --------------------------------------------------------------------------
+
+
+def attend_heads(keys: np.ndarray, values: np.ndarray, q: np.ndarray, scale) -> tuple:
+    """``Session._attend`` (engine.py:235-246), f32 per-head loop.
+
+    keys/values: (H, n, D) f32; q: (H, D) f32.  Returns probs (H, n) and
+    out (H, D), both f32.
+    """
+    heads, n, dim = keys.shape
+    probs = np.empty((heads, n), dtype=F32)
+    out = np.empty((heads, dim), dtype=F32)
+    scale = F32(scale)
+    for h in range(heads):
+        logits = (keys[h] @ q[h]) * scale
+        logits -= logits.max()
+        np.exp(logits, out=logits)
+        probs[h] = logits / logits.sum(dtype=F32)
+        out[h] = probs[h] @ values[h]
+    return probs, out
+
+
+# --------------------------------------------------------------------------
+# KV store
+# --------------------------------------------------------------------------
+
+
+class LayerKV:
+    """One layer's (H, cap, D) f32 key/value store plus token metadata.
+
+    Storage, growth and compaction follow ``_LayerStore`` / ``KvCache``
+    (cache.py:44-67 layout + doubling growth, 112-134 append, 136-156
+    gather_keep).  Head-major (H, cap, D) is kept so each head's keys are a
+    contiguous (n, D) block, exactly what the reference hands to BLAS.
+    """
+
+    def __init__(self, heads: int, head_dim: int):
+        self.n = 0
+        cap = 64
+        self.k = np.zeros((heads, cap, head_dim), dtype=F32)
+        self.v = np.zeros((heads, cap, head_dim), dtype=F32)
+        self.pos = np.zeros(cap, dtype=I64)
+        self.modality = np.zeros(cap, dtype=np.int8)
+        self.round_id = np.zeros(cap, dtype=np.int32)
+
+    def _grow(self) -> None:
+        cap = self.k.shape[1] * 2
+        for name in ("k", "v"):
+            old = getattr(self, name)
+            new = np.zeros((old.shape[0], cap, old.shape[2]), dtype=F32)
+            new[:, : self.n] = old[:, : self.n]
+            setattr(self, name, new)
+        for name in ("pos", "modality", "round_id"):
+            old = getattr(self, name)
+            new = np.zeros(cap, dtype=old.dtype)
+            new[: self.n] = old[: self.n]
+            setattr(self, name, new)
+
+    def append(self, k: np.ndarray, v: np.ndarray, pos: int, modality: int = 0, round_id: int = 0):
+        if self.n > 0 and pos <= self.pos[self.n - 1]:
+            raise ValueError("original_position must be strictly increasing")
+        if self.n == self.k.shape[1]:
+            self._grow()
+        self.k[:, self.n] = k
+        self.v[:, self.n] = v
+        self.pos[self.n] = pos
+        self.modality[self.n] = modality
+        self.round_id[self.n] = round_id
+        self.n += 1
+
+    def gather_keep(self, kept) -> None:
+        idx = np.asarray(kept, dtype=I64)
+        if idx.ndim != 1:
+            raise ValueError("kept must be a 1-D index set")
+        if idx.size:
+            if idx[0] < 0 or idx[-1] >= self.n:
+                raise ValueError(f"kept indices out of range [0, {self.n})")
+            if np.any(np.diff(idx) <= 0):
+                raise ValueError("kept indices must be strictly ascending")
+        m = idx.size
+        self.k[:, :m] = self.k[:, idx]
+        self.v[:, :m] = self.v[:, idx]
+        self.pos[:m] = self.pos[idx]
+        self.modality[:m] = self.modality[idx]
+        self.round_id[:m] = self.round_id[idx]
+        self.n = m
+
+    def keys(self) -> np.ndarray:
+        return self.k[:, : self.n]
+
+    def values(self) -> np.ndarray:
+        return self.v[:, : self.n]
+
+
+# --------------------------------------------------------------------------
+# composed streaming driver
+# --------------------------------------------------------------------------
+
+
+class StreamOracle:
+    """S independent streams x L layers of the reference decode+evict path.
+
+    Per decode step and layer (engine.py:264-273): append, attend over the
+    cache including the new token, head-mean row, window push.  At an
+    eviction (engine.py:310-337, called after a round's prompt
+    engine.py:350-360): ``inf_mllm_decide`` -> ``gather_keep`` ->
+    ``window.remap`` when the decision drops anything.
+
+    ``window`` is the relevance-window row count W; the reference Session ties
+    it to ``recent_len`` (engine.py:147) while the pure policy API takes it
+    freely (policies.py:98), which is how BASELINE's W=32 is expressed.
+    """
+
+    def __init__(self, streams: int, layers: int, heads_q: int, heads_kv: int, head_dim: int,
+                 cfg: PolicyConfig, window: Optional[int] = None):
+        if heads_q % heads_kv:
+            raise ValueError("heads_q must be a multiple of heads_kv")
+        self.S, self.L, self.Hq, self.Hkv, self.D = streams, layers, heads_q, heads_kv, head_dim
+        self.group = heads_q // heads_kv
+        self.cfg = cfg
+        self.W = window if window is not None else cfg.recent_len
+        self.scale = F32(1.0 / np.sqrt(head_dim))  # engine.py:150
+        self.kv = [[LayerKV(heads_kv, head_dim) for _ in range(layers)] for _ in range(streams)]
+        self.win = [[RowWindow(self.W) for _ in range(layers)] for _ in range(streams)]
+        self.pos = [0] * streams
+
+    def length(self, s: int, layer: int) -> int:
+        return self.kv[s][layer].n
+
+    def _expanded(self, s: int, layer: int):
+        st = self.kv[s][layer]
+        k, v = st.keys(), st.values()
+        if self.group > 1:
+            k = np.repeat(k, self.group, axis=0)
+            v = np.repeat(v, self.group, axis=0)
+        return k, v
+
+    def step_layer(self, layer: int, q: np.ndarray, k: np.ndarray, v: np.ndarray,
+                   streams: Optional[Sequence[int]] = None):
+        """One decode step of one layer.  q: (S,Hq,D), k/v: (S,Hkv,D) f32.
+
+        Returns out (S,Hq,D) f32 and the pushed rows (list of f32 vectors).
+        """
+        out = np.zeros((self.S, self.Hq, self.D), dtype=F32)
+        rows = []
+        for s in (range(self.S) if streams is None else streams):
+            st = self.kv[s][layer]
+            st.append(np.asarray(k[s], F32), np.asarray(v[s], F32), self.pos[s])
+            keys, vals = self._expanded(s, layer)
+            probs, o = attend_heads(keys, vals, np.asarray(q[s], F32), self.scale)
+            row = head_mean(probs, self.cfg.head_agg)
+            self.win[s][layer].push(row)
+            out[s] = o
+            rows.append(row)
+        return out, rows
+
+    def advance(self, streams: Optional[Sequence[int]] = None) -> None:
+        for s in (range(self.S) if streams is None else streams):
+            self.pos[s] += 1
+
+    def step(self, q, k, v):
+        """All layers of one token: q (L,S,Hq,D), k/v (L,S,Hkv,D)."""
+        outs = []
+        for layer in range(self.L):
+            o, _ = self.step_layer(layer, q[layer], k[layer], v[layer])
+            outs.append(o)
+        self.advance()
+        return np.stack(outs)
+
+    def decide(self, s: int, layer: int) -> Decision:
+        return saddle_decide(self.win[s][layer], self.kv[s][layer].n, self.cfg)
+
+    def scores(self, s: int, layer: int) -> np.ndarray:
+        return biased_scores(self.win[s][layer], self.kv[s][layer].n, self.cfg)
+
+    def apply(self, s: int, layer: int, kept) -> None:
+        """Compaction half of ``_evict_layer`` (engine.py:332-334)."""
+        kept = np.asarray(kept, dtype=I64)
+        if kept.size != self.kv[s][layer].n:
+            self.kv[s][layer].gather_keep(kept)
+            self.win[s][layer].remap(kept)
+
+    def evict(self):
+        """Decide + apply for every (stream, layer); returns kept[s][l]."""
+        kept = []
+        for s in range(self.S):
+            per = []
+            for layer in range(self.L):
+                d = self.decide(s, layer)
+                self.apply(s, layer, d.kept)
+                per.append(d.kept)
+            kept.append(per)
+        return kept
+
+
+# --------------------------------------------------------------------------
+# near-tie-aware kept-set comparison (north-star parity rule)
+# --------------------------------------------------------------------------
+
+
+def kept_sets_match(cpu_biased: np.ndarray, cpu_kept: np.ndarray, gpu_kept: np.ndarray,
+                    n: int, cfg: PolicyConfig, rel_tol: float = 1e-6) -> tuple:
+    """Kept sets must be identical except where the CPU biased-score gap between
+    a mismatched column and the CPU k-th score is below ``rel_tol`` relative.
+
+    Returns (ok, n_mismatched, worst_gap).
+    """
+    a = set(np.asarray(cpu_kept).tolist())
+    b = set(np.asarray(gpu_kept).tolist())
+    diff = sorted(a ^ b)
+    if not diff:
+        return True, 0, 0.0
+    if len(a) != len(b):
+        return False, len(diff), float("inf")
+    cols = n - cfg.recent_len
+    if any(i >= cols for i in diff):  # the recent window must always agree
+        return False, len(diff), float("inf")
+    s = np.asarray(cpu_biased, dtype=np.float64)
+    kth = np.sort(s)[::-1][cfg.relevant_budget - 1]
+    worst = 0.0
+    for i in diff:
+        gap = abs(s[i] - kth) / max(abs(kth), abs(s[i]), 1e-30)
+        worst = max(worst, gap)
+    return worst <= rel_tol, len(diff), worst
+
+
+# --------------------------------------------------------------------------
+# seeded synthetic inputs (BASELINE.json configs; shapes only, no datasets)
+# --------------------------------------------------------------------------
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even to bfloat16, returned as float32."""
+    a = np.ascontiguousarray(x, dtype=F32)
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = (u + 0x7FFF + lsb) >> 16 << 16
+    out = u.astype(np.uint32).view(F32).copy()
+    nan = np.isnan(a)
+    out[nan] = a[nan]
+    return out
+
+
+def synth_step(rng: np.random.Generator, streams: int, heads_q: int, heads_kv: int, head_dim: int,
+               spike_prob: float, spike_gain: float, bf16: bool):
+    """One token of q/k/v ~ N(0,1); a key spike multiplies all KV heads' key
+    of that (stream, token) by ``spike_gain`` with probability ``spike_prob``."""
+    q = rng.standard_normal((streams, heads_q, head_dim)).astype(F32)
+    k = rng.standard_normal((streams, heads_kv, head_dim)).astype(F32)
+    v = rng.standard_normal((streams, heads_kv, head_dim)).astype(F32)
+    spikes = rng.random(streams) < spike_prob
+    k[spikes] *= F32(spike_gain)
+    if bf16:
+        q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
+    return q, k, v

@@ -1,0 +1,154 @@
+"""Generate golden fixtures by running the REFERENCE implementation itself.
+
+Run in the dev container only (the reference is not present on GPU boxes):
+
+    python tests/golden/make_golden.py
+
+It imports ``streamkv`` from /root/reference/pkg/src and drives the hot path
+exactly as SURVEY.md 7.1/8c describe (KvCache.append -> Session._attend ->
+aggregate_heads -> AttentionWindow(W).push per step; every E steps
+inf_mllm_decide -> gather_keep -> remap).  Inputs come from the seeded
+recipes in ``oracle/streamkv_oracle.py`` so tests can regenerate them.  The
+outputs are written to ``tests/golden/*.npz`` and committed; the oracle is
+checked against them in ``tests/test_oracle_golden.py``.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+from streamkv.cache import KvCache, TokenMeta  # noqa: E402  (reference)
+from streamkv.engine import Session  # noqa: E402
+from streamkv.policies import (  # noqa: E402
+    AttentionWindow,
+    PolicyConfig,
+    aggregate_heads,
+    bias_vector,
+    inf_mllm_decide,
+    top_k_indices,
+    window_mean_scores,
+)
+
+from tests.golden.cases import CASES, case_inputs, kat_instances  # noqa: E402
+
+F32 = np.float32
+
+
+class _ScaleHolder:
+    def __init__(self, head_dim):
+        self._scale = F32(1.0 / np.sqrt(head_dim))
+
+
+def run_reference_case(name: str) -> dict:
+    c = CASES[name]
+    S, L, Hq, Hkv, D = c["S"], c["L"], c["Hq"], c["Hkv"], c["D"]
+    G = Hq // Hkv
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"])
+    holder = _ScaleHolder(D)
+    caches = [KvCache(L, Hkv, D) for _ in range(S)]
+    windows = [[AttentionWindow(c["W"]) for _ in range(L)] for _ in range(S)]
+    q_all, k_all, v_all = case_inputs(name)  # (T, L, S, H, D)
+    T = q_all.shape[0]
+    out_steps = []
+    outs = []
+    kept_log, score_log, evict_steps = [], [], []
+    for t in range(T):
+        step_out = np.zeros((L, S, Hq, D), dtype=F32)
+        for layer in range(L):
+            for s in range(S):
+                caches[s].append(layer, k_all[t, layer, s], v_all[t, layer, s], TokenMeta(t))
+                keys = caches[s].keys(layer)
+                vals = caches[s].values(layer)
+                if G > 1:
+                    keys = np.repeat(keys, G, axis=0)
+                    vals = np.repeat(vals, G, axis=0)
+                probs, o = Session._attend(holder, keys, vals, q_all[t, layer, s])
+                windows[s][layer].push(aggregate_heads(probs, "mean"))
+                step_out[layer, s] = o
+        if t % c["out_every"] == 0 or t == T - 1:
+            out_steps.append(t)
+            outs.append(step_out)
+        if (t + 1) % c["E"] == 0:
+            evict_steps.append(t)
+            for s in range(S):
+                for layer in range(L):
+                    n = caches[s].length(layer)
+                    if n > cfg.budget:
+                        sc = window_mean_scores(windows[s][layer], n, cfg.recent_len) + bias_vector(
+                            n, cfg.recent_len, cfg.bias
+                        )
+                    else:
+                        sc = np.zeros(0, dtype=F32)
+                    d = inf_mllm_decide(windows[s][layer], n, cfg)
+                    kept_log.append(d.kept.astype(np.int32))
+                    score_log.append(sc.astype(F32))
+                    if d.kept.size != n:
+                        caches[s].gather_keep(layer, d.kept)
+                        windows[s][layer].remap(d.kept)
+    final_keys = np.stack([np.stack([caches[s].keys(layer) for layer in range(L)]) for s in range(S)])
+    final_pos = np.stack([np.stack([caches[s].original_positions(layer) for layer in range(L)]) for s in range(S)])
+    return dict(
+        out_steps=np.asarray(out_steps, np.int32),
+        outs=np.stack(outs),
+        evict_steps=np.asarray(evict_steps, np.int32),
+        kept_off=np.cumsum([0] + [k.size for k in kept_log]).astype(np.int64),
+        kept=np.concatenate(kept_log) if kept_log else np.zeros(0, np.int32),
+        score_off=np.cumsum([0] + [s.size for s in score_log]).astype(np.int64),
+        scores=np.concatenate(score_log) if score_log else np.zeros(0, F32),
+        final_keys_sha=np.frombuffer(hashlib.sha256(final_keys.tobytes()).digest(), np.uint8),
+        final_pos=final_pos,
+    )
+
+
+def run_kats() -> dict:
+    """Algorithm-1 known answers on the acceptance-test instance recipe."""
+    kept_log, score_sha = [], []
+    for inst in kat_instances():
+        w = AttentionWindow(len(inst["rows"]))
+        for row in inst["rows"]:
+            w.push(row)
+        cfg = PolicyConfig(recent_len=inst["l"], relevant_budget=inst["r"], bias=inst["b"])
+        d = inf_mllm_decide(w, inst["n"], cfg)
+        kept_log.append(d.kept.astype(np.int32))
+        if inst["n"] > inst["l"]:
+            sc = window_mean_scores(w, inst["n"], inst["l"]) + bias_vector(inst["n"], inst["l"], inst["b"])
+        else:
+            sc = np.zeros(0, F32)
+        score_sha.append(np.frombuffer(hashlib.sha256(sc.astype(F32).tobytes()).digest(), np.uint8))
+    topk = []
+    rng = np.random.default_rng(23)
+    for _ in range(200):
+        size = int(rng.integers(1, 50))
+        scores = rng.choice([0.1, 0.2, 0.3, 0.5], size=size).astype(F32)
+        k = int(rng.integers(0, size + 1))
+        topk.append(top_k_indices(scores, k).astype(np.int32))
+    return dict(
+        kept_off=np.cumsum([0] + [k.size for k in kept_log]).astype(np.int64),
+        kept=np.concatenate(kept_log),
+        score_sha=np.stack(score_sha),
+        topk_off=np.cumsum([0] + [t.size for t in topk]).astype(np.int64),
+        topk=np.concatenate(topk),
+    )
+
+
+def main():
+    for name in CASES:
+        res = run_reference_case(name)
+        np.savez_compressed(os.path.join(HERE, f"ref_{name}.npz"), **res)
+        print(name, "evictions", res["evict_steps"].size, "kept entries", res["kept"].size)
+    kat = run_kats()
+    np.savez_compressed(os.path.join(HERE, "ref_kat_algorithm1.npz"), **kat)
+    print("kat", kat["kept_off"].size - 1)
+
+
+if __name__ == "__main__":
+    main()
