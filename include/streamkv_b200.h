@@ -1,0 +1,160 @@
+/*
+ * streamkv_b200 -- C ABI of the B200 (sm_100a) Inf-MLLM streaming-decode hot path.
+ *
+ * The reference (`streamkv`, pure Python/NumPy) has no FFI; its boundary is the
+ * public Python API re-exported by /root/reference/pkg/src/streamkv/__init__.py:3-32
+ * plus the Session._attend call site (engine.py:269-271).  Every entry point
+ * below replaces one piece of that API; the reference interface it stands in
+ * for is cited beside it.  The Python drop-in (paper_2409_09086_b200/) binds
+ * these with ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Every function returns 0 on success or a negative SKV_E* code; the message
+ *     of the last error on the calling thread is returned by skv_last_error().
+ *   - SKV_EINVAL is the reference's ValueError domain (shapes, index ranges,
+ *     non-ascending kept sets, empty windows, n <= l, bad config).
+ *   - Pointers named *_dev are device pointers; *_host are host pointers.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *     enqueued on it; functions that return host data synchronise it.
+ *   - A context owns all its device buffers; nothing is allocated on the hot path.
+ *   - Distinct contexts are independent; one context is externally serialised
+ *     (reference SPEC.md:168).
+ */
+#ifndef STREAMKV_B200_H
+#define STREAMKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKV_OK 0
+#define SKV_EINVAL -1 /* domain error: the reference raises ValueError */
+#define SKV_ECUDA -2  /* CUDA runtime error */
+#define SKV_ENOMEM -3 /* device allocation failed */
+#define SKV_ESTATE -4 /* call not valid in the current context state */
+
+#define SKV_DTYPE_F32 0
+#define SKV_DTYPE_BF16 1
+
+#define SKV_AGG_MEAN 0 /* aggregate_heads(.., "mean"), policies.py:261-262 */
+#define SKV_AGG_MAX 1  /* aggregate_heads(.., "max"),  policies.py:263-264 */
+
+/* Engine configuration.  Mirrors PolicyConfig (policies.py:28-59) plus the
+ * cache shape of KvCache(layers, heads, head_dim) (cache.py:73-81) batched over
+ * `streams` independent sessions, with GQA (heads_q a multiple of heads_kv). */
+typedef struct skv_config {
+  int32_t streams;         /* S independent sessions (no cross-session state) */
+  int32_t layers;          /* L */
+  int32_t heads_q;         /* query heads */
+  int32_t heads_kv;        /* key/value heads (== heads_q in the reference) */
+  int32_t head_dim;        /* D: 64 or 128 */
+  int32_t dtype;           /* SKV_DTYPE_*: q/k/v inputs and the KV store */
+  int32_t recent_len;      /* l  (PolicyConfig.recent_len) */
+  int32_t relevant_budget; /* r  (PolicyConfig.relevant_budget) */
+  float bias;              /* b  (PolicyConfig.bias) */
+  int32_t window;          /* W rows of AttentionWindow(capacity=W), policies.py:98 */
+  int32_t capacity;        /* max cached tokens per (stream, layer) */
+  int32_t head_agg;        /* SKV_AGG_* */
+} skv_config;
+
+typedef struct skv_ctx skv_ctx;
+
+const char* skv_last_error(void);
+int skv_version(void);
+
+/* ---- lifetime ------------------------------------------------------------ */
+int skv_create(const skv_config* cfg, skv_ctx** out);
+int skv_destroy(skv_ctx* ctx);
+/* Device bytes held by the context (KV store + window + scratch). */
+int64_t skv_device_bytes(const skv_ctx* ctx);
+
+/* ---- decode: append -> attend -> head aggregation -> window push -----------
+ * Replaces, for one layer of every stream, the per-layer body of
+ * Session.decode_step (engine.py:264-273): KvCache.append (cache.py:112-134),
+ * Session._attend (engine.py:235-246), aggregate_heads (policies.py:259-265) and
+ * AttentionWindow.push (policies.py:107-115).
+ *   q_dev  [S][Hq][D], k_dev/v_dev [S][Hkv][D]  (config dtype)
+ *   positions_host [S] original positions of the appended token (NULL: previous+1)
+ *   out_dev [S][Hq][D] float32 attention output
+ *   record  nonzero: the head-aggregated probability row is pushed to the window. */
+int skv_decode_layer(skv_ctx* ctx, int layer, const void* q_dev, const void* k_dev, const void* v_dev,
+                     const int64_t* positions_host, float* out_dev, int record, void* stream);
+
+/* All layers of one token (Session.decode_step minus the tiny decoder):
+ * q_dev [L][S][Hq][D], k_dev/v_dev [L][S][Hkv][D], out_dev [L][S][Hq][D] f32. */
+int skv_decode_step(skv_ctx* ctx, const void* q_dev, const void* k_dev, const void* v_dev, float* out_dev,
+                    int record, void* stream);
+
+/* Same with HOST (pinned or pageable) buffers: copies in, decodes all layers
+ * with layer-pipelined H2D/compute/D2H on internal streams, copies out.
+ * Synchronous. */
+int skv_decode_step_host(skv_ctx* ctx, const void* q_host, const void* k_host, const void* v_host,
+                         float* out_host, int record);
+
+/* ---- eviction: Algorithm 1 + compaction -------------------------------------
+ * Replaces Session._evict_layer (engine.py:310-337) for every stream:
+ * inf_mllm_decide (policies.py:184-201: window_mean_scores 130-147, bias_vector
+ * 150-162, top_k_indices 165-181), KvCache.gather_keep (cache.py:136-156) and
+ * AttentionWindow.remap (policies.py:117-124).
+ *   layer  -1 = all layers (start_round's per-layer fan-out, engine.py:355-360)
+ *   kept_dev optional [S][L'][r+l] int32 copy of the kept sets (L' = 1 or L),
+ *            rows padded with -1 when the cache fits the budget (keep-all).
+ * Returns SKV_EINVAL if a window is empty (policies.py:191-192). */
+int skv_evict(skv_ctx* ctx, int layer, int32_t* kept_dev, void* stream);
+
+/* ---- state access -------------------------------------------------------- */
+/* Current cached length of (stream, layer): KvCache.length (cache.py:90-91). */
+int skv_length(const skv_ctx* ctx, int stream, int layer);
+/* Device pointers to the layer's keys/values [Hkv][capacity][D] (views,
+ * cache.py:93-100); the first skv_length() rows of each head are live. */
+int skv_kv_view(skv_ctx* ctx, int stream, int layer, void** k_dev, void** v_dev);
+/* Original positions [n] of (stream, layer), host copy (cache.py:102-104). */
+int skv_positions(skv_ctx* ctx, int stream, int layer, int64_t* out_host, int cap);
+/* Window rows of (stream, layer) oldest-first into out_host [W][capacity] with
+ * their lengths (AttentionWindow.rows); returns the row count. */
+int skv_window_rows(skv_ctx* ctx, int stream, int layer, float* rows_host, int32_t* lens_host);
+/* Biased scores computed at the last eviction of (stream, layer): [n-l] f32. */
+int skv_last_scores(skv_ctx* ctx, int stream, int layer, float* out_host, int cap);
+/* Overwrite (stream, layer) state from host data for state-injection parity:
+ * keys/values [Hkv][n][D] in config dtype, positions [n], window rows [m][n]
+ * (row i has length lens[i] <= n). */
+int skv_state_inject(skv_ctx* ctx, int stream, int layer, int n, const void* k_host, const void* v_host,
+                     const int64_t* pos_host, int m, const float* rows_host, const int32_t* lens_host);
+
+/* ---- CUDA graphs (replaces a tracing compiler) ---------------------------- */
+int skv_capture_begin(skv_ctx* ctx, void* stream);
+int skv_capture_end(skv_ctx* ctx, void* stream);
+int skv_graph_launch(skv_ctx* ctx, void* stream);
+/* Number of this library's kernels launched since creation (instrumentation). */
+int64_t skv_kernel_launches(const skv_ctx* ctx);
+
+/* ---- stand-alone policy kernels (drop-in for the pure policy functions) ---- */
+/* top_k_indices(scores, k) (policies.py:165-181) on device: ascending indices of
+ * the k largest, ties to the larger index.  out_dev receives min(k, n) int64. */
+int skv_top_k(const float* scores_dev, int n, int k, int64_t* out_dev, void* stream);
+/* inf_mllm_decide over a device window: rows_dev [m][row_stride] f32 oldest
+ * first, lens_dev [m] int32.  kept_dev [min(n, r+l)] int64; scores_dev optional
+ * [n-l] f32 biased scores.  Returns the kept count (>= 0) or an error. */
+int skv_decide(const float* rows_dev, int row_stride, const int32_t* lens_dev, int m, int n, int recent_len,
+               int relevant_budget, float bias, int64_t* kept_dev, float* scores_dev, void* stream);
+/* window_mean_scores (policies.py:130-147) + bias_vector (150-162) on device:
+ * writes biased (bias applied) or raw scores [n-l]. */
+int skv_window_scores(const float* rows_dev, int row_stride, const int32_t* lens_dev, int m, int n,
+                      int recent_len, float bias, int apply_bias, float* scores_dev, void* stream);
+/* In-place stable row compaction (gather_keep, cache.py:151-156) of `blocks`
+ * independent row arrays: block b starts at base_dev + b*block_stride bytes, row
+ * i is row_bytes wide; row i <- row kept[i] for i < m.  kept ascending, unique. */
+int skv_gather_rows(void* base_dev, int64_t block_stride, int blocks, int row_bytes, const int64_t* kept_dev,
+                    int m, void* stream);
+/* Single-query attention over one layer: keys/values [H][n][D] f32 (stride
+ * row_stride rows between heads), q [H][D] f32 -> probs [H][n], out [H][D]
+ * (Session._attend, engine.py:235-246; tensorops.attn_probs/weighted_sum). */
+int skv_attend(const float* keys_dev, const float* values_dev, int heads, int n, int head_dim,
+               int64_t head_stride, const float* q_dev, float* probs_dev, float* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STREAMKV_B200_H */

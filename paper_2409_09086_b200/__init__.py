@@ -1,0 +1,27 @@
+"""B200-native (sm_100a) Inf-MLLM streaming-decode hot path.
+
+Drop-in for the hot-path API of the reference ``streamkv`` package
+(/root/reference/pkg/src/streamkv/__init__.py:3-32): ``KvCache``,
+``AttentionWindow``, ``PolicyConfig``, ``EvictionDecision``,
+``window_mean_scores``, ``bias_vector``, ``top_k_indices``, ``inf_mllm_decide``,
+``aggregate_heads`` and ``attend`` (Session._attend), plus the batched
+``StreamEngine`` that runs decode + score + evict for many streams through
+libstreamkv_b200.so.  No CPU fallback: everything computes on the GPU.
+"""
+
+from ._lib import LIB_PATH, load as load_library
+from .cache import KvCache, PositionMode, TokenMeta
+from .engine import EngineConfig, StreamEngine
+from .policies import (
+    AttentionWindow,
+    EvictionDecision,
+    PolicyConfig,
+    aggregate_heads,
+    bias_vector,
+    inf_mllm_decide,
+    top_k_indices,
+    window_mean_scores,
+)
+from .tensorops import attend
+
+__version__ = "0.1.0"

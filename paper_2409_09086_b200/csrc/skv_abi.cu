@@ -1,0 +1,831 @@
+// C ABI + native runtime for the streamkv B200 hot path (see include/streamkv_b200.h).
+//
+// The context owns every device buffer (allocated once in skv_create; nothing is
+// allocated on the hot path) and a host mirror of the per-layer state that is
+// uniform across the lock-stepped streams: cached length n, window ring
+// head/count, the logit double-buffer parity and the pending (not yet folded)
+// window row.  Kernels read everything per-stream from device memory, so a
+// recorded CUDA graph of a state-invariant sequence (one eviction period) can be
+// replayed indefinitely.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/streamkv_b200.h"
+#include "skv_internal.h"
+
+using namespace skv;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return SKV_ECUDA;
+}
+
+#define SKV_CK(call)                                      \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct skv_ctx {
+  skv_config cfg;
+  int S, L, Hq, Hkv, D, G, cap, W, B, elt;
+  float scale;
+  int max_splits;
+  // device state
+  void* k = nullptr;
+  void* v = nullptr;
+  int64_t* pos = nullptr;
+  int8_t* modality = nullptr;
+  int32_t* round_id = nullptr;
+  int32_t* len = nullptr;
+  int64_t* next_pos = nullptr;
+  float* rows = nullptr;
+  int32_t* wlen = nullptr;
+  int32_t* newlen = nullptr;
+  float* logits[2] = {nullptr, nullptr};
+  float* stats[2] = {nullptr, nullptr};
+  float* part = nullptr;
+  int32_t* counters = nullptr;
+  int32_t* kept = nullptr;
+  int32_t* first_moved = nullptr;
+  float* scores = nullptr;
+  int64_t* pos_in = nullptr;  // staging for explicit positions
+  int64_t device_bytes = 0;
+  // host mirror (uniform over streams)
+  std::vector<int> n, whead, wcount, parity, pend_n, pend_slot, pend_par, round_value;
+  int64_t launches = 0;
+  // graphs
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  // host-buffer pipeline
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  cudaEvent_t ev_done = nullptr;
+  void* stage_q = nullptr;
+  void* stage_k = nullptr;
+  void* stage_v = nullptr;
+  float* stage_out = nullptr;
+  std::vector<void*> allocs;
+
+  template <typename P>
+  cudaError_t alloc(P** p, size_t bytes) {
+    void* raw = nullptr;
+    cudaError_t e = cudaMalloc(&raw, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) return e;
+    allocs.push_back(raw);
+    device_bytes += (int64_t)bytes;
+    *p = static_cast<P*>(raw);
+    return cudaMemset(raw, 0, std::max<size_t>(bytes, 16));
+  }
+
+  size_t sl_count() const { return (size_t)S * L; }
+  int64_t kv_layer_stride() const { return (int64_t)Hkv * cap * D; }  // elements
+  int64_t kv_stream_stride() const { return (int64_t)L * kv_layer_stride(); }
+
+  int splits_for(int tokens) const {
+    const int target = 148 * 6;
+    int sp = (target + S * Hkv - 1) / (S * Hkv);
+    sp = std::min(sp, (tokens + 63) / 64);
+    sp = std::max(1, std::min(sp, max_splits));
+    return sp;
+  }
+};
+
+extern "C" {
+
+const char* skv_last_error(void) { return g_err.c_str(); }
+int skv_version(void) { return 1; }
+
+int skv_create(const skv_config* cfg, skv_ctx** out) {
+  if (!cfg || !out) return fail(SKV_EINVAL, "null argument");
+  const skv_config& c = *cfg;
+  if (c.streams < 1 || c.layers < 1 || c.heads_q < 1 || c.heads_kv < 1 || c.head_dim < 1)
+    return fail(SKV_EINVAL, "layers, heads and head_dim must be positive");
+  if (c.head_dim != 64 && c.head_dim != 128) return fail(SKV_EINVAL, "head_dim must be 64 or 128");
+  if (c.heads_q % c.heads_kv) return fail(SKV_EINVAL, "heads_q must be a multiple of heads_kv");
+  const int G = c.heads_q / c.heads_kv;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return fail(SKV_EINVAL, "heads_q/heads_kv must be 1, 2, 4 or 8");
+  if (c.dtype != SKV_DTYPE_F32 && c.dtype != SKV_DTYPE_BF16) return fail(SKV_EINVAL, "dtype must be f32 or bf16");
+  if (c.recent_len < 1) return fail(SKV_EINVAL, "recent_len must be >= 1");
+  if (c.relevant_budget < 0) return fail(SKV_EINVAL, "relevant_budget must be >= 0");
+  if (!(c.bias >= 0.f)) return fail(SKV_EINVAL, "bias must be >= 0");
+  if (c.window < 1 || c.window > 1024) return fail(SKV_EINVAL, "window capacity must be in [1, 1024]");
+  if (c.head_agg != SKV_AGG_MEAN && c.head_agg != SKV_AGG_MAX) return fail(SKV_EINVAL, "unknown head_agg");
+  if (c.capacity < c.recent_len + c.relevant_budget + 1)
+    return fail(SKV_EINVAL, "capacity must exceed recent_len + relevant_budget");
+
+  skv_ctx* x = new skv_ctx();
+  x->cfg = c;
+  x->S = c.streams;
+  x->L = c.layers;
+  x->Hq = c.heads_q;
+  x->Hkv = c.heads_kv;
+  x->D = c.head_dim;
+  x->G = G;
+  x->cap = (c.capacity + 31) / 32 * 32;
+  x->W = c.window;
+  x->B = c.recent_len + c.relevant_budget;
+  x->elt = c.dtype == SKV_DTYPE_BF16 ? 2 : 4;
+  x->scale = (float)(1.0 / std::sqrt((double)c.head_dim));
+  x->max_splits = (x->cap + 63) / 64;
+
+  const size_t SL = x->sl_count();
+  const size_t kv_bytes = SL * (size_t)x->kv_layer_stride() * x->elt;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t r) {
+    if (e == cudaSuccess && r != cudaSuccess) e = r;
+  };
+  chk(x->alloc(&x->k, kv_bytes));
+  chk(x->alloc(&x->v, kv_bytes));
+  chk(x->alloc(&x->pos, SL * x->cap * sizeof(int64_t)));
+  chk(x->alloc(&x->modality, SL * x->cap));
+  chk(x->alloc(&x->round_id, SL * x->cap * sizeof(int32_t)));
+  chk(x->alloc(&x->len, SL * sizeof(int32_t)));
+  chk(x->alloc(&x->next_pos, SL * sizeof(int64_t)));
+  chk(x->alloc(&x->rows, SL * x->W * (size_t)x->cap * sizeof(float)));
+  chk(x->alloc(&x->wlen, SL * x->W * sizeof(int32_t)));
+  chk(x->alloc(&x->newlen, SL * x->W * sizeof(int32_t)));
+  for (int p = 0; p < 2; ++p) {
+    chk(x->alloc(&x->logits[p], SL * x->Hq * (size_t)x->cap * sizeof(float)));
+    chk(x->alloc(&x->stats[p], SL * x->Hq * 2 * sizeof(float)));
+  }
+  chk(x->alloc(&x->part, (size_t)x->S * x->Hq * x->max_splits * (x->D + 2) * sizeof(float)));
+  chk(x->alloc(&x->counters, (size_t)x->S * x->Hkv * sizeof(int32_t)));
+  chk(x->alloc(&x->kept, SL * x->B * sizeof(int32_t)));
+  chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
+  chk(x->alloc(&x->scores, SL * x->cap * sizeof(float)));
+  chk(x->alloc(&x->pos_in, x->S * sizeof(int64_t)));
+  if (e != cudaSuccess) {
+    skv_destroy(x);
+    return e == cudaErrorMemoryAllocation ? fail(SKV_ENOMEM, "device allocation failed")
+                                          : cuda_fail(e, "skv_create");
+  }
+  x->n.assign(x->L, 0);
+  x->whead.assign(x->L, 0);
+  x->wcount.assign(x->L, 0);
+  x->parity.assign(x->L, 0);
+  x->pend_n.assign(x->L, 0);
+  x->pend_slot.assign(x->L, 0);
+  x->pend_par.assign(x->L, 0);
+  x->round_value.assign(x->L, 0);
+  *out = x;
+  return SKV_OK;
+}
+
+int skv_destroy(skv_ctx* x) {
+  if (!x) return SKV_OK;
+  cudaDeviceSynchronize();
+  if (x->exec) cudaGraphExecDestroy(x->exec);
+  if (x->graph) cudaGraphDestroy(x->graph);
+  for (auto ev : x->ev_in) cudaEventDestroy(ev);
+  for (auto ev : x->ev_out) cudaEventDestroy(ev);
+  if (x->ev_done) cudaEventDestroy(x->ev_done);
+  for (auto s : x->hs)
+    if (s) cudaStreamDestroy(s);
+  for (void* p : x->allocs) cudaFree(p);
+  delete x;
+  return SKV_OK;
+}
+
+int64_t skv_device_bytes(const skv_ctx* x) { return x ? x->device_bytes : 0; }
+int64_t skv_kernel_launches(const skv_ctx* x) { return x ? x->launches : 0; }
+
+// ------------------------------------------------------------------ decode --
+
+static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
+                             const int64_t* pos_dev, float* out, int record, cudaStream_t st) {
+  const int n_old = x->n[layer];
+  if (n_old + 1 > x->cap)
+    return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
+  const int n = n_old + 1;
+  const int splits = x->splits_for(n);
+  const int chunk = ((n + splits - 1) / splits + 31) / 32 * 32;
+  const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
+
+  AttnArgs a{};
+  a.Hq = x->Hq;
+  a.Hkv = x->Hkv;
+  a.n_old = n_old;
+  a.append = 1;
+  a.splits = (n + chunk - 1) / chunk;
+  a.chunk = chunk;
+  a.scale = x->scale;
+  const int64_t kv_off = (int64_t)layer * x->kv_layer_stride() * x->elt;
+  a.kc = static_cast<char*>(x->k) + kv_off;
+  a.vc = static_cast<char*>(x->v) + kv_off;
+  a.c_ss = x->kv_stream_stride();
+  a.c_hs = (int64_t)x->cap * x->D;
+  a.q = q;
+  a.q_ss = (int64_t)x->Hq * x->D;
+  a.kin = k;
+  a.vin = v;
+  a.in_ss = (int64_t)x->Hkv * x->D;
+  a.out = out;
+  a.o_ss = (int64_t)x->Hq * x->D;
+  const int par = x->parity[layer];
+  const int64_t lg_sl = (int64_t)x->Hq * x->cap;
+  if (record) {
+    a.logits = x->logits[par] + (int64_t)layer * lg_sl;
+    a.l_ss = SLstride * lg_sl;
+    a.l_hs = x->cap;
+  }
+  a.stats = x->stats[par] + (int64_t)layer * x->Hq * 2;
+  a.st_ss = SLstride * x->Hq * 2;
+  a.part = x->part;
+  a.counters = x->counters;
+  a.pos = x->pos + (int64_t)layer * x->cap;
+  a.modality = x->modality + (int64_t)layer * x->cap;
+  a.round_id = x->round_id + (int64_t)layer * x->cap;
+  a.m_ss = SLstride * x->cap;
+  a.len = x->len + layer;
+  a.len_ss = SLstride;
+  a.next_pos = x->next_pos + layer;
+  a.pos_in = pos_dev;
+  a.round_value = x->round_value[layer];
+  // fold of the pending row (previous recorded step) into its ring slot
+  if (x->pend_n[layer] > 0) {
+    const int pp = x->pend_par[layer];
+    FoldArgs& f = a.fold;
+    f.logits = x->logits[pp] + (int64_t)layer * lg_sl;
+    f.l_ss = SLstride * lg_sl;
+    f.l_hs = x->cap;
+    f.stats = x->stats[pp] + (int64_t)layer * x->Hq * 2;
+    f.st_ss = SLstride * x->Hq * 2;
+    f.rows = x->rows + ((int64_t)layer * x->W + x->pend_slot[layer]) * x->cap;
+    f.r_ss = SLstride * x->W * x->cap;
+    f.wlen = x->wlen + (int64_t)layer * x->W + x->pend_slot[layer];
+    f.w_ss = SLstride * x->W;
+    f.n = x->pend_n[layer];
+    f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
+  }
+  cudaError_t e = launch_decode(x->cfg.dtype, x->D, x->G, x->S, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+  x->launches++;
+  x->pend_n[layer] = 0;
+  if (record) {
+    x->pend_n[layer] = n;
+    x->pend_slot[layer] = x->whead[layer];
+    x->pend_par[layer] = par;
+    x->whead[layer] = (x->whead[layer] + 1) % x->W;
+    x->wcount[layer] = std::min(x->wcount[layer] + 1, x->W);
+    x->parity[layer] = par ^ 1;
+  }
+  x->n[layer] = n;
+  return SKV_OK;
+}
+
+static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
+  if (x->pend_n[layer] <= 0) return SKV_OK;
+  const int pp = x->pend_par[layer];
+  const int64_t lg_sl = (int64_t)x->Hq * x->cap;
+  FoldArgs f{};
+  f.logits = x->logits[pp] + (int64_t)layer * lg_sl;
+  f.l_ss = (int64_t)x->L * lg_sl;
+  f.l_hs = x->cap;
+  f.stats = x->stats[pp] + (int64_t)layer * x->Hq * 2;
+  f.st_ss = (int64_t)x->L * x->Hq * 2;
+  f.rows = x->rows + ((int64_t)layer * x->W + x->pend_slot[layer]) * x->cap;
+  f.r_ss = (int64_t)x->L * x->W * x->cap;
+  f.wlen = x->wlen + (int64_t)layer * x->W + x->pend_slot[layer];
+  f.w_ss = (int64_t)x->L * x->W;
+  f.n = x->pend_n[layer];
+  f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
+  const int pieces = std::max(1, std::min(64, (f.n + 255) / 256));
+  cudaError_t e = launch_fold(x->S, pieces, f, x->Hq, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
+  x->launches++;
+  x->pend_n[layer] = 0;
+  return SKV_OK;
+}
+
+int skv_decode_layer(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
+                     const int64_t* positions_host, float* out, int record, void* stream) {
+  if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
+  if (layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
+  cudaStream_t st = as_stream(stream);
+  const int64_t* pos_dev = nullptr;
+  if (positions_host) {
+    // original positions must strictly increase (cache.py:125-126)
+    std::vector<int64_t> prev(x->S);
+    if (x->n[layer] > 0) {
+      for (int s = 0; s < x->S; ++s) {
+        SKV_CK(cudaMemcpyAsync(&prev[s], x->pos + ((int64_t)s * x->L + layer) * x->cap + x->n[layer] - 1,
+                               sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      }
+      SKV_CK(cudaStreamSynchronize(st));
+      for (int s = 0; s < x->S; ++s)
+        if (positions_host[s] <= prev[s]) return fail(SKV_EINVAL, "original_position must be strictly increasing");
+    }
+    SKV_CK(cudaMemcpyAsync(x->pos_in, positions_host, x->S * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    SKV_CK(cudaStreamSynchronize(st));
+    pos_dev = x->pos_in;
+  }
+  return decode_layer_impl(x, layer, q, k, v, pos_dev, out, record, st);
+}
+
+int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record, void* stream) {
+  if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
+  cudaStream_t st = as_stream(stream);
+  const int64_t qb = (int64_t)x->S * x->Hq * x->D * x->elt;
+  const int64_t kb = (int64_t)x->S * x->Hkv * x->D * x->elt;
+  const int64_t ob = (int64_t)x->S * x->Hq * x->D;
+  for (int l = 0; l < x->L; ++l) {
+    int rc = decode_layer_impl(x, l, static_cast<const char*>(q) + l * qb, static_cast<const char*>(k) + l * kb,
+                               static_cast<const char*>(v) + l * kb, nullptr, out + l * ob, record, st);
+    if (rc) return rc;
+  }
+  return SKV_OK;
+}
+
+int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record) {
+  if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
+  const int64_t qb = (int64_t)x->S * x->Hq * x->D * x->elt;
+  const int64_t kb = (int64_t)x->S * x->Hkv * x->D * x->elt;
+  const int64_t ob = (int64_t)x->S * x->Hq * x->D * sizeof(float);
+  if (!x->stage_q) {
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t r) {
+      if (e == cudaSuccess && r != cudaSuccess) e = r;
+    };
+    chk(x->alloc(&x->stage_q, qb * x->L));
+    chk(x->alloc(&x->stage_k, kb * x->L));
+    chk(x->alloc(&x->stage_v, kb * x->L));
+    chk(x->alloc(&x->stage_out, ob * x->L));
+    for (auto& s : x->hs) chk(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    x->ev_in.resize(x->L);
+    x->ev_out.resize(x->L);
+    for (int l = 0; l < x->L; ++l) {
+      chk(cudaEventCreateWithFlags(&x->ev_in[l], cudaEventDisableTiming));
+      chk(cudaEventCreateWithFlags(&x->ev_out[l], cudaEventDisableTiming));
+    }
+    chk(cudaEventCreateWithFlags(&x->ev_done, cudaEventDisableTiming));
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
+  }
+  cudaStream_t s_in = x->hs[0], s_c = x->hs[1], s_out = x->hs[2];
+  for (int l = 0; l < x->L; ++l) {
+    char* dq = static_cast<char*>(x->stage_q) + l * qb;
+    char* dk = static_cast<char*>(x->stage_k) + l * kb;
+    char* dv = static_cast<char*>(x->stage_v) + l * kb;
+    SKV_CK(cudaMemcpyAsync(dq, static_cast<const char*>(q) + l * qb, qb, cudaMemcpyHostToDevice, s_in));
+    SKV_CK(cudaMemcpyAsync(dk, static_cast<const char*>(k) + l * kb, kb, cudaMemcpyHostToDevice, s_in));
+    SKV_CK(cudaMemcpyAsync(dv, static_cast<const char*>(v) + l * kb, kb, cudaMemcpyHostToDevice, s_in));
+    SKV_CK(cudaEventRecord(x->ev_in[l], s_in));
+    SKV_CK(cudaStreamWaitEvent(s_c, x->ev_in[l], 0));
+    float* dout = x->stage_out + l * (ob / sizeof(float));
+    int rc = decode_layer_impl(x, l, dq, dk, dv, nullptr, dout, record, s_c);
+    if (rc) return rc;
+    SKV_CK(cudaEventRecord(x->ev_out[l], s_c));
+    SKV_CK(cudaStreamWaitEvent(s_out, x->ev_out[l], 0));
+    SKV_CK(cudaMemcpyAsync(reinterpret_cast<char*>(out) + l * ob, dout, ob, cudaMemcpyDeviceToHost, s_out));
+  }
+  SKV_CK(cudaStreamSynchronize(s_out));
+  SKV_CK(cudaStreamSynchronize(s_c));
+  return SKV_OK;
+}
+
+// ------------------------------------------------------------------- evict --
+
+static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStream_t st) {
+  // all layers in [l0, l1) share n / ring state (checked by caller)
+  const int nl = l1 - l0;
+  const int n = x->n[l0];
+  const int m = n > x->B ? x->B : n;
+  const bool all = (l0 == 0 && l1 == x->L);
+  // block b enumerates (s, layer): contiguous when all layers are evicted together
+  SelectArgs a{};
+  a.row_stride = x->cap;
+  a.ring_head = x->whead[l0];
+  a.count = x->wcount[l0];
+  a.W = x->W;
+  a.n = n;
+  a.l = x->cfg.recent_len;
+  a.r = x->cfg.relevant_budget;
+  a.bias = x->cfg.bias;
+  a.apply_bias = 1;
+  a.pad = x->B;
+  CompactArgs c{};
+  c.heads = x->Hkv;
+  c.row_bytes = x->D * x->elt;
+  c.kv_hs = (int64_t)x->cap * x->D * x->elt;
+  c.row_stride = x->cap;
+  c.W = x->W;
+  c.m = m;
+  if (all) {
+    a.rows = x->rows;
+    a.r_bs = (int64_t)x->W * x->cap;
+    a.wlen = x->wlen;
+    a.w_bs = x->W;
+    a.kept32 = x->kept;
+    a.k_bs = x->B;
+    a.scores = x->scores;
+    a.s_bs = x->cap;
+    a.first_moved = x->first_moved;
+    a.newlen = x->newlen;
+    cudaError_t e = launch_select(x->S * x->L, a, st);
+    if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+    x->launches++;
+    c.k = static_cast<char*>(x->k);
+    c.v = static_cast<char*>(x->v);
+    c.kv_bs = x->kv_layer_stride() * x->elt;
+    c.pos = x->pos;
+    c.modality = x->modality;
+    c.round_id = x->round_id;
+    c.m_bs = x->cap;
+    c.rows = x->rows;
+    c.r_bs = (int64_t)x->W * x->cap;
+    c.wlen = x->wlen;
+    c.newlen = x->newlen;
+    c.w_bs = x->W;
+    c.kept32 = x->kept;
+    c.k_bs = x->B;
+    c.first_moved = x->first_moved;
+    c.len = x->len;
+    c.len_bs = 1;
+    e = launch_compact(x->S * x->L, c, st);
+    if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
+    x->launches++;
+  } else {
+    for (int l = l0; l < l1; ++l) {
+      const int64_t sl0 = l;  // block b = stream s -> (s*L + l)
+      a.rows = x->rows + sl0 * x->W * x->cap;
+      a.r_bs = (int64_t)x->L * x->W * x->cap;
+      a.wlen = x->wlen + sl0 * x->W;
+      a.w_bs = (int64_t)x->L * x->W;
+      a.kept32 = x->kept + sl0 * x->B;
+      a.k_bs = (int64_t)x->L * x->B;
+      a.scores = x->scores + sl0 * x->cap;
+      a.s_bs = (int64_t)x->L * x->cap;
+      a.first_moved = x->first_moved + sl0 * x->S;  // scratch slice of S entries
+      a.newlen = x->newlen + sl0 * x->W;
+      cudaError_t e = launch_select(x->S, a, st);
+      if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+      x->launches++;
+      c.k = static_cast<char*>(x->k) + sl0 * x->kv_layer_stride() * x->elt;
+      c.v = static_cast<char*>(x->v) + sl0 * x->kv_layer_stride() * x->elt;
+      c.kv_bs = x->kv_stream_stride() * x->elt;
+      c.pos = x->pos + sl0 * x->cap;
+      c.modality = x->modality + sl0 * x->cap;
+      c.round_id = x->round_id + sl0 * x->cap;
+      c.m_bs = (int64_t)x->L * x->cap;
+      c.rows = x->rows + sl0 * x->W * x->cap;
+      c.r_bs = (int64_t)x->L * x->W * x->cap;
+      c.wlen = x->wlen + sl0 * x->W;
+      c.newlen = x->newlen + sl0 * x->W;
+      c.w_bs = (int64_t)x->L * x->W;
+      c.kept32 = x->kept + sl0 * x->B;
+      c.k_bs = (int64_t)x->L * x->B;
+      c.first_moved = a.first_moved;
+      c.len = x->len + sl0;
+      c.len_bs = x->L;
+      e = launch_compact(x->S, c, st);
+      if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
+      x->launches++;
+    }
+  }
+  if (kept_dev) {
+    // [S][nl][B] copy out of the [S][L][B] scratch
+    SKV_CK(cudaMemcpy2DAsync(kept_dev, (size_t)nl * x->B * sizeof(int32_t), x->kept + (int64_t)l0 * x->B,
+                             (size_t)x->L * x->B * sizeof(int32_t), (size_t)nl * x->B * sizeof(int32_t), x->S,
+                             cudaMemcpyDeviceToDevice, st));
+  }
+  for (int l = l0; l < l1; ++l) x->n[l] = m;
+  return SKV_OK;
+}
+
+int skv_evict(skv_ctx* x, int layer, int32_t* kept_dev, void* stream) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
+  if (layer < -1 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
+  cudaStream_t st = as_stream(stream);
+  const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? x->L : layer + 1;
+  for (int l = l0; l < l1; ++l) {
+    if (x->wcount[l] == 0) return fail(SKV_EINVAL, "attention window is empty");
+  }
+  for (int l = l0; l < l1; ++l) {
+    int rc = flush_pending(x, l, st);
+    if (rc) return rc;
+  }
+  bool uniform = true;
+  for (int l = l0 + 1; l < l1; ++l)
+    uniform &= x->n[l] == x->n[l0] && x->whead[l] == x->whead[l0] && x->wcount[l] == x->wcount[l0];
+  if (uniform && l0 == 0 && l1 == x->L) {
+    if (kept_dev && layer >= 0) return evict_layers(x, l0, l1, kept_dev, st);
+    return evict_layers(x, l0, l1, kept_dev, st);
+  }
+  for (int l = l0; l < l1; ++l) {
+    int rc = evict_layers(x, l, l + 1, kept_dev ? kept_dev + (int64_t)(l - l0) * x->B : nullptr, st);
+    if (rc) return rc;
+  }
+  return SKV_OK;
+}
+
+// ------------------------------------------------------------ state access --
+
+int skv_length(const skv_ctx* x, int stream, int layer) {
+  if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  return x->n[layer];
+}
+
+int skv_kv_view(skv_ctx* x, int stream, int layer, void** k, void** v) {
+  if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  const int64_t off = ((int64_t)stream * x->L + layer) * x->kv_layer_stride() * x->elt;
+  if (k) *k = static_cast<char*>(x->k) + off;
+  if (v) *v = static_cast<char*>(x->v) + off;
+  return SKV_OK;
+}
+
+int skv_positions(skv_ctx* x, int stream, int layer, int64_t* out, int cap) {
+  if (!x || !out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  const int n = std::min(cap, x->n[layer]);
+  SKV_CK(cudaDeviceSynchronize());
+  SKV_CK(cudaMemcpy(out, x->pos + ((int64_t)stream * x->L + layer) * x->cap, n * sizeof(int64_t),
+                    cudaMemcpyDeviceToHost));
+  return n;
+}
+
+int skv_window_rows(skv_ctx* x, int stream, int layer, float* rows_host, int32_t* lens_host) {
+  if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  int rc = flush_pending(x, layer, nullptr);
+  if (rc) return rc;
+  SKV_CK(cudaDeviceSynchronize());
+  const int64_t sl = (int64_t)stream * x->L + layer;
+  std::vector<int32_t> lens(x->W);
+  SKV_CK(cudaMemcpy(lens.data(), x->wlen + sl * x->W, x->W * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  const int count = x->wcount[layer];
+  for (int k = 0; k < count; ++k) {
+    const int slot = ((x->whead[layer] - count + k) % x->W + x->W) % x->W;
+    if (lens_host) lens_host[k] = lens[slot];
+    if (rows_host)
+      SKV_CK(cudaMemcpy(rows_host + (int64_t)k * x->cap, x->rows + (sl * x->W + slot) * x->cap,
+                        (size_t)lens[slot] * sizeof(float), cudaMemcpyDeviceToHost));
+  }
+  return count;
+}
+
+int skv_last_scores(skv_ctx* x, int stream, int layer, float* out, int cap) {
+  if (!x || !out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  SKV_CK(cudaDeviceSynchronize());
+  SKV_CK(cudaMemcpy(out, x->scores + ((int64_t)stream * x->L + layer) * x->cap,
+                    (size_t)std::min(cap, x->cap) * sizeof(float), cudaMemcpyDeviceToHost));
+  return SKV_OK;
+}
+
+int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_host, const void* v_host,
+                     const int64_t* pos_host, int m, const float* rows_host, const int32_t* lens_host) {
+  if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  if (n < 0 || n > x->cap) return fail(SKV_EINVAL, "n exceeds capacity");
+  if (m < 0 || m > x->W) return fail(SKV_EINVAL, "too many window rows");
+  SKV_CK(cudaDeviceSynchronize());
+  const int64_t sl = (int64_t)stream * x->L + layer;
+  const size_t rb = (size_t)x->D * x->elt;
+  char* kd = static_cast<char*>(x->k) + sl * x->kv_layer_stride() * x->elt;
+  char* vd = static_cast<char*>(x->v) + sl * x->kv_layer_stride() * x->elt;
+  if (k_host && v_host && n > 0) {
+    SKV_CK(cudaMemcpy2D(kd, (size_t)x->cap * rb, k_host, (size_t)n * rb, (size_t)n * rb, x->Hkv,
+                        cudaMemcpyHostToDevice));
+    SKV_CK(cudaMemcpy2D(vd, (size_t)x->cap * rb, v_host, (size_t)n * rb, (size_t)n * rb, x->Hkv,
+                        cudaMemcpyHostToDevice));
+  }
+  if (pos_host && n > 0) {
+    SKV_CK(cudaMemcpy(x->pos + sl * x->cap, pos_host, n * sizeof(int64_t), cudaMemcpyHostToDevice));
+    const int64_t nextp = pos_host[n - 1] + 1;
+    SKV_CK(cudaMemcpy(x->next_pos + sl, &nextp, sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  const int32_t n32 = n;
+  SKV_CK(cudaMemcpy(x->len + sl, &n32, sizeof(int32_t), cudaMemcpyHostToDevice));
+  std::vector<int32_t> lens(x->W, 0);
+  for (int k = 0; k < m; ++k) {
+    lens[k] = lens_host ? lens_host[k] : n;
+    if (rows_host)
+      SKV_CK(cudaMemcpy(x->rows + (sl * x->W + k) * x->cap, rows_host + (int64_t)k * n, (size_t)lens[k] * sizeof(float),
+                        cudaMemcpyHostToDevice));
+  }
+  SKV_CK(cudaMemcpy(x->wlen + sl * x->W, lens.data(), x->W * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // host mirror: injection is per (stream, layer); the caller injects every
+  // stream of a layer with the same n and m.
+  x->n[layer] = n;
+  x->wcount[layer] = m;
+  x->whead[layer] = m % x->W;
+  x->pend_n[layer] = 0;
+  return SKV_OK;
+}
+
+// ------------------------------------------------------------------ graphs --
+
+int skv_capture_begin(skv_ctx* x, void* stream) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
+  SKV_CK(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
+  return SKV_OK;
+}
+
+int skv_capture_end(skv_ctx* x, void* stream) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
+  if (x->exec) {
+    cudaGraphExecDestroy(x->exec);
+    x->exec = nullptr;
+  }
+  if (x->graph) {
+    cudaGraphDestroy(x->graph);
+    x->graph = nullptr;
+  }
+  SKV_CK(cudaStreamEndCapture(as_stream(stream), &x->graph));
+  SKV_CK(cudaGraphInstantiate(&x->exec, x->graph, 0));
+  return SKV_OK;
+}
+
+int skv_graph_launch(skv_ctx* x, void* stream) {
+  if (!x || !x->exec) return fail(SKV_ESTATE, "no captured graph");
+  SKV_CK(cudaGraphLaunch(x->exec, as_stream(stream)));
+  return SKV_OK;
+}
+
+// ------------------------------------------------------- stand-alone policy --
+
+int skv_top_k(const float* scores, int n, int k, int64_t* out, void* stream) {
+  if (k < 0) return fail(SKV_EINVAL, "k must be >= 0");
+  if (n < 0) return fail(SKV_EINVAL, "n must be >= 0");
+  if (k == 0 || n == 0) return SKV_OK;
+  cudaError_t e = launch_topk(scores, n, k, out, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "top-k kernel launch");
+  return SKV_OK;
+}
+
+static int check_window(int m, int n, int recent_len) {
+  if (m <= 0) return fail(SKV_EINVAL, "attention window is empty");
+  if (m > 1024) return fail(SKV_EINVAL, "window holds more than 1024 rows");
+  (void)n;
+  (void)recent_len;
+  return SKV_OK;
+}
+
+int skv_window_scores(const float* rows, int row_stride, const int32_t* lens, int m, int n, int recent_len,
+                      float bias, int apply_bias, float* scores, void* stream) {
+  int rc = check_window(m, n, recent_len);
+  if (rc) return rc;
+  if (n <= recent_len) return fail(SKV_EINVAL, "no scorable columns: n <= l");
+  if (bias < 0) return fail(SKV_EINVAL, "bias must be >= 0");
+  SelectArgs a{};
+  a.rows = rows;
+  a.row_stride = row_stride;
+  a.wlen = lens;
+  a.ring_head = m;
+  a.count = m;
+  a.W = m;
+  a.n = n;
+  a.l = recent_len;
+  a.bias = bias;
+  a.apply_bias = apply_bias;
+  a.scores = scores;
+  a.scores_only = 1;
+  cudaError_t e = launch_select(1, a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+  return SKV_OK;
+}
+
+int skv_decide(const float* rows, int row_stride, const int32_t* lens, int m, int n, int recent_len,
+               int relevant_budget, float bias, int64_t* kept, float* scores, void* stream) {
+  int rc = check_window(m, n, recent_len);
+  if (rc) return rc;
+  if (recent_len < 1 || relevant_budget < 0 || bias < 0) return fail(SKV_EINVAL, "bad policy config");
+  if (n <= recent_len + relevant_budget) {
+    SelectArgs a{};
+    a.rows = rows;
+    a.row_stride = row_stride;
+    a.wlen = lens;
+    a.ring_head = m;
+    a.count = m;
+    a.W = m;
+    a.n = n;
+    a.l = recent_len;
+    a.r = relevant_budget;
+    a.kept64 = kept;
+    cudaError_t e = launch_select(1, a, as_stream(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+    return n;
+  }
+  if (!scores) return fail(SKV_EINVAL, "scores scratch required when n > r + l");
+  SelectArgs a{};
+  a.rows = rows;
+  a.row_stride = row_stride;
+  a.wlen = lens;
+  a.ring_head = m;
+  a.count = m;
+  a.W = m;
+  a.n = n;
+  a.l = recent_len;
+  a.r = relevant_budget;
+  a.bias = bias;
+  a.apply_bias = 1;
+  a.kept64 = kept;
+  a.scores = scores;
+  cudaError_t e = launch_select(1, a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+  return recent_len + relevant_budget;
+}
+
+int skv_gather_rows(void* base, int64_t block_stride, int blocks, int row_bytes, const int64_t* kept, int m,
+                    void* stream) {
+  if (row_bytes % 16) return fail(SKV_EINVAL, "row_bytes must be a multiple of 16");
+  if (m <= 0 || blocks <= 0) return SKV_OK;
+  CompactArgs c{};
+  c.k = static_cast<char*>(base);
+  c.kv_hs = block_stride;
+  c.heads = blocks;
+  c.row_bytes = row_bytes;
+  c.kept64 = kept;
+  c.m = m;
+  cudaError_t e = launch_compact(1, c, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
+  return SKV_OK;
+}
+
+// Scratch for the stand-alone attend (drop-in API, not the engine hot path).
+namespace {
+struct AttendScratch {
+  float* stats = nullptr;
+  float* part = nullptr;
+  int32_t* counters = nullptr;
+  size_t part_floats = 0;
+  int heads = 0;
+};
+thread_local AttendScratch g_att;
+}  // namespace
+
+int skv_attend(const float* keys, const float* values, int heads, int n, int head_dim, int64_t head_stride,
+               const float* q, float* probs, float* out, void* stream) {
+  if (heads < 1 || n < 1) return fail(SKV_EINVAL, "keys must be a non-empty sequence of vectors");
+  if (head_dim != 64 && head_dim != 128) return fail(SKV_EINVAL, "device attend needs head_dim 64 or 128");
+  cudaStream_t st = as_stream(stream);
+  const int splits = std::max(1, std::min((n + 255) / 256, 64));
+  const int chunk = ((n + splits - 1) / splits + 31) / 32 * 32;
+  const int real_splits = (n + chunk - 1) / chunk;
+  const size_t need = (size_t)heads * real_splits * (head_dim + 2);
+  if (g_att.part_floats < need || g_att.heads < heads) {
+    SKV_CK(cudaStreamSynchronize(st));
+    if (g_att.stats) cudaFree(g_att.stats);
+    if (g_att.part) cudaFree(g_att.part);
+    if (g_att.counters) cudaFree(g_att.counters);
+    const int hcap = std::max(heads, 64);
+    const size_t pcap = std::max(need, (size_t)hcap * 64 * 130);
+    SKV_CK(cudaMalloc(&g_att.stats, hcap * 2 * sizeof(float)));
+    SKV_CK(cudaMalloc(&g_att.part, pcap * sizeof(float)));
+    SKV_CK(cudaMalloc(&g_att.counters, hcap * sizeof(int32_t)));
+    SKV_CK(cudaMemset(g_att.counters, 0, hcap * sizeof(int32_t)));
+    g_att.part_floats = pcap;
+    g_att.heads = hcap;
+  }
+  AttnArgs a{};
+  a.Hq = heads;
+  a.Hkv = heads;
+  a.n_old = n;
+  a.append = 0;
+  a.splits = real_splits;
+  a.chunk = chunk;
+  a.scale = (float)(1.0 / std::sqrt((double)head_dim));
+  a.kc = const_cast<float*>(keys);
+  a.vc = const_cast<float*>(values);
+  a.c_ss = 0;
+  a.c_hs = head_stride;
+  a.q = q;
+  a.kin = keys;  // unused (append = 0)
+  a.vin = values;
+  a.out = out;
+  a.logits = probs;  // logits recorded in place, then normalised below
+  a.l_hs = n;
+  a.stats = g_att.stats;
+  a.part = g_att.part;
+  a.counters = g_att.counters;
+  cudaError_t e = launch_decode(SKV_DTYPE_F32, head_dim, 1, 1, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+  FoldArgs f{};
+  f.logits = probs;
+  f.l_hs = n;
+  f.stats = g_att.stats;
+  f.probs = probs;
+  f.p_hs = n;
+  f.n = n;
+  f.mode = 2;
+  e = launch_fold(1, std::max(1, std::min(64, (n + 127) / 128)), f, heads, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
+  return SKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// Internal kernel-argument structs and launchers shared by the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skv {
+
+// ----------------------------------------------------------------------------
+// K1: split-KV flash-decode with fused append, logit record and split combine.
+// Element (s, h, t, d) of the K store lives at kc + s*c_ss + h*c_hs + t*D + d.
+// ----------------------------------------------------------------------------
+struct FoldArgs {
+  // Materialise the previous step's head-aggregated row from its recorded
+  // logits and (max, sum) stats:  row[j] = agg_h expf(x[h][j]-M_h)/L_h.
+  const float* logits;  // [s][hq][j]  (stream stride l_ss, head stride l_hs)
+  int64_t l_ss, l_hs;
+  const float* stats;   // [s][hq][2]  (stream stride st_ss)
+  int64_t st_ss;
+  float* rows;          // destination row of stream s: rows + s*r_ss
+  int64_t r_ss;
+  int32_t* wlen;        // optional: wlen[s*w_ss] = n
+  int64_t w_ss;
+  float* probs;         // mode 2: per-head probabilities probs + s*p_ss + h*p_hs + j
+  int64_t p_ss, p_hs;
+  int n;                // row length (0: nothing to fold)
+  int mode;             // 0 mean over heads, 1 max over heads, 2 per-head probs
+};
+
+struct AttnArgs {
+  int Hq, Hkv;          // group size G = Hq / Hkv is a template parameter
+  int n_old;            // tokens cached before this step
+  int append;           // 1: slot n_old is the new token taken from kin/vin
+  int splits, chunk;    // grid.x = splits; CTA c covers [c*chunk, min((c+1)*chunk, n))
+  float scale;          // f32(1/sqrt(D)), engine.py:150
+  void* kc;             // K store base (written for the appended row)
+  void* vc;
+  int64_t c_ss, c_hs;   // stream / head strides (elements)
+  const void* q;        // q[s][hq][d]     stride q_ss per stream
+  int64_t q_ss;
+  const void* kin;      // kin[s][g][d]    stride in_ss per stream
+  const void* vin;
+  int64_t in_ss;
+  float* out;           // out[s][hq][d]   stride o_ss per stream
+  int64_t o_ss;
+  float* logits;        // optional record target [s][hq][j]
+  int64_t l_ss, l_hs;
+  float* stats;         // [s][hq][2] (M, L) of this step
+  int64_t st_ss;
+  float* part;          // scratch [s][hq][split][D + 2]
+  int32_t* counters;    // [s][g], zero between launches
+  // appended token metadata
+  int64_t* pos;         // pos[s*m_ss + t]
+  int8_t* modality;
+  int32_t* round_id;
+  int64_t m_ss;
+  int32_t* len;         // len[s*len_ss] = n after the step
+  int64_t len_ss;
+  int64_t* next_pos;    // next_pos[s*len_ss]
+  const int64_t* pos_in;  // optional device [S] explicit positions
+  int32_t round_value;
+  FoldArgs fold;        // previous step's row (fold.n == 0: none)
+};
+
+cudaError_t launch_decode(int dtype, int head_dim, int group, int streams, const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_fold(int streams, int pieces, const FoldArgs& f, int Hq, cudaStream_t st);
+
+// ----------------------------------------------------------------------------
+// K2: window-mean score + bias + radix top-k + recent merge (one CTA per window)
+// ----------------------------------------------------------------------------
+struct SelectArgs {
+  const float* rows;    // rows of window b: rows + b*r_bs + slot*row_stride
+  int64_t r_bs;
+  int row_stride;
+  const int32_t* wlen;  // wlen[b*w_bs + slot]
+  int64_t w_bs;
+  int ring_head;        // slot of the oldest row = (ring_head - count) mod W
+  int count, W;         // rows held, ring size
+  int n, l, r;
+  float bias;
+  int apply_bias;       // 0: raw window-mean scores (window_mean_scores only)
+  int32_t* kept32;      // optional [b*k_bs + i] int32
+  int64_t* kept64;      // optional int64 (stand-alone API)
+  int64_t k_bs;
+  float* scores;        // optional [b*s_bs + c]
+  int64_t s_bs;
+  int32_t* first_moved; // optional [b]: first i with kept[i] != i
+  int32_t* newlen;      // optional [b*w_bs + slot] ring lengths after remap
+  int scores_only;      // 1: stop after writing scores
+  int pad;              // keep-all rows: write -1 into kept[n, pad)
+};
+
+cudaError_t launch_select(int batches, const SelectArgs& a, cudaStream_t st);
+cudaError_t launch_topk(const float* scores, int n, int k, int64_t* out, cudaStream_t st);
+
+// ----------------------------------------------------------------------------
+// K3: in-place stable compaction dst[i] = src[kept[i]] for i in [first, m)
+// ----------------------------------------------------------------------------
+struct CompactArgs {
+  // KV rows: block (b, h): base + b*kv_bs + h*kv_hs bytes, rows of row_bytes
+  char* k;
+  char* v;
+  int64_t kv_bs, kv_hs;  // bytes
+  int heads;
+  int row_bytes;
+  // metadata per block b
+  int64_t* pos;
+  int8_t* modality;
+  int32_t* round_id;
+  int64_t m_bs;          // elements
+  // window rows per block b: rows + b*r_bs + slot*row_stride, lengths wlen/newlen
+  float* rows;
+  int64_t r_bs;
+  int row_stride;
+  int32_t* wlen;
+  const int32_t* newlen;
+  int64_t w_bs;
+  int W;
+  // kept sets
+  const int32_t* kept32;
+  const int64_t* kept64;
+  int64_t k_bs;
+  const int32_t* first_moved;  // optional per block
+  int m;                 // kept count
+  int32_t* len;          // optional len[b*len_bs] = m
+  int64_t len_bs;
+};
+
+cudaError_t launch_compact(int blocks, const CompactArgs& a, cudaStream_t st);
+
+}  // namespace skv

@@ -1,0 +1,277 @@
+"""Batched streaming-decode engine over the C ABI (the B200 hot path).
+
+``StreamEngine`` holds S independent streams (sessions) x L layers of a
+size-constrained KV cache on one GPU and runs, through libstreamkv_b200.so:
+
+* ``decode_layer`` / ``decode_step``: per layer, append the token's k/v, attend
+  over the cache (including the new token), aggregate the per-head
+  probabilities and push the row into the relevance window -- the hot body of
+  ``Session.decode_step`` (reference engine.py:264-273);
+* ``evict``: Algorithm 1 (window mean + attention bias + top-r + recent l) and
+  in-place compaction of K/V, token metadata and the window rows --
+  ``Session._evict_layer`` (engine.py:310-337) for every stream and layer;
+* ``run_period``: E decode steps followed by one eviction, the eviction cadence
+  of ``Session.start_round`` with an E-token prompt (engine.py:344-360).
+
+Tensors are torch CUDA tensors; q/k/v use the engine dtype, outputs float32.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import SkvConfig, check
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream] = None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    streams: int
+    layers: int
+    heads_q: int
+    heads_kv: int
+    head_dim: int
+    recent_len: int
+    relevant_budget: int
+    bias: float
+    window: int
+    capacity: int
+    dtype: torch.dtype = torch.bfloat16
+    head_agg: str = "mean"
+
+    @property
+    def budget(self) -> int:
+        return self.recent_len + self.relevant_budget
+
+
+class StreamEngine:
+    """S lock-stepped streams x L layers of the Inf-MLLM decode+evict path."""
+
+    def __init__(self, cfg: EngineConfig):
+        _lib.require_cuda()
+        if cfg.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("dtype must be torch.float32 or torch.bfloat16")
+        if cfg.head_agg not in ("mean", "max"):
+            raise ValueError(f"unknown head_agg {cfg.head_agg!r}")
+        self.cfg = cfg
+        self.lib = _lib.load()
+        c = SkvConfig(
+            streams=cfg.streams,
+            layers=cfg.layers,
+            heads_q=cfg.heads_q,
+            heads_kv=cfg.heads_kv,
+            head_dim=cfg.head_dim,
+            dtype=_lib.DTYPE_BF16 if cfg.dtype == torch.bfloat16 else _lib.DTYPE_F32,
+            recent_len=cfg.recent_len,
+            relevant_budget=cfg.relevant_budget,
+            bias=cfg.bias,
+            window=cfg.window,
+            capacity=cfg.capacity,
+            head_agg=_lib.AGG_MAX if cfg.head_agg == "max" else _lib.AGG_MEAN,
+        )
+        handle = ctypes.c_void_p()
+        torch.cuda.init()
+        check(self.lib.skv_create(ctypes.byref(c), ctypes.byref(handle)))
+        self._h = handle
+        self.cap = (cfg.capacity + 31) // 32 * 32
+        self.elt = 2 if cfg.dtype == torch.bfloat16 else 4
+
+    # ---------------------------------------------------------------- life --
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.skv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.lib.skv_device_bytes(self._h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.skv_kernel_launches(self._h))
+
+    # -------------------------------------------------------------- decode --
+    def _check_io(self, q, k, v, out, lead):
+        c = self.cfg
+        for name, t, heads in (("q", q, c.heads_q), ("k", k, c.heads_kv), ("v", v, c.heads_kv)):
+            want = (*lead, heads, c.head_dim)
+            if tuple(t.shape) != want:
+                raise ValueError(f"{name} shape {tuple(t.shape)} != {want}")
+            if t.dtype != c.dtype or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous CUDA {c.dtype} tensor")
+        want = (*lead, c.heads_q, c.head_dim)
+        if tuple(out.shape) != want or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous float32 CUDA tensor of shape {want}")
+
+    def decode_layer(self, layer: int, q, k, v, out=None, positions=None, record: bool = True):
+        """q (S,Hq,D), k/v (S,Hkv,D) -> out (S,Hq,D) float32."""
+        c = self.cfg
+        if out is None:
+            out = torch.empty((c.streams, c.heads_q, c.head_dim), dtype=torch.float32, device=q.device)
+        self._check_io(q, k, v, out, (c.streams,))
+        pos = None
+        if positions is not None:
+            arr = np.ascontiguousarray(np.asarray(positions, dtype=np.int64).reshape(c.streams))
+            pos = arr.ctypes.data_as(ctypes.c_void_p)
+        check(self.lib.skv_decode_layer(self._h, layer, _ptr(q), _ptr(k), _ptr(v), pos, _ptr(out),
+                                        int(bool(record)), _stream_handle()))
+        return out
+
+    def decode_step(self, q, k, v, out=None, record: bool = True):
+        """All layers of one token: q (L,S,Hq,D), k/v (L,S,Hkv,D) -> out (L,S,Hq,D)."""
+        c = self.cfg
+        if out is None:
+            out = torch.empty((c.layers, c.streams, c.heads_q, c.head_dim), dtype=torch.float32,
+                              device=q.device)
+        self._check_io(q, k, v, out, (c.layers, c.streams))
+        check(self.lib.skv_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), int(bool(record)),
+                                       _stream_handle()))
+        return out
+
+    def decode_step_host(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
+                         record: bool = True):
+        """Same as decode_step with host (ideally pinned) tensors; synchronous."""
+        c = self.cfg
+        lead = (c.layers, c.streams)
+        for name, t, heads in (("q", q, c.heads_q), ("k", k, c.heads_kv), ("v", v, c.heads_kv)):
+            if tuple(t.shape) != (*lead, heads, c.head_dim) or t.dtype != c.dtype or t.is_cuda:
+                raise ValueError(f"{name} must be a host {c.dtype} tensor of shape {(*lead, heads, c.head_dim)}")
+        if out.is_cuda or out.dtype != torch.float32:
+            raise ValueError("out must be a host float32 tensor")
+        check(self.lib.skv_decode_step_host(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), int(bool(record))))
+        return out
+
+    # --------------------------------------------------------------- evict --
+    def evict(self, layer: int = -1, kept: Optional[torch.Tensor] = None):
+        """Algorithm 1 + compaction for every stream of ``layer`` (-1: all layers).
+
+        ``kept`` (optional, int32 CUDA, (S, L', r+l)) receives the kept sets;
+        rows of a keep-all decision hold 0..n-1 padded with -1."""
+        check(self.lib.skv_evict(self._h, int(layer), _ptr(kept), _stream_handle()))
+        return kept
+
+    def run_period(self, q, k, v, out, steps: int, evict: bool = True):
+        """``steps`` decode steps (inputs indexed [t] along dim 0) + one eviction.
+
+        Only the last ``window`` steps record window rows: older rows leave the
+        window before the eviction reads it, so the decisions are identical to
+        recording every step (AttentionWindow.push drops the oldest row,
+        policies.py:113-115)."""
+        first_rec = steps - self.cfg.window
+        for t in range(steps):
+            self.decode_step(q[t], k[t], v[t], out, record=t >= first_rec)
+        if evict:
+            self.evict(-1)
+        return out
+
+    # --------------------------------------------------------------- state --
+    def length(self, stream: int = 0, layer: int = 0) -> int:
+        return check(self.lib.skv_length(self._h, stream, layer))
+
+    def kv(self, stream: int, layer: int):
+        """Views (Hkv, n, D) of the live keys/values of (stream, layer)."""
+        kp, vp = ctypes.c_void_p(), ctypes.c_void_p()
+        check(self.lib.skv_kv_view(self._h, stream, layer, ctypes.byref(kp), ctypes.byref(vp)))
+        c = self.cfg
+        n = self.length(stream, layer)
+        full = (c.heads_kv, self.cap, c.head_dim)
+        kt = _wrap(kp.value, full, c.dtype)
+        vt = _wrap(vp.value, full, c.dtype)
+        return kt[:, :n], vt[:, :n]
+
+    def kv_full(self, stream: int, layer: int):
+        kp, vp = ctypes.c_void_p(), ctypes.c_void_p()
+        check(self.lib.skv_kv_view(self._h, stream, layer, ctypes.byref(kp), ctypes.byref(vp)))
+        c = self.cfg
+        full = (c.heads_kv, self.cap, c.head_dim)
+        return _wrap(kp.value, full, c.dtype), _wrap(vp.value, full, c.dtype)
+
+    def positions(self, stream: int, layer: int) -> np.ndarray:
+        out = np.zeros(self.cap, dtype=np.int64)
+        n = check(self.lib.skv_positions(self._h, stream, layer, out.ctypes.data_as(ctypes.c_void_p), self.cap))
+        return out[:n]
+
+    def window_rows(self, stream: int, layer: int):
+        rows = np.zeros((self.cfg.window, self.cap), dtype=np.float32)
+        lens = np.zeros(self.cfg.window, dtype=np.int32)
+        m = check(self.lib.skv_window_rows(self._h, stream, layer, rows.ctypes.data_as(ctypes.c_void_p),
+                                           lens.ctypes.data_as(ctypes.c_void_p)))
+        return [rows[i, : lens[i]].copy() for i in range(m)]
+
+    def last_scores(self, stream: int, layer: int, cols: int) -> np.ndarray:
+        out = np.zeros(self.cap, dtype=np.float32)
+        check(self.lib.skv_last_scores(self._h, stream, layer, out.ctypes.data_as(ctypes.c_void_p), self.cap))
+        return out[:cols].copy()
+
+    def inject(self, stream: int, layer: int, keys: np.ndarray, values: np.ndarray, positions: np.ndarray,
+               rows=None):
+        """State injection for parity: keys/values (Hkv, n, D) in engine dtype
+        (float32 arrays are rounded to bf16 for a bf16 engine), positions (n,),
+        rows: list of window rows (oldest first)."""
+        c = self.cfg
+        n = keys.shape[1]
+        kt = torch.as_tensor(np.ascontiguousarray(keys, dtype=np.float32)).to(c.dtype).contiguous()
+        vt = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float32)).to(c.dtype).contiguous()
+        pos = np.ascontiguousarray(positions, dtype=np.int64)
+        rows = rows or []
+        m = len(rows)
+        rbuf = np.zeros((max(m, 1), max(n, 1)), dtype=np.float32)
+        lens = np.zeros(max(m, 1), dtype=np.int32)
+        for i, r in enumerate(rows):
+            rbuf[i, : r.size] = r
+            lens[i] = r.size
+        check(self.lib.skv_state_inject(self._h, stream, layer, n, _ptr(kt), _ptr(vt),
+                                        pos.ctypes.data_as(ctypes.c_void_p), m,
+                                        rbuf.ctypes.data_as(ctypes.c_void_p),
+                                        lens.ctypes.data_as(ctypes.c_void_p)))
+
+    # -------------------------------------------------------------- graphs --
+    def capture_begin(self):
+        check(self.lib.skv_capture_begin(self._h, _stream_handle()))
+
+    def capture_end(self):
+        check(self.lib.skv_capture_end(self._h, _stream_handle()))
+
+    def replay(self):
+        check(self.lib.skv_graph_launch(self._h, _stream_handle()))
+
+
+def _wrap(ptr: int, shape, dtype: torch.dtype) -> torch.Tensor:
+    """Zero-copy torch view of engine-owned device memory."""
+    typestr = {torch.float32: "<f4", torch.bfloat16: "<V2"}[dtype]
+    elt = 4 if dtype == torch.float32 else 2
+
+    class _Iface:
+        __cuda_array_interface__ = {
+            "shape": tuple(shape),
+            "typestr": typestr if dtype == torch.float32 else "<i2",
+            "data": (ptr, False),
+            "version": 2,
+            "strides": None,
+        }
+
+    t = torch.as_tensor(_Iface(), device="cuda")
+    if dtype == torch.bfloat16:
+        t = t.view(torch.bfloat16)
+    assert t.element_size() == elt
+    return t

@@ -1,0 +1,214 @@
+"""Drop-in for ``streamkv.policies`` (reference policies.py:28-265) on the GPU.
+
+Same names, argument order, return types and ``ValueError`` domain errors.
+The decision functions run the CUDA kernels of libstreamkv_b200.so:
+``window_mean_scores`` / ``inf_mllm_decide`` the K2 score+bias+radix-select
+kernel, ``top_k_indices`` its block radix top-k.  Inputs may be NumPy arrays /
+lists (results come back as NumPy, like the reference) or CUDA tensors
+(results stay on the device).  The comparison baselines (sliding window,
+sink+recent, heavy hitter; policies.py:204-256) are outside the hot path and
+are not provided.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+
+F32 = np.float32
+
+HEAD_AGG_MEAN = "mean"
+HEAD_AGG_MAX = "max"
+
+
+def _sh():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _to_dev_f32(x):
+    """(tensor on cuda f32, came_from_host)"""
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            return x.to(torch.float32).contiguous(), False
+        return x.to(torch.float32).contiguous().cuda(), True
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=F32))).cuda(), True
+
+
+def _out(t: torch.Tensor, host: bool):
+    return t.cpu().numpy() if host else t
+
+
+@dataclass
+class PolicyConfig:
+    """policies.py:28-59."""
+
+    recent_len: int = 32
+    relevant_budget: int = 2016
+    bias: float = 0.1
+    sink_count: int = 4
+    head_agg: str = HEAD_AGG_MEAN
+
+    def __post_init__(self):
+        if self.recent_len < 1:
+            raise ValueError("recent_len must be >= 1")
+        if self.relevant_budget < 0:
+            raise ValueError("relevant_budget must be >= 0")
+        if self.bias < 0:
+            raise ValueError("bias must be >= 0")
+        if self.sink_count < 0:
+            raise ValueError("sink_count must be >= 0")
+        if self.head_agg not in (HEAD_AGG_MEAN, HEAD_AGG_MAX):
+            raise ValueError(f"unknown head_agg {self.head_agg!r}")
+
+    @property
+    def budget(self) -> int:
+        return self.recent_len + self.relevant_budget
+
+
+@dataclass(frozen=True)
+class EvictionDecision:
+    """policies.py:62-84 (int64 index sets)."""
+
+    relevant: object
+    recent: object
+    kept: object
+
+    @staticmethod
+    def from_sets(relevant, recent) -> "EvictionDecision":
+        rel = np.asarray(sorted(set(int(i) for i in relevant)), dtype=np.int64)
+        rec = np.asarray(sorted(set(int(i) for i in recent)), dtype=np.int64)
+        return EvictionDecision(relevant=rel, recent=rec, kept=np.union1d(rel, rec).astype(np.int64))
+
+    @staticmethod
+    def keep_all(n: int, recent_len: int) -> "EvictionDecision":
+        k = min(recent_len, n)
+        return EvictionDecision(
+            relevant=np.arange(0, n - k, dtype=np.int64),
+            recent=np.arange(n - k, n, dtype=np.int64),
+            kept=np.arange(n, dtype=np.int64),
+        )
+
+
+class AttentionWindow:
+    """Rolling buffer of the last ``capacity`` rows (policies.py:87-127), rows on the GPU."""
+
+    def __init__(self, capacity: int):
+        if capacity < 1:
+            raise ValueError("window capacity must be >= 1")
+        self.capacity = capacity
+        self._rows: List[torch.Tensor] = []
+        self._host = True
+
+    def __len__(self) -> int:
+        return len(self._rows)
+
+    @property
+    def rows(self):
+        return [r.cpu().numpy() for r in self._rows] if self._host else list(self._rows)
+
+    def push(self, row) -> None:
+        r, host = _to_dev_f32(row)
+        if r.ndim != 1 or r.numel() == 0:
+            raise ValueError("row must be a non-empty vector")
+        if self._rows and r.numel() < self._rows[-1].numel():
+            raise ValueError("row column count may not shrink between evictions")
+        self._host = host
+        self._rows.append(r.clone())
+        if len(self._rows) > self.capacity:
+            del self._rows[0]
+
+    def remap(self, kept) -> None:
+        idx = torch.as_tensor(np.asarray(kept, dtype=np.int64) if not isinstance(kept, torch.Tensor) else kept)
+        idx = idx.to(device="cuda", dtype=torch.int64)
+        self._rows = [row[idx[idx < row.numel()]] for row in self._rows]
+
+    def clear(self) -> None:
+        self._rows = []
+
+    def _packed(self, n: int):
+        m = len(self._rows)
+        width = max(max(r.numel() for r in self._rows), n)
+        buf = torch.zeros((m, width), dtype=torch.float32, device="cuda")
+        lens = torch.empty(m, dtype=torch.int32)
+        for i, r in enumerate(self._rows):
+            buf[i, : r.numel()] = r
+            lens[i] = r.numel()
+        return buf, lens.cuda(), width
+
+
+def window_mean_scores(window: AttentionWindow, n: int, l: int):
+    """policies.py:130-147 on device (bit-exact float32 order)."""
+    if len(window) == 0:
+        raise ValueError("attention window is empty")
+    if n <= l:
+        raise ValueError(f"no scorable columns: n={n} <= l={l}")
+    buf, lens, width = window._packed(n)
+    out = torch.empty(n - l, dtype=torch.float32, device="cuda")
+    check(_lib.load().skv_window_scores(_p(buf), width, _p(lens), len(window), n, l, 0.0, 0, _p(out), _sh()))
+    return _out(out, window._host)
+
+
+def bias_vector(n: int, l: int, b: float):
+    """policies.py:150-162: d = f32(b)/f32(n-l); bias[c] = (-d)*f32(n-l-1-c)."""
+    if n <= l:
+        raise ValueError(f"no scorable columns: n={n} <= l={l}")
+    if b < 0:
+        raise ValueError("bias must be >= 0")
+    cols = n - l
+    d = F32(b) / F32(cols)
+    return (-d) * np.arange(cols - 1, -1, -1, dtype=F32)
+
+
+def top_k_indices(scores, k: int):
+    """policies.py:165-181 on device: ascending indices, ties toward the larger index."""
+    if k < 0:
+        raise ValueError("k must be >= 0")
+    s, host = _to_dev_f32(scores)
+    s = s.reshape(-1)
+    n = s.numel()
+    m = min(k, n)
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    if m > 0:
+        check(_lib.load().skv_top_k(_p(s), n, k, _p(out), _sh()))
+    return _out(out, host)
+
+
+def inf_mllm_decide(window: AttentionWindow, n: int, cfg: PolicyConfig) -> EvictionDecision:
+    """policies.py:184-201 on device (K2: scores, bias, radix top-r, recent merge)."""
+    if len(window) == 0:
+        raise ValueError("attention window is empty")
+    l, r = cfg.recent_len, cfg.relevant_budget
+    if n <= r + l:
+        return EvictionDecision.keep_all(n, l)
+    buf, lens, width = window._packed(n)
+    kept = torch.empty(r + l, dtype=torch.int64, device="cuda")
+    scores = torch.empty(n - l, dtype=torch.float32, device="cuda")
+    check(_lib.load().skv_decide(_p(buf), width, _p(lens), len(window), n, l, r, float(cfg.bias), _p(kept),
+                                 _p(scores), _sh()))
+    host = window._host
+    kept_o = _out(kept, host)
+    return EvictionDecision(relevant=kept_o[:r], recent=kept_o[r:], kept=kept_o)
+
+
+def aggregate_heads(per_head, how: str):
+    """policies.py:259-265: sequential float32 head sum / H (or max) on device."""
+    if how not in (HEAD_AGG_MEAN, HEAD_AGG_MAX):
+        raise ValueError(f"unknown head aggregation {how!r}")
+    p, host = _to_dev_f32(per_head)
+    if how == HEAD_AGG_MAX:
+        return _out(p.max(dim=0).values, host)
+    acc = p[0].clone()
+    for h in range(1, p.shape[0]):
+        acc += p[h]
+    return _out(acc / F32(p.shape[0]), host)

@@ -28,7 +28,7 @@ CASES = {
                      dtype="bf16", seed=1003, saddles=0, saddle_gain=1.0, spike_prob=0.005,
                      spike_gain=4.0, out_every=32),
     # window longer than the eviction period: exercises window remap.
-    "wide_window": dict(S=1, L=1, Hq=4, Hkv=4, D=32, T=320, l=16, r=32, W=40, b=0.1, E=16,
+    "wide_window": dict(S=1, L=1, Hq=4, Hkv=4, D=64, T=320, l=16, r=32, W=40, b=0.1, E=16,
                         dtype="f32", seed=1004, saddles=3, saddle_gain=5.0, spike_prob=0.0,
                         spike_gain=1.0, out_every=16),
 }
