@@ -83,11 +83,25 @@ __device__ __forceinline__ void fold_piece(const FoldArgs& f, int s, int piece, 
   if (piece == 0 && tid == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
 }
 
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// CTA that owns global tile t under the even split [c*T/P, (c+1)*T/P).
+__device__ __forceinline__ int tile_owner(int64_t t, int64_t T, int P) {
+  return (int)(((t + 1) * P + T - 1) / T) - 1;
+}
+
+// Persistent stream-K decode: CTA c streams the global tile range
+// [c*T/P, (c+1)*T/P) of the (segment, tile) space, crossing segment (stream,
+// kv-head) boundaries without draining its TMA pipeline.  At the end of each
+// segment piece it publishes a partial (m, l, o) and the last contributor of
+// the segment merges the pieces in CTA order (deterministic).
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
   using Gm = Geo<T, D>;
   constexpr int TT = Gm::TT, RB = Gm::RB, LPR = Gm::LPR, EPL = Gm::EPL, RPW = Gm::RPW;
   constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Gm::STAGES, TILE = Gm::TILE;
+  constexpr int PW = D + 2;  // floats per head in a partial
 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* tiles = smem;
@@ -99,18 +113,12 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
   float* fin = wo + NW * G * D;                          // [G][2] merged (M, L)
   int* flag = reinterpret_cast<int*>(fin + 2 * G);
 
-  const int split = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+  const int c = blockIdx.x, P = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n_old + a.append;
-  const int t0 = split * a.chunk;
-  const int t1 = min(t0 + a.chunk, n);
-  const int ntiles = t1 > t0 ? (t1 - t0 + TT - 1) / TT : 0;
+  const int64_t a0 = (int64_t)c * a.T / P, a1 = (int64_t)(c + 1) * a.T / P;
 
-  const T* kbase = static_cast<const T*>(a.kc) + s * a.c_ss + (int64_t)g * a.c_hs;
-  const T* vbase = static_cast<const T*>(a.vc) + s * a.c_ss + (int64_t)g * a.c_hs;
-  const T* knew = static_cast<const T*>(a.kin) + s * a.in_ss + (int64_t)g * D;
-  const T* vnew = static_cast<const T*>(a.vin) + s * a.in_ss + (int64_t)g * D;
-
+  griddep_launch();
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < STAGES; ++i) {
@@ -124,23 +132,37 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
   if (warp == NW) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      for (int it = 0; it < ntiles; ++it) {
-        const int st = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[st], ph ^ 1);
-        const int ts = t0 + it * TT;
-        const int rows = min(TT, t1 - ts);
+      bool waited = false;
+      if (!a.prefetch) {
+        griddep_wait();
+        waited = true;
+      }
+      int i = 0;
+      for (int64_t t = a0; t < a1; ++t, ++i) {
+        const int sigma = (int)(t / a.nt);
+        const int ts = (int)(t - (int64_t)sigma * a.nt) * TT;
+        const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+        const int rows = min(TT, n - ts);
         const int rc = max(0, min(rows, a.n_old - ts));
+        const int st = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[st], ph ^ 1);
         unsigned char* ks = tiles + (2 * st) * TILE;
         unsigned char* vs = ks + TILE;
         mbar_arrive_expect_tx(&full[st], 2u * rows * RB);
+        const int64_t base = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)ts * D;
         if (rc > 0) {
-          bulk_g2s(ks, kbase + (int64_t)ts * D, rc * RB, &full[st]);
-          bulk_g2s(vs, vbase + (int64_t)ts * D, rc * RB, &full[st]);
+          bulk_g2s(ks, static_cast<const T*>(a.kc) + base, rc * RB, &full[st]);
+          bulk_g2s(vs, static_cast<const T*>(a.vc) + base, rc * RB, &full[st]);
         }
         if (rc < rows) {  // the appended token: straight from the step input
-          bulk_g2s(ks + rc * RB, knew, RB, &full[st]);
-          bulk_g2s(vs + rc * RB, vnew, RB, &full[st]);
+          if (!waited) {
+            griddep_wait();
+            waited = true;
+          }
+          const int64_t in = s * a.in_ss + (int64_t)g * D;
+          bulk_g2s(ks + rc * RB, static_cast<const T*>(a.kin) + in, RB, &full[st]);
+          bulk_g2s(vs + rc * RB, static_cast<const T*>(a.vin) + in, RB, &full[st]);
         }
       }
     }
@@ -148,35 +170,41 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
   }
 
   // -------------------------------------------------------------- consumers
+  griddep_wait();  // q, out, logits, partials and counters cross launches
   const int rsub = lane / LPR, c16 = lane % LPR;
   float qf[G][EPL];
-#pragma unroll
-  for (int h = 0; h < G; ++h)
-    Vec16<T>::load(qf[h], static_cast<const T*>(a.q) + s * a.q_ss + (int64_t)(g * G + h) * D + c16 * EPL);
-
   float m_run[G], l_run[G], o[G][EPL];
+  float* lg = nullptr;
+  int cur = -1;
+  int i = 0;
+  for (int64_t t = a0; t < a1; ++t, ++i) {
+    const int sigma = (int)(t / a.nt);
+    const int tt = (int)(t - (int64_t)sigma * a.nt);
+    const int ts = tt * TT;
+    const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+    if (sigma != cur) {
+      cur = sigma;
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    m_run[h] = -INFINITY;
-    l_run[h] = 0.f;
+      for (int h = 0; h < G; ++h) {
+        Vec16<T>::load(qf[h], static_cast<const T*>(a.q) + s * a.q_ss + (int64_t)(g * G + h) * D + c16 * EPL);
+        m_run[h] = -INFINITY;
+        l_run[h] = 0.f;
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) o[h][e] = 0.f;
-  }
-  float* lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int st = it % STAGES;
-    const uint32_t ph = (it / STAGES) & 1;
-    const int ts = t0 + it * TT;
-    const int rows = min(TT, t1 - ts);
+        for (int e = 0; e < EPL; ++e) o[h][e] = 0.f;
+      }
+      lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+    }
+    const int st = i % STAGES;
+    const uint32_t ph = (i / STAGES) & 1;
+    const int rows = min(TT, n - ts);
     const unsigned char* ks = tiles + (2 * st) * TILE;
     const unsigned char* vs = ks + TILE;
     mbar_wait(&full[st], ph);
 
     float sc[ITERS][G];
 #pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
-      const int row = warp * Gm::RPWARP + i * RPW + rsub;
+    for (int it = 0; it < ITERS; ++it) {
+      const int row = warp * Gm::RPWARP + it * RPW + rsub;
       float kf[EPL];
       Vec16<T>::load(kf, ks + row * RB + c16 * 16);
 #pragma unroll
@@ -186,16 +214,16 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
         for (int e = 0; e < EPL; ++e) d = fmaf(qf[h][e], kf[e], d);
 #pragma unroll
         for (int off = LPR / 2; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-        sc[i][h] = row < rows ? d * a.scale : -INFINITY;
+        sc[it][h] = row < rows ? d * a.scale : -INFINITY;
       }
     }
     if (lg && c16 == 0) {
 #pragma unroll
-      for (int i = 0; i < ITERS; ++i) {
-        const int row = warp * Gm::RPWARP + i * RPW + rsub;
+      for (int it = 0; it < ITERS; ++it) {
+        const int row = warp * Gm::RPWARP + it * RPW + rsub;
         if (row < rows) {
 #pragma unroll
-          for (int h = 0; h < G; ++h) lg[h * a.l_hs + ts + row] = sc[i][h];
+          for (int h = 0; h < G; ++h) lg[h * a.l_hs + ts + row] = sc[it][h];
         }
       }
     }
@@ -204,16 +232,16 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
     for (int h = 0; h < G; ++h) {
       float mt = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < ITERS; ++i) mt = fmaxf(mt, sc[i][h]);
+      for (int it = 0; it < ITERS; ++it) mt = fmaxf(mt, sc[it][h]);
 #pragma unroll
       for (int off = LPR; off < 32; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
       const float mn = fmaxf(m_run[h], mt);
       const float alpha = rescale(m_run[h], mn);
       float ps = 0.f;
 #pragma unroll
-      for (int i = 0; i < ITERS; ++i) {
-        p[i][h] = mn == -INFINITY ? 0.f : exp2f((sc[i][h] - mn) * kLog2e);
-        ps += p[i][h];
+      for (int it = 0; it < ITERS; ++it) {
+        p[it][h] = mn == -INFINITY ? 0.f : exp2f((sc[it][h] - mn) * kLog2e);
+        ps += p[it][h];
       }
       l_run[h] = l_run[h] * alpha + ps;
 #pragma unroll
@@ -221,121 +249,133 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
       m_run[h] = mn;
     }
 #pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
-      const int row = warp * Gm::RPWARP + i * RPW + rsub;
+    for (int it = 0; it < ITERS; ++it) {
+      const int row = warp * Gm::RPWARP + it * RPW + rsub;
       if (row < rows) {
         float vf[EPL];
         Vec16<T>::load(vf, vs + row * RB + c16 * 16);
 #pragma unroll
         for (int h = 0; h < G; ++h)
 #pragma unroll
-          for (int e = 0; e < EPL; ++e) o[h][e] = fmaf(p[i][h], vf[e], o[h][e]);
+          for (int e = 0; e < EPL; ++e) o[h][e] = fmaf(p[it][h], vf[e], o[h][e]);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-  }
 
-  // ---- warp -> CTA partial
+    if (tt != a.nt - 1 && t != a1 - 1) continue;
+
+    // ================= end of this CTA's piece of segment sigma =================
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    float l = l_run[h];
+    for (int h = 0; h < G; ++h) {
+      float l = l_run[h];
 #pragma unroll
-    for (int off = LPR; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      for (int off = LPR; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      float v = o[h][e];
+      for (int e = 0; e < EPL; ++e) {
+        float v = o[h][e];
 #pragma unroll
-      for (int off = LPR; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      o[h][e] = v;
-    }
-    if (rsub == 0) {
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) wo[(warp * G + h) * D + c16 * EPL + e] = o[h][e];
-    }
-    if (lane == 0) {
-      wm[warp * G + h] = m_run[h];
-      wl[warp * G + h] = l;
-    }
-  }
-  consumers_sync();
-  {
-    float* part = a.part + ((int64_t)s * a.Hq + g * G) * a.splits * (D + 2);
-    for (int idx = tid; idx < G * (D + 2); idx += 128) {
-      const int h = idx / (D + 2), d = idx % (D + 2);
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w * G + h]);
-      float acc = 0.f;
-      if (d < D) {
-#pragma unroll
-        for (int w = 0; w < NW; ++w) acc += rescale(wm[w * G + h], M) * wo[(w * G + h) * D + d];
-      } else if (d == D) {
-        acc = M;
-      } else {
-#pragma unroll
-        for (int w = 0; w < NW; ++w) acc += rescale(wm[w * G + h], M) * wl[w * G + h];
+        for (int off = LPR; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        o[h][e] = v;
       }
-      part[((int64_t)h * a.splits + split) * (D + 2) + d] = acc;
+      if (rsub == 0) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) wo[(warp * G + h) * D + c16 * EPL + e] = o[h][e];
+      }
+      if (lane == 0) {
+        wm[warp * G + h] = m_run[h];
+        wl[warp * G + h] = l;
+      }
     }
+    consumers_sync();
+    {
+      float* part = a.part + (int64_t)(sigma + c) * G * PW;
+      for (int idx = tid; idx < G * PW; idx += 128) {
+        const int h = idx / PW, d = idx - h * PW;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w * G + h]);
+        float acc = 0.f;
+        if (d < D) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) acc += rescale(wm[w * G + h], M) * wo[(w * G + h) * D + d];
+        } else if (d == D) {
+          acc = M;
+        } else {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) acc += rescale(wm[w * G + h], M) * wl[w * G + h];
+        }
+        part[idx] = acc;
+      }
+    }
+    // append: the new row and (once per stream) its metadata go to slot n_old
+    if (a.append && tt == a.nt - 1) {
+      const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
+      const int64_t in = s * a.in_ss + (int64_t)g * D;
+      for (int u = tid; u < RB / 16; u += 128) {
+        reinterpret_cast<uint4*>(static_cast<T*>(a.kc) + dst)[u] =
+            reinterpret_cast<const uint4*>(static_cast<const T*>(a.kin) + in)[u];
+        reinterpret_cast<uint4*>(static_cast<T*>(a.vc) + dst)[u] =
+            reinterpret_cast<const uint4*>(static_cast<const T*>(a.vin) + in)[u];
+      }
+      if (g == 0 && tid == 0) {
+        int64_t* np = a.next_pos + s * a.len_ss;
+        const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
+        a.pos[s * a.m_ss + a.n_old] = pv;
+        a.modality[s * a.m_ss + a.n_old] = 0;
+        a.round_id[s * a.m_ss + a.n_old] = a.round_value;
+        *np = pv + 1;
+        a.len[s * a.len_ss] = n;
+      }
+    }
+    __threadfence();
+    consumers_sync();
+    const int64_t seg0 = (int64_t)sigma * a.nt;
+    const int c_lo = tile_owner(seg0, a.T, P);
+    const int c_hi = tile_owner(seg0 + a.nt - 1, a.T, P);
+    if (tid == 0) {
+      const int prev = atomicAdd(&a.counters[sigma], 1);
+      *flag = prev == c_hi - c_lo;
+    }
+    consumers_sync();
+    if (*flag) {
+      __threadfence();
+      if (tid < G) {
+        float M = -INFINITY;
+        for (int cc = c_lo; cc <= c_hi; ++cc) M = fmaxf(M, __ldcg(a.part + ((int64_t)(sigma + cc) * G + tid) * PW + D));
+        float L = 0.f;
+        for (int cc = c_lo; cc <= c_hi; ++cc) {
+          const float* pp = a.part + ((int64_t)(sigma + cc) * G + tid) * PW;
+          L += rescale(__ldcg(pp + D), M) * __ldcg(pp + D + 1);
+        }
+        fin[2 * tid] = M;
+        fin[2 * tid + 1] = L;
+        if (a.stats) {
+          a.stats[s * a.st_ss + (g * G + tid) * 2] = M;
+          a.stats[s * a.st_ss + (g * G + tid) * 2 + 1] = L;
+        }
+      }
+      consumers_sync();
+      for (int idx = tid; idx < G * D; idx += 128) {
+        const int h = idx / D, d = idx - h * D;
+        const float M = fin[2 * h], L = fin[2 * h + 1];
+        float acc = 0.f;
+        for (int cc = c_lo; cc <= c_hi; ++cc) {
+          const float* pp = a.part + ((int64_t)(sigma + cc) * G + h) * PW;
+          acc += rescale(__ldcg(pp + D), M) * __ldcg(pp + d);
+        }
+        a.out[s * a.o_ss + (int64_t)(g * G + h) * D + d] = acc / L;
+      }
+      if (tid == 0) a.counters[sigma] = 0;
+    }
+    consumers_sync();
   }
 
-  // ---- append: the new row and its metadata go to cache slot n_old
-  if (a.append && a.n_old >= t0 && a.n_old < t1) {
-    T* kdst = static_cast<T*>(a.kc) + s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
-    T* vdst = static_cast<T*>(a.vc) + s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
-    for (int i = tid; i < RB / 16; i += 128) {
-      reinterpret_cast<uint4*>(kdst)[i] = reinterpret_cast<const uint4*>(knew)[i];
-      reinterpret_cast<uint4*>(vdst)[i] = reinterpret_cast<const uint4*>(vnew)[i];
-    }
-    if (g == 0 && tid == 0) {
-      int64_t* np = a.next_pos + s * a.len_ss;
-      const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
-      a.pos[s * a.m_ss + a.n_old] = pv;
-      a.modality[s * a.m_ss + a.n_old] = 0;
-      a.round_id[s * a.m_ss + a.n_old] = a.round_value;
-      *np = pv + 1;
-      a.len[s * a.len_ss] = n;
-    }
+  // ---- previous step's window row, spread over the CTAs
+  if (a.fold.n > 0) {
+    const int fp = max(1, P / a.S);
+    for (int idx = c; idx < a.S * fp; idx += P) fold_piece(a.fold, idx / fp, idx % fp, fp, a.Hq, tid, 128);
   }
-
-  // ---- previous step's window row, spread over every CTA of the launch
-  fold_piece(a.fold, s, split * a.Hkv + g, a.splits * a.Hkv, a.Hq, tid, 128);
-
-  // ---- split combine by the last CTA of (stream, kv-head)
-  __threadfence();
-  consumers_sync();
-  if (tid == 0) {
-    const int prev = atomicAdd(&a.counters[s * a.Hkv + g], 1);
-    *flag = prev == a.splits - 1;
-  }
-  consumers_sync();
-  if (!*flag) return;
-  __threadfence();
-  const float* part = a.part + ((int64_t)s * a.Hq + g * G) * a.splits * (D + 2);
-  if (tid < G) {
-    const float* ph = part + (int64_t)tid * a.splits * (D + 2);
-    float M = -INFINITY;
-    for (int c = 0; c < a.splits; ++c) M = fmaxf(M, __ldcg(ph + c * (D + 2) + D));
-    float L = 0.f;
-    for (int c = 0; c < a.splits; ++c) L += rescale(__ldcg(ph + c * (D + 2) + D), M) * __ldcg(ph + c * (D + 2) + D + 1);
-    fin[2 * tid] = M;
-    fin[2 * tid + 1] = L;
-    if (a.stats) {
-      a.stats[s * a.st_ss + (g * G + tid) * 2] = M;
-      a.stats[s * a.st_ss + (g * G + tid) * 2 + 1] = L;
-    }
-  }
-  consumers_sync();
-  for (int idx = tid; idx < G * D; idx += 128) {
-    const int h = idx / D, d = idx % D;
-    const float* ph = part + (int64_t)h * a.splits * (D + 2);
-    const float M = fin[2 * h], L = fin[2 * h + 1];
-    float acc = 0.f;
-    for (int c = 0; c < a.splits; ++c) acc += rescale(__ldcg(ph + c * (D + 2) + D), M) * __ldcg(ph + c * (D + 2) + d);
-    a.out[s * a.o_ss + (int64_t)(g * G + h) * D + d] = acc / L;
-  }
-  if (tid == 0) a.counters[s * a.Hkv + g] = 0;
 }
 
 __global__ void fold_kernel(const FoldArgs f, int Hq) {
@@ -350,7 +390,7 @@ static size_t decode_smem() {
 }
 
 template <typename T, int D, int G>
-static cudaError_t launch_decode_t(int streams, const AttnArgs& a, cudaStream_t st) {
+static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st) {
   const size_t smem = decode_smem<T, D, G>();
   static bool attr = false;
   if (!attr) {
@@ -359,29 +399,66 @@ static cudaError_t launch_decode_t(int streams, const AttnArgs& a, cudaStream_t 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(a.splits, a.Hkv, streams);
-  decode_kernel<T, D, G><<<grid, 160, smem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(160);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_kernel<T, D, G>, a);
+}
+
+template <typename T, int D, int G>
+static int occupancy_t() {
+  static int occ = 0;
+  if (!occ) {
+    const size_t smem = decode_smem<T, D, G>();
+    cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, 160, smem) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+  }
+  return occ;
 }
 
 template <typename T, int D>
-static cudaError_t dispatch_group(int group, int streams, const AttnArgs& a, cudaStream_t st) {
+static cudaError_t dispatch_group(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
   switch (group) {
-    case 1: return launch_decode_t<T, D, 1>(streams, a, st);
-    case 2: return launch_decode_t<T, D, 2>(streams, a, st);
-    case 4: return launch_decode_t<T, D, 4>(streams, a, st);
-    case 8: return launch_decode_t<T, D, 8>(streams, a, st);
+    case 1: return launch_decode_t<T, D, 1>(ctas, a, st);
+    case 2: return launch_decode_t<T, D, 2>(ctas, a, st);
+    case 4: return launch_decode_t<T, D, 4>(ctas, a, st);
+    case 8: return launch_decode_t<T, D, 8>(ctas, a, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_decode(int dtype, int head_dim, int group, int streams, const AttnArgs& a, cudaStream_t st) {
+template <typename T, int D>
+static int occ_group(int group) {
+  switch (group) {
+    case 1: return occupancy_t<T, D, 1>();
+    case 2: return occupancy_t<T, D, 2>();
+    case 4: return occupancy_t<T, D, 4>();
+    case 8: return occupancy_t<T, D, 8>();
+    default: return 1;
+  }
+}
+
+int decode_ctas_per_sm(int dtype, int head_dim, int group) {
+  if (dtype == 1) return head_dim == 128 ? occ_group<__nv_bfloat16, 128>(group) : occ_group<__nv_bfloat16, 64>(group);
+  return head_dim == 128 ? occ_group<float, 128>(group) : occ_group<float, 64>(group);
+}
+
+cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st) {
   if (dtype == 1) {
-    if (head_dim == 128) return dispatch_group<__nv_bfloat16, 128>(group, streams, a, st);
-    if (head_dim == 64) return dispatch_group<__nv_bfloat16, 64>(group, streams, a, st);
+    if (head_dim == 128) return dispatch_group<__nv_bfloat16, 128>(group, ctas, a, st);
+    if (head_dim == 64) return dispatch_group<__nv_bfloat16, 64>(group, ctas, a, st);
   } else {
-    if (head_dim == 128) return dispatch_group<float, 128>(group, streams, a, st);
-    if (head_dim == 64) return dispatch_group<float, 64>(group, streams, a, st);
+    if (head_dim == 128) return dispatch_group<float, 128>(group, ctas, a, st);
+    if (head_dim == 64) return dispatch_group<float, 64>(group, ctas, a, st);
   }
   return cudaErrorInvalidValue;
 }

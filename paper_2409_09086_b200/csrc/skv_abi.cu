@@ -49,7 +49,8 @@ struct skv_ctx {
   skv_config cfg;
   int S, L, Hq, Hkv, D, G, cap, W, B, elt;
   float scale;
-  int max_splits;
+  int max_ctas;    // persistent decode grid bound (CTAs/SM x SMs)
+  int last_layer = -1;  // layer of the last decode launch on the ctx (-1: other work since)
   // device state
   void* k = nullptr;
   void* v = nullptr;
@@ -73,9 +74,27 @@ struct skv_ctx {
   // host mirror (uniform over streams)
   std::vector<int> n, whead, wcount, parity, pend_n, pend_slot, pend_par, round_value;
   int64_t launches = 0;
-  // graphs
+  // graphs: host-mirror snapshots at capture begin / end (a replay moves the
+  // mirror from `gbegin` to `gend`; it is refused unless the mirror is at `gbegin`)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  struct Mirror {
+    std::vector<int> n, whead, wcount, parity, pend_n, pend_slot, pend_par;
+    bool operator==(const Mirror& o) const {
+      return n == o.n && whead == o.whead && wcount == o.wcount && parity == o.parity && pend_n == o.pend_n &&
+             pend_slot == o.pend_slot && pend_par == o.pend_par;
+    }
+  } gbegin, gend;
+  Mirror snap() const { return Mirror{n, whead, wcount, parity, pend_n, pend_slot, pend_par}; }
+  void restore(const Mirror& m) {
+    n = m.n;
+    whead = m.whead;
+    wcount = m.wcount;
+    parity = m.parity;
+    pend_n = m.pend_n;
+    pend_slot = m.pend_slot;
+    pend_par = m.pend_par;
+  }
   // host-buffer pipeline
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_in, ev_out;
@@ -101,13 +120,6 @@ struct skv_ctx {
   int64_t kv_layer_stride() const { return (int64_t)Hkv * cap * D; }  // elements
   int64_t kv_stream_stride() const { return (int64_t)L * kv_layer_stride(); }
 
-  int splits_for(int tokens) const {
-    const int target = 148 * 6;
-    int sp = (target + S * Hkv - 1) / (S * Hkv);
-    sp = std::min(sp, (tokens + 63) / 64);
-    sp = std::max(1, std::min(sp, max_splits));
-    return sp;
-  }
 };
 
 extern "C" {
@@ -146,7 +158,12 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   x->B = c.recent_len + c.relevant_budget;
   x->elt = c.dtype == SKV_DTYPE_BF16 ? 2 : 4;
   x->scale = (float)(1.0 / std::sqrt((double)c.head_dim));
-  x->max_splits = (x->cap + 63) / 64;
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    x->max_ctas = sms * decode_ctas_per_sm(c.dtype, c.head_dim, G);
+  }
 
   const size_t SL = x->sl_count();
   const size_t kv_bytes = SL * (size_t)x->kv_layer_stride() * x->elt;
@@ -168,7 +185,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     chk(x->alloc(&x->logits[p], SL * x->Hq * (size_t)x->cap * sizeof(float)));
     chk(x->alloc(&x->stats[p], SL * x->Hq * 2 * sizeof(float)));
   }
-  chk(x->alloc(&x->part, (size_t)x->S * x->Hq * x->max_splits * (x->D + 2) * sizeof(float)));
+  chk(x->alloc(&x->part, ((size_t)x->S * x->Hkv + x->max_ctas) * x->G * (x->D + 2) * sizeof(float)));
   chk(x->alloc(&x->counters, (size_t)x->S * x->Hkv * sizeof(int32_t)));
   chk(x->alloc(&x->kept, SL * x->B * sizeof(int32_t)));
   chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
@@ -217,8 +234,9 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   if (n_old + 1 > x->cap)
     return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
   const int n = n_old + 1;
-  const int splits = x->splits_for(n);
-  const int chunk = ((n + splits - 1) / splits + 31) / 32 * 32;
+  const int nt = (n + 31) / 32;
+  const int64_t T = (int64_t)x->S * x->Hkv * nt;
+  const int ctas = (int)std::min<int64_t>(T, x->max_ctas);
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
   AttnArgs a{};
@@ -226,8 +244,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.Hkv = x->Hkv;
   a.n_old = n_old;
   a.append = 1;
-  a.splits = (n + chunk - 1) / chunk;
-  a.chunk = chunk;
+  a.nt = nt;
+  a.T = T;
+  a.S = x->S;
+  a.prefetch = x->last_layer >= 0 && x->last_layer != layer;
   a.scale = x->scale;
   const int64_t kv_off = (int64_t)layer * x->kv_layer_stride() * x->elt;
   a.kc = static_cast<char*>(x->k) + kv_off;
@@ -277,9 +297,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     f.n = x->pend_n[layer];
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
   }
-  cudaError_t e = launch_decode(x->cfg.dtype, x->D, x->G, x->S, a, st);
+  cudaError_t e = launch_decode(x->cfg.dtype, x->D, x->G, ctas, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
   x->launches++;
+  x->last_layer = layer;
   x->pend_n[layer] = 0;
   if (record) {
     x->pend_n[layer] = n;
@@ -313,6 +334,7 @@ static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
   cudaError_t e = launch_fold(x->S, pieces, f, x->Hq, st);
   if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
   x->launches++;
+  x->last_layer = -1;
   x->pend_n[layer] = 0;
   return SKV_OK;
 }
@@ -443,6 +465,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
     cudaError_t e = launch_select(x->S * x->L, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
     x->launches++;
+    x->last_layer = -1;
     c.k = static_cast<char*>(x->k);
     c.v = static_cast<char*>(x->v);
     c.kv_bs = x->kv_layer_stride() * x->elt;
@@ -463,6 +486,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
     e = launch_compact(x->S * x->L, c, st);
     if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
     x->launches++;
+    x->last_layer = -1;
   } else {
     for (int l = l0; l < l1; ++l) {
       const int64_t sl0 = l;  // block b = stream s -> (s*L + l)
@@ -479,6 +503,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
       cudaError_t e = launch_select(x->S, a, st);
       if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
       x->launches++;
+      x->last_layer = -1;
       c.k = static_cast<char*>(x->k) + sl0 * x->kv_layer_stride() * x->elt;
       c.v = static_cast<char*>(x->v) + sl0 * x->kv_layer_stride() * x->elt;
       c.kv_bs = x->kv_stream_stride() * x->elt;
@@ -499,6 +524,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
       e = launch_compact(x->S, c, st);
       if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
       x->launches++;
+      x->last_layer = -1;
     }
   }
   if (kept_dev) {
@@ -621,6 +647,7 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   SKV_CK(cudaMemcpy(x->wlen + sl * x->W, lens.data(), x->W * sizeof(int32_t), cudaMemcpyHostToDevice));
   // host mirror: injection is per (stream, layer); the caller injects every
   // stream of a layer with the same n and m.
+  x->last_layer = -1;
   x->n[layer] = n;
   x->wcount[layer] = m;
   x->whead[layer] = m % x->W;
@@ -633,6 +660,7 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
 int skv_capture_begin(skv_ctx* x, void* stream) {
   if (!x) return fail(SKV_EINVAL, "null argument");
   SKV_CK(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
+  x->gbegin = x->snap();
   return SKV_OK;
 }
 
@@ -646,6 +674,8 @@ int skv_capture_end(skv_ctx* x, void* stream) {
     cudaGraphDestroy(x->graph);
     x->graph = nullptr;
   }
+  x->gend = x->snap();
+  x->restore(x->gbegin);  // nothing has executed yet
   SKV_CK(cudaStreamEndCapture(as_stream(stream), &x->graph));
   SKV_CK(cudaGraphInstantiate(&x->exec, x->graph, 0));
   return SKV_OK;
@@ -653,7 +683,10 @@ int skv_capture_end(skv_ctx* x, void* stream) {
 
 int skv_graph_launch(skv_ctx* x, void* stream) {
   if (!x || !x->exec) return fail(SKV_ESTATE, "no captured graph");
+  if (!(x->snap() == x->gbegin))
+    return fail(SKV_ESTATE, "graph replay refused: engine state differs from the state at capture begin");
   SKV_CK(cudaGraphLaunch(x->exec, as_stream(stream)));
+  x->restore(x->gend);
   return SKV_OK;
 }
 
@@ -774,17 +807,20 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   if (heads < 1 || n < 1) return fail(SKV_EINVAL, "keys must be a non-empty sequence of vectors");
   if (head_dim != 64 && head_dim != 128) return fail(SKV_EINVAL, "device attend needs head_dim 64 or 128");
   cudaStream_t st = as_stream(stream);
-  const int splits = std::max(1, std::min((n + 255) / 256, 64));
-  const int chunk = ((n + splits - 1) / splits + 31) / 32 * 32;
-  const int real_splits = (n + chunk - 1) / chunk;
-  const size_t need = (size_t)heads * real_splits * (head_dim + 2);
+  const int nt = (n + 31) / 32;
+  const int64_t T = (int64_t)heads * nt;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ctas = (int)std::min<int64_t>(T, (int64_t)sms * decode_ctas_per_sm(SKV_DTYPE_F32, head_dim, 1));
+  const size_t need = ((size_t)heads + ctas) * (head_dim + 2);
   if (g_att.part_floats < need || g_att.heads < heads) {
     SKV_CK(cudaStreamSynchronize(st));
     if (g_att.stats) cudaFree(g_att.stats);
     if (g_att.part) cudaFree(g_att.part);
     if (g_att.counters) cudaFree(g_att.counters);
     const int hcap = std::max(heads, 64);
-    const size_t pcap = std::max(need, (size_t)hcap * 64 * 130);
+    const size_t pcap = std::max(need, (size_t)(hcap + 1024) * 130);
     SKV_CK(cudaMalloc(&g_att.stats, hcap * 2 * sizeof(float)));
     SKV_CK(cudaMalloc(&g_att.part, pcap * sizeof(float)));
     SKV_CK(cudaMalloc(&g_att.counters, hcap * sizeof(int32_t)));
@@ -797,8 +833,10 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   a.Hkv = heads;
   a.n_old = n;
   a.append = 0;
-  a.splits = real_splits;
-  a.chunk = chunk;
+  a.nt = nt;
+  a.T = T;
+  a.S = 1;
+  a.prefetch = 0;
   a.scale = (float)(1.0 / std::sqrt((double)head_dim));
   a.kc = const_cast<float*>(keys);
   a.vc = const_cast<float*>(values);
@@ -813,7 +851,7 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   a.stats = g_att.stats;
   a.part = g_att.part;
   a.counters = g_att.counters;
-  cudaError_t e = launch_decode(SKV_DTYPE_F32, head_dim, 1, 1, a, st);
+  cudaError_t e = launch_decode(SKV_DTYPE_F32, head_dim, 1, ctas, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
   FoldArgs f{};
   f.logits = probs;

@@ -31,7 +31,13 @@ struct AttnArgs {
   int Hq, Hkv;          // group size G = Hq / Hkv is a template parameter
   int n_old;            // tokens cached before this step
   int append;           // 1: slot n_old is the new token taken from kin/vin
-  int splits, chunk;    // grid.x = splits; CTA c covers [c*chunk, min((c+1)*chunk, n))
+  // persistent stream-K schedule: segment sigma = s*Hkv + g holds nt 32-token
+  // tiles; CTA c of P streams global tiles [c*T/P, (c+1)*T/P); the partial of
+  // (CTA c, segment sigma) lives in piece slot sigma + c.
+  int nt;               // tiles per segment = ceil(n / 32)
+  int64_t T;            // S * Hkv * nt
+  int S;                // streams
+  int prefetch;         // producer may stream cached K/V before griddepcontrol.wait
   float scale;          // f32(1/sqrt(D)), engine.py:150
   void* kc;             // K store base (written for the appended row)
   void* vc;
@@ -47,8 +53,8 @@ struct AttnArgs {
   int64_t l_ss, l_hs;
   float* stats;         // [s][hq][2] (M, L) of this step
   int64_t st_ss;
-  float* part;          // scratch [s][hq][split][D + 2]
-  int32_t* counters;    // [s][g], zero between launches
+  float* part;          // scratch [piece][G][D + 2], piece < S*Hkv + P
+  int32_t* counters;    // [s*Hkv + g], zero between launches
   // appended token metadata
   int64_t* pos;         // pos[s*m_ss + t]
   int8_t* modality;
@@ -62,7 +68,8 @@ struct AttnArgs {
   FoldArgs fold;        // previous step's row (fold.n == 0: none)
 };
 
-cudaError_t launch_decode(int dtype, int head_dim, int group, int streams, const AttnArgs& a, cudaStream_t st);
+cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st);
+int decode_ctas_per_sm(int dtype, int head_dim, int group);
 cudaError_t launch_fold(int streams, int pieces, const FoldArgs& f, int Hq, cudaStream_t st);
 
 // ----------------------------------------------------------------------------
