@@ -49,16 +49,17 @@ __device__ __forceinline__ float rescale(float m, float M) {
 
 // row[j] = agg_h p[h][j] with p = expf(x - M_h) / L_h, for j in [c0, c1).
 // Head order is sequential h = 0..Hq-1 in float32 (aggregate_heads, policies.py:262).
-__device__ void fold_columns(const FoldArgs& f, int s, int c0, int c1, int Hq, int tid, int nthreads) {
+__device__ void fold_columns(const FoldArgs& f, int s, int c0, int c1, int Hq, int tid, int nthreads,
+                             const float* stt = nullptr) {
   const float* lg = f.logits + s * f.l_ss;
-  const float* stt = f.stats + s * f.st_ss;
+  if (!stt) stt = f.stats + s * f.st_ss;
   float* row = f.rows ? f.rows + s * f.r_ss : nullptr;
   for (int j = c0 + tid; j < c1; j += nthreads) {
     float acc = f.mode == 1 ? -INFINITY : 0.f;
-#pragma unroll 8
+#pragma unroll 16
     for (int h = 0; h < Hq; ++h) {
-      const float M = __ldg(stt + 2 * h);
-      const float L = __ldg(stt + 2 * h + 1);
+      const float M = stt[2 * h];
+      const float L = stt[2 * h + 1];
       const float p = __fdiv_rn(expf(__fsub_rn(__ldcs(lg + h * f.l_hs + j), M)), L);
       if (f.mode == 2) {
         f.probs[s * f.p_ss + h * f.p_hs + j] = p;
@@ -97,7 +98,7 @@ __device__ __forceinline__ int tile_owner(int64_t t, int64_t T, int P) {
 // segment piece it publishes a partial (m, l, o) and the last contributor of
 // the segment merges the pieces in CTA order (deterministic).
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(192) decode_kernel(const AttnArgs a) {
   using Gm = Geo<T, D>;
   constexpr int TT = Gm::TT, RB = Gm::RB, LPR = Gm::LPR, EPL = Gm::EPL, RPW = Gm::RPW;
   constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Gm::STAGES, TILE = Gm::TILE;
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
   float* wo = wl + NW * G;                               // [NW][G][D]
   float* fin = wo + NW * G * D;                          // [G][2] merged (M, L)
   int* flag = reinterpret_cast<int*>(fin + 2 * G);
+  float* fstats = fin + 2 * G + 4;                        // [Hq][2] fold warp
 
   const int c = blockIdx.x, P = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -129,6 +131,30 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
   }
   __syncthreads();
 
+  if (warp == NW + 1) {
+    // ---------------------------------------------------------- fold warp
+    // Materialises the previous recorded step's window row (64-column pieces,
+    // pieces c, c+P, ...) while the other warps stream K/V: its load latency
+    // is hidden behind the main loop.
+    const FoldArgs& f = a.fold;
+    if (f.n > 0) {
+      if (!a.prefetch) griddep_wait();  // same layer back to back: wait for its logits
+      const int ppc = (f.n + 63) / 64;
+      for (int piece = c; piece < a.S * ppc; piece += P) {
+        const int s = piece / ppc, col0 = (piece - s * ppc) * 64;
+        const float* stt = f.stats + s * f.st_ss;
+        for (int h = lane; h < a.Hq; h += 32) {
+          fstats[2 * h] = __ldg(stt + 2 * h);
+          fstats[2 * h + 1] = __ldg(stt + 2 * h + 1);
+        }
+        __syncwarp();
+        fold_columns(f, s, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+        __syncwarp();
+        if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
+      }
+    }
+    return;
+  }
   if (warp == NW) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -370,12 +396,6 @@ __global__ void __launch_bounds__(160) decode_kernel(const AttnArgs a) {
     }
     consumers_sync();
   }
-
-  // ---- previous step's window row, spread over the CTAs
-  if (a.fold.n > 0) {
-    const int fp = max(1, P / a.S);
-    for (int idx = c; idx < a.S * fp; idx += P) fold_piece(a.fold, idx / fp, idx % fp, fp, a.Hq, tid, 128);
-  }
 }
 
 __global__ void fold_kernel(const FoldArgs f, int Hq) {
@@ -386,22 +406,22 @@ template <typename T, int D, int G>
 static size_t decode_smem() {
   using Gm = Geo<T, D>;
   return (size_t)Gm::STAGES * 2 * Gm::TILE + 2 * Gm::STAGES * sizeof(uint64_t) +
-         sizeof(float) * (2 * Gm::NW * G + Gm::NW * G * D + 2 * G) + 16;
+         sizeof(float) * (2 * Gm::NW * G + Gm::NW * G * D + 2 * G + 4);
 }
 
 template <typename T, int D, int G>
 static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st) {
-  const size_t smem = decode_smem<T, D, G>();
+  const size_t smem = decode_smem<T, D, G>() + 8 * (size_t)a.Hq;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         (int)(decode_smem<T, D, G>() + 8 * 1024));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(160);
+  cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -416,9 +436,10 @@ template <typename T, int D, int G>
 static int occupancy_t() {
   static int occ = 0;
   if (!occ) {
-    const size_t smem = decode_smem<T, D, G>();
-    cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, 160, smem) != cudaSuccess ||
+    const size_t smem = decode_smem<T, D, G>() + 8 * 64;
+    cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(decode_smem<T, D, G>() + 8 * 1024));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, 192, smem) != cudaSuccess ||
         occ < 1)
       occ = 1;
   }

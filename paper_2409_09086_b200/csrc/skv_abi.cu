@@ -659,14 +659,10 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
 
 int skv_capture_begin(skv_ctx* x, void* stream) {
   if (!x) return fail(SKV_EINVAL, "null argument");
-  SKV_CK(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
-  x->gbegin = x->snap();
-  return SKV_OK;
-}
-
-int skv_capture_end(skv_ctx* x, void* stream) {
-  if (!x) return fail(SKV_EINVAL, "null argument");
+  // release the previous graph before capturing: destroying graph objects is not
+  // permitted while a thread-local capture is active
   if (x->exec) {
+    SKV_CK(cudaStreamSynchronize(as_stream(stream)));
     cudaGraphExecDestroy(x->exec);
     x->exec = nullptr;
   }
@@ -674,6 +670,13 @@ int skv_capture_end(skv_ctx* x, void* stream) {
     cudaGraphDestroy(x->graph);
     x->graph = nullptr;
   }
+  SKV_CK(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
+  x->gbegin = x->snap();
+  return SKV_OK;
+}
+
+int skv_capture_end(skv_ctx* x, void* stream) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
   x->gend = x->snap();
   x->restore(x->gbegin);  // nothing has executed yet
   SKV_CK(cudaStreamEndCapture(as_stream(stream), &x->graph));
