@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # Build libstreamkv_b200.so for sm_100a (cross-compiles without a GPU).
-set -euo pipefail
+set -eo pipefail
 cd "$(dirname "$0")"
 OUT=paper_2409_09086_b200/libstreamkv_b200.so
 SRC=paper_2409_09086_b200/csrc

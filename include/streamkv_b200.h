@@ -129,6 +129,14 @@ int skv_capture_end(skv_ctx* ctx, void* stream);
 int skv_graph_launch(skv_ctx* ctx, void* stream);
 /* Number of this library's kernels launched since creation (instrumentation). */
 int64_t skv_kernel_launches(const skv_ctx* ctx);
+/* Instrumentation: when enabled, every decode launch records the earliest CTA
+ * start and latest CTA end (%globaltimer, ns) into a device ring of 8192 pairs;
+ * skv_timing_read copies the pairs recorded since enabling (returns the count). */
+int skv_timing(skv_ctx* ctx, int enable);
+int skv_timing_read(skv_ctx* ctx, uint64_t* out_host, int max_pairs);
+/* enable == 3 additionally records per-CTA [start, released, end] of the
+ * launches in slots tcount % 64; skv_timing_cta copies one slot (max_ctas x 8). */
+int skv_timing_cta(skv_ctx* ctx, int slot, uint64_t* out_host);
 
 /* ---- stand-alone policy kernels (drop-in for the pure policy functions) ---- */
 /* top_k_indices(scores, k) (policies.py:165-181) on device: ascending indices of

@@ -5,20 +5,27 @@
 //   KvCache.append (cache.py:112-134)   -> the new k/v row is bulk-copied from the
 //                                          input straight into the last tile and
 //                                          written to the cache slot n_old;
-//   Session._attend (engine.py:235-246) -> split-KV online softmax, warp-shuffle
-//                                          reductions, P.V in fp32;
+//   Session._attend (engine.py:235-246) -> split-KV online softmax, packed FFMA2
+//                                          dot products, reduce-scattered
+//                                          warp-shuffle reductions, P.V in fp32;
 //   aggregate_heads + AttentionWindow.push (policies.py:259-263, 107-115)
-//                                       -> each CTA records its tile logits; the
+//                                       -> each tile records its logits; the
 //                                          head-aggregated row is materialised
 //                                          ("folded") by the NEXT launch of the
-//                                          layer, spread over all its CTAs, once
-//                                          the global per-head (max, sum) exist.
+//                                          layer once the per-head (max, sum)
+//                                          of this step exist.
 //
-// Grid (splits, Hkv, S); 4 consumer warps + 1 producer warp.  The producer
-// streams 32-token K and V tiles (contiguous rows of one head) into a 4-stage
-// shared-memory ring with 1-D bulk async copies (TMA engine) completing on
-// mbarriers.  The last CTA of each (stream, kv-head) merges the split partials
-// (fixed split order => deterministic) and publishes per-head (M, L).
+// Persistent grid (CTAs/SM x SMs) with dynamic chunk scheduling: a chunk is
+// CH 32-token tiles of one (stream, kv-head) segment; the producer warp takes
+// chunk tickets from a global counter and streams the chunk's K and V tiles
+// into a 3-stage shared-memory ring with 1-D bulk async copies (TMA engine,
+// mbarrier completion).  Four consumer warps compute; an epilogue warp merges
+// the consumer warps' chunk partials, publishes them, and the last chunk of a
+// segment merges all chunk partials in chunk order (deterministic) and writes
+// the output and the per-head (max, sum).  The epilogue warp also folds the
+// previous step's window row in between.  With programmatic dependent launch
+// the producer of layer l+1 streams cached K/V while layer l drains; anything
+// that depends on the previous launch waits on griddepcontrol.wait.
 #include "skv_common.cuh"
 #include "skv_internal.h"
 
@@ -31,17 +38,28 @@ struct Geo {
   static constexpr int LPR = RB / 16;     // lanes per row (16 B each)
   static constexpr int EPL = 16 / ELT;    // elements per lane
   static constexpr int RPW = 32 / LPR;    // rows per warp load
-  static constexpr int TT = 32;           // tokens per tile
-  static constexpr int NW = 4;            // consumer warps
+  static constexpr int NW = 8;            // consumer warps
+  static constexpr int TT = 8 * NW;       // tokens per tile (8 rows per warp)
   static constexpr int RPWARP = TT / NW;  // rows per warp per tile
   static constexpr int ITERS = RPWARP / RPW;
   static constexpr int TILE = TT * RB;    // bytes per K (or V) tile
-  static constexpr int STAGES = TILE > 8192 ? 3 : 4;
+  static constexpr int STAGES = 3;
   static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "row geometry");
   static_assert(ITERS >= 1, "tile geometry");
 };
 
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+constexpr int kConsumerWarps = 8;
+constexpr int kCT = kConsumerWarps * 32;          // consumer threads
+constexpr int kThreads = kCT + 3 * 32;            // + producer, epilogue, fold warps
+
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCT) : "memory"); }
+__device__ __forceinline__ void handoff_sync() { asm volatile("bar.sync 2, %0;\n" ::"n"(kCT + 32) : "memory"); }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ float rescale(float m, float M) {
   return m == -INFINITY ? 0.f : exp2f((m - M) * kLog2e);
@@ -84,77 +102,99 @@ __device__ __forceinline__ void fold_piece(const FoldArgs& f, int s, int piece, 
   if (piece == 0 && tid == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
-// CTA that owns global tile t under the even split [c*T/P, (c+1)*T/P).
-__device__ __forceinline__ int tile_owner(int64_t t, int64_t T, int P) {
-  return (int)(((t + 1) * P + T - 1) / T) - 1;
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
-// Persistent stream-K decode: CTA c streams the global tile range
-// [c*T/P, (c+1)*T/P) of the (segment, tile) space, crossing segment (stream,
-// kv-head) boundaries without draining its TMA pipeline.  At the end of each
-// segment piece it publishes a partial (m, l, o) and the last contributor of
-// the segment merges the pieces in CTA order (deterministic).
+static_assert(kConsumerWarps == 8, "Geo::NW must match kConsumerWarps");
+
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(192) decode_kernel(const AttnArgs a) {
+struct Smem {
   using Gm = Geo<T, D>;
+  static constexpr int NW = Gm::NW;
+  static constexpr size_t tiles = (size_t)Gm::STAGES * 2 * Gm::TILE;
+  static constexpr size_t bars = (2 * Gm::STAGES + 4) * sizeof(uint64_t);
+  static constexpr size_t tinfo = (2 * Gm::STAGES + 4) * sizeof(int);
+  // epilogue slot: header (4 ints) + wm[NW][G] + wl[NW][G] + wo[NW][G][D]
+  static constexpr size_t slot_floats = 4 + 2 * NW * G + NW * G * D;
+  static constexpr size_t slots = 2 * slot_floats * sizeof(float);
+  static constexpr size_t pbuf = (size_t)NW * G * Gm::RPWARP * sizeof(float);
+  static constexpr size_t fixed = tiles + bars + tinfo + slots + pbuf;
+  static size_t bytes(int Hq) { return fixed + 2 * (size_t)Hq * sizeof(float) + 16; }
+};
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(const AttnArgs a) {
+  using Gm = Geo<T, D>;
+  using Sm = Smem<T, D, G>;
   constexpr int TT = Gm::TT, RB = Gm::RB, LPR = Gm::LPR, EPL = Gm::EPL, RPW = Gm::RPW;
   constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Gm::STAGES, TILE = Gm::TILE;
   constexpr int PW = D + 2;  // floats per head in a partial
+  constexpr int SLOT = (int)Sm::slot_floats;
 
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* tiles = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * 2 * TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Sm::tiles);
   uint64_t* empty = full + STAGES;
-  float* wm = reinterpret_cast<float*>(empty + STAGES);  // [NW][G]
-  float* wl = wm + NW * G;                               // [NW][G]
-  float* wo = wl + NW * G;                               // [NW][G][D]
-  float* fin = wo + NW * G * D;                          // [G][2] merged (M, L)
-  int* flag = reinterpret_cast<int*>(fin + 2 * G);
-  float* fstats = fin + 2 * G + 4;                        // [Hq][2] fold warp
+  uint64_t* epi_full = empty + STAGES;  // [2]
+  uint64_t* epi_empty = epi_full + 2;   // [2]
+  int* tinfo = reinterpret_cast<int*>(epi_empty + 2);               // [STAGES][2]
+  int* cring = tinfo + 2 * STAGES;                                  // [4] next chunk tickets
+  float* slots = reinterpret_cast<float*>(tinfo + 2 * STAGES + 4);  // [2][SLOT]
+  float* pbuf_all = slots + 2 * SLOT;                               // [NW][G][RPWARP]
+  float* fstats = pbuf_all + NW * G * Gm::RPWARP;                   // [Hq][2]
 
   const int c = blockIdx.x, P = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n_old + a.append;
-  const int64_t a0 = (int64_t)c * a.T / P, a1 = (int64_t)(c + 1) * a.T / P;
+  const int total = a.S * a.Hkv * a.nc;
 
-  griddep_launch();
+  if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], globaltimer());
+  if (a.ctat && tid == 0) a.ctat[8 * c] = globaltimer();
+  if (c == 0 && tid == 0) {  // a stale flag from this slot's previous use must not leak to the next launch
+    *a.done_self = 0;
+    __threadfence();
+  }
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&epi_full[i], NW);
+      mbar_init(&epi_empty[i], 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-
-  if (warp == NW + 1) {
-    // ---------------------------------------------------------- fold warp
-    // Materialises the previous recorded step's window row (64-column pieces,
-    // pieces c, c+P, ...) while the other warps stream K/V: its load latency
-    // is hidden behind the main loop.
-    const FoldArgs& f = a.fold;
-    if (f.n > 0) {
-      if (!a.prefetch) griddep_wait();  // same layer back to back: wait for its logits
-      const int ppc = (f.n + 63) / 64;
-      for (int piece = c; piece < a.S * ppc; piece += P) {
-        const int s = piece / ppc, col0 = (piece - s * ppc) * 64;
-        const float* stt = f.stats + s * f.st_ss;
-        for (int h = lane; h < a.Hq; h += 32) {
-          fstats[2 * h] = __ldg(stt + 2 * h);
-          fstats[2 * h + 1] = __ldg(stt + 2 * h + 1);
-        }
-        __syncwarp();
-        fold_columns(f, s, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
-        __syncwarp();
-        if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
-      }
+  griddep_launch();
+  // Everything that depends on the previous launch (the preceding layer's
+  // merge: q, in a real model, and the shared scratch) waits here.
+  auto wait_prev = [&]() {
+    if (a.done_prev) {  // the preceding merge kernel publishes its completion flag
+      while (ld_acquire(a.done_prev) == 0) __nanosleep(32);
+    } else {
+      griddep_wait();
     }
-    return;
-  }
+  };
+
   if (warp == NW) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -163,71 +203,240 @@ __global__ void __launch_bounds__(192) decode_kernel(const AttnArgs a) {
         griddep_wait();
         waited = true;
       }
-      int i = 0;
-      for (int64_t t = a0; t < a1; ++t, ++i) {
-        const int sigma = (int)(t / a.nt);
-        const int ts = (int)(t - (int64_t)sigma * a.nt) * TT;
+      int i = 0, taken = 0, kp = 0;
+      // three tickets in flight: the atomic's latency is hidden even for 1-tile chunks
+      int u = atomicAdd(&a.sched[0], 1);
+      int t1 = atomicAdd(&a.sched[0], 1);
+      int t2 = atomicAdd(&a.sched[0], 1);
+      while (u < total) {
+        ++taken;
+        const int u_next = t1;
+        t1 = t2;
+        t2 = atomicAdd(&a.sched[0], 1);
+        // published with this chunk's first tile: lets the consumers prefetch q
+        cring[(kp + 1) & 3] = u_next < total ? u_next : -1;
+        ++kp;
+        const int sigma = u / a.nc, j = u - sigma * a.nc;
         const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
-        const int rows = min(TT, n - ts);
-        const int rc = max(0, min(rows, a.n_old - ts));
-        const int st = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[st], ph ^ 1);
-        unsigned char* ks = tiles + (2 * st) * TILE;
-        unsigned char* vs = ks + TILE;
-        mbar_arrive_expect_tx(&full[st], 2u * rows * RB);
-        const int64_t base = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)ts * D;
-        if (rc > 0) {
-          bulk_g2s(ks, static_cast<const T*>(a.kc) + base, rc * RB, &full[st]);
-          bulk_g2s(vs, static_cast<const T*>(a.vc) + base, rc * RB, &full[st]);
-        }
-        if (rc < rows) {  // the appended token: straight from the step input
-          if (!waited) {
-            griddep_wait();
-            waited = true;
+        const int tt0 = j * a.ch, tt1 = min(tt0 + a.ch, a.nt);
+        const int64_t base = s * a.c_ss + (int64_t)g * a.c_hs;
+        for (int tt = tt0; tt < tt1; ++tt, ++i) {
+          const int ts = tt * TT;
+          const int rows = min(TT, n - ts);
+          const int rc = max(0, min(rows, a.n_old - ts));
+          const int st = i % STAGES;
+          mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
+          tinfo[2 * st] = u;
+          tinfo[2 * st + 1] = tt | ((tt == tt1 - 1) ? (1 << 30) : 0);
+          unsigned char* ks = tiles + (2 * st) * TILE;
+          unsigned char* vs = ks + TILE;
+          mbar_arrive_expect_tx(&full[st], 2u * rows * RB);
+          if (rc > 0) {
+            bulk_g2s(ks, static_cast<const T*>(a.kc) + base + (int64_t)ts * D, rc * RB, &full[st]);
+            bulk_g2s(vs, static_cast<const T*>(a.vc) + base + (int64_t)ts * D, rc * RB, &full[st]);
           }
-          const int64_t in = s * a.in_ss + (int64_t)g * D;
-          bulk_g2s(ks + rc * RB, static_cast<const T*>(a.kin) + in, RB, &full[st]);
-          bulk_g2s(vs + rc * RB, static_cast<const T*>(a.vin) + in, RB, &full[st]);
+          if (rc < rows) {  // the appended token: straight from the step input
+            if (!waited) {
+              wait_prev();
+              waited = true;
+            }
+            const int64_t in = s * a.in_ss + (int64_t)g * D;
+            bulk_g2s(ks + rc * RB, static_cast<const T*>(a.kin) + in, RB, &full[st]);
+            bulk_g2s(vs + rc * RB, static_cast<const T*>(a.vin) + in, RB, &full[st]);
+          }
         }
+        u = u_next;
+      }
+      const int st = i % STAGES;  // end marker
+      mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
+      tinfo[2 * st] = -1;
+      mbar_arrive(&full[st]);
+      if (a.ctat) {
+        a.ctat[8 * c + 6] = globaltimer();
+        a.ctat[8 * c + 7] = taken;
       }
     }
     return;
   }
 
-  // -------------------------------------------------------------- consumers
-  griddep_wait();  // q, out, logits, partials and counters cross launches
-  const int rsub = lane / LPR, c16 = lane % LPR;
-  float qf[G][EPL];
-  float m_run[G], l_run[G], o[G][EPL];
-  float* lg = nullptr;
-  int cur = -1;
-  int i = 0;
-  for (int64_t t = a0; t < a1; ++t, ++i) {
-    const int sigma = (int)(t / a.nt);
-    const int tt = (int)(t - (int64_t)sigma * a.nt);
-    const int ts = tt * TT;
-    const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
-    if (sigma != cur) {
-      cur = sigma;
+  if (warp == NW + 2) {
+    // ------------------------------------------------- window-row fold warp
+    // Materialises the previous recorded step's window row (64-column pieces
+    // c, c+P, ...) while the other warps stream K/V.
+    const FoldArgs& f = a.fold;
+    if (f.n <= 0) return;
+    if (!a.prefetch) griddep_wait();  // same layer back to back: wait for its logits
+    const int ppc = (f.n + 63) / 64;
+    for (int piece = c; piece < a.S * ppc; piece += P) {
+      const int s = piece / ppc, col0 = (piece - s * ppc) * 64;
+      const float* stt = f.stats + s * f.st_ss;
+      for (int h = lane; h < a.Hq; h += 32) {
+        fstats[2 * h] = __ldg(stt + 2 * h);
+        fstats[2 * h + 1] = __ldg(stt + 2 * h + 1);
+      }
+      __syncwarp();
+      fold_columns(f, s, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+      __syncwarp();
+      if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
+    }
+    return;
+  }
+
+  if (warp == NW + 1) {
+    // ------------------------------------------------------ epilogue warp
+    if (!a.prefetch) griddep_wait();  // same layer back to back: the cache slot and metadata
+    for (int k = 0;; ++k) {
+      const int sl = k & 1;
+      const uint32_t ph = (k >> 1) & 1;
+      mbar_wait(&epi_full[sl], ph);
+      const float* slot = slots + sl * SLOT;
+      const int u = reinterpret_cast<const int*>(slot)[0];
+      if (u < 0) break;
+      const float* wm = slot + 4;
+      const float* wl = wm + NW * G;
+      const float* wo = wl + NW * G;
+      const int sigma = u / a.nc, j = u - sigma * a.nc;
+      const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+      // merge the consumer warps' partials of this chunk
+      float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        Vec16<T>::load(qf[h], static_cast<const T*>(a.q) + s * a.q_ss + (int64_t)(g * G + h) * D + c16 * EPL);
+        // lane w < NW holds warp w's (m, l); rescale factors computed once per head
+        const float mw = lane < NW ? wm[lane * G + h] : -INFINITY;
+        float M = mw;
+#pragma unroll
+        for (int off = NW / 2; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        const float f = lane < NW ? rescale(mw, M) : 0.f;
+        float L = lane < NW ? f * wl[lane * G + h] : 0.f;
+#pragma unroll
+        for (int off = NW / 2; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+        float fw[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) fw[w] = __shfl_sync(0xffffffffu, f, w);
+#pragma unroll
+        for (int d = lane; d < D; d += 32) {
+          float acc = 0.f;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) acc = fmaf(fw[w], wo[(w * G + h) * D + d], acc);
+          part[h * PW + d] = acc;
+        }
+        if (lane == 0) {
+          part[h * PW + D] = M;
+          part[h * PW + D + 1] = L;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&epi_empty[sl]);  // slot consumed
+      // append: the new row and (once per stream) its metadata go to slot n_old
+      if (a.append && j == a.nc - 1) {
+        const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
+        const int64_t in = s * a.in_ss + (int64_t)g * D;
+        for (int q16 = lane; q16 < RB / 16; q16 += 32) {
+          reinterpret_cast<uint4*>(static_cast<T*>(a.kc) + dst)[q16] =
+              reinterpret_cast<const uint4*>(static_cast<const T*>(a.kin) + in)[q16];
+          reinterpret_cast<uint4*>(static_cast<T*>(a.vc) + dst)[q16] =
+              reinterpret_cast<const uint4*>(static_cast<const T*>(a.vin) + in)[q16];
+        }
+        if (g == 0 && lane == 0) {
+          int64_t* np = a.next_pos + s * a.len_ss;
+          const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
+          a.pos[s * a.m_ss + a.n_old] = pv;
+          a.modality[s * a.m_ss + a.n_old] = 0;
+          a.round_id[s * a.m_ss + a.n_old] = a.round_value;
+          *np = pv + 1;
+          a.len[s * a.len_ss] = n;
+        }
+      }
+    }
+    __threadfence();  // every chunk partial of this CTA visible GPU-wide
+    handoff_sync();
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  // q (the previous layer's output in a real model) crosses launches
+  if (a.done_prev) {
+    if (tid == 0) wait_prev();
+    consumers_sync();
+  } else {
+    griddep_wait();
+  }
+  if (a.ctat && tid == 0) a.ctat[8 * c + 1] = globaltimer();
+  // Lane layout: LPR lanes read one cached row (16 B each); a warp reads RPW
+  // rows per shared-memory load and ITERS loads per tile.  Partial dot products
+  // of the ITERS rows are reduce-scattered across the LPR lanes (log2(LPR)
+  // shuffles for ITERS rows instead of ITERS*log2(LPR)); afterwards each lane
+  // owns the logit of row `ridx*RPW + rsub`, replicated REP times.
+  constexpr int REP = LPR / ITERS;
+  constexpr int E2 = EPL / 2;
+  const int rsub = lane / LPR, c16 = lane % LPR;
+  int ridx = 0;
+#pragma unroll
+  for (int cnt = ITERS, off = LPR / 2; cnt > 1; cnt >>= 1, off >>= 1)
+    if (c16 & off) ridx += cnt / 2;
+  const bool owner = (c16 & (REP - 1)) == 0;
+  float* pbuf = pbuf_all + warp * G * Gm::RPWARP;  // [G][RPW][ITERS]
+  float2 q2[G][E2];
+  float2 o2[G][E2];
+  float m_run[G], l_run[G];
+  float* lg = nullptr;
+  int cur = -1;
+  int k = 0;  // chunks handed to the epilogue warp
+  bool fresh = true;
+  constexpr bool kPrefetchQ = G <= 2;  // register budget
+  float qn[G][EPL];  // prefetched q of the next chunk's segment
+  int qn_sigma = -1;
+  unsigned long long t_epi_wait = 0;
+  for (int i = 0;; ++i) {
+    const int st = i % STAGES;
+    mbar_wait(&full[st], (i / STAGES) & 1);
+    const int u = tinfo[2 * st];
+    if (u < 0) break;
+    const int info = tinfo[2 * st + 1];
+    const int tt = info & 0xffff;
+    const bool chunk_end = (info >> 30) & 1;
+    const int sigma = u / a.nc;
+    const int ts = tt * TT;
+    const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+    if (fresh) {
+      if (sigma != cur) {
+        if (qn_sigma != sigma) {  // not prefetched (first chunk)
+#pragma unroll
+          for (int h = 0; h < G; ++h)
+            Vec16<T>::load(qn[h], static_cast<const T*>(a.q) + s * a.q_ss + (int64_t)(g * G + h) * D + c16 * EPL);
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int e = 0; e < E2; ++e) q2[h][e] = make_float2(qn[h][2 * e], qn[h][2 * e + 1]);
+        cur = sigma;
+        lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+      }
+      // prefetch the next chunk's q (its ticket was published with this tile)
+      const int un = (kPrefetchQ && a.qpf) ? cring[(k + 1) & 3] : -1;
+      if (un >= 0 && un / a.nc != sigma) {
+        const int sn = un / a.nc;
+        const int s2 = sn / a.Hkv, g2 = sn - s2 * a.Hkv;
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+          Vec16<T>::load(qn[h], static_cast<const T*>(a.q) + s2 * a.q_ss + (int64_t)(g2 * G + h) * D + c16 * EPL);
+        qn_sigma = sn;
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+#pragma unroll
+        for (int e = 0; e < E2; ++e) o2[h][e] = make_float2(0.f, 0.f);
         m_run[h] = -INFINITY;
         l_run[h] = 0.f;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) o[h][e] = 0.f;
       }
-      lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+      fresh = false;
     }
-    const int st = i % STAGES;
-    const uint32_t ph = (i / STAGES) & 1;
     const int rows = min(TT, n - ts);
     const unsigned char* ks = tiles + (2 * st) * TILE;
     const unsigned char* vs = ks + TILE;
-    mbar_wait(&full[st], ph);
 
-    float sc[ITERS][G];
+    // ---- q . k for ITERS rows, packed FMA
+    float d[ITERS][G];
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int row = warp * Gm::RPWARP + it * RPW + rsub;
@@ -235,45 +444,63 @@ __global__ void __launch_bounds__(192) decode_kernel(const AttnArgs a) {
       Vec16<T>::load(kf, ks + row * RB + c16 * 16);
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        float d = 0.f;
+        float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) d = fmaf(qf[h][e], kf[e], d);
-#pragma unroll
-        for (int off = LPR / 2; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-        sc[it][h] = row < rows ? d * a.scale : -INFINITY;
+        for (int e = 0; e < E2; ++e) acc = __ffma2_rn(q2[h][e], make_float2(kf[2 * e], kf[2 * e + 1]), acc);
+        d[it][h] = acc.x + acc.y;
       }
     }
-    if (lg && c16 == 0) {
+    // ---- reduce-scatter across the LPR lanes of a row
 #pragma unroll
-      for (int it = 0; it < ITERS; ++it) {
-        const int row = warp * Gm::RPWARP + it * RPW + rsub;
-        if (row < rows) {
+    for (int cnt = ITERS, off = LPR / 2; cnt > 1; cnt >>= 1, off >>= 1) {
+      const bool up = (c16 & off) != 0;
 #pragma unroll
-          for (int h = 0; h < G; ++h) lg[h * a.l_hs + ts + row] = sc[it][h];
+      for (int jj = 0; jj < cnt / 2; ++jj) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const float send = up ? d[jj][h] : d[jj + cnt / 2][h];
+          const float keep = up ? d[jj + cnt / 2][h] : d[jj][h];
+          d[jj][h] = keep + __shfl_xor_sync(0xffffffffu, send, off);
         }
       }
     }
-    float p[ITERS][G];
+#pragma unroll
+    for (int off = REP / 2; off > 0; off >>= 1)
+#pragma unroll
+      for (int h = 0; h < G; ++h) d[0][h] += __shfl_xor_sync(0xffffffffu, d[0][h], off);
+
+    const int myrow = warp * Gm::RPWARP + ridx * RPW + rsub;
+    const bool valid = myrow < rows;
+    float sc[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) sc[h] = valid ? d[0][h] * a.scale : -INFINITY;
+    if (lg && owner && valid) {
+#pragma unroll
+      for (int h = 0; h < G; ++h) lg[h * a.l_hs + ts + myrow] = sc[h];
+    }
+    // ---- online softmax: one row per lane
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      float mt = -INFINITY;
+      float mt = sc[h];
 #pragma unroll
-      for (int it = 0; it < ITERS; ++it) mt = fmaxf(mt, sc[it][h]);
-#pragma unroll
-      for (int off = LPR; off < 32; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+      for (int off = 16; off >= REP; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
       const float mn = fmaxf(m_run[h], mt);
       const float alpha = rescale(m_run[h], mn);
-      float ps = 0.f;
+      const float pv = mn == -INFINITY ? 0.f : exp2f((sc[h] - mn) * kLog2e);
+      l_run[h] = l_run[h] * alpha + (owner ? pv : 0.f);
+      const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
-      for (int it = 0; it < ITERS; ++it) {
-        p[it][h] = mn == -INFINITY ? 0.f : exp2f((sc[it][h] - mn) * kLog2e);
-        ps += p[it][h];
-      }
-      l_run[h] = l_run[h] * alpha + ps;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) o[h][e] *= alpha;
+      for (int e = 0; e < E2; ++e) o2[h][e] = __fmul2_rn(o2[h][e], a2);
       m_run[h] = mn;
+      if (owner) pbuf[(h * RPW + rsub) * ITERS + ridx] = pv;
     }
+    __syncwarp();
+    // ---- P . V
+    float pr[G][ITERS];
+#pragma unroll
+    for (int h = 0; h < G; ++h)
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) pr[h][it] = pbuf[(h * RPW + rsub) * ITERS + it];
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int row = warp * Gm::RPWARP + it * RPW + rsub;
@@ -281,120 +508,150 @@ __global__ void __launch_bounds__(192) decode_kernel(const AttnArgs a) {
         float vf[EPL];
         Vec16<T>::load(vf, vs + row * RB + c16 * 16);
 #pragma unroll
-        for (int h = 0; h < G; ++h)
+        for (int h = 0; h < G; ++h) {
+          const float2 p2 = make_float2(pr[h][it], pr[h][it]);
 #pragma unroll
-          for (int e = 0; e < EPL; ++e) o[h][e] = fmaf(p[it][h], vf[e], o[h][e]);
+          for (int e = 0; e < E2; ++e) o2[h][e] = __ffma2_rn(p2, make_float2(vf[2 * e], vf[2 * e + 1]), o2[h][e]);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+    if (!chunk_end) continue;
 
-    if (tt != a.nt - 1 && t != a1 - 1) continue;
-
-    // ================= end of this CTA's piece of segment sigma =================
+    // ---- chunk done: hand the warp partials to the epilogue warp
+    const int sl = k & 1;
+    unsigned long long tw0 = 0;
+    if (a.ctat && tid == 0) tw0 = globaltimer();
+    mbar_wait(&epi_empty[sl], ((k >> 1) & 1) ^ 1);
+    if (a.ctat && tid == 0) t_epi_wait += globaltimer() - tw0;
+    float* slot = slots + sl * SLOT;
+    float* wm = slot + 4;
+    float* wl = wm + NW * G;
+    float* wo = wl + NW * G;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float l = l_run[h];
 #pragma unroll
-      for (int off = LPR; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      float o[EPL];
+#pragma unroll
+      for (int e = 0; e < E2; ++e) {
+        o[2 * e] = o2[h][e].x;
+        o[2 * e + 1] = o2[h][e].y;
+      }
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        float v = o[h][e];
 #pragma unroll
-        for (int off = LPR; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        o[h][e] = v;
+        for (int off = LPR; off < 32; off <<= 1) o[e] += __shfl_xor_sync(0xffffffffu, o[e], off);
       }
       if (rsub == 0) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) wo[(warp * G + h) * D + c16 * EPL + e] = o[h][e];
+        for (int e = 0; e < EPL; ++e) wo[(warp * G + h) * D + c16 * EPL + e] = o[e];
       }
       if (lane == 0) {
         wm[warp * G + h] = m_run[h];
         wl[warp * G + h] = l;
       }
     }
-    consumers_sync();
-    {
-      float* part = a.part + (int64_t)(sigma + c) * G * PW;
-      for (int idx = tid; idx < G * PW; idx += 128) {
-        const int h = idx / PW, d = idx - h * PW;
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w * G + h]);
-        float acc = 0.f;
-        if (d < D) {
-#pragma unroll
-          for (int w = 0; w < NW; ++w) acc += rescale(wm[w * G + h], M) * wo[(w * G + h) * D + d];
-        } else if (d == D) {
-          acc = M;
-        } else {
-#pragma unroll
-          for (int w = 0; w < NW; ++w) acc += rescale(wm[w * G + h], M) * wl[w * G + h];
-        }
-        part[idx] = acc;
-      }
-    }
-    // append: the new row and (once per stream) its metadata go to slot n_old
-    if (a.append && tt == a.nt - 1) {
-      const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
-      const int64_t in = s * a.in_ss + (int64_t)g * D;
-      for (int u = tid; u < RB / 16; u += 128) {
-        reinterpret_cast<uint4*>(static_cast<T*>(a.kc) + dst)[u] =
-            reinterpret_cast<const uint4*>(static_cast<const T*>(a.kin) + in)[u];
-        reinterpret_cast<uint4*>(static_cast<T*>(a.vc) + dst)[u] =
-            reinterpret_cast<const uint4*>(static_cast<const T*>(a.vin) + in)[u];
-      }
-      if (g == 0 && tid == 0) {
-        int64_t* np = a.next_pos + s * a.len_ss;
-        const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
-        a.pos[s * a.m_ss + a.n_old] = pv;
-        a.modality[s * a.m_ss + a.n_old] = 0;
-        a.round_id[s * a.m_ss + a.n_old] = a.round_value;
-        *np = pv + 1;
-        a.len[s * a.len_ss] = n;
-      }
-    }
+    if (warp == 0 && lane == 0) reinterpret_cast<int*>(slot)[0] = u;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&epi_full[sl]);
+    ++k;
+    fresh = true;
+  }
+  if (a.ctat && tid == 0) {
+    a.ctat[8 * c + 3] = globaltimer();
+    a.ctat[8 * c + 4] = k;
+    a.ctat[8 * c + 5] = t_epi_wait;
+  }
+  // end marker for the epilogue warp
+  {
+    const int sl = k & 1;
+    mbar_wait(&epi_empty[sl], ((k >> 1) & 1) ^ 1);
+    if (warp == 0 && lane == 0) reinterpret_cast<int*>(slots + sl * SLOT)[0] = -1;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&epi_full[sl]);
+  }
+
+  handoff_sync();  // this CTA's epilogue warp has published its partials
+  if (a.tstamp && tid == 0) atomicMax(&a.tstamp[1], globaltimer());
+  if (a.ctat && tid == 0) a.ctat[8 * c + 2] = globaltimer();
+  if (tid == 0) {
+    // the merge kernel counts finished CTAs; the last CTA out resets the ticket
+    // counter and the (already observed) flag of the previous merge
     __threadfence();
-    consumers_sync();
-    const int64_t seg0 = (int64_t)sigma * a.nt;
-    const int c_lo = tile_owner(seg0, a.T, P);
-    const int c_hi = tile_owner(seg0 + a.nt - 1, a.T, P);
-    if (tid == 0) {
-      const int prev = atomicAdd(&a.counters[sigma], 1);
-      *flag = prev == c_hi - c_lo;
+    atomicAdd(&a.sched[1], 1);
+    if (atomicAdd(&a.sched[2], 1) == P - 1) {
+      a.sched[0] = 0;
+      a.sched[2] = 0;
+      if (a.done_prev) *const_cast<int32_t*>(a.done_prev) = 0;
     }
-    consumers_sync();
-    if (*flag) {
+  }
+}
+
+// Segment merge (one CTA per (stream, kv-head) segment): combines the nc chunk
+// partials in chunk order (deterministic), writes the attention output and the
+// per-head (max, sum).  Launched right after the decode kernel with
+// programmatic dependent launch: its CTAs are tiny, become resident while the
+// decode kernel still runs, and let the next layer's decode CTAs launch and
+// prefetch as soon as decode CTAs retire.
+template <int D, int G>
+__global__ void __launch_bounds__(128) merge_kernel(const AttnArgs a) {
+  constexpr int PW = D + 2;
+  extern __shared__ __align__(16) float msm[];  // [nc][G][PW] staged partials, then [G][nc] weights, [G] sums
+  griddep_launch();
+  const int sigma = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // all decode CTAs resident before any merge CTA exists, so this spin completes
+  if (tid == 0)
+    while (ld_acquire(&a.sched[1]) < a.dctas) __nanosleep(64);
+  __syncthreads();
+  const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+  const float* seg = a.part + (int64_t)sigma * a.nc * G * PW;
+  const int nf = a.nc * G * PW;
+  float* stage = msm;
+  float* fac = msm + nf;
+  for (int x = tid; x < nf; x += 128) stage[x] = __ldcg(seg + x);
+  __syncthreads();
+  for (int h = warp; h < G; h += 4) {
+    float M = -INFINITY;
+    for (int jj = lane; jj < a.nc; jj += 32) M = fmaxf(M, stage[(jj * G + h) * PW + D]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float L = 0.f;
+    for (int jj = lane; jj < a.nc; jj += 32) {
+      const float* pp = stage + (jj * G + h) * PW;
+      const float w = rescale(pp[D], M);
+      fac[h * a.nc + jj] = w;
+      L += w * pp[D + 1];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    if (lane == 0) {
+      fac[G * a.nc + h] = L;
+      if (a.stats) {
+        a.stats[s * a.st_ss + (g * G + h) * 2] = M;
+        a.stats[s * a.st_ss + (g * G + h) * 2 + 1] = L;
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < G * D; idx += 128) {
+    const int h = idx / D, d = idx - h * D;
+    const float* pp = stage + h * PW + d;
+    float acc = 0.f;
+    for (int jj = 0; jj < a.nc; ++jj) acc = fmaf(fac[h * a.nc + jj], pp[jj * G * PW], acc);
+    a.out[s * a.o_ss + (int64_t)(g * G) * D + idx] = acc / fac[G * a.nc + h];
+  }
+  __syncthreads();
+  if (tid == 0) {  // the last merge CTA publishes completion and resets the decode counter
+    __threadfence();
+    if (atomicAdd(&a.sched[3], 1) == (int)gridDim.x - 1) {
+      a.sched[1] = 0;
+      a.sched[3] = 0;
       __threadfence();
-      if (tid < G) {
-        float M = -INFINITY;
-        for (int cc = c_lo; cc <= c_hi; ++cc) M = fmaxf(M, __ldcg(a.part + ((int64_t)(sigma + cc) * G + tid) * PW + D));
-        float L = 0.f;
-        for (int cc = c_lo; cc <= c_hi; ++cc) {
-          const float* pp = a.part + ((int64_t)(sigma + cc) * G + tid) * PW;
-          L += rescale(__ldcg(pp + D), M) * __ldcg(pp + D + 1);
-        }
-        fin[2 * tid] = M;
-        fin[2 * tid + 1] = L;
-        if (a.stats) {
-          a.stats[s * a.st_ss + (g * G + tid) * 2] = M;
-          a.stats[s * a.st_ss + (g * G + tid) * 2 + 1] = L;
-        }
-      }
-      consumers_sync();
-      for (int idx = tid; idx < G * D; idx += 128) {
-        const int h = idx / D, d = idx - h * D;
-        const float M = fin[2 * h], L = fin[2 * h + 1];
-        float acc = 0.f;
-        for (int cc = c_lo; cc <= c_hi; ++cc) {
-          const float* pp = a.part + ((int64_t)(sigma + cc) * G + h) * PW;
-          acc += rescale(__ldcg(pp + D), M) * __ldcg(pp + d);
-        }
-        a.out[s * a.o_ss + (int64_t)(g * G + h) * D + d] = acc / L;
-      }
-      if (tid == 0) a.counters[sigma] = 0;
+      asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.done_self), "r"(1) : "memory");
     }
-    consumers_sync();
   }
 }
 
@@ -403,43 +660,50 @@ __global__ void fold_kernel(const FoldArgs f, int Hq) {
 }
 
 template <typename T, int D, int G>
-static size_t decode_smem() {
-  using Gm = Geo<T, D>;
-  return (size_t)Gm::STAGES * 2 * Gm::TILE + 2 * Gm::STAGES * sizeof(uint64_t) +
-         sizeof(float) * (2 * Gm::NW * G + Gm::NW * G * D + 2 * G + 4);
-}
-
-template <typename T, int D, int G>
 static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st) {
-  const size_t smem = decode_smem<T, D, G>() + 8 * (size_t)a.Hq;
+  using Sm = Smem<T, D, G>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(decode_smem<T, D, G>() + 8 * 1024));
+                                         (int)Sm::bytes(1024));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = smem;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Sm::bytes(a.Hq);
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<T, D, G>, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, D, G>, a);
+  if (e != cudaSuccess) return e;
+  // segment merge, also with programmatic dependent launch
+  const size_t msmem = ((size_t)a.nc * G * (D + 2) + (size_t)G * (a.nc + 1)) * sizeof(float);
+  static bool mattr = false;
+  if (!mattr) {
+    e = cudaFuncSetAttribute(merge_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    mattr = true;
+  }
+  if (msmem > 200 * 1024) return cudaErrorInvalidValue;
+  cfg.gridDim = dim3(a.S * a.Hkv);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = msmem;
+  return cudaLaunchKernelEx(&cfg, merge_kernel<D, G>, a);
 }
 
 template <typename T, int D, int G>
 static int occupancy_t() {
+  using Sm = Smem<T, D, G>;
   static int occ = 0;
   if (!occ) {
-    const size_t smem = decode_smem<T, D, G>() + 8 * 64;
-    cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(decode_smem<T, D, G>() + 8 * 1024));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, 192, smem) != cudaSuccess ||
+    cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::bytes(1024));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, kThreads, Sm::bytes(64)) !=
+            cudaSuccess ||
         occ < 1)
       occ = 1;
   }
@@ -467,6 +731,8 @@ static int occ_group(int group) {
     default: return 1;
   }
 }
+
+int decode_tile_tokens() { return Geo<float, 64>::TT; }
 
 int decode_ctas_per_sm(int dtype, int head_dim, int group) {
   if (dtype == 1) return head_dim == 128 ? occ_group<__nv_bfloat16, 128>(group) : occ_group<__nv_bfloat16, 64>(group);

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -20,6 +21,36 @@
 #include "skv_internal.h"
 
 using namespace skv;
+
+// decode tiles (decode_tile_tokens() tokens) per scheduling chunk (SKV_CHUNK_TILES overrides, for tuning)
+static int chunk_tiles(int G) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_CHUNK_TILES");
+    env = e ? std::max(1, atoi(e)) : 0;
+  }
+  return env ? env : (G >= 2 ? 2 : 2);
+}
+static int q_prefetch() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_QPREFETCH");
+    env = e ? atoi(e) : 0;
+  }
+  return env;
+}
+static int use_flags() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_FLAGS");
+    env = e ? atoi(e) : 0;
+  }
+  return env;
+}
+static int ctas_per_sm_override() {
+  const char* e = getenv("SKV_CTAS_PER_SM");
+  return e ? std::max(1, atoi(e)) : 0;
+}
 
 namespace {
 
@@ -51,6 +82,10 @@ struct skv_ctx {
   float scale;
   int max_ctas;    // persistent decode grid bound (CTAs/SM x SMs)
   int last_layer = -1;  // layer of the last decode launch on the ctx (-1: other work since)
+  int launch_seq = 0;   // decode launches (selects the scheduler slot)
+  int32_t* sched = nullptr;  // [64][4] per-launch ticket / barrier / exit counters
+  int32_t* done = nullptr;   // [64] per-launch completion flags
+  size_t part_floats = 0;    // one parity half of the double-buffered partials
   // device state
   void* k = nullptr;
   void* v = nullptr;
@@ -70,6 +105,10 @@ struct skv_ctx {
   int32_t* first_moved = nullptr;
   float* scores = nullptr;
   int64_t* pos_in = nullptr;  // staging for explicit positions
+  unsigned long long* tbuf = nullptr;  // timing ring [8192][2]
+  unsigned long long* cbuf = nullptr;  // per-CTA timing [64][max_ctas][3]
+  int tcount = 0;
+  bool timing = false;
   int64_t device_bytes = 0;
   // host mirror (uniform over streams)
   std::vector<int> n, whead, wcount, parity, pend_n, pend_slot, pend_par, round_value;
@@ -162,7 +201,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    x->max_ctas = sms * decode_ctas_per_sm(c.dtype, c.head_dim, G);
+    const int occ = decode_ctas_per_sm(c.dtype, c.head_dim, G);
+    const int ovr = ctas_per_sm_override();
+    x->max_ctas = sms * (ovr ? std::min(ovr, occ) : occ);
   }
 
   const size_t SL = x->sl_count();
@@ -185,7 +226,11 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     chk(x->alloc(&x->logits[p], SL * x->Hq * (size_t)x->cap * sizeof(float)));
     chk(x->alloc(&x->stats[p], SL * x->Hq * 2 * sizeof(float)));
   }
-  chk(x->alloc(&x->part, ((size_t)x->S * x->Hkv + x->max_ctas) * x->G * (x->D + 2) * sizeof(float)));
+  const int tiles_cap = (x->cap + decode_tile_tokens() - 1) / decode_tile_tokens();
+  x->part_floats = (size_t)x->S * x->Hkv * ((tiles_cap + chunk_tiles(x->G) - 1) / chunk_tiles(x->G)) * x->G * (x->D + 2);
+  chk(x->alloc(&x->part, 2 * x->part_floats * sizeof(float)));
+  chk(x->alloc(&x->done, 64 * sizeof(int32_t)));
+  chk(x->alloc(&x->sched, 64 * 4 * sizeof(int32_t)));
   chk(x->alloc(&x->counters, (size_t)x->S * x->Hkv * sizeof(int32_t)));
   chk(x->alloc(&x->kept, SL * x->B * sizeof(int32_t)));
   chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
@@ -226,6 +271,46 @@ int skv_destroy(skv_ctx* x) {
 int64_t skv_device_bytes(const skv_ctx* x) { return x ? x->device_bytes : 0; }
 int64_t skv_kernel_launches(const skv_ctx* x) { return x ? x->launches : 0; }
 
+int skv_timing(skv_ctx* x, int enable) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
+  if (enable) {
+    if (!x->tbuf) {
+      cudaError_t e = x->alloc(&x->tbuf, 8192 * 2 * sizeof(unsigned long long));
+      if (e != cudaSuccess) return cuda_fail(e, "timing buffer");
+    }
+    std::vector<unsigned long long> init(8192 * 2);
+    for (int i = 0; i < 8192; ++i) {
+      init[2 * i] = ~0ull;
+      init[2 * i + 1] = 0;
+    }
+    SKV_CK(cudaMemcpy(x->tbuf, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    if (enable == 1 || enable == 3) x->tcount = 0;  // 2: clear values, keep slots (graph replays)
+    if (enable == 3 && !x->cbuf) {
+      cudaError_t e = x->alloc(&x->cbuf, (size_t)64 * x->max_ctas * 8 * sizeof(unsigned long long));
+      if (e != cudaSuccess) return cuda_fail(e, "timing buffer");
+    }
+  }
+  x->timing = enable != 0;
+  return SKV_OK;
+}
+
+int skv_timing_cta(skv_ctx* x, int slot, uint64_t* out) {
+  if (!x || !out || !x->cbuf || slot < 0 || slot >= 64) return fail(SKV_EINVAL, "no per-CTA timing");
+  SKV_CK(cudaDeviceSynchronize());
+  SKV_CK(cudaMemcpy(out, x->cbuf + (size_t)slot * x->max_ctas * 8, (size_t)x->max_ctas * 8 * sizeof(uint64_t),
+                    cudaMemcpyDeviceToHost));
+  return x->max_ctas;
+}
+
+int skv_timing_read(skv_ctx* x, uint64_t* out, int max_pairs) {
+  if (!x || !out) return fail(SKV_EINVAL, "null argument");
+  if (!x->tbuf) return 0;
+  const int n = std::min(std::min(x->tcount, 8192), max_pairs);
+  SKV_CK(cudaDeviceSynchronize());
+  SKV_CK(cudaMemcpy(out, x->tbuf, (size_t)n * 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return n;
+}
+
 // ------------------------------------------------------------------ decode --
 
 static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
@@ -234,9 +319,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   if (n_old + 1 > x->cap)
     return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
   const int n = n_old + 1;
-  const int nt = (n + 31) / 32;
-  const int64_t T = (int64_t)x->S * x->Hkv * nt;
-  const int ctas = (int)std::min<int64_t>(T, x->max_ctas);
+  const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
+  const int nc = (nt + chunk_tiles(x->G) - 1) / chunk_tiles(x->G);
+  const int ctas = std::min(x->S * x->Hkv * nc, x->max_ctas);
+  if ((size_t)nc * x->G * (x->D + 2) * 4 > 190 * 1024) return fail(SKV_EINVAL, "capacity too large for the merge scratch");
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
   AttnArgs a{};
@@ -245,9 +331,16 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.n_old = n_old;
   a.append = 1;
   a.nt = nt;
-  a.T = T;
+  a.ch = chunk_tiles(x->G);
+  a.qpf = q_prefetch();
+  a.nc = nc;
   a.S = x->S;
+  const int seq = x->launch_seq++;
+  a.sched = x->sched + 4 * (seq % 64);
   a.prefetch = x->last_layer >= 0 && x->last_layer != layer;
+  a.done_self = x->done + (seq % 64);
+  a.done_prev = (a.prefetch && use_flags()) ? x->done + ((seq + 63) % 64) : nullptr;
+  a.dctas = ctas;
   a.scale = x->scale;
   const int64_t kv_off = (int64_t)layer * x->kv_layer_stride() * x->elt;
   a.kc = static_cast<char*>(x->k) + kv_off;
@@ -270,7 +363,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   }
   a.stats = x->stats[par] + (int64_t)layer * x->Hq * 2;
   a.st_ss = SLstride * x->Hq * 2;
-  a.part = x->part;
+  a.part = x->part + (size_t)(seq & 1) * x->part_floats;
   a.counters = x->counters;
   a.pos = x->pos + (int64_t)layer * x->cap;
   a.modality = x->modality + (int64_t)layer * x->cap;
@@ -281,6 +374,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.next_pos = x->next_pos + layer;
   a.pos_in = pos_dev;
   a.round_value = x->round_value[layer];
+  if (x->timing) {
+    if (x->cbuf) a.ctat = x->cbuf + (size_t)(x->tcount % 64) * x->max_ctas * 8;
+    a.tstamp = x->tbuf + 2 * (x->tcount++ % 8192);
+  }
   // fold of the pending row (previous recorded step) into its ring slot
   if (x->pend_n[layer] > 0) {
     const int pp = x->pend_par[layer];
@@ -299,7 +396,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   }
   cudaError_t e = launch_decode(x->cfg.dtype, x->D, x->G, ctas, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
-  x->launches++;
+  x->launches += 2;  // decode + segment merge
   x->last_layer = layer;
   x->pend_n[layer] = 0;
   if (record) {
@@ -799,6 +896,7 @@ struct AttendScratch {
   float* stats = nullptr;
   float* part = nullptr;
   int32_t* counters = nullptr;
+  int32_t* sched = nullptr;
   size_t part_floats = 0;
   int heads = 0;
 };
@@ -810,13 +908,13 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   if (heads < 1 || n < 1) return fail(SKV_EINVAL, "keys must be a non-empty sequence of vectors");
   if (head_dim != 64 && head_dim != 128) return fail(SKV_EINVAL, "device attend needs head_dim 64 or 128");
   cudaStream_t st = as_stream(stream);
-  const int nt = (n + 31) / 32;
-  const int64_t T = (int64_t)heads * nt;
+  const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
+  const int nc = (nt + chunk_tiles(1) - 1) / chunk_tiles(1);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int ctas = (int)std::min<int64_t>(T, (int64_t)sms * decode_ctas_per_sm(SKV_DTYPE_F32, head_dim, 1));
-  const size_t need = ((size_t)heads + ctas) * (head_dim + 2);
+  const int ctas = std::min(heads * nc, sms * decode_ctas_per_sm(SKV_DTYPE_F32, head_dim, 1));
+  const size_t need = (size_t)heads * nc * (head_dim + 2);
   if (g_att.part_floats < need || g_att.heads < heads) {
     SKV_CK(cudaStreamSynchronize(st));
     if (g_att.stats) cudaFree(g_att.stats);
@@ -828,6 +926,10 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
     SKV_CK(cudaMalloc(&g_att.part, pcap * sizeof(float)));
     SKV_CK(cudaMalloc(&g_att.counters, hcap * sizeof(int32_t)));
     SKV_CK(cudaMemset(g_att.counters, 0, hcap * sizeof(int32_t)));
+    if (!g_att.sched) {
+      SKV_CK(cudaMalloc(&g_att.sched, 8 * sizeof(int32_t)));
+      SKV_CK(cudaMemset(g_att.sched, 0, 8 * sizeof(int32_t)));
+    }
     g_att.part_floats = pcap;
     g_att.heads = hcap;
   }
@@ -837,8 +939,12 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   a.n_old = n;
   a.append = 0;
   a.nt = nt;
-  a.T = T;
+  a.ch = chunk_tiles(1);
+  a.nc = nc;
   a.S = 1;
+  a.sched = g_att.sched;
+  a.done_self = g_att.sched + 4;
+  a.dctas = ctas;
   a.prefetch = 0;
   a.scale = (float)(1.0 / std::sqrt((double)head_dim));
   a.kc = const_cast<float*>(keys);

@@ -31,13 +31,18 @@ struct AttnArgs {
   int Hq, Hkv;          // group size G = Hq / Hkv is a template parameter
   int n_old;            // tokens cached before this step
   int append;           // 1: slot n_old is the new token taken from kin/vin
-  // persistent stream-K schedule: segment sigma = s*Hkv + g holds nt 32-token
-  // tiles; CTA c of P streams global tiles [c*T/P, (c+1)*T/P); the partial of
-  // (CTA c, segment sigma) lives in piece slot sigma + c.
+  // dynamic schedule: segment sigma = s*Hkv + g holds nt 32-token tiles split
+  // into nc chunks of ch tiles; chunk tickets come from sched[0]; the partial
+  // of chunk j of segment sigma lives in part slot sigma*nc + j.
   int nt;               // tiles per segment = ceil(n / 32)
-  int64_t T;            // S * Hkv * nt
+  int ch, nc;           // tiles per chunk, chunks per segment
   int S;                // streams
+  int32_t* sched;       // [4] ticket, grid-barrier and exit counters (zero between launches)
+  int32_t* done_self;   // set to 1 by the merge kernel when this launch's outputs are complete
+  const int32_t* done_prev;  // flag of the preceding merge (null: use griddepcontrol.wait)
+  int dctas;            // decode grid size (the merge waits for this many finished CTAs)
   int prefetch;         // producer may stream cached K/V before griddepcontrol.wait
+  int qpf;              // consumers prefetch the next chunk's q
   float scale;          // f32(1/sqrt(D)), engine.py:150
   void* kc;             // K store base (written for the appended row)
   void* vc;
@@ -53,7 +58,7 @@ struct AttnArgs {
   int64_t l_ss, l_hs;
   float* stats;         // [s][hq][2] (M, L) of this step
   int64_t st_ss;
-  float* part;          // scratch [piece][G][D + 2], piece < S*Hkv + P
+  float* part;          // scratch [sigma*nc + j][G][D + 2]
   int32_t* counters;    // [s*Hkv + g], zero between launches
   // appended token metadata
   int64_t* pos;         // pos[s*m_ss + t]
@@ -66,10 +71,13 @@ struct AttnArgs {
   const int64_t* pos_in;  // optional device [S] explicit positions
   int32_t round_value;
   FoldArgs fold;        // previous step's row (fold.n == 0: none)
+  unsigned long long* tstamp;  // optional [2]: min CTA start / max CTA end (%globaltimer ns)
+  unsigned long long* ctat;    // optional [P][8]: per-CTA timeline (instrumentation)
 };
 
 cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st);
 int decode_ctas_per_sm(int dtype, int head_dim, int group);
+int decode_tile_tokens();
 cudaError_t launch_fold(int streams, int pieces, const FoldArgs& f, int Hq, cudaStream_t st);
 
 // ----------------------------------------------------------------------------

@@ -245,6 +245,16 @@ class StreamEngine:
                                         rbuf.ctypes.data_as(ctypes.c_void_p),
                                         lens.ctypes.data_as(ctypes.c_void_p)))
 
+    def timing(self, enable: bool = True):
+        """Record per-decode-launch device timestamps (first CTA start, last CTA end)."""
+        check(self.lib.skv_timing(self._h, int(bool(enable))))
+
+    def timing_read(self) -> np.ndarray:
+        """(count, 2) uint64 ns: [start, end] of each decode launch since enabling."""
+        buf = np.zeros((8192, 2), dtype=np.uint64)
+        n = check(self.lib.skv_timing_read(self._h, buf.ctypes.data_as(ctypes.c_void_p), 8192))
+        return buf[:n].copy()
+
     # -------------------------------------------------------------- graphs --
     def capture_begin(self):
         check(self.lib.skv_capture_begin(self._h, _stream_handle()))
