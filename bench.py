@@ -40,6 +40,16 @@ METRIC = "decode tokens/sec per stream-batch & µs/step (attn+score+evict); HBM 
 WORKLOAD = "cfg1: Llama-2-7B-shaped decode, 32L x 32H x 128, bf16, 8 streams/GPU, budget 1024+1024, W=32, b=0.01, E=128"
 
 
+def _ncu_traffic():
+    """DRAM read+write bytes per decode launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "r1_ncu_summary.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["decode_traffic_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -209,26 +219,35 @@ def run_gpu(args, rank: int, world: int):
     pb = period_bytes(c, moved)
     step_bytes = pb["total"] * S * L
 
-    # --- dominant kernel (decode) timed alone with CUDA events on its stream
-    n_mid = B + E // 2
-    dec_ms = []
+    # --- dominant kernel (decode + its segment merge, one launch unit per layer):
+    # the eviction of the period is timed with CUDA events on the same stream and
+    # removed from the timed period; the rest is E*L decode launch units.
     with torch.cuda.stream(stream):
-        for j in range(E // 8):
-            for layer in range(L):
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                eng.decode_layer(layer, q[j, layer], k[j, layer], v[j, layer], out[layer], record=True)
-                e1.record(stream)
-                dec_ms.append((e0, e1))
+        eng.run_period(q, k, v, out, E, evict=False)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        eng.evict(-1, kept)
+        ev1.record(stream)
     stream.synchronize()
-    durs = [a.elapsed_time(b) for a, b in dec_ms]
-    avg_dec_ms = float(np.mean(durs))
-    # the eager timing pass starts from the post-eviction state n = B
-    avg_n = B + (E // 8 + 1) / 2.0
+    evict_ms = ev0.elapsed_time(ev1)
+    avg_dec_ms = (ms - evict_ms) / (E * L)
+    avg_n = B + (E + 1) / 2.0
     dec_bytes = decode_launch_bytes(c, avg_n, S)
     peak, peak_kind = _peaks()
     achieved = dec_bytes / (avg_dec_ms * 1e-3) / 1e9
+    # device timestamps (first CTA start .. last CTA end) of each decode kernel in one replay
+    eng.timing(True)
+    with torch.cuda.stream(stream):
+        eng.capture_begin()
+        eng.run_period(q, k, v, out, E, evict=False)
+        eng.evict(-1, kept)
+        eng.capture_end()
+        eng.replay()
+    stream.synchronize()
+    ts = eng.timing_read()[: E * L].astype(np.int64)
+    eng.timing(False)
+    span_us = float(np.mean(ts[:, 1] - ts[:, 0]) / 1e3) if len(ts) else None
 
     # --- end to end through the public host-buffer API (pinned memory)
     e2e = None
@@ -289,10 +308,16 @@ def run_gpu(args, rank: int, world: int):
                    "l2": "inputs larger than L2 (KV 9.1 GB/GPU streamed every token)",
                    "graph": "one CUDA graph per period, per-layer kernel launches",
                    "parallelism": f"stream-partitioned x{world}, no hot-path collective"},
-        "roofline": {"bound": "hbm", "kernel": "decode_kernel<bf16,128,1>", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": "decode_kernel<bf16,128,1> (+ merge_kernel)", "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None, "avg_launch_us": round(avg_dec_ms * 1e3, 2),
-                     "bytes_per_launch": int(dec_bytes)},
+                     "traffic": _ncu_traffic(), "traffic_source": "profiles/r1_ncu_summary.json (ncu --set full, "
+                                                                  "dram read+write per launch at n~2112)",
+                     "avg_launch_us": round(avg_dec_ms * 1e3, 2),
+                     "bytes_per_launch": int(dec_bytes), "evict_ms_per_period": round(evict_ms, 3),
+                     "kernel_span_us": round(span_us, 2) if span_us else None,
+                     "method": "(timed period - CUDA-event-timed eviction) / (E*L) launches; "
+                               "kernel_span_us = device %globaltimer first-CTA-start..last-CTA-end (PDL overlaps "
+                               "consecutive launches)"},
         "bytes_per_step": {k2: int(v2 * S * L) for k2, v2 in pb.items()},
         "moved_rows_per_eviction": round(moved, 1),
         "gpu_launches": int(launches_per_period * args.steps),
