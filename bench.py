@@ -329,14 +329,14 @@ def run_gpu(args, rank: int, world: int):
 
 
 # --------------------------------------------------------------- CPU arm --
-def _cpu_worker(job):
-    """Run the oracle (reference algorithm, NumPy f32, 1 BLAS thread) on a set of
-    (stream, layer) lanes: d decode steps + one eviction; returns timings."""
+def _cpu_proc(conn, lanes, d, seed, c):
+    """Worker process: holds `lanes` (stream, layer) states of the oracle
+    (reference algorithm, NumPy f32, one BLAS thread); each request runs d decode
+    steps + one eviction on every lane and returns the two timings."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle.streamkv_oracle import LayerKV, PolicyConfig, RowWindow, attend_heads, head_mean, saddle_decide, \
         bf16_round
 
-    lanes, d, seed, c = job
     H, D = c["heads_q"], c["head_dim"]
     l, r, W = c["recent"], c["relevant"], c["window"]
     B = l + r
@@ -354,42 +354,78 @@ def _cpu_worker(job):
             w.push(rng.dirichlet(np.ones(B)).astype(np.float32))
         stores.append(st)
         wins.append(w)
-    qs = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
-    ks = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
-    vs = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
     scale = np.float32(1.0 / np.sqrt(D))
-    t0 = time.perf_counter()
-    for t in range(d):
+    pos = B
+    conn.send("ready")
+    while conn.recv() is not None:
+        qs = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
+        ks = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
+        vs = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
+        t0 = time.perf_counter()
+        for t in range(d):
+            for i in range(lanes):
+                st = stores[i]
+                st.append(ks[t, i], vs[t, i], pos + t)
+                probs, _ = attend_heads(st.keys(), st.values(), qs[t, i], scale)
+                wins[i].push(head_mean(probs))
+        t1 = time.perf_counter()
         for i in range(lanes):
-            st = stores[i]
-            st.append(ks[t, i], vs[t, i], B + t)
-            probs, _ = attend_heads(st.keys(), st.values(), qs[t, i], scale)
-            wins[i].push(head_mean(probs))
-    t1 = time.perf_counter()
-    for i in range(lanes):
-        dec = saddle_decide(wins[i], stores[i].n, cfg)
-        stores[i].gather_keep(dec.kept)
-        wins[i].remap(dec.kept)
-    t2 = time.perf_counter()
-    return t1 - t0, t2 - t1
+            dec = saddle_decide(wins[i], stores[i].n, cfg)
+            stores[i].gather_keep(dec.kept)
+            wins[i].remap(dec.kept)
+        t2 = time.perf_counter()
+        pos += d
+        conn.send((t1 - t0, t2 - t1))
 
 
-def cpu_sample(d: int = 4, procs: int = None, seed: int = 0):
-    """One bounded sample of the workload on all host cores; returns
-    (tokens/s extrapolated to a full period, details)."""
-    c = dict(CFG)
-    S, L, E = c["streams"], c["layers"], c["period"]
-    lanes_total = S * L
-    procs = procs or min(os.cpu_count() or 1, lanes_total)
-    per = [lanes_total // procs + (1 if i < lanes_total % procs else 0) for i in range(procs)]
-    jobs = [(n, d, seed + i, c) for i, n in enumerate(per) if n > 0]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(len(jobs)) as pool:
-        res = pool.map(_cpu_worker, jobs)
-    # each process covers its lanes for the whole period: E/d decode samples + 1 eviction
-    period_s = max(dec * E / d + ev for dec, ev in res)
-    return S * E / period_s, {"procs": len(jobs), "lanes": lanes_total, "decode_steps_sampled": d,
-                              "period_s": period_s}
+class CpuReference:
+    """The reference algorithm (oracle port) on all host cores: one single-threaded
+    process per group of (stream, layer) lanes of the config-1 workload."""
+
+    def __init__(self, d: int = 2, procs: int = None, seed: int = 0):
+        c = dict(CFG)
+        self.S, self.E, self.d = c["streams"], c["period"], d
+        lanes_total = c["streams"] * c["layers"]
+        procs = procs or min(os.cpu_count() or 1, lanes_total)
+        per = [lanes_total // procs + (1 if i < lanes_total % procs else 0) for i in range(procs)]
+        ctx = mp.get_context("fork")
+        self.conns, self.procs = [], []
+        for i, n in enumerate(per):
+            if n == 0:
+                continue
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_cpu_proc, args=(b, n, d, seed + i, c), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for cn in self.conns:
+            assert cn.recv() == "ready"
+        self.info = {"procs": len(self.procs), "lanes": lanes_total, "decode_steps_sampled": d}
+
+    def sample(self):
+        """tokens/s extrapolated to a full period: each process covers its lanes for
+        E/d decode samples + 1 eviction; the job takes the slowest process."""
+        for cn in self.conns:
+            cn.send(1)
+        res = [cn.recv() for cn in self.conns]
+        period_s = max(dec * self.E / self.d + ev for dec, ev in res)
+        return self.S * self.E / period_s
+
+    def close(self):
+        for cn in self.conns:
+            cn.send(None)
+        for p in self.procs:
+            p.join(timeout=10)
+
+
+def cpu_sample(d: int = 2, procs: int = None, seed: int = 0):
+    ref = CpuReference(d, procs, seed)
+    try:
+        ref.sample()  # warm
+        v = ref.sample()
+    finally:
+        ref.close()
+    return v, ref.info
 
 
 def run_reference(args, rank: int, world: int):
@@ -397,13 +433,14 @@ def run_reference(args, rank: int, world: int):
 
     if rank != 0:
         return None
-    cores = os.cpu_count() or 1
-    vals = []
-    for _ in range(args.warmup):
-        cpu_sample(d=args.ref_decode_steps)
-    for i in range(args.steps):
-        v, info = cpu_sample(d=args.ref_decode_steps, seed=100 + i)
-        vals.append(v)
+    ref = CpuReference(d=args.ref_decode_steps, seed=100)
+    try:
+        for _ in range(args.warmup):
+            ref.sample()
+        vals = [ref.sample() for _ in range(args.steps)]
+    finally:
+        ref.close()
+    info = ref.info
     value = float(np.median(vals))
     c = CFG
     sample = (f"{info['lanes']} (stream, layer) lanes over {info['procs']} processes x 1 BLAS thread: "
