@@ -57,6 +57,9 @@ typedef struct skv_config {
   int32_t window;          /* W rows of AttentionWindow(capacity=W), policies.py:98 */
   int32_t capacity;        /* max cached tokens per (stream, layer) */
   int32_t head_agg;        /* SKV_AGG_* */
+  int32_t heads_q_total;   /* 0, or the query heads of all head shards: a shard's window rows are
+                              its heads' probability sums / heads_q_total, so the shards' rows add
+                              up to the reference head mean */
 } skv_config;
 
 typedef struct skv_ctx skv_ctx;
@@ -103,6 +106,15 @@ int skv_decode_step_host(skv_ctx* ctx, const void* q_host, const void* k_host, c
  *            rows padded with -1 when the cache fits the budget (keep-all).
  * Returns SKV_EINVAL if a window is empty (policies.py:191-192). */
 int skv_evict(skv_ctx* ctx, int layer, int32_t* kept_dev, void* stream);
+
+/* Head-sharded eviction (KV heads split across GPUs, SURVEY 8e "layer" mode):
+ * skv_evict_scores writes this shard's window-mean scores without the bias,
+ * [S][L'][capacity] f32 (first n-l columns valid); the caller sums them across
+ * shards (one all-reduce of (n-l) floats per (stream, layer)), then
+ * skv_evict_apply adds the bias, selects and compacts exactly like skv_evict.
+ * Every shard then holds the same kept sets. */
+int skv_evict_scores(skv_ctx* ctx, int layer, float* scores_dev, void* stream);
+int skv_evict_apply(skv_ctx* ctx, int layer, const float* scores_dev, int32_t* kept_dev, void* stream);
 
 /* ---- state access -------------------------------------------------------- */
 /* Current cached length of (stream, layer): KvCache.length (cache.py:90-91). */

@@ -40,6 +40,7 @@ class SkvConfig(ctypes.Structure):
         ("window", ctypes.c_int32),
         ("capacity", ctypes.c_int32),
         ("head_agg", ctypes.c_int32),
+        ("heads_q_total", ctypes.c_int32),
     ]
 
 
@@ -58,6 +59,8 @@ SIGNATURES = {
     "skv_decode_step": (_I, [_P, _P, _P, _P, _P, _I, _P]),
     "skv_decode_step_host": (_I, [_P, _P, _P, _P, _P, _I]),
     "skv_evict": (_I, [_P, _I, _P, _P]),
+    "skv_evict_scores": (_I, [_P, _I, _P, _P]),
+    "skv_evict_apply": (_I, [_P, _I, _P, _P, _P]),
     "skv_length": (_I, [_P, _I, _I]),
     "skv_kv_view": (_I, [_P, _I, _I, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
     "skv_positions": (_I, [_P, _I, _I, _P, _I]),

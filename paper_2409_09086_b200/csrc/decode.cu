@@ -87,7 +87,7 @@ __device__ void fold_columns(const FoldArgs& f, int s, int c0, int c1, int Hq, i
         acc = __fadd_rn(acc, p);
       }
     }
-    if (f.mode == 0) row[j] = __fdiv_rn(acc, (float)Hq);
+    if (f.mode == 0) row[j] = __fdiv_rn(acc, (float)(f.agg_div ? f.agg_div : Hq));
     else if (f.mode == 1) row[j] = acc;
   }
 }

@@ -181,11 +181,17 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
     const float inv_m = (float)a.count;
     float* sc = a.scores + b * a.s_bs;
     const float* rows = a.rows + b * a.r_bs;
+    const float* sin = a.scores_in ? a.scores_in + b * a.si_bs : nullptr;
     for (int c = tid; c < cols; c += blockDim.x) {
-      float acc = 0.f;
-      for (int k = 0; k < a.count; ++k)
-        if (c < len_of[k]) acc = __fadd_rn(acc, rows[(int64_t)slot_of[k] * a.row_stride + c]);
-      float v = __fdiv_rn(acc, inv_m);
+      float v;
+      if (sin) {
+        v = sin[c];
+      } else {
+        float acc = 0.f;
+        for (int k = 0; k < a.count; ++k)
+          if (c < len_of[k]) acc = __fadd_rn(acc, rows[(int64_t)slot_of[k] * a.row_stride + c]);
+        v = __fdiv_rn(acc, inv_m);
+      }
       if (a.apply_bias) v = __fadd_rn(v, __fmul_rn(negd, (float)(cols - 1 - c)));
       sc[c] = v;
     }

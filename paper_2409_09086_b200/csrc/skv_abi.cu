@@ -79,6 +79,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 struct skv_ctx {
   skv_config cfg;
   int S, L, Hq, Hkv, D, G, cap, W, B, elt;
+  int Hq_total;  // query heads across all head shards (row mean divisor)
   float scale;
   int max_ctas;    // persistent decode grid bound (CTAs/SM x SMs)
   int last_layer = -1;  // layer of the last decode launch on the ctx (-1: other work since)
@@ -181,6 +182,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   if (!(c.bias >= 0.f)) return fail(SKV_EINVAL, "bias must be >= 0");
   if (c.window < 1 || c.window > 1024) return fail(SKV_EINVAL, "window capacity must be in [1, 1024]");
   if (c.head_agg != SKV_AGG_MEAN && c.head_agg != SKV_AGG_MAX) return fail(SKV_EINVAL, "unknown head_agg");
+  if (c.heads_q_total < 0 || (c.heads_q_total > 0 && c.heads_q_total < c.heads_q))
+    return fail(SKV_EINVAL, "heads_q_total must be 0 or >= heads_q");
   if (c.capacity < c.recent_len + c.relevant_budget + 1)
     return fail(SKV_EINVAL, "capacity must exceed recent_len + relevant_budget");
 
@@ -189,6 +192,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   x->S = c.streams;
   x->L = c.layers;
   x->Hq = c.heads_q;
+  x->Hq_total = c.heads_q_total > 0 ? c.heads_q_total : c.heads_q;
   x->Hkv = c.heads_kv;
   x->D = c.head_dim;
   x->G = G;
@@ -393,6 +397,8 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     f.w_ss = SLstride * x->W;
     f.n = x->pend_n[layer];
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
+  f.agg_div = x->Hq_total;
+    f.agg_div = x->Hq_total;
   }
   cudaError_t e = launch_decode(x->cfg.dtype, x->D, x->G, ctas, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
@@ -427,6 +433,7 @@ static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
   f.w_ss = (int64_t)x->L * x->W;
   f.n = x->pend_n[layer];
   f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
+  f.agg_div = x->Hq_total;
   const int pieces = std::max(1, std::min(64, (f.n + 255) / 256));
   cudaError_t e = launch_fold(x->S, pieces, f, x->Hq, st);
   if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
@@ -523,7 +530,10 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
 
 // ------------------------------------------------------------------- evict --
 
-static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStream_t st) {
+// mode 0: decide + compact; 1: write unbiased window-mean scores only (head-sharded
+// partials, [S][L'][cap]); 2: decide from given scores (+bias) + compact.
+static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_ld, int kept_off, cudaStream_t st,
+                        int mode = 0, float* scores_io = nullptr, int scores_ld = 0, int scores_off = 0) {
   // all layers in [l0, l1) share n / ring state (checked by caller)
   const int nl = l1 - l0;
   const int n = x->n[l0];
@@ -539,8 +549,10 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
   a.l = x->cfg.recent_len;
   a.r = x->cfg.relevant_budget;
   a.bias = x->cfg.bias;
-  a.apply_bias = 1;
+  a.apply_bias = mode == 1 ? 0 : 1;
+  a.scores_only = mode == 1;
   a.pad = x->B;
+  if (mode == 1 && n <= x->B) return SKV_OK;  // keep-all decision: nothing to score
   CompactArgs c{};
   c.heads = x->Hkv;
   c.row_bytes = x->D * x->elt;
@@ -555,14 +567,19 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
     a.w_bs = x->W;
     a.kept32 = x->kept;
     a.k_bs = x->B;
-    a.scores = x->scores;
+    a.scores = mode == 1 ? scores_io : x->scores;
     a.s_bs = x->cap;
+    if (mode == 2) {
+      a.scores_in = scores_io;
+      a.si_bs = x->cap;
+    }
     a.first_moved = x->first_moved;
     a.newlen = x->newlen;
     cudaError_t e = launch_select(x->S * x->L, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
     x->launches++;
     x->last_layer = -1;
+    if (mode == 1) return SKV_OK;
     c.k = static_cast<char*>(x->k);
     c.v = static_cast<char*>(x->v);
     c.kv_bs = x->kv_layer_stride() * x->elt;
@@ -593,14 +610,19 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
       a.w_bs = (int64_t)x->L * x->W;
       a.kept32 = x->kept + sl0 * x->B;
       a.k_bs = (int64_t)x->L * x->B;
-      a.scores = x->scores + sl0 * x->cap;
-      a.s_bs = (int64_t)x->L * x->cap;
+      a.scores = mode == 1 ? scores_io + (int64_t)scores_off * x->cap : x->scores + sl0 * x->cap;
+      a.s_bs = mode == 1 ? (int64_t)scores_ld * x->cap : (int64_t)x->L * x->cap;
+      if (mode == 2) {
+        a.scores_in = scores_io + (int64_t)scores_off * x->cap;
+        a.si_bs = (int64_t)scores_ld * x->cap;
+      }
       a.first_moved = x->first_moved + sl0 * x->S;  // scratch slice of S entries
       a.newlen = x->newlen + sl0 * x->W;
       cudaError_t e = launch_select(x->S, a, st);
       if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
       x->launches++;
       x->last_layer = -1;
+      if (mode == 1) continue;
       c.k = static_cast<char*>(x->k) + sl0 * x->kv_layer_stride() * x->elt;
       c.v = static_cast<char*>(x->v) + sl0 * x->kv_layer_stride() * x->elt;
       c.kv_bs = x->kv_stream_stride() * x->elt;
@@ -624,17 +646,18 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, cudaStrea
       x->last_layer = -1;
     }
   }
+  if (mode == 1) return SKV_OK;
   if (kept_dev) {
-    // [S][nl][B] copy out of the [S][L][B] scratch
-    SKV_CK(cudaMemcpy2DAsync(kept_dev, (size_t)nl * x->B * sizeof(int32_t), x->kept + (int64_t)l0 * x->B,
-                             (size_t)x->L * x->B * sizeof(int32_t), (size_t)nl * x->B * sizeof(int32_t), x->S,
-                             cudaMemcpyDeviceToDevice, st));
+    // [S][kept_ld][B] (rows kept_off .. kept_off+nl) out of the [S][L][B] scratch
+    SKV_CK(cudaMemcpy2DAsync(kept_dev + (int64_t)kept_off * x->B, (size_t)kept_ld * x->B * sizeof(int32_t),
+                             x->kept + (int64_t)l0 * x->B, (size_t)x->L * x->B * sizeof(int32_t),
+                             (size_t)nl * x->B * sizeof(int32_t), x->S, cudaMemcpyDeviceToDevice, st));
   }
   for (int l = l0; l < l1; ++l) x->n[l] = m;
   return SKV_OK;
 }
 
-int skv_evict(skv_ctx* x, int layer, int32_t* kept_dev, void* stream) {
+static int evict_common(skv_ctx* x, int layer, int32_t* kept_dev, void* stream, int mode, float* scores) {
   if (!x) return fail(SKV_EINVAL, "null argument");
   if (layer < -1 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
   cudaStream_t st = as_stream(stream);
@@ -642,22 +665,36 @@ int skv_evict(skv_ctx* x, int layer, int32_t* kept_dev, void* stream) {
   for (int l = l0; l < l1; ++l) {
     if (x->wcount[l] == 0) return fail(SKV_EINVAL, "attention window is empty");
   }
-  for (int l = l0; l < l1; ++l) {
-    int rc = flush_pending(x, l, st);
-    if (rc) return rc;
+  if (mode != 2) {
+    for (int l = l0; l < l1; ++l) {
+      int rc = flush_pending(x, l, st);
+      if (rc) return rc;
+    }
   }
   bool uniform = true;
   for (int l = l0 + 1; l < l1; ++l)
     uniform &= x->n[l] == x->n[l0] && x->whead[l] == x->whead[l0] && x->wcount[l] == x->wcount[l0];
-  if (uniform && l0 == 0 && l1 == x->L) {
-    if (kept_dev && layer >= 0) return evict_layers(x, l0, l1, kept_dev, st);
-    return evict_layers(x, l0, l1, kept_dev, st);
-  }
+  const int nl = l1 - l0;
+  if (uniform && l0 == 0 && l1 == x->L) return evict_layers(x, l0, l1, kept_dev, nl, 0, st, mode, scores, nl, 0);
   for (int l = l0; l < l1; ++l) {
-    int rc = evict_layers(x, l, l + 1, kept_dev ? kept_dev + (int64_t)(l - l0) * x->B : nullptr, st);
+    int rc = evict_layers(x, l, l + 1, kept_dev, nl, l - l0, st, mode, scores, nl, l - l0);
     if (rc) return rc;
   }
   return SKV_OK;
+}
+
+int skv_evict(skv_ctx* x, int layer, int32_t* kept_dev, void* stream) {
+  return evict_common(x, layer, kept_dev, stream, 0, nullptr);
+}
+
+int skv_evict_scores(skv_ctx* x, int layer, float* scores_dev, void* stream) {
+  if (!scores_dev) return fail(SKV_EINVAL, "null argument");
+  return evict_common(x, layer, nullptr, stream, 1, scores_dev);
+}
+
+int skv_evict_apply(skv_ctx* x, int layer, const float* scores_dev, int32_t* kept_dev, void* stream) {
+  if (!scores_dev) return fail(SKV_EINVAL, "null argument");
+  return evict_common(x, layer, kept_dev, stream, 2, const_cast<float*>(scores_dev));
 }
 
 // ------------------------------------------------------------ state access --

@@ -25,6 +25,7 @@ struct FoldArgs {
   int64_t p_ss, p_hs;
   int n;                // row length (0: nothing to fold)
   int mode;             // 0 mean over heads, 1 max over heads, 2 per-head probs
+  int agg_div;          // mode 0 divisor (total query heads across shards; 0: Hq)
 };
 
 struct AttnArgs {
@@ -103,6 +104,8 @@ struct SelectArgs {
   int32_t* newlen;      // optional [b*w_bs + slot] ring lengths after remap
   int scores_only;      // 1: stop after writing scores
   int pad;              // keep-all rows: write -1 into kept[n, pad)
+  const float* scores_in;  // optional: window-mean scores given (e.g. reduced across head shards)
+  int64_t si_bs;
 };
 
 cudaError_t launch_select(int batches, const SelectArgs& a, cudaStream_t st);

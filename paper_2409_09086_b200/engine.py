@@ -52,6 +52,7 @@ class EngineConfig:
     capacity: int
     dtype: torch.dtype = torch.bfloat16
     head_agg: str = "mean"
+    heads_q_total: int = 0  # head-sharded engines: query heads of all shards (0: heads_q)
 
     @property
     def budget(self) -> int:
@@ -82,6 +83,7 @@ class StreamEngine:
             window=cfg.window,
             capacity=cfg.capacity,
             head_agg=_lib.AGG_MAX if cfg.head_agg == "max" else _lib.AGG_MEAN,
+            heads_q_total=cfg.heads_q_total,
         )
         handle = ctypes.c_void_p()
         torch.cuda.init()
@@ -168,6 +170,19 @@ class StreamEngine:
         ``kept`` (optional, int32 CUDA, (S, L', r+l)) receives the kept sets;
         rows of a keep-all decision hold 0..n-1 padded with -1."""
         check(self.lib.skv_evict(self._h, int(layer), _ptr(kept), _stream_handle()))
+        return kept
+
+    def evict_scores(self, layer: int = -1) -> torch.Tensor:
+        """This shard's unbiased window-mean scores, (S, L', capacity) f32 (first n-l valid)."""
+        nl = self.cfg.layers if layer < 0 else 1
+        scores = torch.zeros((self.cfg.streams, nl, self.cap), dtype=torch.float32, device="cuda")
+        check(self.lib.skv_evict_scores(self._h, int(layer), _ptr(scores), _stream_handle()))
+        return scores
+
+    def evict_apply(self, scores: torch.Tensor, layer: int = -1, kept: Optional[torch.Tensor] = None):
+        """Bias + top-r + recent merge + compaction from (reduced) window-mean scores."""
+        check(self.lib.skv_evict_apply(self._h, int(layer), _ptr(scores.contiguous()), _ptr(kept),
+                                       _stream_handle()))
         return kept
 
     def run_period(self, q, k, v, out, steps: int, evict: bool = True):
