@@ -1,21 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the Inf-MLLM streaming decode + score + evict hot path on B200.
 
-Workload (BASELINE.json config 1, Llama-2-7B-shaped decode): 32 layers x 32
-heads x head_dim 128, bf16, 8 independent streams per GPU, KV budget 2048 =
-1024 recent + 1024 relevant, relevance window W = 32 queries, attention bias
+Default workload (BASELINE.json config 1, Llama-2-7B-shaped decode): 32 layers
+x 32 heads x head_dim 128, bf16, 8 independent streams per GPU, KV budget 2048
+= 1024 recent + 1024 relevant, relevance window W = 32 queries, attention bias
 b = 0.01, eviction every E = 128 tokens.  Synthetic q/k/v ~ N(0,1) with 1% of
 keys x4 (random-init stand-in; no model weights or datasets).
 
-One bench "step" = one eviction period at steady state: E = 128 decode tokens
-for every stream through all 32 layers (append + attention + relevance row)
-followed by one eviction of every (stream, layer) (score + bias + top-k +
-in-place compaction).  value = decode tokens/s of the whole job.
+One bench "step" = one eviction period at steady state: E decode tokens for
+every stream through all layers (append + attention + relevance row) followed
+by one eviction of every (stream, layer) (score + bias + top-k + in-place
+compaction).  value = decode tokens/s of the whole job.
 
-  python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
+  python bench.py [--gpus N --steps K --warmup W]            # our CUDA path (config 1)
+  python bench.py --workload cfg3|cfg4 [--budget B]           # configs 3 / 4
   python bench.py --impl reference [...]                      # CPU reference arm
-Under torchrun every rank runs its own 8 streams (weak scaling, no collective
-on the hot path); rank 0 prints one JSON line.
+Under torchrun every rank runs its own streams (configs 1 and 4: weak / even
+stream partition, no collective on the hot path) or its own KV heads of the
+single stream (config 3: one all-reduce of the window scores per eviction).
+Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -34,10 +37,31 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(layers=32, heads_q=32, heads_kv=32, head_dim=128, streams=8, recent=1024, relevant=1024,
-           window=32, bias=0.01, period=128, spike_prob=0.01, spike_gain=4.0)
-METRIC = "decode tokens/sec per stream-batch & µs/step (attn+score+evict); HBM GB/s vs peak"
-WORKLOAD = "cfg1: Llama-2-7B-shaped decode, 32L x 32H x 128, bf16, 8 streams/GPU, budget 1024+1024, W=32, b=0.01, E=128"
+METRIC = "decode tokens/sec per stream-batch & \u00b5s/step (attn+score+evict); HBM GB/s vs peak"
+
+WORKLOADS = {
+    "cfg1": dict(layers=32, heads_q=32, heads_kv=32, head_dim=128, streams=8, recent=1024, relevant=1024, window=32,
+                 bias=0.01, period=128, spike_prob=0.01, spike_gain=4.0, shard="streams", scaling="weak",
+                 desc="cfg1: Llama-2-7B-shaped decode, 32L x 32H x 128, bf16, 8 streams/GPU, budget 1024+1024, "
+                      "W=32, b=0.01, E=128"),
+    "cfg3": dict(layers=32, heads_q=32, heads_kv=8, head_dim=128, streams=1, recent=2048, relevant=2048, window=32,
+                 bias=0.01, period=256, spike_prob=0.005, spike_gain=4.0, shard="heads", scaling="strong",
+                 desc="cfg3: Llama-3-8B GQA-shaped decode, 32L x 32q/8kv x 128, bf16, batch 1, budget 2048+2048, "
+                      "W=32, b=0.01, E=256, KV heads sharded over GPUs"),
+    "cfg4": dict(layers=32, heads_q=32, heads_kv=32, head_dim=128, streams=256, recent=1024, relevant=1024, window=32,
+                 bias=0.01, period=128, spike_prob=0.01, spike_gain=4.0, shard="streams", scaling="strong",
+                 desc="cfg4: 256 Llama-2-7B-shaped streams partitioned over GPUs, bf16, W=32, b=0.01, E=128"),
+}
+CFG = WORKLOADS["cfg1"]
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
 
 
 def _ncu_traffic():
@@ -48,15 +72,6 @@ def _ncu_traffic():
             return float(json.load(f)["decode_traffic_bytes_per_launch"])
     except Exception:
         return None
-
-
-def _peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
 
 
 # ------------------------------------------------------------------ clocks --
@@ -113,25 +128,39 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+
+
 # ------------------------------------------------------------- accounting --
-def period_bytes(c, moved_rows_per_sl: float) -> dict:
+def period_bytes(c, hkv: int, moved_rows_per_sl: float) -> dict:
     """Algorithmic HBM bytes of one period, per (stream, layer)."""
     s = 2
-    B, E, Hq, Hkv, D, W, l = c["recent"] + c["relevant"], c["period"], c["heads_q"], c["heads_kv"], c["head_dim"], \
-        c["window"], c["recent"]
-    kv = sum(2 * (B + j) * Hkv * D * s for j in range(1, E + 1))
-    step_io = E * (Hq * D * s + 2 * Hkv * D * s + Hq * D * 4)
+    B, E, D, W, l = c["recent"] + c["relevant"], c["period"], c["head_dim"], c["window"], c["recent"]
+    hq = hkv * (c["heads_q"] // c["heads_kv"])
+    kv = sum(2 * (B + j) * hkv * D * s for j in range(1, E + 1))
+    step_io = E * (hq * D * s + 2 * hkv * D * s + hq * D * 4)
     n_e = B + E
     window = 8 * (n_e - l) * W
-    evict = 4 * (n_e - l) + 4 * B + 4 * moved_rows_per_sl * Hkv * D * s
+    evict = 4 * (n_e - l) + 4 * B + 4 * moved_rows_per_sl * hkv * D * s
     return dict(kv=kv, step_io=step_io, window=window, evict=evict, total=kv + step_io + window + evict)
 
 
-def decode_launch_bytes(c, n: int, streams: int) -> int:
-    """Algorithmic bytes of one decode-kernel launch (one layer, all streams, cache length n)."""
+def decode_launch_bytes(c, hkv: int, n: float, streams: int) -> float:
+    """Algorithmic bytes of one decode launch (one layer, all resident streams, cache length n)."""
     s = 2
-    Hq, Hkv, D = c["heads_q"], c["heads_kv"], c["head_dim"]
-    return streams * (2 * n * Hkv * D * s + Hq * D * s + 2 * Hkv * D * s + Hq * D * 4)
+    hq = hkv * (c["heads_q"] // c["heads_kv"])
+    D = c["head_dim"]
+    return streams * (2 * n * hkv * D * s + hq * D * s + 2 * hkv * D * s + hq * D * 4)
+
+
+def _max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 # --------------------------------------------------------------- GPU arm --
@@ -140,56 +169,97 @@ def run_gpu(args, rank: int, world: int):
     import torch.distributed as dist
 
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
+    from paper_2409_09086_b200.sharding import evict_head_sharded, shard_heads
 
-    c = dict(CFG)
-    S, L, H, Hkv, D = c["streams"], c["layers"], c["heads_q"], c["heads_kv"], c["head_dim"]
+    c = dict(WORKLOADS[args.workload])
+    if args.budget:
+        c["recent"] = c["relevant"] = args.budget // 2
+    L, HQ, HKV, D = c["layers"], c["heads_q"], c["heads_kv"], c["head_dim"]
     l, r, W, E = c["recent"], c["relevant"], c["window"], c["period"]
     B = l + r
+    G = HQ // HKV
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    eng = StreamEngine(EngineConfig(S, L, H, Hkv, D, l, r, c["bias"], W, B + E, torch.bfloat16))
+    sharded = c["shard"] == "heads" and world > 1
+    if c["shard"] == "heads":
+        kvs, qsl = shard_heads(HKV, G, world, rank)
+        hkv, hq, S = kvs.stop - kvs.start, qsl.stop - qsl.start, c["streams"]
+    else:
+        hkv, hq = HKV, HQ
+        S = c["streams"] if c["scaling"] == "weak" else c["streams"] // world
+    # streams resident at once (config 4 at large budgets runs in waves)
+    per_stream = 2 * L * hkv * (B + E) * D * 2 * 1.06
+    free = torch.cuda.mem_get_info(dev)[0] - (12 << 30)
+    resident = max(1, min(S, int(free // per_stream)))
+    waves = -(-S // resident)
+    eng = StreamEngine(EngineConfig(resident, L, hq, hkv, D, l, r, c["bias"], W, B + E, torch.bfloat16,
+                                    heads_q_total=HQ if c["shard"] == "heads" else 0))
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def randn(shape):
         return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
 
     def spiked_keys(shape_lead):
-        k = torch.randn((*shape_lead, Hkv, D), generator=g, device=dev, dtype=torch.float32)
+        k = torch.randn((*shape_lead, hkv, D), generator=g, device=dev, dtype=torch.float32)
         spikes = torch.rand(shape_lead, generator=g, device=dev) < c["spike_prob"]
         k[spikes] *= c["spike_gain"]
         return k.to(torch.bfloat16)
 
     # steady state: every (stream, layer) holds a full budget of B tokens
-    for s in range(S):
+    for s in range(resident):
         for layer in range(L):
             kf, vf = eng.kv_full(s, layer)
-            kk = torch.randn((Hkv, B, D), generator=g, device=dev)
+            kk = torch.randn((hkv, B, D), generator=g, device=dev)
             kk[:, torch.rand(B, generator=g, device=dev) < c["spike_prob"]] *= c["spike_gain"]
             kf[:, :B] = kk.to(torch.bfloat16)
-            vf[:, :B] = randn((Hkv, B, D))
+            vf[:, :B] = randn((hkv, B, D))
             eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
-    q = randn((E, L, S, H, D))
-    k = spiked_keys((E, L, S))
-    v = randn((E, L, S, Hkv, D))
-    out = torch.empty((L, S, H, D), dtype=torch.float32, device=dev)
-    kept = torch.full((S, L, B), -1, dtype=torch.int32, device=dev)
+    # distinct inputs for up to E steps (fewer when many streams are resident), reused cyclically
+    T_in = max(1, min(E, int(3e9 // (L * resident * (hq + 2 * hkv) * D * 2))))
+    q = randn((T_in, L, resident, hq, D))
+    k = spiked_keys((T_in, L, resident))
+    v = randn((T_in, L, resident, hkv, D))
+    out = torch.empty((L, resident, hq, D), dtype=torch.float32, device=dev)
+    kept = torch.full((resident, L, B), -1, dtype=torch.int32, device=dev)
 
-    # one eager period to reach the steady ring state, then capture a period graph
-    eng.run_period(q, k, v, out, E, evict=False)
-    eng.evict(-1, kept)
-    torch.cuda.synchronize()
-    launches0 = eng.kernel_launches
+    def evict():
+        if sharded:
+            evict_head_sharded(eng, -1, kept)
+        else:
+            eng.evict(-1, kept)
+
+    def decode_steps():
+        for t in range(E):  # rows are recorded for the last W steps only (run_period's rule)
+            eng.decode_step(q[t % T_in], k[t % T_in], v[t % T_in], out, record=t >= E - W)
+
+    def period():
+        decode_steps()
+        evict()
+
     stream = torch.cuda.Stream(device=dev)
+    use_graph = not sharded  # NCCL stays outside our own graph capture
     with torch.cuda.stream(stream):
-        eng.capture_begin()
-        eng.run_period(q, k, v, out, E, evict=False)
-        eng.evict(-1, kept)
-        eng.capture_end()
-    launches_per_period = eng.kernel_launches - launches0
-    torch.cuda.synchronize()
+        period()  # reach the steady ring state
+    stream.synchronize()
+    launches0 = eng.kernel_launches
+    if use_graph:
+        with torch.cuda.stream(stream):
+            eng.capture_begin()
+            period()
+            eng.capture_end()
+        launches_per_period = eng.kernel_launches - launches0
+
+        def step():
+            eng.replay()
+    else:
+        with torch.cuda.stream(stream):
+            period()
+        stream.synchronize()
+        launches_per_period = eng.kernel_launches - launches0
+        step = period
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            eng.replay()
+            step()
     stream.synchronize()
 
     clocks = ClockSampler(dev.index)
@@ -202,90 +272,83 @@ def run_gpu(args, rank: int, world: int):
     with torch.cuda.stream(stream):
         t0.record(stream)
         for _ in range(args.steps):
-            eng.replay()
+            step()
         t1.record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1) / args.steps
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    wave_ms = _max_over_ranks(t0.elapsed_time(t1) / args.steps, world, dev)
+    ms = wave_ms * waves  # every resident wave of this rank's streams takes one period
 
     kc = kept.cpu().numpy()
     first_moved = np.argmax(kc != np.arange(B)[None, None, :], axis=-1)
     moved = float(np.mean(B - first_moved))
-    pb = period_bytes(c, moved)
-    step_bytes = pb["total"] * S * L
+    pb = period_bytes(c, hkv, moved)
+    step_bytes_rank = pb["total"] * resident * L * waves
 
-    # --- dominant kernel (decode + its segment merge, one launch unit per layer):
-    # the eviction of the period is timed with CUDA events on the same stream and
-    # removed from the timed period; the rest is E*L decode launch units.
+    # --- dominant kernel (decode + its merge, one launch unit per layer): the
+    # eviction is timed with CUDA events on the same stream and removed from the
+    # period; the rest is E*L decode launch units.
     with torch.cuda.stream(stream):
-        eng.run_period(q, k, v, out, E, evict=False)
+        decode_steps()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        eng.evict(-1, kept)
+        evict()
         ev1.record(stream)
     stream.synchronize()
     evict_ms = ev0.elapsed_time(ev1)
-    avg_dec_ms = (ms - evict_ms) / (E * L)
-    avg_n = B + (E + 1) / 2.0
-    dec_bytes = decode_launch_bytes(c, avg_n, S)
+    avg_dec_ms = (wave_ms - evict_ms) / (E * L)
+    dec_bytes = decode_launch_bytes(c, hkv, B + (E + 1) / 2.0, resident)
     peak, peak_kind = _peaks()
     achieved = dec_bytes / (avg_dec_ms * 1e-3) / 1e9
-    # device timestamps (first CTA start .. last CTA end) of each decode kernel in one replay
-    eng.timing(True)
-    with torch.cuda.stream(stream):
-        eng.capture_begin()
-        eng.run_period(q, k, v, out, E, evict=False)
-        eng.evict(-1, kept)
-        eng.capture_end()
-        eng.replay()
-    stream.synchronize()
-    ts = eng.timing_read()[: E * L].astype(np.int64)
-    eng.timing(False)
-    span_us = float(np.mean(ts[:, 1] - ts[:, 0]) / 1e3) if len(ts) else None
+    span_us = None
+    if use_graph:  # device timestamps (first CTA start .. last CTA end) of each decode kernel in one replay
+        eng.timing(True)
+        with torch.cuda.stream(stream):
+            eng.capture_begin()
+            period()
+            eng.capture_end()
+            eng.replay()
+        stream.synchronize()
+        ts = eng.timing_read()[: E * L].astype(np.int64)
+        eng.timing(False)
+        span_us = float(np.mean(ts[:, 1] - ts[:, 0]) / 1e3) if len(ts) else None
 
     # --- end to end through the public host-buffer API (pinned memory)
     e2e = None
     if args.e2e_steps > 0:
-        eng.evict(-1)  # back to n = B
         qh = q.cpu().pin_memory()
         kh = k.cpu().pin_memory()
         vh = v.cpu().pin_memory()
-        oh = torch.empty((L, S, H, D), dtype=torch.float32).pin_memory()
+        oh = torch.empty((L, resident, hq, D), dtype=torch.float32).pin_memory()
         torch.cuda.synchronize()
-        steps = min(args.e2e_steps, E)
+        steps = min(args.e2e_steps, E, T_in)
         for t in range(4):  # warm-up of the host pipeline
             eng.decode_step_host(qh[t], kh[t], vh[t], oh, record=True)
-        eng.evict(-1)
+        evict()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         tic = time.perf_counter()
         for t in range(steps):
             eng.decode_step_host(qh[t], kh[t], vh[t], oh, record=t >= steps - W)
-        eng.evict(-1)
+        evict()
         torch.cuda.synchronize()
-        el = time.perf_counter() - tic
-        if world > 1:
-            tt = torch.tensor([el], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
+        el = _max_over_ranks(time.perf_counter() - tic, world, dev) * waves
+        job_streams = c["streams"] if c["shard"] == "heads" else S * world
         e2e = {
-            "value": S * world * steps / el,
+            "value": round(job_streams * steps / el, 2),
             "unit": "tokens/s",
             "h2d_bytes_per_step": int(qh[0].numel() * 2 + kh[0].numel() * 2 + vh[0].numel() * 2),
             "d2h_bytes_per_step": int(oh.numel() * 4),
             "steps": steps,
-            "note": "skv_decode_step_host per token (pinned host q/k/v in, f32 outputs out) + skv_evict",
+            "note": "skv_decode_step_host per token (pinned host q/k/v in, f32 outputs out) + eviction",
         }
 
-    tokens = S * E * world
-    value = tokens / (ms * 1e-3)
+    job_streams = c["streams"] if c["shard"] == "heads" else S * world
+    value = job_streams * E / (ms * 1e-3)
+    step_bytes_job = _max_over_ranks(step_bytes_rank, 1, dev) * world
     res = {
         "metric": METRIC,
         "value": round(value, 2),
@@ -295,30 +358,33 @@ def run_gpu(args, rank: int, world: int):
         "warmup": args.warmup,
         "ms_per_step": round(ms, 4),
         "us_per_token_step": round(ms * 1e3 / E, 3),
-        "hbm_gbs_step": round(step_bytes / (ms * 1e-3) / 1e9, 1),
-        "hbm_frac_step": round(step_bytes / (ms * 1e-3) / 1e9 / peak, 4),
+        "hbm_gbs_step": round(step_bytes_job / world / (ms * 1e-3) / 1e9, 1),
+        "hbm_frac_step": round(step_bytes_job / world / (ms * 1e-3) / 1e9 / peak, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": c["scaling"],
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (seeded N(0,1) q/k/v, 1% key spikes x4; random cache at budget)",
-        "config": {"workload": WORKLOAD, "streams_per_gpu": S, "global_streams": S * world, "layers": L,
-                   "heads": H, "head_dim": D, "budget": B, "window": W, "period": E,
-                   "step": "one eviction period: 128 decode tokens x 32 layers x streams + 1 all-layer eviction",
-                   "l2": "inputs larger than L2 (KV 9.1 GB/GPU streamed every token)",
-                   "graph": "one CUDA graph per period, per-layer kernel launches",
-                   "parallelism": f"stream-partitioned x{world}, no hot-path collective"},
-        "roofline": {"bound": "hbm", "kernel": "decode_kernel<bf16,128,1> (+ merge_kernel)", "achieved": round(achieved, 1),
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": _ncu_traffic(), "traffic_source": "profiles/r1_ncu_summary.json (ncu --set full, "
-                                                                  "dram read+write per launch at n~2112)",
-                     "avg_launch_us": round(avg_dec_ms * 1e3, 2),
-                     "bytes_per_launch": int(dec_bytes), "evict_ms_per_period": round(evict_ms, 3),
+        "data": "synthetic (seeded N(0,1) q/k/v, key spikes; random cache at budget)",
+        "config": {"workload": c["desc"], "streams_per_gpu": S, "resident_streams": resident, "waves": waves,
+                   "global_streams": job_streams, "layers": L, "heads_q_per_gpu": hq, "heads_kv_per_gpu": hkv,
+                   "head_dim": D, "budget": B, "window": W, "period": E,
+                   "step": f"one eviction period: {E} decode tokens x {L} layers x streams + 1 all-layer eviction",
+                   "l2": "inputs larger than L2 (the whole KV cache is streamed every token)",
+                   "graph": "one CUDA graph per period, per-layer launches" if use_graph else
+                            "eager per-token launches (NCCL all-reduce at eviction)",
+                   "parallelism": (f"kv-heads sharded x{world} (1 all-reduce of window scores per eviction)"
+                                   if sharded else f"stream-partitioned x{world}, no hot-path collective")},
+        "roofline": {"bound": "hbm", "kernel": f"decode_kernel<bf16,128,{G}> (+ merge_kernel)",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4),
+                     "traffic": _ncu_traffic() if args.workload == "cfg1" and not args.budget else None,
+                     "traffic_source": "profiles/r1_ncu_summary.json (ncu --set full, dram read+write per launch)",
+                     "avg_launch_us": round(avg_dec_ms * 1e3, 2), "bytes_per_launch": int(dec_bytes),
+                     "evict_ms_per_period": round(evict_ms, 3),
                      "kernel_span_us": round(span_us, 2) if span_us else None,
-                     "method": "(timed period - CUDA-event-timed eviction) / (E*L) launches; "
-                               "kernel_span_us = device %globaltimer first-CTA-start..last-CTA-end (PDL overlaps "
-                               "consecutive launches)"},
-        "bytes_per_step": {k2: int(v2 * S * L) for k2, v2 in pb.items()},
+                     "method": "(timed period - CUDA-event-timed eviction) / (E*L) launches; kernel_span_us = "
+                               "device %globaltimer first-CTA-start..last-CTA-end (PDL overlaps neighbours)"},
+        "bytes_per_step": {k2: int(v2 * resident * L * waves * world) for k2, v2 in pb.items()},
         "moved_rows_per_eviction": round(moved, 1),
         "gpu_launches": int(launches_per_period * args.steps),
         "clocks": clk,
@@ -328,7 +394,6 @@ def run_gpu(args, rank: int, world: int):
     return res
 
 
-# --------------------------------------------------------------- CPU arm --
 def _cpu_proc(conn, lanes, d, seed, c):
     """Worker process: holds `lanes` (stream, layer) states of the oracle
     (reference algorithm, NumPy f32, one BLAS thread); each request runs d decode
@@ -443,7 +508,7 @@ def run_reference(args, rank: int, world: int):
     info = ref.info
     value = float(np.median(vals))
     c = CFG
-    sample = (f"{info['lanes']} (stream, layer) lanes over {info['procs']} processes x 1 BLAS thread: "
+    sample = (f"config 1: {info['lanes']} (stream, layer) lanes over {info['procs']} processes x 1 BLAS thread: "
               f"{args.ref_decode_steps} decode steps at n~2048 + 1 eviction per lane, extrapolated to the "
               f"128-token period")
     return {
@@ -451,7 +516,7 @@ def run_reference(args, rank: int, world: int):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(c["streams"] * c["period"] / value * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-rounded inputs)",
-        "data": "synthetic", "config": {"workload": WORKLOAD},
+        "data": "synthetic", "config": {"workload": CFG["desc"]},
         "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": info["procs"], "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -467,6 +532,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=128)
     ap.add_argument("--ref-decode-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS))
+    ap.add_argument("--budget", type=int, default=0, help="config 4 KV budget sweep (1024/2048/4096/8192)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -482,7 +549,7 @@ def main():
         res = run_reference(args, rank, world)
     else:
         res = run_gpu(args, rank, world)
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "cfg1":
             v, info = cpu_sample(d=args.ref_decode_steps, seed=7)
             res["cpu_baseline"] = {
                 "value": round(v, 3), "unit": "tokens/s", "cores": info["procs"], "kind": "port",
