@@ -150,6 +150,20 @@ int skv_timing_read(skv_ctx* ctx, uint64_t* out_host, int max_pairs);
  * launches in slots tcount % 64; skv_timing_cta copies one slot (max_ctas x 8). */
 int skv_timing_cta(skv_ctx* ctx, int slot, uint64_t* out_host);
 
+/* ---- chunked prefill (tcgen05) ------------------------------------------------
+ * Causal attention of a C-token chunk whose k/v rows are already stored at
+ * slots [n0, n0+C) of each (stream, layer, kv-head) segment: query i attends to
+ * slots [0, n0+i].  This is the reference's per-token prompt loop
+ * (Session.start_round, engine.py:350-353, each token through decode_step) as
+ * one tensor-core pass.  bf16, head_dim 128.
+ *   q_dev [S][C][Hq][128] bf16;  k_cache/v_cache [S][L][Hkv][cap][128] bf16
+ *   out_dev [S][C][Hq][128] f32
+ *   logits_dev (optional) [S][W][Hq][lg_cap] f32 scaled logits of the last W
+ *   query rows; stats_dev [S][W][Hq][2] their (max, sum). */
+int skv_prefill_attend(const void* q_dev, int streams, int C, int heads_q, int heads_kv, const void* k_cache,
+                       const void* v_cache, int layers, int layer, int capacity, int n0, float* out_dev, int W,
+                       float* logits_dev, int64_t lg_cap, float* stats_dev, void* stream);
+
 /* ---- stand-alone policy kernels (drop-in for the pure policy functions) ---- */
 /* top_k_indices(scores, k) (policies.py:165-181) on device: ascending indices of
  * the k largest, ties to the larger index.  out_dev receives min(k, n) int64. */

@@ -1012,4 +1012,33 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   return SKV_OK;
 }
 
+int skv_prefill_attend(const void* q, int streams, int C, int Hq, int Hkv, const void* k_cache, const void* v_cache,
+                       int L, int layer, int cap, int n0, float* out, int W, float* logits, int64_t lg_cap,
+                       float* stats, void* stream) {
+  if (!q || !k_cache || !v_cache || !out) return fail(SKV_EINVAL, "null argument");
+  if (streams < 1 || C < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv || L < 1 || layer < 0 || layer >= L)
+    return fail(SKV_EINVAL, "bad prefill geometry");
+  if (n0 < 0 || n0 + C > cap) return fail(SKV_EINVAL, "chunk exceeds the cache capacity");
+  if (W < 0 || W > C) return fail(SKV_EINVAL, "W must be in [0, C]");
+  PrefillArgs a{};
+  a.C = C;
+  a.n0 = n0;
+  a.W = W;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.G = Hq / Hkv;
+  a.L = L;
+  a.layer = layer;
+  a.cap = cap;
+  a.scale = (float)(1.0 / std::sqrt(128.0));
+  a.out = out;
+  a.lg = W > 0 ? logits : nullptr;
+  a.lg_cap = lg_cap;
+  a.st = W > 0 ? stats : nullptr;
+  const int64_t rows = (int64_t)streams * L * Hkv * cap;
+  cudaError_t e = launch_prefill(q, streams, k_cache, v_cache, rows, a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
+  return SKV_OK;
+}
+
 }  // extern "C"

@@ -146,4 +146,22 @@ struct CompactArgs {
 
 cudaError_t launch_compact(int blocks, const CompactArgs& a, cudaStream_t st);
 
+// ----------------------------------------------------------------------------
+// K4: chunked prefill attention (tcgen05), bf16, head_dim 128
+// ----------------------------------------------------------------------------
+struct PrefillArgs {
+  int C, n0;            // chunk length; cached tokens before the chunk (chunk k/v already appended)
+  int W;                // window rows recorded (the last W queries of the chunk)
+  int Hq, Hkv, G;       // heads; G = Hq / Hkv
+  int L, layer, cap;    // cache geometry: segment row = ((s*L + layer)*Hkv + g)*cap
+  float scale;
+  float* out;           // [S][C][Hq][128] f32
+  float* lg;            // optional [S][W][Hq][lg_cap] f32 logits of the recorded rows
+  int64_t lg_cap;
+  float* st;            // optional [S][W][Hq][2] (max, sum)
+};
+
+cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const void* vbase, int64_t kv_rows,
+                           const PrefillArgs& a, cudaStream_t st);
+
 }  // namespace skv

@@ -1,0 +1,80 @@
+"""GPU parity of the tcgen05 chunked-prefill kernel (K4) against a float32
+PyTorch reference of the reference's per-token prompt loop: query i of the
+chunk attends to the cached prefix and chunk tokens 0..i (engine.py:350-353)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _ref(q, kc, vc, n0, C, W):
+    """q [S][C][Hq][D] f32, kc/vc [S][Hkv][n0+C][D] f32 -> out, probs of last W rows."""
+    S, _, Hq, D = q.shape
+    Hkv = kc.shape[1]
+    G = Hq // Hkv
+    scale = np.float32(1.0 / np.sqrt(D))
+    out = torch.zeros((S, C, Hq, D), dtype=torch.float32, device="cuda")
+    logits_last = []
+    for s in range(S):
+        k = kc[s].repeat_interleave(G, dim=0)  # [Hq][N][D]
+        v = vc[s].repeat_interleave(G, dim=0)
+        lg = torch.einsum("chd,hnd->chn", q[s], k) * scale  # [C][Hq][N]
+        n = torch.arange(n0 + C, device="cuda")
+        mask = n[None, :] <= (n0 + torch.arange(C, device="cuda"))[:, None]  # [C][N]
+        lg = lg.masked_fill(~mask[:, None, :], float("-inf"))
+        p = torch.softmax(lg, dim=-1)
+        out[s] = torch.einsum("chn,hnd->chd", p, v)
+        logits_last.append(lg[C - W:])
+    return out, logits_last
+
+
+@pytest.mark.parametrize("S,C,Hq,Hkv,n0,W", [(1, 128, 2, 2, 0, 32), (2, 576, 4, 4, 1000, 32), (1, 32, 8, 2, 513, 32),
+                                             (2, 200, 4, 1, 300, 16)])
+def test_prefill_matches_torch(S, C, Hq, Hkv, n0, W):
+    from paper_2409_09086_b200 import _lib
+
+    lib = _lib.load()
+    D, L, layer = 128, 2, 1
+    cap = ((n0 + C + 31) // 32) * 32 + 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn((S, C, Hq, D), generator=g, device="cuda").to(torch.bfloat16)
+    kc = torch.randn((S, L, Hkv, cap, D), generator=g, device="cuda").to(torch.bfloat16)
+    vc = torch.randn((S, L, Hkv, cap, D), generator=g, device="cuda").to(torch.bfloat16)
+    kc[:, :, :, ::97] *= 4  # key spikes
+    out = torch.full((S, C, Hq, D), float("nan"), dtype=torch.float32, device="cuda")
+    lg_cap = n0 + C
+    logits = torch.zeros((S, W, Hq, lg_cap), dtype=torch.float32, device="cuda")
+    stats = torch.zeros((S, W, Hq, 2), dtype=torch.float32, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    rc = lib.skv_prefill_attend(P(q), S, C, Hq, Hkv, P(kc), P(vc), L, layer, cap, n0, P(out), W, P(logits), lg_cap,
+                                P(stats), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    _lib.check(rc)
+    torch.cuda.synchronize()
+    ref_out, ref_lg = _ref(q.float(), kc[:, layer, :, : n0 + C].float(), vc[:, layer, :, : n0 + C].float(), n0, C, W)
+    err = ((out - ref_out).abs().amax(-1) / ref_out.abs().amax(-1)).max().item()
+    print(f"prefill S={S} C={C} Hq={Hq} Hkv={Hkv} n0={n0}: output rel err {err:.2e}")
+    assert torch.isfinite(out).all()
+    assert err <= 2e-3
+    for s in range(S):
+        for w in range(W):
+            i = C - W + w
+            nv = n0 + i + 1
+            got = logits[s, w, :, :nv]
+            want = ref_lg[s][w, :, :nv]
+            lerr = ((got - want).abs().amax(-1) / want.abs().amax(-1)).max().item()
+            assert lerr <= 1e-5, (s, w, lerr)
+            M = stats[s, w, :, 0]
+            Lsum = stats[s, w, :, 1]
+            np.testing.assert_allclose(M.cpu().numpy(), want.amax(-1).cpu().numpy(), rtol=1e-6, atol=1e-6)
+            Lref = torch.exp(want - want.amax(-1, keepdim=True)).sum(-1)
+            np.testing.assert_allclose(Lsum.cpu().numpy(), Lref.cpu().numpy(), rtol=1e-4)
