@@ -160,6 +160,13 @@ int skv_timing_cta(skv_ctx* ctx, int slot, uint64_t* out_host);
  *   out_dev [S][C][Hq][128] f32
  *   logits_dev (optional) [S][W][Hq][lg_cap] f32 scaled logits of the last W
  *   query rows; stats_dev [S][W][Hq][2] their (max, sum). */
+/* Engine-level chunk: appends the chunk's k/v ([S][C][Hkv][128] bf16) and metadata
+ * (modality, e.g. 1 for image tokens) to `layer`, runs the chunk attention
+ * (q [S][C][Hq][128] bf16 -> out [S][C][Hq][128] f32) and pushes the head-mean
+ * rows of the last min(W, C) tokens into the window, exactly as C calls of
+ * skv_decode_layer would (Session.start_round's prompt loop). */
+int skv_prefill_chunk(skv_ctx* ctx, int layer, const void* q_dev, const void* k_dev, const void* v_dev, int C,
+                      int modality, float* out_dev, void* stream);
 int skv_prefill_attend(const void* q_dev, int streams, int C, int heads_q, int heads_kv, const void* k_cache,
                        const void* v_cache, int layers, int layer, int capacity, int n0, float* out_dev, int W,
                        float* logits_dev, int64_t lg_cap, float* stats_dev, void* stream);

@@ -19,6 +19,8 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "skv_common.cuh"
 #include "skv_internal.h"
 
@@ -419,6 +421,58 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
   }
   dim3 grid((a.C + pf::BM - 1) / pf::BM, a.Hq, streams);
   prefill_kernel<<<grid, 192, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
+  return cudaGetLastError();
+}
+
+}  // namespace skv
+
+namespace skv {
+
+// Appends a C-token chunk's k/v ([S][C][Hkv][D] rows) to cache slots
+// [n0, n0+C) of every (stream, kv-head) segment with token metadata
+// (KvCache.append, cache.py:112-134, for C tokens at once).  Grid (C, S);
+// thread t copies 16 bytes of one head's row.
+__global__ void append_chunk_kernel(const uint4* __restrict__ kin, const uint4* __restrict__ vin, uint4* kc, uint4* vc,
+                                    int64_t c_ss, int64_t c_hs, int Hkv, int units, int n0, int C, int64_t* pos,
+                                    int8_t* modality, int32_t* round_id, int64_t m_ss, const int64_t* next_pos,
+                                    int64_t np_ss, int mod, int rnd) {
+  const int i = blockIdx.x, s = blockIdx.y;
+  for (int idx = threadIdx.x; idx < Hkv * units; idx += blockDim.x) {
+    const int g = idx / units, u = idx - g * units;
+    const int64_t src = ((int64_t)(s * C + i) * Hkv + g) * units + u;
+    const int64_t d2 = s * c_ss + g * c_hs + (int64_t)(n0 + i) * units + u;
+    kc[d2] = kin[src];
+    vc[d2] = vin[src];
+  }
+  if (threadIdx.x == 0) {
+    pos[s * m_ss + n0 + i] = next_pos[s * np_ss] + i;
+    modality[s * m_ss + n0 + i] = (int8_t)mod;
+    round_id[s * m_ss + n0 + i] = rnd;
+  }
+}
+
+// After the chunk: lengths and the next original position of every stream.
+__global__ void chunk_meta_kernel(int32_t* len, int64_t* next_pos, int64_t ss, int n, int C, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S) {
+    len[s * ss] = n;
+    next_pos[s * ss] += C;
+  }
+}
+
+cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
+                                int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,
+                                int8_t* modality, int32_t* round_id, int64_t m_ss, int64_t* next_pos, int32_t* len,
+                                int64_t ss, int mod, int rnd, cudaStream_t st) {
+  dim3 grid(C, S);
+  const int threads = std::min(1024, ((Hkv * units + 31) / 32) * 32);
+  append_chunk_kernel<<<grid, threads, 0, st>>>(static_cast<const uint4*>(kin), static_cast<const uint4*>(vin),
+                                                static_cast<uint4*>(kc), static_cast<uint4*>(vc), c_ss_units,
+                                                c_hs_units, Hkv, units, n0, C, pos, modality, round_id, m_ss, next_pos,
+                                                ss, mod, rnd);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  chunk_meta_kernel<<<(S + 127) / 128, 128, 0, st>>>(len, next_pos, ss, n0 + C, C, S);
   return cudaGetLastError();
 }
 

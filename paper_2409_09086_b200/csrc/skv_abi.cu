@@ -106,6 +106,8 @@ struct skv_ctx {
   int32_t* first_moved = nullptr;
   float* scores = nullptr;
   int64_t* pos_in = nullptr;  // staging for explicit positions
+  float* plogits = nullptr;   // prefill: [S][W][Hq][cap] logits of the recorded rows
+  float* pstats = nullptr;    // prefill: [S][W][Hq][2]
   unsigned long long* tbuf = nullptr;  // timing ring [8192][2]
   unsigned long long* cbuf = nullptr;  // per-CTA timing [64][max_ctas][3]
   int tcount = 0;
@@ -440,6 +442,78 @@ static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
   x->launches++;
   x->last_layer = -1;
   x->pend_n[layer] = 0;
+  return SKV_OK;
+}
+
+int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const void* v, int C, int modality,
+                      float* out, void* stream) {
+  if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
+  if (layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
+  if (x->cfg.dtype != SKV_DTYPE_BF16 || x->D != 128) return fail(SKV_EINVAL, "chunked prefill needs bf16, head_dim 128");
+  if (C < 1) return fail(SKV_EINVAL, "chunk must be non-empty");
+  const int n0 = x->n[layer];
+  if (n0 + C > x->cap) return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
+  cudaStream_t st = as_stream(stream);
+  int rc = flush_pending(x, layer, st);  // keep the window rows in push order
+  if (rc) return rc;
+  if (!x->plogits) {
+    cudaError_t e = x->alloc(&x->plogits, (size_t)x->S * x->W * x->Hq * x->cap * sizeof(float));
+    if (e == cudaSuccess) e = x->alloc(&x->pstats, (size_t)x->S * x->W * x->Hq * 2 * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "prefill scratch");
+  }
+  const int units = x->D * x->elt / 16;
+  const int64_t SLs = x->L;
+  const int64_t kv_off = (int64_t)layer * x->kv_layer_stride() * x->elt;
+  cudaError_t e = launch_append_chunk(k, v, static_cast<char*>(x->k) + kv_off, static_cast<char*>(x->v) + kv_off,
+                                      x->kv_stream_stride() * x->elt / 16, (int64_t)x->cap * units, x->S, x->Hkv,
+                                      units, n0, C, x->pos + (int64_t)layer * x->cap,
+                                      x->modality + (int64_t)layer * x->cap, x->round_id + (int64_t)layer * x->cap,
+                                      SLs * x->cap, x->next_pos + layer, x->len + layer, SLs, modality,
+                                      x->round_value[layer], st);
+  if (e != cudaSuccess) return cuda_fail(e, "append kernel launch");
+  const int wrec = std::min(x->W, C);
+  PrefillArgs a{};
+  a.C = C;
+  a.n0 = n0;
+  a.W = wrec;
+  a.Hq = x->Hq;
+  a.Hkv = x->Hkv;
+  a.G = x->G;
+  a.L = x->L;
+  a.layer = layer;
+  a.cap = x->cap;
+  a.scale = x->scale;
+  a.out = out;
+  a.lg = x->plogits;
+  a.lg_cap = x->cap;
+  a.st = x->pstats;
+  e = launch_prefill(q, x->S, x->k, x->v, (int64_t)x->S * x->L * x->Hkv * x->cap, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
+  x->launches += 3;
+  // fold the recorded rows (oldest first) into the window ring
+  for (int w = 0; w < wrec; ++w) {
+    const int slot = (x->whead[layer] + w) % x->W;
+    FoldArgs f{};
+    f.logits = x->plogits + (int64_t)w * x->Hq * x->cap;
+    f.l_ss = (int64_t)wrec * x->Hq * x->cap;
+    f.l_hs = x->cap;
+    f.stats = x->pstats + (int64_t)w * x->Hq * 2;
+    f.st_ss = (int64_t)wrec * x->Hq * 2;
+    f.rows = x->rows + ((int64_t)layer * x->W + slot) * x->cap;
+    f.r_ss = SLs * x->W * x->cap;
+    f.wlen = x->wlen + (int64_t)layer * x->W + slot;
+    f.w_ss = SLs * x->W;
+    f.n = n0 + (C - wrec + w) + 1;
+    f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
+    f.agg_div = x->Hq_total;
+    e = launch_fold(x->S, std::max(1, std::min(64, (f.n + 255) / 256)), f, x->Hq, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
+    x->launches++;
+  }
+  x->whead[layer] = (x->whead[layer] + wrec) % x->W;
+  x->wcount[layer] = std::min(x->wcount[layer] + wrec, x->W);
+  x->n[layer] = n0 + C;
+  x->last_layer = -1;
   return SKV_OK;
 }
 

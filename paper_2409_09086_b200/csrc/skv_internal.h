@@ -163,5 +163,10 @@ struct PrefillArgs {
 
 cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const void* vbase, int64_t kv_rows,
                            const PrefillArgs& a, cudaStream_t st);
+// strides in 16-byte units; ss = stride of len / next_pos between streams
+cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
+                                int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,
+                                int8_t* modality, int32_t* round_id, int64_t m_ss, int64_t* next_pos, int32_t* len,
+                                int64_t ss, int mod, int rnd, cudaStream_t st);
 
 }  // namespace skv

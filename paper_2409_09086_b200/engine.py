@@ -150,6 +150,21 @@ class StreamEngine:
                                        _stream_handle()))
         return out
 
+    def prefill_chunk(self, layer: int, q, k, v, out=None, modality: int = 0):
+        """A C-token chunk of one layer on the tensor cores: q (S,C,Hq,D), k/v
+        (S,C,Hkv,D) bf16 -> out (S,C,Hq,D) f32; equivalent to C decode_layer calls
+        (the last min(W, C) rows enter the window)."""
+        c = self.cfg
+        S, C = q.shape[0], q.shape[1]
+        if out is None:
+            out = torch.empty((S, C, c.heads_q, c.head_dim), dtype=torch.float32, device=q.device)
+        for name, t, heads in (("q", q, c.heads_q), ("k", k, c.heads_kv), ("v", v, c.heads_kv)):
+            if tuple(t.shape) != (c.streams, C, heads, c.head_dim) or t.dtype != c.dtype or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous {c.dtype} tensor of shape {(c.streams, C, heads, c.head_dim)}")
+        check(self.lib.skv_prefill_chunk(self._h, layer, _ptr(q), _ptr(k), _ptr(v), C, int(modality), _ptr(out),
+                                         _stream_handle()))
+        return out
+
     def decode_step_host(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
                          record: bool = True):
         """Same as decode_step with host (ideally pinned) tensors; synchronous."""

@@ -78,3 +78,61 @@ def test_prefill_matches_torch(S, C, Hq, Hkv, n0, W):
             np.testing.assert_allclose(M.cpu().numpy(), want.amax(-1).cpu().numpy(), rtol=1e-6, atol=1e-6)
             Lref = torch.exp(want - want.amax(-1, keepdim=True)).sum(-1)
             np.testing.assert_allclose(Lsum.cpu().numpy(), Lref.cpu().numpy(), rtol=1e-4)
+
+
+def test_engine_prefill_chunks_match_oracle():
+    """Config-2 shape (reduced): 576-token image chunks (k/v = frame mean +
+    0.5 N(0,1)) and 32-token text chunks through StreamEngine.prefill_chunk,
+    eviction after every chunk, against the CPU oracle stepping the chunk token
+    by token (the reference's prompt loop)."""
+    from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    S, L, H, D = 2, 1, 32, 128
+    l, r, W = 256, 256, 32
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, 0.01, W, B + 576 + 64, torch.bfloat16))
+    orc = StreamOracle(S, L, H, H, D, cfg, window=W)
+    rng = np.random.default_rng(31)
+    F32 = np.float32
+    worst = 0.0
+    kept_buf = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    for frame in range(2):
+        for C, mod in ((576, 1), (32, 0)):
+            q = rng.standard_normal((S, C, H, D)).astype(F32)
+            if mod:
+                mu_k = rng.standard_normal((S, 1, H, D)).astype(F32)
+                mu_v = rng.standard_normal((S, 1, H, D)).astype(F32)
+                k = mu_k + F32(0.5) * rng.standard_normal((S, C, H, D)).astype(F32)
+                v = mu_v + F32(0.5) * rng.standard_normal((S, C, H, D)).astype(F32)
+            else:
+                k = rng.standard_normal((S, C, H, D)).astype(F32)
+                v = rng.standard_normal((S, C, H, D)).astype(F32)
+            q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
+            dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)
+            got = eng.prefill_chunk(0, dev(q), dev(k), dev(v), modality=mod).cpu().numpy()
+            for i in range(C):
+                want, _ = orc.step_layer(0, q[:, i][None][0], k[:, i], v[:, i])
+                orc.advance()
+                g = got[:, i].astype(np.float64)
+                worst = max(worst, float((np.abs(g - want).max(-1) / np.abs(want).max(-1)).max()))
+            n = orc.length(0, 0)
+            rows_g = eng.window_rows(0, 0)
+            rows_c = orc.win[0][0].rows
+            assert [a.size for a in rows_g] == [b.size for b in rows_c]
+            for a_, b_ in zip(rows_g, rows_c):
+                assert float(np.abs(a_ - b_).max() / np.abs(b_).max()) <= 1e-5
+            eng.evict(-1, kept_buf)
+            kc = kept_buf.cpu().numpy()
+            for s in range(S):
+                if n > B:
+                    ok, nbad, gap = kept_sets_match(orc.scores(s, 0), orc.decide(s, 0).kept, kc[s, 0], n, cfg)
+                    assert ok, (frame, C, s, nbad, gap)
+                    orc.apply(s, 0, kc[s, 0].astype(np.int64))
+                else:
+                    np.testing.assert_array_equal(kc[s, 0, :n], np.arange(n))
+            for s in range(S):
+                np.testing.assert_array_equal(eng.positions(s, 0), orc.kv[s][0].pos[: orc.kv[s][0].n])
+    print(f"engine prefill worst output rel err {worst:.2e}")
+    assert worst <= 2e-3
