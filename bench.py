@@ -48,6 +48,11 @@ WORKLOADS = {
                  bias=0.01, period=256, spike_prob=0.005, spike_gain=4.0, shard="heads", scaling="strong",
                  desc="cfg3: Llama-3-8B GQA-shaped decode, 32L x 32q/8kv x 128, bf16, batch 1, budget 2048+2048, "
                       "W=32, b=0.01, E=256, KV heads sharded over GPUs"),
+    "cfg2": dict(layers=32, heads_q=32, heads_kv=32, head_dim=128, streams=4, recent=2048, relevant=2048, window=32,
+                 bias=0.01, period=608, image=576, text=32, shard="streams", scaling="weak",
+                 desc="cfg2: Vicuna-7B-shaped video stream, 32L x 32H x 128, bf16, 4 streams/GPU, budget 2048+2048, "
+                      "frames of 576 image tokens (one tcgen05 prefill chunk) + 32 text tokens, eviction after "
+                      "each chunk"),
     "cfg4": dict(layers=32, heads_q=32, heads_kv=32, head_dim=128, streams=256, recent=1024, relevant=1024, window=32,
                  bias=0.01, period=128, spike_prob=0.01, spike_gain=4.0, shard="streams", scaling="strong",
                  desc="cfg4: 256 Llama-2-7B-shaped streams partitioned over GPUs, bf16, W=32, b=0.01, E=128"),
@@ -394,6 +399,118 @@ def run_gpu(args, rank: int, world: int):
     return res
 
 
+def run_cfg2(args, rank: int, world: int):
+    """Config 2: each step is one video frame per stream -- a 576-token image
+    chunk (chunked prefill on the tensor cores) then a 32-token text chunk, all
+    32 layers, with an all-layer eviction after each chunk."""
+    import torch
+
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    c = dict(WORKLOADS["cfg2"])
+    L, H, D, S = c["layers"], c["heads_q"], c["head_dim"], c["streams"]
+    l, r, W, CI, CT = c["recent"], c["relevant"], c["window"], c["image"], c["text"]
+    B = l + r
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, c["bias"], W, B + CI + 64, torch.bfloat16))
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    for s in range(S):
+        for layer in range(L):
+            kf, vf = eng.kv_full(s, layer)
+            kf[:, :B] = torch.randn((H, B, D), generator=g, device=dev).to(torch.bfloat16)
+            vf[:, :B] = torch.randn((H, B, D), generator=g, device=dev).to(torch.bfloat16)
+            eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
+
+    def chunk_inputs(C, image):
+        q = torch.randn((L, S, C, H, D), generator=g, device=dev)
+        if image:  # k, v = per-(stream, layer, frame, head, dim) mean + 0.5 N(0, 1)
+            k = torch.randn((L, S, 1, H, D), generator=g, device=dev) + 0.5 * torch.randn((L, S, C, H, D), generator=g, device=dev)
+            v = torch.randn((L, S, 1, H, D), generator=g, device=dev) + 0.5 * torch.randn((L, S, C, H, D), generator=g, device=dev)
+        else:
+            k = torch.randn((L, S, C, H, D), generator=g, device=dev)
+            v = torch.randn((L, S, C, H, D), generator=g, device=dev)
+        return [t.to(torch.bfloat16).contiguous() for t in (q, k, v)]
+
+    qi, ki, vi = chunk_inputs(CI, True)
+    qt, kt, vt = chunk_inputs(CT, False)
+    oi = torch.empty((S, CI, H, D), dtype=torch.float32, device=dev)
+    ot = torch.empty((S, CT, H, D), dtype=torch.float32, device=dev)
+
+    def image_chunk():
+        for layer in range(L):
+            eng.prefill_chunk(layer, qi[layer], ki[layer], vi[layer], oi, modality=1)
+
+    def frame():
+        image_chunk()
+        eng.evict(-1)
+        for layer in range(L):
+            eng.prefill_chunk(layer, qt[layer], kt[layer], vt[layer], ot, modality=0)
+        eng.evict(-1)
+
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        frame()
+        launches0 = eng.kernel_launches
+        eng.capture_begin()
+        frame()
+        eng.capture_end()
+        launches_per_frame = eng.kernel_launches - launches0
+        for _ in range(args.warmup):
+            eng.replay()
+    stream.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        for _ in range(args.steps):
+            eng.replay()
+        t1.record(stream)
+    stream.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    # the image chunk alone (32 prefill launches + appends + row folds), CUDA events on its stream
+    with torch.cuda.stream(stream):
+        eng.evict(-1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        image_chunk()
+        e1.record(stream)
+        eng.evict(-1)
+    stream.synchronize()
+    img_ms = e0.elapsed_time(e1)
+    n0 = B  # every chunk starts from the evicted budget
+    flops = 4 * D * (CI * n0 + CI * (CI + 1) / 2) * S * L * H  # useful QK^T + PV flops of the image chunk
+    tflops = flops / (img_ms * 1e-3) / 1e12
+    peak_tf = 1394.7
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak_tf = float(json.load(f)["bf16_tflops_sustained"])
+    except Exception:
+        pass
+    tokens = S * (CI + CT)
+    return {
+        "metric": METRIC, "value": round(tokens / (ms * 1e-3), 2), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (frame-mean image k/v, N(0,1) text)",
+        "config": {"workload": c["desc"], "streams_per_gpu": S, "budget": B, "window": W,
+                   "step": "one frame: 576-token image chunk + 32-token text chunk, 32 layers, 2 evictions",
+                   "graph": "one CUDA graph per frame"},
+        "roofline": {"bound": "tensor", "kernel": "prefill_kernel (image chunk, incl. append + row fold)",
+                     "achieved": round(tflops, 1), "peak": peak_tf, "peak_kind": "measured sustained bf16",
+                     "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4), "traffic": None,
+                     "image_chunk_ms": round(img_ms, 3), "useful_tflop_per_image_chunk": round(flops / 1e12, 3),
+                     "note": "useful causal flops; the kernel issues full 128x128 tiles and a second bf16 P term"},
+        "gpu_launches": int(launches_per_frame * args.steps),
+        "clocks": clk,
+    }
+
+
+# --------------------------------------------------------------- CPU arm --
+
 def _cpu_proc(conn, lanes, d, seed, c):
     """Worker process: holds `lanes` (stream, layer) states of the oracle
     (reference algorithm, NumPy f32, one BLAS thread); each request runs d decode
@@ -547,6 +664,8 @@ def main():
         dist.init_process_group(backend=backend)
     if args.impl == "reference":
         res = run_reference(args, rank, world)
+    elif args.workload == "cfg2":
+        res = run_cfg2(args, rank, world)
     else:
         res = run_gpu(args, rank, world)
         if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "cfg1":

@@ -20,9 +20,11 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "skv_common.cuh"
 #include "skv_internal.h"
+#include "skv_fold.cuh"
 
 namespace skv {
 namespace pf {
@@ -38,7 +40,7 @@ constexpr int SV = SK + 2 * TILE_BYTES;             // 2 stages
 constexpr int SP = SV + 2 * TILE_BYTES;             // P, bf16 high part
 constexpr int SP_LO = SP + TILE_BYTES;              // P - bf16(P), bf16 low part
 constexpr int SBAR = SP_LO + TILE_BYTES;            // barriers after the tiles
-constexpr int SMEM_BYTES = SBAR + 256 + 1024;       // + alignment slack
+constexpr int SMEM_BYTES = SBAR + 128 + 3 * 512 + 1008;  // barriers, row-max exchange, alignment slack
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -147,7 +149,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }  // namespace pf
 
 // One CTA: 128 queries [q0, q0+128) of stream s, query head h (kv head h/G).
-__global__ void __launch_bounds__(192, 1)
+__global__ void __maxnreg__(168)  // 10 warps: <= 3 per SM sub-partition x 168 regs fit its 16K registers
     prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const PrefillArgs a) {
   using namespace pf;
@@ -177,11 +179,11 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
     }
-    mbar_init(p_ready, 4);
+    mbar_init(p_ready, 8);
     mbar_init(o_full, 1);
     mbar_fence_init();
   }
-  if (warp == 5) {  // TMEM: S0 [0,128), S1 [128,256), O [256,384)
+  if (warp == 9) {  // TMEM: S0 [0,128), S1 [128,256), O [256,384)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------------------- producer
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, TILE_BYTES);
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d(smem + SV + st * TILE_BYTES + REGION, &vmap, 64, y, &kv_full[st]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t id_s = idesc(false), id_o = idesc(true, kPHalf);
@@ -243,41 +245,59 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ------------------------------------------------- softmax (row = tid)
-    const int r = tid;                     // TMEM lane == query row
+    // -------------------------- softmax: 8 warps, two threads per query row
+    // thread t owns row t & 127 (its TMEM lane) and key/output columns
+    // [64*hf, 64*hf + 64), hf = t >> 7; the pair exchanges its row maximum
+    // through shared memory once per tile and its row sum once at the end.
+    const int r = tid & 127, hf = tid >> 7;
     const int qi = q0 + r;                 // query index in the chunk
     const bool valid = qi < C;
     const int limit = valid ? n0 + qi + 1 : 1;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + hf * 64;
     const int wrow = qi - (C - a.W);      // window row index (>= 0: recorded)
     const bool rec = valid && a.lg && wrow >= 0;
     float* lgrow = rec ? a.lg + ((int64_t)(s * a.W + wrow) * a.Hq + h) * a.lg_cap : nullptr;
     const bool lg_aligned = (reinterpret_cast<uintptr_t>(lgrow) & 15) == 0;
+    unsigned* xch = reinterpret_cast<unsigned*>(bars + 16);  // [3][128] row maxima (orderable keys)
     float m = -INFINITY, l = 0.f;
-    unsigned char* prow_base = smem + SP + r * 128;
+    unsigned char* prow_base = smem + SP + hf * REGION + r * 128;
     for (int j = 0; j < ntiles; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      float sv[BN];
+      float sv[64];
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
+      for (int c2 = 0; c2 < 2; ++c2) {
         float t32[32];
-        tmem_ld32(lane_base + st * 128 + c4 * 32, t32);
+        tmem_ld32(lane_base + st * 128 + c2 * 32, t32);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c4 * 32 + i] = t32[i];
+        for (int i = 0; i < 32; ++i) sv[c2 * 32 + i] = t32[i];
       }
-      float tmax = -INFINITY;
+      const int tbase = j * BN + hf * 64;
+      float pm = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        const int t = j * BN + i;
-        sv[i] = t < limit ? sv[i] * a.scale : -INFINITY;
-        tmax = fmaxf(tmax, sv[i]);
+      for (int i = 0; i < 64; ++i) {
+        sv[i] = tbase + i < limit ? sv[i] * a.scale : -INFINITY;
+        pm = fmaxf(pm, sv[i]);
       }
+      // pair maximum through a 3-buffer ring of atomicMax keys: buffer (j+2)%3 is
+      // reset here and first used again after the next barrier
+      if (j == 0) {
+        if (hf == 0) {
+          xch[r] = 0u;
+          xch[128 + r] = 0u;
+        }
+        asm volatile("bar.sync 3, 256;\n" ::: "memory");
+      }
+      atomicMax(&xch[(j % 3) * 128 + r], orderable(pm));
+      if (hf == 0) xch[((j + 2) % 3) * 128 + r] = 0u;
+      asm volatile("bar.sync 3, 256;\n" ::: "memory");
+      const unsigned key = xch[(j % 3) * 128 + r];
+      const float tmax = __uint_as_float((key & 0x80000000u) ? (key & 0x7fffffffu) : ~key);
       if (lgrow) {
 #pragma unroll
-        for (int i = 0; i < BN; i += 4) {
-          const int t = j * BN + i;
+        for (int i = 0; i < 64; i += 4) {
+          const int t = tbase + i;
           if (t + 3 < limit && lg_aligned) {
             *reinterpret_cast<float4*>(lgrow + t) = make_float4(sv[i], sv[i + 1], sv[i + 2], sv[i + 3]);
           } else {
@@ -289,40 +309,37 @@ __global__ void __launch_bounds__(192, 1)
       }
       const float mn = fmaxf(m, tmax);
       const float alpha = m == -INFINITY ? 0.f : exp2f((m - mn) * kLog2e);
-      float psum = 0.f;
       // P.V of the previous tile must be done before P is overwritten (and O rescaled)
       if (j > 0) {
         mbar_wait(o_full, (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, mn > m)) {  // rescale O rows in TMEM (warp-uniform tcgen05 ops)
+        if (__any_sync(0xffffffffu, mn > m)) {  // rescale this thread's O columns (warp-uniform tcgen05)
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
+          for (int c2 = 0; c2 < 2; ++c2) {
             float o32[32];
-            tmem_ld32(lane_base + 256 + c4 * 32, o32);
+            tmem_ld32(lane_base + 256 + c2 * 32, o32);
 #pragma unroll
             for (int i = 0; i < 32; ++i) o32[i] *= alpha;
-            tmem_st32(lane_base + 256 + c4 * 32, o32);
+            tmem_st32(lane_base + 256 + c2 * 32, o32);
           }
           tc_wait_st();
         }
       }
+      float psum = 0.f;
 #pragma unroll
-      for (int kc = 0; kc < BN / 8; ++kc) {
-        float p8[8];
+      for (int kc = 0; kc < 8; ++kc) {
+        float p8[8], lo8[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           p8[e] = exp2f((sv[kc * 8 + e] - mn) * kLog2e);
           psum += p8[e];
+          lo8[e] = p8[e] - __bfloat162float(__float2bfloat16_rn(p8[e]));
         }
-        float lo8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) lo8[e] = p8[e] - __bfloat162float(__float2bfloat16_rn(p8[e]));
         const uint4 hi = make_uint4(pack_p(p8[0], p8[1]), pack_p(p8[2], p8[3]), pack_p(p8[4], p8[5]),
                                     pack_p(p8[6], p8[7]));
         const uint4 lo = make_uint4(pack_p(lo8[0], lo8[1]), pack_p(lo8[2], lo8[3]), pack_p(lo8[4], lo8[5]),
                                     pack_p(lo8[6], lo8[7]));
-        const int region = kc >> 3, chunk = kc & 7;
-        const int off = region * REGION + ((chunk ^ (r & 7)) << 4);
+        const int off = (kc ^ (r & 7)) << 4;
         *reinterpret_cast<uint4*>(prow_base + off) = hi;
         *reinterpret_cast<uint4*>(prow_base + (SP_LO - SP) + off) = lo;
       }
@@ -333,30 +350,35 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
     }
-    // epilogue: O / l
+    // epilogue: O / (l_self + l_partner) (two-term sum: the same in either order)
+    float* lx = reinterpret_cast<float*>(xch);
+    asm volatile("bar.sync 3, 256;\n" ::: "memory");  // everyone is done with the max ring
+    lx[hf * 128 + r] = l;
+    asm volatile("bar.sync 3, 256;\n" ::: "memory");
+    const float lt = l + lx[(hf ^ 1) * 128 + r];
     mbar_wait(o_full, (ntiles - 1) & 1);
     tc_fence_after();
-    float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD;
-    const float inv = 1.f / l;
+    float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD + hf * 64;
+    const float inv = 1.f / lt;
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
+    for (int c2 = 0; c2 < 2; ++c2) {
       float o32[32];
-      tmem_ld32(lane_base + 256 + c4 * 32, o32);  // warp-uniform (.sync.aligned)
+      tmem_ld32(lane_base + 256 + c2 * 32, o32);  // warp-uniform (.sync.aligned)
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(orow + c4 * 32 + i) =
+          *reinterpret_cast<float4*>(orow + c2 * 32 + i) =
               make_float4(o32[i] * inv, o32[i + 1] * inv, o32[i + 2] * inv, o32[i + 3] * inv);
       }
     }
-    if (rec && a.st) {
+    if (rec && a.st && hf == 0) {
       a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2] = m;
-      a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = l;
+      a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = lt;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
@@ -420,8 +442,18 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
     attr = true;
   }
   dim3 grid((a.C + pf::BM - 1) / pf::BM, a.Hq, streams);
-  prefill_kernel<<<grid, 192, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
-  return cudaGetLastError();
+  prefill_kernel<<<grid, 320, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, prefill_kernel);
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    fprintf(stderr, "prefill launch failed: regs %d, static smem %zu, dyn smem %d (opt-in max %d), max threads %d\n",
+            fa.numRegs, fa.sharedSizeBytes, pf::SMEM_BYTES, optin, fa.maxThreadsPerBlock);
+  }
+  return e;
 }
 
 }  // namespace skv
@@ -449,6 +481,31 @@ __global__ void append_chunk_kernel(const uint4* __restrict__ kin, const uint4* 
     modality[s * m_ss + n0 + i] = (int8_t)mod;
     round_id[s * m_ss + n0 + i] = rnd;
   }
+}
+
+// Folds the W recorded rows of a chunk into the window ring in one launch:
+// grid (pieces, S, W); row w has n_base + w + 1 columns and goes to ring slot
+// (slot0 + w) mod Wring.
+__global__ void fold_rows_kernel(const FoldArgs f, int Hq, int slot0, int Wring, int n_base, int64_t lg_rs,
+                                 int64_t st_rs, int64_t slot_stride) {
+  const int w = blockIdx.z, s = blockIdx.y;
+  const int slot = (slot0 + w) % Wring;
+  FoldArgs g = f;
+  g.logits = f.logits + w * lg_rs;
+  g.stats = f.stats + w * st_rs;
+  g.rows = f.rows + slot * slot_stride;
+  g.wlen = f.wlen ? f.wlen + slot : nullptr;
+  g.n = n_base + w + 1;
+  fold_piece(g, s, blockIdx.x, gridDim.x, Hq, threadIdx.x, blockDim.x);
+}
+
+cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
+                             int64_t lg_rs, int64_t st_rs, int64_t slot_stride, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int pieces = std::max(1, std::min(32, (n_base + rows + 255) / 256));
+  dim3 grid(pieces, streams, rows);
+  fold_rows_kernel<<<grid, 256, 0, st>>>(f, Hq, slot0, Wring, n_base, lg_rs, st_rs, slot_stride);
+  return cudaGetLastError();
 }
 
 // After the chunk: lengths and the next original position of every stream.

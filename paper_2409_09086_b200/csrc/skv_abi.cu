@@ -490,23 +490,22 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   e = launch_prefill(q, x->S, x->k, x->v, (int64_t)x->S * x->L * x->Hkv * x->cap, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
   x->launches += 3;
-  // fold the recorded rows (oldest first) into the window ring
-  for (int w = 0; w < wrec; ++w) {
-    const int slot = (x->whead[layer] + w) % x->W;
+  // fold the recorded rows (oldest first) into the window ring, one launch
+  {
     FoldArgs f{};
-    f.logits = x->plogits + (int64_t)w * x->Hq * x->cap;
+    f.logits = x->plogits;
     f.l_ss = (int64_t)wrec * x->Hq * x->cap;
     f.l_hs = x->cap;
-    f.stats = x->pstats + (int64_t)w * x->Hq * 2;
+    f.stats = x->pstats;
     f.st_ss = (int64_t)wrec * x->Hq * 2;
-    f.rows = x->rows + ((int64_t)layer * x->W + slot) * x->cap;
+    f.rows = x->rows + (int64_t)layer * x->W * x->cap;
     f.r_ss = SLs * x->W * x->cap;
-    f.wlen = x->wlen + (int64_t)layer * x->W + slot;
+    f.wlen = x->wlen + (int64_t)layer * x->W;
     f.w_ss = SLs * x->W;
-    f.n = n0 + (C - wrec + w) + 1;
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
     f.agg_div = x->Hq_total;
-    e = launch_fold(x->S, std::max(1, std::min(64, (f.n + 255) / 256)), f, x->Hq, st);
+    e = launch_fold_rows(x->S, wrec, f, x->Hq, x->whead[layer], x->W, n0 + C - wrec, (int64_t)x->Hq * x->cap,
+                         (int64_t)x->Hq * 2, x->cap, st);
     if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
     x->launches++;
   }

@@ -163,6 +163,8 @@ struct PrefillArgs {
 
 cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const void* vbase, int64_t kv_rows,
                            const PrefillArgs& a, cudaStream_t st);
+cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
+                             int64_t lg_rs, int64_t st_rs, int64_t slot_stride, cudaStream_t st);
 // strides in 16-byte units; ss = stride of len / next_pos between streams
 cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
                                 int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,

@@ -1,0 +1,30 @@
+"""Run the tcgen05 prefill kernel at the config-2 shape (for ncu / timing)."""
+import ctypes, os, sys
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2409_09086_b200 import _lib
+
+lib = _lib.load()
+S, C, H, D, L, n0 = 4, 576, 32, 128, 1, 4096
+cap = n0 + C + 64
+g = torch.Generator(device="cuda").manual_seed(1)
+q = torch.randn((S, C, H, D), generator=g, device="cuda").to(torch.bfloat16)
+kc = torch.randn((S, L, H, cap, D), generator=g, device="cuda").to(torch.bfloat16)
+vc = torch.randn((S, L, H, cap, D), generator=g, device="cuda").to(torch.bfloat16)
+out = torch.empty((S, C, H, D), dtype=torch.float32, device="cuda")
+P = lambda t: ctypes.c_void_p(t.data_ptr())
+st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+reps = int(os.environ.get("REPS", 5))
+for i in range(2):
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
+torch.cuda.synchronize()
+a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+a.record()
+for i in range(reps):
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
+b.record()
+torch.cuda.synchronize()
+ms = a.elapsed_time(b) / reps
+flops = 4 * D * (C * n0 + C * (C + 1) / 2) * S * H
+print(f"prefill layer: {ms * 1e3:.1f} us, {flops / (ms * 1e-3) / 1e12:.1f} TFLOP/s useful")
