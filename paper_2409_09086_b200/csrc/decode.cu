@@ -44,7 +44,6 @@ struct Geo {
   static constexpr int RPWARP = TT / NW;  // rows per warp per tile
   static constexpr int ITERS = RPWARP / RPW;
   static constexpr int TILE = TT * RB;    // bytes per K (or V) tile
-  static constexpr int STAGES = 3;
   static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "row geometry");
   static_assert(ITERS >= 1, "tile geometry");
 };
@@ -92,9 +91,12 @@ template <typename T, int D, int G>
 struct Smem {
   using Gm = Geo<T, D>;
   static constexpr int NW = Gm::NW;
-  static constexpr size_t tiles = (size_t)Gm::STAGES * 2 * Gm::TILE;
-  static constexpr size_t bars = (2 * Gm::STAGES + 4) * sizeof(uint64_t);
-  static constexpr size_t tinfo = (2 * Gm::STAGES + 4) * sizeof(int);
+  // ring depth: 4 stages (128 KB for bf16 D=128) where one CTA per SM is
+  // resident anyway, so a static 4-tile chunk is prefetched whole under PDL
+  static constexpr int STAGES = G >= 4 ? 4 : 3;
+  static constexpr size_t tiles = (size_t)STAGES * 2 * Gm::TILE;
+  static constexpr size_t bars = (2 * STAGES + 4) * sizeof(uint64_t);
+  static constexpr size_t tinfo = (2 * STAGES + 4) * sizeof(int);
   // epilogue slot: header (4 ints) + wm[NW][G] + wl[NW][G] + wo[NW][G][D]
   static constexpr size_t slot_floats = 4 + 2 * NW * G + NW * G * D;
   static constexpr size_t slots = 2 * slot_floats * sizeof(float);
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   using Gm = Geo<T, D>;
   using Sm = Smem<T, D, G>;
   constexpr int TT = Gm::TT, RB = Gm::RB, LPR = Gm::LPR, EPL = Gm::EPL, RPW = Gm::RPW;
-  constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Gm::STAGES, TILE = Gm::TILE;
+  constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Sm::STAGES, TILE = Gm::TILE;
   constexpr int PW = D + 2;  // floats per head in a partial
   constexpr int SLOT = (int)Sm::slot_floats;
 
@@ -168,15 +170,16 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
         waited = true;
       }
       int i = 0, taken = 0, kp = 0;
-      // three tickets in flight: the atomic's latency is hidden even for 1-tile chunks
-      int u = atomicAdd(&a.sched[0], 1);
-      int t1 = atomicAdd(&a.sched[0], 1);
-      int t2 = atomicAdd(&a.sched[0], 1);
+      // dynamic: three tickets in flight, so the atomic's latency is hidden
+      // even for 1-tile chunks; static (few chunks): chunk blockIdx.x only
+      int u = a.stat ? c : atomicAdd(&a.sched[0], 1);
+      int t1 = a.stat ? total : atomicAdd(&a.sched[0], 1);
+      int t2 = a.stat ? total : atomicAdd(&a.sched[0], 1);
       while (u < total) {
         ++taken;
         const int u_next = t1;
         t1 = t2;
-        t2 = atomicAdd(&a.sched[0], 1);
+        t2 = a.stat ? total : atomicAdd(&a.sched[0], 1);
         // published with this chunk's first tile: lets the consumers prefetch q
         cring[(kp + 1) & 3] = u_next < total ? u_next : -1;
         ++kp;

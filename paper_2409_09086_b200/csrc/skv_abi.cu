@@ -31,6 +31,8 @@ static int chunk_tiles(int G) {
   }
   return env ? env : (G >= 2 ? 2 : 2);
 }
+static bool chunk_tiles_forced() { return getenv("SKV_CHUNK_TILES") != nullptr; }
+constexpr int kStaticMaxTiles = 8;  // largest static chunk (tiles of 64 tokens)
 static int q_prefetch() {
   static int env = -1;
   if (env < 0) {
@@ -326,8 +328,17 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
   const int n = n_old + 1;
   const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
-  const int nc = (nt + chunk_tiles(x->G) - 1) / chunk_tiles(x->G);
-  const int ctas = std::min(x->S * x->Hkv * nc, x->max_ctas);
+  // Few segments (batch-1 GQA, small configs): a static schedule with chunks
+  // just large enough that every chunk gets its own CTA; its tiles are
+  // prefetched under PDL and no CTA idles while another streams a backlog.
+  // Otherwise 2-tile chunks handed out dynamically.
+  const int segs = x->S * x->Hkv;
+  int ch = chunk_tiles(x->G);
+  while (ch < kStaticMaxTiles && (int64_t)segs * ((nt + ch - 1) / ch) > x->max_ctas) ++ch;
+  const bool stat = (int64_t)segs * ((nt + ch - 1) / ch) <= x->max_ctas && !chunk_tiles_forced();
+  if (!stat) ch = chunk_tiles(x->G);
+  const int nc = (nt + ch - 1) / ch;
+  const int ctas = std::min(segs * nc, x->max_ctas);
   if ((size_t)nc * x->G * (x->D + 2) * 4 > 190 * 1024) return fail(SKV_EINVAL, "capacity too large for the merge scratch");
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
@@ -337,10 +348,11 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.n_old = n_old;
   a.append = 1;
   a.nt = nt;
-  a.ch = chunk_tiles(x->G);
+  a.ch = ch;
   a.qpf = q_prefetch();
   a.nc = nc;
   a.S = x->S;
+  a.stat = stat;
   const int seq = x->launch_seq++;
   a.sched = x->sched + 4 * (seq % 64);
   a.prefetch = x->last_layer >= 0 && x->last_layer != layer;

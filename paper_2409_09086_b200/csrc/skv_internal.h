@@ -38,6 +38,7 @@ struct AttnArgs {
   int nt;               // tiles per segment = ceil(n / 32)
   int ch, nc;           // tiles per chunk, chunks per segment
   int S;                // streams
+  int stat;             // 1: static schedule, CTA c runs chunk c (grid = S*Hkv*nc)
   int32_t* sched;       // [4] ticket, grid-barrier and exit counters (zero between launches)
   int32_t* done_self;   // set to 1 by the merge kernel when this launch's outputs are complete
   const int32_t* done_prev;  // flag of the preceding merge (null: use griddepcontrol.wait)

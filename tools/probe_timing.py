@@ -7,7 +7,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2409_09086_b200 import EngineConfig, StreamEngine
 
-S, L, H, D, B, E, W = 8, 32, 32, 128, 2048, 128, 32
+S, L, H, D, W = int(os.environ.get("S", 8)), 32, 32, 128, 32
+B, E = int(os.environ.get("B", 2048)), int(os.environ.get("E", 128))
 Hkv = int(os.environ.get("HKV", 32))
 l = r = B // 2
 dev = torch.device("cuda")
