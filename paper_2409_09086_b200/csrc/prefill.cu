@@ -8,14 +8,22 @@
 // (AttentionWindow.push, policies.py:107-115) -- their f32 logits and per-row
 // (max, sum) are recorded here and folded into head-mean rows afterwards.
 //
-// One CTA = 128 queries x one head.  Warp 4 (TMA producer) loads the Q tile
-// once and 128-key K/V tiles into a 2-stage ring with cp.async.bulk.tensor
-// (128-byte swizzle); warp 5 owns TMEM and issues tcgen05.mma
-// (M=128, N=128, K=16, bf16 -> f32): S = Q K^T into one of two TMEM S buffers,
-// O += P V into a TMEM O accumulator.  Warps 0-3 (one query row per thread)
-// read S with tcgen05.ld, run the online softmax, write P (bf16, swizzled
-// K-major) to shared memory for the P.V MMA, and rescale O in TMEM when a
-// row maximum grows.
+// One CTA = two 128-query tiles of one head ("ping-pong"): while the softmax
+// warpgroup of one tile turns its S tile into P, the tensor core runs the
+// other tile's MMAs.  Warp 8 (TMA producer) loads both Q tiles once and
+// 64-key K and V tiles into 4-stage rings (cp.async.bulk.tensor, 128-byte
+// swizzle).  Warp 9 owns TMEM and issues tcgen05.mma (bf16 -> f32):
+// S_i = Q_i K^T (M=128, N=64) into a double-buffered 64-column TMEM S tile,
+// O_i += P_i V (M=128, N=128) with P read straight from TMEM (the .kind::f16
+// A-from-TMEM form), O_i in its own 128 TMEM columns.  Warps 0-3 / 4-7 (one
+// query row per thread) read S with tcgen05.ld, run the online softmax and
+// write P back over the S columns it came from as two bf16 terms
+// (hi = bf16(p), lo = bf16(p - hi)).  O is rescaled lazily: only when a row
+// maximum grows by more than 2^8 (exact -- O and the row sum share the stale
+// maximum), so the TMEM round trip is rare after the first tiles.
+//
+// TMEM columns: S/P of tile 0 [0,128) (two 64-column buffers), S/P of tile 1
+// [128,256), O of tile 0 [256,384), O of tile 1 [384,512).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -29,18 +37,21 @@
 namespace skv {
 namespace pf {
 
-constexpr int BM = 128;  // queries per CTA
-constexpr int BN = 128;  // keys per tile
-constexpr int HD = 128;  // head dim
-constexpr int REGION = 128 * 64 * 2;                // [128 rows][64 bf16] swizzled region, 16 KB
-constexpr int TILE_BYTES = 2 * REGION;              // 128 rows x 128 dims
+constexpr int BM = 128;                  // queries per Q tile
+constexpr int BN = 64;                   // keys per K/V tile
+constexpr int HD = 128;                  // head dim
+constexpr int QT = 2;                    // Q tiles per CTA
+constexpr int STAGES = 4;                // K/V ring depth
+constexpr int QREGION = BM * 64 * 2;     // [128 rows][64 bf16] swizzled region, 16 KB
+constexpr int Q_BYTES = 2 * QREGION;     // one Q tile, 32 KB
+constexpr int KREGION = BN * 64 * 2;     // [64 rows][64 bf16], 8 KB
+constexpr int KV_BYTES = 2 * KREGION;    // one K (or V) tile, 16 KB
 constexpr int SQ = 0;
-constexpr int SK = SQ + TILE_BYTES;                 // 2 stages
-constexpr int SV = SK + 2 * TILE_BYTES;             // 2 stages
-constexpr int SP = SV + 2 * TILE_BYTES;             // P, bf16 high part
-constexpr int SP_LO = SP + TILE_BYTES;              // P - bf16(P), bf16 low part
-constexpr int SBAR = SP_LO + TILE_BYTES;            // barriers after the tiles
-constexpr int SMEM_BYTES = SBAR + 128 + 3 * 512 + 1008;  // barriers, row-max exchange, alignment slack
+constexpr int SK = SQ + QT * Q_BYTES;
+constexpr int SV = SK + STAGES * KV_BYTES;
+constexpr int SBAR = SV + STAGES * KV_BYTES;
+constexpr int SMEM_BYTES = SBAR + 256 + 1024;  // barriers + alignment slack
+constexpr float kRescaleLog2 = 8.f;            // lazy O rescale threshold (log2 units)
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -65,35 +76,28 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M=128, N=128
-// a_f16: A operand in fp16 (P), B in bf16 (V).
-__host__ __device__ constexpr uint32_t idesc(bool b_mn_major, bool a_f16 = false) {
-  return (1u << 4) | (a_f16 ? 0u : (1u << 7)) | (1u << 10) | (b_mn_major ? (1u << 16) : 0u) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = n;
+// B K-major (K tile of S = Q K^T) or MN-major (V tile of O += P V).
+__host__ __device__ constexpr uint32_t idesc(int n, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn_major ? (1u << 16) : 0u) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
 }
 
-// P enters the P.V MMA as two bf16 terms, hi = bf16(p) and lo = bf16(p - hi)
-// (mixed fp16 x bf16 operands are not a tcgen05 kind::f16 combination): a
-// single bf16 P costs ~2^-9 relative output error, above the 2e-3 bf16
-// tolerance for rows dominated by one key; hi + lo keeps ~2^-16.
-constexpr bool kPHalf = false;
-
-__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
-  if (kPHalf) {
-    const uint32_t l = __half_as_ushort(__float2half_rn(lo));
-    const uint32_t h = __half_as_ushort(__float2half_rn(hi));
-    return l | (h << 16);
-  }
-  const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
-  const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
-  return l | (h << 16);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+// D[tmem] (+)= A[smem] . B[smem]
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]  (A: 128 lanes x 16 bf16 packed in 8 columns)
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
 
@@ -123,33 +127,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
+__device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
       "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(addr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
-      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
-      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])),
-      "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
-      "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])),
-      "r"(__float_as_uint(v[23])), "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])),
-      "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])),
-      "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
-  const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
-  return l | (h << 16);
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
+  uint32_t u[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i]);
+  tmem_st32u(addr, u);
 }
+
 
 }  // namespace pf
 
-// One CTA: 128 queries [q0, q0+128) of stream s, query head h (kv head h/G).
-__global__ void __maxnreg__(168)  // 10 warps: <= 3 per SM sub-partition x 168 regs fit its 16K registers
+// CTA (pair p, head h, stream s): Q tiles t0 = 2p and t0 + 1 (if it exists).
+__global__ void __launch_bounds__(320, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const PrefillArgs a) {
   using namespace pf;
@@ -157,33 +157,53 @@ __global__ void __maxnreg__(168)  // 10 warps: <= 3 per SM sub-partition x 168 r
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SBAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* p_ready = bars + 7;
-  uint64_t* o_full = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* k_full = bars + 1;        // [STAGES]
+  uint64_t* k_empty = bars + 5;       // [STAGES]
+  uint64_t* v_full = bars + 9;        // [STAGES]
+  uint64_t* v_empty = bars + 13;      // [STAGES]
+  uint64_t* s_full = bars + 17;       // [QT][2] S_i(j) in buffer j&1
+  uint64_t* p_full = bars + 21;       // [QT][2] P_i(j) written to buffer j&1 (and O_i rescaled)
+  uint64_t* o_done = bars + 25;       // [QT]    P_i(j) V done
+  uint64_t* o_final = bars + 27;      // [QT]    last P_i V done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
 
-  const int q0 = blockIdx.x * BM, h = blockIdx.y, s = blockIdx.z;
+  const int h = blockIdx.x, s = blockIdx.y;
+  const int nqt = (a.C + BM - 1) / BM, npairs = (nqt + 1) / 2;
+  // heaviest pairs first (later query tiles see more keys); a lone last tile goes last
+  const int z = blockIdx.z;
+  const bool lone = (nqt & 1) && npairs > 1;
+  const int p = lone ? (z < npairs - 1 ? npairs - 2 - z : npairs - 1) : npairs - 1 - z;
   const int g = h / a.G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C, n0 = a.n0;
-  const int q_hi = min(q0 + BM, C);                    // exclusive
-  const int ntiles = (n0 + q_hi + BN - 1) / BN;        // key tiles touched by the causal rows
+  int nkv[QT];
+#pragma unroll
+  for (int i = 0; i < QT; ++i) {
+    const int t = 2 * p + i;
+    nkv[i] = t < nqt ? (n0 + min((t + 1) * BM, C) + BN - 1) / BN : 0;
+  }
+  const int nkv_max = max(nkv[0], nkv[1]);
   const int seg_row = (int)(((int64_t)s * a.L + a.layer) * a.Hkv + g) * a.cap;
 
   if (tid == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
-    mbar_init(p_ready, 8);
-    mbar_init(o_full, 1);
+    for (int i = 0; i < QT; ++i) {
+      mbar_init(&s_full[2 * i], 1);
+      mbar_init(&s_full[2 * i + 1], 1);
+      mbar_init(&p_full[2 * i], 4);
+      mbar_init(&p_full[2 * i + 1], 4);
+      mbar_init(&o_done[i], 1);
+      mbar_init(&o_final[i], 1);
+    }
     mbar_fence_init();
   }
-  if (warp == 9) {  // TMEM: S0 [0,128), S1 [128,256), O [256,384)
+  if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -195,185 +215,202 @@ __global__ void __maxnreg__(168)  // 10 warps: <= 3 per SM sub-partition x 168 r
   if (warp == 8) {
     // ------------------------------------------------------------- producer
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, TILE_BYTES);
-      tma_load_3d(smem + SQ, &qmap, 0, h, s * C + q0, q_full);
-      tma_load_3d(smem + SQ + REGION, &qmap, 64, h, s * C + q0, q_full);
-      for (int j = 0; j < ntiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], 2 * TILE_BYTES);
+      const int ntq = nkv[1] > 0 ? 2 : 1;
+      mbar_arrive_expect_tx(q_full, ntq * Q_BYTES);
+      for (int i = 0; i < ntq; ++i) {
+        const int row = s * C + (2 * p + i) * BM;
+        tma_load_3d(smem + SQ + i * Q_BYTES, &qmap, 0, h, row, q_full);
+        tma_load_3d(smem + SQ + i * Q_BYTES + QREGION, &qmap, 64, h, row, q_full);
+      }
+      for (int j = 0; j < nkv_max; ++j) {
+        const int st = j % STAGES;
+        const uint32_t ph = ((j / STAGES) & 1) ^ 1;
         const int y = seg_row + j * BN;
-        tma_load_2d(smem + SK + st * TILE_BYTES, &kmap, 0, y, &kv_full[st]);
-        tma_load_2d(smem + SK + st * TILE_BYTES + REGION, &kmap, 64, y, &kv_full[st]);
-        tma_load_2d(smem + SV + st * TILE_BYTES, &vmap, 0, y, &kv_full[st]);
-        tma_load_2d(smem + SV + st * TILE_BYTES + REGION, &vmap, 64, y, &kv_full[st]);
+        mbar_wait(&k_empty[st], ph);
+        mbar_arrive_expect_tx(&k_full[st], KV_BYTES);
+        tma_load_2d(smem + SK + st * KV_BYTES, &kmap, 0, y, &k_full[st]);
+        tma_load_2d(smem + SK + st * KV_BYTES + KREGION, &kmap, 64, y, &k_full[st]);
+        mbar_wait(&v_empty[st], ph);
+        mbar_arrive_expect_tx(&v_full[st], KV_BYTES);
+        tma_load_2d(smem + SV + st * KV_BYTES, &vmap, 0, y, &v_full[st]);
+        tma_load_2d(smem + SV + st * KV_BYTES + KREGION, &vmap, 64, y, &v_full[st]);
       }
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t id_s = idesc(false), id_o = idesc(true, kPHalf);
-      const uint32_t sq = smem_u32(smem + SQ), sp = smem_u32(smem + SP), sp_lo = smem_u32(smem + SP_LO);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + SK + st * TILE_BYTES);
+      const uint32_t id_s = idesc(BN, false), id_o = idesc(HD, true);
+      auto issue_s = [&](int i, int j) {  // S_i(j) = Q_i K_j^T into buffer j&1
+        const int st = j % STAGES;
+        const uint32_t sq = smem_u32(smem + SQ + i * Q_BYTES), sk = smem_u32(smem + SK + st * KV_BYTES);
+        const uint32_t d = tmem + i * 128 + (j & 1) * BN;
 #pragma unroll
         for (int ks = 0; ks < HD / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * REGION + (ks & 3) * 32;
-          mma_bf16(tmem + st * 128, smem_desc(sq + off, 16, 1024), smem_desc(sk + off, 16, 1024), id_s, ks > 0);
+          const uint32_t qo = (ks >> 2) * QREGION + (ks & 3) * 32, ko = (ks >> 2) * KREGION + (ks & 3) * 32;
+          mma_ss(d, smem_desc(sq + qo, 16, 1024), smem_desc(sk + ko, 16, 1024), id_s, ks > 0);
         }
-        mma_commit(&s_full[st]);
+        mma_commit(&s_full[2 * i + (j & 1)]);
+      };
+      auto issue_s_both = [&](int j) {
+        if (j >= nkv_max) return;
+        mbar_wait(&k_full[j % STAGES], (j / STAGES) & 1);
+        tc_fence_after();
+        for (int i = 0; i < QT; ++i) {
+          if (j >= nkv[i]) continue;
+          if (j >= 2) {  // buffer j&1 still holds P_i(j-2): its P.V must be done
+            mbar_wait(&o_done[i], ((j - 2) & 1));
+            tc_fence_after();
+          }
+          issue_s(i, j);
+        }
+        mma_commit(&k_empty[j % STAGES]);
       };
       mbar_wait(q_full, 0);
-      issue_s(0);
-      for (int j = 0; j < ntiles; ++j) {
-        if (j + 1 < ntiles) issue_s(j + 1);
-        mbar_wait(p_ready, j & 1);
-        tc_fence_after();
-        const uint32_t sv = smem_u32(smem + SV + (j & 1) * TILE_BYTES);
+      tc_fence_after();
+      issue_s_both(0);
+      issue_s_both(1);
+      for (int j = 0; j < nkv_max; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&v_full[st], (j / STAGES) & 1);
+        const uint32_t sv = smem_u32(smem + SV + st * KV_BYTES);
+        for (int i = 0; i < QT; ++i) {
+          if (j >= nkv[i]) continue;
+          mbar_wait(&p_full[2 * i + (j & 1)], (j >> 1) & 1);
+          tc_fence_after();
+          const uint32_t pa = tmem + i * 128 + (j & 1) * BN;  // P_hi cols [0,32), P_lo [32,64)
 #pragma unroll
-        for (int ks = 0; ks < 2 * (BN / 16); ++ks) {  // P_hi . V, then P_lo . V
-          const int kk = ks & (BN / 16 - 1);
-          const uint32_t pa = (ks < BN / 16 ? sp : sp_lo) + (kk >> 2) * REGION + (kk & 3) * 32;
-          const uint32_t vb = sv + kk * 16 * 128;  // 16 keys of 128-byte rows
-          mma_bf16(tmem + 256, smem_desc(pa, 16, 1024), smem_desc(vb, REGION, 1024), id_o, (j > 0 || ks > 0));
+          for (int ks = 0; ks < 2 * (BN / 16); ++ks) {
+            const int kk = ks & (BN / 16 - 1);
+            const uint32_t at = pa + (ks >= BN / 16 ? 32 : 0) + kk * 8;
+            const uint32_t vb = sv + kk * 16 * 128;  // 16 keys of 128-byte rows
+            mma_ts(tmem + 256 + i * 128, at, smem_desc(vb, KREGION, 1024), id_o, (j > 0 || ks > 0));
+          }
+          mma_commit(&o_done[i]);
+          if (j == nkv[i] - 1) mma_commit(&o_final[i]);
         }
-        mma_commit(o_full);
-        mma_commit(&kv_empty[j & 1]);
+        mma_commit(&v_empty[st]);
+        issue_s_both(j + 2);
       }
     }
   } else {
-    // -------------------------- softmax: 8 warps, two threads per query row
-    // thread t owns row t & 127 (its TMEM lane) and key/output columns
-    // [64*hf, 64*hf + 64), hf = t >> 7; the pair exchanges its row maximum
-    // through shared memory once per tile and its row sum once at the end.
-    const int r = tid & 127, hf = tid >> 7;
-    const int qi = q0 + r;                 // query index in the chunk
+    // ------------------------- softmax: warpgroup i = warps 4i..4i+3, one row per thread
+    const int i = warp >> 2;
+    const int r = tid & 127;
+    const int nk = nkv[i];
+    const int q0 = (2 * p + i) * BM;
+    const int qi = q0 + r;  // query index in the chunk
     const bool valid = qi < C;
-    const int limit = valid ? n0 + qi + 1 : 1;
-    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + hf * 64;
-    const int wrow = qi - (C - a.W);      // window row index (>= 0: recorded)
+    const int limit = valid ? n0 + qi + 1 : n0 + 1;  // keys [0, limit) are visible
+    const int tile_min_limit = n0 + q0 + 1;          // smallest limit of the tile's rows
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t s_base = tmem + lane_off + i * 128;
+    const uint32_t o_base = tmem + lane_off + 256 + i * 128;
+    const int wrow = qi - (C - a.W);  // window row index (>= 0: recorded)
     const bool rec = valid && a.lg && wrow >= 0;
     float* lgrow = rec ? a.lg + ((int64_t)(s * a.W + wrow) * a.Hq + h) * a.lg_cap : nullptr;
+    const bool any_rec = __any_sync(0xffffffffu, rec);
     const bool lg_aligned = (reinterpret_cast<uintptr_t>(lgrow) & 15) == 0;
-    unsigned* xch = reinterpret_cast<unsigned*>(bars + 16);  // [3][128] row maxima (orderable keys)
-    float m = -INFINITY, l = 0.f;
-    unsigned char* prow_base = smem + SP + hf * REGION + r * 128;
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+    const float c1 = a.scale * kLog2e;
+    float m = -INFINITY;  // running (possibly stale) max of the raw q.k
+    float l = 0.f;
+    for (int j = 0; j < nk; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[2 * i + b], (j >> 1) & 1);
       tc_fence_after();
-      float sv[64];
-#pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
+      float sv[BN];
+      {
         float t32[32];
-        tmem_ld32(lane_base + st * 128 + c2 * 32, t32);
+        tmem_ld32(s_base + b * BN, t32);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c2 * 32 + i] = t32[i];
-      }
-      const int tbase = j * BN + hf * 64;
-      float pm = -INFINITY;
+        for (int e = 0; e < 32; ++e) sv[e] = t32[e];
+        tmem_ld32(s_base + b * BN + 32, t32);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        sv[i] = tbase + i < limit ? sv[i] * a.scale : -INFINITY;
-        pm = fmaxf(pm, sv[i]);
+        for (int e = 0; e < 32; ++e) sv[32 + e] = t32[e];
       }
-      // pair maximum through a 3-buffer ring of atomicMax keys: buffer (j+2)%3 is
-      // reset here and first used again after the next barrier
-      if (j == 0) {
-        if (hf == 0) {
-          xch[r] = 0u;
-          xch[128 + r] = 0u;
+      const int tbase = j * BN;
+      if (tbase + BN > tile_min_limit) {  // diagonal / tail tile: causal mask
+#pragma unroll
+        for (int e = 0; e < BN; ++e) sv[e] = tbase + e < limit ? sv[e] : -INFINITY;
+      }
+      float mx = sv[0];
+#pragma unroll
+      for (int e = 1; e < BN; ++e) mx = fmaxf(mx, sv[e]);
+      const float mn = fmaxf(m, mx);
+      const bool grow = (mn - m) * c1 > kRescaleLog2;  // true on the first tile (m = -inf)
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        // O_i row *= 2^((m - mn) c1): P_i(j-1) V must have landed
+        mbar_wait(&o_done[i], (j - 1) & 1);
+        tc_fence_after();
+        const float alpha = grow ? exp2f((m - mn) * c1) : 1.f;
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          float o32[32];
+          tmem_ld32(o_base + c4 * 32, o32);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o32[e] *= alpha;
+          tmem_st32(o_base + c4 * 32, o32);
         }
-        asm volatile("bar.sync 3, 256;\n" ::: "memory");
+        tc_wait_st();
+        if (grow) l *= alpha;
       }
-      atomicMax(&xch[(j % 3) * 128 + r], orderable(pm));
-      if (hf == 0) xch[((j + 2) % 3) * 128 + r] = 0u;
-      asm volatile("bar.sync 3, 256;\n" ::: "memory");
-      const unsigned key = xch[(j % 3) * 128 + r];
-      const float tmax = __uint_as_float((key & 0x80000000u) ? (key & 0x7fffffffu) : ~key);
-      if (lgrow) {
+      if (grow) m = mn;
+      if (any_rec && lgrow) {
 #pragma unroll
-        for (int i = 0; i < 64; i += 4) {
-          const int t = tbase + i;
+        for (int e = 0; e < BN; e += 4) {
+          const int t = tbase + e;
           if (t + 3 < limit && lg_aligned) {
-            *reinterpret_cast<float4*>(lgrow + t) = make_float4(sv[i], sv[i + 1], sv[i + 2], sv[i + 3]);
+            *reinterpret_cast<float4*>(lgrow + t) =
+                make_float4(sv[e] * a.scale, sv[e + 1] * a.scale, sv[e + 2] * a.scale, sv[e + 3] * a.scale);
           } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (t + e < limit) lgrow[t + e] = sv[i + e];
+            for (int x = 0; x < 4; ++x)
+              if (t + x < limit) lgrow[t + x] = sv[e + x] * a.scale;
           }
         }
       }
-      const float mn = fmaxf(m, tmax);
-      const float alpha = m == -INFINITY ? 0.f : exp2f((m - mn) * kLog2e);
-      // P.V of the previous tile must be done before P is overwritten (and O rescaled)
-      if (j > 0) {
-        mbar_wait(o_full, (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, mn > m)) {  // rescale this thread's O columns (warp-uniform tcgen05)
-#pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
-            float o32[32];
-            tmem_ld32(lane_base + 256 + c2 * 32, o32);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o32[i] *= alpha;
-            tmem_st32(lane_base + 256 + c2 * 32, o32);
-          }
-          tc_wait_st();
-        }
-      }
+      const float mo = m * c1;
+      uint32_t hi[BN / 2], lo[BN / 2];
       float psum = 0.f;
 #pragma unroll
-      for (int kc = 0; kc < 8; ++kc) {
-        float p8[8], lo8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          p8[e] = exp2f((sv[kc * 8 + e] - mn) * kLog2e);
-          psum += p8[e];
-          lo8[e] = p8[e] - __bfloat162float(__float2bfloat16_rn(p8[e]));
-        }
-        const uint4 hi = make_uint4(pack_p(p8[0], p8[1]), pack_p(p8[2], p8[3]), pack_p(p8[4], p8[5]),
-                                    pack_p(p8[6], p8[7]));
-        const uint4 lo = make_uint4(pack_p(lo8[0], lo8[1]), pack_p(lo8[2], lo8[3]), pack_p(lo8[4], lo8[5]),
-                                    pack_p(lo8[6], lo8[7]));
-        const int off = (kc ^ (r & 7)) << 4;
-        *reinterpret_cast<uint4*>(prow_base + off) = hi;
-        *reinterpret_cast<uint4*>(prow_base + (SP_LO - SP) + off) = lo;
+      for (int e = 0; e < BN; e += 2) {
+        const float p0 = exp2f(fmaf(sv[e], c1, -mo));
+        const float p1 = exp2f(fmaf(sv[e + 1], c1, -mo));
+        psum += p0 + p1;
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+        const float2 hf = __bfloat1622float2(h2);
+        const __nv_bfloat162 l2 = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+        hi[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+        lo[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
-      l = l * alpha + psum;
-      m = mn;
-      fence_async_smem();
+      l += psum;
+      tmem_st32u(s_base + b * BN, hi);
+      tmem_st32u(s_base + b * BN + 32, lo);
+      tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
+      if (lane == 0) mbar_arrive(&p_full[2 * i + b]);
     }
-    // epilogue: O / (l_self + l_partner) (two-term sum: the same in either order)
-    float* lx = reinterpret_cast<float*>(xch);
-    asm volatile("bar.sync 3, 256;\n" ::: "memory");  // everyone is done with the max ring
-    lx[hf * 128 + r] = l;
-    asm volatile("bar.sync 3, 256;\n" ::: "memory");
-    const float lt = l + lx[(hf ^ 1) * 128 + r];
-    mbar_wait(o_full, (ntiles - 1) & 1);
-    tc_fence_after();
-    float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD + hf * 64;
-    const float inv = 1.f / lt;
+    if (nk > 0) {
+      // epilogue: O / l
+      mbar_wait(&o_final[i], 0);
+      tc_fence_after();
+      float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD;
+      const float inv = 1.f / l;
 #pragma unroll
-    for (int c2 = 0; c2 < 2; ++c2) {
-      float o32[32];
-      tmem_ld32(lane_base + 256 + c2 * 32, o32);  // warp-uniform (.sync.aligned)
-      if (valid) {
+      for (int c4 = 0; c4 < 4; ++c4) {
+        float o32[32];
+        tmem_ld32(o_base + c4 * 32, o32);  // warp-uniform (.sync.aligned)
+        if (valid) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(orow + c2 * 32 + i) =
-              make_float4(o32[i] * inv, o32[i + 1] * inv, o32[i + 2] * inv, o32[i + 3] * inv);
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(orow + c4 * 32 + e) =
+                make_float4(o32[e] * inv, o32[e + 1] * inv, o32[e + 2] * inv, o32[e + 3] * inv);
+        }
       }
-    }
-    if (rec && a.st && hf == 0) {
-      a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2] = m;
-      a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = lt;
+      if (rec && a.st) {
+        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2] = m * a.scale;
+        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = l;
+      }
     }
   }
   tc_fence_before();
@@ -408,7 +445,7 @@ cudaError_t make_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
   if (!enc) return cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)pf::HD, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)pf::HD * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, pf::BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -441,7 +478,8 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.C + pf::BM - 1) / pf::BM, a.Hq, streams);
+  const int nqt = (a.C + pf::BM - 1) / pf::BM;
+  dim3 grid(a.Hq, streams, (nqt + 1) / 2);
   prefill_kernel<<<grid, 320, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
