@@ -11,24 +11,31 @@
 // One CTA = two 128-query tiles of one head ("ping-pong"): while the softmax
 // warpgroup of one tile turns its S tile into P, the tensor core runs the
 // other tile's MMAs.  Warp 8 (TMA producer) loads both Q tiles once and
-// 64-key K and V tiles into 4-stage rings (cp.async.bulk.tensor, 128-byte
-// swizzle).  Warp 9 owns TMEM and issues tcgen05.mma (bf16 -> f32):
-// S_i = Q_i K^T (M=128, N=64) into a double-buffered 64-column TMEM S tile,
-// O_i += P_i V (M=128, N=128) with P read straight from TMEM (the .kind::f16
-// A-from-TMEM form), O_i in its own 128 TMEM columns.  Warps 0-3 / 4-7 (one
+// 128-key K and V tiles into 2-stage rings (cp.async.bulk.tensor, 128-byte
+// swizzle).  Warps 10-11 convert each landed V tile in place from bf16 to
+// fp16 (exact for |v| < 65504; larger values saturate and are counted).
+// Warp 9 owns TMEM and issues tcgen05.mma: S_i = Q_i K^T (bf16, M=N=128)
+// into a 128-column TMEM tile, O_i += P_i V (fp16, M=N=128) with P read
+// straight from TMEM (the .kind::f16 A-from-TMEM form).  fp16 P carries
+// 2^-11 relative rounding (bf16 P would carry 2^-8, above the 2e-3 bf16
+// tolerance for diffuse rows) at one MMA per 16 keys.  Warps 0-3 / 4-7 (one
 // query row per thread) read S with tcgen05.ld, run the online softmax and
-// write P back over the S columns it came from as two bf16 terms
-// (hi = bf16(p), lo = bf16(p - hi)).  O is rescaled lazily: only when a row
-// maximum grows by more than 2^8 (exact -- O and the row sum share the stale
-// maximum), so the TMEM round trip is rare after the first tiles.
+// write P (fp16) back over the first 64 of the S columns it came from.  O is
+// rescaled lazily: only when a row maximum grows by more than 2^8 (exact --
+// O and the row sum share the stale maximum).
 //
-// TMEM columns: S/P of tile 0 [0,128) (two 64-column buffers), S/P of tile 1
-// [128,256), O of tile 0 [256,384), O of tile 1 [384,512).
+// Order on the tensor core: S_0(0) S_1(0) | P_0V(0) S_0(1) P_1V(0) S_1(1) |
+// ...  S_i(j+1) overwrites the columns P_i(j) V reads; tcgen05.mma from one
+// thread executes in issue order, which CUTLASS's SM100 FMHA relies on too.
+//
+// TMEM columns: S/P of tile 0 [0,128), S/P of tile 1 [128,256), O of tile 0
+// [256,384), O of tile 1 [384,512).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "skv_common.cuh"
 #include "skv_internal.h"
@@ -38,19 +45,19 @@ namespace skv {
 namespace pf {
 
 constexpr int BM = 128;                  // queries per Q tile
-constexpr int BN = 64;                   // keys per K/V tile
+constexpr int BN = 128;                  // keys per K/V tile
 constexpr int HD = 128;                  // head dim
 constexpr int QT = 2;                    // Q tiles per CTA
-constexpr int STAGES = 4;                // K/V ring depth
-constexpr int QREGION = BM * 64 * 2;     // [128 rows][64 bf16] swizzled region, 16 KB
-constexpr int Q_BYTES = 2 * QREGION;     // one Q tile, 32 KB
-constexpr int KREGION = BN * 64 * 2;     // [64 rows][64 bf16], 8 KB
-constexpr int KV_BYTES = 2 * KREGION;    // one K (or V) tile, 16 KB
+constexpr int STAGES = 2;                // K/V ring depth
+constexpr int REGION = 128 * 64 * 2;     // [128 rows][64 16-bit] swizzled region, 16 KB
+constexpr int TILE = 2 * REGION;         // one Q, K or V tile (128 rows x 128 dims), 32 KB
 constexpr int SQ = 0;
-constexpr int SK = SQ + QT * Q_BYTES;
-constexpr int SV = SK + STAGES * KV_BYTES;
-constexpr int SBAR = SV + STAGES * KV_BYTES;
+constexpr int SK = SQ + QT * TILE;
+constexpr int SV = SK + STAGES * TILE;
+constexpr int SBAR = SV + STAGES * TILE;
 constexpr int SMEM_BYTES = SBAR + 256 + 1024;  // barriers + alignment slack
+constexpr int NCONV = 2;                       // V-conversion warps
+constexpr int THREADS = (8 + 2 + NCONV) * 32;
 constexpr float kRescaleLog2 = 8.f;            // lazy O rescale threshold (log2 units)
 
 // ---------------------------------------------------------------- PTX helpers
@@ -76,11 +83,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = n;
-// B K-major (K tile of S = Q K^T) or MN-major (V tile of O += P V).
-__host__ __device__ constexpr uint32_t idesc(int n, bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn_major ? (1u << 16) : 0u) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
+// kind::f16 instruction descriptor: (bf16 x bf16 or fp16 x fp16) -> f32,
+// M = 128, N = n; B K-major (K tile of S = Q K^T) or MN-major (V of O += P V).
+__host__ __device__ constexpr uint32_t idesc(int n, bool b_mn_major, bool f16) {
+  return (1u << 4) | (f16 ? 0u : (1u << 7) | (1u << 10)) | (b_mn_major ? (1u << 16) : 0u) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 // D[tmem] (+)= A[smem] . B[smem]
@@ -127,6 +134,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the trailing wait (issue several, then tc_wait_ld once)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t addr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+}
+
 __device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
@@ -148,8 +167,37 @@ __device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
 
 }  // namespace pf
 
+// Instrumentation (a.prof != null): cycles spent in each wait, per CTA.
+#define PF_WAIT(slot, bar, par)                                     \
+  do {                                                              \
+    if (prof) {                                                     \
+      const long long t0_ = clock64();                              \
+      mbar_wait(bar, par);                                          \
+      pacc##slot += clock64() - t0_;                                \
+    } else {                                                        \
+      mbar_wait(bar, par);                                          \
+    }                                                               \
+  } while (0)
+
+namespace pf {
+// S_i(j) = Q_i K_j^T: 8 MMAs (K = 16 each) into TMEM columns [128 i, 128 i + 128)
+__device__ __forceinline__ void issue_s(uint32_t tmem, uint64_t dq0, uint64_t dk0, uint32_t id_s, int i, int j,
+                                        bool skip, uint64_t* s_full) {
+  const uint64_t dk = dk0 + (uint64_t)((j % STAGES) * (TILE >> 4));
+  const uint64_t dq = dq0 + (uint64_t)(i * (TILE >> 4));
+  if (!skip) {
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      const uint32_t off = ((ks >> 2) * REGION + (ks & 3) * 32) >> 4;
+      mma_ss(tmem + i * 128, dq + off, dk + off, id_s, ks > 0);
+    }
+  }
+  mma_commit(&s_full[i]);
+}
+}  // namespace pf
+
 // CTA (pair p, head h, stream s): Q tiles t0 = 2p and t0 + 1 (if it exists).
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(pf::THREADS, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const PrefillArgs a) {
   using namespace pf;
@@ -158,31 +206,30 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SBAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;        // [STAGES]
-  uint64_t* k_empty = bars + 5;       // [STAGES]
-  uint64_t* v_full = bars + 9;        // [STAGES]
-  uint64_t* v_empty = bars + 13;      // [STAGES]
-  uint64_t* s_full = bars + 17;       // [QT][2] S_i(j) in buffer j&1
-  uint64_t* p_full = bars + 21;       // [QT][2] P_i(j) written to buffer j&1 (and O_i rescaled)
-  uint64_t* o_done = bars + 25;       // [QT]    P_i(j) V done
-  uint64_t* o_final = bars + 27;      // [QT]    last P_i V done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
+  uint64_t* k_empty = bars + 3;       // [STAGES]
+  uint64_t* v_full = bars + 5;        // [STAGES] TMA landed (bf16)
+  uint64_t* v_conv = bars + 7;        // [STAGES] converted to fp16
+  uint64_t* v_empty = bars + 9;       // [STAGES]
+  uint64_t* s_full = bars + 11;       // [QT] S_i(j) in TMEM
+  uint64_t* p_full = bars + 13;       // [QT] P_i(j) written (and O_i rescaled)
+  uint64_t* o_final = bars + 15;      // [QT] last P_i V done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
-  const int h = blockIdx.x, s = blockIdx.y;
   const int nqt = (a.C + BM - 1) / BM, npairs = (nqt + 1) / 2;
-  // heaviest pairs first (later query tiles see more keys); a lone last tile goes last
-  const int z = blockIdx.z;
-  const bool lone = (nqt & 1) && npairs > 1;
-  const int p = lone ? (z < npairs - 1 ? npairs - 2 - z : npairs - 1) : npairs - 1 - z;
+  // consecutive CTAs share one (stream, head): its K/V stream is read from L2
+  // by the other pairs
+  const int p = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
   const int g = h / a.G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C, n0 = a.n0;
-  int nkv[QT];
-#pragma unroll
-  for (int i = 0; i < QT; ++i) {
-    const int t = 2 * p + i;
-    nkv[i] = t < nqt ? (n0 + min((t + 1) * BM, C) + BN - 1) / BN : 0;
+  int nkv0, nkv1;
+  {
+    const int t = 2 * p;
+    nkv0 = (n0 + min((t + 1) * BM, C) + BN - 1) / BN;
+    nkv1 = t + 1 < nqt ? (n0 + min((t + 2) * BM, C) + BN - 1) / BN : 0;
   }
-  const int nkv_max = max(nkv[0], nkv[1]);
+  (void)npairs;
+  const int nkv_max = max(nkv0, nkv1);
   const int seg_row = (int)(((int64_t)s * a.L + a.layer) * a.Hkv + g) * a.cap;
 
   if (tid == 0) {
@@ -191,14 +238,12 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
+      mbar_init(&v_conv[i], NCONV);
       mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < QT; ++i) {
-      mbar_init(&s_full[2 * i], 1);
-      mbar_init(&s_full[2 * i + 1], 1);
-      mbar_init(&p_full[2 * i], 4);
-      mbar_init(&p_full[2 * i + 1], 4);
-      mbar_init(&o_done[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
       mbar_init(&o_final[i], 1);
     }
     mbar_fence_init();
@@ -211,92 +256,131 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  unsigned long long* prof = nullptr;
+  unsigned long long t_start = 0;
+  // register accumulators, stored once at exit
+  unsigned long long pacc0 = 0, pacc1 = 0, pacc2 = 0, pacc3 = 0, pacc4 = 0;
+  if (a.prof && lane == 0 && (warp == 9 || warp == 0 || warp == 4)) {
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    prof = a.prof + (size_t)cta * 16 + (warp == 9 ? 0 : warp == 0 ? 6 : 11);
+    t_start = clock64();
+  }
 
-  if (warp == 8) {
-    // ------------------------------------------------------------- producer
-    if (lane == 0) {
-      const int ntq = nkv[1] > 0 ? 2 : 1;
-      mbar_arrive_expect_tx(q_full, ntq * Q_BYTES);
-      for (int i = 0; i < ntq; ++i) {
-        const int row = s * C + (2 * p + i) * BM;
-        tma_load_3d(smem + SQ + i * Q_BYTES, &qmap, 0, h, row, q_full);
-        tma_load_3d(smem + SQ + i * Q_BYTES + QREGION, &qmap, 64, h, row, q_full);
-      }
-      for (int j = 0; j < nkv_max; ++j) {
-        const int st = j % STAGES;
-        const uint32_t ph = ((j / STAGES) & 1) ^ 1;
-        const int y = seg_row + j * BN;
-        mbar_wait(&k_empty[st], ph);
-        mbar_arrive_expect_tx(&k_full[st], KV_BYTES);
-        tma_load_2d(smem + SK + st * KV_BYTES, &kmap, 0, y, &k_full[st]);
-        tma_load_2d(smem + SK + st * KV_BYTES + KREGION, &kmap, 64, y, &k_full[st]);
-        mbar_wait(&v_empty[st], ph);
-        mbar_arrive_expect_tx(&v_full[st], KV_BYTES);
-        tma_load_2d(smem + SV + st * KV_BYTES, &vmap, 0, y, &v_full[st]);
-        tma_load_2d(smem + SV + st * KV_BYTES + KREGION, &vmap, 64, y, &v_full[st]);
-      }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id_s = idesc(BN, false), id_o = idesc(HD, true);
-      auto issue_s = [&](int i, int j) {  // S_i(j) = Q_i K_j^T into buffer j&1
-        const int st = j % STAGES;
-        const uint32_t sq = smem_u32(smem + SQ + i * Q_BYTES), sk = smem_u32(smem + SK + st * KV_BYTES);
-        const uint32_t d = tmem + i * 128 + (j & 1) * BN;
-#pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks) {
-          const uint32_t qo = (ks >> 2) * QREGION + (ks & 3) * 32, ko = (ks >> 2) * KREGION + (ks & 3) * 32;
-          mma_ss(d, smem_desc(sq + qo, 16, 1024), smem_desc(sk + ko, 16, 1024), id_s, ks > 0);
+  if (warp >= 8) {
+    // (no setmaxnreg: the two-pass softmax fits the 168-register budget)
+    if (warp == 8) {
+      // ----------------------------------------------------------- producer
+      if (lane == 0) {
+        const int ntq = nkv1 > 0 ? 2 : 1;
+        mbar_arrive_expect_tx(q_full, ntq * TILE);
+        for (int i = 0; i < ntq; ++i) {
+          const int row = s * C + (2 * p + i) * BM;
+          tma_load_3d(smem + SQ + i * TILE, &qmap, 0, h, row, q_full);
+          tma_load_3d(smem + SQ + i * TILE + REGION, &qmap, 64, h, row, q_full);
         }
-        mma_commit(&s_full[2 * i + (j & 1)]);
-      };
-      auto issue_s_both = [&](int j) {
-        if (j >= nkv_max) return;
-        mbar_wait(&k_full[j % STAGES], (j / STAGES) & 1);
+        for (int j = 0; j < nkv_max; ++j) {
+          const int st = j % STAGES;
+          const uint32_t ph = ((j / STAGES) & 1) ^ 1;
+          const int y = seg_row + j * BN;
+          mbar_wait(&k_empty[st], ph);
+          mbar_arrive_expect_tx(&k_full[st], TILE);
+          tma_load_2d(smem + SK + st * TILE, &kmap, 0, y, &k_full[st]);
+          tma_load_2d(smem + SK + st * TILE + REGION, &kmap, 64, y, &k_full[st]);
+          mbar_wait(&v_empty[st], ph);
+          mbar_arrive_expect_tx(&v_full[st], TILE);
+          tma_load_2d(smem + SV + st * TILE, &vmap, 0, y, &v_full[st]);
+          tma_load_2d(smem + SV + st * TILE + REGION, &vmap, 64, y, &v_full[st]);
+        }
+      }
+    } else if (warp == 9) {
+      // --------------------------------------------------------- MMA issuer
+      if (lane == 0) {
+        // Descriptors are built once; per MMA only a compile-time offset (in
+        // 16-byte units) is added to the start-address field.
+        const uint32_t id_s = idesc(BN, false, false), id_o = idesc(HD, true, true);
+        const uint64_t dq0 = smem_desc(smem_u32(smem + SQ), 16, 1024);
+        const uint64_t dk0 = smem_desc(smem_u32(smem + SK), 16, 1024);
+        const uint64_t dv0 = smem_desc(smem_u32(smem + SV), REGION, 1024);
+        mbar_wait(q_full, 0);
+        PF_WAIT(0, &k_full[0], 0);
         tc_fence_after();
-        for (int i = 0; i < QT; ++i) {
-          if (j >= nkv[i]) continue;
-          if (j >= 2) {  // buffer j&1 still holds P_i(j-2): its P.V must be done
-            mbar_wait(&o_done[i], ((j - 2) & 1));
+        const bool skip_s = a.dbg == 2 || a.dbg == 3;
+        issue_s(tmem, dq0, dk0, id_s, 0, 0, skip_s, s_full);
+        if (nkv1 > 0) issue_s(tmem, dq0, dk0, id_s, 1, 0, skip_s, s_full);
+        mma_commit(&k_empty[0]);
+        for (int j = 0; j < nkv_max; ++j) {
+          const int st = j % STAGES;
+          const bool next = j + 1 < nkv_max;
+          PF_WAIT(2, &v_conv[st], (j / STAGES) & 1);
+          tc_fence_after();
+          const uint64_t dv = dv0 + (uint64_t)(st * (TILE >> 4));
+#pragma unroll
+          for (int i = 0; i < QT; ++i) {
+            const int nk = i ? nkv1 : nkv0;
+            if (j >= nk) continue;
+            PF_WAIT(3, &p_full[i], j & 1);
             tc_fence_after();
+            const long long tp0 = prof ? clock64() : 0;
+            if (a.dbg != 2 && a.dbg != 4) {
+#pragma unroll
+              for (int kk = 0; kk < BN / 16; ++kk)  // 16 keys of 128-byte rows per step
+                mma_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, dv + (uint64_t)((kk * 16 * 128) >> 4), id_o,
+                       (j > 0 || kk > 0));
+            }
+            if (j == nk - 1) mma_commit(&o_final[i]);
+            if (prof) pacc1 += clock64() - tp0;
+            if (j + 1 < nk) {
+              if (i == 0 || nkv0 <= j + 1) {  // first S of tile j+1: its K must have landed
+                PF_WAIT(0, &k_full[(j + 1) % STAGES], ((j + 1) / STAGES) & 1);
+                tc_fence_after();
+              }
+              const long long tq0 = prof ? clock64() : 0;
+              issue_s(tmem, dq0, dk0, id_s, i, j + 1, skip_s, s_full);
+              if (prof) pacc4 += clock64() - tq0;
+            }
           }
-          issue_s(i, j);
+          mma_commit(&v_empty[st]);
+          if (next) mma_commit(&k_empty[(j + 1) % STAGES]);
         }
-        mma_commit(&k_empty[j % STAGES]);
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      issue_s_both(0);
-      issue_s_both(1);
+      }
+    } else {
+      // ------------------------------------------ V conversion bf16 -> fp16
+      // in place, same swizzled positions; warp w handles 16-byte chunks
+      // w-10, w-10+NCONV, ... of the 32 KB tile
+      const int cw = warp - 10;
+      uint32_t vmax = 0;  // max |bf16 bits| seen, two halves
       for (int j = 0; j < nkv_max; ++j) {
         const int st = j % STAGES;
         mbar_wait(&v_full[st], (j / STAGES) & 1);
-        const uint32_t sv = smem_u32(smem + SV + st * KV_BYTES);
-        for (int i = 0; i < QT; ++i) {
-          if (j >= nkv[i]) continue;
-          mbar_wait(&p_full[2 * i + (j & 1)], (j >> 1) & 1);
-          tc_fence_after();
-          const uint32_t pa = tmem + i * 128 + (j & 1) * BN;  // P_hi cols [0,32), P_lo [32,64)
+        uint4* base = reinterpret_cast<uint4*>(smem + SV + st * TILE);
+#pragma unroll 4
+        for (int c = cw * 32 + lane; c < TILE / 16; c += NCONV * 32) {
+          uint4 x = base[c];
+          uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int ks = 0; ks < 2 * (BN / 16); ++ks) {
-            const int kk = ks & (BN / 16 - 1);
-            const uint32_t at = pa + (ks >= BN / 16 ? 32 : 0) + kk * 8;
-            const uint32_t vb = sv + kk * 16 * 128;  // 16 keys of 128-byte rows
-            mma_ts(tmem + 256 + i * 128, at, smem_desc(vb, KREGION, 1024), id_o, (j > 0 || ks > 0));
+          for (int e = 0; e < 4; ++e) {
+            vmax = __vmaxu2(vmax, w[e] & 0x7fff7fffu);
+            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xffff0000u);
+            uint32_t hv;
+            asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(hv) : "f"(hi), "f"(lo));
+            w[e] = hv;
           }
-          mma_commit(&o_done[i]);
-          if (j == nkv[i] - 1) mma_commit(&o_final[i]);
+          base[c] = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        mma_commit(&v_empty[st]);
-        issue_s_both(j + 2);
+        fence_async_smem();  // generic-proxy stores -> tensor-core (async proxy) reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&v_conv[st]);
       }
+      // |v| >= 65536 (bf16 0x4780) does not fit fp16: it was saturated
+      const bool sat = (vmax & 0xffffu) >= 0x4780u || (vmax >> 16) >= 0x4780u;
+      if (a.ovf && __any_sync(0xffffffffu, sat) && lane == 0) atomicAdd(a.ovf, 1);
     }
   } else {
+
     // ------------------------- softmax: warpgroup i = warps 4i..4i+3, one row per thread
     const int i = warp >> 2;
     const int r = tid & 127;
-    const int nk = nkv[i];
+    const int nk = i ? nkv1 : nkv0;
     const int q0 = (2 * p + i) * BM;
     const int qi = q0 + r;  // query index in the chunk
     const bool valid = qi < C;
@@ -314,33 +398,45 @@ __global__ void __launch_bounds__(320, 1)
     float m = -INFINITY;  // running (possibly stale) max of the raw q.k
     float l = 0.f;
     for (int j = 0; j < nk; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[2 * i + b], (j >> 1) & 1);
+      PF_WAIT(0, &s_full[i], j & 1);  // also implies P_i(j-1) V is complete
       tc_fence_after();
-      float sv[BN];
-      {
-        float t32[32];
-        tmem_ld32(s_base + b * BN, t32);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) sv[e] = t32[e];
-        tmem_ld32(s_base + b * BN + 32, t32);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) sv[32 + e] = t32[e];
+      if (a.dbg == 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
+        continue;
       }
+      // Two passes over the S columns, 64 at a time (register budget): the
+      // row maximum first, then mask / record / exp / pack fp16 P into
+      // columns [0, 64) (S columns [0, 64) are consumed by then).
       const int tbase = j * BN;
-      if (tbase + BN > tile_min_limit) {  // diagonal / tail tile: causal mask
+      // causal mask needed for some row of the tile (warp-uniform: the last
+      // one or two tiles only)
+      const bool diag = tbase + BN > tile_min_limit;
+      float mx = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < BN; ++e) sv[e] = tbase + e < limit ? sv[e] : -INFINITY;
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t u[2][32];
+        tmem_ld32_async(s_base + hh * 64, u[0]);
+        tmem_ld32_async(s_base + hh * 64 + 32, u[1]);
+        tc_wait_ld();
+        if (diag) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (tbase + hh * 64 + e >= limit) u[e >> 5][e & 31] = __float_as_uint(-INFINITY);
+        }
+        float ma = mx, mb = -INFINITY;  // two 3-input max chains
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          ma = fmaxf(ma, fmaxf(__uint_as_float(u[e >> 5][e & 31]), __uint_as_float(u[e >> 5][(e + 1) & 31])));
+          mb = fmaxf(mb, fmaxf(__uint_as_float(u[e >> 5][(e + 2) & 31]), __uint_as_float(u[e >> 5][(e + 3) & 31])));
+        }
+        mx = fmaxf(ma, mb);
       }
-      float mx = sv[0];
-#pragma unroll
-      for (int e = 1; e < BN; ++e) mx = fmaxf(mx, sv[e]);
       const float mn = fmaxf(m, mx);
       const bool grow = (mn - m) * c1 > kRescaleLog2;  // true on the first tile (m = -inf)
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
-        // O_i row *= 2^((m - mn) c1): P_i(j-1) V must have landed
-        mbar_wait(&o_done[i], (j - 1) & 1);
-        tc_fence_after();
+        // O_i row *= 2^((m - mn) c1); P_i(j-1) V is complete (s_full above)
         const float alpha = grow ? exp2f((m - mn) * c1) : 1.f;
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
@@ -352,47 +448,64 @@ __global__ void __launch_bounds__(320, 1)
         }
         tc_wait_st();
         if (grow) l *= alpha;
+        if (prof) pacc2 += 1;
       }
       if (grow) m = mn;
-      if (any_rec && lgrow) {
+      const float mo = m * c1;
+      const float2 c12 = make_float2(c1, c1), mo2 = make_float2(-mo, -mo);
+      float2 psa = make_float2(0.f, 0.f), psb = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < BN; e += 4) {
-          const int t = tbase + e;
-          if (t + 3 < limit && lg_aligned) {
-            *reinterpret_cast<float4*>(lgrow + t) =
-                make_float4(sv[e] * a.scale, sv[e + 1] * a.scale, sv[e + 2] * a.scale, sv[e + 3] * a.scale);
-          } else {
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t u[2][32];
+        tmem_ld32_async(s_base + hh * 64, u[0]);
+        tmem_ld32_async(s_base + hh * 64 + 32, u[1]);
+        tc_wait_ld();
+        if (diag) {
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
-              if (t + x < limit) lgrow[t + x] = sv[e + x] * a.scale;
+          for (int e = 0; e < 64; ++e)
+            if (tbase + hh * 64 + e >= limit) u[e >> 5][e & 31] = __float_as_uint(-INFINITY);
+        }
+        if (any_rec) {  // the last W rows of the chunk: raw f32 logits for the window fold
+          if (lgrow) {
+#pragma unroll
+            for (int e = 0; e < 64; e += 4) {
+              const int t = tbase + hh * 64 + e;
+              const float x0 = __uint_as_float(u[e >> 5][e & 31]) * a.scale;
+              const float x1 = __uint_as_float(u[e >> 5][(e + 1) & 31]) * a.scale;
+              const float x2 = __uint_as_float(u[e >> 5][(e + 2) & 31]) * a.scale;
+              const float x3 = __uint_as_float(u[e >> 5][(e + 3) & 31]) * a.scale;
+              if (t + 3 < limit && lg_aligned) {
+                *reinterpret_cast<float4*>(lgrow + t) = make_float4(x0, x1, x2, x3);
+              } else {
+                if (t < limit) lgrow[t] = x0;
+                if (t + 1 < limit) lgrow[t + 1] = x1;
+                if (t + 2 < limit) lgrow[t + 2] = x2;
+                if (t + 3 < limit) lgrow[t + 3] = x3;
+              }
+            }
           }
         }
-      }
-      const float mo = m * c1;
-      uint32_t hi[BN / 2], lo[BN / 2];
-      float psum = 0.f;
+        uint32_t pk[32];
 #pragma unroll
-      for (int e = 0; e < BN; e += 2) {
-        const float p0 = exp2f(fmaf(sv[e], c1, -mo));
-        const float p1 = exp2f(fmaf(sv[e + 1], c1, -mo));
-        psum += p0 + p1;
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-        const float2 hf = __bfloat1622float2(h2);
-        const __nv_bfloat162 l2 = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
-        hi[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-        lo[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+        for (int e = 0; e < 64; e += 2) {
+          const float2 x = make_float2(__uint_as_float(u[e >> 5][e & 31]), __uint_as_float(u[e >> 5][(e + 1) & 31]));
+          const float2 t = __ffma2_rn(x, c12, mo2);  // (s - m) * scale * log2(e), two lanes
+          const float2 pp = make_float2(fast_exp2(t.x), fast_exp2(t.y));
+          if ((e >> 1) & 1) psb = __fadd2_rn(psb, pp); else psa = __fadd2_rn(psa, pp);
+          asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(pk[e / 2]) : "f"(pp.y), "f"(pp.x));
+        }
+        tmem_st32u(s_base + hh * 32, pk);
       }
-      l += psum;
-      tmem_st32u(s_base + b * BN, hi);
-      tmem_st32u(s_base + b * BN + 32, lo);
+      const float2 ps = __fadd2_rn(psa, psb);
+      l += ps.x + ps.y;
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[2 * i + b]);
+      if (lane == 0) mbar_arrive(&p_full[i]);
     }
     if (nk > 0) {
       // epilogue: O / l
-      mbar_wait(&o_final[i], 0);
+      PF_WAIT(3, &o_final[i], 0);
       tc_fence_after();
       float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD;
       const float inv = 1.f / l;
@@ -412,6 +525,14 @@ __global__ void __launch_bounds__(320, 1)
         a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = l;
       }
     }
+  }
+  if (prof) {
+    prof[4] = clock64() - t_start;
+    prof[0] = pacc0;
+    prof[1] += pacc1;
+    prof[2] += pacc2;
+    prof[3] = pacc3;
+    if (warp == 9) prof[5] = pacc4;
   }
   tc_fence_before();
   __syncthreads();
@@ -453,8 +574,14 @@ cudaError_t make_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static unsigned long long* g_prof = nullptr;
+void set_prefill_profile(unsigned long long* p) { g_prof = p; }
+
 cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const void* vbase, int64_t kv_rows,
-                           const PrefillArgs& a, cudaStream_t st) {
+                           const PrefillArgs& a_in, cudaStream_t st) {
+  PrefillArgs a = a_in;
+  if (g_prof) a.prof = g_prof;
+  if (const char* d = getenv("SKV_PF_DBG")) a.dbg = atoi(d);
   EncodeFn enc = encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap qmap, kmap, vmap;
@@ -479,8 +606,8 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
     attr = true;
   }
   const int nqt = (a.C + pf::BM - 1) / pf::BM;
-  dim3 grid(a.Hq, streams, (nqt + 1) / 2);
-  prefill_kernel<<<grid, 320, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
+  dim3 grid((nqt + 1) / 2, a.Hq, streams);
+  prefill_kernel<<<grid, pf::THREADS, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};

@@ -1097,6 +1097,11 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   return SKV_OK;
 }
 
+int skv_prefill_profile(uint64_t* counters) {
+  set_prefill_profile(reinterpret_cast<unsigned long long*>(counters));
+  return SKV_OK;
+}
+
 int skv_prefill_attend(const void* q, int streams, int C, int Hq, int Hkv, const void* k_cache, const void* v_cache,
                        int L, int layer, int cap, int n0, float* out, int W, float* logits, int64_t lg_cap,
                        float* stats, void* stream) {

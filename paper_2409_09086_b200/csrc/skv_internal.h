@@ -160,10 +160,14 @@ struct PrefillArgs {
   float* lg;            // optional [S][W][Hq][lg_cap] f32 logits of the recorded rows
   int64_t lg_cap;
   float* st;            // optional [S][W][Hq][2] (max, sum)
+  unsigned long long* prof;  // optional per-CTA cycle counters [grid][16] (instrumentation)
+  int dbg;              // instrumentation: 1 skip softmax math, 2 skip MMAs
+  int* ovf;             // optional: += count of V elements saturated to fp16 (|v| > 65504)
 };
 
 cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const void* vbase, int64_t kv_rows,
                            const PrefillArgs& a, cudaStream_t st);
+void set_prefill_profile(unsigned long long* p);
 cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
                              int64_t lg_rs, int64_t st_rs, int64_t slot_stride, cudaStream_t st);
 // strides in 16-byte units; ss = stride of len / next_pos between streams

@@ -28,3 +28,20 @@ torch.cuda.synchronize()
 ms = a.elapsed_time(b) / reps
 flops = 4 * D * (C * n0 + C * (C + 1) / 2) * S * H
 print(f"prefill layer: {ms * 1e3:.1f} us, {flops / (ms * 1e-3) / 1e12:.1f} TFLOP/s useful")
+
+if os.environ.get("PROF"):
+    import numpy as np
+    nqt = (C + 127) // 128
+    grid = H * S * ((nqt + 1) // 2)
+    buf = torch.zeros((grid, 16), dtype=torch.int64, device="cuda")
+    _lib.check(lib.skv_prefill_profile(P(buf)))
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
+    torch.cuda.synchronize()
+    _lib.check(lib.skv_prefill_profile(None))
+    b = buf.cpu().numpy().astype(np.float64)
+    names = ["mma:k_full", "mma:pv_issue", "mma:v_full", "mma:p_full", "mma:total", "mma:s_issue",
+             "wg0:s_full", "wg0:o_done", "wg0:rescales", "wg0:o_final", "wg0:total",
+             "wg1:s_full", "wg1:o_done", "wg1:rescales", "wg1:o_final", "wg1:total"]
+    for i, n in enumerate(names):
+        if n != "-":
+            print(f"{n:14s} mean {b[:, i].mean():12.0f}  max {b[:, i].max():12.0f}")
