@@ -717,8 +717,33 @@ cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const At
   return cudaErrorInvalidValue;
 }
 
+// One row per stream, four columns per thread (fold_vec4).
+template <int MODE>
+__global__ void __launch_bounds__(256) fold_vec_kernel(const FoldArgs f, int Hq) {
+  __shared__ float stt[2 * 256];
+  const int s = blockIdx.y;
+  const float* sg = f.stats + s * f.st_ss;
+  for (int x = threadIdx.x; x < 2 * Hq; x += blockDim.x) stt[x] = sg[x];
+  __syncthreads();
+  const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (j0 < f.n)
+    fold_vec4<MODE>(f.logits + s * f.l_ss, f.l_hs, stt, f.rows + s * f.r_ss, j0, f.n, Hq,
+                    (float)(f.agg_div ? f.agg_div : Hq));
+  if (blockIdx.x == 0 && threadIdx.x == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
+}
+
 cudaError_t launch_fold(int streams, int pieces, const FoldArgs& f, int Hq, cudaStream_t st) {
   if (f.n <= 0) return cudaSuccess;
+  const bool vec = f.mode != 2 && Hq <= 256 && f.l_hs % 4 == 0 && f.l_ss % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(f.logits) & 15) == 0;
+  if (vec) {
+    dim3 grid((f.n + 1023) / 1024, streams);
+    if (f.mode == 1)
+      fold_vec_kernel<1><<<grid, 256, 0, st>>>(f, Hq);
+    else
+      fold_vec_kernel<0><<<grid, 256, 0, st>>>(f, Hq);
+    return cudaGetLastError();
+  }
   dim3 grid(pieces, streams);
   fold_kernel<<<grid, 128, 0, st>>>(f, Hq);
   return cudaGetLastError();

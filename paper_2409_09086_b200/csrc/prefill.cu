@@ -215,10 +215,14 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   uint64_t* o_final = bars + 15;      // [QT] last P_i V done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
-  const int nqt = (a.C + BM - 1) / BM, npairs = (nqt + 1) / 2;
-  // consecutive CTAs share one (stream, head): its K/V stream is read from L2
-  // by the other pairs
-  const int p = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  // Longest-first order: the block scheduler hands CTA k to the next free SM,
+  // so listing the two-tile pairs from the last (most keys) to the first, then
+  // the lone last tile of an odd tile count, is a greedy LPT schedule.
+  const int nqt = (a.C + BM - 1) / BM, npairs = (nqt + 1) / 2, full = nqt / 2;
+  const int nsh = gridDim.x / npairs;  // streams x heads
+  const int rank = blockIdx.x / nsh, sh = blockIdx.x - rank * nsh;
+  const int p = rank < full ? full - 1 - rank : full;
+  const int h = sh % a.Hq, s = sh / a.Hq;
   const int g = h / a.G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C, n0 = a.n0;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   // register accumulators, stored once at exit
   unsigned long long pacc0 = 0, pacc1 = 0, pacc2 = 0, pacc3 = 0, pacc4 = 0;
   if (a.prof && lane == 0 && (warp == 9 || warp == 0 || warp == 4)) {
-    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int cta = blockIdx.x;
     prof = a.prof + (size_t)cta * 16 + (warp == 9 ? 0 : warp == 0 ? 6 : 11);
     t_start = clock64();
   }
@@ -606,7 +610,7 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
     attr = true;
   }
   const int nqt = (a.C + pf::BM - 1) / pf::BM;
-  dim3 grid((nqt + 1) / 2, a.Hq, streams);
+  dim3 grid((nqt + 1) / 2 * a.Hq * streams);
   prefill_kernel<<<grid, pf::THREADS, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -649,27 +653,49 @@ __global__ void append_chunk_kernel(const uint4* __restrict__ kin, const uint4* 
 }
 
 // Folds the W recorded rows of a chunk into the window ring in one launch:
-// grid (pieces, S, W); row w has n_base + w + 1 columns and goes to ring slot
-// (slot0 + w) mod Wring.
-__global__ void fold_rows_kernel(const FoldArgs f, int Hq, int slot0, int Wring, int n_base, int64_t lg_rs,
-                                 int64_t st_rs, int64_t slot_stride) {
+// grid (column blocks, S, W); row w has n_base + w + 1 columns and goes to
+// ring slot (slot0 + w) mod Wring.  fold_vec4 (16-byte loads, four columns
+// per thread) when the logit rows are 16-byte aligned, fold_piece otherwise.
+template <int MODE>
+__global__ void __launch_bounds__(256) fold_rows_kernel(const FoldArgs f, int Hq, int slot0, int Wring, int n_base,
+                                                        int64_t lg_rs, int64_t st_rs, int64_t slot_stride, int vec) {
+  __shared__ float stt[2 * 256];
   const int w = blockIdx.z, s = blockIdx.y;
   const int slot = (slot0 + w) % Wring;
-  FoldArgs g = f;
-  g.logits = f.logits + w * lg_rs;
-  g.stats = f.stats + w * st_rs;
-  g.rows = f.rows + slot * slot_stride;
-  g.wlen = f.wlen ? f.wlen + slot : nullptr;
-  g.n = n_base + w + 1;
-  fold_piece(g, s, blockIdx.x, gridDim.x, Hq, threadIdx.x, blockDim.x);
+  const int n = n_base + w + 1;
+  const float* sg = f.stats + w * st_rs + s * f.st_ss;
+  for (int x = threadIdx.x; x < 2 * Hq; x += blockDim.x) stt[x] = sg[x];
+  __syncthreads();
+  if (vec) {
+    const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (j0 < n)
+      fold_vec4<MODE>(f.logits + w * lg_rs + s * f.l_ss, f.l_hs, stt, f.rows + slot * slot_stride + s * f.r_ss, j0,
+                      n, Hq, (float)(f.agg_div ? f.agg_div : Hq));
+  } else {
+    FoldArgs g = f;
+    g.logits = f.logits + w * lg_rs;
+    g.stats = f.stats + w * st_rs;
+    g.rows = f.rows + slot * slot_stride;
+    g.wlen = nullptr;
+    g.n = n;
+    fold_piece(g, s, blockIdx.x, gridDim.x, Hq, threadIdx.x, blockDim.x);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && f.wlen) f.wlen[slot + s * f.w_ss] = n;
 }
 
 cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
                              int64_t lg_rs, int64_t st_rs, int64_t slot_stride, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  const int pieces = std::max(1, std::min(32, (n_base + rows + 255) / 256));
-  dim3 grid(pieces, streams, rows);
-  fold_rows_kernel<<<grid, 256, 0, st>>>(f, Hq, slot0, Wring, n_base, lg_rs, st_rs, slot_stride);
+  if (Hq > 256 || f.mode == 2) return cudaErrorInvalidValue;
+  const int nmax = n_base + rows;
+  const bool vec = (f.l_hs % 4 == 0) && (lg_rs % 4 == 0) && (f.l_ss % 4 == 0) &&
+                   (reinterpret_cast<uintptr_t>(f.logits) & 15) == 0;
+  const int blocks = vec ? (nmax + 1023) / 1024 : std::max(1, std::min(32, (nmax + 255) / 256));
+  dim3 grid(blocks, streams, rows);
+  if (f.mode == 1)
+    fold_rows_kernel<1><<<grid, 256, 0, st>>>(f, Hq, slot0, Wring, n_base, lg_rs, st_rs, slot_stride, vec);
+  else
+    fold_rows_kernel<0><<<grid, 256, 0, st>>>(f, Hq, slot0, Wring, n_base, lg_rs, st_rs, slot_stride, vec);
   return cudaGetLastError();
 }
 

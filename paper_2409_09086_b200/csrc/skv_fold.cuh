@@ -46,4 +46,49 @@ __device__ __forceinline__ void fold_piece(const FoldArgs& f, int s, int piece, 
   if (piece == 0 && tid == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
 }
 
+// Throughput version for stand-alone fold launches: each thread owns four
+// consecutive columns (16-byte logit loads, four independent head-sum
+// chains), the per-head stats are staged in shared memory, and the heads are
+// walked in batches of eight loads in flight.  Same arithmetic per column as
+// fold_columns (sequential head order, expf, IEEE division) -- bit-identical.
+// MODE 0: mean over heads (divisor agg), MODE 1: max over heads.
+template <int MODE>
+__device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t l_hs, const float* __restrict__ stt,
+                                          float* __restrict__ row, int j0, int n, int Hq, float agg) {
+  float acc[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) acc[e] = MODE == 1 ? -INFINITY : 0.f;
+  if (j0 + 3 < n) {
+    for (int h0 = 0; h0 < Hq; h0 += 8) {
+      float4 x[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (h0 + b < Hq) x[b] = __ldcs(reinterpret_cast<const float4*>(lg + (int64_t)(h0 + b) * l_hs + j0));
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (h0 + b < Hq) {
+          const float M = stt[2 * (h0 + b)], L = stt[2 * (h0 + b) + 1];
+          const float v[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float p = __fdiv_rn(expf(__fsub_rn(v[e], M)), L);
+            acc[e] = MODE == 1 ? fmaxf(acc[e], p) : __fadd_rn(acc[e], p);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) row[j0 + e] = MODE == 1 ? acc[e] : __fdiv_rn(acc[e], agg);
+  } else {
+    for (int e = 0; e < 4 && j0 + e < n; ++e) {
+      float a = MODE == 1 ? -INFINITY : 0.f;
+      for (int h = 0; h < Hq; ++h) {
+        const float p = __fdiv_rn(expf(__fsub_rn(__ldcs(lg + (int64_t)h * l_hs + j0 + e), stt[2 * h])), stt[2 * h + 1]);
+        a = MODE == 1 ? fmaxf(a, p) : __fadd_rn(a, p);
+      }
+      row[j0 + e] = MODE == 1 ? a : __fdiv_rn(a, agg);
+    }
+  }
+}
+
 }  // namespace skv

@@ -1,0 +1,27 @@
+"""One config-2 image chunk through StreamEngine.prefill_chunk (append +
+tcgen05 prefill + window-row fold) on 2 layers, for an ncu launch list."""
+import os, sys
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+S, L, H, D, B, CI = 4, 2, 32, 128, 4096, 576
+eng = StreamEngine(EngineConfig(S, L, H, H, D, 2048, 2048, 0.01, 32, B + CI + 64, torch.bfloat16))
+g = torch.Generator(device="cuda").manual_seed(1)
+for s in range(S):
+    for layer in range(L):
+        kf, vf = eng.kv_full(s, layer)
+        kf[:, :B] = torch.randn((H, B, D), generator=g, device="cuda").to(torch.bfloat16)
+        vf[:, :B] = torch.randn((H, B, D), generator=g, device="cuda").to(torch.bfloat16)
+        eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
+q = torch.randn((S, CI, H, D), generator=g, device="cuda").to(torch.bfloat16)
+k = torch.randn((S, CI, H, D), generator=g, device="cuda").to(torch.bfloat16)
+v = torch.randn((S, CI, H, D), generator=g, device="cuda").to(torch.bfloat16)
+out = torch.empty((S, CI, H, D), dtype=torch.float32, device="cuda")
+for layer in range(L):
+    eng.prefill_chunk(layer, q, k, v, out, modality=1)
+torch.cuda.synchronize()
+eng.evict(-1)
+torch.cuda.synchronize()
+print("ok")
