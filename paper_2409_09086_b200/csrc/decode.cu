@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   const int c = blockIdx.x, P = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n_old + a.append;
+  constexpr bool getenv_dbg_t = true;  // TEMP instrumentation
   const int total = a.S * a.Hkv * a.nc;
 
   if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], globaltimer());
@@ -292,8 +293,14 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
           part[h * PW + D + 1] = L;
         }
       }
+      // publish the chunk partial: the segment's merge CTA starts once all
+      // nc chunks of the segment are counted
+      __threadfence();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&epi_empty[sl]);  // slot consumed
+      if (lane == 0) {
+        mbar_arrive(&epi_empty[sl]);  // slot consumed
+        atomicAdd(&a.counters[sigma], 1);
+      }
       // append: the new row and (once per stream) its metadata go to slot n_old
       if (a.append && j == a.nc - 1) {
         const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
@@ -397,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
         l_run[h] = 0.f;
       }
       fresh = false;
+      if (a.ctat && tid == 0 && getenv_dbg_t) a.ctat[8 * c + 5] = globaltimer();
     }
     const int rows = min(TT, n - ts);
     const unsigned char* ks = tiles + (2 * st) * TILE;
@@ -484,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+    if (a.ctat && tid == 0 && getenv_dbg_t && i == 0) a.ctat[8 * c + 4] = globaltimer();
     if (!chunk_end) continue;
 
     // ---- chunk done: hand the warp partials to the epilogue warp
@@ -529,8 +538,10 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   }
   if (a.ctat && tid == 0) {
     a.ctat[8 * c + 3] = globaltimer();
-    a.ctat[8 * c + 4] = k;
-    a.ctat[8 * c + 5] = t_epi_wait;
+    if (!getenv_dbg_t) {
+      a.ctat[8 * c + 4] = k;
+      a.ctat[8 * c + 5] = t_epi_wait;
+    }
   }
   // end marker for the epilogue warp
   {
@@ -545,10 +556,8 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   if (a.tstamp && tid == 0) atomicMax(&a.tstamp[1], globaltimer());
   if (a.ctat && tid == 0) a.ctat[8 * c + 2] = globaltimer();
   if (tid == 0) {
-    // the merge kernel counts finished CTAs; the last CTA out resets the ticket
-    // counter and the (already observed) flag of the previous merge
-    __threadfence();
-    atomicAdd(&a.sched[1], 1);
+    // the last CTA out resets the ticket counter and the (already observed)
+    // flag of the previous merge
     if (atomicAdd(&a.sched[2], 1) == P - 1) {
       a.sched[0] = 0;
       a.sched[2] = 0;
@@ -557,45 +566,52 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   }
 }
 
-// Segment merge (one CTA per (stream, kv-head) segment): combines the nc chunk
-// partials in chunk order (deterministic), writes the attention output and the
-// per-head (max, sum).  Launched right after the decode kernel with
-// programmatic dependent launch: its CTAs are tiny, become resident while the
-// decode kernel still runs, and let the next layer's decode CTAs launch and
-// prefetch as soon as decode CTAs retire.
+// Segment merge (one CTA per (stream, kv-head) segment, one thread per output
+// element): combines the nc chunk partials in chunk order (deterministic),
+// writes the attention output and the per-head (max, sum).  Launched right
+// after the decode kernel with programmatic dependent launch: its CTAs are
+// small, become resident while the decode kernel still runs, and let the next
+// layer's decode CTAs launch and prefetch as soon as decode CTAs retire.
+// Warp h computes head h's chunk weights and row sum; then thread (h, d)
+// accumulates its output element over the chunks with all partial loads of a
+// 16-chunk batch in flight (the previous 128-thread version staged every
+// partial through shared memory first, serialising the L2 round trips).
 template <int D, int G>
-__global__ void __launch_bounds__(128) merge_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(G * D) merge_kernel(const AttnArgs a) {
   constexpr int PW = D + 2;
-  extern __shared__ __align__(16) float msm[];  // [nc][G][PW] staged partials, then [G][nc] weights, [G] sums
+  extern __shared__ __align__(16) float msm[];  // [G][nc] weights, [G] sums
   griddep_launch();
   const int sigma = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // all decode CTAs resident before any merge CTA exists, so this spin completes
-  if (tid == 0)
-    while (ld_acquire(&a.sched[1]) < a.dctas) __nanosleep(64);
+  const int nc = a.nc;
+  // wait until every chunk partial of this segment is published (decode CTAs
+  // are all resident before any merge CTA exists, so the spin completes);
+  // segments finish in ticket order, so most merges overlap the streaming of
+  // later segments
+  if (tid == 0) {
+    while (ld_acquire(&a.counters[sigma]) < nc) __nanosleep(32);
+    a.counters[sigma] = 0;  // next launch: incremented only after this grid completes
+  }
   __syncthreads();
   const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
-  const float* seg = a.part + (int64_t)sigma * a.nc * G * PW;
-  const int nf = a.nc * G * PW;
-  float* stage = msm;
-  float* fac = msm + nf;
-  for (int x = tid; x < nf; x += 128) stage[x] = __ldcg(seg + x);
-  __syncthreads();
-  for (int h = warp; h < G; h += 4) {
+  const float* seg = a.part + (int64_t)sigma * nc * G * PW;
+  float* fac = msm;
+  if (warp < G) {
+    const int h = warp;
     float M = -INFINITY;
-    for (int jj = lane; jj < a.nc; jj += 32) M = fmaxf(M, stage[(jj * G + h) * PW + D]);
+    for (int jj = lane; jj < nc; jj += 32) M = fmaxf(M, __ldcg(seg + (jj * G + h) * PW + D));
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
     float L = 0.f;
-    for (int jj = lane; jj < a.nc; jj += 32) {
-      const float* pp = stage + (jj * G + h) * PW;
-      const float w = rescale(pp[D], M);
-      fac[h * a.nc + jj] = w;
-      L += w * pp[D + 1];
+    for (int jj = lane; jj < nc; jj += 32) {
+      const float* pp = seg + (jj * G + h) * PW;
+      const float w = rescale(__ldcg(pp + D), M);
+      fac[h * nc + jj] = w;
+      L += w * __ldcg(pp + D + 1);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
     if (lane == 0) {
-      fac[G * a.nc + h] = L;
+      fac[G * nc + h] = L;
       if (a.stats) {
         a.stats[s * a.st_ss + (g * G + h) * 2] = M;
         a.stats[s * a.st_ss + (g * G + h) * 2 + 1] = L;
@@ -603,18 +619,26 @@ __global__ void __launch_bounds__(128) merge_kernel(const AttnArgs a) {
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < G * D; idx += 128) {
-    const int h = idx / D, d = idx - h * D;
-    const float* pp = stage + h * PW + d;
+  {
+    const int h = tid / D, d = tid - h * D;
+    const float* pp = seg + h * PW + d;
+    const float* wf = fac + h * nc;
     float acc = 0.f;
-    for (int jj = 0; jj < a.nc; ++jj) acc = fmaf(fac[h * a.nc + jj], pp[jj * G * PW], acc);
-    a.out[s * a.o_ss + (int64_t)(g * G) * D + idx] = acc / fac[G * a.nc + h];
+    int jj = 0;
+    for (; jj + 16 <= nc; jj += 16) {
+      float x[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) x[u] = __ldcg(pp + (jj + u) * G * PW);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc = fmaf(wf[jj + u], x[u], acc);
+    }
+    for (; jj < nc; ++jj) acc = fmaf(wf[jj], __ldcg(pp + jj * G * PW), acc);
+    a.out[s * a.o_ss + (int64_t)(g * G) * D + tid] = acc / fac[G * nc + h];
   }
   __syncthreads();
   if (tid == 0) {  // the last merge CTA publishes completion and resets the decode counter
     __threadfence();
     if (atomicAdd(&a.sched[3], 1) == (int)gridDim.x - 1) {
-      a.sched[1] = 0;
       a.sched[3] = 0;
       __threadfence();
       asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.done_self), "r"(1) : "memory");
@@ -649,16 +673,16 @@ static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st)
   cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, D, G>, a);
   if (e != cudaSuccess) return e;
   // segment merge, also with programmatic dependent launch
-  const size_t msmem = ((size_t)a.nc * G * (D + 2) + (size_t)G * (a.nc + 1)) * sizeof(float);
+  const size_t msmem = (size_t)G * (a.nc + 1) * sizeof(float);
   static bool mattr = false;
   if (!mattr) {
-    e = cudaFuncSetAttribute(merge_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = cudaFuncSetAttribute(merge_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e != cudaSuccess) return e;
     mattr = true;
   }
-  if (msmem > 200 * 1024) return cudaErrorInvalidValue;
+  if (msmem > 64 * 1024) return cudaErrorInvalidValue;
   cfg.gridDim = dim3(a.S * a.Hkv);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(G * D);
   cfg.dynamicSmemBytes = msmem;
   return cudaLaunchKernelEx(&cfg, merge_kernel<D, G>, a);
 }

@@ -239,7 +239,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   chk(x->alloc(&x->part, 2 * x->part_floats * sizeof(float)));
   chk(x->alloc(&x->done, 64 * sizeof(int32_t)));
   chk(x->alloc(&x->sched, 64 * 4 * sizeof(int32_t)));
-  chk(x->alloc(&x->counters, (size_t)x->S * x->Hkv * sizeof(int32_t)));
+  // [4][S*Hkv]: per-launch slot (seq % 4) -- the merge of launch N+1 may be
+  // resident (PDL) before launch N's merge has reset its counters
+  chk(x->alloc(&x->counters, (size_t)4 * x->S * x->Hkv * sizeof(int32_t)));
   chk(x->alloc(&x->kept, SL * x->B * sizeof(int32_t)));
   chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
   chk(x->alloc(&x->scores, SL * x->cap * sizeof(float)));
@@ -339,7 +341,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   if (!stat) ch = chunk_tiles(x->G);
   const int nc = (nt + ch - 1) / ch;
   const int ctas = std::min(segs * nc, x->max_ctas);
-  if ((size_t)nc * x->G * (x->D + 2) * 4 > 190 * 1024) return fail(SKV_EINVAL, "capacity too large for the merge scratch");
+  if ((size_t)(nc + 1) * x->G * 4 > 64 * 1024) return fail(SKV_EINVAL, "capacity too large for the merge scratch");
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
   AttnArgs a{};
@@ -382,7 +384,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.stats = x->stats[par] + (int64_t)layer * x->Hq * 2;
   a.st_ss = SLstride * x->Hq * 2;
   a.part = x->part + (size_t)(seq & 1) * x->part_floats;
-  a.counters = x->counters;
+  a.counters = x->counters + (size_t)(seq % 4) * x->S * x->Hkv;
   a.pos = x->pos + (int64_t)layer * x->cap;
   a.modality = x->modality + (int64_t)layer * x->cap;
   a.round_id = x->round_id + (int64_t)layer * x->cap;
@@ -1046,8 +1048,8 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
     const size_t pcap = std::max(need, (size_t)(hcap + 1024) * 130);
     SKV_CK(cudaMalloc(&g_att.stats, hcap * 2 * sizeof(float)));
     SKV_CK(cudaMalloc(&g_att.part, pcap * sizeof(float)));
-    SKV_CK(cudaMalloc(&g_att.counters, hcap * sizeof(int32_t)));
-    SKV_CK(cudaMemset(g_att.counters, 0, hcap * sizeof(int32_t)));
+    SKV_CK(cudaMalloc(&g_att.counters, 4 * hcap * sizeof(int32_t)));
+    SKV_CK(cudaMemset(g_att.counters, 0, 4 * hcap * sizeof(int32_t)));
     if (!g_att.sched) {
       SKV_CK(cudaMalloc(&g_att.sched, 8 * sizeof(int32_t)));
       SKV_CK(cudaMemset(g_att.sched, 0, 8 * sizeof(int32_t)));
@@ -1081,7 +1083,8 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   a.l_hs = n;
   a.stats = g_att.stats;
   a.part = g_att.part;
-  a.counters = g_att.counters;
+  static int att_seq = 0;
+  a.counters = g_att.counters + (size_t)(att_seq++ % 4) * g_att.heads;
   cudaError_t e = launch_decode(SKV_DTYPE_F32, head_dim, 1, ctas, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
   FoldArgs f{};

@@ -61,7 +61,7 @@ struct AttnArgs {
   float* stats;         // [s][hq][2] (M, L) of this step
   int64_t st_ss;
   float* part;          // scratch [sigma*nc + j][G][D + 2]
-  int32_t* counters;    // [s*Hkv + g], zero between launches
+  int32_t* counters;    // [s*Hkv + g] chunk partials published; reset by the segment's merge CTA
   // appended token metadata
   int64_t* pos;         // pos[s*m_ss + t]
   int8_t* modality;

@@ -73,6 +73,10 @@ for slot in range(40, 44):
     rel = b[:, 1].min()
     st_, end, cend, pend = (b[:, 0] - rel) / 1e3, (b[:, 2] - rel) / 1e3, (b[:, 3] - rel) / 1e3, (b[:, 6] - rel) / 1e3
     chunks, ewait, taken = b[:, 4], b[:, 5] / 1e3, b[:, 7]
+    if os.environ.get("DBGT"):
+        qdone, t0done = (b[:, 5] - rel) / 1e3, (b[:, 4] - rel) / 1e3
+        qq = lambda x: " ".join(f"{np.percentile(x, p):.1f}" for p in (0, 10, 50, 90, 100))
+        print(f"   q loaded: {qq(qdone)}   tile0 done: {qq(t0done)}")
     q = lambda x: " ".join(f"{np.percentile(x, p):.1f}" for p in (0, 10, 50, 90, 100))
     print(f"launch {slot}: CTAs {len(b)} start(rel) [{st_.min():.1f},{st_.max():.1f}]")
     print(f"   producer end p0/10/50/90/100: {q(pend)}  tickets {q(taken)}")
