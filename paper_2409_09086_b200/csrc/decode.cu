@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
 
   if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], globaltimer());
   if (a.ctat && tid == 0) a.ctat[8 * c] = globaltimer();
-  if (c == 0 && tid == 0) {  // a stale flag from this slot's previous use must not leak to the next launch
+  if (c == 0 && tid == 0 && a.done_self) {  // a stale flag from this slot's previous use must not leak
     *a.done_self = 0;
     __threadfence();
   }
@@ -590,58 +590,75 @@ __global__ void __launch_bounds__(G * D) merge_kernel(const AttnArgs a) {
   if (tid == 0) {
     while (ld_acquire(&a.counters[sigma]) < nc) __nanosleep(32);
     a.counters[sigma] = 0;  // next launch: incremented only after this grid completes
+    if (a.mstamp && sigma == 0) a.mstamp[1] = globaltimer();
   }
   __syncthreads();
   const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
   const float* seg = a.part + (int64_t)sigma * nc * G * PW;
   float* fac = msm;
+  // One L2 round trip: every thread issues its output element's partial loads
+  // (first kPre chunks) and warp h its head's (m, l) loads together.
+  constexpr int kPre = 32;
+  const int h = tid / D, d = tid - h * D;
+  const float* pp = seg + h * PW + d;
+  float x[kPre];
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) x[u] = u < nc ? __ldcg(pp + u * G * PW) : 0.f;
   if (warp < G) {
-    const int h = warp;
-    float M = -INFINITY;
-    for (int jj = lane; jj < nc; jj += 32) M = fmaxf(M, __ldcg(seg + (jj * G + h) * PW + D));
+    const int hh = warp;
+    float mj[4], lj[4];  // nc <= 128 chunks per segment on this path (asserted by the host)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int jj = lane + 32 * k;
+      mj[k] = jj < nc ? __ldcg(seg + (jj * G + hh) * PW + D) : -INFINITY;
+      lj[k] = jj < nc ? __ldcg(seg + (jj * G + hh) * PW + D + 1) : 0.f;
+    }
+    float M = fmaxf(fmaxf(mj[0], mj[1]), fmaxf(mj[2], mj[3]));
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
     float L = 0.f;
-    for (int jj = lane; jj < nc; jj += 32) {
-      const float* pp = seg + (jj * G + h) * PW;
-      const float w = rescale(__ldcg(pp + D), M);
-      fac[h * nc + jj] = w;
-      L += w * __ldcg(pp + D + 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int jj = lane + 32 * k;
+      if (jj < nc) {
+        const float w = rescale(mj[k], M);
+        fac[hh * nc + jj] = w;
+        L += w * lj[k];
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
     if (lane == 0) {
-      fac[G * nc + h] = L;
+      fac[G * nc + hh] = L;
       if (a.stats) {
-        a.stats[s * a.st_ss + (g * G + h) * 2] = M;
-        a.stats[s * a.st_ss + (g * G + h) * 2 + 1] = L;
+        a.stats[s * a.st_ss + (g * G + hh) * 2] = M;
+        a.stats[s * a.st_ss + (g * G + hh) * 2 + 1] = L;
       }
     }
   }
   __syncthreads();
   {
-    const int h = tid / D, d = tid - h * D;
-    const float* pp = seg + h * PW + d;
     const float* wf = fac + h * nc;
     float acc = 0.f;
-    int jj = 0;
-    for (; jj + 16 <= nc; jj += 16) {
-      float x[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) x[u] = __ldcg(pp + (jj + u) * G * PW);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) acc = fmaf(wf[jj + u], x[u], acc);
-    }
-    for (; jj < nc; ++jj) acc = fmaf(wf[jj], __ldcg(pp + jj * G * PW), acc);
+    for (int u = 0; u < kPre; ++u)
+      if (u < nc) acc = fmaf(wf[u], x[u], acc);
+    for (int jj = kPre; jj < nc; ++jj) acc = fmaf(wf[jj], __ldcg(pp + jj * G * PW), acc);
     a.out[s * a.o_ss + (int64_t)(g * G) * D + tid] = acc / fac[G * nc + h];
   }
+  // Flag mode only: the last merge CTA publishes completion.  Otherwise the
+  // next launch's griddepcontrol.wait on this grid's completion is the
+  // release, and the fence + atomic chain (about three L2 round trips) is
+  // left off the critical path.
+  if (!a.done_self && !a.mstamp) return;
   __syncthreads();
-  if (tid == 0) {  // the last merge CTA publishes completion and resets the decode counter
+  if (tid == 0) {
     __threadfence();
     if (atomicAdd(&a.sched[3], 1) == (int)gridDim.x - 1) {
       a.sched[3] = 0;
       __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.done_self), "r"(1) : "memory");
+      if (a.done_self) asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(a.done_self), "r"(1) : "memory");
+      if (a.mstamp) a.mstamp[2] = globaltimer();
     }
   }
 }

@@ -296,7 +296,7 @@ int skv_timing(skv_ctx* x, int enable) {
     SKV_CK(cudaMemcpy(x->tbuf, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
     if (enable == 1 || enable == 3) x->tcount = 0;  // 2: clear values, keep slots (graph replays)
     if (enable == 3 && !x->cbuf) {
-      cudaError_t e = x->alloc(&x->cbuf, (size_t)64 * x->max_ctas * 8 * sizeof(unsigned long long));
+      cudaError_t e = x->alloc(&x->cbuf, (size_t)64 * (x->max_ctas + 1) * 8 * sizeof(unsigned long long));
       if (e != cudaSuccess) return cuda_fail(e, "timing buffer");
     }
   }
@@ -307,7 +307,7 @@ int skv_timing(skv_ctx* x, int enable) {
 int skv_timing_cta(skv_ctx* x, int slot, uint64_t* out) {
   if (!x || !out || !x->cbuf || slot < 0 || slot >= 64) return fail(SKV_EINVAL, "no per-CTA timing");
   SKV_CK(cudaDeviceSynchronize());
-  SKV_CK(cudaMemcpy(out, x->cbuf + (size_t)slot * x->max_ctas * 8, (size_t)x->max_ctas * 8 * sizeof(uint64_t),
+  SKV_CK(cudaMemcpy(out, x->cbuf + (size_t)slot * (x->max_ctas + 1) * 8, (size_t)(x->max_ctas + 1) * 8 * sizeof(uint64_t),
                     cudaMemcpyDeviceToHost));
   return x->max_ctas;
 }
@@ -341,7 +341,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   if (!stat) ch = chunk_tiles(x->G);
   const int nc = (nt + ch - 1) / ch;
   const int ctas = std::min(segs * nc, x->max_ctas);
-  if ((size_t)(nc + 1) * x->G * 4 > 64 * 1024) return fail(SKV_EINVAL, "capacity too large for the merge scratch");
+  if (nc > 128) return fail(SKV_EINVAL, "capacity too large for the segment merge (more than 128 chunks)");
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
   AttnArgs a{};
@@ -358,7 +358,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   const int seq = x->launch_seq++;
   a.sched = x->sched + 4 * (seq % 64);
   a.prefetch = x->last_layer >= 0 && x->last_layer != layer;
-  a.done_self = x->done + (seq % 64);
+  a.done_self = use_flags() ? x->done + (seq % 64) : nullptr;
   a.done_prev = (a.prefetch && use_flags()) ? x->done + ((seq + 63) % 64) : nullptr;
   a.dctas = ctas;
   a.scale = x->scale;
@@ -395,7 +395,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.pos_in = pos_dev;
   a.round_value = x->round_value[layer];
   if (x->timing) {
-    if (x->cbuf) a.ctat = x->cbuf + (size_t)(x->tcount % 64) * x->max_ctas * 8;
+    if (x->cbuf) {
+      a.ctat = x->cbuf + (size_t)(x->tcount % 64) * (x->max_ctas + 1) * 8;
+      a.mstamp = a.ctat + (size_t)x->max_ctas * 8;  // extra row: [0, first merge start, last merge end]
+    }
     a.tstamp = x->tbuf + 2 * (x->tcount++ % 8192);
   }
   // fold of the pending row (previous recorded step) into its ring slot
@@ -1033,7 +1036,8 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   if (head_dim != 64 && head_dim != 128) return fail(SKV_EINVAL, "device attend needs head_dim 64 or 128");
   cudaStream_t st = as_stream(stream);
   const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
-  const int nc = (nt + chunk_tiles(1) - 1) / chunk_tiles(1);
+  const int ach = std::max(chunk_tiles(1), (nt + 127) / 128);  // at most 128 chunks (segment merge)
+  const int nc = (nt + ach - 1) / ach;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1063,11 +1067,11 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   a.n_old = n;
   a.append = 0;
   a.nt = nt;
-  a.ch = chunk_tiles(1);
+  a.ch = ach;
   a.nc = nc;
   a.S = 1;
   a.sched = g_att.sched;
-  a.done_self = g_att.sched + 4;
+  a.done_self = nullptr;
   a.dctas = ctas;
   a.prefetch = 0;
   a.scale = (float)(1.0 / std::sqrt((double)head_dim));

@@ -40,7 +40,7 @@ struct AttnArgs {
   int S;                // streams
   int stat;             // 1: static schedule, CTA c runs chunk c (grid = S*Hkv*nc)
   int32_t* sched;       // [4] ticket, grid-barrier and exit counters (zero between launches)
-  int32_t* done_self;   // set to 1 by the merge kernel when this launch's outputs are complete
+  int32_t* done_self;   // flag mode (else null): set to 1 by the merge kernel when this launch's outputs are complete
   const int32_t* done_prev;  // flag of the preceding merge (null: use griddepcontrol.wait)
   int dctas;            // decode grid size (the merge waits for this many finished CTAs)
   int prefetch;         // producer may stream cached K/V before griddepcontrol.wait
@@ -75,6 +75,7 @@ struct AttnArgs {
   FoldArgs fold;        // previous step's row (fold.n == 0: none)
   unsigned long long* tstamp;  // optional [2]: min CTA start / max CTA end (%globaltimer ns)
   unsigned long long* ctat;    // optional [P][8]: per-CTA timeline (instrumentation)
+  unsigned long long* mstamp;  // optional [8]: merge timeline (instrumentation)
 };
 
 cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st);

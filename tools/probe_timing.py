@@ -66,11 +66,15 @@ t0 = None
 for slot in range(40, 44):
     buf = np.zeros((4096, 8), dtype=np.uint64)
     P = eng.lib.skv_timing_cta(eng._h, slot, buf.ctypes.data_as(ctypes.c_void_p))
+    mrow = buf[P].astype(np.int64)
     b = buf[:P].astype(np.int64)
     b = b[b[:, 0] > 0]
     if t0 is None:
         t0 = b[:, 0].min()
     rel = b[:, 1].min()
+    if slot > 40:
+        print(f"   release - previous release: {(rel - prev_rel) / 1e3:.1f} us; - previous last merge end {(rel - prev_mend) / 1e3:.1f} us")
+    prev_rel, prev_mend = rel, mrow[2]
     st_, end, cend, pend = (b[:, 0] - rel) / 1e3, (b[:, 2] - rel) / 1e3, (b[:, 3] - rel) / 1e3, (b[:, 6] - rel) / 1e3
     chunks, ewait, taken = b[:, 4], b[:, 5] / 1e3, b[:, 7]
     if os.environ.get("DBGT"):
@@ -81,7 +85,7 @@ for slot in range(40, 44):
     print(f"launch {slot}: CTAs {len(b)} start(rel) [{st_.min():.1f},{st_.max():.1f}]")
     print(f"   producer end p0/10/50/90/100: {q(pend)}  tickets {q(taken)}")
     print(f"   consumer end: {q(cend)}  chunks {q(chunks)}  epi-wait us {q(ewait)}")
-    print(f"   epilogue end: {q(end)}")
+    print(f"   epilogue end: {q(end)}   merge seg0 start {(mrow[1] - rel) / 1e3:.1f}  last merge end {(mrow[2] - rel) / 1e3:.1f}")
     slow = np.argsort(end)[-3:]
     for j in slow:
         print(f"   slow CTA: start {st_[j]:.1f} prod_end {pend[j]:.1f} cons_end {cend[j]:.1f} epi_end {end[j]:.1f} chunks {chunks[j]} taken {taken[j]} epi_wait {ewait[j]:.1f}")
