@@ -265,10 +265,11 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       const float* wo = wl + NW * G;
       const int sigma = u / a.nc, j = u - sigma * a.nc;
       const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
-      // merge the consumer warps' partials of this chunk
+      // merge the consumer warps' partials of this chunk (static schedule:
+      // the consumers already did)
       float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
+      for (int h = 0; h < (a.stat ? 0 : G); ++h) {
         // lane w < NW holds warp w's (m, l); rescale factors computed once per head
         const float mw = lane < NW ? wm[lane * G + h] : -INFINITY;
         float M = mw;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&epi_empty[sl]);  // slot consumed
-        atomicAdd(&a.counters[sigma], 1);
+        if (!a.stat) atomicAdd(&a.counters[sigma], 1);
       }
       // append: the new row and (once per stream) its metadata go to slot n_old
       if (a.append && j == a.nc - 1) {
@@ -531,6 +532,41 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       }
     }
     if (warp == 0 && lane == 0) reinterpret_cast<int*>(slot)[0] = u;
+    if (a.stat) {
+      // Static schedule (one chunk per CTA, latency-bound small batches): all
+      // consumer threads merge the warp partials instead of the single
+      // epilogue warp (same arithmetic order), then publish the chunk.
+      consumers_sync();
+      const int j = u - sigma * a.nc;
+      float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
+      for (int idx = tid; idx < G * D; idx += kCT) {
+        const int h = idx / D, d = idx - h * D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w * G + h]);
+        float f[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) f[w] = rescale(wm[w * G + h], M);
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc = fmaf(f[w], wo[(w * G + h) * D + d], acc);
+        part[h * PW + d] = acc;
+        if (d == 0) {  // the epilogue warp's xor-tree order over the NW warps
+          float x[NW];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) x[w] = f[w] * wl[w * G + h];
+#pragma unroll
+          for (int off = NW / 2; off > 0; off >>= 1)
+#pragma unroll
+            for (int w = 0; w < off; ++w) x[w] = x[w] + x[w + off];
+          part[h * PW + D] = M;
+          part[h * PW + D + 1] = x[0];
+        }
+      }
+      __threadfence();
+      consumers_sync();
+      if (tid == 0) atomicAdd(&a.counters[sigma], 1);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&epi_full[sl]);
     ++k;

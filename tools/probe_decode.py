@@ -24,7 +24,7 @@ k = torch.randn((L, S, Hkv, D), generator=g, device="cuda").to(torch.bfloat16)
 v = torch.randn((L, S, Hkv, D), generator=g, device="cuda").to(torch.bfloat16)
 out = torch.empty((L, S, H, D), dtype=torch.float32, device="cuda")
 for _ in range(steps):
-    eng.decode_step(q, k, v, out)
+    eng.decode_step(q, k, v, out, record=bool(int(os.environ.get("RECORD", "1"))))
 torch.cuda.synchronize()
 eng.evict(-1)
 torch.cuda.synchronize()
