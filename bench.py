@@ -40,6 +40,11 @@ sys.path.insert(0, ROOT)
 METRIC = "decode tokens/sec per stream-batch & \u00b5s/step (attn+score+evict); HBM GB/s vs peak"
 
 WORKLOADS = {
+    "cfg0": dict(layers=1, heads_q=8, heads_kv=8, head_dim=64, streams=1, recent=128, relevant=128, window=32,
+                 bias=0.01, period=64, spike_prob=4 / 4096, spike_gain=6.0, shard="streams", scaling="weak",
+                 dtype="f32",
+                 desc="cfg0: CPU-runnable toy, 1L x 8H x 64, fp32, batch 1, budget 128+128, W=32, b=0.01, E=64 "
+                      "(L2-resident, launch-bound: the parity config, reported in us/step)"),
     "cfg1": dict(layers=32, heads_q=32, heads_kv=32, head_dim=128, streams=8, recent=1024, relevant=1024, window=32,
                  bias=0.01, period=128, spike_prob=0.01, spike_gain=4.0, shard="streams", scaling="weak",
                  desc="cfg1: Llama-2-7B-shaped decode, 32L x 32H x 128, bf16, 8 streams/GPU, budget 1024+1024, "
@@ -136,9 +141,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- accounting --
+def _elt(c) -> int:
+    return 4 if c.get("dtype") == "f32" else 2
+
+
 def period_bytes(c, hkv: int, moved_rows_per_sl: float) -> dict:
     """Algorithmic HBM bytes of one period, per (stream, layer)."""
-    s = 2
+    s = _elt(c)
     B, E, D, W, l = c["recent"] + c["relevant"], c["period"], c["head_dim"], c["window"], c["recent"]
     hq = hkv * (c["heads_q"] // c["heads_kv"])
     kv = sum(2 * (B + j) * hkv * D * s for j in range(1, E + 1))
@@ -151,7 +160,7 @@ def period_bytes(c, hkv: int, moved_rows_per_sl: float) -> dict:
 
 def decode_launch_bytes(c, hkv: int, n: float, streams: int) -> float:
     """Algorithmic bytes of one decode launch (one layer, all resident streams, cache length n)."""
-    s = 2
+    s = _elt(c)
     hq = hkv * (c["heads_q"] // c["heads_kv"])
     D = c["head_dim"]
     return streams * (2 * n * hkv * D * s + hq * D * s + 2 * hkv * D * s + hq * D * 4)
@@ -193,22 +202,23 @@ def run_gpu(args, rank: int, world: int):
         hkv, hq = HKV, HQ
         S = c["streams"] if c["scaling"] == "weak" else c["streams"] // world
     # streams resident at once (config 4 at large budgets runs in waves)
-    per_stream = 2 * L * hkv * (B + E) * D * 2 * 1.06
+    dt = torch.float32 if c.get("dtype") == "f32" else torch.bfloat16
+    per_stream = 2 * L * hkv * (B + E) * D * _elt(c) * 1.06
     free = torch.cuda.mem_get_info(dev)[0] - (12 << 30)
     resident = max(1, min(S, int(free // per_stream)))
     waves = -(-S // resident)
-    eng = StreamEngine(EngineConfig(resident, L, hq, hkv, D, l, r, c["bias"], W, B + E, torch.bfloat16,
+    eng = StreamEngine(EngineConfig(resident, L, hq, hkv, D, l, r, c["bias"], W, B + E, dt,
                                     heads_q_total=HQ if c["shard"] == "heads" else 0))
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def randn(shape):
-        return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(dt)
 
     def spiked_keys(shape_lead):
         k = torch.randn((*shape_lead, hkv, D), generator=g, device=dev, dtype=torch.float32)
         spikes = torch.rand(shape_lead, generator=g, device=dev) < c["spike_prob"]
         k[spikes] *= c["spike_gain"]
-        return k.to(torch.bfloat16)
+        return k.to(dt)
 
     # steady state: every (stream, layer) holds a full budget of B tokens
     for s in range(resident):
@@ -216,7 +226,7 @@ def run_gpu(args, rank: int, world: int):
             kf, vf = eng.kv_full(s, layer)
             kk = torch.randn((hkv, B, D), generator=g, device=dev)
             kk[:, torch.rand(B, generator=g, device=dev) < c["spike_prob"]] *= c["spike_gain"]
-            kf[:, :B] = kk.to(torch.bfloat16)
+            kf[:, :B] = kk.to(dt)
             vf[:, :B] = randn((hkv, B, D))
             eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
     # distinct inputs for up to E steps (fewer when many streams are resident), reused cyclically
@@ -368,13 +378,15 @@ def run_gpu(args, rank: int, world: int):
         "higher_is_better": True,
         "scaling": c["scaling"],
         "vs_baseline": None,
-        "dtype": "bf16",
+        "dtype": c.get("dtype", "bf16"),
         "data": "synthetic (seeded N(0,1) q/k/v, key spikes; random cache at budget)",
         "config": {"workload": c["desc"], "streams_per_gpu": S, "resident_streams": resident, "waves": waves,
                    "global_streams": job_streams, "layers": L, "heads_q_per_gpu": hq, "heads_kv_per_gpu": hkv,
                    "head_dim": D, "budget": B, "window": W, "period": E,
                    "step": f"one eviction period: {E} decode tokens x {L} layers x streams + 1 all-layer eviction",
-                   "l2": "inputs larger than L2 (the whole KV cache is streamed every token)",
+                   "l2": ("L2-resident by construction (sub-MB working set, not flushed): launch-bound parity config"
+                          if c.get("dtype") == "f32" else
+                          "inputs larger than L2 (the whole KV cache is streamed every token)"),
                    "graph": "one CUDA graph per period, per-layer launches" if use_graph else
                             "eager per-token launches (NCCL all-reduce at eviction)",
                    "parallelism": (f"kv-heads sharded x{world} (1 all-reduce of window scores per eviction)"

@@ -38,6 +38,13 @@ extern "C" {
 #define SKV_DTYPE_F32 0
 #define SKV_DTYPE_BF16 1
 
+/* Eviction policy: the Session's policy switch (engine.py:296-307). */
+#define SKV_POLICY_INF_MLLM 0     /* inf_mllm_decide, policies.py:184-201 (the hot path) */
+#define SKV_POLICY_WINDOW 1       /* sliding_window_decide(n, budget), policies.py:204-213 */
+#define SKV_POLICY_SINK_RECENT 2  /* sink_recent_decide(n, sink_count, budget), policies.py:216-231 */
+#define SKV_POLICY_HEAVY_HITTER 3 /* heavy_hitter_accumulate/decide, policies.py:234-256 */
+#define SKV_POLICY_NONE 4         /* keep everything (EvictionDecision.keep_all, engine.py:298-299) */
+
 #define SKV_AGG_MEAN 0 /* aggregate_heads(.., "mean"), policies.py:261-262 */
 #define SKV_AGG_MAX 1  /* aggregate_heads(.., "max"),  policies.py:263-264 */
 
@@ -60,6 +67,8 @@ typedef struct skv_config {
   int32_t heads_q_total;   /* 0, or the query heads of all head shards: a shard's window rows are
                               its heads' probability sums / heads_q_total, so the shards' rows add
                               up to the reference head mean */
+  int32_t policy;          /* SKV_POLICY_* (zero-initialised configs get the Inf-MLLM policy) */
+  int32_t sink_count;      /* s  (PolicyConfig.sink_count) for SKV_POLICY_SINK_RECENT */
 } skv_config;
 
 typedef struct skv_ctx skv_ctx;
@@ -179,6 +188,19 @@ int skv_prefill_attend(const void* q_dev, int streams, int C, int heads_q, int h
 /* top_k_indices(scores, k) (policies.py:165-181) on device: ascending indices of
  * the k largest, ties to the larger index.  out_dev receives min(k, n) int64. */
 int skv_top_k(const float* scores_dev, int n, int k, int64_t* out_dev, void* stream);
+/* The Session's comparison baselines (engine.py:296-307), device-side:
+ *   SKV_POLICY_WINDOW:       sliding_window_decide(n, budget=recent_len)   policies.py:204-213
+ *   SKV_POLICY_SINK_RECENT:  sink_recent_decide(n, sink_count, recent_len + relevant_budget)
+ *                                                                           policies.py:216-231
+ *   SKV_POLICY_HEAVY_HITTER: heavy_hitter_decide(acc[n], n, relevant_budget, recent_len)
+ *                                                                           policies.py:246-256
+ * kept_dev receives the ascending kept set (sinks/relevant first); returns its
+ * length, or a negative SKV_* code.  scores_dev (>= n floats) is scratch for the
+ * heavy hitter. */
+int skv_policy_decide(int policy, const float* acc_dev, int n, int recent_len, int relevant_budget, int sink_count,
+                      int64_t* kept_dev, float* scores_dev, void* stream);
+/* heavy_hitter_accumulate (policies.py:234-243): out[j] = row[j] + acc[j] (j < na), row[j] otherwise. */
+int skv_hh_accumulate(const float* acc_dev, int na, const float* row_dev, int n, float* out_dev, void* stream);
 /* inf_mllm_decide over a device window: rows_dev [m][row_stride] f32 oldest
  * first, lens_dev [m] int32.  kept_dev [min(n, r+l)] int64; scores_dev optional
  * [n-l] f32 biased scores.  Returns the kept count (>= 0) or an error. */

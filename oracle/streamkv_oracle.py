@@ -187,6 +187,58 @@ def saddle_decide(window: RowWindow, n: int, cfg: PolicyConfig) -> Decision:
     return Decision(relevant=relevant, recent=recent, kept=np.concatenate([relevant, recent]))
 
 
+# --------------------------------------------------------------------------
+# comparison baselines: the Session's other policies
+# --------------------------------------------------------------------------
+
+
+def recent_only(n: int, budget: int) -> Decision:
+    """``sliding_window_decide`` (policies.py:204-213): the last ``budget``."""
+    if budget < 1:
+        raise ValueError("budget must be >= 1")
+    k = min(budget, n)
+    recent = np.arange(n - k, n, dtype=I64)
+    return Decision(relevant=np.empty(0, dtype=I64), recent=recent, kept=recent)
+
+
+def sinks_plus_recent(n: int, s: int, budget: int) -> Decision:
+    """``sink_recent_decide`` (policies.py:216-231): first ``s`` + last ``budget - s``."""
+    if not budget > s >= 0:
+        raise ValueError("require budget > sink_count >= 0")
+    if n <= budget:
+        return Decision.everything(n, min(budget - s, n))
+    sinks = np.arange(min(s, n), dtype=I64)
+    recent = np.arange(n - (budget - s), n, dtype=I64)
+    keep_sinks = sinks[sinks < recent[0]] if recent.size else sinks
+    return Decision(relevant=keep_sinks, recent=recent, kept=np.concatenate([keep_sinks, recent]))
+
+
+def mass_accumulate(acc: np.ndarray, new_row) -> np.ndarray:
+    """``heavy_hitter_accumulate`` (policies.py:234-243): row + acc, padded."""
+    a = np.asarray(acc, dtype=F32)
+    row = np.asarray(new_row, dtype=F32)
+    if a.size > row.size:
+        raise ValueError("accumulator longer than the new row")
+    out = row.copy()
+    out[: a.size] += a
+    return out
+
+
+def mass_decide(acc: np.ndarray, n: int, r: int, l: int) -> Decision:
+    """``heavy_hitter_decide`` (policies.py:246-256): top-r accumulated mass + last l."""
+    a = np.asarray(acc, dtype=F32)
+    if a.size != n:
+        raise ValueError(f"accumulator length {a.size} != n={n}")
+    if n <= r + l:
+        return Decision.everything(n, l)
+    relevant = top_k_newer(a[: n - l], r)
+    recent = np.arange(n - l, n, dtype=I64)
+    return Decision(relevant=relevant, recent=recent, kept=np.concatenate([relevant, recent]))
+
+
+POLICIES = ("inf_mllm", "window", "sink_recent", "heavy_hitter", "none")
+
+
 def head_mean(per_head: np.ndarray, how: str = "mean") -> np.ndarray:
     """``aggregate_heads`` (policies.py:259-265)."""
     if how == "mean":
@@ -312,9 +364,14 @@ class StreamOracle:
     """
 
     def __init__(self, streams: int, layers: int, heads_q: int, heads_kv: int, head_dim: int,
-                 cfg: PolicyConfig, window: Optional[int] = None):
+                 cfg: PolicyConfig, window: Optional[int] = None, policy: str = "inf_mllm"):
         if heads_q % heads_kv:
             raise ValueError("heads_q must be a multiple of heads_kv")
+        if policy not in POLICIES:
+            raise ValueError(f"unknown policy {policy!r}")
+        self.policy = policy
+        # heavy-hitter accumulators, one per (stream, layer) (engine.py:274)
+        self.acc = [[np.zeros(0, dtype=F32) for _ in range(layers)] for _ in range(streams)]
         self.S, self.L, self.Hq, self.Hkv, self.D = streams, layers, heads_q, heads_kv, head_dim
         self.group = heads_q // heads_kv
         self.cfg = cfg
@@ -350,6 +407,7 @@ class StreamOracle:
             probs, o = attend_heads(keys, vals, np.asarray(q[s], F32), self.scale)
             row = head_mean(probs, self.cfg.head_agg)
             self.win[s][layer].push(row)
+            self.acc[s][layer] = mass_accumulate(self.acc[s][layer], row)
             out[s] = o
             rows.append(row)
         return out, rows
@@ -368,7 +426,17 @@ class StreamOracle:
         return np.stack(outs)
 
     def decide(self, s: int, layer: int) -> Decision:
-        return saddle_decide(self.win[s][layer], self.kv[s][layer].n, self.cfg)
+        """The Session's policy switch ``_decide`` (engine.py:293-307)."""
+        n, cfg = self.kv[s][layer].n, self.cfg
+        if self.policy == "none":
+            return Decision.everything(n, min(cfg.recent_len, n))
+        if self.policy == "window":
+            return recent_only(n, cfg.budget)
+        if self.policy == "sink_recent":
+            return sinks_plus_recent(n, cfg.sink_count, cfg.budget)
+        if self.policy == "heavy_hitter":
+            return mass_decide(self.acc[s][layer], n, cfg.relevant_budget, cfg.recent_len)
+        return saddle_decide(self.win[s][layer], n, cfg)
 
     def scores(self, s: int, layer: int) -> np.ndarray:
         return biased_scores(self.win[s][layer], self.kv[s][layer].n, self.cfg)
@@ -379,6 +447,7 @@ class StreamOracle:
         if kept.size != self.kv[s][layer].n:
             self.kv[s][layer].gather_keep(kept)
             self.win[s][layer].remap(kept)
+            self.acc[s][layer] = self.acc[s][layer][kept]  # engine.py:335
 
     def evict(self):
         """Decide + apply for every (stream, layer); returns kept[s][l]."""

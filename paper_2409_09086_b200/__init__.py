@@ -4,7 +4,9 @@ Drop-in for the hot-path API of the reference ``streamkv`` package
 (/root/reference/pkg/src/streamkv/__init__.py:3-32): ``KvCache``,
 ``AttentionWindow``, ``PolicyConfig``, ``EvictionDecision``,
 ``window_mean_scores``, ``bias_vector``, ``top_k_indices``, ``inf_mllm_decide``,
-``aggregate_heads`` and ``attend`` (Session._attend), plus the batched
+``aggregate_heads`` and ``attend`` (Session._attend), the comparison baselines
+``sliding_window_decide``, ``sink_recent_decide``, ``heavy_hitter_accumulate``
+and ``heavy_hitter_decide``, plus the batched
 ``StreamEngine`` that runs decode + score + evict for many streams through
 libstreamkv_b200.so.  No CPU fallback: everything computes on the GPU.
 """
@@ -18,7 +20,11 @@ from .policies import (
     PolicyConfig,
     aggregate_heads,
     bias_vector,
+    heavy_hitter_accumulate,
+    heavy_hitter_decide,
     inf_mllm_decide,
+    sink_recent_decide,
+    sliding_window_decide,
     top_k_indices,
     window_mean_scores,
 )

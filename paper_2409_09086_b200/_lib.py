@@ -25,6 +25,9 @@ DTYPE_BF16 = 1
 AGG_MEAN = 0
 AGG_MAX = 1
 
+# eviction policies (engine.py:296-307)
+POLICIES = {"inf_mllm": 0, "window": 1, "sink_recent": 2, "heavy_hitter": 3, "none": 4}
+
 
 class SkvConfig(ctypes.Structure):
     _fields_ = [
@@ -41,6 +44,8 @@ class SkvConfig(ctypes.Structure):
         ("capacity", ctypes.c_int32),
         ("head_agg", ctypes.c_int32),
         ("heads_q_total", ctypes.c_int32),
+        ("policy", ctypes.c_int32),
+        ("sink_count", ctypes.c_int32),
     ]
 
 
@@ -79,6 +84,8 @@ SIGNATURES = {
     "skv_prefill_attend": (_I, [_P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _P, _I64, _P, _P]),
     "skv_top_k": (_I, [_P, _I, _I, _P, _P]),
     "skv_decide": (_I, [_P, _I, _P, _I, _I, _I, _I, _F, _P, _P, _P]),
+    "skv_policy_decide": (_I, [_I, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "skv_hh_accumulate": (_I, [_P, _I, _P, _I, _P, _P]),
     "skv_window_scores": (_I, [_P, _I, _P, _I, _I, _I, _F, _I, _P, _P]),
     "skv_gather_rows": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "skv_attend": (_I, [_P, _P, _I, _I, _I, _I64, _P, _P, _P, _P]),

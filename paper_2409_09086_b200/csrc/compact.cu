@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kCmpThreads) compact_kernel(const CompactArgs 
   }
   // metadata + window rows + lengths
   if (first < a.m) {
+    if (a.acc) gather_elems<float>(a.acc + b * a.acc_bs, a, b, first, a.m);  // accumulators[kept] (engine.py:335)
     if (a.pos) gather_elems<int64_t>(a.pos + b * a.m_bs, a, b, first, a.m);
     if (a.modality) gather_elems<int8_t>(a.modality + b * a.m_bs, a, b, first, a.m);
     if (a.round_id) gather_elems<int32_t>(a.round_id + b * a.m_bs, a, b, first, a.m);

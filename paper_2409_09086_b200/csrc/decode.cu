@@ -151,7 +151,6 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     mbar_fence_init();
   }
   __syncthreads();
-  griddep_launch();
   // Everything that depends on the previous launch (the preceding layer's
   // merge: q, in a real model, and the shared scratch) waits here.
   auto wait_prev = [&]() {
@@ -336,6 +335,11 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   } else {
     griddep_wait();
   }
+  // Let this launch's merge kernel be scheduled only once this CTA is
+  // released: merges (and the decode launches they release early) then run at
+  // most one launch ahead, which bounds the per-launch counter ring (a tiny
+  // grid would otherwise let a whole captured graph's launches go resident).
+  if (tid == 0) griddep_launch();
   if (a.ctat && tid == 0) a.ctat[8 * c + 1] = globaltimer();
   // Lane layout: LPR lanes read one cached row (16 B each); a warp reads RPW
   // rows per shared-memory load and ITERS loads per tile.  Partial dot products
@@ -805,7 +809,7 @@ __global__ void __launch_bounds__(256) fold_vec_kernel(const FoldArgs f, int Hq)
   const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (j0 < f.n)
     fold_vec4<MODE>(f.logits + s * f.l_ss, f.l_hs, stt, f.rows + s * f.r_ss, j0, f.n, Hq,
-                    (float)(f.agg_div ? f.agg_div : Hq));
+                    (float)(f.agg_div ? f.agg_div : Hq), f.accum);
   if (blockIdx.x == 0 && threadIdx.x == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
 }
 

@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(256) fold_rows_kernel(const FoldArgs f, int Hq
     const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (j0 < n)
       fold_vec4<MODE>(f.logits + w * lg_rs + s * f.l_ss, f.l_hs, stt, f.rows + slot * slot_stride + s * f.r_ss, j0,
-                      n, Hq, (float)(f.agg_div ? f.agg_div : Hq));
+                      n, Hq, (float)(f.agg_div ? f.agg_div : Hq), f.accum);
   } else {
     FoldArgs g = f;
     g.logits = f.logits + w * lg_rs;

@@ -13,6 +13,8 @@
 //     kept = relevant ++ [n-l, n).
 // It also emits what compaction needs: the first moved index (kept[i] != i) and
 // the window row lengths after AttentionWindow.remap (policies.py:117-124).
+#include <algorithm>
+
 #include "skv_common.cuh"
 #include "skv_internal.h"
 
@@ -174,41 +176,60 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
 
   const bool keep_all = !a.scores_only && n <= r + l;
   if (!keep_all) {
-    // ---- window-mean scores (+ bias)
     const int cols = n - l;
-    const float d = __fdiv_rn(a.bias, (float)cols);
-    const float negd = -d;
-    const float inv_m = (float)a.count;
     float* sc = a.scores + b * a.s_bs;
-    const float* rows = a.rows + b * a.r_bs;
-    const float* sin = a.scores_in ? a.scores_in + b * a.si_bs : nullptr;
-    for (int c = tid; c < cols; c += blockDim.x) {
-      float v;
-      if (sin) {
-        v = sin[c];
-      } else {
-        float acc = 0.f;
-        for (int k = 0; k < a.count; ++k)
-          if (c < len_of[k]) acc = __fadd_rn(acc, rows[(int64_t)slot_of[k] * a.row_stride + c]);
-        v = __fdiv_rn(acc, inv_m);
+    if (a.policy == 1 || a.policy == 2) {
+      // sliding_window_decide / sink_recent_decide (policies.py:204-231):
+      // kept = [0, s) ++ [n - (B - s), n), s = 0 for the sliding window
+      const int B = r + l, s0 = a.policy == 2 ? a.sink : 0;
+      for (int i = tid; i < B; i += blockDim.x) {
+        const int v = i < s0 ? i : n - B + i;
+        if (k32) k32[i] = v;
+        if (k64) k64[i] = v;
       }
-      if (a.apply_bias) v = __fadd_rn(v, __fmul_rn(negd, (float)(cols - 1 - c)));
-      sc[c] = v;
-    }
-    __syncthreads();
-    if (a.scores_only) return;
+      if (tid == 0 && a.first_moved) a.first_moved[b] = s0;
+    } else {
+      if (a.policy == 3) {
+        // heavy_hitter_decide (policies.py:246-256): top-r of the accumulated
+        // mass acc[:n-l], no averaging, no bias
+        const float* acc = a.acc + b * a.acc_bs;
+        for (int c = tid; c < cols; c += blockDim.x) sc[c] = acc[c];
+      } else {
+        // ---- window-mean scores (+ bias), policies.py:130-162
+        const float d = __fdiv_rn(a.bias, (float)cols);
+        const float negd = -d;
+        const float inv_m = (float)a.count;
+        const float* rows = a.rows + b * a.r_bs;
+        const float* sin = a.scores_in ? a.scores_in + b * a.si_bs : nullptr;
+        for (int c = tid; c < cols; c += blockDim.x) {
+          float v;
+          if (sin) {
+            v = sin[c];
+          } else {
+            float acc = 0.f;
+            for (int k = 0; k < a.count; ++k)
+              if (c < len_of[k]) acc = __fadd_rn(acc, rows[(int64_t)slot_of[k] * a.row_stride + c]);
+            v = __fdiv_rn(acc, inv_m);
+          }
+          if (a.apply_bias) v = __fadd_rn(v, __fmul_rn(negd, (float)(cols - 1 - c)));
+          sc[c] = v;
+        }
+      }
+      __syncthreads();
+      if (a.scores_only) return;
 
-    // ---- top-r + recent merge
-    int first = 0;
-    if (r > 0) {
-      topk_block(sc, cols, r, k32, k64, sm);
-      first = sm.first_unsel;
+      // ---- top-r + recent merge
+      int first = 0;
+      if (r > 0) {
+        topk_block(sc, cols, r, k32, k64, sm);
+        first = sm.first_unsel;
+      }
+      for (int i = tid; i < l; i += blockDim.x) {
+        if (k32) k32[r + i] = n - l + i;
+        if (k64) k64[r + i] = n - l + i;
+      }
+      if (tid == 0 && a.first_moved) a.first_moved[b] = first;
     }
-    for (int i = tid; i < l; i += blockDim.x) {
-      if (k32) k32[r + i] = n - l + i;
-      if (k64) k64[r + i] = n - l + i;
-    }
-    if (tid == 0 && a.first_moved) a.first_moved[b] = first;
     __syncthreads();
     // ---- window lengths after remap: #{i : kept[i] < len}
     if (a.newlen) {
@@ -252,6 +273,18 @@ __global__ void __launch_bounds__(kSelThreads) topk_kernel(const float* scores, 
 cudaError_t launch_select(int batches, const SelectArgs& a, cudaStream_t st) {
   if (a.W > 1024) return cudaErrorInvalidValue;
   select_kernel<<<batches, kSelThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void hh_accumulate_kernel(const float* __restrict__ acc, int na, const float* __restrict__ row, int n,
+                                     float* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    out[j] = j < na ? __fadd_rn(row[j], acc[j]) : row[j];
+}
+
+cudaError_t launch_hh_accumulate(const float* acc, int na, const float* row, int n, float* out, cudaStream_t st) {
+  const int blocks = std::min(1024, (n + 255) / 256);
+  hh_accumulate_kernel<<<blocks, 256, 0, st>>>(acc, na, row, n, out);
   return cudaGetLastError();
 }
 

@@ -104,6 +104,7 @@ struct skv_ctx {
   float* stats[2] = {nullptr, nullptr};
   float* part = nullptr;
   int32_t* counters = nullptr;
+  float* acc = nullptr;  // heavy-hitter accumulators [S][L][cap] (SKV_POLICY_HEAVY_HITTER)
   int32_t* kept = nullptr;
   int32_t* first_moved = nullptr;
   float* scores = nullptr;
@@ -190,6 +191,10 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
     return fail(SKV_EINVAL, "heads_q_total must be 0 or >= heads_q");
   if (c.capacity < c.recent_len + c.relevant_budget + 1)
     return fail(SKV_EINVAL, "capacity must exceed recent_len + relevant_budget");
+  if (c.policy < SKV_POLICY_INF_MLLM || c.policy > SKV_POLICY_NONE) return fail(SKV_EINVAL, "unknown policy");
+  // sink_recent_decide: require budget > sink_count >= 0 (policies.py:218-219)
+  if (c.policy == SKV_POLICY_SINK_RECENT && !(c.recent_len + c.relevant_budget > c.sink_count && c.sink_count >= 0))
+    return fail(SKV_EINVAL, "require budget > sink_count >= 0");
 
   skv_ctx* x = new skv_ctx();
   x->cfg = c;
@@ -246,6 +251,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
   chk(x->alloc(&x->scores, SL * x->cap * sizeof(float)));
   chk(x->alloc(&x->pos_in, x->S * sizeof(int64_t)));
+  // heavy-hitter accumulators (engine.py:274): one column per cached token
+  if (c.policy == SKV_POLICY_HEAVY_HITTER) chk(x->alloc(&x->acc, SL * (size_t)x->cap * sizeof(float)));
   if (e != cudaSuccess) {
     skv_destroy(x);
     return e == cudaErrorMemoryAllocation ? fail(SKV_ENOMEM, "device allocation failed")
@@ -323,8 +330,28 @@ int skv_timing_read(skv_ctx* x, uint64_t* out, int max_pairs) {
 
 // ------------------------------------------------------------------ decode --
 
+// Where the folded (head-aggregated) row of a recorded step goes: the window
+// ring slot (Inf-MLLM), or added into the heavy-hitter accumulator.
+static void fold_target(skv_ctx* x, int layer, int slot, FoldArgs& f) {
+  if (x->cfg.policy == SKV_POLICY_HEAVY_HITTER) {
+    f.rows = x->acc + (int64_t)layer * x->cap;
+    f.r_ss = (int64_t)x->L * x->cap;
+    f.wlen = nullptr;
+    f.accum = 1;
+  } else {
+    f.rows = x->rows + ((int64_t)layer * x->W + slot) * x->cap;
+    f.r_ss = (int64_t)x->L * x->W * x->cap;
+    f.wlen = x->wlen + (int64_t)layer * x->W + slot;
+    f.w_ss = (int64_t)x->L * x->W;
+  }
+}
+
 static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
                              const int64_t* pos_dev, float* out, int record, cudaStream_t st) {
+  // Rows feed only the Inf-MLLM window and the heavy-hitter accumulator; the
+  // heavy hitter needs every step's row (engine.py:274)
+  if (x->cfg.policy == SKV_POLICY_HEAVY_HITTER) record = 1;
+  else if (x->cfg.policy != SKV_POLICY_INF_MLLM) record = 0;
   const int n_old = x->n[layer];
   if (n_old + 1 > x->cap)
     return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
@@ -410,10 +437,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     f.l_hs = x->cap;
     f.stats = x->stats[pp] + (int64_t)layer * x->Hq * 2;
     f.st_ss = SLstride * x->Hq * 2;
-    f.rows = x->rows + ((int64_t)layer * x->W + x->pend_slot[layer]) * x->cap;
-    f.r_ss = SLstride * x->W * x->cap;
-    f.wlen = x->wlen + (int64_t)layer * x->W + x->pend_slot[layer];
-    f.w_ss = SLstride * x->W;
+    fold_target(x, layer, x->pend_slot[layer], f);
     f.n = x->pend_n[layer];
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
   f.agg_div = x->Hq_total;
@@ -428,8 +452,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     x->pend_n[layer] = n;
     x->pend_slot[layer] = x->whead[layer];
     x->pend_par[layer] = par;
-    x->whead[layer] = (x->whead[layer] + 1) % x->W;
-    x->wcount[layer] = std::min(x->wcount[layer] + 1, x->W);
+    if (x->cfg.policy == SKV_POLICY_INF_MLLM) {  // the heavy hitter accumulates instead of pushing
+      x->whead[layer] = (x->whead[layer] + 1) % x->W;
+      x->wcount[layer] = std::min(x->wcount[layer] + 1, x->W);
+    }
     x->parity[layer] = par ^ 1;
   }
   x->n[layer] = n;
@@ -446,10 +472,7 @@ static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
   f.l_hs = x->cap;
   f.stats = x->stats[pp] + (int64_t)layer * x->Hq * 2;
   f.st_ss = (int64_t)x->L * x->Hq * 2;
-  f.rows = x->rows + ((int64_t)layer * x->W + x->pend_slot[layer]) * x->cap;
-  f.r_ss = (int64_t)x->L * x->W * x->cap;
-  f.wlen = x->wlen + (int64_t)layer * x->W + x->pend_slot[layer];
-  f.w_ss = (int64_t)x->L * x->W;
+  fold_target(x, layer, x->pend_slot[layer], f);
   f.n = x->pend_n[layer];
   f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
   f.agg_div = x->Hq_total;
@@ -468,6 +491,8 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   if (layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
   if (x->cfg.dtype != SKV_DTYPE_BF16 || x->D != 128) return fail(SKV_EINVAL, "chunked prefill needs bf16, head_dim 128");
   if (C < 1) return fail(SKV_EINVAL, "chunk must be non-empty");
+  if (x->cfg.policy == SKV_POLICY_HEAVY_HITTER)
+    return fail(SKV_EINVAL, "the heavy-hitter policy needs every token's row: feed prompts through decode steps");
   const int n0 = x->n[layer];
   if (n0 + C > x->cap) return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
   cudaStream_t st = as_stream(stream);
@@ -488,7 +513,9 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
                                       SLs * x->cap, x->next_pos + layer, x->len + layer, SLs, modality,
                                       x->round_value[layer], st);
   if (e != cudaSuccess) return cuda_fail(e, "append kernel launch");
-  const int wrec = std::min(x->W, C);
+  // window rows are recorded for the Inf-MLLM policy only (the index-range
+  // baselines need none)
+  const int wrec = x->cfg.policy == SKV_POLICY_INF_MLLM ? std::min(x->W, C) : 0;
   PrefillArgs a{};
   a.C = C;
   a.n0 = n0;
@@ -501,14 +528,14 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   a.cap = x->cap;
   a.scale = x->scale;
   a.out = out;
-  a.lg = x->plogits;
+  a.lg = wrec ? x->plogits : nullptr;
   a.lg_cap = x->cap;
-  a.st = x->pstats;
+  a.st = wrec ? x->pstats : nullptr;
   e = launch_prefill(q, x->S, x->k, x->v, (int64_t)x->S * x->L * x->Hkv * x->cap, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
   x->launches += 3;
   // fold the recorded rows (oldest first) into the window ring, one launch
-  {
+  if (wrec > 0) {
     FoldArgs f{};
     f.logits = x->plogits;
     f.l_ss = (int64_t)wrec * x->Hq * x->cap;
@@ -642,6 +669,8 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
   a.apply_bias = mode == 1 ? 0 : 1;
   a.scores_only = mode == 1;
   a.pad = x->B;
+  a.policy = x->cfg.policy;
+  a.sink = x->cfg.sink_count;
   if (mode == 1 && n <= x->B) return SKV_OK;  // keep-all decision: nothing to score
   CompactArgs c{};
   c.heads = x->Hkv;
@@ -665,6 +694,8 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     }
     a.first_moved = x->first_moved;
     a.newlen = x->newlen;
+    a.acc = x->acc;
+    a.acc_bs = x->cap;
     cudaError_t e = launch_select(x->S * x->L, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
     x->launches++;
@@ -687,6 +718,8 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     c.first_moved = x->first_moved;
     c.len = x->len;
     c.len_bs = 1;
+    c.acc = x->acc;
+    c.acc_bs = x->cap;
     e = launch_compact(x->S * x->L, c, st);
     if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
     x->launches++;
@@ -708,6 +741,8 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       }
       a.first_moved = x->first_moved + sl0 * x->S;  // scratch slice of S entries
       a.newlen = x->newlen + sl0 * x->W;
+      a.acc = x->acc ? x->acc + sl0 * x->cap : nullptr;
+      a.acc_bs = (int64_t)x->L * x->cap;
       cudaError_t e = launch_select(x->S, a, st);
       if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
       x->launches++;
@@ -730,6 +765,8 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       c.first_moved = a.first_moved;
       c.len = x->len + sl0;
       c.len_bs = x->L;
+      c.acc = x->acc ? x->acc + sl0 * x->cap : nullptr;
+      c.acc_bs = (int64_t)x->L * x->cap;
       e = launch_compact(x->S, c, st);
       if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
       x->launches++;
@@ -752,8 +789,12 @@ static int evict_common(skv_ctx* x, int layer, int32_t* kept_dev, void* stream, 
   if (layer < -1 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
   cudaStream_t st = as_stream(stream);
   const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? x->L : layer + 1;
+  if (x->cfg.policy == SKV_POLICY_NONE) return SKV_OK;  // keep_all: nothing changes (engine.py:298-299)
+  if (x->cfg.policy != SKV_POLICY_INF_MLLM && mode != 0)
+    return fail(SKV_EINVAL, "score export / apply is defined for the Inf-MLLM policy only");
   for (int l = l0; l < l1; ++l) {
-    if (x->wcount[l] == 0) return fail(SKV_EINVAL, "attention window is empty");
+    if (x->cfg.policy == SKV_POLICY_INF_MLLM && x->wcount[l] == 0)
+      return fail(SKV_EINVAL, "attention window is empty");
   }
   if (mode != 2) {
     for (int l = l0; l < l1; ++l) {
@@ -872,6 +913,8 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   // host mirror: injection is per (stream, layer); the caller injects every
   // stream of a layer with the same n and m.
   x->last_layer = -1;
+  if (x->acc)  // heavy hitter: injected tokens start with no accumulated mass
+    SKV_CK(cudaMemset(x->acc + ((int64_t)stream * x->L + layer) * x->cap, 0, (size_t)x->cap * sizeof(float)));
   x->n[layer] = n;
   x->wcount[layer] = m;
   x->whead[layer] = m % x->W;
@@ -957,6 +1000,48 @@ int skv_window_scores(const float* rows, int row_stride, const int32_t* lens, in
   a.scores_only = 1;
   cudaError_t e = launch_select(1, a, as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+  return SKV_OK;
+}
+
+int skv_policy_decide(int policy, const float* acc, int n, int recent_len, int relevant_budget, int sink_count,
+                      int64_t* kept, float* scores, void* stream) {
+  if (n < 0) return fail(SKV_EINVAL, "n must be >= 0");
+  if (policy == SKV_POLICY_WINDOW) {
+    if (recent_len < 1) return fail(SKV_EINVAL, "budget must be >= 1");
+    relevant_budget = 0;
+    sink_count = 0;
+  } else if (policy == SKV_POLICY_SINK_RECENT) {
+    if (!(recent_len + relevant_budget > sink_count && sink_count >= 0))
+      return fail(SKV_EINVAL, "require budget > sink_count >= 0");
+  } else if (policy == SKV_POLICY_HEAVY_HITTER) {
+    if (recent_len < 1 || relevant_budget < 0) return fail(SKV_EINVAL, "bad policy config");
+    if (n > recent_len + relevant_budget && (!acc || !scores))
+      return fail(SKV_EINVAL, "accumulator and scores scratch required when n > r + l");
+  } else {
+    return fail(SKV_EINVAL, "policy must be window, sink_recent or heavy_hitter");
+  }
+  if (n == 0) return 0;
+  SelectArgs a{};
+  a.W = 1;
+  a.n = n;
+  a.l = recent_len;
+  a.r = relevant_budget;
+  a.policy = policy;
+  a.sink = sink_count;
+  a.acc = acc;
+  a.scores = scores;
+  a.kept64 = kept;
+  cudaError_t e = launch_select(1, a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
+  return std::min(n, recent_len + relevant_budget);
+}
+
+int skv_hh_accumulate(const float* acc, int na, const float* row, int n, float* out, void* stream) {
+  if (na < 0 || n < 0) return fail(SKV_EINVAL, "lengths must be >= 0");
+  if (na > n) return fail(SKV_EINVAL, "accumulator longer than the new row");
+  if (n == 0) return SKV_OK;
+  cudaError_t e = launch_hh_accumulate(acc, na, row, n, out, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "accumulate kernel launch");
   return SKV_OK;
 }
 

@@ -31,8 +31,10 @@ __device__ __forceinline__ void fold_columns(const FoldArgs& f, int s, int c0, i
         acc = __fadd_rn(acc, p);
       }
     }
-    if (f.mode == 0) row[j] = __fdiv_rn(acc, (float)(f.agg_div ? f.agg_div : Hq));
-    else if (f.mode == 1) row[j] = acc;
+    if (f.mode != 2) {
+      const float v = f.mode == 0 ? __fdiv_rn(acc, (float)(f.agg_div ? f.agg_div : Hq)) : acc;
+      row[j] = (f.accum && j < f.n - 1) ? __fadd_rn(row[j], v) : v;
+    }
   }
 }
 
@@ -54,7 +56,7 @@ __device__ __forceinline__ void fold_piece(const FoldArgs& f, int s, int piece, 
 // MODE 0: mean over heads (divisor agg), MODE 1: max over heads.
 template <int MODE>
 __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t l_hs, const float* __restrict__ stt,
-                                          float* __restrict__ row, int j0, int n, int Hq, float agg) {
+                                          float* __restrict__ row, int j0, int n, int Hq, float agg, int accum = 0) {
   float acc[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) acc[e] = MODE == 1 ? -INFINITY : 0.f;
@@ -78,7 +80,10 @@ __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t 
       }
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) row[j0 + e] = MODE == 1 ? acc[e] : __fdiv_rn(acc[e], agg);
+    for (int e = 0; e < 4; ++e) {
+      const float v = MODE == 1 ? acc[e] : __fdiv_rn(acc[e], agg);
+      row[j0 + e] = (accum && j0 + e < n - 1) ? __fadd_rn(row[j0 + e], v) : v;
+    }
   } else {
     for (int e = 0; e < 4 && j0 + e < n; ++e) {
       float a = MODE == 1 ? -INFINITY : 0.f;
@@ -86,7 +91,8 @@ __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t 
         const float p = __fdiv_rn(expf(__fsub_rn(__ldcs(lg + (int64_t)h * l_hs + j0 + e), stt[2 * h])), stt[2 * h + 1]);
         a = MODE == 1 ? fmaxf(a, p) : __fadd_rn(a, p);
       }
-      row[j0 + e] = MODE == 1 ? a : __fdiv_rn(a, agg);
+      const float v = MODE == 1 ? a : __fdiv_rn(a, agg);
+      row[j0 + e] = (accum && j0 + e < n - 1) ? __fadd_rn(row[j0 + e], v) : v;
     }
   }
 }

@@ -26,6 +26,8 @@ struct FoldArgs {
   int n;                // row length (0: nothing to fold)
   int mode;             // 0 mean over heads, 1 max over heads, 2 per-head probs
   int agg_div;          // mode 0 divisor (total query heads across shards; 0: Hq)
+  int accum;            // heavy hitter: row[j] += value for j < n-1, row[n-1] = value
+                        // (heavy_hitter_accumulate, policies.py:234-243)
 };
 
 struct AttnArgs {
@@ -108,9 +110,15 @@ struct SelectArgs {
   int pad;              // keep-all rows: write -1 into kept[n, pad)
   const float* scores_in;  // optional: window-mean scores given (e.g. reduced across head shards)
   int64_t si_bs;
+  int policy;           // SKV_POLICY_* (0 Inf-MLLM, 1 window, 2 sink+recent, 3 heavy hitter)
+  int sink;             // sink_count (policy 2)
+  const float* acc;     // heavy-hitter accumulators acc + b*acc_bs (policy 3)
+  int64_t acc_bs;
 };
 
 cudaError_t launch_select(int batches, const SelectArgs& a, cudaStream_t st);
+// heavy_hitter_accumulate (policies.py:234-243): out[j] = row[j] + (j < na ? acc[j] : 0)
+cudaError_t launch_hh_accumulate(const float* acc, int na, const float* row, int n, float* out, cudaStream_t st);
 cudaError_t launch_topk(const float* scores, int n, int k, int64_t* out, cudaStream_t st);
 
 // ----------------------------------------------------------------------------
@@ -144,6 +152,8 @@ struct CompactArgs {
   int m;                 // kept count
   int32_t* len;          // optional len[b*len_bs] = m
   int64_t len_bs;
+  float* acc;            // optional heavy-hitter accumulators acc + b*acc_bs, gathered like a row of length n
+  int64_t acc_bs;
 };
 
 cudaError_t launch_compact(int blocks, const CompactArgs& a, cudaStream_t st);

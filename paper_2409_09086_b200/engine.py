@@ -53,6 +53,10 @@ class EngineConfig:
     dtype: torch.dtype = torch.bfloat16
     head_agg: str = "mean"
     heads_q_total: int = 0  # head-sharded engines: query heads of all shards (0: heads_q)
+    # Session policy switch (engine.py:296-307): "inf_mllm" (the hot path),
+    # "window", "sink_recent", "heavy_hitter" or "none"
+    policy: str = "inf_mllm"
+    sink_count: int = 4
 
     @property
     def budget(self) -> int:
@@ -68,6 +72,8 @@ class StreamEngine:
             raise ValueError("dtype must be torch.float32 or torch.bfloat16")
         if cfg.head_agg not in ("mean", "max"):
             raise ValueError(f"unknown head_agg {cfg.head_agg!r}")
+        if cfg.policy not in _lib.POLICIES:
+            raise ValueError(f"unknown policy {cfg.policy!r}")
         self.cfg = cfg
         self.lib = _lib.load()
         c = SkvConfig(
@@ -84,6 +90,8 @@ class StreamEngine:
             capacity=cfg.capacity,
             head_agg=_lib.AGG_MAX if cfg.head_agg == "max" else _lib.AGG_MEAN,
             heads_q_total=cfg.heads_q_total,
+            policy=_lib.POLICIES[cfg.policy],
+            sink_count=cfg.sink_count,
         )
         handle = ctypes.c_void_p()
         torch.cuda.init()

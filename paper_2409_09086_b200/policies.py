@@ -5,9 +5,9 @@ The decision functions run the CUDA kernels of libstreamkv_b200.so:
 ``window_mean_scores`` / ``inf_mllm_decide`` the K2 score+bias+radix-select
 kernel, ``top_k_indices`` its block radix top-k.  Inputs may be NumPy arrays /
 lists (results come back as NumPy, like the reference) or CUDA tensors
-(results stay on the device).  The comparison baselines (sliding window,
-sink+recent, heavy hitter; policies.py:204-256) are outside the hot path and
-are not provided.
+(results stay on the device).  The Session's comparison baselines (sliding
+window, sink+recent, heavy hitter; policies.py:204-256) run on the same select
+kernel (``skv_policy_decide``) and a device accumulate kernel.
 """
 
 from __future__ import annotations
@@ -199,6 +199,61 @@ def inf_mllm_decide(window: AttentionWindow, n: int, cfg: PolicyConfig) -> Evict
     host = window._host
     kept_o = _out(kept, host)
     return EvictionDecision(relevant=kept_o[:r], recent=kept_o[r:], kept=kept_o)
+
+
+_POLICY_WINDOW, _POLICY_SINK_RECENT, _POLICY_HEAVY_HITTER = 1, 2, 3
+
+
+def _policy_decide(policy: int, acc, n: int, recent_len: int, relevant_budget: int, sink: int, host: bool):
+    kept = torch.empty(max(1, min(n, recent_len + relevant_budget)), dtype=torch.int64, device="cuda")
+    scores = torch.empty(max(1, n), dtype=torch.float32, device="cuda") if acc is not None else None
+    m = check(_lib.load().skv_policy_decide(policy, _p(acc) if acc is not None else None, n, recent_len,
+                                            relevant_budget, sink, _p(kept), _p(scores) if scores is not None else None,
+                                            _sh()))
+    return _out(kept[:m], host)
+
+
+def sliding_window_decide(n: int, budget: int) -> EvictionDecision:
+    """policies.py:204-213 on device: keep only the last ``budget`` positions."""
+    if budget < 1:
+        raise ValueError("budget must be >= 1")
+    recent = _policy_decide(_POLICY_WINDOW, None, n, budget, 0, 0, True)
+    return EvictionDecision(relevant=np.empty(0, dtype=np.int64), recent=recent, kept=recent)
+
+
+def sink_recent_decide(n: int, s: int, budget: int) -> EvictionDecision:
+    """policies.py:216-231 on device: the first ``s`` sinks plus the last ``budget - s``."""
+    if not budget > s >= 0:
+        raise ValueError("require budget > sink_count >= 0")
+    if n <= budget:
+        return EvictionDecision.keep_all(n, min(budget - s, n))
+    kept = _policy_decide(_POLICY_SINK_RECENT, None, n, budget - s, s, s, True)
+    return EvictionDecision(relevant=kept[:s], recent=kept[s:], kept=kept)
+
+
+def heavy_hitter_accumulate(acc, new_row):
+    """policies.py:234-243 on device: ``new_row`` plus the (shorter) running accumulator."""
+    a, host_a = _to_dev_f32(acc)
+    row, host = _to_dev_f32(new_row)
+    a, row = a.reshape(-1), row.reshape(-1)
+    if a.numel() > row.numel():
+        raise ValueError("accumulator longer than the new row")
+    out = torch.empty_like(row)
+    check(_lib.load().skv_hh_accumulate(_p(a), a.numel(), _p(row), row.numel(), _p(out), _sh()))
+    return _out(out, host)
+
+
+def heavy_hitter_decide(acc, n: int, r: int, l: int) -> EvictionDecision:
+    """policies.py:246-256 on device: the ``r`` largest accumulated masses of the
+    first ``n - l`` columns (ties to the newer) plus the last ``l``."""
+    a, host = _to_dev_f32(acc)
+    a = a.reshape(-1)
+    if a.numel() != n:
+        raise ValueError(f"accumulator length {a.numel()} != n={n}")
+    if n <= r + l:
+        return EvictionDecision.keep_all(n, l)
+    kept = _policy_decide(_POLICY_HEAVY_HITTER, a, n, l, r, 0, host)
+    return EvictionDecision(relevant=kept[:r], recent=kept[r:], kept=kept)
 
 
 def aggregate_heads(per_head, how: str):

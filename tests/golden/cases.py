@@ -31,6 +31,20 @@ CASES = {
     "wide_window": dict(S=1, L=1, Hq=4, Hkv=4, D=64, T=320, l=16, r=32, W=40, b=0.1, E=16,
                         dtype="f32", seed=1004, saddles=3, saddle_gain=5.0, spike_prob=0.0,
                         spike_gain=1.0, out_every=16),
+    # The Session's comparison baselines (engine.py:296-307):
+    # heavy-hitter accumulated mass, sliding window, sink + recent.
+    "hh_mini": dict(S=1, L=2, Hq=8, Hkv=8, D=64, T=384, l=32, r=32, W=16, b=0.01, E=32,
+                    dtype="f32", seed=1005, saddles=4, saddle_gain=5.0, spike_prob=0.0,
+                    spike_gain=1.0, out_every=32, policy="heavy_hitter"),
+    "hh_gqa_bf16": dict(S=2, L=1, Hq=8, Hkv=2, D=128, T=320, l=48, r=80, W=16, b=0.01, E=64,
+                        dtype="bf16", seed=1006, saddles=0, saddle_gain=1.0, spike_prob=0.01,
+                        spike_gain=4.0, out_every=64, policy="heavy_hitter"),
+    "window_mini": dict(S=1, L=1, Hq=4, Hkv=4, D=64, T=256, l=32, r=32, W=16, b=0.01, E=32,
+                        dtype="bf16", seed=1007, saddles=0, saddle_gain=1.0, spike_prob=0.0,
+                        spike_gain=1.0, out_every=32, policy="window"),
+    "sink_mini": dict(S=2, L=1, Hq=4, Hkv=2, D=128, T=256, l=24, r=40, W=16, b=0.01, E=32,
+                      dtype="bf16", seed=1008, saddles=0, saddle_gain=1.0, spike_prob=0.0,
+                      spike_gain=1.0, out_every=32, policy="sink_recent", sink=4),
 }
 
 

@@ -33,7 +33,11 @@ from streamkv.policies import (  # noqa: E402
     PolicyConfig,
     aggregate_heads,
     bias_vector,
+    heavy_hitter_accumulate,
+    heavy_hitter_decide,
     inf_mllm_decide,
+    sink_recent_decide,
+    sliding_window_decide,
     top_k_indices,
     window_mean_scores,
 )
@@ -52,10 +56,12 @@ def run_reference_case(name: str) -> dict:
     c = CASES[name]
     S, L, Hq, Hkv, D = c["S"], c["L"], c["Hq"], c["Hkv"], c["D"]
     G = Hq // Hkv
-    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"])
+    policy = c.get("policy", "inf_mllm")
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"], sink_count=c.get("sink", 4))
     holder = _ScaleHolder(D)
     caches = [KvCache(L, Hkv, D) for _ in range(S)]
     windows = [[AttentionWindow(c["W"]) for _ in range(L)] for _ in range(S)]
+    accs = [[np.zeros(0, dtype=F32) for _ in range(L)] for _ in range(S)]  # engine.py:274
     q_all, k_all, v_all = case_inputs(name)  # (T, L, S, H, D)
     T = q_all.shape[0]
     out_steps = []
@@ -72,7 +78,9 @@ def run_reference_case(name: str) -> dict:
                     keys = np.repeat(keys, G, axis=0)
                     vals = np.repeat(vals, G, axis=0)
                 probs, o = Session._attend(holder, keys, vals, q_all[t, layer, s])
-                windows[s][layer].push(aggregate_heads(probs, "mean"))
+                row = aggregate_heads(probs, "mean")
+                windows[s][layer].push(row)
+                accs[s][layer] = heavy_hitter_accumulate(accs[s][layer], row)
                 step_out[layer, s] = o
         if t % c["out_every"] == 0 or t == T - 1:
             out_steps.append(t)
@@ -82,18 +90,28 @@ def run_reference_case(name: str) -> dict:
             for s in range(S):
                 for layer in range(L):
                     n = caches[s].length(layer)
-                    if n > cfg.budget:
-                        sc = window_mean_scores(windows[s][layer], n, cfg.recent_len) + bias_vector(
-                            n, cfg.recent_len, cfg.bias
-                        )
+                    sc = np.zeros(0, dtype=F32)
+                    # the Session's policy switch, engine.py:296-307
+                    if policy == "heavy_hitter":
+                        if n > cfg.budget:
+                            sc = accs[s][layer][: n - cfg.recent_len].copy()
+                        d = heavy_hitter_decide(accs[s][layer], n, cfg.relevant_budget, cfg.recent_len)
+                    elif policy == "window":
+                        d = sliding_window_decide(n, cfg.budget)
+                    elif policy == "sink_recent":
+                        d = sink_recent_decide(n, cfg.sink_count, cfg.budget)
                     else:
-                        sc = np.zeros(0, dtype=F32)
-                    d = inf_mllm_decide(windows[s][layer], n, cfg)
+                        if n > cfg.budget:
+                            sc = window_mean_scores(windows[s][layer], n, cfg.recent_len) + bias_vector(
+                                n, cfg.recent_len, cfg.bias
+                            )
+                        d = inf_mllm_decide(windows[s][layer], n, cfg)
                     kept_log.append(d.kept.astype(np.int32))
                     score_log.append(sc.astype(F32))
                     if d.kept.size != n:
                         caches[s].gather_keep(layer, d.kept)
                         windows[s][layer].remap(d.kept)
+                        accs[s][layer] = accs[s][layer][d.kept]  # engine.py:335
     final_keys = np.stack([np.stack([caches[s].keys(layer) for layer in range(L)]) for s in range(S)])
     final_pos = np.stack([np.stack([caches[s].original_positions(layer) for layer in range(L)]) for s in range(S)])
     return dict(
@@ -141,10 +159,15 @@ def run_kats() -> dict:
 
 
 def main():
+    only = set(sys.argv[1:])  # optional: regenerate just these cases
     for name in CASES:
+        if only and name not in only:
+            continue
         res = run_reference_case(name)
         np.savez_compressed(os.path.join(HERE, f"ref_{name}.npz"), **res)
         print(name, "evictions", res["evict_steps"].size, "kept entries", res["kept"].size)
+    if only:
+        return
     kat = run_kats()
     np.savez_compressed(os.path.join(HERE, "ref_kat_algorithm1.npz"), **kat)
     print("kat", kat["kept_off"].size - 1)

@@ -21,8 +21,9 @@ def run_oracle_case(name: str, kept_override=None) -> dict:
     decisions so an allowed near-tie cannot cascade).
     """
     c = CASES[name]
-    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"])
-    orc = StreamOracle(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], cfg, window=c["W"])
+    policy = c.get("policy", "inf_mllm")
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"], sink_count=c.get("sink", 4))
+    orc = StreamOracle(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], cfg, window=c["W"], policy=policy)
     q_all, k_all, v_all = case_inputs(name)
     T = q_all.shape[0]
     out_steps, outs = [], []
@@ -41,7 +42,12 @@ def run_oracle_case(name: str, kept_override=None) -> dict:
             for s in range(c["S"]):
                 for layer in range(c["L"]):
                     n = orc.length(s, layer)
-                    sc = orc.scores(s, layer) if n > cfg.budget else np.zeros(0, F32)
+                    if n <= cfg.budget or policy in ("window", "sink_recent", "none"):
+                        sc = np.zeros(0, F32)
+                    elif policy == "heavy_hitter":
+                        sc = orc.acc[s][layer][: n - cfg.recent_len].copy()
+                    else:
+                        sc = orc.scores(s, layer)
                     kept = orc.decide(s, layer).kept
                     if kept_override is not None:
                         kept = kept_override(t, s, layer, kept, sc, n)

@@ -55,3 +55,28 @@ def test_config_validation_without_gpu():
     with pytest.raises(ValueError):
         _lib.check(_lib.SKV_EINVAL)
     assert lib.skv_top_k(None, 4, -1, None, None) == _lib.SKV_EINVAL
+
+
+def test_policy_validation_without_gpu():
+    """The Session's policy switch (engine.py:296-307) and sink_recent_decide's
+    budget > sink_count >= 0 rule (policies.py:218-219) are checked host-side."""
+    from paper_2409_09086_b200 import _lib
+
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("library not built")
+    lib = _lib.load()
+    c = _lib.SkvConfig(streams=1, layers=1, heads_q=4, heads_kv=4, head_dim=128, dtype=1, recent_len=4,
+                       relevant_budget=4, bias=0.1, window=4, capacity=64, head_agg=0, policy=9)
+    h = ctypes.c_void_p()
+    assert lib.skv_create(ctypes.byref(c), ctypes.byref(h)) == _lib.SKV_EINVAL
+    assert b"policy" in lib.skv_last_error()
+    c.policy = _lib.POLICIES["sink_recent"]
+    c.sink_count = 8  # budget 8 is not > 8
+    assert lib.skv_create(ctypes.byref(c), ctypes.byref(h)) == _lib.SKV_EINVAL
+    assert b"sink_count" in lib.skv_last_error()
+    # stand-alone decisions: argument checks precede any device work
+    assert lib.skv_policy_decide(0, None, 4, 2, 2, 0, None, None, None) == _lib.SKV_EINVAL
+    assert lib.skv_policy_decide(_lib.POLICIES["window"], None, 4, 0, 0, 0, None, None, None) == _lib.SKV_EINVAL
+    assert lib.skv_policy_decide(_lib.POLICIES["heavy_hitter"], None, 9, 2, 2, 0, None, None, None) == _lib.SKV_EINVAL
+    assert lib.skv_hh_accumulate(None, 5, None, 4, None, None) == _lib.SKV_EINVAL
+    assert lib.skv_policy_decide(_lib.POLICIES["window"], None, 0, 4, 0, 0, None, None, None) == 0

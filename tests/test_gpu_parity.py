@@ -50,7 +50,7 @@ def _engine(c, capacity=None):
     dt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
     cap = capacity or (c["l"] + c["r"] + c["E"])
     return StreamEngine(EngineConfig(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], c["l"], c["r"], c["b"], c["W"],
-                                     cap, dt))
+                                     cap, dt, policy=c.get("policy", "inf_mllm"), sink_count=c.get("sink", 4)))
 
 
 def _dev(a, dtype):
@@ -305,3 +305,34 @@ def test_full_size_config1_properties():
         ka = eng.kv(s, layer)[0]
         idx = torch.from_numpy(kc[s, layer].astype(np.int64)).cuda()
         assert torch.equal(ka, kb[:, idx])
+
+
+def test_baseline_policy_dropins_match_oracle():
+    """sliding_window_decide / sink_recent_decide / heavy_hitter_accumulate /
+    heavy_hitter_decide (policies.py:204-256) on the device vs the oracle
+    (pinned to the reference by the golden engine cases)."""
+    from oracle.streamkv_oracle import mass_accumulate, mass_decide, recent_only, sinks_plus_recent
+    import paper_2409_09086_b200 as p
+
+    rng = np.random.default_rng(77)
+    for _ in range(60):
+        n = int(rng.integers(1, 600))
+        budget = int(rng.integers(1, 300))
+        got = p.sliding_window_decide(n, budget)
+        want = recent_only(n, budget)
+        np.testing.assert_array_equal(got.kept, want.kept)
+        s = int(rng.integers(0, budget)) if budget > 1 else 0
+        if budget > s:
+            got = p.sink_recent_decide(n, s, budget)
+            want = sinks_plus_recent(n, s, budget)
+            np.testing.assert_array_equal(got.kept, want.kept)
+            np.testing.assert_array_equal(got.relevant, want.relevant)
+        acc = rng.random(max(0, n - int(rng.integers(0, 3)))).astype(F32)
+        row = rng.random(n).astype(F32)
+        np.testing.assert_array_equal(p.heavy_hitter_accumulate(acc, row), mass_accumulate(acc, row))
+        a2 = rng.choice(np.array([0.1, 0.2, 0.3, 0.5], F32), size=n)  # ties: the newer index wins
+        r, l = int(rng.integers(0, 100)), int(rng.integers(1, 100))
+        got = p.heavy_hitter_decide(a2, n, r, l)
+        want = mass_decide(a2, n, r, l)
+        np.testing.assert_array_equal(got.kept, want.kept)
+        np.testing.assert_array_equal(got.relevant, want.relevant)
