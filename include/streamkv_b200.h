@@ -45,6 +45,16 @@ extern "C" {
 #define SKV_POLICY_HEAVY_HITTER 3 /* heavy_hitter_accumulate/decide, policies.py:234-256 */
 #define SKV_POLICY_NONE 4         /* keep everything (EvictionDecision.keep_all, engine.py:298-299) */
 
+/* Rotary positions of the cached keys (PositionMode, cache.py:24-34; the
+ * Session's rotary helpers engine.py:198-233).  With RoPE on, q and k inputs
+ * are pre-rotation: the engine rotates q and the new k at the token's
+ * position, keeps raw keys (what cache.keys() returns) next to the rotated
+ * keys it attends over, and after a compaction re-rotates the moved keys at
+ * their new slots (cache-relative, _refresh_rotations engine.py:339-342). */
+#define SKV_ROPE_NONE 0           /* inputs already rotated (the BASELINE configs) */
+#define SKV_ROPE_CACHE_RELATIVE 1 /* PositionMode.CACHE_RELATIVE: position = cache slot */
+#define SKV_ROPE_ORIGINAL 2       /* PositionMode.ORIGINAL: position = original stream position */
+
 #define SKV_AGG_MEAN 0 /* aggregate_heads(.., "mean"), policies.py:261-262 */
 #define SKV_AGG_MAX 1  /* aggregate_heads(.., "max"),  policies.py:263-264 */
 
@@ -69,6 +79,8 @@ typedef struct skv_config {
                               up to the reference head mean */
   int32_t policy;          /* SKV_POLICY_* (zero-initialised configs get the Inf-MLLM policy) */
   int32_t sink_count;      /* s  (PolicyConfig.sink_count) for SKV_POLICY_SINK_RECENT */
+  int32_t rope_mode;       /* SKV_ROPE_* (0: q/k arrive rotated) */
+  float rope_base;         /* ModelSpec.rope_base (engine.py:69), e.g. 10000 */
 } skv_config;
 
 typedef struct skv_ctx skv_ctx;

@@ -345,6 +345,55 @@ class LayerKV:
 
 
 # --------------------------------------------------------------------------
+# rotary positions
+# --------------------------------------------------------------------------
+
+
+class Rotary:
+    """The reference Session's rotary helpers (engine.py:175-180, 198-233):
+    inv_freq = base ** (-2 i / D) in f64, cos/sin tables grown in f64 and cast
+    to f32, interleaved (even, odd) pairs rotated with f32 products."""
+
+    def __init__(self, head_dim: int, base: float = 10000.0):
+        half = head_dim // 2
+        self.inv_freq = base ** (-2.0 * np.arange(half, dtype=np.float64) / head_dim)  # engine.py:176-178
+        self.cos = np.zeros((0, half), dtype=F32)
+        self.sin = np.zeros((0, half), dtype=F32)
+
+    def _trig(self, upto: int) -> None:  # engine.py:200-207
+        if upto <= self.cos.shape[0]:
+            return
+        size = max(upto, 256, self.cos.shape[0] * 2)
+        pos = np.arange(size, dtype=np.float64)[:, None]
+        ang = pos * self.inv_freq
+        self.cos = np.cos(ang).astype(F32)
+        self.sin = np.sin(ang).astype(F32)
+
+    def rotate_one(self, vec: np.ndarray, position: int) -> np.ndarray:  # engine.py:209-219
+        self._trig(position + 1)
+        cos, sin = self.cos[position], self.sin[position]
+        even, odd = vec[:, 0::2], vec[:, 1::2]
+        out = np.empty_like(vec)
+        out[:, 0::2] = even * cos - odd * sin
+        out[:, 1::2] = even * sin + odd * cos
+        return out
+
+    def rotate_many(self, block: np.ndarray, positions: np.ndarray) -> np.ndarray:  # engine.py:221-233
+        if positions.size == 0:
+            return block.copy()
+        self._trig(int(positions.max()) + 1)
+        cos, sin = self.cos[positions], self.sin[positions]
+        even, odd = block[:, :, 0::2], block[:, :, 1::2]
+        out = np.empty_like(block)
+        out[:, :, 0::2] = even * cos - odd * sin
+        out[:, :, 1::2] = even * sin + odd * cos
+        return out
+
+
+ROPE_MODES = (None, "cache_relative", "original")
+
+
+# --------------------------------------------------------------------------
 # composed streaming driver (SURVEY 7.1 step 1 / 8c)
 # --------------------------------------------------------------------------
 
@@ -364,12 +413,22 @@ class StreamOracle:
     """
 
     def __init__(self, streams: int, layers: int, heads_q: int, heads_kv: int, head_dim: int,
-                 cfg: PolicyConfig, window: Optional[int] = None, policy: str = "inf_mllm"):
+                 cfg: PolicyConfig, window: Optional[int] = None, policy: str = "inf_mllm",
+                 rope: Optional[str] = None, rope_base: float = 10000.0, rope_round=None):
         if heads_q % heads_kv:
             raise ValueError("heads_q must be a multiple of heads_kv")
         if policy not in POLICIES:
             raise ValueError(f"unknown policy {policy!r}")
         self.policy = policy
+        if rope not in ROPE_MODES:
+            raise ValueError(f"unknown rope mode {rope!r}")
+        # Rotary positions: raw keys stay in the cache, rotated keys (the
+        # Session's _rot store) are what attention reads.  rope_round models a
+        # bf16 engine, whose rotated q / k are bf16 values (pass bf16_round).
+        self.rope = rope
+        self.rotary = Rotary(head_dim, rope_base) if rope else None
+        self.rope_round = rope_round
+        self.rot = [[np.zeros((heads_kv, 0, head_dim), dtype=F32) for _ in range(layers)] for _ in range(streams)]
         # heavy-hitter accumulators, one per (stream, layer) (engine.py:274)
         self.acc = [[np.zeros(0, dtype=F32) for _ in range(layers)] for _ in range(streams)]
         self.S, self.L, self.Hq, self.Hkv, self.D = streams, layers, heads_q, heads_kv, head_dim
@@ -386,7 +445,7 @@ class StreamOracle:
 
     def _expanded(self, s: int, layer: int):
         st = self.kv[s][layer]
-        k, v = st.keys(), st.values()
+        k, v = (st.keys() if not self.rope else self.rot[s][layer]), st.values()
         if self.group > 1:
             k = np.repeat(k, self.group, axis=0)
             v = np.repeat(v, self.group, axis=0)
@@ -403,8 +462,16 @@ class StreamOracle:
         for s in (range(self.S) if streams is None else streams):
             st = self.kv[s][layer]
             st.append(np.asarray(k[s], F32), np.asarray(v[s], F32), self.pos[s])
+            qs = np.asarray(q[s], F32)
+            if self.rope:  # engine.py:265-268: rotate the new key and the query at one position
+                p = st.n - 1 if self.rope == "cache_relative" else self.pos[s]
+                rk = self.rotary.rotate_one(np.asarray(k[s], F32), p)
+                qs = self.rotary.rotate_one(qs, p)
+                if self.rope_round is not None:
+                    rk, qs = self.rope_round(rk), self.rope_round(qs)
+                self.rot[s][layer] = np.concatenate([self.rot[s][layer], rk[:, None, :]], axis=1)
             keys, vals = self._expanded(s, layer)
-            probs, o = attend_heads(keys, vals, np.asarray(q[s], F32), self.scale)
+            probs, o = attend_heads(keys, vals, qs, self.scale)
             row = head_mean(probs, self.cfg.head_agg)
             self.win[s][layer].push(row)
             self.acc[s][layer] = mass_accumulate(self.acc[s][layer], row)
@@ -448,6 +515,11 @@ class StreamOracle:
             self.kv[s][layer].gather_keep(kept)
             self.win[s][layer].remap(kept)
             self.acc[s][layer] = self.acc[s][layer][kept]  # engine.py:335
+            if self.rope:  # _refresh_rotations, engine.py:339-342 (positions_for, cache.py:160-165)
+                st = self.kv[s][layer]
+                positions = np.arange(st.n, dtype=I64) if self.rope == "cache_relative" else st.pos[: st.n].copy()
+                rot = self.rotary.rotate_many(st.keys(), positions)
+                self.rot[s][layer] = self.rope_round(rot) if self.rope_round is not None else rot
 
     def evict(self):
         """Decide + apply for every (stream, layer); returns kept[s][l]."""

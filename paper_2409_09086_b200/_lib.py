@@ -27,6 +27,8 @@ AGG_MAX = 1
 
 # eviction policies (engine.py:296-307)
 POLICIES = {"inf_mllm": 0, "window": 1, "sink_recent": 2, "heavy_hitter": 3, "none": 4}
+# rotary position modes (PositionMode, cache.py:24-34); None: inputs arrive rotated
+ROPE_MODES = {None: 0, "cache_relative": 1, "original": 2}
 
 
 class SkvConfig(ctypes.Structure):
@@ -46,6 +48,8 @@ class SkvConfig(ctypes.Structure):
         ("heads_q_total", ctypes.c_int32),
         ("policy", ctypes.c_int32),
         ("sink_count", ctypes.c_int32),
+        ("rope_mode", ctypes.c_int32),
+        ("rope_base", ctypes.c_float),
     ]
 
 

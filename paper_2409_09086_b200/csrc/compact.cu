@@ -81,6 +81,16 @@ __global__ void __launch_bounds__(kCmpThreads) compact_kernel(const CompactArgs 
     const int units = a.row_bytes / 16;
     uint4* kx = reinterpret_cast<uint4*>(a.k + b * a.kv_bs + h * a.kv_hs);
     uint4* vx = a.v ? reinterpret_cast<uint4*>(a.v + b * a.kv_bs + h * a.kv_hs) : nullptr;
+    if (a.k_raw) {
+      uint4* rx = reinterpret_cast<uint4*>(a.k_raw + b * a.kv_bs + h * a.kv_hs);
+      if (a.rope_cr) {
+        // cache-relative RoPE: the moved keys change position, so only the raw
+        // rows move here; rope_rows_kernel re-rotates them at their new slots
+        gather_rows16(rx, vx, units, a, b, first, a.m);
+        return;
+      }
+      gather_rows16(rx, nullptr, units, a, b, first, a.m);  // original positions: rotations move as-is
+    }
     gather_rows16(kx, vx, units, a, b, first, a.m);
     return;
   }

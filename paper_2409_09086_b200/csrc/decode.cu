@@ -93,14 +93,19 @@ struct Smem {
   static constexpr int NW = Gm::NW;
   // ring depth: 4 stages (128 KB for bf16 D=128) where one CTA per SM is
   // resident anyway, so a static 4-tile chunk is prefetched whole under PDL
-  static constexpr int STAGES = G >= 4 ? 4 : 3;
-  static constexpr size_t tiles = (size_t)STAGES * 2 * Gm::TILE;
-  static constexpr size_t bars = (2 * STAGES + 4) * sizeof(uint64_t);
-  static constexpr size_t tinfo = (2 * STAGES + 4) * sizeof(int);
   // epilogue slot: header (4 ints) + wm[NW][G] + wl[NW][G] + wo[NW][G][D]
   static constexpr size_t slot_floats = 4 + 2 * NW * G + NW * G * D;
   static constexpr size_t slots = 2 * slot_floats * sizeof(float);
   static constexpr size_t pbuf = (size_t)NW * G * Gm::RPWARP * sizeof(float);
+  // ring depth: as many K+V stages as fit next to the slots and 8 KB of fold
+  // stats (f32 at D = 128 is 64 KB per stage: 2 stages)
+  static constexpr int WANT = G >= 4 ? 4 : 3;
+  static constexpr int SCAP = (int)((232448 - slots - pbuf - 8192 - 512) / (2 * Gm::TILE));
+  static constexpr int STAGES = WANT < SCAP ? WANT : SCAP;
+  static_assert(STAGES >= 2, "decode ring needs two stages");
+  static constexpr size_t tiles = (size_t)STAGES * 2 * Gm::TILE;
+  static constexpr size_t bars = (2 * STAGES + 4) * sizeof(uint64_t);
+  static constexpr size_t tinfo = (2 * STAGES + 4) * sizeof(int);
   static constexpr size_t fixed = tiles + bars + tinfo + slots + pbuf;
   static size_t bytes(int Hq) { return fixed + 2 * (size_t)Hq * sizeof(float) + 16; }
 };
@@ -310,6 +315,9 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
               reinterpret_cast<const uint4*>(static_cast<const T*>(a.kin) + in)[q16];
           reinterpret_cast<uint4*>(static_cast<T*>(a.vc) + dst)[q16] =
               reinterpret_cast<const uint4*>(static_cast<const T*>(a.vin) + in)[q16];
+          if (a.kraw)  // RoPE: the raw key goes to the raw store (cache.keys())
+            reinterpret_cast<uint4*>(static_cast<T*>(a.kc_raw) + dst)[q16] =
+                reinterpret_cast<const uint4*>(static_cast<const T*>(a.kraw) + in)[q16];
         }
         if (g == 0 && lane == 0) {
           int64_t* np = a.next_pos + s * a.len_ss;

@@ -637,7 +637,8 @@ namespace skv {
 __global__ void append_chunk_kernel(const uint4* __restrict__ kin, const uint4* __restrict__ vin, uint4* kc, uint4* vc,
                                     int64_t c_ss, int64_t c_hs, int Hkv, int units, int n0, int C, int64_t* pos,
                                     int8_t* modality, int32_t* round_id, int64_t m_ss, const int64_t* next_pos,
-                                    int64_t np_ss, int mod, int rnd) {
+                                    int64_t np_ss, int mod, int rnd, const uint4* __restrict__ kraw_in,
+                                    uint4* kraw_c) {
   const int i = blockIdx.x, s = blockIdx.y;
   for (int idx = threadIdx.x; idx < Hkv * units; idx += blockDim.x) {
     const int g = idx / units, u = idx - g * units;
@@ -645,6 +646,7 @@ __global__ void append_chunk_kernel(const uint4* __restrict__ kin, const uint4* 
     const int64_t d2 = s * c_ss + g * c_hs + (int64_t)(n0 + i) * units + u;
     kc[d2] = kin[src];
     vc[d2] = vin[src];
+    if (kraw_c) kraw_c[d2] = kraw_in[src];  // RoPE: raw keys
   }
   if (threadIdx.x == 0) {
     pos[s * m_ss + n0 + i] = next_pos[s * np_ss] + i;
@@ -712,13 +714,14 @@ __global__ void chunk_meta_kernel(int32_t* len, int64_t* next_pos, int64_t ss, i
 cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
                                 int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,
                                 int8_t* modality, int32_t* round_id, int64_t m_ss, int64_t* next_pos, int32_t* len,
-                                int64_t ss, int mod, int rnd, cudaStream_t st) {
+                                int64_t ss, int mod, int rnd, cudaStream_t st, const void* kraw_in, void* kraw_c) {
   dim3 grid(C, S);
   const int threads = std::min(1024, ((Hkv * units + 31) / 32) * 32);
   append_chunk_kernel<<<grid, threads, 0, st>>>(static_cast<const uint4*>(kin), static_cast<const uint4*>(vin),
                                                 static_cast<uint4*>(kc), static_cast<uint4*>(vc), c_ss_units,
                                                 c_hs_units, Hkv, units, n0, C, pos, modality, round_id, m_ss, next_pos,
-                                                ss, mod, rnd);
+                                                ss, mod, rnd, static_cast<const uint4*>(kraw_in),
+                                                static_cast<uint4*>(kraw_c));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   chunk_meta_kernel<<<(S + 127) / 128, 128, 0, st>>>(len, next_pos, ss, n0 + C, C, S);

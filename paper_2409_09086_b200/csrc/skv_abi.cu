@@ -105,6 +105,17 @@ struct skv_ctx {
   float* part = nullptr;
   int32_t* counters = nullptr;
   float* acc = nullptr;  // heavy-hitter accumulators [S][L][cap] (SKV_POLICY_HEAVY_HITTER)
+  // RoPE engines: raw key store (cache.keys()), f64 inverse frequencies, the
+  // cache-relative cos/sin table [cap][D/2], rotated q / new-k scratch
+  void* kraw = nullptr;
+  double* inv_freq = nullptr;
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  void* qr = nullptr;
+  void* kr = nullptr;
+  void* pqr = nullptr;  // prefill: rotated chunk q / k
+  void* pkr = nullptr;
+  size_t p_tokens = 0;  // S*C capacity of pqr/pkr
   int32_t* kept = nullptr;
   int32_t* first_moved = nullptr;
   float* scores = nullptr;
@@ -192,6 +203,8 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   if (c.capacity < c.recent_len + c.relevant_budget + 1)
     return fail(SKV_EINVAL, "capacity must exceed recent_len + relevant_budget");
   if (c.policy < SKV_POLICY_INF_MLLM || c.policy > SKV_POLICY_NONE) return fail(SKV_EINVAL, "unknown policy");
+  if (c.rope_mode < SKV_ROPE_NONE || c.rope_mode > SKV_ROPE_ORIGINAL) return fail(SKV_EINVAL, "unknown rope mode");
+  if (c.rope_mode != SKV_ROPE_NONE && !(c.rope_base > 0.f)) return fail(SKV_EINVAL, "rope_base must be > 0");
   // sink_recent_decide: require budget > sink_count >= 0 (policies.py:218-219)
   if (c.policy == SKV_POLICY_SINK_RECENT && !(c.recent_len + c.relevant_budget > c.sink_count && c.sink_count >= 0))
     return fail(SKV_EINVAL, "require budget > sink_count >= 0");
@@ -253,6 +266,32 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   chk(x->alloc(&x->pos_in, x->S * sizeof(int64_t)));
   // heavy-hitter accumulators (engine.py:274): one column per cached token
   if (c.policy == SKV_POLICY_HEAVY_HITTER) chk(x->alloc(&x->acc, SL * (size_t)x->cap * sizeof(float)));
+  if (c.rope_mode != SKV_ROPE_NONE) {
+    const int half = x->D / 2;
+    chk(x->alloc(&x->kraw, kv_bytes));
+    chk(x->alloc(&x->inv_freq, half * sizeof(double)));
+    chk(x->alloc(&x->rope_cos, (size_t)x->cap * half * sizeof(float)));
+    chk(x->alloc(&x->rope_sin, (size_t)x->cap * half * sizeof(float)));
+    chk(x->alloc(&x->qr, (size_t)x->S * x->Hq * x->D * x->elt));
+    chk(x->alloc(&x->kr, (size_t)x->S * x->Hkv * x->D * x->elt));
+    if (e == cudaSuccess) {
+      // inv_freq = base ** (-2 i / D) and the f32 cos/sin of pos * inv_freq,
+      // both in f64 like engine.py:176-178, 200-207; cache-relative positions
+      // are slot indices, so the table covers every position that mode uses
+      std::vector<double> inv(half);
+      for (int i = 0; i < half; ++i) inv[i] = std::pow((double)c.rope_base, -2.0 * i / x->D);
+      std::vector<float> tc((size_t)x->cap * half), ts((size_t)x->cap * half);
+      for (int p = 0; p < x->cap; ++p)
+        for (int i = 0; i < half; ++i) {
+          const double ang = (double)p * inv[i];
+          tc[(size_t)p * half + i] = (float)std::cos(ang);
+          ts[(size_t)p * half + i] = (float)std::sin(ang);
+        }
+      chk(cudaMemcpy(x->inv_freq, inv.data(), half * sizeof(double), cudaMemcpyHostToDevice));
+      chk(cudaMemcpy(x->rope_cos, tc.data(), tc.size() * sizeof(float), cudaMemcpyHostToDevice));
+      chk(cudaMemcpy(x->rope_sin, ts.data(), ts.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+  }
   if (e != cudaSuccess) {
     skv_destroy(x);
     return e == cudaErrorMemoryAllocation ? fail(SKV_ENOMEM, "device allocation failed")
@@ -330,6 +369,47 @@ int skv_timing_read(skv_ctx* x, uint64_t* out, int max_pairs) {
 
 // ------------------------------------------------------------------ decode --
 
+static RopeArgs rope_base_args(skv_ctx* x) {
+  RopeArgs r{};
+  r.Hq = x->Hq;
+  r.Hkv = x->Hkv;
+  r.D = x->D;
+  r.mode = x->cfg.rope_mode;
+  r.inv_freq = x->inv_freq;
+  r.tcos = x->rope_cos;
+  r.tsin = x->rope_sin;
+  r.tab_rows = x->cfg.rope_mode == SKV_ROPE_CACHE_RELATIVE ? x->cap : 0;
+  return r;
+}
+
+// Rotated keys of rows [r0 or first[b], r1) from the raw store: every
+// (stream, layer) block of layers [l0, l1).
+static int rope_rows(skv_ctx* x, int l0, int l1, int r0, int r1, const int32_t* first, cudaStream_t st) {
+  RopeRowsArgs rr{};
+  rr.ra = rope_base_args(x);
+  rr.D = x->D;
+  rr.r0 = r0;
+  rr.r1 = r1;
+  rr.hs = (int64_t)x->cap * x->D;
+  const bool all = l0 == 0 && l1 == x->L;
+  for (int l = l0; l < (all ? l0 + 1 : l1); ++l) {
+    const int64_t off = (int64_t)l * x->kv_layer_stride() * x->elt;
+    rr.raw = static_cast<char*>(x->kraw) + off;
+    rr.rot = static_cast<char*>(x->k) + off;
+    rr.bs = all ? x->kv_layer_stride() : x->kv_stream_stride();
+    rr.first = first ? first + (all ? 0 : (int64_t)l * x->S) : nullptr;
+    if (x->cfg.rope_mode == SKV_ROPE_ORIGINAL) {
+      rr.pos = x->pos + (int64_t)l * x->cap;
+      rr.pos_bs = all ? x->cap : (int64_t)x->L * x->cap;
+      if (all) rr.pos = x->pos;
+    }
+    cudaError_t e = launch_rope_rows(x->cfg.dtype, x->Hkv, all ? x->S * x->L : x->S, rr, st);
+    if (e != cudaSuccess) return cuda_fail(e, "rope kernel launch");
+    x->launches++;
+  }
+  return SKV_OK;
+}
+
 // Where the folded (head-aggregated) row of a recorded step goes: the window
 // ring slot (Inf-MLLM), or added into the heavy-hitter accumulator.
 static void fold_target(skv_ctx* x, int layer, int slot, FoldArgs& f) {
@@ -355,6 +435,28 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   const int n_old = x->n[layer];
   if (n_old + 1 > x->cap)
     return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
+  const void* kraw_in = nullptr;
+  if (x->cfg.rope_mode != SKV_ROPE_NONE) {
+    // rotate q and the new k at the token's position (engine.py:265-268)
+    RopeArgs ra = rope_base_args(x);
+    ra.pos0 = n_old;  // cache-relative: the new token's slot
+    ra.pos_in = pos_dev;
+    ra.next_pos = x->next_pos + layer;
+    ra.np_ss = x->L;
+    ra.q = q;
+    ra.qr = x->qr;
+    ra.q_ss = (int64_t)x->Hq * x->D;
+    ra.k = k;
+    ra.kr = x->kr;
+    ra.k_ss = (int64_t)x->Hkv * x->D;
+    cudaError_t e = launch_rope_tokens(x->cfg.dtype, 1, x->S, ra, st);
+    if (e != cudaSuccess) return cuda_fail(e, "rope kernel launch");
+    x->launches++;
+    x->last_layer = -1;
+    kraw_in = k;
+    q = x->qr;
+    k = x->kr;
+  }
   const int n = n_old + 1;
   const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
   // Few segments (batch-1 GQA, small configs): a static schedule with chunks
@@ -399,6 +501,10 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   a.kin = k;
   a.vin = v;
   a.in_ss = (int64_t)x->Hkv * x->D;
+  if (kraw_in) {
+    a.kraw = kraw_in;
+    a.kc_raw = static_cast<char*>(x->kraw) + kv_off;
+  }
   a.out = out;
   a.o_ss = (int64_t)x->Hq * x->D;
   const int par = x->parity[layer];
@@ -506,12 +612,42 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   const int units = x->D * x->elt / 16;
   const int64_t SLs = x->L;
   const int64_t kv_off = (int64_t)layer * x->kv_layer_stride() * x->elt;
+  const void* kraw_in = nullptr;
+  if (x->cfg.rope_mode != SKV_ROPE_NONE) {
+    // rotate the chunk's q and k at positions n0 + i (cache-relative) or the
+    // original stream positions
+    const size_t need = (size_t)x->S * C;
+    if (x->p_tokens < need) {
+      SKV_CK(cudaStreamSynchronize(st));
+      cudaError_t ea = x->alloc(&x->pqr, need * x->Hq * x->D * x->elt);
+      if (ea == cudaSuccess) ea = x->alloc(&x->pkr, need * x->Hkv * x->D * x->elt);
+      if (ea != cudaSuccess) return cuda_fail(ea, "rope scratch");
+      x->p_tokens = need;
+    }
+    RopeArgs ra = rope_base_args(x);
+    ra.pos0 = n0;
+    ra.next_pos = x->next_pos + layer;
+    ra.np_ss = x->L;
+    ra.q = q;
+    ra.qr = x->pqr;
+    ra.q_ss = (int64_t)C * x->Hq * x->D;
+    ra.k = k;
+    ra.kr = x->pkr;
+    ra.k_ss = (int64_t)C * x->Hkv * x->D;
+    cudaError_t er = launch_rope_tokens(x->cfg.dtype, C, x->S, ra, st);
+    if (er != cudaSuccess) return cuda_fail(er, "rope kernel launch");
+    x->launches++;
+    kraw_in = k;
+    q = x->pqr;
+    k = x->pkr;
+  }
   cudaError_t e = launch_append_chunk(k, v, static_cast<char*>(x->k) + kv_off, static_cast<char*>(x->v) + kv_off,
                                       x->kv_stream_stride() * x->elt / 16, (int64_t)x->cap * units, x->S, x->Hkv,
                                       units, n0, C, x->pos + (int64_t)layer * x->cap,
                                       x->modality + (int64_t)layer * x->cap, x->round_id + (int64_t)layer * x->cap,
                                       SLs * x->cap, x->next_pos + layer, x->len + layer, SLs, modality,
-                                      x->round_value[layer], st);
+                                      x->round_value[layer], st, kraw_in,
+                                      kraw_in ? static_cast<char*>(x->kraw) + kv_off : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "append kernel launch");
   // window rows are recorded for the Inf-MLLM policy only (the index-range
   // baselines need none)
@@ -720,10 +856,16 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     c.len_bs = 1;
     c.acc = x->acc;
     c.acc_bs = x->cap;
+    c.k_raw = static_cast<char*>(x->kraw);
+    c.rope_cr = x->cfg.rope_mode == SKV_ROPE_CACHE_RELATIVE;
     e = launch_compact(x->S * x->L, c, st);
     if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
     x->launches++;
     x->last_layer = -1;
+    if (c.rope_cr) {  // _refresh_rotations (engine.py:339-342): moved keys at their new slots
+      int rc = rope_rows(x, 0, x->L, 0, m, x->first_moved, st);
+      if (rc) return rc;
+    }
   } else {
     for (int l = l0; l < l1; ++l) {
       const int64_t sl0 = l;  // block b = stream s -> (s*L + l)
@@ -767,10 +909,16 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       c.len_bs = x->L;
       c.acc = x->acc ? x->acc + sl0 * x->cap : nullptr;
       c.acc_bs = (int64_t)x->L * x->cap;
+      c.k_raw = x->kraw ? static_cast<char*>(x->kraw) + sl0 * x->kv_layer_stride() * x->elt : nullptr;
+      c.rope_cr = x->cfg.rope_mode == SKV_ROPE_CACHE_RELATIVE;
       e = launch_compact(x->S, c, st);
       if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
       x->launches++;
       x->last_layer = -1;
+      if (c.rope_cr) {
+        int rc = rope_rows(x, l, l + 1, 0, m, x->first_moved, st);
+        if (rc) return rc;
+      }
     }
   }
   if (mode == 1) return SKV_OK;
@@ -838,7 +986,8 @@ int skv_length(const skv_ctx* x, int stream, int layer) {
 int skv_kv_view(skv_ctx* x, int stream, int layer, void** k, void** v) {
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   const int64_t off = ((int64_t)stream * x->L + layer) * x->kv_layer_stride() * x->elt;
-  if (k) *k = static_cast<char*>(x->k) + off;
+  // RoPE engines: the raw keys (KvCache.keys(), cache.py:93-96)
+  if (k) *k = static_cast<char*>(x->kraw ? x->kraw : x->k) + off;
   if (v) *v = static_cast<char*>(x->v) + off;
   return SKV_OK;
 }
@@ -887,7 +1036,8 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   SKV_CK(cudaDeviceSynchronize());
   const int64_t sl = (int64_t)stream * x->L + layer;
   const size_t rb = (size_t)x->D * x->elt;
-  char* kd = static_cast<char*>(x->k) + sl * x->kv_layer_stride() * x->elt;
+  // RoPE engines take raw keys (into the raw store) and rotate them below
+  char* kd = static_cast<char*>(x->kraw ? x->kraw : x->k) + sl * x->kv_layer_stride() * x->elt;
   char* vd = static_cast<char*>(x->v) + sl * x->kv_layer_stride() * x->elt;
   if (k_host && v_host && n > 0) {
     SKV_CK(cudaMemcpy2D(kd, (size_t)x->cap * rb, k_host, (size_t)n * rb, (size_t)n * rb, x->Hkv,
@@ -915,6 +1065,11 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   x->last_layer = -1;
   if (x->acc)  // heavy hitter: injected tokens start with no accumulated mass
     SKV_CK(cudaMemset(x->acc + ((int64_t)stream * x->L + layer) * x->cap, 0, (size_t)x->cap * sizeof(float)));
+  if (x->kraw && n > 0) {  // rotated keys of the injected tokens (every stream of the layer)
+    int rc = rope_rows(x, layer, layer + 1, 0, n, nullptr, nullptr);
+    if (rc) return rc;
+    SKV_CK(cudaDeviceSynchronize());
+  }
   x->n[layer] = n;
   x->wcount[layer] = m;
   x->whead[layer] = m % x->W;

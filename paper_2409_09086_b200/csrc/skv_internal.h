@@ -53,6 +53,8 @@ struct AttnArgs {
   int64_t c_ss, c_hs;   // stream / head strides (elements)
   const void* q;        // q[s][hq][d]     stride q_ss per stream
   int64_t q_ss;
+  const void* kraw;     // RoPE: the raw new k (same layout as kin), stored to kc_raw at slot n_old
+  void* kc_raw;
   const void* kin;      // kin[s][g][d]    stride in_ss per stream
   const void* vin;
   int64_t in_ss;
@@ -154,6 +156,9 @@ struct CompactArgs {
   int64_t len_bs;
   float* acc;            // optional heavy-hitter accumulators acc + b*acc_bs, gathered like a row of length n
   int64_t acc_bs;
+  char* k_raw;           // RoPE: raw key store (layout of k), gathered too
+  int rope_cr;           // RoPE cache-relative: gather raw keys + values only (the rotated
+                         // rows are recomputed from the raw ones afterwards)
 };
 
 cudaError_t launch_compact(int blocks, const CompactArgs& a, cudaStream_t st);
@@ -185,6 +190,44 @@ cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, i
 cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
                                 int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,
                                 int8_t* modality, int32_t* round_id, int64_t m_ss, int64_t* next_pos, int32_t* len,
-                                int64_t ss, int mod, int rnd, cudaStream_t st);
+                                int64_t ss, int mod, int rnd, cudaStream_t st, const void* kraw_in = nullptr,
+                                void* kraw_c = nullptr);
+
+// ----------------------------------------------------------------------------
+// RoPE (RoPE-enabled engines): rotate q / new k, and raw -> rotated key rows
+// ----------------------------------------------------------------------------
+struct RopeArgs {
+  int Hq, Hkv, D;
+  int mode;              // 1 cache-relative (position = slot index), 2 original position
+  int64_t pos0;          // mode 1: position of token 0 (its cache slot)
+  const int64_t* pos_in; // mode 2: explicit positions [S], else next_pos[s * np_ss]
+  const int64_t* next_pos;
+  int64_t np_ss;
+  const double* inv_freq;  // [D/2] base^(-2i/D) in f64 (engine.py:176-178)
+  const float* tcos;     // optional [tab_rows][D/2] f32 table for positions < tab_rows
+  const float* tsin;
+  int64_t tab_rows;
+  const void* q;         // [S][T][Hq][D], stream stride q_ss
+  void* qr;
+  int64_t q_ss;
+  const void* k;         // [S][T][Hkv][D], stream stride k_ss
+  void* kr;
+  int64_t k_ss;
+};
+
+struct RopeRowsArgs {
+  RopeArgs ra;           // D, inv_freq, tables
+  int D;
+  const void* raw;       // raw key store, segment (b, h) at raw + b*bs + h*hs (elements)
+  void* rot;             // rotated key store, same layout
+  int64_t bs, hs;
+  int r0, r1;            // rows [r0, r1) (r0 replaced by first[b] when given)
+  const int32_t* first;  // optional per block
+  const int64_t* pos;    // optional per-row positions pos[b*pos_bs + row] (original mode)
+  int64_t pos_bs;
+};
+
+cudaError_t launch_rope_tokens(int dtype, int tokens, int streams, const RopeArgs& a, cudaStream_t st);
+cudaError_t launch_rope_rows(int dtype, int heads, int blocks, const RopeRowsArgs& a, cudaStream_t st);
 
 }  // namespace skv

@@ -57,6 +57,10 @@ class EngineConfig:
     # "window", "sink_recent", "heavy_hitter" or "none"
     policy: str = "inf_mllm"
     sink_count: int = 4
+    # rotary positions (None: q/k arrive rotated, as in the BASELINE configs;
+    # "cache_relative" / "original": PositionMode, cache.py:24-34)
+    rope: Optional[str] = None
+    rope_base: float = 10000.0
 
     @property
     def budget(self) -> int:
@@ -74,6 +78,8 @@ class StreamEngine:
             raise ValueError(f"unknown head_agg {cfg.head_agg!r}")
         if cfg.policy not in _lib.POLICIES:
             raise ValueError(f"unknown policy {cfg.policy!r}")
+        if cfg.rope not in _lib.ROPE_MODES:
+            raise ValueError(f"unknown rope mode {cfg.rope!r}")
         self.cfg = cfg
         self.lib = _lib.load()
         c = SkvConfig(
@@ -92,6 +98,8 @@ class StreamEngine:
             heads_q_total=cfg.heads_q_total,
             policy=_lib.POLICIES[cfg.policy],
             sink_count=cfg.sink_count,
+            rope_mode=_lib.ROPE_MODES[cfg.rope],
+            rope_base=cfg.rope_base,
         )
         handle = ctypes.c_void_p()
         torch.cuda.init()

@@ -45,6 +45,16 @@ CASES = {
     "sink_mini": dict(S=2, L=1, Hq=4, Hkv=2, D=128, T=256, l=24, r=40, W=16, b=0.01, E=32,
                       dtype="bf16", seed=1008, saddles=0, saddle_gain=1.0, spike_prob=0.0,
                       spike_gain=1.0, out_every=32, policy="sink_recent", sink=4),
+    # Rotary positions driven through the reference Session's own rotary
+    # helpers (engine.py:198-233, 339-342): pre-rotation q/k inputs, raw keys
+    # cached, cache-relative re-rotation after every compaction / original
+    # stream positions.  f32 so the reference's rotated keys are reproduced.
+    "rope_cr": dict(S=1, L=2, Hq=4, Hkv=4, D=64, T=256, l=32, r=32, W=16, b=0.01, E=32,
+                    dtype="f32", seed=1009, saddles=3, saddle_gain=5.0, spike_prob=0.0,
+                    spike_gain=1.0, out_every=32, rope="cache_relative", rope_base=10000.0),
+    "rope_orig_gqa": dict(S=2, L=1, Hq=8, Hkv=2, D=128, T=224, l=32, r=48, W=16, b=0.01, E=32,
+                          dtype="f32", seed=1010, saddles=0, saddle_gain=1.0, spike_prob=0.01,
+                          spike_gain=4.0, out_every=32, rope="original", rope_base=500000.0),
 }
 
 

@@ -26,7 +26,9 @@ REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, REPO)
 
-from streamkv.cache import KvCache, TokenMeta  # noqa: E402  (reference)
+import types  # noqa: E402
+
+from streamkv.cache import KvCache, PositionMode, TokenMeta  # noqa: E402  (reference)
 from streamkv.engine import Session  # noqa: E402
 from streamkv.policies import (  # noqa: E402
     AttentionWindow,
@@ -62,6 +64,18 @@ def run_reference_case(name: str) -> dict:
     caches = [KvCache(L, Hkv, D) for _ in range(S)]
     windows = [[AttentionWindow(c["W"]) for _ in range(L)] for _ in range(S)]
     accs = [[np.zeros(0, dtype=F32) for _ in range(L)] for _ in range(S)]  # engine.py:274
+    rope = c.get("rope")
+    if rope:
+        # the reference Session's rotary helpers on a holder with their state
+        # (engine.py:175-180 init, 198-233 helpers)
+        rot = types.SimpleNamespace()
+        half = D // 2
+        rot._inv_freq = c["rope_base"] ** (-2.0 * np.arange(half, dtype=np.float64) / D)
+        rot._cos = np.zeros((0, half), dtype=F32)
+        rot._sin = np.zeros((0, half), dtype=F32)
+        rot._trig = types.MethodType(Session._trig, rot)
+        mode = PositionMode.CACHE_RELATIVE if rope == "cache_relative" else PositionMode.ORIGINAL
+        rstore = [[np.zeros((Hkv, 0, D), dtype=F32) for _ in range(L)] for _ in range(S)]
     q_all, k_all, v_all = case_inputs(name)  # (T, L, S, H, D)
     T = q_all.shape[0]
     out_steps = []
@@ -74,10 +88,18 @@ def run_reference_case(name: str) -> dict:
                 caches[s].append(layer, k_all[t, layer, s], v_all[t, layer, s], TokenMeta(t))
                 keys = caches[s].keys(layer)
                 vals = caches[s].values(layer)
+                qv = q_all[t, layer, s]
+                if rope:  # engine.py:265-268
+                    n = caches[s].length(layer)
+                    p = n - 1 if mode == PositionMode.CACHE_RELATIVE else t
+                    rk = Session._rotate_one(rot, k_all[t, layer, s], p)
+                    rstore[s][layer] = np.concatenate([rstore[s][layer], rk[:, None, :]], axis=1)
+                    keys = rstore[s][layer]
+                    qv = Session._rotate_one(rot, qv, p)
                 if G > 1:
                     keys = np.repeat(keys, G, axis=0)
                     vals = np.repeat(vals, G, axis=0)
-                probs, o = Session._attend(holder, keys, vals, q_all[t, layer, s])
+                probs, o = Session._attend(holder, keys, vals, qv)
                 row = aggregate_heads(probs, "mean")
                 windows[s][layer].push(row)
                 accs[s][layer] = heavy_hitter_accumulate(accs[s][layer], row)
@@ -112,6 +134,9 @@ def run_reference_case(name: str) -> dict:
                         caches[s].gather_keep(layer, d.kept)
                         windows[s][layer].remap(d.kept)
                         accs[s][layer] = accs[s][layer][d.kept]  # engine.py:335
+                        if rope:  # _refresh_rotations, engine.py:339-342
+                            rstore[s][layer] = Session._rotate_many(
+                                rot, caches[s].keys(layer), caches[s].positions_for(layer, mode))
     final_keys = np.stack([np.stack([caches[s].keys(layer) for layer in range(L)]) for s in range(S)])
     final_pos = np.stack([np.stack([caches[s].original_positions(layer) for layer in range(L)]) for s in range(S)])
     return dict(

@@ -50,7 +50,8 @@ def _engine(c, capacity=None):
     dt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
     cap = capacity or (c["l"] + c["r"] + c["E"])
     return StreamEngine(EngineConfig(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], c["l"], c["r"], c["b"], c["W"],
-                                     cap, dt, policy=c.get("policy", "inf_mllm"), sink_count=c.get("sink", 4)))
+                                     cap, dt, policy=c.get("policy", "inf_mllm"), sink_count=c.get("sink", 4),
+                                     rope=c.get("rope"), rope_base=c.get("rope_base", 10000.0)))
 
 
 def _dev(a, dtype):
@@ -336,3 +337,48 @@ def test_baseline_policy_dropins_match_oracle():
         want = mass_decide(a2, n, r, l)
         np.testing.assert_array_equal(got.kept, want.kept)
         np.testing.assert_array_equal(got.relevant, want.relevant)
+
+
+@pytest.mark.parametrize("mode", ["cache_relative", "original"])
+def test_rope_bf16_engine_vs_oracle(mode):
+    """bf16 RoPE engine (pre-rotation q/k in; raw keys cached; rotated keys
+    attended; cache-relative re-rotation after each compaction) against the
+    oracle restating the reference rotary helpers, with the bf16 rounding of
+    the rotated q / k a bf16 engine stores."""
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    S, L, Hq, Hkv, D = 2, 2, 8, 2, 128
+    l, r, W, E, T = 64, 64, 16, 32, 224
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, l + r + E, torch.bfloat16, rope=mode,
+                                    rope_base=10000.0))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W, rope=mode, rope_round=bf16_round)
+    rng = np.random.default_rng(41)
+    out = torch.empty((S, Hq, D), dtype=torch.float32, device="cuda")
+    kept_buf = torch.full((S, L, l + r), -1, dtype=torch.int32, device="cuda")
+    worst = 0.0
+    for t in range(T):
+        q = bf16_round(rng.standard_normal((L, S, Hq, D)).astype(F32))
+        k = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+        v = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+        for layer in range(L):
+            want, _ = orc.step_layer(layer, q[layer], k[layer], v[layer])
+            eng.decode_layer(layer, _dev(q[layer], torch.bfloat16), _dev(k[layer], torch.bfloat16),
+                             _dev(v[layer], torch.bfloat16), out, record=True)
+            worst = max(worst, rel_err(out.cpu().numpy(), want))
+        orc.advance()
+        if (t + 1) % E == 0:
+            n = orc.length(0, 0)
+            eng.evict(-1, kept_buf)
+            kc = kept_buf.cpu().numpy()
+            for s in range(S):
+                for layer in range(L):
+                    if n > cfg.budget:
+                        ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept,
+                                                        kc[s, layer], n, cfg)
+                        assert ok, (t, s, layer, nbad, gap)
+                    orc.apply(s, layer, kc[s, layer][: min(n, cfg.budget)].astype(np.int64))
+                    kg, _ = eng.kv(s, layer)  # raw keys, like KvCache.keys()
+                    np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+    print(f"rope {mode}: worst output rel err {worst:.2e}")
+    assert worst <= 2e-3
