@@ -213,6 +213,14 @@ int skv_policy_decide(int policy, const float* acc_dev, int n, int recent_len, i
                       int64_t* kept_dev, float* scores_dev, void* stream);
 /* heavy_hitter_accumulate (policies.py:234-243): out[j] = row[j] + acc[j] (j < na), row[j] otherwise. */
 int skv_hh_accumulate(const float* acc_dev, int na, const float* row_dev, int n, float* out_dev, void* stream);
+/* Trace replay (replay.py:139-142): out[i] = f32(probs[live[i]] / total) with
+ * the f64 total of the projected values -- a full-stream attention row seen
+ * through the surviving cache columns. */
+int skv_project_row(const float* probs_dev, int n, const int64_t* live_dev, int m, float* out_dev, void* stream);
+/* retained_mass (metrics.py:46-62) per row: out_dev[r] = f64 sum of
+ * rows[r][kept[i]] over kept[i] < lens[r]; rows_dev [m][row_stride]. */
+int skv_masked_row_sums(const float* rows_dev, int row_stride, const int32_t* lens_dev, int m,
+                        const int64_t* kept_dev, int k, double* out_dev, void* stream);
 /* inf_mllm_decide over a device window: rows_dev [m][row_stride] f32 oldest
  * first, lens_dev [m] int32.  kept_dev [min(n, r+l)] int64; scores_dev optional
  * [n-l] f32 biased scores.  Returns the kept count (>= 0) or an error. */

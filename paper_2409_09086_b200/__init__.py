@@ -28,6 +28,9 @@ from .policies import (
     top_k_indices,
     window_mean_scores,
 )
+from .metrics import MetricsRow, planted_recall, retained_mass, topk_overlap
+from .replay import ReplayResult, replay_trace
 from .tensorops import attend
+from .traceio import TraceFormatError, read_trace, read_trace_file
 
 __version__ = "0.1.0"

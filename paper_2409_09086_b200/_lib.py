@@ -90,6 +90,8 @@ SIGNATURES = {
     "skv_decide": (_I, [_P, _I, _P, _I, _I, _I, _I, _F, _P, _P, _P]),
     "skv_policy_decide": (_I, [_I, _P, _I, _I, _I, _I, _P, _P, _P]),
     "skv_hh_accumulate": (_I, [_P, _I, _P, _I, _P, _P]),
+    "skv_project_row": (_I, [_P, _I, _P, _I, _P, _P]),
+    "skv_masked_row_sums": (_I, [_P, _I, _P, _I, _P, _I, _P, _P]),
     "skv_window_scores": (_I, [_P, _I, _P, _I, _I, _I, _F, _I, _P, _P]),
     "skv_gather_rows": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "skv_attend": (_I, [_P, _P, _I, _I, _I, _I64, _P, _P, _P, _P]),

@@ -196,6 +196,17 @@ __device__ __forceinline__ void issue_s(uint32_t tmem, uint64_t dq0, uint64_t dk
 }
 }  // namespace pf
 
+// Instrumentation timeline (a.prof and a.timeline): CTA 0's MMA thread logs
+// (event, clock) pairs after the per-CTA counters.
+#define PF_T(ev)                                                                  \
+  do {                                                                            \
+    if (tl && tln < 2000) {                                                       \
+      tl[2 * tln] = (ev);                                                         \
+      tl[2 * tln + 1] = clock64();                                                \
+      ++tln;                                                                      \
+    }                                                                             \
+  } while (0)
+
 // CTA (pair p, head h, stream s): Q tiles t0 = 2p and t0 + 1 (if it exists).
 __global__ void __launch_bounds__(pf::THREADS, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
@@ -306,8 +317,12 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
         const uint64_t dq0 = smem_desc(smem_u32(smem + SQ), 16, 1024);
         const uint64_t dk0 = smem_desc(smem_u32(smem + SK), 16, 1024);
         const uint64_t dv0 = smem_desc(smem_u32(smem + SV), REGION, 1024);
+        unsigned long long* tl = (a.prof && a.timeline && blockIdx.x == 0) ? a.prof + 16 * gridDim.x : nullptr;
+        int tln = 0;
         mbar_wait(q_full, 0);
+        PF_T(1);
         PF_WAIT(0, &k_full[0], 0);
+        PF_T(2);
         tc_fence_after();
         const bool skip_s = a.dbg == 2 || a.dbg == 3;
         issue_s(tmem, dq0, dk0, id_s, 0, 0, skip_s, s_full);
@@ -316,14 +331,18 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
         for (int j = 0; j < nkv_max; ++j) {
           const int st = j % STAGES;
           const bool next = j + 1 < nkv_max;
+          PF_T(10);
           PF_WAIT(2, &v_conv[st], (j / STAGES) & 1);
+          PF_T(11);
           tc_fence_after();
           const uint64_t dv = dv0 + (uint64_t)(st * (TILE >> 4));
 #pragma unroll
           for (int i = 0; i < QT; ++i) {
             const int nk = i ? nkv1 : nkv0;
             if (j >= nk) continue;
+            PF_T(20 + i);
             PF_WAIT(3, &p_full[i], j & 1);
+            PF_T(30 + i);
             tc_fence_after();
             const long long tp0 = prof ? clock64() : 0;
             if (a.dbg != 2 && a.dbg != 4) {
@@ -336,7 +355,9 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
             if (prof) pacc1 += clock64() - tp0;
             if (j + 1 < nk) {
               if (i == 0 || nkv0 <= j + 1) {  // first S of tile j+1: its K must have landed
+                PF_T(40);
                 PF_WAIT(0, &k_full[(j + 1) % STAGES], ((j + 1) / STAGES) & 1);
+                PF_T(41);
                 tc_fence_after();
               }
               const long long tq0 = prof ? clock64() : 0;
@@ -344,6 +365,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
               if (prof) pacc4 += clock64() - tq0;
             }
           }
+          PF_T(50);
           mma_commit(&v_empty[st]);
           if (next) mma_commit(&k_empty[(j + 1) % STAGES]);
         }
@@ -587,6 +609,7 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
   PrefillArgs a = a_in;
   if (g_prof) a.prof = g_prof;
   if (const char* d = getenv("SKV_PF_DBG")) a.dbg = atoi(d);
+  if (const char* d = getenv("SKV_PF_TL")) a.timeline = atoi(d);
   EncodeFn enc = encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap qmap, kmap, vmap;

@@ -288,6 +288,73 @@ cudaError_t launch_hh_accumulate(const float* acc, int na, const float* row, int
   return cudaGetLastError();
 }
 
+// replay_trace's projection (replay.py:139-142): out[i] = f32(f64(probs[live[i]]) / sum),
+// sum = the f64 total of the projected values (one block).
+__global__ void __launch_bounds__(1024) project_row_kernel(const float* __restrict__ probs, int n,
+                                                           const int64_t* __restrict__ live, int m,
+                                                           float* __restrict__ out) {
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t c = live[i];
+    acc += (c >= 0 && c < n) ? (double)probs[c] : 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) part[0] = v;
+  }
+  __syncthreads();
+  const double total = part[0];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t c = live[i];
+    const double p = (c >= 0 && c < n) ? (double)probs[c] : 0.0;
+    out[i] = total > 0.0 ? (float)(p / total) : (float)p;
+  }
+}
+
+// retained_mass's per-row sums (metrics.py:46-62): out[r] = f64 sum of
+// rows[r][kept[i]] over kept[i] < lens[r].  One block per row.
+__global__ void __launch_bounds__(256) masked_row_sums_kernel(const float* __restrict__ rows, int row_stride,
+                                                              const int32_t* __restrict__ lens,
+                                                              const int64_t* __restrict__ kept, int k,
+                                                              double* __restrict__ out) {
+  __shared__ double part[8];
+  const int r = blockIdx.x;
+  const int len = lens[r];
+  const float* row = rows + (int64_t)r * row_stride;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const int64_t c = kept[i];
+    if (c >= 0 && c < len) acc += (double)row[c];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += part[w];
+    out[r] = v;
+  }
+}
+
+cudaError_t launch_project_row(const float* probs, int n, const int64_t* live, int m, float* out, cudaStream_t st) {
+  project_row_kernel<<<1, 1024, 0, st>>>(probs, n, live, m, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_masked_row_sums(const float* rows, int row_stride, const int32_t* lens, int m, const int64_t* kept,
+                                   int k, double* out, cudaStream_t st) {
+  masked_row_sums_kernel<<<m, 256, 0, st>>>(rows, row_stride, lens, kept, k, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_topk(const float* scores, int n, int k, int64_t* out, cudaStream_t st) {
   topk_kernel<<<1, kSelThreads, 0, st>>>(scores, n, k, out);
   return cudaGetLastError();

@@ -1191,6 +1191,25 @@ int skv_policy_decide(int policy, const float* acc, int n, int recent_len, int r
   return std::min(n, recent_len + relevant_budget);
 }
 
+int skv_project_row(const float* probs, int n, const int64_t* live, int m, float* out, void* stream) {
+  if (n < 0 || m < 0) return fail(SKV_EINVAL, "lengths must be >= 0");
+  if (m == 0) return SKV_OK;
+  if (!probs || !live || !out) return fail(SKV_EINVAL, "null argument");
+  cudaError_t e = launch_project_row(probs, n, live, m, out, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "projection kernel launch");
+  return SKV_OK;
+}
+
+int skv_masked_row_sums(const float* rows, int row_stride, const int32_t* lens, int m, const int64_t* kept, int k,
+                        double* out, void* stream) {
+  if (m < 0 || k < 0 || row_stride < 0) return fail(SKV_EINVAL, "lengths must be >= 0");
+  if (m == 0) return SKV_OK;
+  if (!rows || !lens || !out || (k > 0 && !kept)) return fail(SKV_EINVAL, "null argument");
+  cudaError_t e = launch_masked_row_sums(rows, row_stride, lens, m, kept, k, out, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "row-sum kernel launch");
+  return SKV_OK;
+}
+
 int skv_hh_accumulate(const float* acc, int na, const float* row, int n, float* out, void* stream) {
   if (na < 0 || n < 0) return fail(SKV_EINVAL, "lengths must be >= 0");
   if (na > n) return fail(SKV_EINVAL, "accumulator longer than the new row");

@@ -119,6 +119,9 @@ struct SelectArgs {
 };
 
 cudaError_t launch_select(int batches, const SelectArgs& a, cudaStream_t st);
+cudaError_t launch_project_row(const float* probs, int n, const int64_t* live, int m, float* out, cudaStream_t st);
+cudaError_t launch_masked_row_sums(const float* rows, int row_stride, const int32_t* lens, int m, const int64_t* kept,
+                                   int k, double* out, cudaStream_t st);
 // heavy_hitter_accumulate (policies.py:234-243): out[j] = row[j] + (j < na ? acc[j] : 0)
 cudaError_t launch_hh_accumulate(const float* acc, int na, const float* row, int n, float* out, cudaStream_t st);
 cudaError_t launch_topk(const float* scores, int n, int k, int64_t* out, cudaStream_t st);
@@ -178,6 +181,7 @@ struct PrefillArgs {
   float* st;            // optional [S][W][Hq][2] (max, sum)
   unsigned long long* prof;  // optional per-CTA cycle counters [grid][16] (instrumentation)
   int dbg;              // instrumentation: 1 skip softmax math, 2 skip MMAs
+  int timeline;         // instrumentation: CTA 0's MMA-thread event timeline into prof
   int* ovf;             // optional: += count of V elements saturated to fp16 (|v| > 65504)
 };
 

@@ -33,12 +33,23 @@ if os.environ.get("PROF"):
     import numpy as np
     nqt = (C + 127) // 128
     grid = H * S * ((nqt + 1) // 2)
-    buf = torch.zeros((grid, 16), dtype=torch.int64, device="cuda")
+    buf = torch.zeros((grid * 16 + 4096,), dtype=torch.int64, device="cuda")
     _lib.check(lib.skv_prefill_profile(P(buf)))
     _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
     torch.cuda.synchronize()
     _lib.check(lib.skv_prefill_profile(None))
-    b = buf.cpu().numpy().astype(np.float64)
+    ball = buf.cpu().numpy()
+    b = ball[: grid * 16].reshape(grid, 16).astype(np.float64)
+    if os.environ.get("SKV_PF_TL"):
+        tl = ball[grid * 16:].reshape(-1, 2)
+        tl = tl[tl[:, 1] > 0]
+        t0 = tl[0, 1]
+        names = {1: "q", 2: "k0", 10: "wait_v", 11: "v_ok", 20: "wait_p0", 21: "wait_p1", 30: "p0_ok", 31: "p1_ok",
+                 40: "wait_k", 41: "k_ok", 50: "tile_done"}
+        prev = t0
+        for ev, t in tl[:120]:
+            print(f"{names.get(int(ev), ev):10s} {t - t0:8d} (+{t - prev})")
+            prev = t
     names = ["mma:k_full", "mma:pv_issue", "mma:v_full", "mma:p_full", "mma:total", "mma:s_issue",
              "wg0:s_full", "wg0:o_done", "wg0:rescales", "wg0:o_final", "wg0:total",
              "wg1:s_full", "wg1:o_done", "wg1:rescales", "wg1:o_final", "wg1:total"]
