@@ -48,12 +48,24 @@ struct Geo {
   static_assert(ITERS >= 1, "tile geometry");
 };
 
-constexpr int kConsumerWarps = 8;
-constexpr int kCT = kConsumerWarps * 32;          // consumer threads
-constexpr int kThreads = kCT + 3 * 32;            // + producer, epilogue, fold warps
+// Consumer warps: NW row-warps x HS head groups.  GQA groups of 4+ heads are
+// split over two warps per row slice (HS = 2: each warp carries half the
+// group's q / accumulators), which doubles the warps per SM on the
+// latency-bound small-batch path at the cost of reading each K/V row twice
+// from shared memory.
+template <int G>
+struct Cw {
+  static constexpr int HS = G >= 4 ? 2 : 1;  // head groups
+  static constexpr int GH = G / HS;          // heads per consumer warp
+  static constexpr int NCW = 8 * HS;         // consumer warps
+  static constexpr int CT = NCW * 32;        // consumer threads
+  static constexpr int THREADS = CT + 3 * 32;  // + producer, epilogue, fold warps
+};
 
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kCT) : "memory"); }
-__device__ __forceinline__ void handoff_sync() { asm volatile("bar.sync 2, %0;\n" ::"n"(kCT + 32) : "memory"); }
+template <int CT>
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(CT) : "memory"); }
+template <int CT>
+__device__ __forceinline__ void handoff_sync() { asm volatile("bar.sync 2, %0;\n" ::"n"(CT + 32) : "memory"); }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -85,7 +97,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-static_assert(kConsumerWarps == 8, "Geo::NW must match kConsumerWarps");
 
 template <typename T, int D, int G>
 struct Smem {
@@ -111,9 +122,10 @@ struct Smem {
 };
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kernel(const AttnArgs a) {
   using Gm = Geo<T, D>;
   using Sm = Smem<T, D, G>;
+  constexpr int HS = Cw<G>::HS, GH = Cw<G>::GH, NCW = Cw<G>::NCW, kCT = Cw<G>::CT;
   constexpr int TT = Gm::TT, RB = Gm::RB, LPR = Gm::LPR, EPL = Gm::EPL, RPW = Gm::RPW;
   constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Sm::STAGES, TILE = Gm::TILE;
   constexpr int PW = D + 2;  // floats per head in a partial
@@ -134,7 +146,6 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   const int c = blockIdx.x, P = gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n_old + a.append;
-  constexpr bool getenv_dbg_t = true;  // TEMP instrumentation
   const int total = a.S * a.Hkv * a.nc;
 
   if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], globaltimer());
@@ -147,10 +158,10 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
 #pragma unroll
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], NW);
+      mbar_init(&empty[i], NCW);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&epi_full[i], NW);
+      mbar_init(&epi_full[i], NCW);
       mbar_init(&epi_empty[i], 1);
     }
     mbar_fence_init();
@@ -166,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     }
   };
 
-  if (warp == NW) {
+  if (warp == NCW) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       bool waited = false;
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     return;
   }
 
-  if (warp == NW + 2) {
+  if (warp == NCW + 2) {
     // ------------------------------------------------- window-row fold warp
     // Materialises the previous recorded step's window row (64-column pieces
     // c, c+P, ...) while the other warps stream K/V.
@@ -254,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     return;
   }
 
-  if (warp == NW + 1) {
+  if (warp == NCW + 1) {
     // ------------------------------------------------------ epilogue warp
     if (!a.prefetch) griddep_wait();  // same layer back to back: the cache slot and metadata
     for (int k = 0;; ++k) {
@@ -331,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       }
     }
     __threadfence();  // every chunk partial of this CTA visible GPU-wide
-    handoff_sync();
+    handoff_sync<kCT>();
     return;
   }
 
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   // q (the previous layer's output in a real model) crosses launches
   if (a.done_prev) {
     if (tid == 0) wait_prev();
-    consumers_sync();
+    consumers_sync<kCT>();
   } else {
     griddep_wait();
   }
@@ -362,16 +373,19 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   for (int cnt = ITERS, off = LPR / 2; cnt > 1; cnt >>= 1, off >>= 1)
     if (c16 & off) ridx += cnt / 2;
   const bool owner = (c16 & (REP - 1)) == 0;
-  float* pbuf = pbuf_all + warp * G * Gm::RPWARP;  // [G][RPW][ITERS]
-  float2 q2[G][E2];
-  float2 o2[G][E2];
-  float m_run[G], l_run[G];
+  // row-warp rw takes rows [rw*RPWARP, ...) of each tile; head group hg the
+  // group's heads [h0, h0 + GH)
+  const int rw = warp % NW, hg = warp / NW, h0 = hg * GH;
+  float* pbuf = pbuf_all + warp * GH * Gm::RPWARP;  // [GH][RPW][ITERS]
+  float2 q2[GH][E2];
+  float2 o2[GH][E2];
+  float m_run[GH], l_run[GH];
   float* lg = nullptr;
   int cur = -1;
   int k = 0;  // chunks handed to the epilogue warp
   bool fresh = true;
   constexpr bool kPrefetchQ = G <= 2;  // register budget
-  float qn[G][EPL];  // prefetched q of the next chunk's segment
+  float qn[GH][EPL];  // prefetched q of the next chunk's segment
   int qn_sigma = -1;
   unsigned long long t_epi_wait = 0;
   for (int i = 0;; ++i) {
@@ -389,15 +403,15 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       if (sigma != cur) {
         if (qn_sigma != sigma) {  // not prefetched (first chunk)
 #pragma unroll
-          for (int h = 0; h < G; ++h)
-            Vec16<T>::load(qn[h], static_cast<const T*>(a.q) + s * a.q_ss + (int64_t)(g * G + h) * D + c16 * EPL);
+          for (int h = 0; h < GH; ++h)
+            Vec16<T>::load(qn[h], static_cast<const T*>(a.q) + s * a.q_ss + (int64_t)(g * G + h0 + h) * D + c16 * EPL);
         }
 #pragma unroll
-        for (int h = 0; h < G; ++h)
+        for (int h = 0; h < GH; ++h)
 #pragma unroll
           for (int e = 0; e < E2; ++e) q2[h][e] = make_float2(qn[h][2 * e], qn[h][2 * e + 1]);
         cur = sigma;
-        lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+        lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G + h0) * a.l_hs : nullptr;
       }
       // prefetch the next chunk's q (its ticket was published with this tile)
       const int un = (kPrefetchQ && a.qpf) ? cring[(k + 1) & 3] : -1;
@@ -405,33 +419,32 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
         const int sn = un / a.nc;
         const int s2 = sn / a.Hkv, g2 = sn - s2 * a.Hkv;
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-          Vec16<T>::load(qn[h], static_cast<const T*>(a.q) + s2 * a.q_ss + (int64_t)(g2 * G + h) * D + c16 * EPL);
+        for (int h = 0; h < GH; ++h)
+          Vec16<T>::load(qn[h], static_cast<const T*>(a.q) + s2 * a.q_ss + (int64_t)(g2 * G + h0 + h) * D + c16 * EPL);
         qn_sigma = sn;
       }
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
+      for (int h = 0; h < GH; ++h) {
 #pragma unroll
         for (int e = 0; e < E2; ++e) o2[h][e] = make_float2(0.f, 0.f);
         m_run[h] = -INFINITY;
         l_run[h] = 0.f;
       }
       fresh = false;
-      if (a.ctat && tid == 0 && getenv_dbg_t) a.ctat[8 * c + 5] = globaltimer();
     }
     const int rows = min(TT, n - ts);
     const unsigned char* ks = tiles + (2 * st) * TILE;
     const unsigned char* vs = ks + TILE;
 
     // ---- q . k for ITERS rows, packed FMA
-    float d[ITERS][G];
+    float d[ITERS][GH];
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
-      const int row = warp * Gm::RPWARP + it * RPW + rsub;
+      const int row = rw * Gm::RPWARP + it * RPW + rsub;
       float kf[EPL];
       Vec16<T>::load(kf, ks + row * RB + c16 * 16);
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
+      for (int h = 0; h < GH; ++h) {
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int e = 0; e < E2; ++e) acc = __ffma2_rn(q2[h][e], make_float2(kf[2 * e], kf[2 * e + 1]), acc);
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
 #pragma unroll
       for (int jj = 0; jj < cnt / 2; ++jj) {
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
+        for (int h = 0; h < GH; ++h) {
           const float send = up ? d[jj][h] : d[jj + cnt / 2][h];
           const float keep = up ? d[jj + cnt / 2][h] : d[jj][h];
           d[jj][h] = keep + __shfl_xor_sync(0xffffffffu, send, off);
@@ -455,26 +468,26 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
 #pragma unroll
     for (int off = REP / 2; off > 0; off >>= 1)
 #pragma unroll
-      for (int h = 0; h < G; ++h) d[0][h] += __shfl_xor_sync(0xffffffffu, d[0][h], off);
+      for (int h = 0; h < GH; ++h) d[0][h] += __shfl_xor_sync(0xffffffffu, d[0][h], off);
 
-    const int myrow = warp * Gm::RPWARP + ridx * RPW + rsub;
+    const int myrow = rw * Gm::RPWARP + ridx * RPW + rsub;
     const bool valid = myrow < rows;
-    float sc[G];
+    float sc[GH];
 #pragma unroll
-    for (int h = 0; h < G; ++h) sc[h] = valid ? d[0][h] * a.scale : -INFINITY;
+    for (int h = 0; h < GH; ++h) sc[h] = valid ? d[0][h] * a.scale : -INFINITY;
     if (lg && owner && valid) {
 #pragma unroll
-      for (int h = 0; h < G; ++h) lg[h * a.l_hs + ts + myrow] = sc[h];
+      for (int h = 0; h < GH; ++h) lg[h * a.l_hs + ts + myrow] = sc[h];
     }
     // ---- online softmax: one row per lane
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
+    for (int h = 0; h < GH; ++h) {
       float mt = sc[h];
 #pragma unroll
       for (int off = 16; off >= REP; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
       const float mn = fmaxf(m_run[h], mt);
       const float alpha = rescale(m_run[h], mn);
-      const float pv = mn == -INFINITY ? 0.f : exp2f((sc[h] - mn) * kLog2e);
+      const float pv = mn == -INFINITY ? 0.f : fast_exp2((sc[h] - mn) * kLog2e);
       l_run[h] = l_run[h] * alpha + (owner ? pv : 0.f);
       const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
@@ -484,19 +497,19 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     }
     __syncwarp();
     // ---- P . V
-    float pr[G][ITERS];
+    float pr[GH][ITERS];
 #pragma unroll
-    for (int h = 0; h < G; ++h)
+    for (int h = 0; h < GH; ++h)
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) pr[h][it] = pbuf[(h * RPW + rsub) * ITERS + it];
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
-      const int row = warp * Gm::RPWARP + it * RPW + rsub;
+      const int row = rw * Gm::RPWARP + it * RPW + rsub;
       if (row < rows) {
         float vf[EPL];
         Vec16<T>::load(vf, vs + row * RB + c16 * 16);
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
+        for (int h = 0; h < GH; ++h) {
           const float2 p2 = make_float2(pr[h][it], pr[h][it]);
 #pragma unroll
           for (int e = 0; e < E2; ++e) o2[h][e] = __ffma2_rn(p2, make_float2(vf[2 * e], vf[2 * e + 1]), o2[h][e]);
@@ -505,7 +518,6 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if (a.ctat && tid == 0 && getenv_dbg_t && i == 0) a.ctat[8 * c + 4] = globaltimer();
     if (!chunk_end) continue;
 
     // ---- chunk done: hand the warp partials to the epilogue warp
@@ -519,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     float* wl = wm + NW * G;
     float* wo = wl + NW * G;
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
+    for (int h = 0; h < GH; ++h) {
       float l = l_run[h];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
@@ -536,11 +548,11 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       }
       if (rsub == 0) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) wo[(warp * G + h) * D + c16 * EPL + e] = o[e];
+        for (int e = 0; e < EPL; ++e) wo[(rw * G + h0 + h) * D + c16 * EPL + e] = o[e];
       }
       if (lane == 0) {
-        wm[warp * G + h] = m_run[h];
-        wl[warp * G + h] = l;
+        wm[rw * G + h0 + h] = m_run[h];
+        wl[rw * G + h0 + h] = l;
       }
     }
     if (warp == 0 && lane == 0) reinterpret_cast<int*>(slot)[0] = u;
@@ -548,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
       // Static schedule (one chunk per CTA, latency-bound small batches): all
       // consumer threads merge the warp partials instead of the single
       // epilogue warp (same arithmetic order), then publish the chunk.
-      consumers_sync();
+      consumers_sync<kCT>();
       const int j = u - sigma * a.nc;
       float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
       for (int idx = tid; idx < G * D; idx += kCT) {
@@ -576,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
         }
       }
       __threadfence();
-      consumers_sync();
+      consumers_sync<kCT>();
       if (tid == 0) atomicAdd(&a.counters[sigma], 1);
     }
     __syncwarp();
@@ -586,10 +598,8 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
   }
   if (a.ctat && tid == 0) {
     a.ctat[8 * c + 3] = globaltimer();
-    if (!getenv_dbg_t) {
-      a.ctat[8 * c + 4] = k;
-      a.ctat[8 * c + 5] = t_epi_wait;
-    }
+    a.ctat[8 * c + 4] = k;
+    a.ctat[8 * c + 5] = t_epi_wait;
   }
   // end marker for the epilogue warp
   {
@@ -600,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, (G >= 4 ? 1 : 2)) decode_kernel(cons
     if (lane == 0) mbar_arrive(&epi_full[sl]);
   }
 
-  handoff_sync();  // this CTA's epilogue warp has published its partials
+  handoff_sync<kCT>();  // this CTA's epilogue warp has published its partials
   if (a.tstamp && tid == 0) atomicMax(&a.tstamp[1], globaltimer());
   if (a.ctat && tid == 0) a.ctat[8 * c + 2] = globaltimer();
   if (tid == 0) {
@@ -727,7 +737,7 @@ static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st)
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(Cw<G>::THREADS);
   cfg.dynamicSmemBytes = Sm::bytes(a.Hq);
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -758,7 +768,7 @@ static int occupancy_t() {
   static int occ = 0;
   if (!occ) {
     cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::bytes(1024));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, kThreads, Sm::bytes(64)) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, Cw<G>::THREADS, Sm::bytes(64)) !=
             cudaSuccess ||
         occ < 1)
       occ = 1;
