@@ -8,4 +8,4 @@ timeout 300 python bench.py --workload cfg0 --no-cpu-baseline > gpurun_out/bench
 timeout 400 python bench.py --workload cfg2 --no-cpu-baseline > gpurun_out/bench_cfg2.log 2>&1
 timeout 400 python bench.py --workload cfg3 --no-cpu-baseline > gpurun_out/bench_cfg3.log 2>&1
 for b in 1024 2048 4096 8192; do timeout 900 python bench.py --workload cfg4 --budget $b --no-cpu-baseline --steps 3 --e2e-steps 0 > gpurun_out/bench_cfg4_$b.log 2>&1; done
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_cfg1.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu1.log 2>&1
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode_kernel|merge_kernel|select_kernel|compact_kernel|fold" -c 600 --csv --log-file gpurun_out/launches_cfg1.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu1.log 2>&1
