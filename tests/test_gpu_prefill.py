@@ -143,3 +143,40 @@ def test_engine_prefill_chunks_match_oracle():
                 np.testing.assert_array_equal(eng.positions(s, 0), orc.kv[s][0].pos[: orc.kv[s][0].n])
     print(f"engine prefill worst output rel err {worst:.2e}")
     assert worst <= 2e-3
+
+
+def test_prefill_config2_full_shape():
+    """BASELINE config 2's image chunk at full shape (4 streams x 32 heads,
+    576 queries over a 4096-token cache + the chunk) against float32 torch,
+    on a sample of heads per stream (all CTAs of the launch run)."""
+    from paper_2409_09086_b200 import _lib
+
+    lib = _lib.load()
+    S, C, H, D, n0, L, W = 4, 576, 32, 128, 4096, 1, 32
+    cap = n0 + C + 64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn((S, C, H, D), generator=g, device="cuda").to(torch.bfloat16)
+    kc = torch.randn((S, L, H, cap, D), generator=g, device="cuda").to(torch.bfloat16)
+    vc = torch.randn((S, L, H, cap, D), generator=g, device="cuda").to(torch.bfloat16)
+    kc[:, :, :, ::101] *= 4
+    out = torch.full((S, C, H, D), float("nan"), dtype=torch.float32, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None,
+                                      ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    scale = 1.0 / np.sqrt(D)
+    worst = 0.0
+    for s in range(S):
+        for h in (0, 7, 19, 31):
+            k = kc[s, 0, h, : n0 + C].float()
+            v = vc[s, 0, h, : n0 + C].float()
+            lg = (q[s, :, h].float() @ k.T) * scale  # [C][n]
+            idx = torch.arange(n0 + C, device="cuda")
+            mask = idx[None, :] <= (n0 + torch.arange(C, device="cuda"))[:, None]
+            p = torch.softmax(lg.masked_fill(~mask, float("-inf")), dim=-1)
+            ref = p @ v
+            err = ((out[s, :, h] - ref).abs().amax(-1) / ref.abs().amax(-1)).max().item()
+            worst = max(worst, err)
+    print(f"config-2 full-shape prefill worst rel err {worst:.2e}")
+    assert worst <= 2e-3
