@@ -54,20 +54,20 @@ __device__ __forceinline__ void fold_piece(const FoldArgs& f, int s, int piece, 
 // walked in batches of eight loads in flight.  Same arithmetic per column as
 // fold_columns (sequential head order, expf, IEEE division) -- bit-identical.
 // MODE 0: mean over heads (divisor agg), MODE 1: max over heads.
-template <int MODE>
+template <int MODE, int HB = 8>
 __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t l_hs, const float* __restrict__ stt,
                                           float* __restrict__ row, int j0, int n, int Hq, float agg, int accum = 0) {
   float acc[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) acc[e] = MODE == 1 ? -INFINITY : 0.f;
   if (j0 + 3 < n) {
-    for (int h0 = 0; h0 < Hq; h0 += 8) {
-      float4 x[8];
+    for (int h0 = 0; h0 < Hq; h0 += HB) {
+      float4 x[HB];
 #pragma unroll
-      for (int b = 0; b < 8; ++b)
+      for (int b = 0; b < HB; ++b)
         if (h0 + b < Hq) x[b] = __ldcs(reinterpret_cast<const float4*>(lg + (int64_t)(h0 + b) * l_hs + j0));
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
+      for (int b = 0; b < HB; ++b) {
         if (h0 + b < Hq) {
           const float M = stt[2 * (h0 + b)], L = stt[2 * (h0 + b) + 1];
           const float v[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
