@@ -15,15 +15,19 @@
 //                                          layer once the per-head (max, sum)
 //                                          of this step exist.
 //
-// Persistent grid (CTAs/SM x SMs) with dynamic chunk scheduling: a chunk is
-// CH 32-token tiles of one (stream, kv-head) segment; the producer warp takes
-// chunk tickets from a global counter and streams the chunk's K and V tiles
-// into a 3-stage shared-memory ring with 1-D bulk async copies (TMA engine,
-// mbarrier completion).  Four consumer warps compute; an epilogue warp merges
-// the consumer warps' chunk partials, publishes them, and the last chunk of a
-// segment merges all chunk partials in chunk order (deterministic) and writes
-// the output and the per-head (max, sum).  The epilogue warp also folds the
-// previous step's window row in between.  With programmatic dependent launch
+// Persistent grid (CTAs/SM x SMs).  A chunk is a run of 64-token tiles of one
+// (stream, kv-head) segment: large batches take 4-tile chunk tickets from a
+// global counter (three in flight), small batches run a static schedule of
+// one 2..8-tile chunk per CTA.  The producer warp streams each K and V tile
+// into a 3-4 stage shared-memory ring with 1-D bulk async copies (TMA engine,
+// mbarrier completion).  8 consumer warps (16 for GQA groups of 4+: two per
+// row slice, each with half the group's heads) compute; a chunk's warp
+// partials are merged by the epilogue warp (dynamic schedule, overlapped with
+// the next chunk) or by all consumer threads (static), published and counted
+// per segment.  merge_kernel (next in the stream, PDL) merges a segment's
+// chunk partials in chunk order as soon as they are all counted and writes the
+// output and per-head (max, sum).  A fold warp materialises the previous
+// recorded step's window row meanwhile.  Under programmatic dependent launch
 // the producer of layer l+1 streams cached K/V while layer l drains; anything
 // that depends on the previous launch waits on griddepcontrol.wait.
 #include "skv_common.cuh"
