@@ -195,9 +195,19 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       int u = a.stat ? c : atomicAdd(&a.sched[0], 1);
       int t1 = a.stat ? total : atomicAdd(&a.sched[0], 1);
       int t2 = a.stat ? total : atomicAdd(&a.sched[0], 1);
+      // Dynamic tickets hand out every segment's chunks but its last first,
+      // then the last chunks (the short remainder chunk, and the one holding
+      // the appended token, which waits for the previous launch): the launch
+      // ends on the smallest work and no producer stalls on the release early.
+      const int nce = a.nc - 1, early = a.S * a.Hkv * nce;
+      auto slot_of = [&](int t) {  // ticket -> chunk slot sigma * nc + j
+        if (a.stat || t >= total) return t;
+        return t < early ? (t / nce) * a.nc + (t % nce) : (t - early) * a.nc + nce;
+      };
+      u = slot_of(u);
       while (u < total) {
         ++taken;
-        const int u_next = t1;
+        const int u_next = slot_of(t1);
         t1 = t2;
         t2 = a.stat ? total : atomicAdd(&a.sched[0], 1);
         // published with this chunk's first tile: lets the consumers prefetch q
@@ -445,13 +455,13 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int row = rw * Gm::RPWARP + it * RPW + rsub;
-      float kf[EPL];
-      Vec16<T>::load(kf, ks + row * RB + c16 * 16);
+      float2 kf[E2];
+      Vec16<T>::load2(kf, ks + row * RB + c16 * 16);
 #pragma unroll
       for (int h = 0; h < GH; ++h) {
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < E2; ++e) acc = __ffma2_rn(q2[h][e], make_float2(kf[2 * e], kf[2 * e + 1]), acc);
+        for (int e = 0; e < E2; ++e) acc = __ffma2_rn(q2[h][e], kf[e], acc);
         d[it][h] = acc.x + acc.y;
       }
     }
@@ -510,13 +520,13 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
     for (int it = 0; it < ITERS; ++it) {
       const int row = rw * Gm::RPWARP + it * RPW + rsub;
       if (row < rows) {
-        float vf[EPL];
-        Vec16<T>::load(vf, vs + row * RB + c16 * 16);
+        float2 vf[E2];
+        Vec16<T>::load2(vf, vs + row * RB + c16 * 16);
 #pragma unroll
         for (int h = 0; h < GH; ++h) {
           const float2 p2 = make_float2(pr[h][it], pr[h][it]);
 #pragma unroll
-          for (int e = 0; e < E2; ++e) o2[h][e] = __ffma2_rn(p2, make_float2(vf[2 * e], vf[2 * e + 1]), o2[h][e]);
+          for (int e = 0; e < E2; ++e) o2[h][e] = __ffma2_rn(p2, vf[e], o2[h][e]);
         }
       }
     }

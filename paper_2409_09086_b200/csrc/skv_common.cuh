@@ -75,6 +75,12 @@ struct Vec16<float> {
     float4 v = *reinterpret_cast<const float4*>(p);
     out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
   }
+  // element pairs, ready as packed FFMA2 operands
+  __device__ __forceinline__ static void load2(float2 (&out)[2], const void* p) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    out[0] = make_float2(v.x, v.y);
+    out[1] = make_float2(v.z, v.w);
+  }
 };
 
 template <>
@@ -88,6 +94,13 @@ struct Vec16<__nv_bfloat16> {
       out[2 * i] = __uint_as_float(w[i] << 16);
       out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
     }
+  }
+  // element pairs built in place as FFMA2 register pairs (no pair-assembly moves)
+  __device__ __forceinline__ static void load2(float2 (&out)[4], const void* p) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
   }
 };
 
