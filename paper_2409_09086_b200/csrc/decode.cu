@@ -77,6 +77,13 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
+// Publication of a chunk partial: a gpu-scope release add after a warp/CTA
+// barrier orders every participating thread's partial stores before the
+// count (release is cumulative), without a membar.gl per thread.
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ float rescale(float m, float M) {
   return m == -INFINITY ? 0.f : exp2f((m - M) * kLog2e);
 }
@@ -325,11 +332,10 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       }
       // publish the chunk partial: the segment's merge CTA starts once all
       // nc chunks of the segment are counted
-      __threadfence();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&epi_empty[sl]);  // slot consumed
-        if (!a.stat) atomicAdd(&a.counters[sigma], 1);
+        if (!a.stat) red_release_add(&a.counters[sigma], 1);
       }
       // append: the new row and (once per stream) its metadata go to slot n_old
       if (a.append && j == a.nc - 1) {
@@ -601,9 +607,8 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
           part[h * PW + D + 1] = x[0];
         }
       }
-      __threadfence();
       consumers_sync<kCT>();
-      if (tid == 0) atomicAdd(&a.counters[sigma], 1);
+      if (tid == 0) red_release_add(&a.counters[sigma], 1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&epi_full[sl]);
@@ -660,7 +665,8 @@ __global__ void __launch_bounds__(G * D) merge_kernel(const AttnArgs a) {
   // segments finish in ticket order, so most merges overlap the streaming of
   // later segments
   if (tid == 0) {
-    while (ld_acquire(&a.counters[sigma]) < nc) __nanosleep(32);
+    while (ld_acquire(&a.counters[sigma]) < nc) {
+    }
     a.counters[sigma] = 0;  // next launch: incremented only after this grid completes
     if (a.mstamp && sigma == 0) a.mstamp[1] = globaltimer();
   }
