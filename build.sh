@@ -7,7 +7,7 @@ SRC=paper_2409_09086_b200/csrc
 mkdir -p build
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v"
 objs=()
-for f in decode select compact prefill rope skv_abi; do
+for f in decode decode_tc select compact prefill rope skv_abi; do
   nvcc $FLAGS -c $SRC/$f.cu -o build/$f.o 2> build/$f.ptxas.log || { cat build/$f.ptxas.log; exit 1; }
   objs+=(build/$f.o)
 done

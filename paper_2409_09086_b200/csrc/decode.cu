@@ -745,6 +745,9 @@ __global__ void fold_kernel(const FoldArgs f, int Hq) {
   fold_piece(f, blockIdx.y, blockIdx.x, gridDim.x, Hq, threadIdx.x, blockDim.x);
 }
 
+template <int D, int G>
+static cudaError_t launch_merge_t(const AttnArgs& a, cudaStream_t st);
+
 template <typename T, int D, int G>
 static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st) {
   using Sm = Smem<T, D, G>;
@@ -767,6 +770,19 @@ static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st)
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<T, D, G>, a);
   if (e != cudaSuccess) return e;
+  return launch_merge_t<D, G>(a, st);
+}
+
+template <int D, int G>
+static cudaError_t launch_merge_t(const AttnArgs& a, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaSuccess;
   // segment merge, also with programmatic dependent launch
   const size_t msmem = (size_t)G * (a.nc + 1) * sizeof(float);
   static bool mattr = false;
@@ -849,6 +865,17 @@ __global__ void __launch_bounds__(256) fold_vec_kernel(const FoldArgs f, int Hq)
     fold_vec4<MODE>(f.logits + s * f.l_ss, f.l_hs, stt, f.rows + s * f.r_ss, j0, f.n, Hq,
                     (float)(f.agg_div ? f.agg_div : Hq), f.accum);
   if (blockIdx.x == 0 && threadIdx.x == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
+}
+
+cudaError_t launch_merge(int head_dim, int group, const AttnArgs& a, cudaStream_t st) {
+  if (head_dim != 128) return cudaErrorInvalidValue;
+  switch (group) {
+    case 1: return launch_merge_t<128, 1>(a, st);
+    case 2: return launch_merge_t<128, 2>(a, st);
+    case 4: return launch_merge_t<128, 4>(a, st);
+    case 8: return launch_merge_t<128, 8>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_fold(int streams, int pieces, const FoldArgs& f, int Hq, cudaStream_t st) {

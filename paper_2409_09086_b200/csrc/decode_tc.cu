@@ -1,0 +1,412 @@
+// K1 small-batch GQA variant: the decode of a latency-bound launch (one
+// chunk per CTA, the static schedule of config 3) on the tensor cores with
+// warp-level mma.sync, so each CTA's math fits in a few hundred instructions
+// per warp instead of ~1000 CUDA-core instructions per 64-token tile.
+//
+// Same contract as decode_kernel (Session._attend + KvCache.append, reference
+// engine.py:235-246, 264): per (stream, kv-head) segment the chunk's partial
+// (o, m, l) per query head, published to merge_kernel.  Per CTA:
+//   * the producer warp loads the chunk's K and V tiles (64 rows x 128 dims,
+//     bf16) with cp.async.bulk.tensor into 128-byte-swizzled shared memory,
+//     before griddepcontrol.wait (PDL prefetch); if the chunk holds the
+//     appended token, the new k/v row is written into its slot after release;
+//   * consumer warp w owns 32 keys: S = Q K^T with mma.m16n8k16 (M = the
+//     group's query heads padded to 16, N = 8 keys, K = 16 dims; B fragments
+//     by ldmatrix from the swizzled tile, conflict-free), softmax over its 32
+//     keys in registers, then O = P V with P taken straight from the S
+//     accumulators (the flash-attention register trick) as two bf16 terms
+//     (hi + lo: a single bf16 P would carry 2^-8 relative error) and V
+//     fragments by ldmatrix.trans;
+//   * the warps' (m, l, o) are merged in chunk order by all consumer threads
+//     and published like the CUDA-core kernel's static path.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "skv_common.cuh"
+#include "skv_fold.cuh"
+#include "skv_internal.h"
+
+namespace skv {
+namespace tcd {
+
+constexpr int D = 128;
+constexpr int TT = 64;                 // rows per tile
+constexpr int REGION = TT * 128;       // [64 rows][64 bf16] swizzled, 8 KB
+constexpr int TILE = 2 * REGION;       // 64 rows x 128 dims, 16 KB
+constexpr int MAXT = 4;                // tiles per chunk (8 warps x 32 keys)
+constexpr int NW = 8;                  // consumer warps
+constexpr int CT = NW * 32;
+constexpr int THREADS = CT + 96;       // + producer, epilogue, fold warps
+constexpr int PW = D + 2;
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+// D = A(16x16, rows 8..15 zero) . B(16x8) + D, bf16 inputs, f32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// byte offset of (row r of a 64-row tile, 16-byte dim chunk cd in 0..15)
+__device__ __forceinline__ uint32_t swz(int r, int cd) {
+  return (uint32_t)((cd >> 3) * REGION + r * 128 + (((cd & 7) ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(CT) : "memory"); }
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ float rescale(float m, float M) { return m == -INFINITY ? 0.f : exp2f((m - M) * kLog2e); }
+
+template <int G>
+struct Smem {
+  static constexpr size_t tiles = (size_t)2 * MAXT * TILE;  // K tiles then V tiles
+  static constexpr size_t slot_floats = 4 + 2 * NW * G + NW * G * D;
+  static constexpr size_t bytes = tiles + slot_floats * 4 + 64 + 1024 + 8 * 1024;  // + bars, align, fold stats
+};
+
+}  // namespace tcd
+
+// One CTA = chunk blockIdx.x (static schedule): segment sigma = c / nc,
+// tiles [j*ch, min((j+1)*ch, nt)).
+template <int G>
+__global__ void __launch_bounds__(tcd::THREADS, 1)
+    decode_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                     const AttnArgs a) {
+  using namespace tcd;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* ktiles = smem;
+  unsigned char* vtiles = smem + MAXT * TILE;
+  float* slot = reinterpret_cast<float*>(smem + Smem<G>::tiles);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slot + Smem<G>::slot_floats);
+  uint64_t* full = bars;      // TMA of every tile
+  uint64_t* row_ok = bars + 1;  // appended row written (chunks that hold it)
+  float* fstats = reinterpret_cast<float*>(bars + 4);  // fold warp: [Hq][2]
+
+  const int c = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n_old + a.append;
+  const int sigma = c / a.nc, j = c - sigma * a.nc;
+  const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+  const int tt0 = j * a.ch, tt1 = min(tt0 + a.ch, a.nt);
+  const int ntile = tt1 - tt0;
+  const int k0 = tt0 * TT;                       // first key of the chunk
+  const int kend = min(tt1 * TT, n);             // keys [k0, kend) are valid
+  const bool has_new = a.append && a.n_old >= k0 && a.n_old < kend;
+  const int seg_row = (int)(((int64_t)s * a.L + a.layer) * a.Hkv + g) * a.cap;
+
+  if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], gtimer());
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_init(row_ok, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------------------------------------------------- producer
+    if (!a.prefetch) griddep_wait();  // same layer back to back: its appended row
+    if (lane == 0) {
+      mbar_arrive_expect_tx(full, 2u * ntile * TILE);
+      for (int t = 0; t < ntile; ++t) {
+        const int y = seg_row + (tt0 + t) * TT;
+        tma_load_2d(ktiles + t * TILE, &kmap, 0, y, full);
+        tma_load_2d(ktiles + t * TILE + REGION, &kmap, 64, y, full);
+        tma_load_2d(vtiles + t * TILE, &vmap, 0, y, full);
+        tma_load_2d(vtiles + t * TILE + REGION, &vmap, 64, y, full);
+      }
+    }
+    if (has_new) {
+      // the new token's k/v (a real model's previous-layer output) cross the
+      // launch: after release, over the TMA copy of its (stale) cache slot
+      griddep_wait();
+      mbar_wait(full, 0);
+      const int kk = a.n_old - k0, t = kk / TT, r = kk % TT;
+      const int cd = lane & 15;
+      const uint4* in = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(lane < 16 ? a.kin : a.vin) +
+                                                       s * a.in_ss + (int64_t)g * D);
+      unsigned char* dst = (lane < 16 ? ktiles : vtiles) + t * TILE + swz(r, cd);
+      *reinterpret_cast<uint4*>(dst) = in[cd];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(row_ok);
+    }
+    return;
+  }
+
+  if (warp == NW + 2) {
+    // ------------------------------------------------- window-row fold warp
+    const FoldArgs& f = a.fold;
+    if (f.n <= 0) return;
+    if (!a.prefetch) griddep_wait();
+    const int P = gridDim.x;
+    const int ppc = (f.n + 63) / 64;
+    for (int piece = c; piece < a.S * ppc; piece += P) {
+      const int s2 = piece / ppc, col0 = (piece - s2 * ppc) * 64;
+      const float* stt = f.stats + s2 * f.st_ss;
+      for (int h = lane; h < a.Hq; h += 32) {
+        fstats[2 * h] = __ldg(stt + 2 * h);
+        fstats[2 * h + 1] = __ldg(stt + 2 * h + 1);
+      }
+      __syncwarp();
+      fold_columns(f, s2, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+      __syncwarp();
+      if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s2 * f.w_ss] = f.n;
+    }
+    return;
+  }
+
+  if (warp == NW + 1) {
+    // ------------------------------------------- epilogue warp: the append
+    if (a.append && j == a.nc - 1) {
+      griddep_wait();  // the new row is the previous layer's output in a real model
+      const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
+      const int64_t in = s * a.in_ss + (int64_t)g * D;
+      for (int q16 = lane; q16 < D * 2 / 16; q16 += 32) {
+        reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.kc) + dst)[q16] =
+            reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.kin) + in)[q16];
+        reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.vc) + dst)[q16] =
+            reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.vin) + in)[q16];
+        if (a.kraw)
+          reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.kc_raw) + dst)[q16] =
+              reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.kraw) + in)[q16];
+      }
+      if (g == 0 && lane == 0) {
+        int64_t* np = a.next_pos + s * a.len_ss;
+        const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
+        a.pos[s * a.m_ss + a.n_old] = pv;
+        a.modality[s * a.m_ss + a.n_old] = 0;
+        a.round_id[s * a.m_ss + a.n_old] = a.round_value;
+        *np = pv + 1;
+        a.len[s * a.len_ss] = n;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  griddep_wait();
+  if (tid == 0) griddep_launch();
+  const int gid = lane >> 2, tig = lane & 3;
+  const bool real = gid < G;  // rows >= G of the 16-row MMA are padding
+  // q A-fragments (row gid = head g*G + gid): a0 = q[16ks + 2tig..+1], a2 = q[16ks + 8 + 2tig..+1]
+  uint32_t qa[8][2];
+  {
+    const uint32_t* qrow =
+        reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(a.q) + s * a.q_ss + (int64_t)(g * G + (real ? gid : 0)) * D);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qa[ks][0] = real ? qrow[8 * ks + tig] : 0u;
+      qa[ks][1] = real ? qrow[8 * ks + 4 + tig] : 0u;
+    }
+  }
+  mbar_wait(full, 0);
+  if (has_new) mbar_wait(row_ok, 0);
+
+  const int wk0 = warp * 32;  // this warp's keys [wk0, wk0 + 32) of the chunk
+  const uint32_t kbase = smem_u32(ktiles), vbase = smem_u32(vtiles);
+  float m = -INFINITY, l = 0.f;
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float* lgrow = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs : nullptr;
+  if (wk0 < ntile * TT) {
+    // ---- S = Q K^T for 4 n-tiles of 8 keys
+    float sacc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+      const int kk = wk0 + nt * 8 + (lane & 7);  // key row this lane addresses
+      const int t = kk >> 6, r = kk & 63;
+#pragma unroll
+      for (int ks2 = 0; ks2 < 4; ++ks2) {  // two k-steps (32 dims) per ldmatrix.x4
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kbase + t * TILE + swz(r, 4 * ks2 + (lane >> 3)), b0, b1, b2, b3);
+        mma16816(sacc[nt], qa[2 * ks2][0], qa[2 * ks2][1], b0, b1);
+        mma16816(sacc[nt], qa[2 * ks2 + 1][0], qa[2 * ks2 + 1][1], b2, b3);
+      }
+    }
+    // ---- softmax over the warp's 32 keys (row gid): logits x = s * scale
+    float x[4][2];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
+        x[nt][e] = key < kend ? sacc[nt][e] * a.scale : -INFINITY;
+        mx = fmaxf(mx, x[nt][e]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    m = mx;
+    float p[4][2];
+    float ls = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        p[nt][e] = m == -INFINITY ? 0.f : fast_exp2((x[nt][e] - m) * kLog2e);
+        ls += p[nt][e];
+      }
+    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+    l = ls;
+    if (lgrow && real) {  // recorded steps: raw f32 logits for the window fold
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
+          if (key < kend) lgrow[key] = x[nt][e];
+        }
+    }
+    // ---- O = P V: k-steps of 16 keys, P from the S accumulators (hi + lo)
+#pragma unroll
+    for (int kq = 0; kq < 2; ++kq) {
+      const uint32_t ah0 = pack_bf16(p[2 * kq][0], p[2 * kq][1]);
+      const uint32_t ah2 = pack_bf16(p[2 * kq + 1][0], p[2 * kq + 1][1]);
+      const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
+      const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
+      const uint32_t al0 = pack_bf16(p[2 * kq][0] - h0.x, p[2 * kq][1] - h0.y);
+      const uint32_t al2 = pack_bf16(p[2 * kq + 1][0] - h2.x, p[2 * kq + 1][1] - h2.y);
+      // lane's ldmatrix.trans row: key 16kq + 8*(matrix & 1) + (lane & 7), dim chunk nb/8 + (matrix >> 1)
+      const int kk = wk0 + 16 * kq + 8 * ((lane >> 3) & 1) + (lane & 7);
+      const int t = kk >> 6, r = kk & 63;
+#pragma unroll
+      for (int np = 0; np < 8; ++np) {  // pairs of n-tiles (16 dims)
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vbase + t * TILE + swz(r, 2 * np + (lane >> 4)), b0, b1, b2, b3);
+        mma16816(o[2 * np], ah0, ah2, b0, b1);
+        mma16816(o[2 * np], al0, al2, b0, b1);
+        mma16816(o[2 * np + 1], ah0, ah2, b2, b3);
+        mma16816(o[2 * np + 1], al0, al2, b2, b3);
+      }
+    }
+  }
+  // ---- warp partials to the slot: wm[NW][G], wl[NW][G], wo[NW][G][D]
+  float* wm = slot + 4;
+  float* wl = wm + NW * G;
+  float* wo = wl + NW * G;
+  if (real) {
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+      *reinterpret_cast<float2*>(wo + (warp * G + gid) * D + 8 * nt + 2 * tig) = make_float2(o[nt][0], o[nt][1]);
+    if (tig == 0) {
+      wm[warp * G + gid] = m;
+      wl[warp * G + gid] = l;
+    }
+  }
+  consumers_sync();
+  // ---- merge the warp partials in warp order and publish the chunk partial
+  float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
+  for (int idx = tid; idx < G * D; idx += CT) {
+    const int h = idx / D, d = idx - h * D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w * G + h]);
+    float f[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) f[w] = rescale(wm[w * G + h], M);
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) acc = fmaf(f[w], wo[(w * G + h) * D + d], acc);
+    part[h * PW + d] = acc;
+    if (d == 0) {
+      float xs[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) xs[w] = f[w] * wl[w * G + h];
+#pragma unroll
+      for (int off = NW / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int w = 0; w < off; ++w) xs[w] = xs[w] + xs[w + off];
+      part[h * PW + D] = M;
+      part[h * PW + D + 1] = xs[0];
+    }
+  }
+  consumers_sync();
+  if (tid == 0) {
+    red_release_add(&a.counters[sigma], 1);
+    if (a.tstamp) atomicMax(&a.tstamp[1], gtimer());
+  }
+}
+
+cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
+  if (a.ch > tcd::MAXT || !a.stat) return cudaErrorInvalidValue;
+  CUtensorMap kmap, vmap;
+  cudaError_t e = make_kv_map(&kmap, a.kc_base, a.total_rows, tcd::TT);
+  if (e != cudaSuccess) return e;
+  e = make_kv_map(&vmap, a.vc_base, a.total_rows, tcd::TT);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(tcd::THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (group == 4) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(decode_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)tcd::Smem<4>::bytes);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    cfg.dynamicSmemBytes = tcd::Smem<4>::bytes;
+    e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<4>, kmap, vmap, a);
+  } else if (group == 8) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(decode_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)tcd::Smem<8>::bytes);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    cfg.dynamicSmemBytes = tcd::Smem<8>::bytes;
+    e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<8>, kmap, vmap, a);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  return launch_merge(128, group, a, st);
+}
+
+}  // namespace skv

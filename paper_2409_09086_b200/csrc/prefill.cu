@@ -588,12 +588,12 @@ EncodeFn encoder() {
 }
 }  // namespace
 
-cudaError_t make_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
+cudaError_t make_kv_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
   EncodeFn enc = encoder();
   if (!enc) return cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)pf::HD, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)pf::HD * 2};
-  cuuint32_t box[2] = {64, pf::BN};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -623,9 +623,9 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  cudaError_t e = make_kv_map(&kmap, kbase, kv_rows);
+  cudaError_t e = make_kv_map(&kmap, kbase, kv_rows, pf::BN);
   if (e != cudaSuccess) return e;
-  e = make_kv_map(&vmap, vbase, kv_rows);
+  e = make_kv_map(&vmap, vbase, kv_rows, pf::BN);
   if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {

@@ -53,6 +53,14 @@ static int use_flags() {
   }
   return env;
 }
+static int use_tc_decode() {  // SKV_TC_DECODE=0 keeps GQA small batches on the CUDA-core kernel
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_TC_DECODE");
+    env = e ? atoi(e) : 1;
+  }
+  return env;
+}
 static int ctas_per_sm_override() {
   const char* e = getenv("SKV_CTAS_PER_SM");
   return e ? std::max(1, atoi(e)) : 0;
@@ -555,7 +563,19 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   f.agg_div = x->Hq_total;
     f.agg_div = x->Hq_total;
   }
-  cudaError_t e = launch_decode(x->cfg.dtype, x->D, x->G, ctas, a, st);
+  cudaError_t e;
+  if (stat && x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && ch <= 4 && use_tc_decode()) {
+    // latency-bound GQA launch: the tensor-core (mma.sync) chunk kernel
+    a.L = x->L;
+    a.layer = layer;
+    a.cap = x->cap;
+    a.kc_base = x->k;
+    a.vc_base = x->v;
+    a.total_rows = (int64_t)x->S * x->L * x->Hkv * x->cap;
+    e = launch_decode_tc(x->G, ctas, a, st);
+  } else {
+    e = launch_decode(x->cfg.dtype, x->D, x->G, ctas, a, st);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
   x->launches += 2;  // decode + segment merge
   x->last_layer = layer;

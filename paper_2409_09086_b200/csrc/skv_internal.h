@@ -77,12 +77,21 @@ struct AttnArgs {
   const int64_t* pos_in;  // optional device [S] explicit positions
   int32_t round_value;
   FoldArgs fold;        // previous step's row (fold.n == 0: none)
+  // tensor-core small-batch path (decode_tc.cu): whole-store views for TMA
+  int L, layer, cap;
+  const void* kc_base;  // K / V store bases, [total_rows][D]
+  const void* vc_base;
+  int64_t total_rows;
   unsigned long long* tstamp;  // optional [2]: min CTA start / max CTA end (%globaltimer ns)
   unsigned long long* ctat;    // optional [P][8]: per-CTA timeline (instrumentation)
   unsigned long long* mstamp;  // optional [8]: merge timeline (instrumentation)
 };
 
 cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st);
+// static-schedule GQA launches (bf16, D = 128, group 4 or 8, chunks <= 4 tiles) on mma.sync
+cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st);
+// the segment merge alone (PDL), after a decode launch
+cudaError_t launch_merge(int head_dim, int group, const AttnArgs& a, cudaStream_t st);
 int decode_ctas_per_sm(int dtype, int head_dim, int group);
 int decode_tile_tokens();
 cudaError_t launch_fold(int streams, int pieces, const FoldArgs& f, int Hq, cudaStream_t st);
@@ -184,6 +193,10 @@ struct PrefillArgs {
   int timeline;         // instrumentation: CTA 0's MMA-thread event timeline into prof
   int* ovf;             // optional: += count of V elements saturated to fp16 (|v| > 65504)
 };
+
+#include <cuda.h>
+// 2-D TMA view of a [rows][128] bf16 store, 64-dim x box_rows boxes, 128-byte swizzle
+cudaError_t make_kv_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 
 cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const void* vbase, int64_t kv_rows,
                            const PrefillArgs& a, cudaStream_t st);
