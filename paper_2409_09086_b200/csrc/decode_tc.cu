@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
   const int seg_row = (int)(((int64_t)s * a.L + a.layer) * a.Hkv + g) * a.cap;
 
   if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], gtimer());
+  if (a.ctat && tid == 0) a.ctat[8 * blockIdx.x] = gtimer();
   if (tid == 0) {
     mbar_init(full, 1);
     mbar_init(row_ok, 1);
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
   // ------------------------------------------------------------ consumers
   griddep_wait();
   if (tid == 0) griddep_launch();
+  if (a.ctat && tid == 0) a.ctat[8 * c + 1] = gtimer();
   const int gid = lane >> 2, tig = lane & 3;
   const bool real = gid < G;  // rows >= G of the 16-row MMA are padding
   // q A-fragments (row gid = head g*G + gid): a0 = q[16ks + 2tig..+1], a2 = q[16ks + 8 + 2tig..+1]
@@ -333,6 +335,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
     }
   }
   consumers_sync();
+  if (a.ctat && tid == 0) a.ctat[8 * c + 3] = gtimer();
   // ---- merge the warp partials in warp order and publish the chunk partial
   float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
   for (int idx = tid; idx < G * D; idx += CT) {
@@ -363,6 +366,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
   if (tid == 0) {
     red_release_add(&a.counters[sigma], 1);
     if (a.tstamp) atomicMax(&a.tstamp[1], gtimer());
+    if (a.ctat) a.ctat[8 * c + 2] = gtimer();
   }
 }
 
