@@ -382,3 +382,48 @@ def test_rope_bf16_engine_vs_oracle(mode):
                     np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
     print(f"rope {mode}: worst output rel err {worst:.2e}")
     assert worst <= 2e-3
+
+
+@pytest.mark.parametrize(
+    "dt,D,G",
+    [("bf16", 64, 1), ("bf16", 64, 4), ("bf16", 128, 2), ("bf16", 128, 8), ("f32", 64, 2), ("f32", 128, 1),
+     ("f32", 128, 8)],
+)
+def test_decode_instantiations_vs_oracle(dt, D, G):
+    """Every (dtype, head_dim, GQA group) decode instantiation -- including the
+    tensor-core chunk kernel for groups of 8 -- over a few eviction periods
+    against the oracle: outputs, kept sets, positions."""
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    S, L, Hkv = 2, 1, 2
+    Hq = Hkv * G
+    l, r, W, E, T = 32, 32, 8, 16, 96
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, l + r + E, tdt))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    rng = np.random.default_rng(G * 1000 + D)
+    out = torch.empty((S, Hq, D), dtype=torch.float32, device="cuda")
+    kept_buf = torch.full((S, L, l + r), -1, dtype=torch.int32, device="cuda")
+    worst = 0.0
+    rnd = bf16_round if dt == "bf16" else (lambda a: a)
+    for t in range(T):
+        q = rnd(rng.standard_normal((S, Hq, D)).astype(F32))
+        k = rnd(rng.standard_normal((S, Hkv, D)).astype(F32))
+        v = rnd(rng.standard_normal((S, Hkv, D)).astype(F32))
+        want, _ = orc.step_layer(0, q, k, v)
+        orc.advance()
+        eng.decode_layer(0, _dev(q, tdt), _dev(k, tdt), _dev(v, tdt), out, record=True)
+        worst = max(worst, rel_err(out.cpu().numpy(), want))
+        if (t + 1) % E == 0:
+            n = orc.length(0, 0)
+            eng.evict(-1, kept_buf)
+            kc = kept_buf.cpu().numpy()
+            for s in range(S):
+                if n > cfg.budget:
+                    ok, nbad, gap = kept_sets_match(orc.scores(s, 0), orc.decide(s, 0).kept, kc[s, 0], n, cfg)
+                    assert ok, (t, s, nbad, gap)
+                orc.apply(s, 0, kc[s, 0][: min(n, cfg.budget)].astype(np.int64))
+                np.testing.assert_array_equal(eng.positions(s, 0), orc.kv[s][0].pos[: orc.kv[s][0].n])
+    print(f"{dt} D={D} G={G}: worst output rel err {worst:.2e}")
+    assert worst <= tol_for(dt)
