@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1319,6 +1320,10 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
                const float* q, float* probs, float* out, void* stream) {
   if (heads < 1 || n < 1) return fail(SKV_EINVAL, "keys must be a non-empty sequence of vectors");
   if (head_dim != 64 && head_dim != 128) return fail(SKV_EINVAL, "device attend needs head_dim 64 or 128");
+  // the stand-alone attend shares one scratch context: calls from several
+  // host threads are serialised (engine contexts have no shared state)
+  static std::mutex att_mu;
+  std::lock_guard<std::mutex> lock(att_mu);
   cudaStream_t st = as_stream(stream);
   const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
   const int ach = std::max(chunk_tiles(1), (nt + 127) / 128);  // at most 128 chunks (segment merge)
