@@ -183,7 +183,7 @@ def run_gpu(args, rank: int, world: int):
     import torch.distributed as dist
 
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
-    from paper_2409_09086_b200.sharding import evict_head_sharded, shard_heads
+    from paper_2409_09086_b200.sharding import evict_head_sharded, gather_results, shard_heads
 
     c = dict(WORKLOADS[args.workload])
     if args.budget:
@@ -361,6 +361,17 @@ def run_gpu(args, rank: int, world: int):
             "note": "skv_decode_step_host per token (pinned host q/k/v in, f32 outputs out) + eviction",
         }
 
+    # the one collective outside the hot path: outputs and kept
+    # sets of every rank gathered after the timed region
+    gathered = None
+    if world > 1:
+        torch.cuda.synchronize()
+        g_out = gather_results(out, dim=2 if sharded else 1)
+        g_kept = kept if sharded else gather_results(kept, dim=0)
+        torch.cuda.synchronize()
+        gathered = {"op": "all_gather (NCCL) of outputs" + ("" if sharded else " and kept sets"),
+                    "bytes": int(g_out.numel() * g_out.element_size() + (0 if sharded else g_kept.numel() * 4)),
+                    "timed": False}
     job_streams = c["streams"] if c["shard"] == "heads" else S * world
     value = job_streams * E / (ms * 1e-3)
     step_bytes_job = _max_over_ranks(step_bytes_rank, 1, dev) * world
@@ -389,6 +400,7 @@ def run_gpu(args, rank: int, world: int):
                           "inputs larger than L2 (the whole KV cache is streamed every token)"),
                    "graph": "one CUDA graph per period, per-layer launches" if use_graph else
                             "eager per-token launches (NCCL all-reduce at eviction)",
+                   "result_gather": gathered,
                    "parallelism": (f"kv-heads sharded x{world} (1 all-reduce of window scores per eviction)"
                                    if sharded else f"stream-partitioned x{world}, no hot-path collective")},
         "roofline": {"bound": "hbm", "kernel": f"decode_kernel<bf16,128,{G}> (+ merge_kernel)",

@@ -41,3 +41,24 @@ def evict_head_sharded(engine, layer: int = -1, kept: Optional[torch.Tensor] = N
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(scores, op=dist.ReduceOp.SUM, group=group)
     return engine.evict_apply(scores, layer, kept)
+
+
+def gather_results(t: torch.Tensor, dim: int = 0, group=None) -> torch.Tensor:
+    """The one collective outside the hot path (SURVEY 8e "collective for
+    results"): every rank's block of per-stream outputs / kept indices,
+    concatenated along ``dim`` in rank order (all ranks receive it).  Single
+    process: ``t`` itself.  Shapes may differ along ``dim`` only."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t
+    world = dist.get_world_size(group)
+    sizes = torch.tensor([t.shape[dim]], dtype=torch.int64, device=t.device)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    cap = int(max(int(x.item()) for x in all_sizes))
+    pad = list(t.shape)
+    pad[dim] = cap
+    buf = torch.zeros(pad, dtype=t.dtype, device=t.device)
+    buf.narrow(dim, 0, t.shape[dim]).copy_(t)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p.narrow(dim, 0, int(n.item())) for p, n in zip(parts, all_sizes)], dim=dim)

@@ -144,3 +144,27 @@ def test_shard_heads_partition():
     assert [b[1] for b in blocks] == [slice(0, 8), slice(8, 16), slice(16, 24), slice(24, 32)]
     with pytest.raises(ValueError):
         shard_heads(8, 4, 3, 0)
+
+
+def _gather_worker(rank, world, port, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_09086_b200.sharding import gather_results
+
+        # rank r holds streams [2r, 2r + r + 1): ragged blocks along dim 0
+        t = torch.arange(10 * rank, 10 * rank + 4 * (rank + 1), dtype=torch.int32).reshape(rank + 1, 4)
+        ret[rank] = gather_results(t).numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_results_concatenates_rank_blocks():
+    mgr = tmp.Manager()
+    ret = mgr.dict()
+    port = 31500 + int(np.random.default_rng().integers(0, 2000))
+    tmp.spawn(_gather_worker, args=(2, port, ret), nprocs=2, join=True)
+    want = np.concatenate([np.arange(0, 4).reshape(1, 4), np.arange(10, 18).reshape(2, 4)]).astype(np.int32)
+    np.testing.assert_array_equal(ret[0], want)
+    np.testing.assert_array_equal(ret[1], want)
