@@ -372,11 +372,34 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
 
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
   if (a.ch > tcd::MAXT || !a.stat) return cudaErrorInvalidValue;
-  CUtensorMap kmap, vmap;
-  cudaError_t e = make_kv_map(&kmap, a.kc_base, a.total_rows, tcd::TT);
-  if (e != cudaSuccess) return e;
-  e = make_kv_map(&vmap, a.vc_base, a.total_rows, tcd::TT);
-  if (e != cudaSuccess) return e;
+  // tensor maps depend only on the store (base, rows): encode once per store
+  // (host-side encoding costs microseconds per launch on batch-1 steps)
+  struct MapCache {
+    const void* kb = nullptr;
+    const void* vb = nullptr;
+    int64_t rows = 0;
+    CUtensorMap k, v;
+  };
+  static thread_local MapCache cache[4];
+  static thread_local int next = 0;
+  MapCache* m = nullptr;
+  for (auto& e : cache)
+    if (e.kb == a.kc_base && e.vb == a.vc_base && e.rows == a.total_rows) m = &e;
+  cudaError_t e = cudaSuccess;
+  if (!m) {
+    m = &cache[next++ % 4];
+    e = make_kv_map(&m->k, a.kc_base, a.total_rows, tcd::TT);
+    if (e == cudaSuccess) e = make_kv_map(&m->v, a.vc_base, a.total_rows, tcd::TT);
+    if (e != cudaSuccess) {
+      m->kb = nullptr;
+      return e;
+    }
+    m->kb = a.kc_base;
+    m->vb = a.vc_base;
+    m->rows = a.total_rows;
+  }
+  const CUtensorMap& kmap = m->k;
+  const CUtensorMap& vmap = m->v;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(tcd::THREADS);

@@ -787,21 +787,30 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
   }
   cudaStream_t s_in = x->hs[0], s_c = x->hs[1], s_out = x->hs[2];
-  for (int l = 0; l < x->L; ++l) {
-    char* dq = static_cast<char*>(x->stage_q) + l * qb;
-    char* dk = static_cast<char*>(x->stage_k) + l * kb;
-    char* dv = static_cast<char*>(x->stage_v) + l * kb;
-    SKV_CK(cudaMemcpyAsync(dq, static_cast<const char*>(q) + l * qb, qb, cudaMemcpyHostToDevice, s_in));
-    SKV_CK(cudaMemcpyAsync(dk, static_cast<const char*>(k) + l * kb, kb, cudaMemcpyHostToDevice, s_in));
-    SKV_CK(cudaMemcpyAsync(dv, static_cast<const char*>(v) + l * kb, kb, cudaMemcpyHostToDevice, s_in));
-    SKV_CK(cudaEventRecord(x->ev_in[l], s_in));
-    SKV_CK(cudaStreamWaitEvent(s_c, x->ev_in[l], 0));
-    float* dout = x->stage_out + l * (ob / sizeof(float));
-    int rc = decode_layer_impl(x, l, dq, dk, dv, nullptr, dout, record, s_c);
-    if (rc) return rc;
-    SKV_CK(cudaEventRecord(x->ev_out[l], s_c));
-    SKV_CK(cudaStreamWaitEvent(s_out, x->ev_out[l], 0));
-    SKV_CK(cudaMemcpyAsync(reinterpret_cast<char*>(out) + l * ob, dout, ob, cudaMemcpyDeviceToHost, s_out));
+  // Layers in (up to) four groups: one copy per tensor and group in, one out,
+  // so the copies of group i+1 / i-1 overlap group i's kernels while the host
+  // issues ~3x fewer runtime calls per token (batch-1 steps are host-bound).
+  const int grp = std::max(1, (x->L + 3) / 4);
+  for (int l0 = 0; l0 < x->L; l0 += grp) {
+    const int nl = std::min(grp, x->L - l0);
+    SKV_CK(cudaMemcpyAsync(static_cast<char*>(x->stage_q) + l0 * qb, static_cast<const char*>(q) + l0 * qb, nl * qb,
+                           cudaMemcpyHostToDevice, s_in));
+    SKV_CK(cudaMemcpyAsync(static_cast<char*>(x->stage_k) + l0 * kb, static_cast<const char*>(k) + l0 * kb, nl * kb,
+                           cudaMemcpyHostToDevice, s_in));
+    SKV_CK(cudaMemcpyAsync(static_cast<char*>(x->stage_v) + l0 * kb, static_cast<const char*>(v) + l0 * kb, nl * kb,
+                           cudaMemcpyHostToDevice, s_in));
+    SKV_CK(cudaEventRecord(x->ev_in[l0], s_in));
+    SKV_CK(cudaStreamWaitEvent(s_c, x->ev_in[l0], 0));
+    for (int l = l0; l < l0 + nl; ++l) {
+      int rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb, static_cast<char*>(x->stage_k) + l * kb,
+                                 static_cast<char*>(x->stage_v) + l * kb, nullptr,
+                                 x->stage_out + l * (ob / sizeof(float)), record, s_c);
+      if (rc) return rc;
+    }
+    SKV_CK(cudaEventRecord(x->ev_out[l0], s_c));
+    SKV_CK(cudaStreamWaitEvent(s_out, x->ev_out[l0], 0));
+    SKV_CK(cudaMemcpyAsync(reinterpret_cast<char*>(out) + l0 * ob, x->stage_out + l0 * (ob / sizeof(float)), nl * ob,
+                           cudaMemcpyDeviceToHost, s_out));
   }
   SKV_CK(cudaStreamSynchronize(s_out));
   SKV_CK(cudaStreamSynchronize(s_c));
