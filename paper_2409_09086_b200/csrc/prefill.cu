@@ -11,16 +11,18 @@
 // One CTA = two 128-query tiles of one head ("ping-pong"): while the softmax
 // warpgroup of one tile turns its S tile into P, the tensor core runs the
 // other tile's MMAs.  Warp 8 (TMA producer) loads both Q tiles once and
-// 128-key K and V tiles into 2-stage rings (cp.async.bulk.tensor, 128-byte
-// swizzle).  Warps 10-11 convert each landed V tile in place from bf16 to
+// 128-key K and V tiles into 3- and 2-stage rings, K one tile ahead of V
+// (cp.async.bulk.tensor, 128-byte swizzle).  Warps 10-11 convert each landed V tile in place from bf16 to
 // fp16 (exact for |v| < 65504; larger values saturate and are counted).
 // Warp 9 owns TMEM and issues tcgen05.mma: S_i = Q_i K^T (bf16, M=N=128)
 // into a 128-column TMEM tile, O_i += P_i V (fp16, M=N=128) with P read
 // straight from TMEM (the .kind::f16 A-from-TMEM form).  fp16 P carries
 // 2^-11 relative rounding (bf16 P would carry 2^-8, above the 2e-3 bf16
 // tolerance for diffuse rows) at one MMA per 16 keys.  Warps 0-3 / 4-7 (one
-// query row per thread) read S with tcgen05.ld, run the online softmax and
-// write P (fp16) back over the first 64 of the S columns it came from.  O is
+// query row per thread) read a whole S row with one tcgen05.ld wait, run the
+// online softmax -- a quarter of the exponentials on the FMA pipe
+// (exp2_poly2), the rest on the SFU -- and write P (fp16) back over the
+// first 64 of the S columns it came from.  O is
 // rescaled lazily: only when a row maximum grows by more than 2^8 (exact --
 // O and the row sum share the stale maximum).
 //
@@ -48,17 +50,19 @@ constexpr int BM = 128;                  // queries per Q tile
 constexpr int BN = 128;                  // keys per K/V tile
 constexpr int HD = 128;                  // head dim
 constexpr int QT = 2;                    // Q tiles per CTA
-constexpr int STAGES = 2;                // K/V ring depth
+constexpr int KST = 3;                   // K ring depth (S(j+1) runs a step ahead of P(j) V(j))
+constexpr int STAGES = 2;                // V ring depth
 constexpr int REGION = 128 * 64 * 2;     // [128 rows][64 16-bit] swizzled region, 16 KB
 constexpr int TILE = 2 * REGION;         // one Q, K or V tile (128 rows x 128 dims), 32 KB
 constexpr int SQ = 0;
 constexpr int SK = SQ + QT * TILE;
-constexpr int SV = SK + STAGES * TILE;
+constexpr int SV = SK + KST * TILE;
 constexpr int SBAR = SV + STAGES * TILE;
 constexpr int SMEM_BYTES = SBAR + 256 + 1024;  // barriers + alignment slack
 constexpr int NCONV = 2;                       // V-conversion warps
 constexpr int THREADS = (8 + 2 + NCONV) * 32;
 constexpr float kRescaleLog2 = 8.f;            // lazy O rescale threshold (log2 units)
+constexpr int kDefaultPoly = 2;                // exp2 pairs (of 8) on the FMA-pipe polynomial (0-4)
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -180,10 +184,48 @@ __device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
   } while (0)
 
 namespace pf {
+// 2^t for two lanes on the FMA pipe instead of the SFU (MUFU.EX2 issues at
+// 16 lanes/clk/SM, the softmax's bound): t = j + f by the 1.5*2^23
+// round-to-nearest shifter, f in [-0.5, 0.5], 2^f by a degree-3 minimax
+// polynomial (relative error 8.3e-5, below fp16 P's 2^-11 rounding), j added
+// into the exponent field.  t is clamped at -125 (the result is then a
+// positive denormal: fp16 0, like the SFU path's flush).
+__device__ __forceinline__ float2 exp2_poly2(float2 t) {
+  t.x = fmaxf(t.x, -125.f);
+  t.y = fmaxf(t.y, -125.f);
+  const float2 sh = make_float2(12582912.f, 12582912.f), nsh = make_float2(-12582912.f, -12582912.f);
+  const float2 m1 = make_float2(-1.f, -1.f);
+  const float2 y = __fadd2_rn(t, sh);                  // round(t) in the low mantissa bits
+  const float2 f = __ffma2_rn(__fadd2_rn(y, nsh), m1, t);  // t - round(t), exact
+  float2 p = __ffma2_rn(f, make_float2(0.055212993f, 0.055212993f), make_float2(0.24271414f, 0.24271414f));
+  p = __ffma2_rn(p, f, make_float2(0.69326216f, 0.69326216f));
+  p = __ffma2_rn(p, f, make_float2(0.99991959f, 0.99991959f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(y.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(y.y) << 23)));
+}
+
+// exp + row-sum + fp16 pack of 64 S columns; POLY of every 8 column pairs
+// go through exp2_poly2, the rest through MUFU.EX2.
+template <int POLY>
+__device__ __forceinline__ void exp_pack64(const uint32_t (&u)[2][32], float2 c12, float2 mo2, float2& psa,
+                                           float2& psb, uint32_t (&pk)[32]) {
+#pragma unroll
+  for (int e = 0; e < 64; e += 2) {
+    const float2 x = make_float2(__uint_as_float(u[e >> 5][e & 31]), __uint_as_float(u[e >> 5][(e + 1) & 31]));
+    const float2 t = __ffma2_rn(x, c12, mo2);  // (s - m) * scale * log2(e), two lanes
+    const int pr = (e >> 1) & 7;
+    const bool poly = POLY == 4 ? (pr & 1) == 0 : POLY == 3 ? (pr == 0 || pr == 3 || pr == 5)
+                    : POLY == 2 ? (pr == 0 || pr == 4) : POLY == 1 ? pr == 0 : false;
+    const float2 pp = poly ? exp2_poly2(t) : make_float2(fast_exp2(t.x), fast_exp2(t.y));
+    if ((e >> 1) & 1) psb = __fadd2_rn(psb, pp); else psa = __fadd2_rn(psa, pp);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(pk[e / 2]) : "f"(pp.y), "f"(pp.x));
+  }
+}
+
 // S_i(j) = Q_i K_j^T: 8 MMAs (K = 16 each) into TMEM columns [128 i, 128 i + 128)
 __device__ __forceinline__ void issue_s(uint32_t tmem, uint64_t dq0, uint64_t dk0, uint32_t id_s, int i, int j,
                                         bool skip, uint64_t* s_full) {
-  const uint64_t dk = dk0 + (uint64_t)((j % STAGES) * (TILE >> 4));
+  const uint64_t dk = dk0 + (uint64_t)((j % KST) * (TILE >> 4));
   const uint64_t dq = dq0 + (uint64_t)(i * (TILE >> 4));
   if (!skip) {
 #pragma unroll
@@ -208,6 +250,7 @@ __device__ __forceinline__ void issue_s(uint32_t tmem, uint64_t dq0, uint64_t dk
   } while (0)
 
 // CTA (pair p, head h, stream s): Q tiles t0 = 2p and t0 + 1 (if it exists).
+template <int POLY, bool PROF>
 __global__ void __launch_bounds__(pf::THREADS, 1)
     prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const PrefillArgs a) {
@@ -216,15 +259,15 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SBAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;        // [STAGES]
-  uint64_t* k_empty = bars + 3;       // [STAGES]
-  uint64_t* v_full = bars + 5;        // [STAGES] TMA landed (bf16)
-  uint64_t* v_conv = bars + 7;        // [STAGES] converted to fp16
-  uint64_t* v_empty = bars + 9;       // [STAGES]
-  uint64_t* s_full = bars + 11;       // [QT] S_i(j) in TMEM
-  uint64_t* p_full = bars + 13;       // [QT] P_i(j) written (and O_i rescaled)
-  uint64_t* o_final = bars + 15;      // [QT] last P_i V done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* k_full = bars + 1;        // [KST]
+  uint64_t* k_empty = bars + 4;       // [KST]
+  uint64_t* v_full = bars + 7;        // [STAGES] TMA landed (bf16)
+  uint64_t* v_conv = bars + 9;        // [STAGES] converted to fp16
+  uint64_t* v_empty = bars + 11;      // [STAGES]
+  uint64_t* s_full = bars + 13;       // [QT] S_i(j) in TMEM
+  uint64_t* p_full = bars + 15;       // [QT] P_i(j) written (and O_i rescaled)
+  uint64_t* o_final = bars + 17;      // [QT] last P_i V done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   // The pairs of one (stream, head) are consecutive CTAs, so its K/V stream
   // is read from DRAM once and served to the other pairs from L2 (a
@@ -250,9 +293,11 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
 
   if (tid == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < KST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < STAGES; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_conv[i], NCONV);
       mbar_init(&v_empty[i], 1);
@@ -276,7 +321,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   unsigned long long t_start = 0;
   // register accumulators, stored once at exit
   unsigned long long pacc0 = 0, pacc1 = 0, pacc2 = 0, pacc3 = 0, pacc4 = 0;
-  if (a.prof && lane == 0 && (warp == 9 || warp == 0 || warp == 4)) {
+  if (PROF && a.prof && lane == 0 && (warp == 9 || warp == 0 || warp == 4)) {
     const int cta = blockIdx.x;
     prof = a.prof + (size_t)cta * 16 + (warp == 9 ? 0 : warp == 0 ? 6 : 11);
     t_start = clock64();
@@ -294,18 +339,24 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
           tma_load_3d(smem + SQ + i * TILE, &qmap, 0, h, row, q_full);
           tma_load_3d(smem + SQ + i * TILE + REGION, &qmap, 64, h, row, q_full);
         }
-        for (int j = 0; j < nkv_max; ++j) {
-          const int st = j % STAGES;
-          const uint32_t ph = ((j / STAGES) & 1) ^ 1;
-          const int y = seg_row + j * BN;
-          mbar_wait(&k_empty[st], ph);
-          mbar_arrive_expect_tx(&k_full[st], TILE);
-          tma_load_2d(smem + SK + st * TILE, &kmap, 0, y, &k_full[st]);
-          tma_load_2d(smem + SK + st * TILE + REGION, &kmap, 64, y, &k_full[st]);
-          mbar_wait(&v_empty[st], ph);
-          mbar_arrive_expect_tx(&v_full[st], TILE);
-          tma_load_2d(smem + SV + st * TILE, &vmap, 0, y, &v_full[st]);
-          tma_load_2d(smem + SV + st * TILE + REGION, &vmap, 64, y, &v_full[st]);
+        // K runs one tile ahead of V (S(j+1) is issued before P(j) V(j))
+        for (int j = 0; j <= nkv_max; ++j) {
+          if (j < nkv_max) {
+            const int st = j % KST;
+            const int y = seg_row + j * BN;
+            mbar_wait(&k_empty[st], ((j / KST) & 1) ^ 1);
+            mbar_arrive_expect_tx(&k_full[st], TILE);
+            tma_load_2d(smem + SK + st * TILE, &kmap, 0, y, &k_full[st]);
+            tma_load_2d(smem + SK + st * TILE + REGION, &kmap, 64, y, &k_full[st]);
+          }
+          if (j > 0) {
+            const int jv = j - 1, st = jv % STAGES;
+            const int y = seg_row + jv * BN;
+            mbar_wait(&v_empty[st], ((jv / STAGES) & 1) ^ 1);
+            mbar_arrive_expect_tx(&v_full[st], TILE);
+            tma_load_2d(smem + SV + st * TILE, &vmap, 0, y, &v_full[st]);
+            tma_load_2d(smem + SV + st * TILE + REGION, &vmap, 64, y, &v_full[st]);
+          }
         }
       }
     } else if (warp == 9) {
@@ -317,7 +368,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
         const uint64_t dq0 = smem_desc(smem_u32(smem + SQ), 16, 1024);
         const uint64_t dk0 = smem_desc(smem_u32(smem + SK), 16, 1024);
         const uint64_t dv0 = smem_desc(smem_u32(smem + SV), REGION, 1024);
-        unsigned long long* tl = (a.prof && a.timeline && blockIdx.x == 0) ? a.prof + 16 * gridDim.x : nullptr;
+        unsigned long long* tl = (PROF && a.prof && a.timeline && blockIdx.x == 0) ? a.prof + 16 * gridDim.x : nullptr;
         int tln = 0;
         mbar_wait(q_full, 0);
         PF_T(1);
@@ -356,7 +407,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
             if (j + 1 < nk) {
               if (i == 0 || nkv0 <= j + 1) {  // first S of tile j+1: its K must have landed
                 PF_T(40);
-                PF_WAIT(0, &k_full[(j + 1) % STAGES], ((j + 1) / STAGES) & 1);
+                PF_WAIT(0, &k_full[(j + 1) % KST], ((j + 1) / KST) & 1);
                 PF_T(41);
                 tc_fence_after();
               }
@@ -367,7 +418,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
           }
           PF_T(50);
           mma_commit(&v_empty[st]);
-          if (next) mma_commit(&k_empty[(j + 1) % STAGES]);
+          if (next) mma_commit(&k_empty[(j + 1) % KST]);
         }
       }
     } else {
@@ -381,7 +432,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
         mbar_wait(&v_full[st], (j / STAGES) & 1);
         uint4* base = reinterpret_cast<uint4*>(smem + SV + st * TILE);
 #pragma unroll 4
-        for (int c = cw * 32 + lane; c < TILE / 16; c += NCONV * 32) {
+        for (int c = cw * 32 + lane; c < ((a.dbg == 5 || a.dbg == 6) ? 0 : TILE / 16); c += NCONV * 32) {
           uint4 x = base[c];
           uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -418,7 +469,11 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     const uint32_t o_base = tmem + lane_off + 256 + i * 128;
     const int wrow = qi - (C - a.W);  // window row index (>= 0: recorded)
     const bool rec = valid && a.lg && wrow >= 0;
-    float* lgrow = rec ? a.lg + ((int64_t)(s * a.W + wrow) * a.Hq + h) * a.lg_cap : nullptr;
+    // row-major [S][W][Hq][lg_cap] (ABI), or column-quad-major (engine):
+    // quad t/4 of recorded row wrow at ((s*Hq + h)*(lg_cap/4) + t/4)*4W + 4*wrow
+    float* lgrow = !rec ? nullptr
+                 : a.lg_t ? a.lg + (int64_t)(s * a.Hq + h) * (a.lg_cap / 4) * (4 * a.W) + 4 * wrow
+                          : a.lg + ((int64_t)(s * a.W + wrow) * a.Hq + h) * a.lg_cap;
     const bool any_rec = __any_sync(0xffffffffu, rec);
     const bool lg_aligned = (reinterpret_cast<uintptr_t>(lgrow) & 15) == 0;
     const float c1 = a.scale * kLog2e;
@@ -427,44 +482,89 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     for (int j = 0; j < nk; ++j) {
       PF_WAIT(0, &s_full[i], j & 1);  // also implies P_i(j-1) V is complete
       tc_fence_after();
-      if (a.dbg == 1) {
+      if (a.dbg == 1 || a.dbg == 6) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[i]);
         continue;
       }
-      // Two passes over the S columns, 64 at a time (register budget): the
-      // row maximum first, then mask / record / exp / pack fp16 P into
-      // columns [0, 64) (S columns [0, 64) are consumed by then).
       const int tbase = j * BN;
       // causal mask needed for some row of the tile (warp-uniform: the last
       // one or two tiles only)
       const bool diag = tbase + BN > tile_min_limit;
-      float mx = -INFINITY;
+      // One pass: all 128 S columns of the row in registers (one TMEM load
+      // wait), row maximum, causal mask, record, exp + row sum + fp16 P into
+      // columns [0, 64), then the (rare) lazy O rescale.
+      uint32_t u[2][2][32];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) tmem_ld32_async(s_base + q4 * 32, u[q4 >> 1][q4 & 1]);
+      tc_wait_ld();
+#define PF_U(e) u[(e) >> 6][((e) >> 5) & 1][(e) & 31]
+      if (diag) {
+#pragma unroll
+        for (int e = 0; e < 128; ++e)
+          if (tbase + e >= limit) PF_U(e) = __float_as_uint(-INFINITY);
+      }
+      float mx4[4] = {m, -INFINITY, -INFINITY, -INFINITY};  // four 3-input max chains
+#pragma unroll
+      for (int e = 0; e < 128; e += 8) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          mx4[c] = fmaxf(mx4[c], fmaxf(__uint_as_float(PF_U(e + 2 * c)), __uint_as_float(PF_U(e + 2 * c + 1))));
+      }
+      const float mn = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));  // max(m, row max)
+      const bool grow = (mn - m) * c1 > kRescaleLog2;  // true on the first tile (m = -inf)
+      const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
+      // O row *= alpha below; P(j-1) V is complete (s_full above)
+      const float alpha = grow ? exp2f((m - mn) * c1) : 1.f;
+      if (grow) m = mn;
+      const float mo = m * c1;
+      const float2 c12 = make_float2(c1, c1), mo2 = make_float2(-mo, -mo);
+      if (any_rec && lgrow && a.dbg != 7) {  // the last W rows of the chunk: raw f32 logits for the window fold
+        if (a.lg_t) {
+          // one 512-byte run per column quad across the warp's recorded rows;
+          // raw q.k (the fold applies the scale: the same f32 product), so the
+          // stores read the live S registers and no temporaries serialise them
+          float* dst = lgrow + (int64_t)(tbase >> 2) * (4 * a.W);
+#pragma unroll
+          for (int e = 0; e < 128; e += 4)
+            *reinterpret_cast<float4*>(dst + (int64_t)(e >> 2) * (4 * a.W)) =
+                make_float4(__uint_as_float(PF_U(e)), __uint_as_float(PF_U(e + 1)), __uint_as_float(PF_U(e + 2)),
+                            __uint_as_float(PF_U(e + 3)));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 128; e += 4) {
+            const int t = tbase + e;
+            const float x0 = __uint_as_float(PF_U(e)) * a.scale;
+            const float x1 = __uint_as_float(PF_U(e + 1)) * a.scale;
+            const float x2 = __uint_as_float(PF_U(e + 2)) * a.scale;
+            const float x3 = __uint_as_float(PF_U(e + 3)) * a.scale;
+            if (t + 3 < limit && lg_aligned) {
+              *reinterpret_cast<float4*>(lgrow + t) = make_float4(x0, x1, x2, x3);
+            } else {
+              if (t < limit) lgrow[t] = x0;
+              if (t + 1 < limit) lgrow[t + 1] = x1;
+              if (t + 2 < limit) lgrow[t + 2] = x2;
+              if (t + 3 < limit) lgrow[t + 3] = x3;
+            }
+          }
+        }
+      }
+      float2 psa = make_float2(0.f, 0.f), psb = make_float2(0.f, 0.f);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        uint32_t u[2][32];
-        tmem_ld32_async(s_base + hh * 64, u[0]);
-        tmem_ld32_async(s_base + hh * 64 + 32, u[1]);
-        tc_wait_ld();
-        if (diag) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (tbase + hh * 64 + e >= limit) u[e >> 5][e & 31] = __float_as_uint(-INFINITY);
-        }
-        float ma = mx, mb = -INFINITY;  // two 3-input max chains
-#pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          ma = fmaxf(ma, fmaxf(__uint_as_float(u[e >> 5][e & 31]), __uint_as_float(u[e >> 5][(e + 1) & 31])));
-          mb = fmaxf(mb, fmaxf(__uint_as_float(u[e >> 5][(e + 2) & 31]), __uint_as_float(u[e >> 5][(e + 3) & 31])));
-        }
-        mx = fmaxf(ma, mb);
+        uint32_t pk[32];
+        // recorded rows (window statistics) stay on the SFU path
+        if (POLY > 0 && !any_rec)
+          exp_pack64<POLY>(u[hh], c12, mo2, psa, psb, pk);
+        else
+          exp_pack64<0>(u[hh], c12, mo2, psa, psb, pk);
+        tmem_st32u(s_base + hh * 32, pk);
       }
-      const float mn = fmaxf(m, mx);
-      const bool grow = (mn - m) * c1 > kRescaleLog2;  // true on the first tile (m = -inf)
-      if (j > 0 && __any_sync(0xffffffffu, grow)) {
-        // O_i row *= 2^((m - mn) c1); P_i(j-1) V is complete (s_full above)
-        const float alpha = grow ? exp2f((m - mn) * c1) : 1.f;
+      const float2 ps = __fadd2_rn(psa, psb);
+      if (grow && j > 0) l *= alpha;
+      l += ps.x + ps.y;
+      if (rescale) {
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
           float o32[32];
@@ -473,62 +573,13 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
           for (int e = 0; e < 32; ++e) o32[e] *= alpha;
           tmem_st32(o_base + c4 * 32, o32);
         }
-        tc_wait_st();
-        if (grow) l *= alpha;
         if (prof) pacc2 += 1;
       }
-      if (grow) m = mn;
-      const float mo = m * c1;
-      const float2 c12 = make_float2(c1, c1), mo2 = make_float2(-mo, -mo);
-      float2 psa = make_float2(0.f, 0.f), psb = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t u[2][32];
-        tmem_ld32_async(s_base + hh * 64, u[0]);
-        tmem_ld32_async(s_base + hh * 64 + 32, u[1]);
-        tc_wait_ld();
-        if (diag) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (tbase + hh * 64 + e >= limit) u[e >> 5][e & 31] = __float_as_uint(-INFINITY);
-        }
-        if (any_rec) {  // the last W rows of the chunk: raw f32 logits for the window fold
-          if (lgrow) {
-#pragma unroll
-            for (int e = 0; e < 64; e += 4) {
-              const int t = tbase + hh * 64 + e;
-              const float x0 = __uint_as_float(u[e >> 5][e & 31]) * a.scale;
-              const float x1 = __uint_as_float(u[e >> 5][(e + 1) & 31]) * a.scale;
-              const float x2 = __uint_as_float(u[e >> 5][(e + 2) & 31]) * a.scale;
-              const float x3 = __uint_as_float(u[e >> 5][(e + 3) & 31]) * a.scale;
-              if (t + 3 < limit && lg_aligned) {
-                *reinterpret_cast<float4*>(lgrow + t) = make_float4(x0, x1, x2, x3);
-              } else {
-                if (t < limit) lgrow[t] = x0;
-                if (t + 1 < limit) lgrow[t + 1] = x1;
-                if (t + 2 < limit) lgrow[t + 2] = x2;
-                if (t + 3 < limit) lgrow[t + 3] = x3;
-              }
-            }
-          }
-        }
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-          const float2 x = make_float2(__uint_as_float(u[e >> 5][e & 31]), __uint_as_float(u[e >> 5][(e + 1) & 31]));
-          const float2 t = __ffma2_rn(x, c12, mo2);  // (s - m) * scale * log2(e), two lanes
-          const float2 pp = make_float2(fast_exp2(t.x), fast_exp2(t.y));
-          if ((e >> 1) & 1) psb = __fadd2_rn(psb, pp); else psa = __fadd2_rn(psa, pp);
-          asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(pk[e / 2]) : "f"(pp.y), "f"(pp.x));
-        }
-        tmem_st32u(s_base + hh * 32, pk);
-      }
-      const float2 ps = __fadd2_rn(psa, psb);
-      l += ps.x + ps.y;
       tc_wait_st();
-      tc_fence_before();
+      if (a.dbg != 13) tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i]);
+#undef PF_U
     }
     if (nk > 0) {
       // epilogue: O / l
@@ -627,19 +678,35 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
   if (e != cudaSuccess) return e;
   e = make_kv_map(&vmap, vbase, kv_rows, pf::BN);
   if (e != cudaSuccess) return e;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::SMEM_BYTES);
+  // exp2 split between the SFU and the FMA pipe: POLY of every 8 column
+  // pairs on the polynomial (SKV_PF_POLY overrides; 0 = SFU only)
+  static int poly = -1;
+  if (poly < 0) {
+    const char* pe = getenv("SKV_PF_POLY");
+    poly = pe ? std::min(4, std::max(0, atoi(pe))) : pf::kDefaultPoly;
+  }
+  // instrumented build (per-CTA wait counters, timeline) only when profiling
+  using Kern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, PrefillArgs);
+  static const Kern kerns[2][5] = {
+      {prefill_kernel<0, false>, prefill_kernel<1, false>, prefill_kernel<2, false>, prefill_kernel<3, false>,
+       prefill_kernel<4, false>},
+      {prefill_kernel<0, true>, prefill_kernel<1, true>, prefill_kernel<2, true>, prefill_kernel<3, true>,
+       prefill_kernel<4, true>}};
+  const int ki = (a.prof ? 5 : 0) + poly;
+  const Kern kern = kerns[a.prof ? 1 : 0][poly];
+  static bool attr[10] = {};
+  if (!attr[ki]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[ki] = true;
   }
   const int nqt = (a.C + pf::BM - 1) / pf::BM;
   dim3 grid((nqt + 1) / 2 * a.Hq * streams);
-  prefill_kernel<<<grid, pf::THREADS, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
+  kern<<<grid, pf::THREADS, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, prefill_kernel);
+    cudaFuncGetAttributes(&fa, kern);
     int optin = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -707,6 +774,94 @@ __global__ void __launch_bounds__(256) fold_rows_kernel(const FoldArgs f, int Hq
     fold_piece(g, s, blockIdx.x, gridDim.x, Hq, threadIdx.x, blockDim.x);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && f.wlen) f.wlen[slot + s * f.w_ss] = n;
+}
+
+// Fold from the column-quad-major record layout (PrefillArgs::lg_t): lane =
+// recorded row w (coalesced 16-byte logit loads across the warp), warp = one
+// column quad; the CTA's [32 rows][32 columns] results go through shared
+// memory so each window row is written in contiguous 128-byte runs.  Same
+// per-column arithmetic as fold_vec4 (sequential heads, expf, IEEE division).
+template <int MODE>
+__global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int Hq, int W, int64_t ncol4, int slot0,
+                                                          int Wring, int n_base, int64_t slot_stride, float scale) {
+  extern __shared__ float fsm[];
+  float* stt = fsm;                 // [32][2 Hq]
+  float* tile = fsm + 64 * Hq;      // [32][33]
+  const int s = blockIdx.y, wg = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = wg * 32 + lane;
+  const bool wv = w < W;
+  for (int x = tid; x < 64 * Hq; x += blockDim.x) {
+    const int wl = x / (2 * Hq), k = x - wl * 2 * Hq;
+    stt[x] = wg * 32 + wl < W ? f.stats[((int64_t)s * W + wg * 32 + wl) * 2 * Hq + k] : 0.f;
+  }
+  __syncthreads();
+  const float* sw = stt + lane * 2 * Hq;
+  const float agg = (float)(f.agg_div ? f.agg_div : Hq);
+  const int64_t hstride = ncol4 * 4 * W;  // floats between heads
+  const int64_t t4 = (int64_t)blockIdx.x * 8 + warp;
+  float acc[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) acc[e] = MODE == 1 ? -INFINITY : 0.f;
+  if (wv && t4 < ncol4) {
+    const float* src = f.logits + (int64_t)s * Hq * hstride + t4 * 4 * W + 4 * w;
+    constexpr int HB = 8;
+    for (int h0 = 0; h0 < Hq; h0 += HB) {
+      float4 x[HB];
+#pragma unroll
+      for (int b = 0; b < HB; ++b)
+        if (h0 + b < Hq) x[b] = __ldcs(reinterpret_cast<const float4*>(src + (int64_t)(h0 + b) * hstride));
+#pragma unroll
+      for (int b = 0; b < HB; ++b) {
+        if (h0 + b < Hq) {
+          const float M = sw[2 * (h0 + b)], L = sw[2 * (h0 + b) + 1];
+          const float v[4] = {__fmul_rn(x[b].x, scale), __fmul_rn(x[b].y, scale), __fmul_rn(x[b].z, scale),
+                             __fmul_rn(x[b].w, scale)};  // logit = f32(q.k * scale)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float p = __fdiv_rn(expf(__fsub_rn(v[e], M)), L);
+            acc[e] = MODE == 1 ? fmaxf(acc[e], p) : __fadd_rn(acc[e], p);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) tile[lane * 33 + warp * 4 + e] = MODE == 1 ? acc[e] : __fdiv_rn(acc[e], agg);
+  __syncthreads();
+  for (int wl = warp; wl < 32; wl += 8) {
+    const int ww = wg * 32 + wl;
+    if (ww >= W) break;
+    const int n = n_base + ww + 1;
+    const int slot = (slot0 + ww) % Wring;
+    float* row = f.rows + (int64_t)slot * slot_stride + (int64_t)s * f.r_ss;
+    const int j = blockIdx.x * 32 + lane;
+    if (j < n) {
+      const float v = tile[wl * 33 + lane];
+      row[j] = (f.accum && j < n - 1) ? __fadd_rn(row[j], v) : v;
+    }
+    if (blockIdx.x == 0 && lane == 0 && f.wlen) f.wlen[slot + s * f.w_ss] = n;
+  }
+}
+
+cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
+                               int64_t lg_cap, int64_t slot_stride, float scale, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  if (Hq > 256 || f.mode == 2 || lg_cap % 128) return cudaErrorInvalidValue;
+  const int nmax = n_base + rows;
+  const size_t smem = (size_t)(64 * Hq + 32 * 33) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fold_rows_t_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    cudaFuncSetAttribute(fold_rows_t_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    attr = true;
+  }
+  dim3 grid((nmax + 31) / 32, streams, (rows + 31) / 32);
+  if (f.mode == 1)
+    fold_rows_t_kernel<1><<<grid, 256, smem, st>>>(f, Hq, rows, lg_cap / 4, slot0, Wring, n_base, slot_stride, scale);
+  else
+    fold_rows_t_kernel<0><<<grid, 256, smem, st>>>(f, Hq, rows, lg_cap / 4, slot0, Wring, n_base, slot_stride, scale);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,

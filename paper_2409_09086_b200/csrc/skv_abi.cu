@@ -133,7 +133,8 @@ struct skv_ctx {
   int32_t* first_moved = nullptr;
   float* scores = nullptr;
   int64_t* pos_in = nullptr;  // staging for explicit positions
-  float* plogits = nullptr;   // prefill: [S][W][Hq][cap] logits of the recorded rows
+  float* plogits = nullptr;   // prefill: [S][Hq][plg_cap/4][W][4] logits of the recorded rows
+  int64_t plg_cap() const { return (cap + 127) / 128 * 128; }
   float* pstats = nullptr;    // prefill: [S][W][Hq][2]
   unsigned long long* tbuf = nullptr;  // timing ring [8192][2]
   unsigned long long* cbuf = nullptr;  // per-CTA timing [64][max_ctas][3]
@@ -561,7 +562,6 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     fold_target(x, layer, x->pend_slot[layer], f);
     f.n = x->pend_n[layer];
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
-  f.agg_div = x->Hq_total;
     f.agg_div = x->Hq_total;
   }
   cudaError_t e;
@@ -632,7 +632,7 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   int rc = flush_pending(x, layer, st);  // keep the window rows in push order
   if (rc) return rc;
   if (!x->plogits) {
-    cudaError_t e = x->alloc(&x->plogits, (size_t)x->S * x->W * x->Hq * x->cap * sizeof(float));
+    cudaError_t e = x->alloc(&x->plogits, (size_t)x->S * x->W * x->Hq * x->plg_cap() * sizeof(float));
     if (e == cudaSuccess) e = x->alloc(&x->pstats, (size_t)x->S * x->W * x->Hq * 2 * sizeof(float));
     if (e != cudaSuccess) return cuda_fail(e, "prefill scratch");
   }
@@ -692,7 +692,8 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   a.scale = x->scale;
   a.out = out;
   a.lg = wrec ? x->plogits : nullptr;
-  a.lg_cap = x->cap;
+  a.lg_cap = x->plg_cap();
+  a.lg_t = 1;
   a.st = wrec ? x->pstats : nullptr;
   e = launch_prefill(q, x->S, x->k, x->v, (int64_t)x->S * x->L * x->Hkv * x->cap, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
@@ -711,8 +712,7 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
     f.w_ss = SLs * x->W;
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
     f.agg_div = x->Hq_total;
-    e = launch_fold_rows(x->S, wrec, f, x->Hq, x->whead[layer], x->W, n0 + C - wrec, (int64_t)x->Hq * x->cap,
-                         (int64_t)x->Hq * 2, x->cap, st);
+    e = launch_fold_rows_t(x->S, wrec, f, x->Hq, x->whead[layer], x->W, n0 + C - wrec, x->plg_cap(), x->cap, x->scale, st);
     if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
     x->launches++;
   }
@@ -1430,6 +1430,7 @@ int skv_prefill_attend(const void* q, int streams, int C, int Hq, int Hkv, const
   a.out = out;
   a.lg = W > 0 ? logits : nullptr;
   a.lg_cap = lg_cap;
+  if (const char* e = getenv("SKV_PF_LGT")) a.lg_t = atoi(e) && lg_cap % 128 == 0;  // experiment: engine layout
   a.st = W > 0 ? stats : nullptr;
   const int64_t rows = (int64_t)streams * L * Hkv * cap;
   cudaError_t e = launch_prefill(q, streams, k_cache, v_cache, rows, a, as_stream(stream));

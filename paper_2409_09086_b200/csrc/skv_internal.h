@@ -192,6 +192,8 @@ struct PrefillArgs {
   int dbg;              // instrumentation: 1 skip softmax math, 2 skip MMAs
   int timeline;         // instrumentation: CTA 0's MMA-thread event timeline into prof
   int* ovf;             // optional: += count of V elements saturated to fp16 (|v| > 65504)
+  int lg_t;             // 1: lg is [S][Hq][lg_cap/4][W][4] raw q.k (unscaled; column quads outermost: the
+                        // recorded rows of a warp store 512 contiguous bytes per quad); lg_cap % 128 == 0
 };
 
 #include <cuda.h>
@@ -203,6 +205,9 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
 void set_prefill_profile(unsigned long long* p);
 cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
                              int64_t lg_rs, int64_t st_rs, int64_t slot_stride, cudaStream_t st);
+// fold of the recorded rows from the column-quad-major layout (PrefillArgs::lg_t)
+cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
+                               int64_t lg_cap, int64_t slot_stride, float scale, cudaStream_t st);
 // strides in 16-byte units; ss = stride of len / next_pos between streams
 cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
                                 int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,

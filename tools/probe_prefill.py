@@ -16,13 +16,17 @@ out = torch.empty((S, C, H, D), dtype=torch.float32, device="cuda")
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 reps = int(os.environ.get("REPS", 5))
+W = int(os.environ.get("REC", 0))  # record the last W rows' logits + stats (engine path)
+lg = torch.empty((S, max(W, 1), H, cap), dtype=torch.float32, device="cuda")
+stt = torch.empty((S, max(W, 1), H, 2), dtype=torch.float32, device="cuda")
+RA = (W, P(lg), cap, P(stt)) if W else (0, None, 0, None)
 for i in range(2):
-    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), *RA, st))
 torch.cuda.synchronize()
 a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
 a.record()
 for i in range(reps):
-    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), *RA, st))
 b.record()
 torch.cuda.synchronize()
 ms = a.elapsed_time(b) / reps
@@ -35,7 +39,7 @@ if os.environ.get("PROF"):
     grid = H * S * ((nqt + 1) // 2)
     buf = torch.zeros((grid * 16 + 4096,), dtype=torch.int64, device="cuda")
     _lib.check(lib.skv_prefill_profile(P(buf)))
-    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), 0, None, 0, None, st))
+    _lib.check(lib.skv_prefill_attend(P(q), S, C, H, H, P(kc), P(vc), L, 0, cap, n0, P(out), *RA, st))
     torch.cuda.synchronize()
     _lib.check(lib.skv_prefill_profile(None))
     ball = buf.cpu().numpy()
