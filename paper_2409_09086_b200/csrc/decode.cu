@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       const float* stt = f.stats + s * f.st_ss;
       for (int h = lane; h < a.Hq; h += 32) {
         fstats[2 * h] = __ldg(stt + 2 * h);
-        fstats[2 * h + 1] = __ldg(stt + 2 * h + 1);
+        fstats[2 * h + 1] = __frcp_rn(__ldg(stt + 2 * h + 1));  // staged as 1/L
       }
       __syncwarp();
       fold_columns(f, s, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(256) fold_vec_kernel(const FoldArgs f, int Hq)
   __shared__ float stt[2 * 256];
   const int s = blockIdx.y;
   const float* sg = f.stats + s * f.st_ss;
-  for (int x = threadIdx.x; x < 2 * Hq; x += blockDim.x) stt[x] = sg[x];
+  for (int x = threadIdx.x; x < 2 * Hq; x += blockDim.x) stt[x] = (x & 1) ? __frcp_rn(sg[x]) : sg[x];  // (M, 1/L)
   __syncthreads();
   const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (j0 < f.n)

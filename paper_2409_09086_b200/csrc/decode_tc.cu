@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       const float* stt = f.stats + s2 * f.st_ss;
       for (int h = lane; h < a.Hq; h += 32) {
         fstats[2 * h] = __ldg(stt + 2 * h);
-        fstats[2 * h + 1] = __ldg(stt + 2 * h + 1);
+        fstats[2 * h + 1] = __frcp_rn(__ldg(stt + 2 * h + 1));  // staged as 1/L
       }
       __syncwarp();
       fold_columns(f, s2, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);

@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(256) fold_rows_kernel(const FoldArgs f, int Hq
   const int slot = (slot0 + w) % Wring;
   const int n = n_base + w + 1;
   const float* sg = f.stats + w * st_rs + s * f.st_ss;
-  for (int x = threadIdx.x; x < 2 * Hq; x += blockDim.x) stt[x] = sg[x];
+  for (int x = threadIdx.x; x < 2 * Hq; x += blockDim.x) stt[x] = (x & 1) ? __frcp_rn(sg[x]) : sg[x];  // (M, 1/L)
   __syncthreads();
   if (vec) {
     const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(256) fold_rows_kernel(const FoldArgs f, int Hq
 // recorded row w (coalesced 16-byte logit loads across the warp), warp = one
 // column quad; the CTA's [32 rows][32 columns] results go through shared
 // memory so each window row is written in contiguous 128-byte runs.  Same
-// per-column arithmetic as fold_vec4 (sequential heads, expf, IEEE division).
+// per-column arithmetic as fold_vec4 (sequential heads, fold_prob).
 template <int MODE>
 __global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int Hq, int W, int64_t ncol4, int slot0,
                                                           int Wring, int n_base, int64_t slot_stride, float scale) {
@@ -793,7 +793,8 @@ __global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int 
   const bool wv = w < W;
   for (int x = tid; x < 64 * Hq; x += blockDim.x) {
     const int wl = x / (2 * Hq), k = x - wl * 2 * Hq;
-    stt[x] = wg * 32 + wl < W ? f.stats[((int64_t)s * W + wg * 32 + wl) * 2 * Hq + k] : 0.f;
+    const float v = wg * 32 + wl < W ? f.stats[((int64_t)s * W + wg * 32 + wl) * 2 * Hq + k] : 1.f;
+    stt[x] = (k & 1) ? __frcp_rn(v) : v;  // (M, 1/L)
   }
   __syncthreads();
   const float* sw = stt + lane * 2 * Hq;
@@ -814,12 +815,12 @@ __global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int 
 #pragma unroll
       for (int b = 0; b < HB; ++b) {
         if (h0 + b < Hq) {
-          const float M = sw[2 * (h0 + b)], L = sw[2 * (h0 + b) + 1];
+          const float M = sw[2 * (h0 + b)], rL = sw[2 * (h0 + b) + 1];
           const float v[4] = {__fmul_rn(x[b].x, scale), __fmul_rn(x[b].y, scale), __fmul_rn(x[b].z, scale),
                              __fmul_rn(x[b].w, scale)};  // logit = f32(q.k * scale)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float p = __fdiv_rn(expf(__fsub_rn(v[e], M)), L);
+            const float p = fold_prob(v[e], M, rL);
             acc[e] = MODE == 1 ? fmaxf(acc[e], p) : __fadd_rn(acc[e], p);
           }
         }

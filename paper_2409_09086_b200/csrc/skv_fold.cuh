@@ -9,10 +9,17 @@
 
 namespace skv {
 
-// row[j] = agg_h p[h][j] with p = expf(x - M_h) / L_h, for j in [c0, c1).
+// p = expf(x - M) * (1/L): the row sum's reciprocal (__frcp_rn, IEEE) is
+// formed once per (row, head) and staged next to M, so the per-column cost is
+// one expf and one multiply (within 1.5 ulp of expf(x - M) / L).
+__device__ __forceinline__ float fold_prob(float x, float M, float rL) { return __fmul_rn(expf(__fsub_rn(x, M)), rL); }
+
+// row[j] = agg_h p[h][j] with p = fold_prob(x, M_h, 1/L_h), for j in [c0, c1).
 // Head order is sequential h = 0..Hq-1 in float32 (aggregate_heads, policies.py:262).
+// stt: staged (M_h, 1/L_h) pairs, or null to read (M_h, L_h) from f.stats.
 __device__ __forceinline__ void fold_columns(const FoldArgs& f, int s, int c0, int c1, int Hq, int tid, int nthreads,
                              const float* stt = nullptr) {
+  const bool staged = stt != nullptr;
   const float* lg = f.logits + s * f.l_ss;
   if (!stt) stt = f.stats + s * f.st_ss;
   float* row = f.rows ? f.rows + s * f.r_ss : nullptr;
@@ -21,8 +28,8 @@ __device__ __forceinline__ void fold_columns(const FoldArgs& f, int s, int c0, i
 #pragma unroll 16
     for (int h = 0; h < Hq; ++h) {
       const float M = stt[2 * h];
-      const float L = stt[2 * h + 1];
-      const float p = __fdiv_rn(expf(__fsub_rn(__ldcs(lg + h * f.l_hs + j), M)), L);
+      const float rL = staged ? stt[2 * h + 1] : __frcp_rn(stt[2 * h + 1]);
+      const float p = fold_prob(__ldcs(lg + h * f.l_hs + j), M, rL);
       if (f.mode == 2) {
         f.probs[s * f.p_ss + h * f.p_hs + j] = p;
       } else if (f.mode == 1) {
@@ -50,9 +57,9 @@ __device__ __forceinline__ void fold_piece(const FoldArgs& f, int s, int piece, 
 
 // Throughput version for stand-alone fold launches: each thread owns four
 // consecutive columns (16-byte logit loads, four independent head-sum
-// chains), the per-head stats are staged in shared memory, and the heads are
-// walked in batches of eight loads in flight.  Same arithmetic per column as
-// fold_columns (sequential head order, expf, IEEE division) -- bit-identical.
+// chains), the per-head (M, 1/L) are staged in shared memory, and the heads
+// are walked in batches of eight loads in flight.  Same arithmetic per column
+// as fold_columns (sequential head order, fold_prob) -- bit-identical.
 // MODE 0: mean over heads (divisor agg), MODE 1: max over heads.
 template <int MODE, int HB = 8>
 __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t l_hs, const float* __restrict__ stt,
@@ -69,11 +76,11 @@ __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t 
 #pragma unroll
       for (int b = 0; b < HB; ++b) {
         if (h0 + b < Hq) {
-          const float M = stt[2 * (h0 + b)], L = stt[2 * (h0 + b) + 1];
+          const float M = stt[2 * (h0 + b)], rL = stt[2 * (h0 + b) + 1];
           const float v[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float p = __fdiv_rn(expf(__fsub_rn(v[e], M)), L);
+            const float p = fold_prob(v[e], M, rL);
             acc[e] = MODE == 1 ? fmaxf(acc[e], p) : __fadd_rn(acc[e], p);
           }
         }
@@ -88,7 +95,7 @@ __device__ __forceinline__ void fold_vec4(const float* __restrict__ lg, int64_t 
     for (int e = 0; e < 4 && j0 + e < n; ++e) {
       float a = MODE == 1 ? -INFINITY : 0.f;
       for (int h = 0; h < Hq; ++h) {
-        const float p = __fdiv_rn(expf(__fsub_rn(__ldcs(lg + (int64_t)h * l_hs + j0 + e), stt[2 * h])), stt[2 * h + 1]);
+        const float p = fold_prob(__ldcs(lg + (int64_t)h * l_hs + j0 + e), stt[2 * h], stt[2 * h + 1]);
         a = MODE == 1 ? fmaxf(a, p) : __fadd_rn(a, p);
       }
       const float v = MODE == 1 ? a : __fdiv_rn(a, agg);
