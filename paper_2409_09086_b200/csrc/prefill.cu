@@ -791,10 +791,19 @@ __global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = wg * 32 + lane;
   const bool wv = w < W;
-  for (int x = tid; x < 64 * Hq; x += blockDim.x) {
-    const int wl = x / (2 * Hq), k = x - wl * 2 * Hq;
-    const float v = wg * 32 + wl < W ? f.stats[((int64_t)s * W + wg * 32 + wl) * 2 * Hq + k] : 1.f;
-    stt[x] = (k & 1) ? __frcp_rn(v) : v;  // (M, 1/L)
+  // stage (M, 1/L) of the 32 rows: eight loads in flight per thread
+  for (int x0 = tid; x0 < 64 * Hq; x0 += 8 * 256) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int x = x0 + i * 256, wl = x / (2 * Hq), k = x - wl * 2 * Hq;
+      v[i] = (x < 64 * Hq && wg * 32 + wl < W) ? f.stats[((int64_t)s * W + wg * 32 + wl) * 2 * Hq + k] : 1.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int x = x0 + i * 256;
+      if (x < 64 * Hq) stt[x] = (x & 1) ? __frcp_rn(v[i]) : v[i];  // (M, 1/L)
+    }
   }
   __syncthreads();
   const float* sw = stt + lane * 2 * Hq;
@@ -806,18 +815,22 @@ __global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int 
   for (int e = 0; e < 4; ++e) acc[e] = MODE == 1 ? -INFINITY : 0.f;
   if (wv && t4 < ncol4) {
     const float* src = f.logits + (int64_t)s * Hq * hstride + t4 * 4 * W + 4 * w;
+    // rolling prefetch: the loads of heads h+8..h+15 are in flight while
+    // head h's columns are folded (sequential head order is kept)
     constexpr int HB = 8;
-    for (int h0 = 0; h0 < Hq; h0 += HB) {
-      float4 x[HB];
+    float4 x[HB];
 #pragma unroll
-      for (int b = 0; b < HB; ++b)
-        if (h0 + b < Hq) x[b] = __ldcs(reinterpret_cast<const float4*>(src + (int64_t)(h0 + b) * hstride));
+    for (int b = 0; b < HB; ++b)
+      if (b < Hq) x[b] = __ldcs(reinterpret_cast<const float4*>(src + (int64_t)b * hstride));
+    for (int h0 = 0; h0 < Hq; h0 += HB) {
 #pragma unroll
       for (int b = 0; b < HB; ++b) {
-        if (h0 + b < Hq) {
-          const float M = sw[2 * (h0 + b)], rL = sw[2 * (h0 + b) + 1];
+        const int h = h0 + b;
+        if (h < Hq) {
+          const float M = sw[2 * h], rL = sw[2 * h + 1];
           const float v[4] = {__fmul_rn(x[b].x, scale), __fmul_rn(x[b].y, scale), __fmul_rn(x[b].z, scale),
-                             __fmul_rn(x[b].w, scale)};  // logit = f32(q.k * scale)
+                              __fmul_rn(x[b].w, scale)};  // logit = f32(q.k * scale)
+          if (h + HB < Hq) x[b] = __ldcs(reinterpret_cast<const float4*>(src + (int64_t)(h + HB) * hstride));
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float p = fold_prob(v[e], M, rL);
