@@ -222,6 +222,24 @@ __device__ __forceinline__ void exp_pack64(const uint32_t (&u)[2][32], float2 c1
   }
 }
 
+// S_i = Q_qt K^T from K ring stage kst into TMEM tile i (split mode: both
+// TMEM tiles use Q tile 0 against different key tiles)
+__device__ __forceinline__ void issue_s_at(uint32_t tmem, uint64_t dq0, uint64_t dk0, uint32_t id_s, int i, int qt,
+                                           int kst, uint64_t* s_full) {
+  const uint64_t dk = dk0 + (uint64_t)(kst * (TILE >> 4));
+  const uint64_t dq = dq0 + (uint64_t)(qt * (TILE >> 4));
+#pragma unroll
+  for (int ks = 0; ks < HD / 16; ++ks) {
+    const uint32_t off = ((ks >> 2) * REGION + (ks & 3) * 32) >> 4;
+    mma_ss(tmem + i * 128, dq + off, dk + off, id_s, ks > 0);
+  }
+  mma_commit(&s_full[i]);
+}
+
+// ring position of (TMEM tile i, its step j) in split mode: tile 0's key
+// tiles and tile 1's alternate; a last extra tile of tile 1 comes at the end
+__device__ __forceinline__ int sp_pos(int i, int j, int nk0) { return j < nk0 ? 2 * j + i : 2 * nk0; }
+
 // S_i(j) = Q_i K_j^T: 8 MMAs (K = 16 each) into TMEM columns [128 i, 128 i + 128)
 __device__ __forceinline__ void issue_s(uint32_t tmem, uint64_t dq0, uint64_t dk0, uint32_t id_s, int i, int j,
                                         bool skip, uint64_t* s_full) {
@@ -288,7 +306,20 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     nkv1 = t + 1 < nqt ? (n0 + min((t + 2) * BM, C) + BN - 1) / BN : 0;
   }
   (void)npairs;
+  // Split mode (a lone Q tile with enough keys): the second softmax
+  // warpgroup and TMEM half take the upper half of the key tiles for the same
+  // queries, and the two partial (O, m, l) are merged in the epilogue -- two
+  // softmax chains in flight instead of one.  Every row must see a key of the
+  // upper half's first tile (no all-masked first step).
+  const int q0t = 2 * p * BM;
+  const bool sp = a.split && nkv1 == 0 && nkv0 >= 2 && (nkv0 / 2) * BN < n0 + q0t + 1;
+  const int hsp = sp ? nkv0 / 2 : 0;
+  if (sp) {
+    nkv1 = nkv0 - hsp;
+    nkv0 = hsp;
+  }
   const int nkv_max = max(nkv0, nkv1);
+  const int npos = sp ? nkv0 + nkv1 : nkv_max;  // K/V ring positions
   const int seg_row = (int)(((int64_t)s * a.L + a.layer) * a.Hkv + g) * a.cap;
 
   if (tid == 0) {
@@ -332,18 +363,20 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     if (warp == 8) {
       // ----------------------------------------------------------- producer
       if (lane == 0) {
-        const int ntq = nkv1 > 0 ? 2 : 1;
+        const int ntq = (nkv1 > 0 && !sp) ? 2 : 1;
         mbar_arrive_expect_tx(q_full, ntq * TILE);
         for (int i = 0; i < ntq; ++i) {
           const int row = s * C + (2 * p + i) * BM;
           tma_load_3d(smem + SQ + i * TILE, &qmap, 0, h, row, q_full);
           tma_load_3d(smem + SQ + i * TILE + REGION, &qmap, 64, h, row, q_full);
         }
-        // K runs one tile ahead of V (S(j+1) is issued before P(j) V(j))
-        for (int j = 0; j <= nkv_max; ++j) {
-          if (j < nkv_max) {
+        // K runs one tile ahead of V (S(j+1) is issued before P(j) V(j));
+        // position r holds key tile r, or in split mode the alternating halves
+        for (int j = 0; j <= npos; ++j) {
+          if (j < npos) {
             const int st = j % KST;
-            const int y = seg_row + j * BN;
+            const int kt = !sp ? j : j < 2 * nkv0 ? ((j & 1) ? hsp + (j >> 1) : (j >> 1)) : hsp + nkv0;
+            const int y = seg_row + kt * BN;
             mbar_wait(&k_empty[st], ((j / KST) & 1) ^ 1);
             mbar_arrive_expect_tx(&k_full[st], TILE);
             tma_load_2d(smem + SK + st * TILE, &kmap, 0, y, &k_full[st]);
@@ -351,7 +384,8 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
           }
           if (j > 0) {
             const int jv = j - 1, st = jv % STAGES;
-            const int y = seg_row + jv * BN;
+            const int kt = !sp ? jv : jv < 2 * nkv0 ? ((jv & 1) ? hsp + (jv >> 1) : (jv >> 1)) : hsp + nkv0;
+            const int y = seg_row + kt * BN;
             mbar_wait(&v_empty[st], ((jv / STAGES) & 1) ^ 1);
             mbar_arrive_expect_tx(&v_full[st], TILE);
             tma_load_2d(smem + SV + st * TILE, &vmap, 0, y, &v_full[st]);
@@ -372,6 +406,43 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
         int tln = 0;
         mbar_wait(q_full, 0);
         PF_T(1);
+        if (sp) {
+          // split mode: each TMEM tile walks its own key half through the
+          // shared rings (positions alternate), Q tile 0 for both
+#pragma unroll
+          for (int i = 0; i < QT; ++i) {
+            const int r = sp_pos(i, 0, nkv0);
+            mbar_wait(&k_full[r % KST], (r / KST) & 1);
+            tc_fence_after();
+            issue_s_at(tmem, dq0, dk0, id_s, i, 0, r % KST, s_full);
+            mma_commit(&k_empty[r % KST]);
+          }
+          for (int j = 0; j < nkv_max; ++j) {
+#pragma unroll
+            for (int i = 0; i < QT; ++i) {
+              const int nk = i ? nkv1 : nkv0;
+              if (j >= nk) continue;
+              const int r = sp_pos(i, j, nkv0), vst = r % STAGES;
+              mbar_wait(&v_conv[vst], (r / STAGES) & 1);
+              mbar_wait(&p_full[i], j & 1);
+              tc_fence_after();
+              const uint64_t dv = dv0 + (uint64_t)(vst * (TILE >> 4));
+#pragma unroll
+              for (int kk = 0; kk < BN / 16; ++kk)
+                mma_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, dv + (uint64_t)((kk * 16 * 128) >> 4), id_o,
+                       (j > 0 || kk > 0));
+              if (j == nk - 1) mma_commit(&o_final[i]);
+              mma_commit(&v_empty[vst]);
+              if (j + 1 < nk) {
+                const int r2 = sp_pos(i, j + 1, nkv0);
+                mbar_wait(&k_full[r2 % KST], (r2 / KST) & 1);
+                tc_fence_after();
+                issue_s_at(tmem, dq0, dk0, id_s, i, 0, r2 % KST, s_full);
+                mma_commit(&k_empty[r2 % KST]);
+              }
+            }
+          }
+        } else {
         PF_WAIT(0, &k_full[0], 0);
         PF_T(2);
         tc_fence_after();
@@ -420,6 +491,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
           mma_commit(&v_empty[st]);
           if (next) mma_commit(&k_empty[(j + 1) % KST]);
         }
+        }  // !sp
       }
     } else {
       // ------------------------------------------ V conversion bf16 -> fp16
@@ -427,7 +499,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
       // w-10, w-10+NCONV, ... of the 32 KB tile
       const int cw = warp - 10;
       uint32_t vmax = 0;  // max |bf16 bits| seen, two halves
-      for (int j = 0; j < nkv_max; ++j) {
+      for (int j = 0; j < npos; ++j) {
         const int st = j % STAGES;
         mbar_wait(&v_full[st], (j / STAGES) & 1);
         uint4* base = reinterpret_cast<uint4*>(smem + SV + st * TILE);
@@ -459,7 +531,8 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     const int i = warp >> 2;
     const int r = tid & 127;
     const int nk = i ? nkv1 : nkv0;
-    const int q0 = (2 * p + i) * BM;
+    const int q0 = sp ? q0t : (2 * p + i) * BM;
+    const int kt0 = (sp && i) ? hsp : 0;  // first key tile of this warpgroup
     const int qi = q0 + r;  // query index in the chunk
     const bool valid = qi < C;
     const int limit = valid ? n0 + qi + 1 : n0 + 1;  // keys [0, limit) are visible
@@ -488,7 +561,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
         if (lane == 0) mbar_arrive(&p_full[i]);
         continue;
       }
-      const int tbase = j * BN;
+      const int tbase = (kt0 + j) * BN;
       // causal mask needed for some row of the tile (warp-uniform: the last
       // one or two tiles only)
       const bool diag = tbase + BN > tile_min_limit;
@@ -581,7 +654,41 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
       if (lane == 0) mbar_arrive(&p_full[i]);
 #undef PF_U
     }
-    if (nk > 0) {
+    if (sp) {
+      // split epilogue: merge the two halves' (O, m, l) per row; warpgroup i
+      // writes output columns [64 i, 64 i + 64) (warps w and w + 4 address the
+      // same TMEM lanes); the exchange goes through the unused Q tile 1 slot
+      mbar_wait(&o_final[i], 0);
+      tc_fence_after();
+      float* xch = reinterpret_cast<float*>(smem + SQ + TILE);
+      xch[(2 * i) * 128 + r] = m;
+      xch[(2 * i + 1) * 128 + r] = l;
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
+      const float m0 = xch[r], l0 = xch[128 + r], m1 = xch[256 + r], l1 = xch[384 + r];
+      const float M = fmaxf(m0, m1);
+      const float f0 = exp2f((m0 - M) * c1), f1 = exp2f((m1 - M) * c1);
+      const float L = l0 * f0 + l1 * f1;
+      const float inv = 1.f / L;
+      const uint32_t ob = tmem + lane_off + 256 + 64 * i;
+      float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD + 64 * i;
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        float o0[32], o1[32];
+        tmem_ld32(ob + c2 * 32, o0);
+        tmem_ld32(ob + 128 + c2 * 32, o1);
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(orow + c2 * 32 + e) =
+                make_float4((o0[e] * f0 + o1[e] * f1) * inv, (o0[e + 1] * f0 + o1[e + 1] * f1) * inv,
+                            (o0[e + 2] * f0 + o1[e + 2] * f1) * inv, (o0[e + 3] * f0 + o1[e + 3] * f1) * inv);
+        }
+      }
+      if (i == 0 && rec && a.st) {
+        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2] = M * a.scale;
+        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = L;
+      }
+    } else if (nk > 0) {
       // epilogue: O / l
       PF_WAIT(3, &o_final[i], 0);
       tc_fence_after();
@@ -659,6 +766,14 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
                            const PrefillArgs& a_in, cudaStream_t st) {
   PrefillArgs a = a_in;
   if (g_prof) a.prof = g_prof;
+  {
+    static int split = -1;  // SKV_PF_SPLIT=0 disables the lone-tile key split
+    if (split < 0) {
+      const char* e = getenv("SKV_PF_SPLIT");
+      split = e ? atoi(e) != 0 : 1;
+    }
+    a.split = split;
+  }
   if (const char* d = getenv("SKV_PF_DBG")) a.dbg = atoi(d);
   if (const char* d = getenv("SKV_PF_TL")) a.timeline = atoi(d);
   EncodeFn enc = encoder();
