@@ -38,8 +38,12 @@ def _ref(q, kc, vc, n0, C, W):
     return out, logits_last
 
 
+# lone Q tiles with enough keys split their key tiles over both warpgroups:
+# (576, 1000) and (32, 513) split unevenly, (32, 2016) evenly, (64, 100) may
+# not split (a row would see no key of the upper half's first tile)
 @pytest.mark.parametrize("S,C,Hq,Hkv,n0,W", [(1, 128, 2, 2, 0, 32), (2, 576, 4, 4, 1000, 32), (1, 32, 8, 2, 513, 32),
-                                             (2, 200, 4, 1, 300, 16)])
+                                             (2, 200, 4, 1, 300, 16), (1, 32, 4, 4, 2016, 32),
+                                             (1, 64, 2, 2, 100, 32)])
 def test_prefill_matches_torch(S, C, Hq, Hkv, n0, W):
     from paper_2409_09086_b200 import _lib
 
