@@ -91,16 +91,18 @@ def test_prefill_matches_torch(S, C, Hq, Hkv, n0, W):
             assert perr <= 1e-5, (s, w, perr)
 
 
-def test_engine_prefill_chunks_match_oracle():
+@pytest.mark.parametrize("W", [32, 48])
+def test_engine_prefill_chunks_match_oracle(W):
     """Config-2 shape (reduced): 576-token image chunks (k/v = frame mean +
     0.5 N(0,1)) and 32-token text chunks through StreamEngine.prefill_chunk,
     eviction after every chunk, against the CPU oracle stepping the chunk token
-    by token (the reference's prompt loop)."""
+    by token (the reference's prompt loop).  W = 48 records more rows than one
+    fold row-group (32) holds and wraps the window ring."""
     from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
 
     S, L, H, D = 2, 1, 32, 128
-    l, r, W = 256, 256, 32
+    l, r = 256, 256
     B = l + r
     cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
     eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, 0.01, W, B + 576 + 64, torch.bfloat16))
