@@ -291,10 +291,27 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   // is read from DRAM once and served to the other pairs from L2 (a
   // longest-first order over all heads measured the same time with 2.5x the
   // DRAM traffic); within a head the two-tile pairs go from the last (most
-  // keys) to the first, then the lone last tile of an odd tile count.
+  // keys) to the first.  The lone last tiles of an odd tile count (split over
+  // both warpgroups: about half a pair's time) come after all pairs and fill
+  // the last wave (config 2: 257 -> 237 us per layer).
   const int nqt = (a.C + BM - 1) / BM, npairs = (nqt + 1) / 2, full = nqt / 2;
-  const int sh = blockIdx.x / npairs, rank = blockIdx.x - sh * npairs;
-  const int p = rank < full ? full - 1 - rank : full;
+  int sh, p;
+  if (a.order == 1 && npairs > full) {
+    // two-tile CTAs first (head-major, L2 reuse within a head), the lone last
+    // tiles (about half the work) at the end to fill the last wave
+    const int nfull = a.S * a.Hq * full;
+    if ((int)blockIdx.x < nfull) {
+      sh = blockIdx.x / full;
+      p = full - 1 - (int)(blockIdx.x - sh * full);
+    } else {
+      sh = blockIdx.x - nfull;
+      p = full;
+    }
+  } else {
+    sh = blockIdx.x / npairs;
+    const int rank = blockIdx.x - sh * npairs;
+    p = rank < full ? full - 1 - rank : full;
+  }
   const int h = sh % a.Hq, s = sh / a.Hq;
   const int g = h / a.G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -767,6 +784,14 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
   PrefillArgs a = a_in;
   if (g_prof) a.prof = g_prof;
   {
+    static int order = -1;  // SKV_PF_ORDER=0: head-major pairs then each head's lone tile
+    if (order < 0) {
+      const char* e = getenv("SKV_PF_ORDER");
+      order = e ? atoi(e) : 1;
+    }
+    a.order = order;
+  }
+  {
     static int split = -1;  // SKV_PF_SPLIT=0 disables the lone-tile key split
     if (split < 0) {
       const char* e = getenv("SKV_PF_SPLIT");
@@ -816,6 +841,7 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
     attr[ki] = true;
   }
   const int nqt = (a.C + pf::BM - 1) / pf::BM;
+  a.S = streams;
   dim3 grid((nqt + 1) / 2 * a.Hq * streams);
   kern<<<grid, pf::THREADS, pf::SMEM_BYTES, st>>>(qmap, kmap, vmap, a);
   e = cudaGetLastError();

@@ -193,6 +193,8 @@ struct PrefillArgs {
   int timeline;         // instrumentation: CTA 0's MMA-thread event timeline into prof
   int* ovf;             // optional: += count of V elements saturated to fp16 (|v| > 65504)
   int split;            // 1: a CTA with one Q tile splits its key tiles over both softmax warpgroups
+  int order;            // CTA order: 0 head-major (pairs then the lone tile per head), 1 lone tiles last
+  int S;                // streams (CTA order 1)
   int lg_t;             // 1: lg is [S][Hq][lg_cap/4][W][4] raw q.k (unscaled; column quads outermost: the
                         // recorded rows of a warp store 512 contiguous bytes per quad); lg_cap % 128 == 0
 };
