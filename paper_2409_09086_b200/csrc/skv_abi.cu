@@ -790,7 +790,12 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
   // Layers in (up to) four groups: one copy per tensor and group in, one out,
   // so the copies of group i+1 / i-1 overlap group i's kernels while the host
   // issues ~3x fewer runtime calls per token (batch-1 steps are host-bound).
-  const int grp = std::max(1, (x->L + 3) / 4);
+  static int ngroups = -1;  // SKV_HOST_GROUPS overrides the group count
+  if (ngroups < 0) {
+    const char* e = getenv("SKV_HOST_GROUPS");
+    ngroups = e ? std::max(1, atoi(e)) : 4;
+  }
+  const int grp = std::max(1, (x->L + ngroups - 1) / ngroups);
   for (int l0 = 0; l0 < x->L; l0 += grp) {
     const int nl = std::min(grp, x->L - l0);
     SKV_CK(cudaMemcpyAsync(static_cast<char*>(x->stage_q) + l0 * qb, static_cast<const char*>(q) + l0 * qb, nl * qb,
