@@ -999,6 +999,132 @@ __global__ void __launch_bounds__(256) fold_rows_t_kernel(const FoldArgs f, int 
   }
 }
 
+// Bulk-staged variant (the default): a CTA owns 16 column quads (64 columns)
+// of 32 recorded rows and walks the heads; a producer warp copies each
+// head's slab (one 8 KB cp.async.bulk when W = 32, else 512 bytes per quad)
+// into an 8-deep shared-memory ring, so each SM keeps ~128 KB of logits in
+// flight without holding registers.  Lane = recorded row, warp = two quads; same per-column
+// arithmetic as fold_rows_t_kernel (sequential heads, fold_prob).
+namespace fb {
+#ifndef SKV_FB_Q4
+#define SKV_FB_Q4 16
+#endif
+#ifndef SKV_FB_NST
+#define SKV_FB_NST 8
+#endif
+constexpr int Q4 = SKV_FB_Q4;    // column quads per CTA
+constexpr int NST = SKV_FB_NST;  // ring depth (heads in flight)
+constexpr int SLAB = Q4 * 32 * 16;  // one head's bytes: [quad][row][4 floats]
+}  // namespace fb
+
+template <int MODE>
+__global__ void __launch_bounds__(288) fold_rows_tb_kernel(const FoldArgs f, int Hq, int W, int64_t ncol4, int slot0,
+                                                           int Wring, int n_base, int64_t slot_stride, float scale) {
+  using namespace fb;
+  extern __shared__ __align__(128) unsigned char fbs[];
+  float* ring = reinterpret_cast<float*>(fbs);                       // [NST][Q4][32][4]
+  uint64_t* full = reinterpret_cast<uint64_t*>(fbs + NST * SLAB);    // [NST]
+  uint64_t* empty = full + NST;                                      // [NST]
+  float* stt = reinterpret_cast<float*>(empty + NST);                // [32][2 Hq]
+  float* tile = stt + 64 * Hq;                                       // [32][Q4*4 + 1]
+  const int s = blockIdx.y, wg = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows = min(32, W - wg * 32);
+  const int64_t q0 = (int64_t)blockIdx.x * Q4;
+  const int nq = (int)min((int64_t)Q4, ncol4 - q0);
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);  // one arrive per consumer warp
+    }
+    mbar_fence_init();
+  }
+  // stage (M, 1/L) of the 32 rows: eight loads in flight per thread
+  for (int x0 = tid; x0 < 64 * Hq && tid < 256; x0 += 8 * 256) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int x = x0 + i * 256, wl = x / (2 * Hq), k = x - wl * 2 * Hq;
+      v[i] = (x < 64 * Hq && wl < rows) ? f.stats[((int64_t)s * W + wg * 32 + wl) * 2 * Hq + k] : 1.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int x = x0 + i * 256;
+      if (x < 64 * Hq) stt[x] = (x & 1) ? __frcp_rn(v[i]) : v[i];  // (M, 1/L)
+    }
+  }
+  __syncthreads();
+  const int64_t hstride = ncol4 * 4 * W;  // floats between heads
+  const float* base = f.logits + (int64_t)s * Hq * hstride + q0 * 4 * W + 4 * wg * 32;
+  const uint32_t rb = (uint32_t)rows * 16;  // bytes of one quad's rows
+  // producer: warp 0 lane 0 keeps NST heads in flight (refills as warps free slots)
+  auto issue = [&](int h) {
+    const int st = h % NST;
+    float* dst = ring + st * (SLAB / 4);
+    mbar_arrive_expect_tx(&full[st], rb * nq);
+    if (rows == W && W == 32) {  // the quads' rows are contiguous: one copy
+      bulk_g2s(dst, base + (int64_t)h * hstride, rb * nq, &full[st]);
+    } else {
+      for (int q = 0; q < nq; ++q) bulk_g2s(dst + q * 32 * 4, base + (int64_t)h * hstride + q * 4 * W, rb, &full[st]);
+    }
+  };
+  if (warp == 8) {
+    // producer warp: keeps NST heads in flight, refilling a slot once all
+    // eight consumer warps have read it
+    if (lane == 0) {
+      for (int h = 0; h < Hq; ++h) {
+        if (h >= NST) mbar_wait(&empty[h % NST], ((h / NST) - 1) & 1);
+        issue(h);
+      }
+    }
+    return;
+  }
+  const float* sw = stt + lane * 2 * Hq;
+  const float agg = (float)(f.agg_div ? f.agg_div : Hq);
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = MODE == 1 ? -INFINITY : 0.f;
+  const int qa = warp * 2;  // this warp's quads qa, qa + 1
+  for (int h = 0; h < Hq; ++h) {
+    const int st = h % NST;
+    mbar_wait(&full[st], (h / NST) & 1);
+    const float* slab = ring + st * (SLAB / 4);
+    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+    if (lane < rows) {
+      if (qa < nq) x0 = *reinterpret_cast<const float4*>(slab + (qa * 32 + lane) * 4);
+      if (qa + 1 < nq) x1 = *reinterpret_cast<const float4*>(slab + ((qa + 1) * 32 + lane) * 4);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    const float M = sw[2 * h], rL = sw[2 * h + 1];
+    const float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float p = fold_prob(__fmul_rn(v[e], scale), M, rL);  // logit = f32(q.k * scale)
+      acc[e] = MODE == 1 ? fmaxf(acc[e], p) : __fadd_rn(acc[e], p);
+    }
+  }
+  constexpr int TW = Q4 * 4 + 1;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) tile[lane * TW + qa * 4 + e] = MODE == 1 ? acc[e] : __fdiv_rn(acc[e], agg);
+  asm volatile("bar.sync 1, 256;\n" ::: "memory");  // the 8 consumer warps (the producer has left)
+  for (int wl = warp; wl < rows; wl += 8) {
+    const int ww = wg * 32 + wl;
+    const int n = n_base + ww + 1;
+    const int slot = (slot0 + ww) % Wring;
+    float* row = f.rows + (int64_t)slot * slot_stride + (int64_t)s * f.r_ss;
+#pragma unroll
+    for (int c = lane; c < Q4 * 4; c += 32) {
+      const int64_t j = q0 * 4 + c;
+      if (j < n) {
+        const float val = tile[wl * TW + c];
+        row[j] = (f.accum && j < n - 1) ? __fadd_rn(row[j], val) : val;
+      }
+    }
+    if (blockIdx.x == 0 && lane == 0 && f.wlen) f.wlen[slot + s * f.w_ss] = n;
+  }
+}
+
 cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq, int slot0, int Wring, int n_base,
                                int64_t lg_cap, int64_t slot_stride, float scale, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
@@ -1010,6 +1136,29 @@ cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq,
     cudaFuncSetAttribute(fold_rows_t_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     cudaFuncSetAttribute(fold_rows_t_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     attr = true;
+  }
+  static int bulk = -1;  // SKV_FOLD_BULK=0: the register-prefetch variant
+  if (bulk < 0) {
+    const char* e = getenv("SKV_FOLD_BULK");
+    bulk = e ? atoi(e) != 0 : 1;
+  }
+  if (bulk) {
+    const size_t bsmem = (size_t)fb::NST * fb::SLAB + 2 * fb::NST * sizeof(uint64_t) +
+                         (size_t)(64 * Hq + 32 * (fb::Q4 * 4 + 1)) * sizeof(float);
+    static bool battr = false;
+    if (!battr) {
+      cudaFuncSetAttribute(fold_rows_tb_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(fold_rows_tb_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      battr = true;
+    }
+    const int64_t ncol4 = lg_cap / 4;
+    const int64_t need4 = ((int64_t)nmax + 3) / 4;  // quads any row needs
+    dim3 bgrid((unsigned)((std::min(need4, ncol4) + fb::Q4 - 1) / fb::Q4), streams, (rows + 31) / 32);
+    if (f.mode == 1)
+      fold_rows_tb_kernel<1><<<bgrid, 288, bsmem, st>>>(f, Hq, rows, ncol4, slot0, Wring, n_base, slot_stride, scale);
+    else
+      fold_rows_tb_kernel<0><<<bgrid, 288, bsmem, st>>>(f, Hq, rows, ncol4, slot0, Wring, n_base, slot_stride, scale);
+    return cudaGetLastError();
   }
   dim3 grid((nmax + 31) / 32, streams, (rows + 31) / 32);
   if (f.mode == 1)
