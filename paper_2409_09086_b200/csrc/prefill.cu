@@ -18,11 +18,12 @@
 // into a 128-column TMEM tile, O_i += P_i V (fp16, M=N=128) with P read
 // straight from TMEM (the .kind::f16 A-from-TMEM form).  fp16 P carries
 // 2^-11 relative rounding (bf16 P would carry 2^-8, above the 2e-3 bf16
-// tolerance for diffuse rows) at one MMA per 16 keys.  Warps 0-3 / 4-7 (one
-// query row per thread) read a whole S row with one tcgen05.ld wait, run the
-// online softmax -- a quarter of the exponentials on the FMA pipe
-// (exp2_poly2), the rest on the SFU -- and write P (fp16) back over the
-// first 64 of the S columns it came from.  O is
+// tolerance for diffuse rows) at one MMA per 16 keys.  Warps 0-7 take the two
+// Q tiles in turn, two threads per query row: warp w reads the 64 S columns
+// [64 (w >> 2), +64) of TMEM lanes 32 (w & 3), the halves' row maxima meet in
+// shared memory, and each runs the online softmax on its half -- a quarter of
+// the exponentials on the FMA pipe (exp2_poly2), the rest on the SFU -- and
+// writes its half of P (fp16) back over the first 64 S columns.  O is
 // rescaled lazily: only when a row maximum grows by more than 2^8 (exact --
 // O and the row sum share the stale maximum).
 //
@@ -58,7 +59,8 @@ constexpr int SQ = 0;
 constexpr int SK = SQ + QT * TILE;
 constexpr int SV = SK + KST * TILE;
 constexpr int SBAR = SV + STAGES * TILE;
-constexpr int SMEM_BYTES = SBAR + 256 + 1024;  // barriers + alignment slack
+constexpr int SXCH = SBAR + 256;               // [2 halves][128 rows] row-max exchange (softmax)
+constexpr int SMEM_BYTES = SXCH + 1024 + 1024;  // barriers, exchange, alignment slack
 constexpr int NCONV = 2;                       // V-conversion warps
 constexpr int THREADS = (8 + 2 + NCONV) * 32;
 constexpr float kRescaleLog2 = 8.f;            // lazy O rescale threshold (log2 units)
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     }
     for (int i = 0; i < QT; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 8);  // every softmax warp (both column halves)
       mbar_init(&o_final[i], 1);
     }
     mbar_fence_init();
@@ -544,156 +546,182 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
     }
   } else {
 
-    // ------------------------- softmax: warpgroup i = warps 4i..4i+3, one row per thread
-    const int i = warp >> 2;
-    const int r = tid & 127;
-    const int nk = i ? nkv1 : nkv0;
-    const int q0 = sp ? q0t : (2 * p + i) * BM;
-    const int kt0 = (sp && i) ? hsp : 0;  // first key tile of this warpgroup
-    const int qi = q0 + r;  // query index in the chunk
-    const bool valid = qi < C;
-    const int limit = valid ? n0 + qi + 1 : n0 + 1;  // keys [0, limit) are visible
-    const int tile_min_limit = n0 + q0 + 1;          // smallest limit of the tile's rows
+    // ------------------- softmax: the 8 warps take both Q tiles in turn.
+    // Warp w covers TMEM lanes 32 (w & 3) (rows) and S columns
+    // [64 c, 64 c + 64), c = w >> 2: both warps of a lane quadrant form the
+    // row maximum over all 128 columns (identical, no exchange) and each
+    // exponentiates its half -- half the per-step latency of one thread per
+    // row, so a tile's softmax fits in the other tile's MMAs.
+    const int c = warp >> 2;
+    const int r = tid & 127;  // row of the tile: 32 (warp & 3) + lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t s_base = tmem + lane_off + i * 128;
-    const uint32_t o_base = tmem + lane_off + 256 + i * 128;
-    const int wrow = qi - (C - a.W);  // window row index (>= 0: recorded)
-    const bool rec = valid && a.lg && wrow >= 0;
-    // row-major [S][W][Hq][lg_cap] (ABI), or column-quad-major (engine):
-    // quad t/4 of recorded row wrow at ((s*Hq + h)*(lg_cap/4) + t/4)*4W + 4*wrow
-    float* lgrow = !rec ? nullptr
-                 : a.lg_t ? a.lg + (int64_t)(s * a.Hq + h) * (a.lg_cap / 4) * (4 * a.W) + 4 * wrow
-                          : a.lg + ((int64_t)(s * a.W + wrow) * a.Hq + h) * a.lg_cap;
-    const bool any_rec = __any_sync(0xffffffffu, rec);
-    const bool lg_aligned = (reinterpret_cast<uintptr_t>(lgrow) & 15) == 0;
     const float c1 = a.scale * kLog2e;
-    float m = -INFINITY;  // running (possibly stale) max of the raw q.k
-    float l = 0.f;
-    for (int j = 0; j < nk; ++j) {
-      PF_WAIT(0, &s_full[i], j & 1);  // also implies P_i(j-1) V is complete
-      tc_fence_after();
-      if (a.dbg == 1 || a.dbg == 6) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[i]);
-        continue;
-      }
-      const int tbase = (kt0 + j) * BN;
-      // causal mask needed for some row of the tile (warp-uniform: the last
-      // one or two tiles only)
-      const bool diag = tbase + BN > tile_min_limit;
-      // One pass: all 128 S columns of the row in registers (one TMEM load
-      // wait), row maximum, causal mask, record, exp + row sum + fp16 P into
-      // columns [0, 64), then the (rare) lazy O rescale.
-      uint32_t u[2][2][32];
+    float m[QT], l[QT];
+    int qi[QT], limit[QT], tml[QT], kt0[QT], nk[QT], wrow[QT];
+    bool valid[QT], rec[QT], any_rec[QT], lg_aligned[QT];
+    float* lgrow[QT];
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) tmem_ld32_async(s_base + q4 * 32, u[q4 >> 1][q4 & 1]);
-      tc_wait_ld();
-#define PF_U(e) u[(e) >> 6][((e) >> 5) & 1][(e) & 31]
-      if (diag) {
+    for (int i = 0; i < QT; ++i) {
+      m[i] = -INFINITY;  // running (possibly stale) max of the raw q.k
+      l[i] = 0.f;        // this half's share of the row sum
+      nk[i] = i ? nkv1 : nkv0;
+      const int q0 = sp ? q0t : (2 * p + i) * BM;
+      kt0[i] = (sp && i) ? hsp : 0;  // first key tile of TMEM tile i
+      qi[i] = q0 + r;                 // query index in the chunk
+      valid[i] = qi[i] < C;
+      limit[i] = valid[i] ? n0 + qi[i] + 1 : n0 + 1;  // keys [0, limit) are visible
+      tml[i] = n0 + q0 + 1;                           // smallest limit of the tile's rows
+      wrow[i] = qi[i] - (C - a.W);                    // window row index (>= 0: recorded)
+      rec[i] = valid[i] && a.lg && wrow[i] >= 0;
+      // row-major [S][W][Hq][lg_cap] (ABI), or column-quad-major (engine):
+      // quad t/4 of recorded row wrow at ((s*Hq + h)*(lg_cap/4) + t/4)*4W + 4*wrow
+      lgrow[i] = !rec[i] ? nullptr
+               : a.lg_t ? a.lg + (int64_t)(s * a.Hq + h) * (a.lg_cap / 4) * (4 * a.W) + 4 * wrow[i]
+                        : a.lg + ((int64_t)(s * a.W + wrow[i]) * a.Hq + h) * a.lg_cap;
+      any_rec[i] = __any_sync(0xffffffffu, rec[i]);
+      lg_aligned[i] = (reinterpret_cast<uintptr_t>(lgrow[i]) & 15) == 0;
+    }
+    const int pair_bar = 1 + (warp & 3);  // the two warps of this lane quadrant
+    float* xmax = reinterpret_cast<float*>(smem + SXCH);
+    for (int j = 0; j < nkv_max; ++j) {
 #pragma unroll
-        for (int e = 0; e < 128; ++e)
-          if (tbase + e >= limit) PF_U(e) = __float_as_uint(-INFINITY);
-      }
-      float mx4[4] = {m, -INFINITY, -INFINITY, -INFINITY};  // four 3-input max chains
+      for (int i = 0; i < QT; ++i) {
+        if (j >= nk[i]) continue;
+        PF_WAIT(0, &s_full[i], j & 1);  // also implies P_i(j-1) V is complete
+        tc_fence_after();
+        if (a.dbg == 1 || a.dbg == 6) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[i]);
+          continue;
+        }
+        const uint32_t s_base = tmem + lane_off + i * 128;
+        const uint32_t o_base = tmem + lane_off + 256 + i * 128 + 64 * c;
+        const int tbase = (kt0[i] + j) * BN;
+        // causal mask needed for some row of the tile (warp-uniform: the last
+        // one or two tiles only)
+        const bool diag = tbase + BN > tml[i];
+        // this warp's 64 columns; the row max meets the partner half's in
+        // shared memory (two pair barriers: the buffer is reused every step)
+        uint32_t own[2][32];
+        tmem_ld32_async(s_base + 64 * c, own[0]);
+        tmem_ld32_async(s_base + 64 * c + 32, own[1]);
+        tc_wait_ld();
+        const int cb = 64 * c;  // this warp's first column
+#define PF_U(e) own[(e) >> 5][(e) & 31]
+        if (diag) {
 #pragma unroll
-      for (int e = 0; e < 128; e += 8) {
+          for (int e = 0; e < 64; ++e)
+            if (tbase + cb + e >= limit[i]) PF_U(e) = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {m[i], -INFINITY, -INFINITY, -INFINITY};  // four 3-input max chains
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          mx4[c] = fmaxf(mx4[c], fmaxf(__uint_as_float(PF_U(e + 2 * c)), __uint_as_float(PF_U(e + 2 * c + 1))));
-      }
-      const float mn = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));  // max(m, row max)
-      const bool grow = (mn - m) * c1 > kRescaleLog2;  // true on the first tile (m = -inf)
-      const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
-      // O row *= alpha below; P(j-1) V is complete (s_full above)
-      const float alpha = grow ? exp2f((m - mn) * c1) : 1.f;
-      if (grow) m = mn;
-      const float mo = m * c1;
-      const float2 c12 = make_float2(c1, c1), mo2 = make_float2(-mo, -mo);
-      if (any_rec && lgrow && a.dbg != 7) {  // the last W rows of the chunk: raw f32 logits for the window fold
-        if (a.lg_t) {
-          // one 512-byte run per column quad across the warp's recorded rows;
-          // raw q.k (the fold applies the scale: the same f32 product), so the
-          // stores read the live S registers and no temporaries serialise them
-          float* dst = lgrow + (int64_t)(tbase >> 2) * (4 * a.W);
+        for (int e = 0; e < 64; e += 8) {
 #pragma unroll
-          for (int e = 0; e < 128; e += 4)
-            *reinterpret_cast<float4*>(dst + (int64_t)(e >> 2) * (4 * a.W)) =
-                make_float4(__uint_as_float(PF_U(e)), __uint_as_float(PF_U(e + 1)), __uint_as_float(PF_U(e + 2)),
-                            __uint_as_float(PF_U(e + 3)));
-        } else {
+          for (int k = 0; k < 4; ++k)
+            mx4[k] = fmaxf(mx4[k], fmaxf(__uint_as_float(PF_U(e + 2 * k)), __uint_as_float(PF_U(e + 2 * k + 1))));
+        }
+        const float mh = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));  // max(m, half max)
+        xmax[c * 128 + r] = mh;
+        // both halves have their S (loaded) and their max before either
+        // writes P over S columns [0, 64) or reads the other max
+        asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar) : "memory");
+        const float mn = fmaxf(mh, xmax[(c ^ 1) * 128 + r]);  // max(m, row max)
+        asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar) : "memory");  // buffer free again
+        const bool grow = (mn - m[i]) * c1 > kRescaleLog2;  // true on the first tile (m = -inf)
+        const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
+        const float alpha = grow ? exp2f((m[i] - mn) * c1) : 1.f;
+        if (grow) m[i] = mn;
+        const float mo = m[i] * c1;
+        const float2 c12 = make_float2(c1, c1), mo2 = make_float2(-mo, -mo);
+        if (any_rec[i] && lgrow[i] && a.dbg != 7) {  // the last W rows: raw f32 logits for the window fold
+          if (a.lg_t) {
+            // one 512-byte run per column quad across the warp's recorded rows;
+            // raw q.k (the fold applies the scale: the same f32 product), so the
+            // stores read the live S registers and no temporaries serialise them
+            float* dst = lgrow[i] + (int64_t)((tbase + cb) >> 2) * (4 * a.W);
 #pragma unroll
-          for (int e = 0; e < 128; e += 4) {
-            const int t = tbase + e;
-            const float x0 = __uint_as_float(PF_U(e)) * a.scale;
-            const float x1 = __uint_as_float(PF_U(e + 1)) * a.scale;
-            const float x2 = __uint_as_float(PF_U(e + 2)) * a.scale;
-            const float x3 = __uint_as_float(PF_U(e + 3)) * a.scale;
-            if (t + 3 < limit && lg_aligned) {
-              *reinterpret_cast<float4*>(lgrow + t) = make_float4(x0, x1, x2, x3);
-            } else {
-              if (t < limit) lgrow[t] = x0;
-              if (t + 1 < limit) lgrow[t + 1] = x1;
-              if (t + 2 < limit) lgrow[t + 2] = x2;
-              if (t + 3 < limit) lgrow[t + 3] = x3;
+            for (int e = 0; e < 64; e += 4)
+              *reinterpret_cast<float4*>(dst + (int64_t)(e >> 2) * (4 * a.W)) =
+                  make_float4(__uint_as_float(own[e >> 5][e & 31]), __uint_as_float(own[e >> 5][(e + 1) & 31]),
+                              __uint_as_float(own[e >> 5][(e + 2) & 31]), __uint_as_float(own[e >> 5][(e + 3) & 31]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 64; e += 4) {
+              const int t = tbase + cb + e;
+              const float x0 = __uint_as_float(own[e >> 5][e & 31]) * a.scale;
+              const float x1 = __uint_as_float(own[e >> 5][(e + 1) & 31]) * a.scale;
+              const float x2 = __uint_as_float(own[e >> 5][(e + 2) & 31]) * a.scale;
+              const float x3 = __uint_as_float(own[e >> 5][(e + 3) & 31]) * a.scale;
+              if (t + 3 < limit[i] && lg_aligned[i]) {
+                *reinterpret_cast<float4*>(lgrow[i] + t) = make_float4(x0, x1, x2, x3);
+              } else {
+                if (t < limit[i]) lgrow[i][t] = x0;
+                if (t + 1 < limit[i]) lgrow[i][t + 1] = x1;
+                if (t + 2 < limit[i]) lgrow[i][t + 2] = x2;
+                if (t + 3 < limit[i]) lgrow[i][t + 3] = x3;
+              }
             }
           }
         }
-      }
-      float2 psa = make_float2(0.f, 0.f), psb = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t pk[32];
-        // recorded rows (window statistics) stay on the SFU path
-        if (POLY > 0 && !any_rec)
-          exp_pack64<POLY>(u[hh], c12, mo2, psa, psb, pk);
-        else
-          exp_pack64<0>(u[hh], c12, mo2, psa, psb, pk);
-        tmem_st32u(s_base + hh * 32, pk);
-      }
-      const float2 ps = __fadd2_rn(psa, psb);
-      if (grow && j > 0) l *= alpha;
-      l += ps.x + ps.y;
-      if (rescale) {
-#pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          float o32[32];
-          tmem_ld32(o_base + c4 * 32, o32);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o32[e] *= alpha;
-          tmem_st32(o_base + c4 * 32, o32);
+        float2 psa = make_float2(0.f, 0.f), psb = make_float2(0.f, 0.f);
+        {
+          uint32_t pk[32];
+          // recorded rows (window statistics) stay on the SFU path
+          if (POLY > 0 && !any_rec[i])
+            exp_pack64<POLY>(own, c12, mo2, psa, psb, pk);
+          else
+            exp_pack64<0>(own, c12, mo2, psa, psb, pk);
+          tmem_st32u(s_base + c * 32, pk);  // fp16 P of columns [64 c, 64 c + 64)
         }
-        if (prof) pacc2 += 1;
-      }
-      tc_wait_st();
-      if (a.dbg != 13) tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[i]);
+        const float2 ps = __fadd2_rn(psa, psb);
+        if (grow && j > 0) l[i] *= alpha;
+        l[i] += ps.x + ps.y;
+        if (rescale) {  // this warp's half of the O row
+#pragma unroll
+          for (int c4 = 0; c4 < 2; ++c4) {
+            float o32[32];
+            tmem_ld32(o_base + c4 * 32, o32);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o32[e] *= alpha;
+            tmem_st32(o_base + c4 * 32, o32);
+          }
+          if (prof) pacc2 += 1;
+        }
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
 #undef PF_U
+      }
     }
+    // ---- epilogue: the two halves' row sums meet in shared memory (the K
+    // ring is idle once both tiles' last P V completed)
+#pragma unroll
+    for (int i = 0; i < QT; ++i)
+      if (nk[i] > 0) PF_WAIT(3, &o_final[i], 0);
+    tc_fence_after();
+    float* xl = reinterpret_cast<float*>(smem + SK);  // [tile][half][128 rows]
+#pragma unroll
+    for (int i = 0; i < QT; ++i) xl[(2 * i + c) * 128 + r] = l[i];
+    asm volatile("bar.sync 5, 256;\n" ::: "memory");
+    float L[QT];
+#pragma unroll
+    for (int i = 0; i < QT; ++i) L[i] = xl[(2 * i) * 128 + r] + xl[(2 * i + 1) * 128 + r];
     if (sp) {
-      // split epilogue: merge the two halves' (O, m, l) per row; warpgroup i
-      // writes output columns [64 i, 64 i + 64) (warps w and w + 4 address the
-      // same TMEM lanes); the exchange goes through the unused Q tile 1 slot
-      mbar_wait(&o_final[i], 0);
-      tc_fence_after();
-      float* xch = reinterpret_cast<float*>(smem + SQ + TILE);
-      xch[(2 * i) * 128 + r] = m;
-      xch[(2 * i + 1) * 128 + r] = l;
-      asm volatile("bar.sync 1, 256;\n" ::: "memory");
-      const float m0 = xch[r], l0 = xch[128 + r], m1 = xch[256 + r], l1 = xch[384 + r];
-      const float M = fmaxf(m0, m1);
-      const float f0 = exp2f((m0 - M) * c1), f1 = exp2f((m1 - M) * c1);
-      const float L = l0 * f0 + l1 * f1;
-      const float inv = 1.f / L;
-      const uint32_t ob = tmem + lane_off + 256 + 64 * i;
-      float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD + 64 * i;
+      // split: both TMEM tiles hold the same rows over the two key halves
+      const float M = fmaxf(m[0], m[1]);
+      const float f0 = exp2f((m[0] - M) * c1), f1 = exp2f((m[1] - M) * c1);
+      const float Lt = L[0] * f0 + L[1] * f1;
+      const float inv = 1.f / Lt;
+      const uint32_t ob = tmem + lane_off + 256 + 64 * c;
+      float* orow = a.out + ((int64_t)(s * C + (valid[0] ? qi[0] : 0)) * a.Hq + h) * HD + 64 * c;
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
         float o0[32], o1[32];
         tmem_ld32(ob + c2 * 32, o0);
         tmem_ld32(ob + 128 + c2 * 32, o1);
-        if (valid) {
+        if (valid[0]) {
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             *reinterpret_cast<float4*>(orow + c2 * 32 + e) =
@@ -701,30 +729,32 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
                             (o0[e + 2] * f0 + o1[e + 2] * f1) * inv, (o0[e + 3] * f0 + o1[e + 3] * f1) * inv);
         }
       }
-      if (i == 0 && rec && a.st) {
-        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2] = M * a.scale;
-        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = L;
+      if (c == 0 && rec[0] && a.st) {
+        a.st[((int64_t)(s * a.W + wrow[0]) * a.Hq + h) * 2] = M * a.scale;
+        a.st[((int64_t)(s * a.W + wrow[0]) * a.Hq + h) * 2 + 1] = Lt;
       }
-    } else if (nk > 0) {
-      // epilogue: O / l
-      PF_WAIT(3, &o_final[i], 0);
-      tc_fence_after();
-      float* orow = a.out + ((int64_t)(s * C + (valid ? qi : 0)) * a.Hq + h) * HD;
-      const float inv = 1.f / l;
+    } else {
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        float o32[32];
-        tmem_ld32(o_base + c4 * 32, o32);  // warp-uniform (.sync.aligned)
-        if (valid) {
+      for (int i = 0; i < QT; ++i) {
+        if (nk[i] == 0) continue;
+        const uint32_t ob = tmem + lane_off + 256 + i * 128 + 64 * c;
+        float* orow = a.out + ((int64_t)(s * C + (valid[i] ? qi[i] : 0)) * a.Hq + h) * HD + 64 * c;
+        const float inv = 1.f / L[i];
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(orow + c4 * 32 + e) =
-                make_float4(o32[e] * inv, o32[e + 1] * inv, o32[e + 2] * inv, o32[e + 3] * inv);
+        for (int c2 = 0; c2 < 2; ++c2) {
+          float o32[32];
+          tmem_ld32(ob + c2 * 32, o32);  // warp-uniform (.sync.aligned)
+          if (valid[i]) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(orow + c2 * 32 + e) =
+                  make_float4(o32[e] * inv, o32[e + 1] * inv, o32[e + 2] * inv, o32[e + 3] * inv);
+          }
         }
-      }
-      if (rec && a.st) {
-        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2] = m * a.scale;
-        a.st[((int64_t)(s * a.W + wrow) * a.Hq + h) * 2 + 1] = l;
+        if (c == 0 && rec[i] && a.st) {
+          a.st[((int64_t)(s * a.W + wrow[i]) * a.Hq + h) * 2] = m[i] * a.scale;
+          a.st[((int64_t)(s * a.W + wrow[i]) * a.Hq + h) * 2 + 1] = L[i];
+        }
       }
     }
   }
