@@ -11,7 +11,7 @@
 // One CTA = two 128-query tiles of one head ("ping-pong"): while the softmax
 // warpgroup of one tile turns its S tile into P, the tensor core runs the
 // other tile's MMAs.  Warp 8 (TMA producer) loads both Q tiles once and
-// 128-key K and V tiles into 3- and 2-stage rings, K one tile ahead of V
+// 128-key K and V tiles into 2- and 3-stage rings, K one tile ahead of V
 // (cp.async.bulk.tensor, 128-byte swizzle).  Warps 10-11 convert each landed V tile in place from bf16 to
 // fp16 (exact for |v| < 65504; larger values saturate and are counted).
 // Warp 9 owns TMEM and issues tcgen05.mma: S_i = Q_i K^T (bf16, M=N=128)
@@ -51,8 +51,14 @@ constexpr int BM = 128;                  // queries per Q tile
 constexpr int BN = 128;                  // keys per K/V tile
 constexpr int HD = 128;                  // head dim
 constexpr int QT = 2;                    // Q tiles per CTA
-constexpr int KST = 3;                   // K ring depth (S(j+1) runs a step ahead of P(j) V(j))
-constexpr int STAGES = 2;                // V ring depth
+#ifndef KST_V
+#define KST_V 2
+#endif
+#ifndef VST_V
+#define VST_V 3
+#endif
+constexpr int KST = KST_V;                 // K ring depth (S(j+1) runs a step ahead of P(j) V(j))
+constexpr int STAGES = VST_V;              // V ring depth
 constexpr int REGION = 128 * 64 * 2;     // [128 rows][64 16-bit] swizzled region, 16 KB
 constexpr int TILE = 2 * REGION;         // one Q, K or V tile (128 rows x 128 dims), 32 KB
 constexpr int SQ = 0;
@@ -279,15 +285,15 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SBAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;        // [KST]
-  uint64_t* k_empty = bars + 4;       // [KST]
-  uint64_t* v_full = bars + 7;        // [STAGES] TMA landed (bf16)
-  uint64_t* v_conv = bars + 9;        // [STAGES] converted to fp16
-  uint64_t* v_empty = bars + 11;      // [STAGES]
-  uint64_t* s_full = bars + 13;       // [QT] S_i(j) in TMEM
-  uint64_t* p_full = bars + 15;       // [QT] P_i(j) written (and O_i rescaled)
-  uint64_t* o_final = bars + 17;      // [QT] last P_i V done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+  uint64_t* k_full = bars + 1;            // [KST]
+  uint64_t* k_empty = k_full + KST;       // [KST]
+  uint64_t* v_full = k_empty + KST;       // [STAGES] TMA landed (bf16)
+  uint64_t* v_conv = v_full + STAGES;     // [STAGES] converted to fp16
+  uint64_t* v_empty = v_conv + STAGES;    // [STAGES]
+  uint64_t* s_full = v_empty + STAGES;    // [QT] S_i(j) in TMEM
+  uint64_t* p_full = s_full + QT;         // [QT] P_i(j) written (and O_i rescaled)
+  uint64_t* o_final = p_full + QT;        // [QT] last P_i V done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + QT);
 
   // The pairs of one (stream, head) are consecutive CTAs, so its K/V stream
   // is read from DRAM once and served to the other pairs from L2 (a
