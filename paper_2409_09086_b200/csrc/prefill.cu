@@ -21,8 +21,8 @@
 // tolerance for diffuse rows) at one MMA per 16 keys.  Warps 0-7 take the two
 // Q tiles in turn, two threads per query row: warp w reads the 64 S columns
 // [64 (w >> 2), +64) of TMEM lanes 32 (w & 3), the halves' row maxima meet in
-// shared memory, and each runs the online softmax on its half -- a quarter of
-// the exponentials on the FMA pipe (exp2_poly2), the rest on the SFU -- and
+// shared memory, and each runs the online softmax on its half (exponentials
+// on the SFU; exp2_poly2 can take a share on the FMA pipe, SKV_PF_POLY) and
 // writes its half of P (fp16) back over the first 64 S columns.  O is
 // rescaled lazily: only when a row maximum grows by more than 2^8 (exact --
 // O and the row sum share the stale maximum).
@@ -70,7 +70,8 @@ constexpr int SMEM_BYTES = SXCH + 1024 + 1024;  // barriers, exchange, alignment
 constexpr int NCONV = 2;                       // V-conversion warps
 constexpr int THREADS = (8 + 2 + NCONV) * 32;
 constexpr float kRescaleLog2 = 8.f;            // lazy O rescale threshold (log2 units)
-constexpr int kDefaultPoly = 2;                // exp2 pairs (of 8) on the FMA-pipe polynomial (0-4)
+constexpr int kDefaultPoly = 0;                // exp2 pairs (of 8) on the FMA-pipe polynomial (0-4;
+                                               // 2 paid off with one thread per row, not with two)
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
