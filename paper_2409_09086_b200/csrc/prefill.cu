@@ -67,7 +67,10 @@ constexpr int SV = SK + KST * TILE;
 constexpr int SBAR = SV + STAGES * TILE;
 constexpr int SXCH = SBAR + 256;               // [2 halves][128 rows] row-max exchange (softmax)
 constexpr int SMEM_BYTES = SXCH + 1024 + 1024;  // barriers, exchange, alignment slack
-constexpr int NCONV = 2;                       // V-conversion warps
+#ifndef NCONV_V
+#define NCONV_V 2
+#endif
+constexpr int NCONV = NCONV_V;                       // V-conversion warps
 constexpr int THREADS = (8 + 2 + NCONV) * 32;
 constexpr float kRescaleLog2 = 8.f;            // lazy O rescale threshold (log2 units)
 constexpr int kDefaultPoly = 0;                // exp2 pairs (of 8) on the FMA-pipe polynomial (0-4;
