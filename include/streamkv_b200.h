@@ -113,9 +113,10 @@ int skv_decode_step(skv_ctx* ctx, const void* q_dev, const void* k_dev, const vo
 
 /* Same with HOST (pinned or pageable) buffers: copies in, decodes all layers
  * with layer-pipelined H2D/compute/D2H on internal streams, copies out.
- * Synchronous. */
+ * Synchronous.  Work already enqueued on `stream` (an eviction, a prefill
+ * chunk) completes before the pipeline touches the cache. */
 int skv_decode_step_host(skv_ctx* ctx, const void* q_host, const void* k_host, const void* v_host,
-                         float* out_host, int record);
+                         float* out_host, int record, void* stream);
 
 /* ---- eviction: Algorithm 1 + compaction -------------------------------------
  * Replaces Session._evict_layer (engine.py:310-337) for every stream:
@@ -137,7 +138,16 @@ int skv_evict(skv_ctx* ctx, int layer, int32_t* kept_dev, void* stream);
 int skv_evict_scores(skv_ctx* ctx, int layer, float* scores_dev, void* stream);
 int skv_evict_apply(skv_ctx* ctx, int layer, const float* scores_dev, int32_t* kept_dev, void* stream);
 
-/* ---- state access -------------------------------------------------------- */
+/* ---- state access --------------------------------------------------------
+ * The streams of one layer run in lock step (one length per layer): a layer
+ * whose streams were injected with different lengths or row counts refuses
+ * decode / prefill / evict with SKV_ESTATE until every stream of it has been
+ * injected alike (the reference's per-Session lengths, cache.py:90-91, are
+ * only representable when they agree). */
+/* Synchronise `stream` and report sticky device errors: SKV_EINVAL after a
+ * chunked prefill read a value |v| >= 65504 (its fp16 P.V saturated).  Every
+ * call that returns host data reports them too. */
+int skv_sync(skv_ctx* ctx, void* stream);
 /* Current cached length of (stream, layer): KvCache.length (cache.py:90-91). */
 int skv_length(const skv_ctx* ctx, int stream, int layer);
 /* Device pointers to the layer's keys/values [Hkv][capacity][D] (views,
@@ -150,9 +160,19 @@ int skv_positions(skv_ctx* ctx, int stream, int layer, int64_t* out_host, int ca
 int skv_window_rows(skv_ctx* ctx, int stream, int layer, float* rows_host, int32_t* lens_host);
 /* Biased scores computed at the last eviction of (stream, layer): [n-l] f32. */
 int skv_last_scores(skv_ctx* ctx, int stream, int layer, float* out_host, int cap);
+/* Dump (stream, layer) state to host buffers (KvCache.debug_snapshot,
+ * cache.py:172-180, with the tensors): *n_out / *m_out receive the length and
+ * window row count (call with null buffers first to size them); then
+ * keys/values [Hkv][n][D] in config dtype (raw keys for RoPE engines),
+ * positions [n], modality [n], round ids [n], window rows [m][n] oldest first
+ * (row i zero-padded after lens[i]).  Any buffer may be null. */
+int skv_state_dump(skv_ctx* ctx, int stream, int layer, int* n_out, int* m_out, void* k_host, void* v_host,
+                   int64_t* pos_host, int8_t* modality_host, int32_t* round_host, float* rows_host,
+                   int32_t* lens_host);
 /* Overwrite (stream, layer) state from host data for state-injection parity:
  * keys/values [Hkv][n][D] in config dtype, positions [n], window rows [m][n]
- * (row i has length lens[i] <= n). */
+ * (row i has length lens[i], 1 <= lens[i] <= n, non-decreasing oldest to
+ * newest like AttentionWindow.push, policies.py:107-115; SKV_EINVAL otherwise). */
 int skv_state_inject(skv_ctx* ctx, int stream, int layer, int n, const void* k_host, const void* v_host,
                      const int64_t* pos_host, int m, const float* rows_host, const int32_t* lens_host);
 

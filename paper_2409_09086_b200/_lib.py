@@ -66,7 +66,7 @@ SIGNATURES = {
     "skv_device_bytes": (_I64, [_P]),
     "skv_decode_layer": (_I, [_P, _I, _P, _P, _P, _P, _P, _I, _P]),
     "skv_decode_step": (_I, [_P, _P, _P, _P, _P, _I, _P]),
-    "skv_decode_step_host": (_I, [_P, _P, _P, _P, _P, _I]),
+    "skv_decode_step_host": (_I, [_P, _P, _P, _P, _P, _I, _P]),
     "skv_evict": (_I, [_P, _I, _P, _P]),
     "skv_evict_scores": (_I, [_P, _I, _P, _P]),
     "skv_evict_apply": (_I, [_P, _I, _P, _P, _P]),
@@ -76,6 +76,8 @@ SIGNATURES = {
     "skv_window_rows": (_I, [_P, _I, _I, _P, _P]),
     "skv_last_scores": (_I, [_P, _I, _I, _P, _I]),
     "skv_state_inject": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _P, _P]),
+    "skv_state_dump": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "skv_sync": (_I, [_P, _P]),
     "skv_capture_begin": (_I, [_P, _P]),
     "skv_capture_end": (_I, [_P, _P]),
     "skv_graph_launch": (_I, [_P, _P]),

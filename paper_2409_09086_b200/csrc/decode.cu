@@ -33,6 +33,7 @@
 #include "skv_common.cuh"
 #include "skv_internal.h"
 #include "skv_fold.cuh"
+#include "skv_append.cuh"
 
 namespace skv {
 
@@ -136,7 +137,7 @@ template <typename T, int D, int G>
 __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kernel(const AttnArgs a) {
   using Gm = Geo<T, D>;
   using Sm = Smem<T, D, G>;
-  constexpr int HS = Cw<G>::HS, GH = Cw<G>::GH, NCW = Cw<G>::NCW, kCT = Cw<G>::CT;
+  constexpr int GH = Cw<G>::GH, NCW = Cw<G>::NCW, kCT = Cw<G>::CT;
   constexpr int TT = Gm::TT, RB = Gm::RB, LPR = Gm::LPR, EPL = Gm::EPL, RPW = Gm::RPW;
   constexpr int NW = Gm::NW, ITERS = Gm::ITERS, STAGES = Sm::STAGES, TILE = Gm::TILE;
   constexpr int PW = D + 2;  // floats per head in a partial
@@ -300,7 +301,6 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       const float* wl = wm + NW * G;
       const float* wo = wl + NW * G;
       const int sigma = u / a.nc, j = u - sigma * a.nc;
-      const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
       // merge the consumer warps' partials of this chunk (static schedule:
       // the consumers already did)
       float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
@@ -330,35 +330,16 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
           part[h * PW + D + 1] = L;
         }
       }
-      // publish the chunk partial: the segment's merge CTA starts once all
-      // nc chunks of the segment are counted
+      // append (dynamic schedule; the static one appends in the consumers):
+      // the new row and its metadata are stored before the chunk is published
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&epi_empty[sl]);  // slot consumed
-        if (!a.stat) red_release_add(&a.counters[sigma], 1);
-      }
-      // append: the new row and (once per stream) its metadata go to slot n_old
-      if (a.append && j == a.nc - 1) {
-        const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
-        const int64_t in = s * a.in_ss + (int64_t)g * D;
-        for (int q16 = lane; q16 < RB / 16; q16 += 32) {
-          reinterpret_cast<uint4*>(static_cast<T*>(a.kc) + dst)[q16] =
-              reinterpret_cast<const uint4*>(static_cast<const T*>(a.kin) + in)[q16];
-          reinterpret_cast<uint4*>(static_cast<T*>(a.vc) + dst)[q16] =
-              reinterpret_cast<const uint4*>(static_cast<const T*>(a.vin) + in)[q16];
-          if (a.kraw)  // RoPE: the raw key goes to the raw store (cache.keys())
-            reinterpret_cast<uint4*>(static_cast<T*>(a.kc_raw) + dst)[q16] =
-                reinterpret_cast<const uint4*>(static_cast<const T*>(a.kraw) + in)[q16];
-        }
-        if (g == 0 && lane == 0) {
-          int64_t* np = a.next_pos + s * a.len_ss;
-          const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
-          a.pos[s * a.m_ss + a.n_old] = pv;
-          a.modality[s * a.m_ss + a.n_old] = 0;
-          a.round_id[s * a.m_ss + a.n_old] = a.round_value;
-          *np = pv + 1;
-          a.len[s * a.len_ss] = n;
-        }
+      if (lane == 0) mbar_arrive(&epi_empty[sl]);  // slot consumed
+      if (!a.stat) {
+        if (a.append && j == a.nc - 1) append_row<T, D>(a, sigma, n, lane, 32);
+        __syncwarp();
+        // publish the chunk partial: the segment's merge CTA starts once all
+        // nc chunks of the segment are counted
+        if (lane == 0) red_release_add(&a.counters[sigma], 1);
       }
     }
     __threadfence();  // every chunk partial of this CTA visible GPU-wide
@@ -607,6 +588,8 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
           part[h * PW + D + 1] = x[0];
         }
       }
+      // the segment's last chunk stores the appended row before publishing
+      if (a.append && j == a.nc - 1) append_row<T, D>(a, sigma, n, tid, kCT);
       consumers_sync<kCT>();
       if (tid == 0) red_release_add(&a.counters[sigma], 1);
     }
@@ -751,12 +734,12 @@ static cudaError_t launch_merge_t(const AttnArgs& a, cudaStream_t st);
 template <typename T, int D, int G>
 static cudaError_t launch_decode_t(int ctas, const AttnArgs& a, cudaStream_t st) {
   using Sm = Smem<T, D, G>;
-  static bool attr = false;
-  if (!attr) {
+  static DevOnce attr;
+  if (!attr.here()) {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Sm::bytes(1024));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.here() = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
@@ -785,11 +768,11 @@ static cudaError_t launch_merge_t(const AttnArgs& a, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   // segment merge, also with programmatic dependent launch
   const size_t msmem = (size_t)G * (a.nc + 1) * sizeof(float);
-  static bool mattr = false;
-  if (!mattr) {
+  static DevOnce mattr;
+  if (!mattr.here()) {
     e = cudaFuncSetAttribute(merge_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e != cudaSuccess) return e;
-    mattr = true;
+    mattr.here() = true;
   }
   if (msmem > 64 * 1024) return cudaErrorInvalidValue;
   cfg.gridDim = dim3(a.S * a.Hkv);
@@ -801,7 +784,8 @@ static cudaError_t launch_merge_t(const AttnArgs& a, cudaStream_t st) {
 template <typename T, int D, int G>
 static int occupancy_t() {
   using Sm = Smem<T, D, G>;
-  static int occ = 0;
+  static int occ_dev[kMaxDevices] = {};
+  int& occ = occ_dev[device_slot()];
   if (!occ) {
     cudaFuncSetAttribute(decode_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::bytes(1024));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<T, D, G>, Cw<G>::THREADS, Sm::bytes(64)) !=

@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include "skv_common.cuh"
+#include "skv_append.cuh"
 #include "skv_fold.cuh"
 #include "skv_internal.h"
 
@@ -38,7 +39,7 @@ constexpr int TILE = 2 * REGION;       // 64 rows x 128 dims, 16 KB
 constexpr int MAXT = 4;                // tiles per chunk (8 warps x 32 keys)
 constexpr int NW = 8;                  // consumer warps
 constexpr int CT = NW * 32;
-constexpr int THREADS = CT + 96;       // + producer, epilogue, fold warps
+constexpr int THREADS = CT + 96;       // + producer, (idle) epilogue, fold warps
 constexpr int PW = D + 2;
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -192,34 +193,6 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
     return;
   }
 
-  if (warp == NW + 1) {
-    // ------------------------------------------- epilogue warp: the append
-    if (a.append && j == a.nc - 1) {
-      griddep_wait();  // the new row is the previous layer's output in a real model
-      const int64_t dst = s * a.c_ss + (int64_t)g * a.c_hs + (int64_t)a.n_old * D;
-      const int64_t in = s * a.in_ss + (int64_t)g * D;
-      for (int q16 = lane; q16 < D * 2 / 16; q16 += 32) {
-        reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.kc) + dst)[q16] =
-            reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.kin) + in)[q16];
-        reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.vc) + dst)[q16] =
-            reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.vin) + in)[q16];
-        if (a.kraw)
-          reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.kc_raw) + dst)[q16] =
-              reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.kraw) + in)[q16];
-      }
-      if (g == 0 && lane == 0) {
-        int64_t* np = a.next_pos + s * a.len_ss;
-        const int64_t pv = a.pos_in ? a.pos_in[s] : *np;
-        a.pos[s * a.m_ss + a.n_old] = pv;
-        a.modality[s * a.m_ss + a.n_old] = 0;
-        a.round_id[s * a.m_ss + a.n_old] = a.round_value;
-        *np = pv + 1;
-        a.len[s * a.len_ss] = n;
-      }
-    }
-    return;
-  }
-
   // ------------------------------------------------------------ consumers
   griddep_wait();
   if (tid == 0) griddep_launch();
@@ -362,6 +335,9 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       part[h * PW + D + 1] = xs[0];
     }
   }
+  // KvCache.append: the segment's last chunk stores the new row and its
+  // metadata before publishing (the merge, and so the next launch, sees them)
+  if (a.append && j == a.nc - 1) append_row<__nv_bfloat16, D>(a, sigma, n, tid, CT);
   consumers_sync();
   if (tid == 0) {
     red_release_add(&a.counters[sigma], 1);
@@ -410,22 +386,22 @@ cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   if (group == 4) {
-    static bool attr = false;
-    if (!attr) {
+    static DevOnce attr;
+    if (!attr.here()) {
       e = cudaFuncSetAttribute(decode_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)tcd::Smem<4>::bytes);
       if (e != cudaSuccess) return e;
-      attr = true;
+      attr.here() = true;
     }
     cfg.dynamicSmemBytes = tcd::Smem<4>::bytes;
     e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<4>, kmap, vmap, a);
   } else if (group == 8) {
-    static bool attr = false;
-    if (!attr) {
+    static DevOnce attr;
+    if (!attr.here()) {
       e = cudaFuncSetAttribute(decode_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)tcd::Smem<8>::bytes);
       if (e != cudaSuccess) return e;
-      attr = true;
+      attr.here() = true;
     }
     cfg.dynamicSmemBytes = tcd::Smem<8>::bytes;
     e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<8>, kmap, vmap, a);

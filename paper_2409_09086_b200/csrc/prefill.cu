@@ -839,8 +839,15 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
     }
     a.split = split;
   }
+#ifdef SKV_INSTRUMENT
+  // instrumentation build only (build.sh with SKV_INSTRUMENT=1): these skip
+  // MMAs / softmax / V conversion and would corrupt outputs in a product run
   if (const char* d = getenv("SKV_PF_DBG")) a.dbg = atoi(d);
   if (const char* d = getenv("SKV_PF_TL")) a.timeline = atoi(d);
+#else
+  a.dbg = 0;
+  a.timeline = 0;
+#endif
   EncodeFn enc = encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap qmap, kmap, vmap;
@@ -874,11 +881,11 @@ cudaError_t launch_prefill(const void* q, int streams, const void* kbase, const 
        prefill_kernel<4, true>}};
   const int ki = (a.prof ? 5 : 0) + poly;
   const Kern kern = kerns[a.prof ? 1 : 0][poly];
-  static bool attr[10] = {};
-  if (!attr[ki]) {
+  static DevOnce attr[10];
+  if (!attr[ki].here()) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr[ki] = true;
+    attr[ki].here() = true;
   }
   const int nqt = (a.C + pf::BM - 1) / pf::BM;
   a.S = streams;
@@ -1171,11 +1178,11 @@ cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq,
   if (Hq > 256 || f.mode == 2 || lg_cap % 128) return cudaErrorInvalidValue;
   const int nmax = n_base + rows;
   const size_t smem = (size_t)(64 * Hq + 32 * 33) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
+  static DevOnce attr;
+  if (!attr.here()) {
     cudaFuncSetAttribute(fold_rows_t_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     cudaFuncSetAttribute(fold_rows_t_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-    attr = true;
+    attr.here() = true;
   }
   static int bulk = -1;  // SKV_FOLD_BULK=0: the register-prefetch variant
   if (bulk < 0) {
@@ -1185,11 +1192,11 @@ cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq,
   if (bulk) {
     const size_t bsmem = (size_t)fb::NST * fb::SLAB + 2 * fb::NST * sizeof(uint64_t) +
                          (size_t)(64 * Hq + 32 * (fb::Q4 * 4 + 1)) * sizeof(float);
-    static bool battr = false;
-    if (!battr) {
+    static DevOnce battr;
+    if (!battr.here()) {
       cudaFuncSetAttribute(fold_rows_tb_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(fold_rows_tb_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      battr = true;
+      battr.here() = true;
     }
     const int64_t ncol4 = lg_cap / 4;
     const int64_t need4 = ((int64_t)nmax + 3) / 4;  // quads any row needs

@@ -38,6 +38,7 @@ static int chunk_tiles(int G) {
 }
 static bool chunk_tiles_forced() { return getenv("SKV_CHUNK_TILES") != nullptr; }
 constexpr int kStaticMaxTiles = 8;  // largest static chunk (tiles of 64 tokens)
+constexpr int kMaxChunks = 128;     // chunks per segment the merge kernel combines
 static int q_prefetch() {
   static int env = -1;
   if (env < 0) {
@@ -133,6 +134,10 @@ struct skv_ctx {
   int32_t* first_moved = nullptr;
   float* scores = nullptr;
   int64_t* pos_in = nullptr;  // staging for explicit positions
+  // sticky device error word: bit 0 = a chunked prefill saw |v| >= 65504 (its
+  // fp16 P.V saturated); reported (and cleared) by skv_sync and every call
+  // that returns host data
+  int32_t* err_word = nullptr;
   float* plogits = nullptr;   // prefill: [S][Hq][plg_cap/4][W][4] logits of the recorded rows
   int64_t plg_cap() const { return (cap + 127) / 128 * 128; }
   float* pstats = nullptr;    // prefill: [S][W][Hq][2]
@@ -143,6 +148,11 @@ struct skv_ctx {
   int64_t device_bytes = 0;
   // host mirror (uniform over streams)
   std::vector<int> n, whead, wcount, parity, pend_n, pend_slot, pend_par, round_value;
+  // per-(stream, layer) lengths / window rows set by skv_state_inject while a
+  // layer's streams disagree (ragged[layer]); the kernels run every stream of
+  // a layer in lock step, so a ragged layer refuses work until it is uniform
+  std::vector<int> sn, sm;
+  std::vector<char> ragged;
   int64_t launches = 0;
   // graphs: host-mirror snapshots at capture begin / end (a replay moves the
   // mirror from `gbegin` to `gend`; it is refused unless the mirror is at `gbegin`)
@@ -169,6 +179,7 @@ struct skv_ctx {
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_in, ev_out;
   cudaEvent_t ev_done = nullptr;
+  cudaEvent_t ev_entry = nullptr;  // caller's stream at entry of skv_decode_step_host
   void* stage_q = nullptr;
   void* stage_k = nullptr;
   void* stage_v = nullptr;
@@ -192,6 +203,33 @@ struct skv_ctx {
 
 };
 
+// A layer whose streams were injected with different lengths / window rows
+// cannot run: every kernel takes one length per layer (lock-stepped streams).
+static int ragged_fail(const skv_ctx* x, int layer) {
+  int s1 = 1;
+  while (s1 < x->S && x->sn[(size_t)s1 * x->L + layer] == x->sn[layer] &&
+         x->sm[(size_t)s1 * x->L + layer] == x->sm[layer])
+    ++s1;
+  char buf[256];
+  snprintf(buf, sizeof buf,
+           "layer %d: streams hold different states (stream 0: n=%d, %d window rows; stream %d: n=%d, %d rows); "
+           "the engine runs the streams of a layer in lock step -- inject every stream with the same n and rows",
+           layer, x->sn[layer], x->sm[layer], s1, s1 < x->S ? x->sn[(size_t)s1 * x->L + layer] : -1,
+           s1 < x->S ? x->sm[(size_t)s1 * x->L + layer] : -1);
+  return fail(SKV_ESTATE, buf);
+}
+
+// Sticky device errors (skv_ctx::err_word), read with a synchronisation.
+static int check_sticky(skv_ctx* x) {
+  int32_t w = 0;
+  SKV_CK(cudaMemcpy(&w, x->err_word, sizeof w, cudaMemcpyDeviceToHost));
+  if (w == 0) return SKV_OK;
+  SKV_CK(cudaMemset(x->err_word, 0, sizeof w));
+  return fail(SKV_EINVAL,
+              "value overflow: a chunked prefill read |v| >= 65504, which its fp16 P.V cannot represent "
+              "(outputs of that chunk are saturated)");
+}
+
 extern "C" {
 
 const char* skv_last_error(void) { return g_err.c_str(); }
@@ -214,6 +252,11 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   if (c.head_agg != SKV_AGG_MEAN && c.head_agg != SKV_AGG_MAX) return fail(SKV_EINVAL, "unknown head_agg");
   if (c.heads_q_total < 0 || (c.heads_q_total > 0 && c.heads_q_total < c.heads_q))
     return fail(SKV_EINVAL, "heads_q_total must be 0 or >= heads_q");
+  // a head shard's max over its own heads cannot be combined by the score sum
+  // of the sharded eviction (the reference max runs over all heads,
+  // policies.py:263-264)
+  if (c.head_agg == SKV_AGG_MAX && c.heads_q_total > c.heads_q)
+    return fail(SKV_EINVAL, "head_agg='max' cannot be head-sharded (heads_q_total > heads_q)");
   if (c.capacity < c.recent_len + c.relevant_budget + 1)
     return fail(SKV_EINVAL, "capacity must exceed recent_len + relevant_budget");
   if (c.policy < SKV_POLICY_INF_MLLM || c.policy > SKV_POLICY_NONE) return fail(SKV_EINVAL, "unknown policy");
@@ -280,6 +323,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
   chk(x->alloc(&x->scores, SL * x->cap * sizeof(float)));
   chk(x->alloc(&x->pos_in, x->S * sizeof(int64_t)));
+  chk(x->alloc(&x->err_word, sizeof(int32_t)));
   // heavy-hitter accumulators (engine.py:274): one column per cached token
   if (c.policy == SKV_POLICY_HEAVY_HITTER) chk(x->alloc(&x->acc, SL * (size_t)x->cap * sizeof(float)));
   if (c.rope_mode != SKV_ROPE_NONE) {
@@ -321,6 +365,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   x->pend_slot.assign(x->L, 0);
   x->pend_par.assign(x->L, 0);
   x->round_value.assign(x->L, 0);
+  x->sn.assign(SL, 0);
+  x->sm.assign(SL, 0);
+  x->ragged.assign(x->L, 0);
   *out = x;
   return SKV_OK;
 }
@@ -333,6 +380,7 @@ int skv_destroy(skv_ctx* x) {
   for (auto ev : x->ev_in) cudaEventDestroy(ev);
   for (auto ev : x->ev_out) cudaEventDestroy(ev);
   if (x->ev_done) cudaEventDestroy(x->ev_done);
+  if (x->ev_entry) cudaEventDestroy(x->ev_entry);
   for (auto s : x->hs)
     if (s) cudaStreamDestroy(s);
   for (void* p : x->allocs) cudaFree(p);
@@ -448,9 +496,30 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   // heavy hitter needs every step's row (engine.py:274)
   if (x->cfg.policy == SKV_POLICY_HEAVY_HITTER) record = 1;
   else if (x->cfg.policy != SKV_POLICY_INF_MLLM) record = 0;
+  if (x->ragged[layer]) return ragged_fail(x, layer);
   const int n_old = x->n[layer];
   if (n_old + 1 > x->cap)
     return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
+  // schedule first: nothing is launched (and no host state moves) unless the
+  // whole step can be issued
+  const int n = n_old + 1;
+  const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
+  // Few segments (batch-1 GQA, small configs): a static schedule with chunks
+  // just large enough that every chunk gets its own CTA; its tiles are
+  // prefetched under PDL and no CTA idles while another streams a backlog.
+  // Otherwise chunk_tiles() tiles per chunk handed out dynamically.  Either
+  // way a segment has at most kMaxChunks chunks (the segment merge's limit):
+  // long caches get longer chunks.
+  const int segs = x->S * x->Hkv;
+  int ch = 2;  // static chunks start small (latency-bound: as many CTAs as fit)
+  while (ch < kStaticMaxTiles &&
+         ((int64_t)segs * ((nt + ch - 1) / ch) > x->max_ctas || (nt + ch - 1) / ch > kMaxChunks))
+    ++ch;
+  const bool stat = (int64_t)segs * ((nt + ch - 1) / ch) <= x->max_ctas && (nt + ch - 1) / ch <= kMaxChunks &&
+                    !chunk_tiles_forced();
+  if (!stat) ch = std::max(chunk_tiles(x->G), (nt + kMaxChunks - 1) / kMaxChunks);
+  const int nc = (nt + ch - 1) / ch;
+  const int ctas = std::min(segs * nc, x->max_ctas);
   const void* kraw_in = nullptr;
   if (x->cfg.rope_mode != SKV_ROPE_NONE) {
     // rotate q and the new k at the token's position (engine.py:265-268)
@@ -473,20 +542,6 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     q = x->qr;
     k = x->kr;
   }
-  const int n = n_old + 1;
-  const int nt = (n + decode_tile_tokens() - 1) / decode_tile_tokens();
-  // Few segments (batch-1 GQA, small configs): a static schedule with chunks
-  // just large enough that every chunk gets its own CTA; its tiles are
-  // prefetched under PDL and no CTA idles while another streams a backlog.
-  // Otherwise 2-tile chunks handed out dynamically.
-  const int segs = x->S * x->Hkv;
-  int ch = 2;  // static chunks start small (latency-bound: as many CTAs as fit)
-  while (ch < kStaticMaxTiles && (int64_t)segs * ((nt + ch - 1) / ch) > x->max_ctas) ++ch;
-  const bool stat = (int64_t)segs * ((nt + ch - 1) / ch) <= x->max_ctas && !chunk_tiles_forced();
-  if (!stat) ch = chunk_tiles(x->G);
-  const int nc = (nt + ch - 1) / ch;
-  const int ctas = std::min(segs * nc, x->max_ctas);
-  if (nc > 128) return fail(SKV_EINVAL, "capacity too large for the segment merge (more than 128 chunks)");
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
   AttnArgs a{};
@@ -626,6 +681,7 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   if (C < 1) return fail(SKV_EINVAL, "chunk must be non-empty");
   if (x->cfg.policy == SKV_POLICY_HEAVY_HITTER)
     return fail(SKV_EINVAL, "the heavy-hitter policy needs every token's row: feed prompts through decode steps");
+  if (x->ragged[layer]) return ragged_fail(x, layer);
   const int n0 = x->n[layer];
   if (n0 + C > x->cap) return fail(SKV_ESTATE, "cache capacity exceeded: evict before appending more tokens");
   cudaStream_t st = as_stream(stream);
@@ -695,6 +751,7 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   a.lg_cap = x->plg_cap();
   a.lg_t = 1;
   a.st = wrec ? x->pstats : nullptr;
+  a.ovf = x->err_word;  // |v| >= 65504 saturates the fp16 V: sticky error (skv_sync)
   e = launch_prefill(q, x->S, x->k, x->v, (int64_t)x->S * x->L * x->Hkv * x->cap, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
   x->launches += 3;
@@ -762,7 +819,8 @@ int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, flo
   return SKV_OK;
 }
 
-int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record) {
+int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
+                         void* stream) {
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
   const int64_t qb = (int64_t)x->S * x->Hq * x->D * x->elt;
   const int64_t kb = (int64_t)x->S * x->Hkv * x->D * x->elt;
@@ -784,9 +842,15 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
       chk(cudaEventCreateWithFlags(&x->ev_out[l], cudaEventDisableTiming));
     }
     chk(cudaEventCreateWithFlags(&x->ev_done, cudaEventDisableTiming));
+    chk(cudaEventCreateWithFlags(&x->ev_entry, cudaEventDisableTiming));
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
   }
   cudaStream_t s_in = x->hs[0], s_c = x->hs[1], s_out = x->hs[2];
+  // work the caller enqueued before this call (an eviction, a prefill chunk,
+  // a state injection) completes before the pipeline reads or writes the cache
+  SKV_CK(cudaEventRecord(x->ev_entry, as_stream(stream)));
+  SKV_CK(cudaStreamWaitEvent(s_in, x->ev_entry, 0));
+  SKV_CK(cudaStreamWaitEvent(s_c, x->ev_entry, 0));
   // Layers in (up to) four groups: one copy per tensor and group in, one out,
   // so the copies of group i+1 / i-1 overlap group i's kernels while the host
   // issues ~3x fewer runtime calls per token (batch-1 steps are host-bound).
@@ -819,7 +883,7 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
   }
   SKV_CK(cudaStreamSynchronize(s_out));
   SKV_CK(cudaStreamSynchronize(s_c));
-  return SKV_OK;
+  return check_sticky(x);
 }
 
 // ------------------------------------------------------------------- evict --
@@ -981,6 +1045,8 @@ static int evict_common(skv_ctx* x, int layer, int32_t* kept_dev, void* stream, 
   if (x->cfg.policy == SKV_POLICY_NONE) return SKV_OK;  // keep_all: nothing changes (engine.py:298-299)
   if (x->cfg.policy != SKV_POLICY_INF_MLLM && mode != 0)
     return fail(SKV_EINVAL, "score export / apply is defined for the Inf-MLLM policy only");
+  for (int l = l0; l < l1; ++l)
+    if (x->ragged[l]) return ragged_fail(x, l);
   for (int l = l0; l < l1; ++l) {
     if (x->cfg.policy == SKV_POLICY_INF_MLLM && x->wcount[l] == 0)
       return fail(SKV_EINVAL, "attention window is empty");
@@ -1021,7 +1087,7 @@ int skv_evict_apply(skv_ctx* x, int layer, const float* scores_dev, int32_t* kep
 
 int skv_length(const skv_ctx* x, int stream, int layer) {
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
-  return x->n[layer];
+  return x->ragged[layer] ? std::max(0, x->sn[(size_t)stream * x->L + layer]) : x->n[layer];
 }
 
 int skv_kv_view(skv_ctx* x, int stream, int layer, void** k, void** v) {
@@ -1033,32 +1099,112 @@ int skv_kv_view(skv_ctx* x, int stream, int layer, void** k, void** v) {
   return SKV_OK;
 }
 
+// Current (length, window rows, ring head) of (stream, layer): the layer's
+// mirror, or the stream's injected state while the layer is ragged.
+static int stream_state(const skv_ctx* x, int stream, int layer, int* n, int* m, int* head) {
+  if (!x->ragged[layer]) {
+    *n = x->n[layer];
+    *m = x->wcount[layer];
+    *head = x->whead[layer];
+    return SKV_OK;
+  }
+  const size_t sl = (size_t)stream * x->L + layer;
+  if (x->sn[sl] < 0) return ragged_fail(x, layer);
+  *n = x->sn[sl];
+  *m = x->sm[sl];
+  *head = x->sm[sl] % x->W;
+  return SKV_OK;
+}
+
 int skv_positions(skv_ctx* x, int stream, int layer, int64_t* out, int cap) {
   if (!x || !out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
-  const int n = std::min(cap, x->n[layer]);
+  int nn, mm, hh;
+  int rc = stream_state(x, stream, layer, &nn, &mm, &hh);
+  if (rc) return rc;
+  const int n = std::min(cap, nn);
   SKV_CK(cudaDeviceSynchronize());
   SKV_CK(cudaMemcpy(out, x->pos + ((int64_t)stream * x->L + layer) * x->cap, n * sizeof(int64_t),
                     cudaMemcpyDeviceToHost));
-  return n;
+  rc = check_sticky(x);
+  return rc ? rc : n;
 }
 
 int skv_window_rows(skv_ctx* x, int stream, int layer, float* rows_host, int32_t* lens_host) {
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
-  int rc = flush_pending(x, layer, nullptr);
+  int nn, count, head;
+  int rc = stream_state(x, stream, layer, &nn, &count, &head);
   if (rc) return rc;
+  if (!x->ragged[layer]) {
+    rc = flush_pending(x, layer, nullptr);
+    if (rc) return rc;
+  }
   SKV_CK(cudaDeviceSynchronize());
   const int64_t sl = (int64_t)stream * x->L + layer;
   std::vector<int32_t> lens(x->W);
   SKV_CK(cudaMemcpy(lens.data(), x->wlen + sl * x->W, x->W * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  const int count = x->wcount[layer];
   for (int k = 0; k < count; ++k) {
-    const int slot = ((x->whead[layer] - count + k) % x->W + x->W) % x->W;
+    const int slot = ((head - count + k) % x->W + x->W) % x->W;
     if (lens_host) lens_host[k] = lens[slot];
     if (rows_host)
       SKV_CK(cudaMemcpy(rows_host + (int64_t)k * x->cap, x->rows + (sl * x->W + slot) * x->cap,
                         (size_t)lens[slot] * sizeof(float), cudaMemcpyDeviceToHost));
   }
-  return count;
+  rc = check_sticky(x);
+  return rc ? rc : count;
+}
+
+int skv_state_dump(skv_ctx* x, int stream, int layer, int* n_out, int* m_out, void* k_host, void* v_host,
+                   int64_t* pos_host, int8_t* modality_host, int32_t* round_host, float* rows_host,
+                   int32_t* lens_host) {
+  if (!x || !n_out || !m_out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
+    return fail(SKV_EINVAL, "out of range");
+  int n, m, head;
+  int rc = stream_state(x, stream, layer, &n, &m, &head);
+  if (rc) return rc;
+  if (!x->ragged[layer]) {
+    rc = flush_pending(x, layer, nullptr);  // the newest window row is materialised
+    if (rc) return rc;
+  }
+  SKV_CK(cudaDeviceSynchronize());
+  *n_out = n;
+  *m_out = m;
+  const int64_t sl = (int64_t)stream * x->L + layer;
+  const size_t rb = (size_t)x->D * x->elt;
+  const char* kd = static_cast<const char*>(x->kraw ? x->kraw : x->k) + sl * x->kv_layer_stride() * x->elt;
+  const char* vd = static_cast<const char*>(x->v) + sl * x->kv_layer_stride() * x->elt;
+  if (n > 0) {
+    if (k_host)
+      SKV_CK(cudaMemcpy2D(k_host, (size_t)n * rb, kd, (size_t)x->cap * rb, (size_t)n * rb, x->Hkv,
+                          cudaMemcpyDeviceToHost));
+    if (v_host)
+      SKV_CK(cudaMemcpy2D(v_host, (size_t)n * rb, vd, (size_t)x->cap * rb, (size_t)n * rb, x->Hkv,
+                          cudaMemcpyDeviceToHost));
+    if (pos_host) SKV_CK(cudaMemcpy(pos_host, x->pos + sl * x->cap, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (modality_host) SKV_CK(cudaMemcpy(modality_host, x->modality + sl * x->cap, n, cudaMemcpyDeviceToHost));
+    if (round_host)
+      SKV_CK(cudaMemcpy(round_host, x->round_id + sl * x->cap, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  if (m > 0 && (rows_host || lens_host)) {
+    std::vector<int32_t> lens(x->W);
+    SKV_CK(cudaMemcpy(lens.data(), x->wlen + sl * x->W, x->W * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < m; ++k) {
+      const int slot = ((head - m + k) % x->W + x->W) % x->W;
+      const int len = std::min(lens[slot], n);
+      if (lens_host) lens_host[k] = len;
+      if (rows_host) {
+        SKV_CK(cudaMemcpy(rows_host + (int64_t)k * n, x->rows + (sl * x->W + slot) * x->cap, (size_t)len * sizeof(float),
+                          cudaMemcpyDeviceToHost));
+        std::fill(rows_host + (int64_t)k * n + len, rows_host + (int64_t)(k + 1) * n, 0.f);
+      }
+    }
+  }
+  return check_sticky(x);
+}
+
+int skv_sync(skv_ctx* x, void* stream) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
+  SKV_CK(cudaStreamSynchronize(as_stream(stream)));
+  return check_sticky(x);
 }
 
 int skv_last_scores(skv_ctx* x, int stream, int layer, float* out, int cap) {
@@ -1074,6 +1220,14 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   if (n < 0 || n > x->cap) return fail(SKV_EINVAL, "n exceeds capacity");
   if (m < 0 || m > x->W) return fail(SKV_EINVAL, "too many window rows");
+  // window rows: 0 < len <= n, oldest first and never shrinking towards the
+  // newest (AttentionWindow.push, policies.py:107-115)
+  std::vector<int32_t> lens(x->W, 0);
+  for (int k = 0; k < m; ++k) {
+    lens[k] = lens_host ? lens_host[k] : n;
+    if (lens[k] < 1 || lens[k] > n) return fail(SKV_EINVAL, "window row lengths must be in [1, n]");
+    if (k > 0 && lens[k] < lens[k - 1]) return fail(SKV_EINVAL, "window rows may not shrink (oldest first)");
+  }
   SKV_CK(cudaDeviceSynchronize());
   const int64_t sl = (int64_t)stream * x->L + layer;
   const size_t rb = (size_t)x->D * x->elt;
@@ -1093,16 +1247,11 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   }
   const int32_t n32 = n;
   SKV_CK(cudaMemcpy(x->len + sl, &n32, sizeof(int32_t), cudaMemcpyHostToDevice));
-  std::vector<int32_t> lens(x->W, 0);
-  for (int k = 0; k < m; ++k) {
-    lens[k] = lens_host ? lens_host[k] : n;
+  for (int k = 0; k < m; ++k)
     if (rows_host)
       SKV_CK(cudaMemcpy(x->rows + (sl * x->W + k) * x->cap, rows_host + (int64_t)k * n, (size_t)lens[k] * sizeof(float),
                         cudaMemcpyHostToDevice));
-  }
   SKV_CK(cudaMemcpy(x->wlen + sl * x->W, lens.data(), x->W * sizeof(int32_t), cudaMemcpyHostToDevice));
-  // host mirror: injection is per (stream, layer); the caller injects every
-  // stream of a layer with the same n and m.
   x->last_layer = -1;
   if (x->acc)  // heavy hitter: injected tokens start with no accumulated mass
     SKV_CK(cudaMemset(x->acc + ((int64_t)stream * x->L + layer) * x->cap, 0, (size_t)x->cap * sizeof(float)));
@@ -1111,6 +1260,17 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
     if (rc) return rc;
     SKV_CK(cudaDeviceSynchronize());
   }
+  // host mirror: one state per layer.  Injecting one stream rewrites its ring
+  // from slot 0, so the layer is unusable (ragged) until every stream of it has
+  // been injected with the same n and row count.
+  if (!x->ragged[layer])
+    for (int s = 0; s < x->S; ++s) x->sn[(size_t)s * x->L + layer] = x->sm[(size_t)s * x->L + layer] = -1;
+  x->sn[sl] = n;
+  x->sm[sl] = m;
+  bool rg = false;
+  for (int s = 1; s < x->S; ++s)
+    rg |= x->sn[(size_t)s * x->L + layer] != x->sn[layer] || x->sm[(size_t)s * x->L + layer] != x->sm[layer];
+  x->ragged[layer] = rg;
   x->n[layer] = n;
   x->wcount[layer] = m;
   x->whead[layer] = m % x->W;
@@ -1326,6 +1486,7 @@ struct AttendScratch {
   int32_t* sched = nullptr;
   size_t part_floats = 0;
   int heads = 0;
+  int dev = -1;  // device the scratch lives on
 };
 thread_local AttendScratch g_att;
 }  // namespace
@@ -1347,6 +1508,10 @@ int skv_attend(const float* keys, const float* values, int heads, int n, int hea
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ctas = std::min(heads * nc, sms * decode_ctas_per_sm(SKV_DTYPE_F32, head_dim, 1));
   const size_t need = (size_t)heads * nc * (head_dim + 2);
+  if (g_att.dev != dev) {  // this thread moved to another device: fresh scratch there
+    g_att = AttendScratch{};
+    g_att.dev = dev;
+  }
   if (g_att.part_floats < need || g_att.heads < heads) {
     SKV_CK(cudaStreamSynchronize(st));
     if (g_att.stats) cudaFree(g_att.stats);
@@ -1421,6 +1586,9 @@ int skv_prefill_attend(const void* q, int streams, int C, int Hq, int Hkv, const
     return fail(SKV_EINVAL, "bad prefill geometry");
   if (n0 < 0 || n0 + C > cap) return fail(SKV_EINVAL, "chunk exceeds the cache capacity");
   if (W < 0 || W > C) return fail(SKV_EINVAL, "W must be in [0, C]");
+  // recorded logit rows hold n0 + C columns
+  if (W > 0 && (!logits || !stats)) return fail(SKV_EINVAL, "W > 0 needs logits and stats buffers");
+  if (W > 0 && lg_cap < (int64_t)n0 + C) return fail(SKV_EINVAL, "lg_cap must be >= n0 + C");
   PrefillArgs a{};
   a.C = C;
   a.n0 = n0;
@@ -1435,7 +1603,9 @@ int skv_prefill_attend(const void* q, int streams, int C, int Hq, int Hkv, const
   a.out = out;
   a.lg = W > 0 ? logits : nullptr;
   a.lg_cap = lg_cap;
+#ifdef SKV_INSTRUMENT
   if (const char* e = getenv("SKV_PF_LGT")) a.lg_t = atoi(e) && lg_cap % 128 == 0;  // experiment: engine layout
+#endif
   a.st = W > 0 ? stats : nullptr;
   const int64_t rows = (int64_t)streams * L * Hkv * cap;
   cudaError_t e = launch_prefill(q, streams, k_cache, v_cache, rows, a, as_stream(stream));

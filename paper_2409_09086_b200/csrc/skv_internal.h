@@ -6,6 +6,20 @@
 
 namespace skv {
 
+// Kernel function attributes (dynamic shared memory opt-in) are per device:
+// "set once" flags are kept per device so a process that drives several GPUs
+// sets them on each.
+constexpr int kMaxDevices = 64;
+inline int device_slot() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+struct DevOnce {
+  bool done[kMaxDevices] = {};
+  bool& here() { return done[device_slot()]; }
+};
+
 // ----------------------------------------------------------------------------
 // K1: split-KV flash-decode with fused append, logit record and split combine.
 // Element (s, h, t, d) of the K store lives at kc + s*c_ss + h*c_hs + t*D + d.

@@ -183,7 +183,9 @@ class StreamEngine:
 
     def decode_step_host(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
                          record: bool = True):
-        """Same as decode_step with host (ideally pinned) tensors; synchronous."""
+        """Same as decode_step with host (ideally pinned) tensors; synchronous.
+        Work already enqueued on the current torch stream (evictions, prefill
+        chunks) is ordered before it."""
         c = self.cfg
         lead = (c.layers, c.streams)
         for name, t, heads in (("q", q, c.heads_q), ("k", k, c.heads_kv), ("v", v, c.heads_kv)):
@@ -191,7 +193,8 @@ class StreamEngine:
                 raise ValueError(f"{name} must be a host {c.dtype} tensor of shape {(*lead, heads, c.head_dim)}")
         if out.is_cuda or out.dtype != torch.float32:
             raise ValueError("out must be a host float32 tensor")
-        check(self.lib.skv_decode_step_host(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), int(bool(record))))
+        check(self.lib.skv_decode_step_host(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), int(bool(record)),
+                                            _stream_handle()))
         return out
 
     # --------------------------------------------------------------- evict --
@@ -231,6 +234,33 @@ class StreamEngine:
         return out
 
     # --------------------------------------------------------------- state --
+    def sync(self):
+        """Synchronise the current stream and raise the engine's sticky device
+        errors (ValueError when a chunked prefill saturated |v| >= 65504)."""
+        check(self.lib.skv_sync(self._h, _stream_handle()))
+
+    def state_dump(self, stream: int, layer: int) -> dict:
+        """Host copy of one (stream, layer) state (KvCache.debug_snapshot,
+        cache.py:172-180, with the tensors): keys/values (Hkv, n, D) float32,
+        positions, modalities, round ids, window rows (oldest first)."""
+        n, m = ctypes.c_int(), ctypes.c_int()
+        check(self.lib.skv_state_dump(self._h, stream, layer, ctypes.byref(n), ctypes.byref(m), *([None] * 7)))
+        n, m = n.value, m.value
+        c = self.cfg
+        kt = torch.empty((c.heads_kv, n, c.head_dim), dtype=c.dtype)
+        vt = torch.empty_like(kt)
+        pos = np.zeros(n, np.int64)
+        mod = np.zeros(n, np.int8)
+        rnd = np.zeros(n, np.int32)
+        rows = np.zeros((max(m, 1), max(n, 1)), np.float32)
+        lens = np.zeros(max(m, 1), np.int32)
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        check(self.lib.skv_state_dump(self._h, stream, layer, ctypes.byref(ctypes.c_int()),
+                                      ctypes.byref(ctypes.c_int()), _ptr(kt), _ptr(vt), P(pos), P(mod), P(rnd),
+                                      P(rows), P(lens)))
+        return {"n": n, "keys": kt.float().numpy(), "values": vt.float().numpy(), "original_positions": pos,
+                "modalities": mod, "round_ids": rnd, "rows": [rows[i, : lens[i]].copy() for i in range(m)]}
+
     def length(self, stream: int = 0, layer: int = 0) -> int:
         return check(self.lib.skv_length(self._h, stream, layer))
 

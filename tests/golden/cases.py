@@ -55,6 +55,14 @@ CASES = {
     "rope_orig_gqa": dict(S=2, L=1, Hq=8, Hkv=2, D=128, T=224, l=32, r=48, W=16, b=0.01, E=32,
                           dtype="f32", seed=1010, saddles=0, saddle_gain=1.0, spike_prob=0.01,
                           spike_gain=4.0, out_every=32, rope="original", rope_base=500000.0),
+    # aggregate_heads(.., "max") (policies.py:263-264) through the Session's
+    # head_agg switch (engine.py:272): GQA bf16 and f32 with saddle keys.
+    "max_mini": dict(S=2, L=2, Hq=8, Hkv=2, D=128, T=320, l=48, r=48, W=16, b=0.01, E=64,
+                     dtype="bf16", seed=1011, saddles=0, saddle_gain=1.0, spike_prob=0.01,
+                     spike_gain=4.0, out_every=64, head_agg="max"),
+    "max_f32": dict(S=1, L=1, Hq=8, Hkv=8, D=64, T=256, l=32, r=32, W=32, b=0.01, E=32,
+                    dtype="f32", seed=1012, saddles=3, saddle_gain=6.0, spike_prob=0.0,
+                    spike_gain=1.0, out_every=32, head_agg="max"),
 }
 
 

@@ -59,7 +59,8 @@ def run_reference_case(name: str) -> dict:
     S, L, Hq, Hkv, D = c["S"], c["L"], c["Hq"], c["Hkv"], c["D"]
     G = Hq // Hkv
     policy = c.get("policy", "inf_mllm")
-    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"], sink_count=c.get("sink", 4))
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"], sink_count=c.get("sink", 4),
+                       head_agg=c.get("head_agg", "mean"))
     holder = _ScaleHolder(D)
     caches = [KvCache(L, Hkv, D) for _ in range(S)]
     windows = [[AttentionWindow(c["W"]) for _ in range(L)] for _ in range(S)]
@@ -100,7 +101,7 @@ def run_reference_case(name: str) -> dict:
                     keys = np.repeat(keys, G, axis=0)
                     vals = np.repeat(vals, G, axis=0)
                 probs, o = Session._attend(holder, keys, vals, qv)
-                row = aggregate_heads(probs, "mean")
+                row = aggregate_heads(probs, cfg.head_agg)  # engine.py:272
                 windows[s][layer].push(row)
                 accs[s][layer] = heavy_hitter_accumulate(accs[s][layer], row)
                 step_out[layer, s] = o

@@ -22,7 +22,8 @@ def run_oracle_case(name: str, kept_override=None) -> dict:
     """
     c = CASES[name]
     policy = c.get("policy", "inf_mllm")
-    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"], sink_count=c.get("sink", 4))
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"], sink_count=c.get("sink", 4),
+                       head_agg=c.get("head_agg", "mean"))
     orc = StreamOracle(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], cfg, window=c["W"], policy=policy,
                        rope=c.get("rope"), rope_base=c.get("rope_base", 10000.0))
     q_all, k_all, v_all = case_inputs(name)

@@ -50,7 +50,8 @@ def _engine(c, capacity=None):
     dt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
     cap = capacity or (c["l"] + c["r"] + c["E"])
     return StreamEngine(EngineConfig(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], c["l"], c["r"], c["b"], c["W"],
-                                     cap, dt, policy=c.get("policy", "inf_mllm"), sink_count=c.get("sink", 4),
+                                     cap, dt, head_agg=c.get("head_agg", "mean"),
+                                     policy=c.get("policy", "inf_mllm"), sink_count=c.get("sink", 4),
                                      rope=c.get("rope"), rope_base=c.get("rope_base", 10000.0)))
 
 
@@ -104,10 +105,17 @@ def test_engine_matches_reference_golden(name):
     print(f"[{name}] worst output rel err {worst_out:.2e}, worst score rel err {worst_score:.2e} (tol {tol})")
     assert worst_out <= tol
     assert worst_score <= tol
-    # final cache: positions bit-exact; keys are exact copies of the bf16/f32 inputs
+    # final cache: positions bit-exact; keys are exact copies of the bf16/f32
+    # inputs, so the SHA-256 of the stacked f32 keys equals the reference's
+    import hashlib
+
     for s in range(c["S"]):
         for layer in range(c["L"]):
             np.testing.assert_array_equal(eng.positions(s, layer), ref["final_pos"][s, layer])
+    final_keys = np.stack([np.stack([eng.kv(s, layer)[0].float().cpu().numpy() for layer in range(c["L"])])
+                           for s in range(c["S"])]).astype(F32)
+    sha = np.frombuffer(hashlib.sha256(np.ascontiguousarray(final_keys).tobytes()).digest(), np.uint8)
+    np.testing.assert_array_equal(sha, ref["final_keys_sha"], err_msg=f"{name}: final keys differ")
 
 
 def _inject_random(eng, orc, rng, n0, c, dt_name):
@@ -135,8 +143,11 @@ def _inject_random(eng, orc, rng, n0, c, dt_name):
         dict(S=1, L=2, Hq=32, Hkv=32, D=128, l=1024, r=1024, W=32, b=0.01, E=128, dtype="bf16", periods=2),
         # BASELINE config 3 GQA shape (32 q / 8 kv heads, l = r = 2048, E = 256)
         dict(S=1, L=1, Hq=32, Hkv=8, D=128, l=2048, r=2048, W=32, b=0.01, E=256, dtype="bf16", periods=2),
+        # BASELINE config 4's two largest budgets (l = r = B/2, E = 128)
+        dict(S=1, L=1, Hq=32, Hkv=32, D=128, l=2048, r=2048, W=32, b=0.01, E=128, dtype="bf16", periods=2),
+        dict(S=1, L=1, Hq=32, Hkv=32, D=128, l=4096, r=4096, W=32, b=0.01, E=128, dtype="bf16", periods=2),
     ],
-    ids=["cfg1-shape", "cfg3-shape"],
+    ids=["cfg1-shape", "cfg3-shape", "cfg4-B4096", "cfg4-B8192"],
 )
 def test_baseline_shapes_state_injection(shape):
     """State-injection parity at BASELINE per-layer shapes: inject a full cache,
@@ -306,6 +317,73 @@ def test_full_size_config1_properties():
         ka = eng.kv(s, layer)[0]
         idx = torch.from_numpy(kc[s, layer].astype(np.int64)).cuda()
         assert torch.equal(ka, kb[:, idx])
+
+
+def test_full_size_config1_sampled_lanes_vs_oracle():
+    """BASELINE config 1 at full size (8 streams x 32 layers x 32 heads x 128,
+    bf16, l = r = 1024, W = 32, E = 128): one period from a random full cache,
+    then three sampled (stream, layer) lanes against the oracle -- every
+    step's output, the window rows, the biased scores, the kept set and the
+    compacted K/V (the lanes' initial state read back with skv_state_dump)."""
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    S, L, H, D, l, r, W, E = 8, 32, 32, 128, 1024, 1024, 32, 128
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, 0.01, W, B + E, torch.bfloat16))
+    g = torch.Generator(device="cuda").manual_seed(17)
+    for s in range(S):
+        for layer in range(L):
+            kf, vf = eng.kv_full(s, layer)
+            kk = torch.randn((H, B, D), generator=g, device="cuda")
+            kk[:, torch.rand(B, generator=g, device="cuda") < 0.01] *= 4.0
+            kf[:, :B] = kk.to(torch.bfloat16)
+            vf[:, :B] = torch.randn((H, B, D), generator=g, device="cuda").to(torch.bfloat16)
+            eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
+    lanes = [(0, 0), (5, 13), (7, 31)]
+    orcs = {}
+    for s, layer in lanes:
+        d = eng.state_dump(s, layer)
+        o = StreamOracle(1, 1, H, H, D, cfg, window=W)
+        for t in range(B):
+            o.kv[0][0].append(d["keys"][:, t], d["values"][:, t], t)
+        o.pos = [B]
+        orcs[s, layer] = o
+    q = torch.randn((E, L, S, H, D), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((E, L, S, H, D), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((E, L, S, H, D), generator=g, device="cuda").to(torch.bfloat16)
+    out = torch.empty((L, S, H, D), dtype=torch.float32, device="cuda")
+    lane_out = {ln: [] for ln in lanes}
+    for t in range(E):
+        eng.decode_step(q[t], k[t], v[t], out, record=t >= E - W)
+        for s, layer in lanes:
+            lane_out[s, layer].append(out[layer, s].clone())
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    rows_g = {ln: eng.window_rows(*ln) for ln in lanes}
+    eng.evict(-1, kept)
+    kc = kept.cpu().numpy()
+    qh, kh, vh = (x.float().cpu().numpy() for x in (q, k, v))
+    worst_out = worst_row = worst_score = 0.0
+    for (s, layer), o in orcs.items():
+        for t in range(E):
+            want, _ = o.step_layer(0, qh[t, layer, s][None], kh[t, layer, s][None], vh[t, layer, s][None])
+            o.advance()
+            worst_out = max(worst_out, rel_err(lane_out[s, layer][t].cpu().numpy()[None], want))
+        rows_c = o.win[0][0].rows
+        assert [a.size for a in rows_g[s, layer]] == [b.size for b in rows_c]
+        for a, b in zip(rows_g[s, layer], rows_c):
+            worst_row = max(worst_row, float(np.abs(a - b).max() / np.abs(b).max()))
+        sc = o.scores(0, 0)
+        gs = eng.last_scores(s, layer, sc.size)
+        worst_score = max(worst_score, float(np.abs(gs - sc).max() / np.abs(sc).max()))
+        ok, nbad, gap = kept_sets_match(sc, o.decide(0, 0).kept, kc[s, layer], B + E, cfg)
+        assert ok, (s, layer, nbad, gap)
+        o.apply(0, 0, kc[s, layer].astype(np.int64))
+        kg, vg = eng.kv(s, layer)
+        np.testing.assert_array_equal(kg.float().cpu().numpy(), o.kv[0][0].keys())
+        np.testing.assert_array_equal(vg.float().cpu().numpy(), o.kv[0][0].values())
+    print(f"cfg1 full-size lanes: out {worst_out:.2e} rows {worst_row:.2e} scores {worst_score:.2e}")
+    assert worst_out <= 2e-3 and worst_row <= 2e-3 and worst_score <= 2e-3
 
 
 def test_baseline_policy_dropins_match_oracle():

@@ -91,25 +91,42 @@ def test_prefill_matches_torch(S, C, Hq, Hkv, n0, W):
             assert perr <= 1e-5, (s, w, perr)
 
 
-@pytest.mark.parametrize("W", [32, 48])
-def test_engine_prefill_chunks_match_oracle(W):
-    """Config-2 shape (reduced): 576-token image chunks (k/v = frame mean +
-    0.5 N(0,1)) and 32-token text chunks through StreamEngine.prefill_chunk,
-    eviction after every chunk, against the CPU oracle stepping the chunk token
-    by token (the reference's prompt loop).  W = 48 records more rows than one
-    fold row-group (32) holds and wraps the window ring."""
+@pytest.mark.parametrize(
+    "S,l,W,agg,n_init",
+    [(2, 256, 32, "mean", 0), (2, 256, 48, "mean", 0), (2, 256, 32, "max", 0),
+     # BASELINE config 2's budget (l = r = 2048) from a full injected cache
+     (1, 2048, 32, "mean", 4096)],
+    ids=["l256-W32", "l256-W48", "l256-max", "cfg2-budget"],
+)
+def test_engine_prefill_chunks_match_oracle(S, l, W, agg, n_init):
+    """Config-2 shape: 576-token image chunks (k/v = frame mean + 0.5 N(0,1))
+    and 32-token text chunks through StreamEngine.prefill_chunk, eviction after
+    every chunk, against the CPU oracle stepping the chunk token by token (the
+    reference's prompt loop): outputs, window rows, kept sets, K/V after each
+    compaction, positions.  W = 48 records more rows than one fold row-group
+    (32) holds and wraps the window ring; "max" is aggregate_heads(.., "max")
+    (policies.py:263-264) through the chunk fold; the last case runs config
+    2's budget l = r = 2048 from a full cache."""
     from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
 
-    S, L, H, D = 2, 1, 32, 128
-    l, r = 256, 256
+    L, H, D = 1, 32, 128
+    r = l
     B = l + r
-    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
-    eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, 0.01, W, B + 576 + 64, torch.bfloat16))
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01, head_agg=agg)
+    eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, 0.01, W, B + 576 + 64, torch.bfloat16, head_agg=agg))
     orc = StreamOracle(S, L, H, H, D, cfg, window=W)
     rng = np.random.default_rng(31)
     F32 = np.float32
     worst = 0.0
+    if n_init:
+        for s in range(S):
+            k0 = bf16_round(rng.standard_normal((H, n_init, D)).astype(F32))
+            v0 = bf16_round(rng.standard_normal((H, n_init, D)).astype(F32))
+            eng.inject(s, 0, k0, v0, np.arange(n_init, dtype=np.int64))
+            for t in range(n_init):
+                orc.kv[s][0].append(k0[:, t], v0[:, t], t)
+        orc.pos = [n_init] * S
     kept_buf = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
     for frame in range(2):
         for C, mod in ((576, 1), (32, 0)):
@@ -147,6 +164,9 @@ def test_engine_prefill_chunks_match_oracle(W):
                     np.testing.assert_array_equal(kc[s, 0, :n], np.arange(n))
             for s in range(S):
                 np.testing.assert_array_equal(eng.positions(s, 0), orc.kv[s][0].pos[: orc.kv[s][0].n])
+                kg, vg = eng.kv(s, 0)  # compaction is a pure copy
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][0].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][0].values())
     print(f"engine prefill worst output rel err {worst:.2e}")
     assert worst <= 2e-3
 

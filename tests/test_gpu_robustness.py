@@ -1,0 +1,214 @@
+"""GPU robustness: stream ordering of the host-buffer API, domain checks on
+the C ABI, the sticky prefill overflow error, per-stream state rules, the
+state dump, and caches longer than the segment merge's chunk limit.
+
+Each case either compares against the CPU oracle (tests infrastructure) or
+asserts the reference's error behaviour (ValueError for domain errors)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match  # noqa: E402
+from tests.gpu_helpers import rel_err  # noqa: E402
+
+F32 = np.float32
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _eng(S, L, Hq, Hkv, D, l, r, W, cap, dt=torch.bfloat16, **kw):
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    return StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, cap, dt, **kw))
+
+
+def _inject_both(eng, orc, rng, S, L, Hkv, D, n0):
+    for s in range(S):
+        for layer in range(L):
+            k = bf16_round(rng.standard_normal((Hkv, n0, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((Hkv, n0, D)).astype(F32))
+            eng.inject(s, layer, k, v, np.arange(n0, dtype=np.int64))
+            for t in range(n0):
+                orc.kv[s][layer].append(k[:, t], v[:, t], t)
+    orc.pos = [n0] * S
+
+
+def test_decode_step_host_ordered_after_evict_and_prefill():
+    """skv_decode_step_host must not overtake an eviction or a
+    prefill chunk the caller enqueued without synchronising; checked against
+    the oracle running the same sequence."""
+    S, L, Hq, Hkv, D = 2, 2, 16, 4, 128
+    l, r, W, E, C = 256, 256, 16, 32, 48
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = _eng(S, L, Hq, Hkv, D, l, r, W, B + E + C + 8)
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    rng = np.random.default_rng(9)
+    _inject_both(eng, orc, rng, S, L, Hkv, D, B)
+    out_h = torch.empty((L, S, Hq, D), dtype=torch.float32).pin_memory()
+    worst = 0.0
+
+    def inputs(lead):
+        q = bf16_round(rng.standard_normal((*lead, Hq, D)).astype(F32))
+        k = bf16_round(rng.standard_normal((*lead, Hkv, D)).astype(F32))
+        v = bf16_round(rng.standard_normal((*lead, Hkv, D)).astype(F32))
+        return q, k, v
+
+    def host_step():
+        nonlocal worst
+        q, k, v = inputs((L, S))
+        hq, hk, hv = (torch.from_numpy(a).to(torch.bfloat16).pin_memory() for a in (q, k, v))
+        eng.decode_step_host(hq, hk, hv, out_h, record=True)
+        worst = max(worst, rel_err(out_h.numpy(), orc.step(q, k, v)))
+
+    for _ in range(E):
+        host_step()
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    eng.evict(-1, kept)
+    n = B + E
+    decisions = {(s, layer): orc.decide(s, layer) for s in range(S) for layer in range(L)}
+    scores = {(s, layer): orc.scores(s, layer) for s in range(S) for layer in range(L)}
+    host_q = inputs((L, S))  # generated before the kept sets are read back
+    hq, hk, hv = (torch.from_numpy(a).to(torch.bfloat16).pin_memory() for a in host_q)
+    eng.decode_step_host(hq, hk, hv, out_h, record=True)  # no sync after the eviction
+    kc = kept.cpu().numpy()
+    for (s, layer), d in decisions.items():
+        ok, nbad, gap = kept_sets_match(scores[(s, layer)], d.kept, kc[s, layer], n, cfg)
+        assert ok, (s, layer, nbad, gap)
+        orc.apply(s, layer, kc[s, layer].astype(np.int64))
+    worst = max(worst, rel_err(out_h.numpy(), orc.step(*host_q)))
+    # prefill chunk, then a host step without synchronising
+    q, k, v = inputs((L, S, C))
+    kv_in = [tuple(torch.from_numpy(np.ascontiguousarray(a[layer])).to("cuda", torch.bfloat16) for a in (q, k, v))
+             for layer in range(L)]
+    for layer in range(L):
+        eng.prefill_chunk(layer, *kv_in[layer])
+    for i in range(C):
+        orc.step(q[:, :, i], k[:, :, i], v[:, :, i])
+    host_step()
+    print(f"worst output rel err {worst:.2e}")
+    assert worst <= 2e-3
+
+
+def test_head_agg_max_rejected_when_head_sharded():
+    """a shard's max over its heads cannot be summed across shards."""
+    with pytest.raises(ValueError, match="max"):
+        _eng(1, 1, 8, 2, 128, 32, 32, 8, 128, head_agg="max", heads_q_total=16)
+    _eng(1, 1, 8, 2, 128, 32, 32, 8, 128, head_agg="max").close()  # unsharded max is fine
+
+
+def test_prefill_large_v_raises_on_sync():
+    """|v| >= 65504 saturates the prefill's fp16 V -- the
+    engine reports it (sticky ValueError on sync / host reads) instead of
+    returning silently wrong outputs."""
+    S, L, H, D, C = 1, 1, 4, 128, 64
+    eng = _eng(S, L, H, H, D, 64, 64, 8, 64 + 64 + C)
+    rng = np.random.default_rng(3)
+    q = torch.from_numpy(rng.standard_normal((S, C, H, D)).astype(F32)).to("cuda", torch.bfloat16)
+    k = torch.from_numpy(rng.standard_normal((S, C, H, D)).astype(F32)).to("cuda", torch.bfloat16)
+    v = torch.from_numpy(rng.standard_normal((S, C, H, D)).astype(F32)).to("cuda", torch.bfloat16)
+    eng.prefill_chunk(0, q, k, v)
+    eng.sync()  # in range: no error
+    v2 = v.clone()
+    v2[0, 5, 1, 7] = 70000.0
+    eng.prefill_chunk(0, q, k, v2)
+    with pytest.raises(ValueError, match="65504"):
+        eng.sync()
+    eng.sync()  # reported once, then cleared
+
+
+def test_inject_validates_window_rows_and_ragged_streams():
+    """row lengths must lie in [1, n] and never shrink; streams of a
+    layer that disagree refuse work (SKV_ESTATE) until injected alike."""
+    S, L, H, D = 2, 1, 4, 64
+    eng = _eng(S, L, H, H, D, 16, 16, 4, 64, dt=torch.float32)
+    n = 40
+    k = np.zeros((H, n, D), F32)
+    pos = np.arange(n, dtype=np.int64)
+    with pytest.raises(ValueError):
+        eng.inject(0, 0, k, k, pos, rows=[np.ones(n + 5, F32)])  # longer than n
+    with pytest.raises(ValueError):
+        eng.inject(0, 0, k, k, pos, rows=[np.ones(30, F32), np.ones(20, F32)])  # shrinks
+    eng.inject(0, 0, k, k, pos, rows=[np.ones(20, F32) / 20, np.ones(n, F32) / n])
+    q = torch.zeros((S, H, D), device="cuda")
+    with pytest.raises(RuntimeError, match="lock step"):
+        eng.decode_layer(0, q, q, q)  # stream 1 not injected yet
+    assert eng.length(0, 0) == n
+    eng.inject(1, 0, k, k, pos, rows=[np.ones(20, F32) / 20, np.ones(n, F32) / n])
+    eng.decode_layer(0, q, q, q)
+    assert eng.length(1, 0) == n + 1
+
+
+def test_state_dump_roundtrip():
+    """skv_state_dump returns what skv_state_inject wrote, and the cache after
+    decode steps + an eviction in logical order."""
+    S, L, Hq, Hkv, D = 2, 2, 8, 2, 128
+    l, r, W, E = 32, 32, 8, 16
+    B = l + r
+    eng = _eng(S, L, Hq, Hkv, D, l, r, W, B + E)
+    rng = np.random.default_rng(12)
+    ks, vs = {}, {}
+    for s in range(S):
+        for layer in range(L):
+            k = bf16_round(rng.standard_normal((Hkv, B, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((Hkv, B, D)).astype(F32))
+            rows = [rng.dirichlet(np.ones(B)).astype(F32) for _ in range(3)]
+            eng.inject(s, layer, k, v, np.arange(B, dtype=np.int64) * 3, rows=rows)
+            ks[s, layer], vs[s, layer] = k, v
+            d = eng.state_dump(s, layer)
+            assert d["n"] == B
+            np.testing.assert_array_equal(d["keys"], k)
+            np.testing.assert_array_equal(d["values"], v)
+            np.testing.assert_array_equal(d["original_positions"], np.arange(B) * 3)
+            assert len(d["rows"]) == 3
+            for a, b in zip(d["rows"], rows):
+                np.testing.assert_array_equal(a, b)
+    for t in range(E):
+        q = torch.from_numpy(rng.standard_normal((L, S, Hq, D)).astype(F32)).to("cuda", torch.bfloat16)
+        kk = torch.from_numpy(rng.standard_normal((L, S, Hkv, D)).astype(F32)).to("cuda", torch.bfloat16)
+        eng.decode_step(q, kk, kk, record=True)
+    eng.evict(-1)
+    for s in range(S):
+        for layer in range(L):
+            d = eng.state_dump(s, layer)
+            kg, vg = eng.kv(s, layer)
+            np.testing.assert_array_equal(d["keys"], kg.float().cpu().numpy())
+            np.testing.assert_array_equal(d["values"], vg.float().cpu().numpy())
+            np.testing.assert_array_equal(d["original_positions"], eng.positions(s, layer))
+            assert d["n"] == B and len(d["rows"]) == W
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_cache_longer_than_merge_chunk_limit(G):
+    """caches beyond 128 chunks of the default chunk size (n > 32K)
+    take longer chunks instead of failing mid-stream."""
+    Hkv, D = 2, 128
+    Hq = Hkv * G
+    n0 = 40_000
+    eng = _eng(1, 1, Hq, Hkv, D, 64, 64, 4, n0 + 8)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    kf, vf = eng.kv_full(0, 0)
+    kf[:, :n0] = torch.randn((Hkv, n0, D), generator=g, device="cuda").to(torch.bfloat16)
+    vf[:, :n0] = torch.randn((Hkv, n0, D), generator=g, device="cuda").to(torch.bfloat16)
+    eng.lib.skv_state_inject(eng._h, 0, 0, n0, None, None, None, 0, None, None)
+    for _ in range(3):
+        q = torch.randn((1, Hq, D), generator=g, device="cuda").to(torch.bfloat16)
+        k = torch.randn((1, Hkv, D), generator=g, device="cuda").to(torch.bfloat16)
+        v = torch.randn((1, Hkv, D), generator=g, device="cuda").to(torch.bfloat16)
+        out = eng.decode_layer(0, q, k, v, record=False)
+        n = eng.length(0, 0)
+        kk, vv = eng.kv(0, 0)
+        K = kk.float().repeat_interleave(G, 0)
+        V = vv.float().repeat_interleave(G, 0)
+        p = torch.softmax((K @ q[0].float()[:, :, None])[..., 0] / np.sqrt(D), dim=-1)
+        ref = (p[:, None, :] @ V)[:, 0]
+        assert n == n0 + _ + 1
+        assert rel_err(out[0].cpu().numpy(), ref.cpu().numpy()) < 2e-3
