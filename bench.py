@@ -166,6 +166,28 @@ def decode_launch_bytes(c, hkv: int, n: float, streams: int) -> float:
     return streams * (2 * n * hkv * D * s + hq * D * s + 2 * hkv * D * s + hq * D * 4)
 
 
+def workload_config(c, S, resident, waves, world, job_streams, hq, hkv, use_graph, gathered, sharded,
+                    select="layer") -> dict:
+    """The `config` object of a bench line (identical keys for both arms)."""
+    B, E, L = c["recent"] + c["relevant"], c["period"], c["layers"]
+    return {"workload": c["desc"], "streams_per_gpu": S, "resident_streams": resident, "waves": waves,
+            "global_streams": job_streams, "layers": L, "heads_q_per_gpu": hq, "heads_kv_per_gpu": hkv,
+            "head_dim": c["head_dim"], "budget": B, "window": c["window"], "period": E,
+            "step": f"one eviction period: {E} decode tokens x {L} layers x streams + 1 all-layer eviction",
+            "l2": ("L2-resident by construction (sub-MB working set, not flushed): launch-bound parity config"
+                   if c.get("dtype") == "f32" else
+                   "inputs larger than L2 (the whole KV cache is streamed every token)"),
+            "graph": (None if use_graph is None else
+                      "one CUDA graph per period, per-layer launches" if use_graph else
+                      "eager per-token launches (NCCL all-reduce at eviction)"),
+            "result_gather": gathered,
+            "select": (select if select == "layer" else
+                       "kv_head (per KV-head-group decisions: NOT the reference's per-layer selection)"),
+            "parallelism": (f"kv-heads sharded x{world}, select=kv_head: no collective" if select == "kv_head" else
+                            f"kv-heads sharded x{world} (1 all-reduce of window scores per eviction)"
+                            if sharded else f"stream-partitioned x{world}, no hot-path collective")}
+
+
 def _max_over_ranks(x: float, world: int, device) -> float:
     if world == 1:
         return x
@@ -183,7 +205,7 @@ def run_gpu(args, rank: int, world: int):
     import torch.distributed as dist
 
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
-    from paper_2409_09086_b200.sharding import evict_head_sharded, gather_results, shard_heads
+    from paper_2409_09086_b200.sharding import KvHeadEngine, evict_head_sharded, gather_results, shard_heads
 
     c = dict(WORKLOADS[args.workload])
     if args.budget:
@@ -194,7 +216,8 @@ def run_gpu(args, rank: int, world: int):
     G = HQ // HKV
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    sharded = c["shard"] == "heads" and world > 1
+    select = args.select if c["shard"] == "heads" else "layer"
+    sharded = c["shard"] == "heads" and world > 1 and select == "layer"
     if c["shard"] == "heads":
         kvs, qsl = shard_heads(HKV, G, world, rank)
         hkv, hq, S = kvs.stop - kvs.start, qsl.stop - qsl.start, c["streams"]
@@ -207,8 +230,11 @@ def run_gpu(args, rank: int, world: int):
     free = torch.cuda.mem_get_info(dev)[0] - (12 << 30)
     resident = max(1, min(S, int(free // per_stream)))
     waves = -(-S // resident)
-    eng = StreamEngine(EngineConfig(resident, L, hq, hkv, D, l, r, c["bias"], W, B + E, dt,
-                                    heads_q_total=HQ if c["shard"] == "heads" else 0))
+    ecfg = EngineConfig(resident, L, hq, hkv, D, l, r, c["bias"], W, B + E, dt,
+                        heads_q_total=HQ if c["shard"] == "heads" and select == "layer" else 0)
+    eng = KvHeadEngine(ecfg) if select == "kv_head" else StreamEngine(ecfg)
+    core = eng.inner if select == "kv_head" else eng  # the StreamEngine holding the device state
+    units = hkv if select == "kv_head" else 1          # selection units per stream
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def randn(shape):
@@ -221,21 +247,23 @@ def run_gpu(args, rank: int, world: int):
         return k.to(dt)
 
     # steady state: every (stream, layer) holds a full budget of B tokens
-    for s in range(resident):
+    for u in range(resident * units):
         for layer in range(L):
-            kf, vf = eng.kv_full(s, layer)
-            kk = torch.randn((hkv, B, D), generator=g, device=dev)
+            kf, vf = core.kv_full(u, layer)
+            hk = hkv // units
+            kk = torch.randn((hk, B, D), generator=g, device=dev)
             kk[:, torch.rand(B, generator=g, device=dev) < c["spike_prob"]] *= c["spike_gain"]
             kf[:, :B] = kk.to(dt)
-            vf[:, :B] = randn((hkv, B, D))
-            eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
+            vf[:, :B] = randn((hk, B, D))
+            core.lib.skv_state_inject(core._h, u, layer, B, None, None, None, 0, None, None)
     # distinct inputs for up to E steps (fewer when many streams are resident), reused cyclically
     T_in = max(1, min(E, int(3e9 // (L * resident * (hq + 2 * hkv) * D * 2))))
     q = randn((T_in, L, resident, hq, D))
     k = spiked_keys((T_in, L, resident))
     v = randn((T_in, L, resident, hkv, D))
     out = torch.empty((L, resident, hq, D), dtype=torch.float32, device=dev)
-    kept = torch.full((resident, L, B), -1, dtype=torch.int32, device=dev)
+    kept = torch.full((resident, units, L, B) if units > 1 else (resident, L, B), -1, dtype=torch.int32,
+                      device=dev)
 
     def evict():
         if sharded:
@@ -252,16 +280,28 @@ def run_gpu(args, rank: int, world: int):
         evict()
 
     stream = torch.cuda.Stream(device=dev)
-    use_graph = not sharded  # NCCL stays outside our own graph capture
     with torch.cuda.stream(stream):
-        period()  # reach the steady ring state
+        period()  # reach the steady ring state (and create the NCCL communicator eagerly)
     stream.synchronize()
     launches0 = eng.kernel_launches
-    if use_graph:
+    # one CUDA graph per period; head-sharded layer mode captures the NCCL
+    # all-reduce of the window scores inside it too, and falls back to eager
+    # launches if this NCCL / driver cannot capture it
+    use_graph = True
+    try:
         with torch.cuda.stream(stream):
             eng.capture_begin()
-            period()
-            eng.capture_end()
+            try:
+                period()
+            finally:
+                eng.capture_end()
+    except Exception as exc:  # noqa: BLE001
+        if not sharded:
+            raise
+        print(f"[bench] NCCL capture failed ({exc}); eager sharded periods", file=sys.stderr)
+        torch.cuda.synchronize()
+        use_graph = False
+    if use_graph:
         launches_per_period = eng.kernel_launches - launches0
 
         def step():
@@ -296,8 +336,12 @@ def run_gpu(args, rank: int, world: int):
     ms = wave_ms * waves  # every resident wave of this rank's streams takes one period
 
     kc = kept.cpu().numpy()
-    first_moved = np.argmax(kc != np.arange(B)[None, None, :], axis=-1)
-    moved = float(np.mean(B - first_moved))
+    mv = core.moved_rows()  # slot map: rows actually moved by the last eviction
+    if mv is not None:
+        moved = float(mv.mean())
+    else:  # dense stable compaction moves every row after the first evicted one
+        first_moved = np.argmax(kc != np.arange(B)[None, None, :], axis=-1)
+        moved = float(np.mean(B - first_moved))
     pb = period_bytes(c, hkv, moved)
     step_bytes_rank = pb["total"] * resident * L * waves
 
@@ -318,16 +362,16 @@ def run_gpu(args, rank: int, world: int):
     peak, peak_kind = _peaks()
     achieved = dec_bytes / (avg_dec_ms * 1e-3) / 1e9
     span_us = None
-    if use_graph:  # device timestamps (first CTA start .. last CTA end) of each decode kernel in one replay
-        eng.timing(True)
+    if use_graph and not sharded:  # device timestamps (first CTA start .. last CTA end) of each decode kernel
+        core.timing(True)
         with torch.cuda.stream(stream):
             eng.capture_begin()
             period()
             eng.capture_end()
             eng.replay()
         stream.synchronize()
-        ts = eng.timing_read()[: E * L].astype(np.int64)
-        eng.timing(False)
+        ts = core.timing_read()[: E * L].astype(np.int64)
+        core.timing(False)
         span_us = float(np.mean(ts[:, 1] - ts[:, 0]) / 1e3) if len(ts) else None
 
     # --- end to end through the public host-buffer API (pinned memory)
@@ -366,8 +410,9 @@ def run_gpu(args, rank: int, world: int):
     gathered = None
     if world > 1:
         torch.cuda.synchronize()
-        g_out = gather_results(out, dim=2 if sharded else 1)
-        g_kept = kept if sharded else gather_results(kept, dim=0)
+        heads_split = c["shard"] == "heads"
+        g_out = gather_results(out, dim=2 if heads_split else 1)
+        g_kept = kept if sharded else gather_results(kept, dim=1 if heads_split else 0)
         torch.cuda.synchronize()
         gathered = {"op": "all_gather (NCCL) of outputs" + ("" if sharded else " and kept sets"),
                     "bytes": int(g_out.numel() * g_out.element_size() + (0 if sharded else g_kept.numel() * 4)),
@@ -391,18 +436,9 @@ def run_gpu(args, rank: int, world: int):
         "vs_baseline": None,
         "dtype": c.get("dtype", "bf16"),
         "data": "synthetic (seeded N(0,1) q/k/v, key spikes; random cache at budget)",
-        "config": {"workload": c["desc"], "streams_per_gpu": S, "resident_streams": resident, "waves": waves,
-                   "global_streams": job_streams, "layers": L, "heads_q_per_gpu": hq, "heads_kv_per_gpu": hkv,
-                   "head_dim": D, "budget": B, "window": W, "period": E,
-                   "step": f"one eviction period: {E} decode tokens x {L} layers x streams + 1 all-layer eviction",
-                   "l2": ("L2-resident by construction (sub-MB working set, not flushed): launch-bound parity config"
-                          if c.get("dtype") == "f32" else
-                          "inputs larger than L2 (the whole KV cache is streamed every token)"),
-                   "graph": "one CUDA graph per period, per-layer launches" if use_graph else
-                            "eager per-token launches (NCCL all-reduce at eviction)",
-                   "result_gather": gathered,
-                   "parallelism": (f"kv-heads sharded x{world} (1 all-reduce of window scores per eviction)"
-                                   if sharded else f"stream-partitioned x{world}, no hot-path collective")},
+        "config": workload_config(c, S=S, resident=resident, waves=waves, world=world, job_streams=job_streams,
+                                  hq=hq, hkv=hkv, use_graph=use_graph, gathered=gathered, sharded=sharded,
+                                  select=select),
         "roofline": {"bound": "hbm", "kernel": f"decode_kernel<bf16,128,{G}> (+ merge_kernel)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
@@ -636,10 +672,13 @@ def run_cfg2(args, rank: int, world: int):
 
 # --------------------------------------------------------------- CPU arm --
 
-def _cpu_proc(conn, lanes, d, seed, c):
+def _cpu_proc(conn, lanes, seed, c):
     """Worker process: holds `lanes` (stream, layer) states of the oracle
-    (reference algorithm, NumPy f32, one BLAS thread); each request runs d decode
-    steps + one eviction on every lane and returns the two timings."""
+    (the reference algorithm restated in NumPy f32, one BLAS thread).  On
+    request ("period", E) it runs a whole eviction period on every lane --
+    E decode steps (append, attention, head-mean row, window push) and one
+    eviction (Algorithm 1 + gather_keep + window remap) -- and returns its own
+    elapsed time; ("warm", d) runs d decode steps on one lane (untimed)."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle.streamkv_oracle import LayerKV, PolicyConfig, RowWindow, attend_heads, head_mean, saddle_decide, \
         bf16_round
@@ -656,20 +695,27 @@ def _cpu_proc(conn, lanes, d, seed, c):
         vb = bf16_round(rng.standard_normal((B, H, D)).astype(np.float32))
         for t in range(B):
             st.append(kb[t], vb[t], t)
-        w = RowWindow(W)
-        for _ in range(W - d):
-            w.push(rng.dirichlet(np.ones(B)).astype(np.float32))
         stores.append(st)
-        wins.append(w)
+        wins.append(RowWindow(W))
     scale = np.float32(1.0 / np.sqrt(D))
     pos = B
     conn.send("ready")
-    while conn.recv() is not None:
-        qs = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
-        ks = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
-        vs = bf16_round(rng.standard_normal((d, lanes, H, D)).astype(np.float32))
+    while True:
+        req = conn.recv()
+        if req is None:
+            break
+        kind, E = req
+        steps = E if kind == "period" else 1
+        qs = bf16_round(rng.standard_normal((steps, lanes, H, D)).astype(np.float32))
+        ks = bf16_round(rng.standard_normal((steps, lanes, H, D)).astype(np.float32))
+        vs = bf16_round(rng.standard_normal((steps, lanes, H, D)).astype(np.float32))
+        if kind == "warm":
+            st = stores[0]
+            probs, _ = attend_heads(st.keys(), st.values(), qs[0, 0], scale)
+            conn.send((0.0, 0.0))
+            continue
         t0 = time.perf_counter()
-        for t in range(d):
+        for t in range(E):
             for i in range(lanes):
                 st = stores[i]
                 st.append(ks[t, i], vs[t, i], pos + t)
@@ -681,17 +727,34 @@ def _cpu_proc(conn, lanes, d, seed, c):
             stores[i].gather_keep(dec.kept)
             wins[i].remap(dec.kept)
         t2 = time.perf_counter()
-        pos += d
+        pos += E
         conn.send((t1 - t0, t2 - t1))
 
 
-class CpuReference:
-    """The reference algorithm (oracle port) on all host cores: one single-threaded
-    process per group of (stream, layer) lanes of the config-1 workload."""
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    def __init__(self, d: int = 2, procs: int = None, seed: int = 0):
+
+class CpuReference:
+    """The reference algorithm (oracle port: the reference is pure Python, so
+    there is nothing to compile) on all host cores: one single-threaded
+    process per group of (stream, layer) lanes of the config-1 workload.  A
+    sample is one WHOLE eviction period of every lane -- 128 decode tokens x
+    32 layers x 8 streams plus the all-layer eviction -- measured, not
+    extrapolated; the period time is the slowest process's (they run
+    concurrently)."""
+
+    def __init__(self, procs: int = None, seed: int = 0):
         c = dict(CFG)
-        self.S, self.E, self.d = c["streams"], c["period"], d
+        self.c = c
+        self.S, self.E = c["streams"], c["period"]
         lanes_total = c["streams"] * c["layers"]
         procs = procs or min(os.cpu_count() or 1, lanes_total)
         per = [lanes_total // procs + (1 if i < lanes_total % procs else 0) for i in range(procs)]
@@ -701,22 +764,29 @@ class CpuReference:
             if n == 0:
                 continue
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_cpu_proc, args=(b, n, d, seed + i, c), daemon=True)
+            p = ctx.Process(target=_cpu_proc, args=(b, n, seed + i, c), daemon=True)
             p.start()
             self.conns.append(a)
             self.procs.append(p)
         for cn in self.conns:
             assert cn.recv() == "ready"
-        self.info = {"procs": len(self.procs), "lanes": lanes_total, "decode_steps_sampled": d}
+        self.info = {"procs": len(self.procs), "lanes": lanes_total, "host_cpus": os.cpu_count(),
+                     "cpu_model": _cpu_model()}
 
-    def sample(self):
-        """tokens/s extrapolated to a full period: each process covers its lanes for
-        E/d decode samples + 1 eviction; the job takes the slowest process."""
+    def warm(self):
         for cn in self.conns:
-            cn.send(1)
+            cn.send(("warm", 1))
+        for cn in self.conns:
+            cn.recv()
+
+    def period(self):
+        """Seconds of one whole period (all lanes): (job time, decode part, evict part)."""
+        for cn in self.conns:
+            cn.send(("period", self.E))
         res = [cn.recv() for cn in self.conns]
-        period_s = max(dec * self.E / self.d + ev for dec, ev in res)
-        return self.S * self.E / period_s
+        tot = [d + e for d, e in res]
+        k = int(np.argmax(tot))
+        return tot[k], res[k][0], res[k][1]
 
     def close(self):
         for cn in self.conns:
@@ -725,14 +795,21 @@ class CpuReference:
             p.join(timeout=10)
 
 
-def cpu_sample(d: int = 2, procs: int = None, seed: int = 0):
-    ref = CpuReference(d, procs, seed)
+def _cpu_sample_text(info, periods):
+    return (f"config 1, {periods} whole eviction period(s): {info['lanes']} (stream, layer) lanes x (128 decode "
+            f"tokens + 1 eviction) on {info['procs']} single-thread processes ({info['host_cpus']} host CPUs, "
+            f"{info['cpu_model']}); measured, not extrapolated")
+
+
+def cpu_sample(procs: int = None, seed: int = 0):
+    """The GPU arm's cpu_baseline leg: one whole period (~10-30 s of CPU work)."""
+    ref = CpuReference(procs, seed)
     try:
-        ref.sample()  # warm
-        v = ref.sample()
+        ref.warm()
+        sec, _, _ = ref.period()
     finally:
         ref.close()
-    return v, ref.info
+    return ref.S * ref.E / sec, ref.info
 
 
 def run_reference(args, rank: int, world: int):
@@ -740,27 +817,33 @@ def run_reference(args, rank: int, world: int):
 
     if rank != 0:
         return None
-    ref = CpuReference(d=args.ref_decode_steps, seed=100)
+    ref = CpuReference(seed=100)
     try:
-        for _ in range(args.warmup):
-            ref.sample()
-        vals = [ref.sample() for _ in range(args.steps)]
+        for _ in range(args.warmup):  # untimed: one decode step per process (page-in, BLAS warm-up)
+            ref.warm()
+        per = [ref.period() for _ in range(args.steps)]
     finally:
         ref.close()
     info = ref.info
-    value = float(np.median(vals))
-    c = CFG
-    sample = (f"config 1: {info['lanes']} (stream, layer) lanes over {info['procs']} processes x 1 BLAS thread: "
-              f"{args.ref_decode_steps} decode steps at n~2048 + 1 eviction per lane, extrapolated to the "
-              f"128-token period")
+    secs = np.array([p[0] for p in per])
+    value = float(ref.S * ref.E * len(secs) / secs.sum())
+    c = dict(CFG)
     return {
         "metric": METRIC, "impl": "reference", "value": round(value, 3), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(c["streams"] * c["period"] / value * 1e3, 1),
+        "ms_per_step": round(float(secs.mean()) * 1e3, 1),
+        "us_per_token_step": round(float(secs.mean()) * 1e6 / ref.E, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-rounded inputs)",
-        "data": "synthetic", "config": {"workload": CFG["desc"]},
+        "data": "synthetic (seeded N(0,1) q/k/v; random cache at budget)",
+        "config": workload_config(c, S=c["streams"], resident=c["streams"], waves=1, world=world,
+                                  job_streams=c["streams"] * world, hq=c["heads_q"], hkv=c["heads_kv"],
+                                  use_graph=None, gathered=None, sharded=False),
+        "timing": {"decode_s_per_period": round(float(np.mean([p[1] for p in per])), 3),
+                   "evict_s_per_period": round(float(np.mean([p[2] for p in per])), 3),
+                   "warmup": "one decode step per process (untimed)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": info["procs"], "kind": "port",
-                         "sample": sample},
+                         "host_cpus": info["host_cpus"], "cpu_model": info["cpu_model"],
+                         "sample": _cpu_sample_text(info, args.steps)},
         "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -772,10 +855,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=128)
-    ap.add_argument("--ref-decode-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS))
     ap.add_argument("--budget", type=int, default=0, help="config 4 KV budget sweep (1024/2048/4096/8192)")
+    ap.add_argument("--select", default="layer", choices=["layer", "kv_head"],
+                    help="config 3: per-layer selection over all heads (reference semantics; one all-reduce per "
+                         "eviction when sharded) or per KV-head group (no collective; labelled non-reference)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -794,12 +879,10 @@ def main():
     else:
         res = run_gpu(args, rank, world)
         if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "cfg1":
-            v, info = cpu_sample(d=args.ref_decode_steps, seed=7)
+            v, info = cpu_sample(seed=7)
             res["cpu_baseline"] = {
                 "value": round(v, 3), "unit": "tokens/s", "cores": info["procs"], "kind": "port",
-                "sample": f"oracle port: {info['lanes']} (stream, layer) lanes, {args.ref_decode_steps} decode "
-                          f"steps + 1 eviction each on {info['procs']} single-thread processes, extrapolated "
-                          f"to a 128-token period",
+                "host_cpus": info["host_cpus"], "cpu_model": info["cpu_model"], "sample": _cpu_sample_text(info, 1),
             }
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)

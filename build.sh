@@ -11,7 +11,7 @@ FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 if [ "${SKV_INSTRUMENT:-0}" = "1" ]; then FLAGS="$FLAGS -DSKV_INSTRUMENT=1"; fi
 objs=()
 pids=()
-for f in decode decode_tc select compact prefill rope skv_abi; do
+for f in decode decode_tc select compact prefill rope tensorops replay skv_abi; do
   nvcc $FLAGS -c $SRC/$f.cu -o build/$f.o 2> build/$f.ptxas.log &
   pids+=($!)
   objs+=(build/$f.o)

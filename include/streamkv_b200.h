@@ -150,9 +150,21 @@ int skv_evict_apply(skv_ctx* ctx, int layer, const float* scores_dev, int32_t* k
 int skv_sync(skv_ctx* ctx, void* stream);
 /* Current cached length of (stream, layer): KvCache.length (cache.py:90-91). */
 int skv_length(const skv_ctx* ctx, int stream, int layer);
-/* Device pointers to the layer's keys/values [Hkv][capacity][D] (views,
- * cache.py:93-100); the first skv_length() rows of each head are live. */
+/* Device pointers to the layer's key/value storage [Hkv][capacity][D]; the
+ * first skv_length() rows of each head are live.  Engines with a slot map
+ * (all but cache-relative RoPE) keep rows in PHYSICAL order: logical slot c
+ * (KvCache.keys()[:, c], cache.py:93-100) is physical row perm[c] of
+ * skv_slot_map().  An eviction then moves only the kept rows that lie beyond
+ * the kept count (the survivors of the tokens appended since the previous
+ * eviction) instead of shifting every row after the first evicted one. */
 int skv_kv_view(skv_ctx* ctx, int stream, int layer, void** k_dev, void** v_dev);
+/* Device pointer to the slot map of (stream, layer): int32 [capacity],
+ * perm[c] = physical row of logical slot c for c < skv_length(); null for
+ * densely compacted engines (identity). */
+int skv_slot_map(skv_ctx* ctx, int stream, int layer, int32_t** perm_dev);
+/* Rows moved per (stream, layer) by the last eviction, int32 [S][L] host copy
+ * (slot-map engines; SKV_ESTATE otherwise). */
+int skv_moved_rows(skv_ctx* ctx, int32_t* out_host);
 /* Original positions [n] of (stream, layer), host copy (cache.py:102-104). */
 int skv_positions(skv_ctx* ctx, int stream, int layer, int64_t* out_host, int cap);
 /* Window rows of (stream, layer) oldest-first into out_host [W][capacity] with
@@ -260,6 +272,56 @@ int skv_gather_rows(void* base_dev, int64_t block_stride, int blocks, int row_by
  * (Session._attend, engine.py:235-246; tensorops.attn_probs/weighted_sum). */
 int skv_attend(const float* keys_dev, const float* values_dev, int heads, int n, int head_dim,
                int64_t head_stride, const float* q_dev, float* probs_dev, float* out_dev, void* stream);
+
+/* ---- single-row tensor ops (tensorops.py:26-111) --------------------------
+ * Device float32 buffers; the host validates shapes / finiteness (where the
+ * reference raises ValueError) before calling. */
+/* softmax_row (tensorops.py:26-35): out = exp(x - max) / sum, n >= 1. */
+int skv_softmax_row(const float* logits_dev, int n, float* out_dev, void* stream);
+/* attn_probs (tensorops.py:86-102): softmax_row((keys @ q) * scale), keys [n][dim]. */
+int skv_attn_probs(const float* q_dev, const float* keys_dev, int n, int dim, float scale, float* out_dev,
+                   void* stream);
+/* weighted_sum (tensorops.py:105-111): out[dim] = probs[n] @ values[n][dim]. */
+int skv_weighted_sum(const float* probs_dev, const float* values_dev, int n, int dim, float* out_dev, void* stream);
+/* rope_apply (tensorops.py:38-64): pairs rotated by position * base^(-2i/dim)
+ * (angles in float64); synchronous. */
+int skv_rope_apply(const float* v_dev, int dim, int64_t position, double base, float* out_dev, void* stream);
+
+/* ---- batched trace replay (replay.py:72-180) --------
+ * One trace layer's device state: its virtual cache of surviving stream column
+ * ids, the window of projected rows (AttentionWindow(recent_len)) and, for the
+ * heavy hitter, the accumulator plus staging rows.  All device pointers. */
+typedef struct skv_replay_state {
+  int64_t* live;      /* [cap] surviving stream column ids */
+  float* ring;        /* [window][cap] projected rows */
+  int32_t* ring_len;  /* [window] row lengths */
+  int32_t* newlen;    /* [window] scratch: lengths after a remap */
+  float* acc;         /* [cap] heavy-hitter accumulator, or null (not tracked) */
+  float* stage;       /* [stage_rows][cap] projected rows of one batch (heavy hitter) */
+  int32_t stage_rows;
+  int32_t cap;        /* max live columns */
+  int32_t window;     /* ring rows (= recent_len) */
+} skv_replay_state;
+/* Push R recorded rows of one layer (trace_rows + row_off[i], row_n[i] floats,
+ * oldest first): each is projected onto live = live[0, nl_dec) ++ [n_dec, n_i)
+ * and renormalised (f64 total), the last min(R, window) enter the ring from
+ * slot ring_head on, and (acc != null) heavy_hitter_accumulate runs over all R
+ * starting from an accumulator of acc_len columns. */
+int skv_replay_rows(const skv_replay_state* st, const float* trace_rows, const int64_t* row_off,
+                    const int32_t* row_n, int R, int nl_dec, int n_dec, int ring_head, int acc_len, void* stream);
+/* One decision of a replayed layer: the policy (SKV_POLICY_*) over n live
+ * columns and the ring (oldest at ring_head - ring_count), then the round's
+ * metrics from the nraw raw rows (retained mass per row -> mass_out[nraw] f64;
+ * counts_out[0] = |chosen relevant ids (first rc kept) & oracle top-r| or -1,
+ * counts_out[1] = planted ids kept), then the remap of live ids, accumulator
+ * and ring rows.  kept_out [r+l] int64 receives the kept indices (into live);
+ * scores [>= max(n, stream_n)] f32 and top [relevant_budget] i32 are scratch.
+ * Returns the kept count. */
+int skv_replay_evict(const skv_replay_state* st, int policy, int n, int ring_head, int ring_count, int recent_len,
+                     int relevant_budget, int sink_count, float bias, int rc, int64_t* kept_out, float* scores,
+                     int32_t* top, const float* trace_rows, const int64_t* raw_off, const int32_t* raw_n, int nraw,
+                     int stream_n, const int64_t* truth, int ntruth, double* mass_out, int32_t* counts_out,
+                     void* stream);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,8 @@ SIGNATURES = {
     "skv_state_inject": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _P, _P]),
     "skv_state_dump": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "skv_sync": (_I, [_P, _P]),
+    "skv_slot_map": (_I, [_P, _I, _I, ctypes.POINTER(_P)]),
+    "skv_moved_rows": (_I, [_P, _P]),
     "skv_capture_begin": (_I, [_P, _P]),
     "skv_capture_end": (_I, [_P, _P]),
     "skv_graph_launch": (_I, [_P, _P]),
@@ -97,6 +99,13 @@ SIGNATURES = {
     "skv_window_scores": (_I, [_P, _I, _P, _I, _I, _I, _F, _I, _P, _P]),
     "skv_gather_rows": (_I, [_P, _I64, _I, _I, _P, _I, _P]),
     "skv_attend": (_I, [_P, _P, _I, _I, _I, _I64, _P, _P, _P, _P]),
+    "skv_softmax_row": (_I, [_P, _I, _P, _P]),
+    "skv_attn_probs": (_I, [_P, _P, _I, _I, _F, _P, _P]),
+    "skv_weighted_sum": (_I, [_P, _P, _I, _I, _P, _P]),
+    "skv_rope_apply": (_I, [_P, _I, _I64, ctypes.c_double, _P, _P]),
+    "skv_replay_rows": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
+    "skv_replay_evict": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _I, _P, _P,
+                              _P]),
 }
 
 _lib = None

@@ -8,6 +8,14 @@
 // to read.  One CTA per (block, head) for the K/V rows (16-byte vectors, 4 per
 // thread per array in flight); one extra CTA per block for token metadata and
 // the window rows.  The identity prefix [0, first) is skipped.
+//
+// Slot-map engines (CompactArgs::moves) skip the stable shift altogether: the
+// selection kernel planned which kept rows must move (at most the tokens
+// appended since the last eviction), each row moves once from a source row
+// >= m to a free destination row < m, and the logical order lives in the slot
+// map.  Token metadata and window lengths are still gathered in logical order.
+#include <algorithm>
+
 #include "skv_common.cuh"
 #include "skv_internal.h"
 
@@ -73,8 +81,61 @@ __device__ void gather_elems(E* x, const CompactArgs& a, int b, int first, int m
   }
 }
 
+// Planned row moves (src -> dst, disjoint): each thread copies 16-byte units of
+// the listed rows of up to three arrays of one head segment.
+__device__ void move_rows16(uint4* x, uint4* y, uint4* z, int units, const int32_t* trip, int count) {
+  for (int idx = threadIdx.x; idx < count * units; idx += kCmpThreads) {
+    const int j = idx / units, u = idx - j * units;
+    const int64_t src = (int64_t)trip[3 * j] * units + u, dst = (int64_t)trip[3 * j + 1] * units + u;
+    const uint4 xv = x[src];
+    const uint4 yv = y ? y[src] : uint4{};
+    const uint4 zv = z ? z[src] : uint4{};
+    x[dst] = xv;
+    if (y) y[dst] = yv;
+    if (z) z[dst] = zv;
+  }
+}
+
 __global__ void __launch_bounds__(kCmpThreads) compact_kernel(const CompactArgs a) {
   const int h = blockIdx.x, b = blockIdx.y;
+  if (a.moves) {
+    // ---- slot-map compaction: planned moves only
+    const int32_t* trip = a.moves + b * a.mv_bs;
+    const int count = a.mcount[b * a.mc_bs];
+    if (h < a.heads) {
+      const int units = a.row_bytes / 16;
+      uint4* kx = reinterpret_cast<uint4*>(a.k + b * a.kv_bs + h * a.kv_hs);
+      uint4* vx = reinterpret_cast<uint4*>(a.v + b * a.kv_bs + h * a.kv_hs);
+      uint4* rx = a.k_raw ? reinterpret_cast<uint4*>(a.k_raw + b * a.kv_bs + h * a.kv_hs) : nullptr;
+      move_rows16(kx, vx, rx, units, trip, count);
+      return;
+    }
+    const int first = a.first_moved ? min(a.first_moved[b], a.m) : 0;
+    if (first < a.m) {  // token metadata: logical order (cache.py:154-156)
+      if (a.pos) gather_elems<int64_t>(a.pos + b * a.m_bs, a, b, first, a.m);
+      if (a.modality) gather_elems<int8_t>(a.modality + b * a.m_bs, a, b, first, a.m);
+      if (a.round_id) gather_elems<int32_t>(a.round_id + b * a.m_bs, a, b, first, a.m);
+    }
+    // accumulators (engine.py:335) and window-row values sit at physical rows:
+    // a row keeps the mover's value when the mover lies inside its new length
+    if (a.acc) {
+      float* acc = a.acc + b * a.acc_bs;
+      for (int j = threadIdx.x; j < count; j += kCmpThreads) acc[trip[3 * j + 1]] = acc[trip[3 * j]];
+    }
+    if (a.rows) {
+      for (int idx = threadIdx.x; idx < a.W * count; idx += kCmpThreads) {
+        const int w = idx / count, j = idx - w * count;
+        if (trip[3 * j + 2] < a.newlen[b * a.w_bs + w]) {
+          float* row = a.rows + b * a.r_bs + (int64_t)w * a.row_stride;
+          row[trip[3 * j + 1]] = row[trip[3 * j]];
+        }
+      }
+      __syncthreads();
+      for (int w = threadIdx.x; w < a.W; w += blockDim.x) a.wlen[b * a.w_bs + w] = a.newlen[b * a.w_bs + w];
+    }
+    if (threadIdx.x == 0 && a.len) a.len[b * a.len_bs] = a.m;
+    return;
+  }
   const int first = a.first_moved ? min(a.first_moved[b], a.m) : 0;
   if (h < a.heads) {
     if (first >= a.m) return;
@@ -116,6 +177,23 @@ cudaError_t launch_compact(int blocks, const CompactArgs& a, cudaStream_t st) {
   if (a.row_bytes % 16) return cudaErrorInvalidValue;
   dim3 grid(a.heads + 1, blocks);
   compact_kernel<<<grid, kCmpThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace skv
+
+namespace skv {
+
+// p[i] = i % period for i < count (identity slot maps).
+__global__ void iota_kernel(int32_t* p, int64_t count, int period) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)(i % period);
+}
+
+cudaError_t launch_iota(int32_t* p, int64_t count, int period, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>(4096, (count + 255) / 256);
+  if (blocks <= 0) return cudaSuccess;
+  iota_kernel<<<blocks, 256, 0, st>>>(p, count, period);
   return cudaGetLastError();
 }
 

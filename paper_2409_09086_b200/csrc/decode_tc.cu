@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
     return;
   }
 
+  if (warp == NW + 1) return;  // (the append is done by the consumers before they publish)
+
   // ------------------------------------------------------------ consumers
   griddep_wait();
   if (tid == 0) griddep_launch();

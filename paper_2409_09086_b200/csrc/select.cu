@@ -11,150 +11,88 @@
 //     toward the larger index, ascending output by a block-wide scan;
 //   inf_mllm_decide (policies.py:184-201): keep-all when n <= r+l, otherwise
 //     kept = relevant ++ [n-l, n).
-// It also emits what compaction needs: the first moved index (kept[i] != i) and
-// the window row lengths after AttentionWindow.remap (policies.py:117-124).
+// It also emits what compaction needs: the first moved index (kept[i] != i),
+// the window row lengths after AttentionWindow.remap (policies.py:117-124)
+// and, for engines with a slot map, the plan of the compaction (plan_moves).
 #include <algorithm>
 
 #include "skv_common.cuh"
 #include "skv_internal.h"
+#include "skv_topk.cuh"
 
 namespace skv {
 
 constexpr int kSelThreads = 1024;
 
-struct ScanSmem {
-  int warp_sums[32];
-  int total;
-};
-
-// Block-wide exclusive scan of one int per thread.  All threads must call.
-__device__ int block_excl_scan(int v, ScanSmem& sm, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sm.warp_sums[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = lane < nw ? sm.warp_sums[lane] : 0;
-    int incl = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane < nw) sm.warp_sums[lane] = incl - w;
-    if (lane == 31) sm.total = incl;
-  }
-  __syncthreads();
-  const int excl = sm.warp_sums[warp] + x - v;
-  total = sm.total;
-  __syncthreads();
-  return excl;
-}
-
-struct TopkSmem {
-  unsigned hist[256];
-  unsigned prefix;
-  int krem;
-  int first_unsel;
-  ScanSmem scan;
-};
-
-// Select the k largest of scores[0, cols) (ties -> larger index) and write their
-// indices ascending to out32/out64[0, k).  Requires 0 < k < cols.  Returns
-// (through smem) the smallest unselected index.
-__device__ void topk_block(const float* scores, int cols, int k, int32_t* out32, int64_t* out64, TopkSmem& sm) {
+// Slot-map compaction plan for one (stream, layer).  Logical slot c lives in
+// physical row perm[c]; rows [0, n) hold exactly the live tokens.  After the
+// decision keeps `kept` (ascending, m entries) the kept tokens must occupy rows
+// [0, m) again.  Those already there stay put; each kept token whose row is
+// >= m moves into a row of [0, m) freed by an evicted token (the i-th such
+// mover, in logical order, to the i-th free row, ascending).  Sources (>= m)
+// and destinations (< m) are disjoint, so the moves are hazard-free and
+// independent.  The logical order (cache.py:151-156: stable, ascending) is
+// carried by the new perm; token metadata and window lengths stay logical.
+// At most n - m rows move -- the tokens appended since the last eviction that
+// survive it -- instead of every row after the first evicted one.
+__device__ void plan_moves(const SelectArgs& a, int b, int n, int m, const int32_t* k32, const int64_t* k64,
+                           unsigned* used, ScanSmem& scan) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  unsigned prefix = 0, mask = 0;
-  int krem = k;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    for (int i = tid; i < 256; i += nt) sm.hist[i] = 0;
-    __syncthreads();
-    for (int c = tid; c < cols; c += nt) {
-      const unsigned u = orderable(scores[c]);
-      if ((u & mask) == prefix) atomicAdd(&sm.hist[(u >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (tid < 32) {
-      // lane L owns bins [8L, 8L+8); find the digit holding the krem-th largest
-      unsigned local[8];
-      unsigned lsum = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        local[i] = sm.hist[8 * tid + i];
-        lsum += local[i];
-      }
-      unsigned suffix = lsum;  // inclusive suffix sum over lanes >= tid
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_down_sync(0xffffffffu, suffix, o);
-        if (tid + o < 32) suffix += y;
-      }
-      const unsigned above = suffix - lsum;  // count in lanes > tid
-      if (above < (unsigned)krem && suffix >= (unsigned)krem) {
-        unsigned acc = above;
-        int digit = 8 * tid;
-        for (int i = 7; i >= 0; --i) {
-          if (acc + local[i] >= (unsigned)krem) {
-            digit = 8 * tid + i;
-            break;
-          }
-          acc += local[i];
-        }
-        sm.prefix = prefix | ((unsigned)digit << shift);
-        sm.krem = krem - (int)acc;
-      }
-    }
-    __syncthreads();
-    prefix = sm.prefix;
-    krem = sm.krem;
-    mask |= 255u << shift;
-    __syncthreads();
-  }
-  const unsigned thr = prefix;  // key of the k-th largest; take krem of its ties
-
-  // contiguous segment per thread so scans preserve index order
-  const int seg = (cols + nt - 1) / nt;
-  const int c0 = min(tid * seg, cols), c1 = min(c0 + seg, cols);
-  int eq = 0;
-  for (int c = c0; c < c1; ++c) eq += orderable(scores[c]) == thr;
-  int eq_total;
-  const int eq_before = block_excl_scan(eq, sm.scan, eq_total);
-  if (tid == 0) sm.first_unsel = cols;
+  int32_t* perm = a.perm + b * a.pm_bs;
+  int32_t* pk = a.moves + b * a.mv_bs;     // [m] physical row of kept[i]
+  int32_t* trip = pk + a.row_stride;       // [count][3] (src, dst, logical index); region = 4 x capacity
+  const int words = (m + 31) / 32;
+  for (int w = tid; w < words; w += nt) used[w] = 0;
   __syncthreads();
-  int nsel = 0, r = eq_before, first_un = cols;
-  for (int c = c0; c < c1; ++c) {
-    const unsigned u = orderable(scores[c]);
-    bool sel = u > thr;
-    if (u == thr) {
-      sel = (eq_total - 1 - r) < krem;  // newest ties win
-      ++r;
-    }
-    nsel += sel;
-    if (!sel && first_un == cols) first_un = c;
+  for (int i = tid; i < m; i += nt) {
+    const int c = k32 ? k32[i] : (int)k64[i];
+    const int p = perm[c];
+    pk[i] = p;
+    if (p < m) atomicOr(&used[p >> 5], 1u << (p & 31));
   }
-  if (first_un < cols) atomicMin(&sm.first_unsel, first_un);
-  int sel_total;
-  int pos = block_excl_scan(nsel, sm.scan, sel_total);
-  r = eq_before;
-  for (int c = c0; c < c1; ++c) {
-    const unsigned u = orderable(scores[c]);
-    bool sel = u > thr;
-    if (u == thr) {
-      sel = (eq_total - 1 - r) < krem;
-      ++r;
-    }
-    if (sel) {
-      if (out32) out32[pos] = c;
-      if (out64) out64[pos] = c;
-      ++pos;
+  __syncthreads();
+  // free rows of [0, m), ascending: contiguous word ranges per thread
+  const int wseg = (words + nt - 1) / nt;
+  const int w0 = min(tid * wseg, words), w1 = min(w0 + wseg, words);
+  auto free_bits = [&](int w) {
+    const unsigned valid = (w == words - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : 0xffffffffu;
+    return ~used[w] & valid;
+  };
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(free_bits(w));
+  int holes_total;
+  int rank = block_excl_scan(cnt, scan, holes_total);
+  for (int w = w0; w < w1; ++w) {
+    unsigned f = free_bits(w);
+    while (f) {
+      const int bit = __ffs(f) - 1;
+      f &= f - 1;
+      trip[3 * rank + 1] = 32 * w + bit;
+      ++rank;
     }
   }
+  __syncthreads();
+  // movers in logical order take the free rows in ascending order
+  const int seg = (m + nt - 1) / nt;
+  const int i0 = min(tid * seg, m), i1 = min(i0 + seg, m);
+  int mv = 0;
+  for (int i = i0; i < i1; ++i) mv += pk[i] >= m;
+  int movers_total;
+  int j = block_excl_scan(mv, scan, movers_total);
+  for (int i = i0; i < i1; ++i) {
+    const int p = pk[i];
+    if (p >= m) {
+      const int dst = trip[3 * j + 1];
+      trip[3 * j] = p;
+      trip[3 * j + 2] = i;
+      perm[i] = dst;
+      ++j;
+    } else {
+      perm[i] = p;
+    }
+  }
+  for (int i = m + tid; i < n; i += nt) perm[i] = i;  // appends land at their logical slot
+  if (tid == 0) a.mcount[b * a.mc_bs] = movers_total;  // == holes_total
   __syncthreads();
 }
 
@@ -162,6 +100,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
   __shared__ TopkSmem sm;
   __shared__ int slot_of[1024];
   __shared__ int len_of[1024];
+  __shared__ unsigned used_rows[kMaxMapRows / 32];
   const int b = blockIdx.x, tid = threadIdx.x;
   const int n = a.n, l = a.l, r = a.r;
   int32_t* k32 = a.kept32 ? a.kept32 + b * a.k_bs : nullptr;
@@ -193,7 +132,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
         // heavy_hitter_decide (policies.py:246-256): top-r of the accumulated
         // mass acc[:n-l], no averaging, no bias
         const float* acc = a.acc + b * a.acc_bs;
-        for (int c = tid; c < cols; c += blockDim.x) sc[c] = acc[c];
+        const int32_t* pm = a.perm ? a.perm + b * a.pm_bs : nullptr;
+        for (int c = tid; c < cols; c += blockDim.x) sc[c] = acc[pm ? pm[c] : c];
       } else {
         // ---- window-mean scores (+ bias), policies.py:130-162
         const float d = __fdiv_rn(a.bias, (float)cols);
@@ -201,14 +141,17 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
         const float inv_m = (float)a.count;
         const float* rows = a.rows + b * a.r_bs;
         const float* sin = a.scores_in ? a.scores_in + b * a.si_bs : nullptr;
+        const int32_t* pm = a.perm ? a.perm + b * a.pm_bs : nullptr;
         for (int c = tid; c < cols; c += blockDim.x) {
           float v;
           if (sin) {
             v = sin[c];
           } else {
+            // row values sit at the column's physical row (slot map)
+            const int pc = pm ? pm[c] : c;
             float acc = 0.f;
             for (int k = 0; k < a.count; ++k)
-              if (c < len_of[k]) acc = __fadd_rn(acc, rows[(int64_t)slot_of[k] * a.row_stride + c]);
+              if (c < len_of[k]) acc = __fadd_rn(acc, rows[(int64_t)slot_of[k] * a.row_stride + pc]);
             v = __fdiv_rn(acc, inv_m);
           }
           if (a.apply_bias) v = __fadd_rn(v, __fmul_rn(negd, (float)(cols - 1 - c)));
@@ -231,6 +174,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
       if (tid == 0 && a.first_moved) a.first_moved[b] = first;
     }
     __syncthreads();
+    if (a.moves) plan_moves(a, b, n, r + l, k32, k64, used_rows, sm.scan);
     // ---- window lengths after remap: #{i : kept[i] < len}
     if (a.newlen) {
       for (int k = tid; k < a.count; k += blockDim.x) {
@@ -255,6 +199,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
       if (k64) k64[i] = -1;
     }
     if (tid == 0 && a.first_moved) a.first_moved[b] = n;
+    if (tid == 0 && a.moves) a.mcount[b * a.mc_bs] = 0;  // keep-all: nothing moves
     if (a.newlen)
       for (int k = tid; k < a.count; k += blockDim.x) a.newlen[b * a.w_bs + slot_of[k]] = len_of[k];
   }

@@ -132,6 +132,15 @@ struct skv_ctx {
   size_t p_tokens = 0;  // S*C capacity of pqr/pkr
   int32_t* kept = nullptr;
   int32_t* first_moved = nullptr;
+  // slot map (see select.cu plan_moves): perm [S][L][cap] logical slot ->
+  // physical row; moves [S][L][4 cap] planning scratch + (src, dst, index)
+  // triplets; mcount [S][L] rows moved by the last eviction.  Off (dense
+  // stable compaction) for cache-relative RoPE, whose moved keys change
+  // position anyway.
+  bool slotmap = false;
+  int32_t* perm = nullptr;
+  int32_t* moves = nullptr;
+  int32_t* mcount = nullptr;
   float* scores = nullptr;
   int64_t* pos_in = nullptr;  // staging for explicit positions
   // sticky device error word: bit 0 = a chunked prefill saw |v| >= 65504 (its
@@ -202,6 +211,10 @@ struct skv_ctx {
   int64_t kv_stream_stride() const { return (int64_t)L * kv_layer_stride(); }
 
 };
+
+namespace skv {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace skv
 
 // A layer whose streams were injected with different lengths / window rows
 // cannot run: every kernel takes one length per layer (lock-stepped streams).
@@ -324,6 +337,14 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   chk(x->alloc(&x->scores, SL * x->cap * sizeof(float)));
   chk(x->alloc(&x->pos_in, x->S * sizeof(int64_t)));
   chk(x->alloc(&x->err_word, sizeof(int32_t)));
+  x->slotmap = c.rope_mode != SKV_ROPE_CACHE_RELATIVE && x->cap <= kMaxMapRows;
+  if (x->slotmap) {
+    chk(x->alloc(&x->perm, SL * x->cap * sizeof(int32_t)));
+    chk(x->alloc(&x->moves, SL * 4 * (size_t)x->cap * sizeof(int32_t)));
+    chk(x->alloc(&x->mcount, SL * sizeof(int32_t)));
+    if (e == cudaSuccess) chk(launch_iota(x->perm, (int64_t)SL * x->cap, x->cap, nullptr));
+    if (e == cudaSuccess) chk(cudaDeviceSynchronize());
+  }
   // heavy-hitter accumulators (engine.py:274): one column per cached token
   if (c.policy == SKV_POLICY_HEAVY_HITTER) chk(x->alloc(&x->acc, SL * (size_t)x->cap * sizeof(float)));
   if (c.rope_mode != SKV_ROPE_NONE) {
@@ -937,6 +958,16 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     a.newlen = x->newlen;
     a.acc = x->acc;
     a.acc_bs = x->cap;
+    if (x->slotmap) {
+      a.perm = x->perm;
+      a.pm_bs = x->cap;
+      if (mode != 1) {
+        a.moves = x->moves;
+        a.mv_bs = 4 * (int64_t)x->cap;
+        a.mcount = x->mcount;
+        a.mc_bs = 1;
+      }
+    }
     cudaError_t e = launch_select(x->S * x->L, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
     x->launches++;
@@ -963,6 +994,12 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     c.acc_bs = x->cap;
     c.k_raw = static_cast<char*>(x->kraw);
     c.rope_cr = x->cfg.rope_mode == SKV_ROPE_CACHE_RELATIVE;
+    if (x->slotmap) {
+      c.moves = x->moves;
+      c.mv_bs = 4 * (int64_t)x->cap;
+      c.mcount = x->mcount;
+      c.mc_bs = 1;
+    }
     e = launch_compact(x->S * x->L, c, st);
     if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
     x->launches++;
@@ -990,6 +1027,16 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       a.newlen = x->newlen + sl0 * x->W;
       a.acc = x->acc ? x->acc + sl0 * x->cap : nullptr;
       a.acc_bs = (int64_t)x->L * x->cap;
+      if (x->slotmap) {
+        a.perm = x->perm + sl0 * x->cap;
+        a.pm_bs = (int64_t)x->L * x->cap;
+        if (mode != 1) {
+          a.moves = x->moves + sl0 * 4 * (int64_t)x->cap;
+          a.mv_bs = (int64_t)x->L * 4 * x->cap;
+          a.mcount = x->mcount + sl0;
+          a.mc_bs = x->L;
+        }
+      }
       cudaError_t e = launch_select(x->S, a, st);
       if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
       x->launches++;
@@ -1016,6 +1063,12 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       c.acc_bs = (int64_t)x->L * x->cap;
       c.k_raw = x->kraw ? static_cast<char*>(x->kraw) + sl0 * x->kv_layer_stride() * x->elt : nullptr;
       c.rope_cr = x->cfg.rope_mode == SKV_ROPE_CACHE_RELATIVE;
+      if (x->slotmap) {
+        c.moves = a.moves;
+        c.mv_bs = a.mv_bs;
+        c.mcount = a.mcount;
+        c.mc_bs = a.mc_bs;
+      }
       e = launch_compact(x->S, c, st);
       if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
       x->launches++;
@@ -1116,6 +1169,17 @@ static int stream_state(const skv_ctx* x, int stream, int layer, int* n, int* m,
   return SKV_OK;
 }
 
+// Host copy of the slot map of (stream, layer) (identity without one).
+static int host_perm(const skv_ctx* x, int64_t sl, int n, std::vector<int32_t>& perm) {
+  perm.resize(std::max(n, 1));
+  if (!x->perm) {
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    return SKV_OK;
+  }
+  if (n > 0) SKV_CK(cudaMemcpy(perm.data(), x->perm + sl * x->cap, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return SKV_OK;
+}
+
 int skv_positions(skv_ctx* x, int stream, int layer, int64_t* out, int cap) {
   if (!x || !out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   int nn, mm, hh;
@@ -1140,14 +1204,20 @@ int skv_window_rows(skv_ctx* x, int stream, int layer, float* rows_host, int32_t
   }
   SKV_CK(cudaDeviceSynchronize());
   const int64_t sl = (int64_t)stream * x->L + layer;
-  std::vector<int32_t> lens(x->W);
+  std::vector<int32_t> lens(x->W), perm;
   SKV_CK(cudaMemcpy(lens.data(), x->wlen + sl * x->W, x->W * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  rc = host_perm(x, sl, nn, perm);
+  if (rc) return rc;
+  std::vector<float> phys(std::max(nn, 1));
   for (int k = 0; k < count; ++k) {
     const int slot = ((head - count + k) % x->W + x->W) % x->W;
-    if (lens_host) lens_host[k] = lens[slot];
-    if (rows_host)
-      SKV_CK(cudaMemcpy(rows_host + (int64_t)k * x->cap, x->rows + (sl * x->W + slot) * x->cap,
-                        (size_t)lens[slot] * sizeof(float), cudaMemcpyDeviceToHost));
+    const int len = std::min(lens[slot], nn);
+    if (lens_host) lens_host[k] = len;
+    if (rows_host && nn > 0) {  // values sit at physical rows: logical column c <- perm[c]
+      SKV_CK(cudaMemcpy(phys.data(), x->rows + (sl * x->W + slot) * x->cap, (size_t)nn * sizeof(float),
+                        cudaMemcpyDeviceToHost));
+      for (int c = 0; c < len; ++c) rows_host[(int64_t)k * x->cap + c] = phys[perm[c]];
+    }
   }
   rc = check_sticky(x);
   return rc ? rc : count;
@@ -1172,13 +1242,22 @@ int skv_state_dump(skv_ctx* x, int stream, int layer, int* n_out, int* m_out, vo
   const size_t rb = (size_t)x->D * x->elt;
   const char* kd = static_cast<const char*>(x->kraw ? x->kraw : x->k) + sl * x->kv_layer_stride() * x->elt;
   const char* vd = static_cast<const char*>(x->v) + sl * x->kv_layer_stride() * x->elt;
+  std::vector<int32_t> perm;
+  rc = host_perm(x, sl, n, perm);
+  if (rc) return rc;
   if (n > 0) {
-    if (k_host)
-      SKV_CK(cudaMemcpy2D(k_host, (size_t)n * rb, kd, (size_t)x->cap * rb, (size_t)n * rb, x->Hkv,
+    // K/V rows are physical: read the segment, emit logical row c = physical perm[c]
+    std::vector<char> seg((size_t)n * rb);
+    for (int pass = 0; pass < 2; ++pass) {
+      char* dst = static_cast<char*>(pass ? v_host : k_host);
+      if (!dst) continue;
+      for (int h = 0; h < x->Hkv; ++h) {
+        SKV_CK(cudaMemcpy(seg.data(), (pass ? vd : kd) + (size_t)h * x->cap * rb, (size_t)n * rb,
                           cudaMemcpyDeviceToHost));
-    if (v_host)
-      SKV_CK(cudaMemcpy2D(v_host, (size_t)n * rb, vd, (size_t)x->cap * rb, (size_t)n * rb, x->Hkv,
-                          cudaMemcpyDeviceToHost));
+        for (int c = 0; c < n; ++c)
+          memcpy(dst + ((size_t)h * n + c) * rb, seg.data() + (size_t)perm[c] * rb, rb);
+      }
+    }
     if (pos_host) SKV_CK(cudaMemcpy(pos_host, x->pos + sl * x->cap, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
     if (modality_host) SKV_CK(cudaMemcpy(modality_host, x->modality + sl * x->cap, n, cudaMemcpyDeviceToHost));
     if (round_host)
@@ -1186,19 +1265,36 @@ int skv_state_dump(skv_ctx* x, int stream, int layer, int* n_out, int* m_out, vo
   }
   if (m > 0 && (rows_host || lens_host)) {
     std::vector<int32_t> lens(x->W);
+    std::vector<float> phys(std::max(n, 1));
     SKV_CK(cudaMemcpy(lens.data(), x->wlen + sl * x->W, x->W * sizeof(int32_t), cudaMemcpyDeviceToHost));
     for (int k = 0; k < m; ++k) {
       const int slot = ((head - m + k) % x->W + x->W) % x->W;
       const int len = std::min(lens[slot], n);
       if (lens_host) lens_host[k] = len;
       if (rows_host) {
-        SKV_CK(cudaMemcpy(rows_host + (int64_t)k * n, x->rows + (sl * x->W + slot) * x->cap, (size_t)len * sizeof(float),
-                          cudaMemcpyDeviceToHost));
-        std::fill(rows_host + (int64_t)k * n + len, rows_host + (int64_t)(k + 1) * n, 0.f);
+        if (n > 0)
+          SKV_CK(cudaMemcpy(phys.data(), x->rows + (sl * x->W + slot) * x->cap, (size_t)n * sizeof(float),
+                            cudaMemcpyDeviceToHost));
+        for (int c = 0; c < n; ++c) rows_host[(int64_t)k * n + c] = c < len ? phys[perm[c]] : 0.f;
       }
     }
   }
   return check_sticky(x);
+}
+
+int skv_slot_map(skv_ctx* x, int stream, int layer, int32_t** perm_dev) {
+  if (!x || !perm_dev || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
+    return fail(SKV_EINVAL, "out of range");
+  *perm_dev = x->perm ? x->perm + ((int64_t)stream * x->L + layer) * x->cap : nullptr;
+  return SKV_OK;
+}
+
+int skv_moved_rows(skv_ctx* x, int32_t* out_host) {
+  if (!x || !out_host) return fail(SKV_EINVAL, "null argument");
+  if (!x->mcount) return fail(SKV_ESTATE, "no slot map: this engine compacts densely");
+  SKV_CK(cudaDeviceSynchronize());
+  SKV_CK(cudaMemcpy(out_host, x->mcount, x->sl_count() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return SKV_OK;
 }
 
 int skv_sync(skv_ctx* x, void* stream) {
@@ -1247,6 +1343,10 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
   }
   const int32_t n32 = n;
   SKV_CK(cudaMemcpy(x->len + sl, &n32, sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (x->perm) {  // injected rows are in logical order: identity slot map
+    SKV_CK(launch_iota(x->perm + sl * x->cap, x->cap, x->cap, nullptr));
+    SKV_CK(cudaDeviceSynchronize());
+  }
   for (int k = 0; k < m; ++k)
     if (rows_host)
       SKV_CK(cudaMemcpy(x->rows + (sl * x->W + k) * x->cap, rows_host + (int64_t)k * n, (size_t)lens[k] * sizeof(float),

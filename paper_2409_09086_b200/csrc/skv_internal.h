@@ -15,6 +15,9 @@ inline int device_slot() {
   if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
   return d;
 }
+// Records the calling thread's error message (skv_last_error) and returns code.
+int set_error(int code, const char* msg);
+
 struct DevOnce {
   bool done[kMaxDevices] = {};
   bool& here() { return done[device_slot()]; }
@@ -139,6 +142,19 @@ struct SelectArgs {
   int sink;             // sink_count (policy 2)
   const float* acc;     // heavy-hitter accumulators acc + b*acc_bs (policy 3)
   int64_t acc_bs;
+  // Slot map (engine evictions): perm + b*pm_bs maps logical slot c -> the
+  // physical row holding it (identity beyond the last eviction's kept count).
+  // Window rows and accumulators are stored by physical row and read through
+  // it.  With `moves` set, the kernel also plans the compaction: the kept
+  // tokens whose rows lie at or beyond m move into the rows in [0, m) freed by
+  // evicted tokens (moves + b*mv_bs: [count][3] = src row, dst row, logical
+  // index; mcount[b] = count) and perm is rewritten for the new order.
+  int32_t* perm;
+  int64_t pm_bs;
+  int32_t* moves;
+  int64_t mv_bs;
+  int32_t* mcount;      // mcount[b * mc_bs]
+  int64_t mc_bs;
 };
 
 cudaError_t launch_select(int batches, const SelectArgs& a, cudaStream_t st);
@@ -185,9 +201,20 @@ struct CompactArgs {
   char* k_raw;           // RoPE: raw key store (layout of k), gathered too
   int rope_cr;           // RoPE cache-relative: gather raw keys + values only (the rotated
                          // rows are recomputed from the raw ones afterwards)
+  // Slot-map compaction (SelectArgs::moves): with `moves` set, K/V (and raw
+  // key) rows, window-row values and accumulators move only along the planned
+  // (src -> dst) list; token metadata and window lengths are still gathered
+  // in logical order from `kept`.
+  const int32_t* moves;
+  int64_t mv_bs;
+  const int32_t* mcount;  // mcount[b * mc_bs]
+  int64_t mc_bs;
 };
 
 cudaError_t launch_compact(int blocks, const CompactArgs& a, cudaStream_t st);
+// p[i] = i % period, i < count (identity slot maps)
+cudaError_t launch_iota(int32_t* p, int64_t count, int period, cudaStream_t st);
+constexpr int kMaxMapRows = 8192 * 32;  // slot-map engines: capacity bound of the selection's row bitmap
 
 // ----------------------------------------------------------------------------
 // K4: chunked prefill attention (tcgen05), bf16, head_dim 128

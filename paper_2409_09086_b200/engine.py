@@ -264,23 +264,45 @@ class StreamEngine:
     def length(self, stream: int = 0, layer: int = 0) -> int:
         return check(self.lib.skv_length(self._h, stream, layer))
 
-    def kv(self, stream: int, layer: int):
-        """Views (Hkv, n, D) of the live keys/values of (stream, layer)."""
-        kp, vp = ctypes.c_void_p(), ctypes.c_void_p()
-        check(self.lib.skv_kv_view(self._h, stream, layer, ctypes.byref(kp), ctypes.byref(vp)))
-        c = self.cfg
+    def slot_map(self, stream: int, layer: int) -> Optional[torch.Tensor]:
+        """int32 (n,) view: logical slot -> physical row (None: identity)."""
+        pp = ctypes.c_void_p()
+        check(self.lib.skv_slot_map(self._h, stream, layer, ctypes.byref(pp)))
+        if not pp.value:
+            return None
         n = self.length(stream, layer)
-        full = (c.heads_kv, self.cap, c.head_dim)
-        kt = _wrap(kp.value, full, c.dtype)
-        vt = _wrap(vp.value, full, c.dtype)
-        return kt[:, :n], vt[:, :n]
+        return _wrap(pp.value, (self.cap,), torch.int32)[:n]
+
+    def kv(self, stream: int, layer: int):
+        """Keys/values (Hkv, n, D) of (stream, layer) in logical (cache) order
+        -- KvCache.keys()/values().  Without a slot map (or before the first
+        eviction) these are views of the store; otherwise gathered copies."""
+        kt, vt = self.kv_full(stream, layer)
+        n = self.length(stream, layer)
+        perm = self.slot_map(stream, layer)
+        if perm is None:
+            return kt[:, :n], vt[:, :n]
+        idx = perm.long()
+        if bool((idx == torch.arange(n, device=idx.device)).all()):
+            return kt[:, :n], vt[:, :n]
+        return kt.index_select(1, idx), vt.index_select(1, idx)
 
     def kv_full(self, stream: int, layer: int):
+        """Views (Hkv, capacity, D) of the PHYSICAL key/value storage."""
         kp, vp = ctypes.c_void_p(), ctypes.c_void_p()
         check(self.lib.skv_kv_view(self._h, stream, layer, ctypes.byref(kp), ctypes.byref(vp)))
         c = self.cfg
         full = (c.heads_kv, self.cap, c.head_dim)
         return _wrap(kp.value, full, c.dtype), _wrap(vp.value, full, c.dtype)
+
+    def moved_rows(self) -> Optional[np.ndarray]:
+        """(S, L) rows moved by the last eviction (None: dense compaction)."""
+        out = np.zeros((self.cfg.streams, self.cfg.layers), np.int32)
+        rc = self.lib.skv_moved_rows(self._h, out.ctypes.data_as(ctypes.c_void_p))
+        if rc == _lib.SKV_ESTATE:
+            return None
+        check(rc)
+        return out
 
     def positions(self, stream: int, layer: int) -> np.ndarray:
         out = np.zeros(self.cap, dtype=np.int64)
@@ -344,13 +366,13 @@ class StreamEngine:
 
 def _wrap(ptr: int, shape, dtype: torch.dtype) -> torch.Tensor:
     """Zero-copy torch view of engine-owned device memory."""
-    typestr = {torch.float32: "<f4", torch.bfloat16: "<V2"}[dtype]
-    elt = 4 if dtype == torch.float32 else 2
+    typestr = {torch.float32: "<f4", torch.bfloat16: "<i2", torch.int32: "<i4"}[dtype]
+    elt = 2 if dtype == torch.bfloat16 else 4
 
     class _Iface:
         __cuda_array_interface__ = {
             "shape": tuple(shape),
-            "typestr": typestr if dtype == torch.float32 else "<i2",
+            "typestr": typestr,
             "data": (ptr, False),
             "version": 2,
             "strides": None,

@@ -212,3 +212,43 @@ def test_cache_longer_than_merge_chunk_limit(G):
         ref = (p[:, None, :] @ V)[:, 0]
         assert n == n0 + _ + 1
         assert rel_err(out[0].cpu().numpy(), ref.cpu().numpy()) < 2e-3
+
+
+def test_slot_map_moves_only_the_survivors_of_the_period():
+    """Slot-map compaction: with l >= E every token appended in the period is
+    in the recent window, so exactly E rows move per (stream, layer) -- not
+    the ~B rows a stable in-place shift moves -- and the cache read back in
+    logical order equals the oracle's gather_keep (cache.py:136-156)."""
+    S, L, Hq, Hkv, D = 2, 2, 8, 2, 128
+    l, r, W, E = 64, 64, 8, 32
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = _eng(S, L, Hq, Hkv, D, l, r, W, B + E)
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    rng = np.random.default_rng(21)
+    _inject_both(eng, orc, rng, S, L, Hkv, D, B)
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    for period in range(3):
+        for _ in range(E):
+            q = bf16_round(rng.standard_normal((L, S, Hq, D)).astype(F32))
+            k = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            eng.decode_step(*(torch.from_numpy(a).to("cuda", torch.bfloat16) for a in (q, k, v)), record=True)
+            orc.step(q, k, v)
+        eng.evict(-1, kept)
+        kc = kept.cpu().numpy()
+        np.testing.assert_array_equal(eng.moved_rows(), np.full((S, L), E))
+        for s in range(S):
+            for layer in range(L):
+                ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept, kc[s, layer],
+                                                B + E, cfg)
+                assert ok, (period, s, layer, nbad, gap)
+                orc.apply(s, layer, kc[s, layer].astype(np.int64))
+                kg, vg = eng.kv(s, layer)
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
+                perm = eng.slot_map(s, layer).cpu().numpy()
+                assert sorted(perm.tolist()) == list(range(B))  # rows [0, B) hold exactly the kept tokens
+    # cache-relative RoPE engines compact densely (their moved keys change position anyway)
+    dense = _eng(1, 1, 8, 2, 128, 32, 32, 8, 80, rope="cache_relative")
+    assert dense.moved_rows() is None and dense.slot_map(0, 0) is None

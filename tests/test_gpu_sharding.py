@@ -79,3 +79,70 @@ def test_two_kv_head_shards_match_unsharded_reference():
                     np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys()[kvs])
     print(f"sharded worst output rel err {worst:.2e}")
     assert worst <= 2e-3
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_kv_head_selection_matches_per_group_reference(world):
+    """select="kv_head" (the collective-free mode): every
+    KV-head group keeps its own window of G-head mean rows and its own
+    Algorithm-1 decision.  Oracle: the reference pipeline run per group
+    (StreamOracle over S*Hkv pseudo-streams of one KV head and G query heads).
+    With world = 2 the KV heads split over two shard engines that never
+    exchange anything."""
+    from paper_2409_09086_b200 import EngineConfig
+    from paper_2409_09086_b200.sharding import KvHeadEngine, shard_heads
+
+    S, L, HQ, HKV, D = 1, 2, 32, 8, 128
+    l, r, W, E, periods = 256, 256, 32, 64, 2
+    B = l + r
+    G = HQ // HKV
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    shards = []
+    for rank in range(world):
+        kvs, qs = shard_heads(HKV, G, world, rank)
+        eng = KvHeadEngine(EngineConfig(S, L, qs.stop - qs.start, kvs.stop - kvs.start, D, l, r, 0.01, W, B + E,
+                                        torch.bfloat16))
+        shards.append((kvs, qs, eng))
+    orc = StreamOracle(S * HKV, L, G, 1, D, cfg, window=W)  # one pseudo-stream per KV-head group
+    rng = np.random.default_rng(123)
+    for s in range(S):
+        for layer in range(L):
+            k = bf16_round(rng.standard_normal((HKV, B, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((HKV, B, D)).astype(F32))
+            pos = np.arange(B, dtype=np.int64)
+            for kvs, _, eng in shards:
+                for gl, g in enumerate(range(kvs.start, kvs.stop)):
+                    eng.inject_group(s, layer, gl, k[g:g + 1], v[g:g + 1], pos)
+            for g in range(HKV):
+                for t in range(B):
+                    orc.kv[s * HKV + g][layer].append(k[g:g + 1, t], v[g:g + 1, t], t)
+    orc.pos = [B] * (S * HKV)
+    worst = 0.0
+    for period in range(periods):
+        for t in range(E):
+            qs_, ks_, vs_ = zip(*[synth_step(rng, S, HQ, HKV, D, 0.005, 4.0, True) for _ in range(L)])
+            q, k, v = np.stack(qs_), np.stack(ks_), np.stack(vs_)
+            want = orc.step(q.reshape(L, S * HKV, G, D), k.reshape(L, S * HKV, 1, D), v.reshape(L, S * HKV, 1, D))
+            want = want.reshape(L, S, HQ, D)
+            for kvs, qsl, eng in shards:
+                dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)
+                got = eng.decode_step(dev(q[:, :, qsl]), dev(k[:, :, kvs]), dev(v[:, :, kvs]), record=True)
+                worst = max(worst, rel_err(got.cpu().numpy(), want[:, :, qsl]))
+        n = orc.length(0, 0)
+        for kvs, _, eng in shards:
+            hk = kvs.stop - kvs.start
+            kept = torch.full((S, hk, L, B), -1, dtype=torch.int32, device="cuda")
+            eng.evict(-1, kept)
+            kc = kept.cpu().numpy()
+            for s in range(S):
+                for gl, g in enumerate(range(kvs.start, kvs.stop)):
+                    ps = s * HKV + g
+                    for layer in range(L):
+                        d = orc.decide(ps, layer)
+                        ok, nbad, gap = kept_sets_match(orc.scores(ps, layer), d.kept, kc[s, gl, layer], n, cfg)
+                        assert ok, (period, s, g, layer, nbad, gap)
+                        orc.apply(ps, layer, kc[s, gl, layer].astype(np.int64))
+                        kg, _ = eng.inner.kv(s * hk + gl, layer)
+                        np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[ps][layer].keys())
+    print(f"kv_head world={world} worst output rel err {worst:.2e}")
+    assert worst <= 2e-3

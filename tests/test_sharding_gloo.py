@@ -168,3 +168,81 @@ def test_gather_results_concatenates_rank_blocks():
     want = np.concatenate([np.arange(0, 4).reshape(1, 4), np.arange(10, 18).reshape(2, 4)]).astype(np.int32)
     np.testing.assert_array_equal(ret[0], want)
     np.testing.assert_array_equal(ret[1], want)
+
+
+# ---- select="kv_head": per KV-head-group decisions, no collective -------------
+
+def _kvh_worker(rank, world, port, q_all, k_all, v_all, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2409_09086_b200.sharding import gather_results
+
+        G = HQ // HKV
+        kvs, qs = shard_heads(HKV, G, world, rank)
+        hk = kvs.stop - kvs.start
+        cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.05)
+        # this rank's groups as pseudo-streams (KvHeadEngine's layout: unit = s*hk + local group)
+        orc = StreamOracle(S * hk, L, G, 1, D, cfg, window=W)
+
+        def forbidden(*a, **k):
+            raise AssertionError("kv_head selection must not communicate on the hot path")
+
+        real = dist.all_reduce, dist.all_gather
+        dist.all_reduce = dist.all_gather = forbidden
+        decisions = []
+        try:
+            for t in range(T):
+                q = q_all[t][:, :, qs].reshape(L, S * hk, G, D)
+                k = k_all[t][:, :, kvs].reshape(L, S * hk, 1, D)
+                v = v_all[t][:, :, kvs].reshape(L, S * hk, 1, D)
+                orc.step(q, k, v)
+                if (t + 1) % E == 0:
+                    per = np.full((S * hk, L, l + r), -1, np.int64)
+                    for u in range(S * hk):
+                        for ly in range(L):
+                            ks = orc.decide(u, ly).kept
+                            per[u, ly, : ks.size] = ks
+                            orc.apply(u, ly, ks)
+                    decisions.append(per.reshape(S, hk, L, l + r))
+        finally:
+            dist.all_reduce, dist.all_gather = real
+        # results leave through the one collective outside the hot path
+        ret[rank] = [gather_results(torch.from_numpy(d), dim=1).numpy() for d in decisions]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kv_head_selection_sharded_without_collectives():
+    """World-size-2 gloo: each rank decides for its own KV-head groups only
+    (no collective until the result gather); the gathered decisions equal the
+    reference pipeline run per group on one process."""
+    rng = np.random.default_rng(78)
+    q_all = rng.standard_normal((T, L, S, HQ, D)).astype(F32)
+    k_all = rng.standard_normal((T, L, S, HKV, D)).astype(F32)
+    v_all = rng.standard_normal((T, L, S, HKV, D)).astype(F32)
+    k_all[rng.random((T, L, S)) < 0.05] *= F32(4)
+    mgr = tmp.Manager()
+    ret = mgr.dict()
+    port = 27500 + int(rng.integers(0, 2000))
+    tmp.spawn(_kvh_worker, args=(2, port, q_all, k_all, v_all, ret), nprocs=2, join=True)
+    d0, d1 = ret[0], ret[1]
+    assert len(d0) == len(d1) == T // E
+    G = HQ // HKV
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.05)
+    orc = StreamOracle(S * HKV, L, G, 1, D, cfg, window=W)
+    ei = 0
+    for t in range(T):
+        orc.step(q_all[t].reshape(L, S * HKV, G, D), k_all[t].reshape(L, S * HKV, 1, D),
+                 v_all[t].reshape(L, S * HKV, 1, D))
+        if (t + 1) % E == 0:
+            for s in range(S):
+                for g in range(HKV):
+                    for ly in range(L):
+                        u = s * HKV + g
+                        want = orc.decide(u, ly).kept
+                        np.testing.assert_array_equal(d0[ei][s, g, ly, : want.size], want)
+                        np.testing.assert_array_equal(d1[ei][s, g, ly, : want.size], want)
+                        orc.apply(u, ly, want)
+            ei += 1
