@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kCmpThreads) compact_kernel(const CompactArgs 
   const int h = blockIdx.x, b = blockIdx.y;
   if (a.moves) {
     // ---- slot-map compaction: planned moves only
-    const int32_t* trip = a.moves + b * a.mv_bs;
+    const int32_t* trip = a.moves + b * a.mv_bs + a.row_stride;  // after the [capacity] planning scratch
     const int count = a.mcount[b * a.mc_bs];
     if (h < a.heads) {
       const int units = a.row_bytes / 16;

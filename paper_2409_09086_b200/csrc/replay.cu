@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(kRepThreads)
     if (srow) srow[j] = v;
   }
   if (threadIdx.x == 0 && to_ring) ring_len[(ring_head + i) % window] = nl;
+  // the batch's last row materialises the stream ids appended since the last
+  // decision (live[j] for j >= nl_dec is only read by later launches)
+  if (i == R - 1)
+    for (int j = nl_dec + threadIdx.x; j < nl; j += blockDim.x) const_cast<int64_t*>(live)[j] = (int64_t)n_dec + (j - nl_dec);
 }
 
 // heavy_hitter_accumulate over the batch rows in order: thread j owns column j.
