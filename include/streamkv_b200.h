@@ -158,6 +158,16 @@ int skv_length(const skv_ctx* ctx, int stream, int layer);
  * the kept count (the survivors of the tokens appended since the previous
  * eviction) instead of shifting every row after the first evicted one. */
 int skv_kv_view(skv_ctx* ctx, int stream, int layer, void** k_dev, void** v_dev);
+/* Device view of the window ring of (stream, layer): rows [W][stride] f32
+ * (values at PHYSICAL rows, see skv_slot_map), lengths [W], the ring head
+ * (next slot) and row count (oldest = (head - count) mod W).  Returns the row
+ * stride.  A pending recorded row is materialised first (stream-ordered on
+ * the legacy stream). */
+int skv_window_view(skv_ctx* ctx, int stream, int layer, float** rows_dev, int32_t** lens_dev, int* ring_head,
+                    int* count);
+/* Device pointer to the original positions [capacity] int64 of (stream, layer)
+ * (logical order; first skv_length() valid). */
+int skv_positions_view(skv_ctx* ctx, int stream, int layer, int64_t** pos_dev);
 /* Device pointer to the slot map of (stream, layer): int32 [capacity],
  * perm[c] = physical row of logical slot c for c < skv_length(); null for
  * densely compacted engines (identity). */
@@ -317,6 +327,17 @@ int skv_replay_rows(const skv_replay_state* st, const float* trace_rows, const i
  * and ring rows.  kept_out [r+l] int64 receives the kept indices (into live);
  * scores [>= max(n, stream_n)] f32 and top [relevant_budget] i32 are scratch.
  * Returns the kept count. */
+/* A round's quality metrics on the device (metrics.py:46-73; the Session's
+ * oracle metrics engine.py:314-331 and replay.py:150-166): kept stream ids
+ * live[kept[i]] (i < km; the first rc are the relevant set), nrows scoring
+ * rows rows_base + row_off[k] of row_n[k] floats in stream coordinates
+ * (oldest first), stream length stream_n.  mass_out[k] = f64 mass of row k
+ * on the kept ids; counts_out[0] = |relevant ids & oracle top-r| (-1 when
+ * undefined), counts_out[1] = planted ids (truth[ntruth]) among the kept. */
+int skv_round_metrics(const int64_t* kept, int km, int rc, const int64_t* live, const float* rows_base,
+                      const int64_t* row_off, const int32_t* row_n, int nrows, int stream_n, int recent_len,
+                      int relevant_budget, const int64_t* truth, int ntruth, float* scores, int32_t* top,
+                      double* mass_out, int32_t* counts_out, void* stream);
 int skv_replay_evict(const skv_replay_state* st, int policy, int n, int ring_head, int ring_count, int recent_len,
                      int relevant_budget, int sink_count, float bias, int rc, int64_t* kept_out, float* scores,
                      int32_t* top, const float* trace_rows, const int64_t* raw_off, const int32_t* raw_n, int nraw,

@@ -439,6 +439,33 @@ class StreamOracle:
         self.kv = [[LayerKV(heads_kv, head_dim) for _ in range(layers)] for _ in range(streams)]
         self.win = [[RowWindow(self.W) for _ in range(layers)] for _ in range(streams)]
         self.pos = [0] * streams
+        self.shadow = False
+
+    def enable_shadow(self) -> None:
+        """Session(oracle=True) (engine.py:142-151): a never-evicted shadow
+        cache plus the last recent_len head-aggregated rows over it."""
+        self.shadow = True
+        S, L = self.S, self.L
+        self.skv = [[LayerKV(self.Hkv, self.D) for _ in range(L)] for _ in range(S)]
+        self.srows = [[RowWindow(self.cfg.recent_len) for _ in range(L)] for _ in range(S)]
+
+    def shadow_metrics(self, s: int, layer: int, decision: "Decision"):
+        """_evict_layer's oracle metrics (engine.py:314-331), before compaction:
+        (retained mass, top-r overlap or None)."""
+        orig = self.kv[s][layer].pos[: self.kv[s][layer].n]
+        kept_ids, relevant_ids = orig[decision.kept], orig[decision.relevant]
+        rows = self.srows[s][layer].rows
+        mass = retained_mass_rows(rows, kept_ids)
+        ns, l = self.skv[s][layer].n, self.cfg.recent_len
+        overlap = None
+        if ns > l and self.cfg.relevant_budget >= 1:
+            cols = ns - l
+            acc = np.zeros(cols, dtype=F32)
+            for row in rows:
+                m = min(row.size, cols)
+                acc[:m] += row[:m]
+            overlap = topk_overlap_ids(acc / F32(len(rows)), relevant_ids, self.cfg.relevant_budget)
+        return mass, overlap
 
     def length(self, s: int, layer: int) -> int:
         return self.kv[s][layer].n
@@ -477,6 +504,14 @@ class StreamOracle:
             self.acc[s][layer] = mass_accumulate(self.acc[s][layer], row)
             out[s] = o
             rows.append(row)
+            if self.shadow:  # engine.py:275-284 (no RoPE in the shadow restatement)
+                ss = self.skv[s][layer]
+                ss.append(np.asarray(k[s], F32), np.asarray(v[s], F32), self.pos[s])
+                sk, sv = ss.keys(), ss.values()
+                if self.group > 1:
+                    sk, sv = np.repeat(sk, self.group, axis=0), np.repeat(sv, self.group, axis=0)
+                sprobs, _ = attend_heads(sk, sv, np.asarray(q[s], F32), self.scale)
+                self.srows[s][layer].push(head_mean(sprobs, self.cfg.head_agg))
         return out, rows
 
     def advance(self, streams: Optional[Sequence[int]] = None) -> None:
@@ -532,6 +567,29 @@ class StreamOracle:
                 per.append(d.kept)
             kept.append(per)
         return kept
+
+
+# --------------------------------------------------------------------------
+# quality metrics (metrics.py:46-73)
+# --------------------------------------------------------------------------
+
+
+def retained_mass_rows(rows, kept_ids) -> float:
+    """retained_mass (metrics.py:46-62): mean over rows of the f64 mass on kept ids."""
+    if not rows:
+        raise ValueError("retained_mass needs at least one scoring row")
+    idx = np.asarray(kept_ids, dtype=I64)
+    total = 0.0
+    for row in rows:
+        sel = idx[idx < row.size]
+        total += float(row[sel].sum(dtype=np.float64)) if sel.size else 0.0
+    return total / len(rows)
+
+
+def topk_overlap_ids(oracle_scores, relevant_ids, r: int) -> float:
+    """topk_overlap (metrics.py:65-73): |relevant & oracle top-r| / r."""
+    top = set(int(i) for i in top_k_newer(np.asarray(oracle_scores, dtype=F32), r))
+    return len(top & set(int(i) for i in np.asarray(relevant_ids, dtype=I64))) / r
 
 
 # --------------------------------------------------------------------------

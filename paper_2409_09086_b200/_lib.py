@@ -12,7 +12,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstreamkv_b200.so")
+# SKV_LIB points the binding at another build of the same ABI (A/B timing of
+# kernel variants with tools/; the product path uses the in-tree library)
+LIB_PATH = os.environ.get("SKV_LIB") or os.path.join(_HERE, "libstreamkv_b200.so")
 
 SKV_OK = 0
 SKV_EINVAL = -1
@@ -103,6 +105,10 @@ SIGNATURES = {
     "skv_attn_probs": (_I, [_P, _P, _I, _I, _F, _P, _P]),
     "skv_weighted_sum": (_I, [_P, _P, _I, _I, _P, _P]),
     "skv_rope_apply": (_I, [_P, _I, _I64, ctypes.c_double, _P, _P]),
+    "skv_window_view": (_I, [_P, _I, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I),
+                             ctypes.POINTER(_I)]),
+    "skv_positions_view": (_I, [_P, _I, _I, ctypes.POINTER(_P)]),
+    "skv_round_metrics": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P]),
     "skv_replay_rows": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "skv_replay_evict": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _I, _P, _P,
                               _P]),

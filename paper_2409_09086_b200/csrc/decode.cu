@@ -301,6 +301,9 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       const float* wl = wm + NW * G;
       const float* wo = wl + NW * G;
       const int sigma = u / a.nc, j = u - sigma * a.nc;
+      // the segment's last chunk appends the new row first: its stores are in
+      // flight while the partials merge, and precede the chunk's publication
+      if (!a.stat && a.append && j == a.nc - 1) append_row<T, D>(a, sigma, n, lane, 32);
       // merge the consumer warps' partials of this chunk (static schedule:
       // the consumers already did)
       float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
@@ -330,12 +333,9 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
           part[h * PW + D + 1] = L;
         }
       }
-      // append (dynamic schedule; the static one appends in the consumers):
-      // the new row and its metadata are stored before the chunk is published
       __syncwarp();
       if (lane == 0) mbar_arrive(&epi_empty[sl]);  // slot consumed
       if (!a.stat) {
-        if (a.append && j == a.nc - 1) append_row<T, D>(a, sigma, n, lane, 32);
         __syncwarp();
         // publish the chunk partial: the segment's merge CTA starts once all
         // nc chunks of the segment are counted
@@ -563,6 +563,8 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       // epilogue warp (same arithmetic order), then publish the chunk.
       consumers_sync<kCT>();
       const int j = u - sigma * a.nc;
+      // the segment's last chunk stores the appended row (before publishing)
+      if (a.append && j == a.nc - 1) append_row<T, D>(a, sigma, n, tid, kCT);
       float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
       for (int idx = tid; idx < G * D; idx += kCT) {
         const int h = idx / D, d = idx - h * D;
@@ -588,8 +590,6 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
           part[h * PW + D + 1] = x[0];
         }
       }
-      // the segment's last chunk stores the appended row before publishing
-      if (a.append && j == a.nc - 1) append_row<T, D>(a, sigma, n, tid, kCT);
       consumers_sync<kCT>();
       if (tid == 0) red_release_add(&a.counters[sigma], 1);
     }

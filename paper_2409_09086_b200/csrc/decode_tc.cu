@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
   consumers_sync();
   if (a.ctat && tid == 0) a.ctat[8 * c + 3] = gtimer();
   // ---- merge the warp partials in warp order and publish the chunk partial
+  // KvCache.append: the segment's last chunk stores the new row and its
+  // metadata before publishing (the merge, and so the next launch, sees them)
+  if (a.append && j == a.nc - 1) append_row<__nv_bfloat16, D>(a, sigma, n, tid, CT);
   float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
   for (int idx = tid; idx < G * D; idx += CT) {
     const int h = idx / D, d = idx - h * D;
@@ -337,9 +340,6 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       part[h * PW + D + 1] = xs[0];
     }
   }
-  // KvCache.append: the segment's last chunk stores the new row and its
-  // metadata before publishing (the merge, and so the next launch, sees them)
-  if (a.append && j == a.nc - 1) append_row<__nv_bfloat16, D>(a, sigma, n, tid, CT);
   consumers_sync();
   if (tid == 0) {
     red_release_add(&a.counters[sigma], 1);

@@ -197,6 +197,27 @@ int skv_replay_rows(const skv_replay_state* st, const float* trace_rows, const i
   return SKV_OK;
 }
 
+int skv_round_metrics(const int64_t* kept, int km, int rc, const int64_t* live, const float* rows_base,
+                      const int64_t* row_off, const int32_t* row_n, int nrows, int stream_n, int recent_len,
+                      int relevant_budget, const int64_t* truth, int ntruth, float* scores, int32_t* top,
+                      double* mass_out, int32_t* counts_out, void* stream) {
+  if (!kept || !live || !rows_base || !row_off || !row_n || !scores || !top || !mass_out || !counts_out)
+    return set_error(SKV_EINVAL, "null argument");
+  if (nrows < 1) return set_error(SKV_EINVAL, "retained_mass needs at least one scoring row");
+  const int words = (std::max(stream_n, 1) + 31) / 32;
+  const size_t smem = 2 * (size_t)words * sizeof(unsigned);
+  if (smem > 160 * 1024) return set_error(SKV_EINVAL, "stream too long for the metrics kernel");
+  static DevOnce attr;
+  if (!attr.here()) {
+    cudaFuncSetAttribute(replay_metrics_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr.here() = true;
+  }
+  replay_metrics_kernel<<<1, kMetThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      kept, km, rc, live, rows_base, row_off, row_n, nrows, stream_n, recent_len, relevant_budget, truth, ntruth,
+      scores, top, mass_out, counts_out);
+  return cudaGetLastError() == cudaSuccess ? SKV_OK : set_error(SKV_ECUDA, "metrics kernel launch");
+}
+
 int skv_replay_evict(const skv_replay_state* st, int policy, int n, int ring_head, int ring_count, int recent_len,
                      int relevant_budget, int sink_count, float bias, int rc, int64_t* kept_out, float* scores,
                      int32_t* top, const float* trace_rows, const int64_t* raw_off, const int32_t* raw_n, int nraw,

@@ -1282,6 +1282,31 @@ int skv_state_dump(skv_ctx* x, int stream, int layer, int* n_out, int* m_out, vo
   return check_sticky(x);
 }
 
+int skv_window_view(skv_ctx* x, int stream, int layer, float** rows_dev, int32_t** lens_dev, int* ring_head,
+                    int* count) {
+  if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
+  int n, m, head;
+  int rc = stream_state(x, stream, layer, &n, &m, &head);
+  if (rc) return rc;
+  if (!x->ragged[layer]) {
+    rc = flush_pending(x, layer, nullptr);  // the newest recorded row is materialised (stream-ordered)
+    if (rc) return rc;
+  }
+  const int64_t sl = (int64_t)stream * x->L + layer;
+  if (rows_dev) *rows_dev = x->rows + sl * x->W * x->cap;
+  if (lens_dev) *lens_dev = x->wlen + sl * x->W;
+  if (ring_head) *ring_head = head;
+  if (count) *count = m;
+  return x->cap;  // row stride (floats)
+}
+
+int skv_positions_view(skv_ctx* x, int stream, int layer, int64_t** pos_dev) {
+  if (!x || !pos_dev || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
+    return fail(SKV_EINVAL, "out of range");
+  *pos_dev = x->pos + ((int64_t)stream * x->L + layer) * x->cap;
+  return SKV_OK;
+}
+
 int skv_slot_map(skv_ctx* x, int stream, int layer, int32_t** perm_dev) {
   if (!x || !perm_dev || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
     return fail(SKV_EINVAL, "out of range");

@@ -37,7 +37,9 @@ __device__ __forceinline__ void append_row(const AttnArgs& a, int sigma, int n, 
     *np = pv + 1;
     a.len[s * a.len_ss] = n;
   }
-  __threadfence();  // visible GPU-wide before the caller's barrier + release of the chunk count
+  // no fence here: the caller's barrier (__syncwarp / bar.sync) followed by the
+  // gpu-scope release add of the chunk count is cumulative over these stores,
+  // exactly as it is for the chunk partial itself
 }
 
 }  // namespace skv

@@ -63,6 +63,12 @@ CASES = {
     "max_f32": dict(S=1, L=1, Hq=8, Hkv=8, D=64, T=256, l=32, r=32, W=32, b=0.01, E=32,
                     dtype="f32", seed=1012, saddles=3, saddle_gain=6.0, spike_prob=0.0,
                     spike_gain=1.0, out_every=32, head_agg="max"),
+    # Session(oracle=True)'s live quality metrics against a never-evicted
+    # shadow cache (engine.py:275-284, 314-331): retained mass and top-r
+    # overlap at every eviction.
+    "shadow_mini": dict(S=2, L=2, Hq=8, Hkv=2, D=64, T=384, l=32, r=32, W=16, b=0.01, E=64,
+                        dtype="f32", seed=1013, saddles=4, saddle_gain=6.0, spike_prob=0.0,
+                        spike_gain=1.0, out_every=64, shadow=True),
 }
 
 

@@ -29,7 +29,10 @@ sys.path.insert(0, REPO)
 import types  # noqa: E402
 
 from streamkv.cache import KvCache, PositionMode, TokenMeta  # noqa: E402  (reference)
+from collections import deque  # noqa: E402
+
 from streamkv.engine import Session  # noqa: E402
+from streamkv.metrics import retained_mass, topk_overlap  # noqa: E402
 from streamkv.policies import (  # noqa: E402
     AttentionWindow,
     PolicyConfig,
@@ -77,6 +80,13 @@ def run_reference_case(name: str) -> dict:
         rot._trig = types.MethodType(Session._trig, rot)
         mode = PositionMode.CACHE_RELATIVE if rope == "cache_relative" else PositionMode.ORIGINAL
         rstore = [[np.zeros((Hkv, 0, D), dtype=F32) for _ in range(L)] for _ in range(S)]
+    # Session(oracle=True)'s shadow: a never-evicted cache and the last
+    # recent_len head-aggregated rows over it (engine.py:142-151, 275-284)
+    shadow = c.get("shadow", False)
+    if shadow:
+        scaches = [KvCache(L, Hkv, D) for _ in range(S)]
+        srows = [[deque(maxlen=c["l"]) for _ in range(L)] for _ in range(S)]
+    shadow_mass, shadow_overlap = [], []
     q_all, k_all, v_all = case_inputs(name)  # (T, L, S, H, D)
     T = q_all.shape[0]
     out_steps = []
@@ -105,6 +115,13 @@ def run_reference_case(name: str) -> dict:
                 windows[s][layer].push(row)
                 accs[s][layer] = heavy_hitter_accumulate(accs[s][layer], row)
                 step_out[layer, s] = o
+                if shadow:
+                    scaches[s].append(layer, k_all[t, layer, s], v_all[t, layer, s], TokenMeta(t))
+                    sk, sv = scaches[s].keys(layer), scaches[s].values(layer)
+                    if G > 1:
+                        sk, sv = np.repeat(sk, G, axis=0), np.repeat(sv, G, axis=0)
+                    sprobs, _ = Session._attend(holder, sk, sv, q_all[t, layer, s])
+                    srows[s][layer].append(aggregate_heads(sprobs, cfg.head_agg))
         if t % c["out_every"] == 0 or t == T - 1:
             out_steps.append(t)
             outs.append(step_out)
@@ -131,6 +148,21 @@ def run_reference_case(name: str) -> dict:
                         d = inf_mllm_decide(windows[s][layer], n, cfg)
                     kept_log.append(d.kept.astype(np.int32))
                     score_log.append(sc.astype(F32))
+                    if shadow:  # _evict_layer's oracle metrics, engine.py:314-331
+                        orig = caches[s].original_positions(layer)
+                        kept_ids, relevant_ids = orig[d.kept], orig[d.relevant]
+                        rows = list(srows[s][layer])
+                        shadow_mass.append(retained_mass(rows, kept_ids))
+                        ov = np.nan
+                        ns = scaches[s].length(layer)
+                        if ns > cfg.recent_len and cfg.relevant_budget >= 1:
+                            cols = ns - cfg.recent_len
+                            acc = np.zeros(cols, dtype=F32)
+                            for row in rows:
+                                m = min(row.size, cols)
+                                acc[:m] += row[:m]
+                            ov = topk_overlap(acc / F32(len(rows)), relevant_ids, cfg.relevant_budget)
+                        shadow_overlap.append(ov)
                     if d.kept.size != n:
                         caches[s].gather_keep(layer, d.kept)
                         windows[s][layer].remap(d.kept)
@@ -150,6 +182,8 @@ def run_reference_case(name: str) -> dict:
         scores=np.concatenate(score_log) if score_log else np.zeros(0, F32),
         final_keys_sha=np.frombuffer(hashlib.sha256(final_keys.tobytes()).digest(), np.uint8),
         final_pos=final_pos,
+        shadow_mass=np.asarray(shadow_mass, np.float64),
+        shadow_overlap=np.asarray(shadow_overlap, np.float64),
     )
 
 

@@ -26,6 +26,9 @@ def run_oracle_case(name: str, kept_override=None) -> dict:
                        head_agg=c.get("head_agg", "mean"))
     orc = StreamOracle(c["S"], c["L"], c["Hq"], c["Hkv"], c["D"], cfg, window=c["W"], policy=policy,
                        rope=c.get("rope"), rope_base=c.get("rope_base", 10000.0))
+    if c.get("shadow"):
+        orc.enable_shadow()
+    shadow_mass, shadow_overlap = [], []
     q_all, k_all, v_all = case_inputs(name)
     T = q_all.shape[0]
     out_steps, outs = [], []
@@ -50,7 +53,12 @@ def run_oracle_case(name: str, kept_override=None) -> dict:
                         sc = orc.acc[s][layer][: n - cfg.recent_len].copy()
                     else:
                         sc = orc.scores(s, layer)
-                    kept = orc.decide(s, layer).kept
+                    dec = orc.decide(s, layer)
+                    kept = dec.kept
+                    if orc.shadow:
+                        mass, ov = orc.shadow_metrics(s, layer, dec)
+                        shadow_mass.append(mass)
+                        shadow_overlap.append(np.nan if ov is None else ov)
                     if kept_override is not None:
                         kept = kept_override(t, s, layer, kept, sc, n)
                     kept_log.append(np.asarray(kept).astype(np.int32))
@@ -70,5 +78,7 @@ def run_oracle_case(name: str, kept_override=None) -> dict:
         scores=np.concatenate(score_log) if score_log else np.zeros(0, F32),
         final_keys_sha=np.frombuffer(hashlib.sha256(final_keys.tobytes()).digest(), np.uint8),
         final_pos=final_pos,
+        shadow_mass=np.asarray(shadow_mass, np.float64),
+        shadow_overlap=np.asarray(shadow_overlap, np.float64),
         oracle=orc,
     )

@@ -52,6 +52,10 @@ def test_oracle_matches_reference_run(name):
     np.testing.assert_allclose(got["outs"], ref["outs"], rtol=0, atol=1e-6)
     np.testing.assert_array_equal(got["final_pos"], ref["final_pos"])
     np.testing.assert_array_equal(got["final_keys_sha"], ref["final_keys_sha"])
+    if "shadow_mass" in ref and ref["shadow_mass"].size:  # Session(oracle=True) metrics
+        np.testing.assert_allclose(got["shadow_mass"], ref["shadow_mass"], rtol=1e-12)
+        np.testing.assert_array_equal(np.isnan(got["shadow_overlap"]), np.isnan(ref["shadow_overlap"]))
+        np.testing.assert_array_equal(np.nan_to_num(got["shadow_overlap"]), np.nan_to_num(ref["shadow_overlap"]))
 
 
 def test_algorithm1_kats_match_reference():
