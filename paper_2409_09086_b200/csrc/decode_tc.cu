@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       __syncwarp();
       if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s2 * f.w_ss] = f.n;
     }
+    if (a.ctat && lane == 0) a.ctat[8 * c + 6] = gtimer();  // instrumentation: fold warp done
     return;
   }
 

@@ -57,8 +57,9 @@ print(f"record steps (last {W}): {rec[-W:].mean():.2f} us; non-record: {rec[:-W]
 eng.lib.skv_timing(eng._h, 3)
 eng.evict(-1); torch.cuda.synchronize()
 with torch.cuda.stream(st):
-    eng.decode_step(q[0], k[0], v[0], out, record=False)
-    eng.decode_step(q[1], k[1], v[1], out, record=False)
+    rec = bool(int(os.environ.get("REC", "0")))
+    eng.decode_step(q[0], k[0], v[0], out, record=rec)
+    eng.decode_step(q[1], k[1], v[1], out, record=rec)
 st.synchronize()
 import ctypes
 P = None
