@@ -93,6 +93,11 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ float rescale(float m, float M) { return m == -INFINITY ? 0.f : exp2f((m - M) * kLog2e); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <int G>
 struct Smem {
@@ -102,6 +107,97 @@ struct Smem {
 };
 
 }  // namespace tcd
+
+namespace tcd {
+
+// One consumer warp's 32 keys [wk0, wk0 + 32) of the chunk in shared memory:
+// S = Q K^T for 4 n-tiles of 8 keys (mma.m16n8k16, B fragments by ldmatrix
+// from the swizzled tile), then the softmax over the warp's keys (row gid =
+// query head): p = exp2((x - m) log2e), row max m and sum l.  Recorded steps
+// store the raw logits x = s * scale to lgrow (null: not recorded).
+__device__ __forceinline__ void warp_scores(const uint32_t (&qa)[8][2], uint32_t kbase, int wk0, int lane, int k0,
+                                            int kend, float scale, float* lgrow, float (&p)[4][2], float& m,
+                                            float& l) {
+  const int tig = lane & 3;
+  float sacc[4][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+    const int kk = wk0 + nt * 8 + (lane & 7);  // key row this lane addresses
+    const int t = kk >> 6, r = kk & 63;
+#pragma unroll
+    for (int ks2 = 0; ks2 < 4; ++ks2) {  // two k-steps (32 dims) per ldmatrix.x4
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(kbase + t * TILE + swz(r, 4 * ks2 + (lane >> 3)), b0, b1, b2, b3);
+      mma16816(sacc[nt], qa[2 * ks2][0], qa[2 * ks2][1], b0, b1);
+      mma16816(sacc[nt], qa[2 * ks2 + 1][0], qa[2 * ks2 + 1][1], b2, b3);
+    }
+  }
+  // ---- softmax over the warp's 32 keys (row gid): logits x = s * scale
+  float x[4][2];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
+      x[nt][e] = key < kend ? sacc[nt][e] * scale : -INFINITY;
+      mx = fmaxf(mx, x[nt][e]);
+    }
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  m = mx;
+  float ls = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      p[nt][e] = m == -INFINITY ? 0.f : fast_exp2((x[nt][e] - m) * kLog2e);
+      ls += p[nt][e];
+    }
+  ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+  ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+  l = ls;
+  if (lgrow) {  // recorded steps: raw f32 logits for the window fold
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
+        if (key < kend) lgrow[key] = x[nt][e];
+      }
+  }
+}
+
+// O += P V over the warp's 32 keys: k-steps of 16 keys, P from the S
+// accumulators as two bf16 terms (hi + lo), V fragments by ldmatrix.trans.
+__device__ __forceinline__ void warp_pv(const float (&p)[4][2], uint32_t vbase, int wk0, int lane,
+                                        float (&o)[16][4]) {
+#pragma unroll
+  for (int kq = 0; kq < 2; ++kq) {
+    const uint32_t ah0 = pack_bf16(p[2 * kq][0], p[2 * kq][1]);
+    const uint32_t ah2 = pack_bf16(p[2 * kq + 1][0], p[2 * kq + 1][1]);
+    const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
+    const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
+    const uint32_t al0 = pack_bf16(p[2 * kq][0] - h0.x, p[2 * kq][1] - h0.y);
+    const uint32_t al2 = pack_bf16(p[2 * kq + 1][0] - h2.x, p[2 * kq + 1][1] - h2.y);
+    // lane's ldmatrix.trans row: key 16kq + 8*(matrix & 1) + (lane & 7), dim chunk nb/8 + (matrix >> 1)
+    const int kk = wk0 + 16 * kq + 8 * ((lane >> 3) & 1) + (lane & 7);
+    const int t = kk >> 6, r = kk & 63;
+#pragma unroll
+    for (int np = 0; np < 8; ++np) {  // pairs of n-tiles (16 dims)
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(vbase + t * TILE + swz(r, 2 * np + (lane >> 4)), b0, b1, b2, b3);
+      mma16816(o[2 * np], ah0, ah2, b0, b1);
+      mma16816(o[2 * np], al0, al2, b0, b1);
+      mma16816(o[2 * np + 1], ah0, ah2, b2, b3);
+      mma16816(o[2 * np + 1], al0, al2, b2, b3);
+    }
+  }
+}
+
+}  // namespace tcd
+
 
 // One CTA = chunk blockIdx.x (static schedule): segment sigma = c / nc,
 // tiles [j*ch, min((j+1)*ch, nt)).
@@ -224,78 +320,9 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float* lgrow = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs : nullptr;
   if (wk0 < ntile * TT) {
-    // ---- S = Q K^T for 4 n-tiles of 8 keys
-    float sacc[4][4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-      const int kk = wk0 + nt * 8 + (lane & 7);  // key row this lane addresses
-      const int t = kk >> 6, r = kk & 63;
-#pragma unroll
-      for (int ks2 = 0; ks2 < 4; ++ks2) {  // two k-steps (32 dims) per ldmatrix.x4
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kbase + t * TILE + swz(r, 4 * ks2 + (lane >> 3)), b0, b1, b2, b3);
-        mma16816(sacc[nt], qa[2 * ks2][0], qa[2 * ks2][1], b0, b1);
-        mma16816(sacc[nt], qa[2 * ks2 + 1][0], qa[2 * ks2 + 1][1], b2, b3);
-      }
-    }
-    // ---- softmax over the warp's 32 keys (row gid): logits x = s * scale
-    float x[4][2];
-    float mx = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
-        x[nt][e] = key < kend ? sacc[nt][e] * a.scale : -INFINITY;
-        mx = fmaxf(mx, x[nt][e]);
-      }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    m = mx;
     float p[4][2];
-    float ls = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        p[nt][e] = m == -INFINITY ? 0.f : fast_exp2((x[nt][e] - m) * kLog2e);
-        ls += p[nt][e];
-      }
-    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-    l = ls;
-    if (lgrow && real) {  // recorded steps: raw f32 logits for the window fold
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
-          if (key < kend) lgrow[key] = x[nt][e];
-        }
-    }
-    // ---- O = P V: k-steps of 16 keys, P from the S accumulators (hi + lo)
-#pragma unroll
-    for (int kq = 0; kq < 2; ++kq) {
-      const uint32_t ah0 = pack_bf16(p[2 * kq][0], p[2 * kq][1]);
-      const uint32_t ah2 = pack_bf16(p[2 * kq + 1][0], p[2 * kq + 1][1]);
-      const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
-      const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
-      const uint32_t al0 = pack_bf16(p[2 * kq][0] - h0.x, p[2 * kq][1] - h0.y);
-      const uint32_t al2 = pack_bf16(p[2 * kq + 1][0] - h2.x, p[2 * kq + 1][1] - h2.y);
-      // lane's ldmatrix.trans row: key 16kq + 8*(matrix & 1) + (lane & 7), dim chunk nb/8 + (matrix >> 1)
-      const int kk = wk0 + 16 * kq + 8 * ((lane >> 3) & 1) + (lane & 7);
-      const int t = kk >> 6, r = kk & 63;
-#pragma unroll
-      for (int np = 0; np < 8; ++np) {  // pairs of n-tiles (16 dims)
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vbase + t * TILE + swz(r, 2 * np + (lane >> 4)), b0, b1, b2, b3);
-        mma16816(o[2 * np], ah0, ah2, b0, b1);
-        mma16816(o[2 * np], al0, al2, b0, b1);
-        mma16816(o[2 * np + 1], ah0, ah2, b2, b3);
-        mma16816(o[2 * np + 1], al0, al2, b2, b3);
-      }
-    }
+    warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, real ? lgrow : nullptr, p, m, l);
+    warp_pv(p, vbase, wk0, lane, o);
   }
   // ---- warp partials to the slot: wm[NW][G], wl[NW][G], wo[NW][G][D]
   float* wm = slot + 4;
@@ -346,6 +373,296 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
     red_release_add(&a.counters[sigma], 1);
     if (a.tstamp) atomicMax(&a.tstamp[1], gtimer());
     if (a.ctat) a.ctat[8 * c + 2] = gtimer();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// All layers of one token in one persistent launch (static schedule: CTA c
+// owns chunk j of segment sigma in every layer).  Per layer l the producer
+// streams the chunk's K tiles as soon as the consumers are done with layer
+// l-1's K (and V likewise), so layer l's cache is in shared memory before its
+// queries are released; the consumers wait for layer l-1's outputs
+// (layer_done[l-1], the model's dependency; griddepcontrol.wait for layer 0),
+// compute the chunk exactly like decode_tc_kernel and publish its partial;
+// the CTA whose publication completes the segment merges it (merge_kernel's
+// arithmetic and order) and releases layer_done[l].  No launch or grid
+// completion sits on the layer-to-layer chain.  All CTAs must be co-resident
+// (grid <= SMs at one CTA per SM); dependents launch only after every CTA has
+// started (griddepcontrol.launch_dependents after layer 0's release).
+template <int G>
+__global__ void __launch_bounds__(tcd::THREADS, 1)
+    decode_tc_layers_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                            const AttnArgs a, const LayerSteps ls) {
+  using namespace tcd;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* ktiles = smem;
+  unsigned char* vtiles = smem + MAXT * TILE;
+  float* slot = reinterpret_cast<float*>(smem + Smem<G>::tiles);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slot + Smem<G>::slot_floats);
+  uint64_t* kfull = bars;      // layer l's K tiles landed (phase l & 1)
+  uint64_t* vfull = bars + 1;
+  uint64_t* kfree = bars + 2;  // consumers done with layer l's K
+  uint64_t* vfree = bars + 3;
+  float* fstats = reinterpret_cast<float*>(bars + 4);  // fold warp: [Hq][2]
+  int* merger = reinterpret_cast<int*>(slot);          // slot[0]: this CTA merges the segment
+
+  const int c = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n_old + a.append;
+  const int sigma = c / a.nc, j = c - sigma * a.nc;
+  const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+  const int segs = a.S * a.Hkv;
+  const int tt0 = j * a.ch, tt1 = min(tt0 + a.ch, a.nt);
+  const int ntile = tt1 - tt0;
+  const int k0 = tt0 * TT;
+  const int kend = min(tt1 * TT, n);
+  const bool has_new = a.append && a.n_old >= k0 && a.n_old < kend;
+  // the previous token's row (appended by the preceding launch) lies in this chunk
+  const bool has_prev = a.n_old - 1 >= k0 && a.n_old - 1 < kend;
+
+  if (tid == 0) {
+    mbar_init(kfull, 1);
+    mbar_init(vfull, 1);
+    mbar_init(kfree, NW);
+    mbar_init(vfree, NW);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      if (!ls.prefetch0 || has_prev) griddep_wait();  // rows the preceding launch wrote
+      for (int l = 0; l < ls.L; ++l) {
+        const int seg_row = (int)(((int64_t)s * a.L + a.layer + l) * a.Hkv + g) * a.cap;
+        if (l > 0) mbar_wait(kfree, (l - 1) & 1);
+        mbar_arrive_expect_tx(kfull, (uint32_t)ntile * TILE);
+        for (int t = 0; t < ntile; ++t) {
+          const int y = seg_row + (tt0 + t) * TT;
+          tma_load_2d(ktiles + t * TILE, &kmap, 0, y, kfull);
+          tma_load_2d(ktiles + t * TILE + REGION, &kmap, 64, y, kfull);
+        }
+        if (l > 0) mbar_wait(vfree, (l - 1) & 1);
+        mbar_arrive_expect_tx(vfull, (uint32_t)ntile * TILE);
+        for (int t = 0; t < ntile; ++t) {
+          const int y = seg_row + (tt0 + t) * TT;
+          tma_load_2d(vtiles + t * TILE, &vmap, 0, y, vfull);
+          tma_load_2d(vtiles + t * TILE + REGION, &vmap, 64, y, vfull);
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp == NW + 2) {
+    // ------------------------------------------------- window-row fold warp
+    // the previous token's recorded rows of every layer (written by the
+    // preceding launch) materialise into their ring slots
+    if (a.fold.n <= 0) return;
+    griddep_wait();
+    const int P = gridDim.x;
+    const int ppc = (a.fold.n + 63) / 64;
+    for (int l = 0; l < ls.L; ++l) {
+      FoldArgs f = a.fold;
+      f.logits += l * ls.lg_ls;
+      f.stats += l * ls.st_ls;
+      f.rows += l * ls.fr_ls;
+      if (f.wlen) f.wlen += l * ls.fw_ls;
+      for (int piece = c; piece < a.S * ppc; piece += P) {
+        const int s2 = piece / ppc, col0 = (piece - s2 * ppc) * 64;
+        const float* stt = f.stats + s2 * f.st_ss;
+        for (int h = lane; h < a.Hq; h += 32) {
+          fstats[2 * h] = __ldg(stt + 2 * h);
+          fstats[2 * h + 1] = __frcp_rn(__ldg(stt + 2 * h + 1));  // staged as 1/L
+        }
+        __syncwarp();
+        fold_columns(f, s2, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+        __syncwarp();
+        if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s2 * f.w_ss] = f.n;
+      }
+    }
+    return;
+  }
+
+  if (warp == NW + 1) return;
+
+  // ------------------------------------------------------------ consumers
+  const int gid = lane >> 2, tig = lane & 3;
+  const bool real = gid < G;  // rows >= G of the 16-row MMA are padding
+  const uint32_t kbase = smem_u32(ktiles), vbase = smem_u32(vtiles);
+  const int wk0 = warp * 32;
+  float* wm = slot + 4;
+  float* wl = wm + NW * G;
+  float* wo = wl + NW * G;
+  for (int l = 0; l < ls.L; ++l) {
+    // ---- layer l's inputs are the previous layer's outputs in a real model
+    if (l == 0) {
+      griddep_wait();
+      if (tid == 0) griddep_launch();  // every CTA has started: dependents cannot starve this grid
+    } else {
+      if (tid == 0)
+        while (ld_acquire(&ls.layer_done[l - 1]) < segs) {
+        }
+      consumers_sync();
+    }
+    const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
+    uint32_t qa[8][2];
+    {
+      const uint32_t* qrow =
+          reinterpret_cast<const uint32_t*>(q + s * a.q_ss + (int64_t)(g * G + (real ? gid : 0)) * D);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        qa[ks][0] = real ? qrow[8 * ks + tig] : 0u;
+        qa[ks][1] = real ? qrow[8 * ks + 4 + tig] : 0u;
+      }
+    }
+    const uint32_t ph = l & 1;
+    mbar_wait(kfull, ph);
+    if (has_new) {
+      // the new token's k/v replace their (stale) cache slot in the tiles
+      if (warp == 0) {
+        if (lane >= 16) mbar_wait(vfull, ph);
+        const int kk = a.n_old - k0, t = kk / TT, r = kk % TT;
+        const int cd = lane & 15;
+        const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(lane < 16 ? a.kin : a.vin) + l * ls.in_ls;
+        const uint4* in = reinterpret_cast<const uint4*>(src + s * a.in_ss + (int64_t)g * D);
+        *reinterpret_cast<uint4*>((lane < 16 ? ktiles : vtiles) + t * TILE + swz(r, cd)) = in[cd];
+      }
+      consumers_sync();
+    }
+    float m = -INFINITY, lsum = 0.f;
+    float o[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float* lgrow = a.logits ? a.logits + l * ls.lg_ls + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs
+                            : nullptr;
+    float p[4][2];
+    const bool active = wk0 < ntile * TT;
+    if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, real ? lgrow : nullptr, p, m, lsum);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(kfree);
+    mbar_wait(vfull, ph);
+    if (active) warp_pv(p, vbase, wk0, lane, o);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(vfree);
+    // ---- warp partials -> chunk partial (decode_tc_kernel's order)
+    if (real) {
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+        *reinterpret_cast<float2*>(wo + (warp * G + gid) * D + 8 * nt + 2 * tig) = make_float2(o[nt][0], o[nt][1]);
+      if (tig == 0) {
+        wm[warp * G + gid] = m;
+        wl[warp * G + gid] = lsum;
+      }
+    }
+    consumers_sync();
+    if (a.append && j == a.nc - 1) {
+      AttnArgs al = a;  // layer l's cache rows and token metadata
+      al.kc = static_cast<__nv_bfloat16*>(a.kc) + l * ls.kv_ls;
+      al.vc = static_cast<__nv_bfloat16*>(a.vc) + l * ls.kv_ls;
+      al.kin = static_cast<const __nv_bfloat16*>(a.kin) + l * ls.in_ls;
+      al.vin = static_cast<const __nv_bfloat16*>(a.vin) + l * ls.in_ls;
+      al.pos = a.pos + l * ls.m_ls;
+      al.modality = a.modality + l * ls.m_ls;
+      al.round_id = a.round_id + l * ls.m_ls;
+      al.len = a.len + l;
+      al.next_pos = a.next_pos + l;
+      append_row<__nv_bfloat16, D>(al, sigma, n, tid, CT);
+    }
+    float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PW;
+    for (int idx = tid; idx < G * D; idx += CT) {
+      const int h = idx / D, d = idx - h * D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w * G + h]);
+      float f[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) f[w] = rescale(wm[w * G + h], M);
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) acc = fmaf(f[w], wo[(w * G + h) * D + d], acc);
+      part[h * PW + d] = acc;
+      if (d == 0) {
+        float xs[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) xs[w] = f[w] * wl[w * G + h];
+#pragma unroll
+        for (int off = NW / 2; off > 0; off >>= 1)
+#pragma unroll
+          for (int w = 0; w < off; ++w) xs[w] = xs[w] + xs[w + off];
+        part[h * PW + D] = M;
+        part[h * PW + D + 1] = xs[0];
+      }
+    }
+    consumers_sync();
+    if (tid == 0) {
+      int old;  // publish; the chunk completing the segment merges it
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(&ls.seg_count[sigma]) : "memory");
+      *merger = old == a.nc - 1;
+    }
+    consumers_sync();
+    if (*merger) {
+      // ---- segment merge (merge_kernel's arithmetic): chunk weights per head
+      // by warp h, then each output element over the chunks in order
+      const int nc = a.nc;
+      const float* seg = a.part + (int64_t)sigma * nc * G * PW;
+      float* fac = wo;  // the warp partials are consumed
+      float* stats = a.stats + l * ls.st_ls;
+      if (warp < G) {
+        const int hh = warp;
+        float mj[4], lj[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int jj = lane + 32 * k;
+          mj[k] = jj < nc ? __ldcg(seg + (jj * G + hh) * PW + D) : -INFINITY;
+          lj[k] = jj < nc ? __ldcg(seg + (jj * G + hh) * PW + D + 1) : 0.f;
+        }
+        float M = fmaxf(fmaxf(mj[0], mj[1]), fmaxf(mj[2], mj[3]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        float L = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int jj = lane + 32 * k;
+          if (jj < nc) {
+            const float w = rescale(mj[k], M);
+            fac[hh * nc + jj] = w;
+            L += w * lj[k];
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+        if (lane == 0) {
+          fac[G * nc + hh] = L;
+          stats[s * a.st_ss + (g * G + hh) * 2] = M;
+          stats[s * a.st_ss + (g * G + hh) * 2 + 1] = L;
+        }
+      }
+      consumers_sync();
+      float* out = a.out + l * ls.o_ls + s * a.o_ss + (int64_t)(g * G) * D;
+      for (int idx = tid; idx < G * D; idx += CT) {
+        const int h = idx / D, d = idx - h * D;
+        const float* wf = fac + h * nc;
+        const float* pp = seg + h * PW + d;
+        float acc = 0.f;
+        for (int jj = 0; jj < nc; ++jj) acc = fmaf(wf[jj], __ldcg(pp + jj * G * PW), acc);
+        out[idx] = acc / fac[G * nc + h];
+      }
+      consumers_sync();
+      if (tid == 0) {
+        ls.seg_count[sigma] = 0;
+        red_release_add(&ls.layer_done[l], 1);
+      }
+    }
+  }
+  if (tid == 0) {
+    // the last CTA out resets the layer counters for the next launch (the
+    // next launch's consumers read them only after griddepcontrol.wait)
+    if (atomicAdd(ls.exit_count, 1) == (int)gridDim.x - 1) {
+      for (int l = 0; l < ls.L; ++l) ls.layer_done[l] = 0;
+      *ls.exit_count = 0;
+    }
   }
 }
 
@@ -413,6 +730,46 @@ cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_
   }
   if (e != cudaSuccess) return e;
   return launch_merge(128, group, a, st);
+}
+
+cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st) {
+  if (a.ch > tcd::MAXT || !a.stat || a.nc > 128) return cudaErrorInvalidValue;
+  CUtensorMap kmap, vmap;
+  cudaError_t e = make_kv_map(&kmap, a.kc_base, a.total_rows, tcd::TT);
+  if (e == cudaSuccess) e = make_kv_map(&vmap, a.vc_base, a.total_rows, tcd::TT);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(tcd::THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (group == 4) {
+    static DevOnce attr;
+    if (!attr.here()) {
+      e = cudaFuncSetAttribute(decode_tc_layers_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)tcd::Smem<4>::bytes);
+      if (e != cudaSuccess) return e;
+      attr.here() = true;
+    }
+    cfg.dynamicSmemBytes = tcd::Smem<4>::bytes;
+    return cudaLaunchKernelEx(&cfg, decode_tc_layers_kernel<4>, kmap, vmap, a, ls);
+  }
+  if (group == 8) {
+    static DevOnce attr;
+    if (!attr.here()) {
+      e = cudaFuncSetAttribute(decode_tc_layers_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)tcd::Smem<8>::bytes);
+      if (e != cudaSuccess) return e;
+      attr.here() = true;
+    }
+    cfg.dynamicSmemBytes = tcd::Smem<8>::bytes;
+    return cudaLaunchKernelEx(&cfg, decode_tc_layers_kernel<8>, kmap, vmap, a, ls);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace skv

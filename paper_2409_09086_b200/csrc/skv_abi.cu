@@ -99,6 +99,8 @@ struct skv_ctx {
   float scale;
   int max_ctas;    // persistent decode grid bound (CTAs/SM x SMs)
   int last_layer = -1;  // layer of the last decode launch on the ctx (-1: other work since)
+  bool layers_chain = false;  // the last launch was an all-layer persistent decode step
+  int32_t* lay_cnt = nullptr;  // persistent decode: [S*Hkv] segment chunk counters, [L] layers done, [1] exits
   int launch_seq = 0;   // decode launches (selects the scheduler slot)
   int32_t* sched = nullptr;  // [64][4] per-launch ticket / barrier / exit counters
   int32_t* done = nullptr;   // [64] per-launch completion flags
@@ -511,8 +513,16 @@ static void fold_target(skv_ctx* x, int layer, int slot, FoldArgs& f) {
   }
 }
 
-static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
-                             const int64_t* pos_dev, float* out, int record, cudaStream_t st) {
+// A decode launch's schedule and arguments for one layer (no kernel of the
+// attention itself is launched here; RoPE rotation of q / new k is).
+struct DecodePlan {
+  AttnArgs a;
+  int record, n, nt, ch, nc, ctas, par;
+  bool stat, tc;
+};
+
+static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, const void* v, const int64_t* pos_dev,
+                         float* out, int record, cudaStream_t st, DecodePlan& plan) {
   // Rows feed only the Inf-MLLM window and the heavy-hitter accumulator; the
   // heavy hitter needs every step's row (engine.py:274)
   if (x->cfg.policy == SKV_POLICY_HEAVY_HITTER) record = 1;
@@ -559,6 +569,7 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     if (e != cudaSuccess) return cuda_fail(e, "rope kernel launch");
     x->launches++;
     x->last_layer = -1;
+    x->layers_chain = false;
     kraw_in = k;
     q = x->qr;
     k = x->kr;
@@ -640,34 +651,54 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
     f.mode = x->cfg.head_agg == SKV_AGG_MAX ? 1 : 0;
     f.agg_div = x->Hq_total;
   }
-  cudaError_t e;
-  if (stat && x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && ch <= 4 && use_tc_decode()) {
-    // latency-bound GQA launch: the tensor-core (mma.sync) chunk kernel
-    a.L = x->L;
-    a.layer = layer;
-    a.cap = x->cap;
-    a.kc_base = x->k;
-    a.vc_base = x->v;
-    a.total_rows = (int64_t)x->S * x->L * x->Hkv * x->cap;
-    e = launch_decode_tc(x->G, ctas, a, st);
-  } else {
-    e = launch_decode(x->cfg.dtype, x->D, x->G, ctas, a, st);
+  plan.a = a;
+  plan.record = record;
+  plan.n = n;
+  plan.nt = nt;
+  plan.ch = ch;
+  plan.nc = nc;
+  plan.ctas = ctas;
+  plan.par = par;
+  plan.stat = stat;
+  plan.tc = stat && x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && ch <= 4 && use_tc_decode();
+  if (plan.tc) {
+    plan.a.L = x->L;
+    plan.a.layer = layer;
+    plan.a.cap = x->cap;
+    plan.a.kc_base = x->k;
+    plan.a.vc_base = x->v;
+    plan.a.total_rows = (int64_t)x->S * x->L * x->Hkv * x->cap;
   }
-  if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
-  x->launches += 2;  // decode + segment merge
-  x->last_layer = layer;
+  return SKV_OK;
+}
+
+// Host mirror after a decode of `layer` (uniform over the streams).
+static void commit_layer(skv_ctx* x, int layer, const DecodePlan& p) {
   x->pend_n[layer] = 0;
-  if (record) {
-    x->pend_n[layer] = n;
+  if (p.record) {
+    x->pend_n[layer] = p.n;
     x->pend_slot[layer] = x->whead[layer];
-    x->pend_par[layer] = par;
+    x->pend_par[layer] = p.par;
     if (x->cfg.policy == SKV_POLICY_INF_MLLM) {  // the heavy hitter accumulates instead of pushing
       x->whead[layer] = (x->whead[layer] + 1) % x->W;
       x->wcount[layer] = std::min(x->wcount[layer] + 1, x->W);
     }
-    x->parity[layer] = par ^ 1;
+    x->parity[layer] = p.par ^ 1;
   }
-  x->n[layer] = n;
+  x->n[layer] = p.n;
+}
+
+static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
+                             const int64_t* pos_dev, float* out, int record, cudaStream_t st) {
+  DecodePlan p;
+  int rc = prepare_layer(x, layer, q, k, v, pos_dev, out, record, st, p);
+  if (rc) return rc;
+  cudaError_t e = p.tc ? launch_decode_tc(x->G, p.ctas, p.a, st) : launch_decode(x->cfg.dtype, x->D, x->G, p.ctas, p.a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+  x->launches += 2;  // decode + segment merge
+  x->last_layer = layer;
+  x->layers_chain = false;
+  commit_layer(x, layer, p);
   return SKV_OK;
 }
 
@@ -690,6 +721,7 @@ static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
   if (e != cudaSuccess) return cuda_fail(e, "fold kernel launch");
   x->launches++;
   x->last_layer = -1;
+  x->layers_chain = false;
   x->pend_n[layer] = 0;
   return SKV_OK;
 }
@@ -798,6 +830,7 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   x->wcount[layer] = std::min(x->wcount[layer] + wrec, x->W);
   x->n[layer] = n0 + C;
   x->last_layer = -1;
+  x->layers_chain = false;
   return SKV_OK;
 }
 
@@ -826,9 +859,71 @@ int skv_decode_layer(skv_ctx* x, int layer, const void* q, const void* k, const 
   return decode_layer_impl(x, layer, q, k, v, pos_dev, out, record, st);
 }
 
+static int use_layers_kernel() {  // SKV_LAYERS=0 keeps all-layer steps on per-layer launches (A/B)
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_LAYERS");
+    env = e ? atoi(e) : 1;
+  }
+  return env;
+}
+
+// All layers of one token in one persistent launch (decode_tc_layers_kernel)
+// when every layer is in the same state and its decode would run on the
+// static tensor-core schedule (latency-bound GQA steps, config 3).  Returns
+// 1 when launched, 0 to fall back to per-layer launches.
+static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
+                              cudaStream_t st) {
+  if (x->L < 2 || !use_layers_kernel() || x->cfg.rope_mode != SKV_ROPE_NONE || x->timing) return 0;
+  for (int l = 0; l < x->L; ++l)
+    if (x->ragged[l] || x->n[l] != x->n[0] || x->parity[l] != x->parity[0] || x->pend_n[l] != x->pend_n[0] ||
+        x->pend_slot[l] != x->pend_slot[0] || x->pend_par[l] != x->pend_par[0] || x->whead[l] != x->whead[0] ||
+        x->wcount[l] != x->wcount[0] || x->round_value[l] != x->round_value[0])
+      return 0;
+  if (!(x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && use_tc_decode())) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  DecodePlan p;
+  int rc = prepare_layer(x, 0, q, k, v, nullptr, out, record, st, p);
+  if (rc) return rc;
+  if (!p.tc || p.ctas != x->S * x->Hkv * p.nc || p.ctas > sms) return 0;  // every CTA co-resident, one chunk each
+  if (!x->lay_cnt) {
+    cudaError_t e = x->alloc(&x->lay_cnt, ((size_t)x->S * x->Hkv + x->L + 1) * sizeof(int32_t));
+    if (e != cudaSuccess) return cuda_fail(e, "layer counters");
+  }
+  LayerSteps ls{};
+  ls.L = x->L;
+  ls.q_ls = (int64_t)x->S * x->Hq * x->D;
+  ls.in_ls = (int64_t)x->S * x->Hkv * x->D;
+  ls.o_ls = (int64_t)x->S * x->Hq * x->D;
+  ls.kv_ls = x->kv_layer_stride();
+  ls.m_ls = x->cap;
+  ls.lg_ls = (int64_t)x->Hq * x->cap;
+  ls.st_ls = (int64_t)x->Hq * 2;
+  ls.fr_ls = x->cfg.policy == SKV_POLICY_HEAVY_HITTER ? x->cap : (int64_t)x->W * x->cap;
+  ls.fw_ls = x->W;
+  ls.seg_count = x->lay_cnt;
+  ls.layer_done = x->lay_cnt + (size_t)x->S * x->Hkv;
+  ls.exit_count = ls.layer_done + x->L;
+  ls.prefetch0 = x->layers_chain ? 1 : 0;
+  cudaError_t e = launch_decode_tc_layers(x->G, p.ctas, p.a, ls, st);
+  if (e != cudaSuccess) return cuda_fail(e, "decode (all layers) kernel launch");
+  x->launches += 1;
+  x->last_layer = -1;
+  x->layers_chain = true;
+  for (int l = 0; l < x->L; ++l) commit_layer(x, l, p);
+  return 1;
+}
+
 int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record, void* stream) {
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
   cudaStream_t st = as_stream(stream);
+  {
+    const int rc = decode_step_layers(x, q, k, v, out, record, st);
+    if (rc < 0) return rc;
+    if (rc == 1) return SKV_OK;
+  }
   const int64_t qb = (int64_t)x->S * x->Hq * x->D * x->elt;
   const int64_t kb = (int64_t)x->S * x->Hkv * x->D * x->elt;
   const int64_t ob = (int64_t)x->S * x->Hq * x->D;
@@ -972,6 +1067,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
     x->launches++;
     x->last_layer = -1;
+    x->layers_chain = false;
     if (mode == 1) return SKV_OK;
     c.k = static_cast<char*>(x->k);
     c.v = static_cast<char*>(x->v);
@@ -1004,6 +1100,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
     if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
     x->launches++;
     x->last_layer = -1;
+    x->layers_chain = false;
     if (c.rope_cr) {  // _refresh_rotations (engine.py:339-342): moved keys at their new slots
       int rc = rope_rows(x, 0, x->L, 0, m, x->first_moved, st);
       if (rc) return rc;
@@ -1041,6 +1138,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       if (e != cudaSuccess) return cuda_fail(e, "select kernel launch");
       x->launches++;
       x->last_layer = -1;
+      x->layers_chain = false;
       if (mode == 1) continue;
       c.k = static_cast<char*>(x->k) + sl0 * x->kv_layer_stride() * x->elt;
       c.v = static_cast<char*>(x->v) + sl0 * x->kv_layer_stride() * x->elt;
@@ -1073,6 +1171,7 @@ static int evict_layers(skv_ctx* x, int l0, int l1, int32_t* kept_dev, int kept_
       if (e != cudaSuccess) return cuda_fail(e, "compact kernel launch");
       x->launches++;
       x->last_layer = -1;
+      x->layers_chain = false;
       if (c.rope_cr) {
         int rc = rope_rows(x, l, l + 1, 0, m, x->first_moved, st);
         if (rc) return rc;
@@ -1378,6 +1477,7 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
                         cudaMemcpyHostToDevice));
   SKV_CK(cudaMemcpy(x->wlen + sl * x->W, lens.data(), x->W * sizeof(int32_t), cudaMemcpyHostToDevice));
   x->last_layer = -1;
+  x->layers_chain = false;
   if (x->acc)  // heavy hitter: injected tokens start with no accumulated mass
     SKV_CK(cudaMemset(x->acc + ((int64_t)stream * x->L + layer) * x->cap, 0, (size_t)x->cap * sizeof(float)));
   if (x->kraw && n > 0) {  // rotated keys of the injected tokens (every stream of the layer)

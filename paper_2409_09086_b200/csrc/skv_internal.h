@@ -105,6 +105,26 @@ struct AttnArgs {
 };
 
 cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st);
+
+// All layers of one token in one persistent launch (decode_tc_layers_kernel):
+// AttnArgs describe layer 0; layer l's pointers advance by these strides.
+// The segment merge runs inside the kernel (the CTA publishing a segment's
+// last chunk merges it) and layer l+1's queries wait for layer l's outputs
+// through layer_done[l] -- the model's layer-to-layer dependency, with no
+// launch boundary on the chain.
+struct LayerSteps {
+  int L;                      // layers of the launch (layer 0 = args' layer)
+  int64_t q_ls, in_ls, o_ls;  // elements between layers of q / new k,v / out
+  int64_t kv_ls;              // K/V store elements between layers (kc, vc)
+  int64_t m_ls;               // token metadata elements between layers
+  int64_t lg_ls, st_ls;       // recorded logits / (max, sum) stats floats between layers
+  int64_t fr_ls, fw_ls;       // pending fold: window row floats / lengths between layers
+  int32_t* seg_count;         // [S*Hkv] published chunks (reset by the merging CTA)
+  int32_t* layer_done;        // [L] merged segments per layer (reset by the last CTA out)
+  int32_t* exit_count;        // [1]
+  int prefetch0;              // 1: layer 0's cached K/V may stream before griddepcontrol.wait
+};
+cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st);
 // static-schedule GQA launches (bf16, D = 128, group 4 or 8, chunks <= 4 tiles) on mma.sync
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st);
 // the segment merge alone (PDL), after a decode launch

@@ -252,3 +252,50 @@ def test_slot_map_moves_only_the_survivors_of_the_period():
     # cache-relative RoPE engines compact densely (their moved keys change position anyway)
     dense = _eng(1, 1, 8, 2, 128, 32, 32, 8, 80, rope="cache_relative")
     assert dense.moved_rows() is None and dense.slot_map(0, 0) is None
+
+
+@pytest.mark.parametrize("G", [4, 8])
+def test_all_layer_persistent_decode_matches_oracle(G):
+    """decode_step of a latency-bound GQA engine runs all layers in one
+    persistent launch (decode_tc_layers_kernel: in-kernel segment merge,
+    layer l+1 released by layer l's outputs).  Against the oracle over three
+    periods: outputs, window rows, kept sets, compacted K/V."""
+    S, L, Hkv, D = 1, 4, 32 // G, 128
+    Hq = Hkv * G
+    l, r, W, E = 512, 512, 16, 64
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = _eng(S, L, Hq, Hkv, D, l, r, W, B + E)
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    rng = np.random.default_rng(60 + G)
+    _inject_both(eng, orc, rng, S, L, Hkv, D, B)
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    worst = worst_row = 0.0
+    for period in range(3):
+        for t in range(E):
+            q = bf16_round(rng.standard_normal((L, S, Hq, D)).astype(F32))
+            k = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            before = eng.kernel_launches
+            got = eng.decode_step(*(torch.from_numpy(a).to("cuda", torch.bfloat16) for a in (q, k, v)),
+                                  record=t >= E - W).cpu().numpy()
+            assert eng.kernel_launches - before == 1  # one launch for all layers
+            worst = max(worst, rel_err(got, orc.step(q, k, v)))
+        for s in range(S):
+            for layer in range(L):
+                for a_, b_ in zip(eng.window_rows(s, layer), orc.win[s][layer].rows[-W:]):
+                    worst_row = max(worst_row, float(np.abs(a_ - b_).max() / np.abs(b_).max()))
+        eng.evict(-1, kept)
+        kc = kept.cpu().numpy()
+        for s in range(S):
+            for layer in range(L):
+                ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept, kc[s, layer],
+                                                B + E, cfg)
+                assert ok, (period, s, layer, nbad, gap)
+                orc.apply(s, layer, kc[s, layer].astype(np.int64))
+                kg, vg = eng.kv(s, layer)
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
+                np.testing.assert_array_equal(eng.positions(s, layer), orc.kv[s][layer].pos[: orc.kv[s][layer].n])
+    print(f"persistent G={G}: worst out {worst:.2e} rows {worst_row:.2e}")
+    assert worst <= 2e-3 and worst_row <= 2e-3
