@@ -506,6 +506,8 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
         }
       consumers_sync();
     }
+    unsigned long long* tl = ls.tl ? ls.tl + ((int64_t)l * gridDim.x + c) * 8 : nullptr;
+    if (tl && tid == 0) tl[0] = gtimer();  // released
     const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
     uint32_t qa[8][2];
     {
@@ -518,7 +520,9 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       }
     }
     const uint32_t ph = l & 1;
+    if (tl && tid == 0) tl[1] = gtimer();  // q loaded
     mbar_wait(kfull, ph);
+    if (tl && tid == 0) tl[2] = gtimer();  // K tiles in
     if (has_new) {
       // the new token's k/v replace their (stale) cache slot in the tiles
       if (warp == 0) {
@@ -546,6 +550,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
     if (active) warp_pv(p, vbase, wk0, lane, o);
     __syncwarp();
     if (lane == 0) mbar_arrive(vfree);
+    if (tl && tid == 0) tl[3] = gtimer();  // warp 0 math done
     // ---- warp partials -> chunk partial (decode_tc_kernel's order)
     if (real) {
 #pragma unroll
@@ -600,6 +605,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       int old;  // publish; the chunk completing the segment merges it
       asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(&ls.seg_count[sigma]) : "memory");
       *merger = old == a.nc - 1;
+      if (tl) tl[4] = gtimer();  // published
     }
     consumers_sync();
     if (*merger) {
@@ -653,6 +659,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       if (tid == 0) {
         ls.seg_count[sigma] = 0;
         red_release_add(&ls.layer_done[l], 1);
+        if (tl) tl[5] = gtimer();  // segment merged + released
       }
     }
   }

@@ -101,6 +101,7 @@ struct skv_ctx {
   int last_layer = -1;  // layer of the last decode launch on the ctx (-1: other work since)
   bool layers_chain = false;  // the last launch was an all-layer persistent decode step
   int32_t* lay_cnt = nullptr;  // persistent decode: [S*Hkv] segment chunk counters, [L] layers done, [1] exits
+  unsigned long long* lay_tl = nullptr;  // instrumentation: persistent decode timeline (skv_layers_timeline)
   int launch_seq = 0;   // decode launches (selects the scheduler slot)
   int32_t* sched = nullptr;  // [64][4] per-launch ticket / barrier / exit counters
   int32_t* done = nullptr;   // [64] per-launch completion flags
@@ -434,6 +435,12 @@ int skv_timing(skv_ctx* x, int enable) {
     }
   }
   x->timing = enable != 0;
+  return SKV_OK;
+}
+
+int skv_layers_timeline(skv_ctx* x, uint64_t* buf_dev) {
+  if (!x) return fail(SKV_EINVAL, "null argument");
+  x->lay_tl = reinterpret_cast<unsigned long long*>(buf_dev);
   return SKV_OK;
 }
 
@@ -859,11 +866,11 @@ int skv_decode_layer(skv_ctx* x, int layer, const void* q, const void* k, const 
   return decode_layer_impl(x, layer, q, k, v, pos_dev, out, record, st);
 }
 
-static int use_layers_kernel() {  // SKV_LAYERS=0 keeps all-layer steps on per-layer launches (A/B)
+static int use_layers_kernel() {  // SKV_LAYERS=1 runs all-layer steps in one persistent launch (A/B)
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("SKV_LAYERS");
-    env = e ? atoi(e) : 1;
+    env = e ? atoi(e) : 0;
   }
   return env;
 }
@@ -907,6 +914,7 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   ls.layer_done = x->lay_cnt + (size_t)x->S * x->Hkv;
   ls.exit_count = ls.layer_done + x->L;
   ls.prefetch0 = x->layers_chain ? 1 : 0;
+  ls.tl = x->lay_tl;
   cudaError_t e = launch_decode_tc_layers(x->G, p.ctas, p.a, ls, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode (all layers) kernel launch");
   x->launches += 1;

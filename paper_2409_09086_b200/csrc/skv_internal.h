@@ -123,6 +123,7 @@ struct LayerSteps {
   int32_t* layer_done;        // [L] merged segments per layer (reset by the last CTA out)
   int32_t* exit_count;        // [1]
   int prefetch0;              // 1: layer 0's cached K/V may stream before griddepcontrol.wait
+  unsigned long long* tl;     // instrumentation (null: off): [L][grid][8] %globaltimer per CTA and layer
 };
 cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st);
 // static-schedule GQA launches (bf16, D = 128, group 4 or 8, chunks <= 4 tiles) on mma.sync
