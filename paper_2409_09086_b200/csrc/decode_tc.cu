@@ -23,6 +23,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "skv_common.cuh"
 #include "skv_append.cuh"
@@ -93,6 +95,7 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ float rescale(float m, float M) { return m == -INFINITY ? 0.f : exp2f((m - M) * kLog2e); }
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -673,6 +676,335 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// All layers of one token, one thread-block cluster per (stream, kv-head)
+// segment: cluster rank j owns chunk j (tiles [j ch, (j+1) ch)) in every layer,
+// so the cluster's CTAs are co-resident for the whole token and the segment
+// merge runs over distributed shared memory instead of a global round trip:
+//   * every rank writes its chunk partial (o, m, l per query head) into its own
+//     shared memory (double-buffered by layer parity) and arrives, with cluster
+//     release semantics, on every rank's `ready` mbarrier;
+//   * every rank waits on its own `ready`, then merges a slice of the segment's
+//     output elements reading all ranks' partials with ld.shared::cluster
+//     (merge_kernel's arithmetic: chunk weights rescale(m_j, M), L = sum w_j l_j,
+//     out = sum_j w_j o_j / L in chunk order), stores them and releases
+//     layer_done[l] (target: segments x ranks);
+//   * layer l+1's consumers wait for layer_done[l] (the model's dependency),
+//     while the producer has already streamed layer l+1's K/V into the tiles
+//     freed by layer l.
+template <int G, int MT>
+struct ClSmem {
+  static constexpr int NWC = 2 * MT;                        // consumer warps (32 keys each)
+  static constexpr int THREADS = NWC * 32 + 96;             // + producer, fold, spare warps
+  static constexpr size_t tiles = (size_t)2 * MT * tcd::TILE;
+  static constexpr size_t slot_floats = 4 + 2 * NWC * G + NWC * G * tcd::D;
+  static constexpr size_t cpart_floats = 2 * G * tcd::PW;  // [parity][G][D + 2]
+  // + barriers, 1024-byte alignment slack and the fold warp's (M, 1/L) per query head
+  static size_t bytes(int Hq) { return tiles + (slot_floats + cpart_floats) * 4 + 128 + 1024 + (size_t)Hq * 8; }
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_cluster(uint32_t addr) {
+  float v;  // (ordered after the acquire wait by the barrier below it; no clobber so loads overlap)
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int G, int MT>
+__global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                                         const AttnArgs a, const LayerSteps ls) {
+  using namespace tcd;
+  using Sm = ClSmem<G, MT>;
+  constexpr int NWC = Sm::NWC, CTC = NWC * 32;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* ktiles = smem;
+  unsigned char* vtiles = smem + MT * TILE;
+  float* slot = reinterpret_cast<float*>(smem + Sm::tiles);
+  float* cpart = slot + Sm::slot_floats;  // [2][G][PW]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cpart + Sm::cpart_floats);
+  uint64_t* kfull = bars;
+  uint64_t* vfull = bars + 1;
+  uint64_t* kfree = bars + 2;
+  uint64_t* vfree = bars + 3;
+  uint64_t* ready = bars + 4;  // [2] by layer parity: one arrive per cluster rank
+  float* fstats = reinterpret_cast<float*>(bars + 16);  // fold warp: [Hq][2]
+
+  const int CS = a.nc;  // cluster size == chunks per segment
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j = (int)cluster_rank();
+  const int sigma = blockIdx.x / CS;
+  const int n = a.n_old + a.append;
+  const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+  const int segs = a.S * a.Hkv;
+  const int tt0 = min(j * a.ch, a.nt), tt1 = min(tt0 + a.ch, a.nt);
+  const int ntile = tt1 - tt0;
+  const int k0 = tt0 * TT;
+  const int kend = min(tt1 * TT, n);
+  const bool has_new = a.append && a.n_old >= k0 && a.n_old < kend;
+  const bool has_prev = a.n_old - 1 >= k0 && a.n_old - 1 < kend;
+
+  if (tid == 0) {
+    mbar_init(kfull, 1);
+    mbar_init(vfull, 1);
+    mbar_init(kfree, NWC);
+    mbar_init(vfree, NWC);
+    mbar_init(&ready[0], CS);
+    mbar_init(&ready[1], CS);
+    mbar_fence_init();
+  }
+  cluster_sync_all();  // every rank's barriers exist before any remote arrive
+
+  if (warp == NWC) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0 && ntile > 0) {
+      if (!ls.prefetch0 || has_prev) griddep_wait();
+      for (int l = 0; l < ls.L; ++l) {
+        const int seg_row = (int)(((int64_t)s * a.L + a.layer + l) * a.Hkv + g) * a.cap;
+        if (l > 0) mbar_wait(kfree, (l - 1) & 1);
+        mbar_arrive_expect_tx(kfull, (uint32_t)ntile * TILE);
+        for (int t = 0; t < ntile; ++t) {
+          const int y = seg_row + (tt0 + t) * TT;
+          tma_load_2d(ktiles + t * TILE, &kmap, 0, y, kfull);
+          tma_load_2d(ktiles + t * TILE + REGION, &kmap, 64, y, kfull);
+        }
+        if (l > 0) mbar_wait(vfree, (l - 1) & 1);
+        mbar_arrive_expect_tx(vfull, (uint32_t)ntile * TILE);
+        for (int t = 0; t < ntile; ++t) {
+          const int y = seg_row + (tt0 + t) * TT;
+          tma_load_2d(vtiles + t * TILE, &vmap, 0, y, vfull);
+          tma_load_2d(vtiles + t * TILE + REGION, &vmap, 64, y, vfull);
+        }
+      }
+    }
+  } else if (warp == NWC + 1) {
+    // ------------------------------------------------- window-row fold warp
+    if (a.fold.n > 0) {
+      griddep_wait();
+      const int P = gridDim.x, c = blockIdx.x;
+      const int ppc = (a.fold.n + 63) / 64;
+      for (int l = 0; l < ls.L; ++l) {
+        FoldArgs f = a.fold;
+        f.logits += l * ls.lg_ls;
+        f.stats += l * ls.st_ls;
+        f.rows += l * ls.fr_ls;
+        if (f.wlen) f.wlen += l * ls.fw_ls;
+        for (int piece = c; piece < a.S * ppc; piece += P) {
+          const int s2 = piece / ppc, col0 = (piece - s2 * ppc) * 64;
+          const float* stt = f.stats + s2 * f.st_ss;
+          for (int h = lane; h < a.Hq; h += 32) {
+            fstats[2 * h] = __ldg(stt + 2 * h);
+            fstats[2 * h + 1] = __frcp_rn(__ldg(stt + 2 * h + 1));  // staged as 1/L
+          }
+          __syncwarp();
+          fold_columns(f, s2, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+          __syncwarp();
+          if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s2 * f.w_ss] = f.n;
+        }
+      }
+    }
+  } else if (warp < NWC) {
+    // ------------------------------------------------------------ consumers
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool real = gid < G;
+    const uint32_t kbase = smem_u32(ktiles), vbase = smem_u32(vtiles);
+    const int wk0 = warp * 32;
+    float* wm = slot + 4;
+    float* wl = wm + NWC * G;
+    float* wo = wl + NWC * G;
+    const int total_out = G * D;
+    const int per_rank = (total_out + CS - 1) / CS;  // output elements this rank merges
+    for (int l = 0; l < ls.L; ++l) {
+      if (l == 0) {
+        griddep_wait();
+        if (tid == 0) griddep_launch();
+      } else {
+        if (tid == 0)
+          while (ld_acquire(&ls.layer_done[l - 1]) < segs * CS) {
+          }
+        bar_sync_n(1, CTC);
+      }
+      unsigned long long* tl = ls.tl ? ls.tl + ((int64_t)l * gridDim.x + blockIdx.x) * 8 : nullptr;
+      if (tl && tid == 0) tl[0] = gtimer();
+      const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
+      uint32_t qa[8][2];
+      {
+        const uint32_t* qrow =
+            reinterpret_cast<const uint32_t*>(q + s * a.q_ss + (int64_t)(g * G + (real ? gid : 0)) * D);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          qa[ks][0] = real ? qrow[8 * ks + tig] : 0u;
+          qa[ks][1] = real ? qrow[8 * ks + 4 + tig] : 0u;
+        }
+      }
+      const uint32_t ph = l & 1;
+      const bool any = ntile > 0;
+      if (any) mbar_wait(kfull, ph);
+      if (tl && tid == 0) tl[1] = gtimer();
+      if (has_new) {
+        if (warp == 0) {
+          if (lane >= 16) mbar_wait(vfull, ph);
+          const int kk = a.n_old - k0, t = kk / TT, r = kk % TT;
+          const int cd = lane & 15;
+          const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(lane < 16 ? a.kin : a.vin) + l * ls.in_ls;
+          const uint4* in = reinterpret_cast<const uint4*>(src + s * a.in_ss + (int64_t)g * D);
+          *reinterpret_cast<uint4*>((lane < 16 ? ktiles : vtiles) + t * TILE + swz(r, cd)) = in[cd];
+        }
+        bar_sync_n(1, CTC);
+      }
+      float m = -INFINITY, lsum = 0.f;
+      float o[16][4];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      float* lgrow = a.logits ? a.logits + l * ls.lg_ls + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs
+                              : nullptr;
+      float p[4][2];
+      const bool active = wk0 < ntile * TT;
+      if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, real ? lgrow : nullptr, p, m, lsum);
+      __syncwarp();
+      if (lane == 0 && any) mbar_arrive(kfree);
+      if (any) mbar_wait(vfull, ph);
+      if (active) warp_pv(p, vbase, wk0, lane, o);
+      __syncwarp();
+      if (lane == 0 && any) mbar_arrive(vfree);
+      if (tl && tid == 0) tl[2] = gtimer();
+      if (real) {
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(wo + (warp * G + gid) * D + 8 * nt + 2 * tig) = make_float2(o[nt][0], o[nt][1]);
+        if (tig == 0) {
+          wm[warp * G + gid] = m;
+          wl[warp * G + gid] = lsum;
+        }
+      }
+      bar_sync_n(1, CTC);
+      if (has_new) {
+        AttnArgs al = a;  // layer l's cache rows and token metadata
+        al.kc = static_cast<__nv_bfloat16*>(a.kc) + l * ls.kv_ls;
+        al.vc = static_cast<__nv_bfloat16*>(a.vc) + l * ls.kv_ls;
+        al.kin = static_cast<const __nv_bfloat16*>(a.kin) + l * ls.in_ls;
+        al.vin = static_cast<const __nv_bfloat16*>(a.vin) + l * ls.in_ls;
+        al.pos = a.pos + l * ls.m_ls;
+        al.modality = a.modality + l * ls.m_ls;
+        al.round_id = a.round_id + l * ls.m_ls;
+        al.len = a.len + l;
+        al.next_pos = a.next_pos + l;
+        append_row<__nv_bfloat16, D>(al, sigma, n, tid, CTC);
+      }
+      // ---- chunk partial (decode_tc_kernel's warp order) into this rank's buffer
+      float* cp = cpart + (l & 1) * G * PW;
+      for (int idx = tid; idx < G * D; idx += CTC) {
+        const int h = idx / D, d = idx - h * D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NWC; ++w) M = fmaxf(M, wm[w * G + h]);
+        float f[NWC];
+#pragma unroll
+        for (int w = 0; w < NWC; ++w) f[w] = rescale(wm[w * G + h], M);
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < NWC; ++w) acc = fmaf(f[w], wo[(w * G + h) * D + d], acc);
+        cp[h * PW + d] = acc;
+        if (d == 0) {
+          float xs = 0.f;  // warps in order (NWC need not be a power of two)
+#pragma unroll
+          for (int w = 0; w < NWC; ++w) xs += f[w] * wl[w * G + h];
+          cp[h * PW + D] = M;
+          cp[h * PW + D + 1] = xs;
+        }
+      }
+      bar_sync_n(1, CTC);
+      // ---- publish to every rank of the cluster (release at cluster scope)
+      if (tid < CS) arrive_remote(map_rank(smem_u32(&ready[l & 1]), (uint32_t)tid));
+      if (tl && tid == 0) tl[3] = gtimer();
+      wait_cluster(&ready[l & 1], (l >> 1) & 1);
+      // ---- merge this rank's slice of the segment's output elements: every
+      // rank's (m, l) per head staged once, then each element's CS partial
+      // values loaded together (distributed shared memory round trips overlap)
+      const uint32_t cp_local = smem_u32(cpart + (l & 1) * G * PW);
+      float* out = a.out + l * ls.o_ls + s * a.o_ss + (int64_t)(g * G) * D;
+      float* stats = a.stats + l * ls.st_ls;
+      float* stg = wm;  // [G][16] m, [G][16] l, [G][16] weights, [G] L (warp partials consumed)
+      if (tid < G * CS) {
+        const int h = tid / CS, r = tid - (tid / CS) * CS;
+        stg[h * 16 + r] = ld_cluster(map_rank(cp_local + (h * PW + D) * 4, r));
+        stg[G * 16 + h * 16 + r] = ld_cluster(map_rank(cp_local + (h * PW + D + 1) * 4, r));
+      }
+      bar_sync_n(1, CTC);
+      if (tid < G) {
+        const int h = tid;
+        float M = -INFINITY;
+        for (int r = 0; r < CS; ++r) M = fmaxf(M, stg[h * 16 + r]);
+        float L = 0.f;
+        for (int r = 0; r < CS; ++r) {
+          const float w = rescale(stg[h * 16 + r], M);
+          stg[2 * G * 16 + h * 16 + r] = w;
+          L += w * stg[G * 16 + h * 16 + r];
+        }
+        stg[3 * G * 16 + h] = L;
+        if (j == 0) {
+          stats[s * a.st_ss + (g * G + h) * 2] = M;
+          stats[s * a.st_ss + (g * G + h) * 2 + 1] = L;
+        }
+      }
+      bar_sync_n(1, CTC);
+      for (int e = tid; e < per_rank; e += CTC) {
+        const int idx = j + e * CS;  // strided over ranks
+        if (idx >= total_out) break;
+        const int h = idx / D, d = idx - h * D;
+        float ov[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) ov[r] = r < CS ? ld_cluster(map_rank(cp_local + (h * PW + d) * 4, r)) : 0.f;
+        const float* w = stg + 2 * G * 16 + h * 16;
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (r < CS) acc = fmaf(w[r], ov[r], acc);
+        out[idx] = acc / stg[3 * G * 16 + h];
+      }
+      bar_sync_n(1, CTC);
+      if (tid == 0) {
+        red_release_add(&ls.layer_done[l], 1);
+        if (tl) tl[4] = gtimer();
+      }
+    }
+    if (tid == 0) {
+      if (atomicAdd(ls.exit_count, 1) == (int)gridDim.x - 1) {
+        for (int l = 0; l < ls.L; ++l) ls.layer_done[l] = 0;
+        *ls.exit_count = 0;
+      }
+    }
+  }
+  cluster_sync_all();  // no rank leaves while another may still read its partials
+}
+
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
   if (a.ch > tcd::MAXT || !a.stat) return cudaErrorInvalidValue;
   // tensor maps depend only on the store (base, rows): encode once per store
@@ -776,6 +1108,53 @@ cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, cons
     cfg.dynamicSmemBytes = tcd::Smem<8>::bytes;
     return cudaLaunchKernelEx(&cfg, decode_tc_layers_kernel<8>, kmap, vmap, a, ls);
   }
+  return cudaErrorInvalidValue;
+}
+
+// Cluster variant: one cluster of a.nc CTAs per segment (a.nc <= 16).
+cudaError_t launch_decode_tc_cluster(int group, int mt, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st,
+                                     int* max_clusters) {
+  CUtensorMap kmap, vmap;
+  cudaError_t e = make_kv_map(&kmap, a.kc_base, a.total_rows, tcd::TT);
+  if (e == cudaSuccess) e = make_kv_map(&vmap, a.vc_base, a.total_rows, tcd::TT);
+  if (e != cudaSuccess) return e;
+  const int segs = a.S * a.Hkv;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(segs * a.nc);
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = a.nc;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  static DevOnce attrs_set[2][8];  // per instantiation (G, mt): kern has one type for all of them
+  auto run = [&](auto kern, int threads, size_t smem_bytes) -> cudaError_t {
+    DevOnce& attr = attrs_set[group == 8][mt & 7];
+    if (!attr.here()) {
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (r != cudaSuccess) return r;
+      attr.here() = true;
+    }
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    if (smem_bytes > 227 * 1024) return cudaErrorInvalidValue;
+    if (max_clusters) {  // co-residency check only
+      cudaLaunchConfig_t q = cfg;
+      q.numAttrs = 2;
+      return cudaOccupancyMaxActiveClusters(max_clusters, kern, &q);
+    }
+    return cudaLaunchKernelEx(&cfg, kern, kmap, vmap, a, ls);
+  };
+  if (group == 4 && mt == 4) return run(decode_tc_cluster_kernel<4, 4>, ClSmem<4, 4>::THREADS, ClSmem<4, 4>::bytes(a.Hq));
+  if (group == 4 && mt == 5) return run(decode_tc_cluster_kernel<4, 5>, ClSmem<4, 5>::THREADS, ClSmem<4, 5>::bytes(a.Hq));
+  if (group == 4 && mt == 6) return run(decode_tc_cluster_kernel<4, 6>, ClSmem<4, 6>::THREADS, ClSmem<4, 6>::bytes(a.Hq));
+  if (group == 8 && mt == 4) return run(decode_tc_cluster_kernel<8, 4>, ClSmem<8, 4>::THREADS, ClSmem<8, 4>::bytes(a.Hq));
+  if (group == 8 && mt == 5) return run(decode_tc_cluster_kernel<8, 5>, ClSmem<8, 5>::THREADS, ClSmem<8, 5>::bytes(a.Hq));
   return cudaErrorInvalidValue;
 }
 

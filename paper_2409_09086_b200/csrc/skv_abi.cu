@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -102,6 +103,7 @@ struct skv_ctx {
   bool layers_chain = false;  // the last launch was an all-layer persistent decode step
   int32_t* lay_cnt = nullptr;  // persistent decode: [S*Hkv] segment chunk counters, [L] layers done, [1] exits
   unsigned long long* lay_tl = nullptr;  // instrumentation: persistent decode timeline (skv_layers_timeline)
+  std::map<int, int> cluster_fit;  // (G, chunk tiles, cluster size) -> co-resident clusters
   int launch_seq = 0;   // decode launches (selects the scheduler slot)
   int32_t* sched = nullptr;  // [64][4] per-launch ticket / barrier / exit counters
   int32_t* done = nullptr;   // [64] per-launch completion flags
@@ -866,11 +868,14 @@ int skv_decode_layer(skv_ctx* x, int layer, const void* q, const void* k, const 
   return decode_layer_impl(x, layer, q, k, v, pos_dev, out, record, st);
 }
 
-static int use_layers_kernel() {  // SKV_LAYERS=1 runs all-layer steps in one persistent launch (A/B)
+// All-layer decode steps of latency-bound GQA engines: 1 (default) one
+// persistent launch with a cluster per segment; 0 per-layer launches; 2 the
+// persistent launch with a last-arriver global merge (A/B only)
+static int use_layers_kernel() {
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("SKV_LAYERS");
-    env = e ? atoi(e) : 0;
+    env = e ? atoi(e) : 1;
   }
   return env;
 }
@@ -894,7 +899,42 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   DecodePlan p;
   int rc = prepare_layer(x, 0, q, k, v, nullptr, out, record, st, p);
   if (rc) return rc;
-  if (!p.tc || p.ctas != x->S * x->Hkv * p.nc || p.ctas > sms) return 0;  // every CTA co-resident, one chunk each
+  const int segs = x->S * x->Hkv;
+  // cluster variant (default): one cluster of CS <= 16 CTAs per segment,
+  // chunks of mt = 4 or 5 tiles; all clusters must be co-resident
+  // (the smallest chunk whose cluster of CS <= 16 CTAs per segment fits: a
+  // GPC must hold a whole cluster, and not every GPC has 16 free SMs)
+  int mt = 0, CS = 0;
+  bool cluster = false;
+
+  for (int t = 4; t <= (x->G == 4 ? 6 : 5) && use_layers_kernel() == 1 && !cluster; ++t) {
+    const int cs = (p.nt + t - 1) / t;
+    if (cs > 16 || segs * cs > sms) continue;
+    const int key = (x->G * 8 + t) * 32 + cs;
+    auto it = x->cluster_fit.find(key);
+    if (it == x->cluster_fit.end()) {
+      AttnArgs qa = p.a;
+      qa.nc = cs;
+      qa.ch = t;
+      int maxc = 0;
+      cudaError_t e = launch_decode_tc_cluster(x->G, t, qa, LayerSteps{}, st, &maxc);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        maxc = 0;
+      }
+      if (getenv("SKV_DEBUG_CLUSTER"))
+        fprintf(stderr, "[skv] cluster fit G=%d mt=%d CS=%d segs=%d: %d co-resident clusters (%s)\n", x->G, t, cs,
+                segs, maxc, cudaGetErrorString(e));
+      it = x->cluster_fit.emplace(key, maxc).first;
+    }
+    if (it->second >= segs) {
+      cluster = true;
+      mt = t;
+      CS = cs;
+    }
+  }
+  if (!cluster && (!p.tc || p.ctas != segs * p.nc || p.ctas > sms || use_layers_kernel() != 2))
+    return 0;  // per-layer launches
   if (!x->lay_cnt) {
     cudaError_t e = x->alloc(&x->lay_cnt, ((size_t)x->S * x->Hkv + x->L + 1) * sizeof(int32_t));
     if (e != cudaSuccess) return cuda_fail(e, "layer counters");
@@ -915,7 +955,15 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   ls.exit_count = ls.layer_done + x->L;
   ls.prefetch0 = x->layers_chain ? 1 : 0;
   ls.tl = x->lay_tl;
-  cudaError_t e = launch_decode_tc_layers(x->G, p.ctas, p.a, ls, st);
+  cudaError_t e;
+  if (cluster) {
+    AttnArgs ca = p.a;
+    ca.nc = CS;
+    ca.ch = mt;
+    e = launch_decode_tc_cluster(x->G, mt, ca, ls, st);
+  } else {
+    e = launch_decode_tc_layers(x->G, p.ctas, p.a, ls, st);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "decode (all layers) kernel launch");
   x->launches += 1;
   x->last_layer = -1;

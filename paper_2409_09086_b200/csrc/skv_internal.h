@@ -126,6 +126,11 @@ struct LayerSteps {
   unsigned long long* tl;     // instrumentation (null: off): [L][grid][8] %globaltimer per CTA and layer
 };
 cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st);
+// cluster variant: a.nc (<= 16) CTAs per segment form a cluster, chunks of up
+// to mt (4 or 5) tiles; with max_clusters set, only reports how many such
+// clusters can be co-resident
+cudaError_t launch_decode_tc_cluster(int group, int mt, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st,
+                                     int* max_clusters = nullptr);
 // static-schedule GQA launches (bf16, D = 128, group 4 or 8, chunks <= 4 tiles) on mma.sync
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st);
 // the segment merge alone (PDL), after a decode launch

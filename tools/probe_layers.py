@@ -6,7 +6,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2409_09086_b200 import EngineConfig, StreamEngine
-S, L, Hq, Hkv, D, B, E, W = 1, 32, 32, 8, 128, 4096, 256, 32
+S, L, Hq, Hkv, D, B, E, W = 1, 32, 32, 8, 128, int(os.environ.get("B", 4096)), 256, 32
 eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, B // 2, B // 2, 0.01, W, B + E, torch.bfloat16))
 g = torch.Generator(device="cuda").manual_seed(1)
 for layer in range(L):
@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 a = tl.cpu().numpy()
 P = int((a[0, :, 0] > 0).sum())
 a = a[:, :P]
-names = ["released", "q loaded", "K in", "math done", "published", "merged"]
+names = ["released", "q+K in", "math done", "published", "merged", "-"]
 prev = None
 for l in range(L):
     r0 = a[l, :, 0].min()
