@@ -74,11 +74,13 @@ def _peaks():
     return 6650.0, "fallback"
 
 
+NCU_SUMMARY = "profiles/r2_ncu_summary.json"
+
+
 def _ncu_traffic():
     """DRAM read+write bytes per decode launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "r1_ncu_summary.json")
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, NCU_SUMMARY)) as f:
             return float(json.load(f)["decode_traffic_bytes_per_launch"])
     except Exception:
         return None
@@ -382,27 +384,31 @@ def run_gpu(args, rank: int, world: int):
         vh = v.cpu().pin_memory()
         oh = torch.empty((L, resident, hq, D), dtype=torch.float32).pin_memory()
         torch.cuda.synchronize()
-        steps = min(args.e2e_steps, E, T_in)
-        for t in range(4):  # warm-up of the host pipeline
-            eng.decode_step_host(qh[t], kh[t], vh[t], oh, record=True)
-        evict()
+        steps = E  # one whole eviction period: the engine states (and their cached graphs) repeat
+
+        def host_period():
+            for t in range(steps):
+                eng.decode_step_host(qh[t % T_in], kh[t % T_in], vh[t % T_in], oh, record=t >= steps - W)
+            evict()
+
+        host_period()  # warm-up: one period (captures the per-state host-step graphs)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         tic = time.perf_counter()
-        for t in range(steps):
-            eng.decode_step_host(qh[t], kh[t], vh[t], oh, record=t >= steps - W)
-        evict()
+        host_period()
         torch.cuda.synchronize()
         el = _max_over_ranks(time.perf_counter() - tic, world, dev) * waves
         job_streams = c["streams"] if c["shard"] == "heads" else S * world
         e2e = {
             "value": round(job_streams * steps / el, 2),
             "unit": "tokens/s",
-            "h2d_bytes_per_step": int(qh[0].numel() * 2 + kh[0].numel() * 2 + vh[0].numel() * 2),
-            "d2h_bytes_per_step": int(oh.numel() * 4),
-            "steps": steps,
-            "note": "skv_decode_step_host per token (pinned host q/k/v in, f32 outputs out) + eviction",
+            # a bench step is one period: `steps` tokens, each copying its q/k/v in and its outputs out
+            "h2d_bytes_per_step": int(steps * sum(t[0].numel() * t.element_size() for t in (qh, kh, vh))),
+            "d2h_bytes_per_step": int(steps * oh.numel() * oh.element_size()),
+            "tokens_per_step": steps,
+            "note": "one period through skv_decode_step_host (pinned host q/k/v in, f32 outputs out every token; "
+                    "one CUDA graph per token, cached per engine state) + the eviction, wall clock",
         }
 
     # the one collective outside the hot path: outputs and kept
@@ -443,7 +449,7 @@ def run_gpu(args, rank: int, world: int):
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
                      "traffic": _ncu_traffic() if args.workload == "cfg1" and not args.budget else None,
-                     "traffic_source": "profiles/r1_ncu_summary.json (ncu --set full, dram read+write per launch)",
+                     "traffic_source": NCU_SUMMARY + " (ncu --set full, dram read+write per launch)",
                      "avg_launch_us": round(avg_dec_ms * 1e3, 2), "bytes_per_launch": int(dec_bytes),
                      "evict_ms_per_period": round(evict_ms, 3),
                      "kernel_span_us": round(span_us, 2) if span_us else None,

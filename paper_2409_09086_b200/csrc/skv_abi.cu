@@ -199,6 +199,15 @@ struct skv_ctx {
   void* stage_v = nullptr;
   float* stage_out = nullptr;
   std::vector<void*> allocs;
+  // host-buffer steps captured as graphs, per engine state (host_step_graph)
+  struct HostGraph {
+    Mirror pre, post;
+    int record = 0, last_layer = -1, post_last_layer = -1, launches = 0;
+    bool chain = false, post_chain = false;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t nq = nullptr, nk = nullptr, nv = nullptr, nout = nullptr;
+  };
+  std::vector<HostGraph> hgraphs;
 
   template <typename P>
   cudaError_t alloc(P** p, size_t bytes) {
@@ -401,6 +410,7 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
 int skv_destroy(skv_ctx* x) {
   if (!x) return SKV_OK;
   cudaDeviceSynchronize();
+  for (auto& e : x->hgraphs) cudaGraphExecDestroy(e.exec);
   if (x->exec) cudaGraphExecDestroy(x->exec);
   if (x->graph) cudaGraphDestroy(x->graph);
   for (auto ev : x->ev_in) cudaEventDestroy(ev);
@@ -991,6 +1001,118 @@ int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, flo
   return SKV_OK;
 }
 
+static bool pinned_host(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Host-buffer decode step as one CUDA graph: [H2D q, k, v] -> every layer's
+// decode -> [D2H out].  Graphs are cached per engine state (a steady-state
+// period revisits the same states), and each call only rebinds the four copy
+// nodes to the caller's pinned buffers, so a token costs one graph launch
+// instead of ~3 runtime calls per layer.  Returns 1 when launched on s_c,
+// 0 when not applicable (pageable buffers, SKV_HOST_GRAPHS=0).
+static int host_step_graph(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
+                           cudaStream_t s_c, int64_t qb, int64_t kb, int64_t ob) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("SKV_HOST_GRAPHS");
+    enabled = e ? atoi(e) : 1;
+  }
+  if (!enabled || x->timing) return 0;
+  if (!pinned_host(q) || !pinned_host(k) || !pinned_host(v) || !pinned_host(out)) return 0;
+  const skv_ctx::Mirror pre = x->snap();
+  skv_ctx::HostGraph* hg = nullptr;
+  for (auto& e : x->hgraphs)
+    if (e.record == record && e.last_layer == x->last_layer && e.chain == x->layers_chain && e.pre == pre) {
+      hg = &e;
+      break;
+    }
+  const size_t L = x->L;
+  if (!hg) {
+    if (x->hgraphs.size() >= 1024) {  // bounded cache
+      for (auto& e : x->hgraphs) cudaGraphExecDestroy(e.exec);
+      x->hgraphs.clear();
+    }
+    skv_ctx::HostGraph ng;
+    ng.pre = pre;
+    ng.record = record;
+    ng.last_layer = x->last_layer;
+    ng.chain = x->layers_chain;
+    const int launches0 = (int)x->launches;
+    SKV_CK(cudaStreamBeginCapture(s_c, cudaStreamCaptureModeThreadLocal));
+    int rc = SKV_OK;
+    auto ck = [&](cudaError_t e) {
+      if (rc == SKV_OK && e != cudaSuccess) rc = cuda_fail(e, "host step capture");
+    };
+    ck(cudaMemcpyAsync(x->stage_q, q, qb * L, cudaMemcpyHostToDevice, s_c));
+    ck(cudaMemcpyAsync(x->stage_k, k, kb * L, cudaMemcpyHostToDevice, s_c));
+    ck(cudaMemcpyAsync(x->stage_v, v, kb * L, cudaMemcpyHostToDevice, s_c));
+    for (int l = 0; l < x->L && rc == SKV_OK; ++l)
+      rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb, static_cast<char*>(x->stage_k) + l * kb,
+                             static_cast<char*>(x->stage_v) + l * kb, nullptr, x->stage_out + l * (ob / sizeof(float)),
+                             record, s_c);
+    ck(cudaMemcpyAsync(out, x->stage_out, ob * L, cudaMemcpyDeviceToHost, s_c));
+    cudaGraph_t g = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(s_c, &g);
+    ng.post = x->snap();
+    ng.post_last_layer = x->last_layer;
+    ng.post_chain = x->layers_chain;
+    ng.launches = (int)x->launches - launches0;
+    x->restore(pre);
+    x->last_layer = ng.last_layer;
+    x->layers_chain = ng.chain;
+    x->launches = launches0;
+    if (rc != SKV_OK || ee != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return rc != SKV_OK ? rc : cuda_fail(ee, "host step capture");
+    }
+    // the four copy nodes, recognised by their staging side
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    int found = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nd, &t);
+      if (t != cudaGraphNodeTypeMemcpy) continue;
+      cudaMemcpy3DParms mp{};
+      cudaGraphMemcpyNodeGetParams(nd, &mp);
+      const void* dst = mp.dstPtr.ptr;
+      const void* src = mp.srcPtr.ptr;
+      if (dst == x->stage_q) ng.nq = nd, ++found;
+      else if (dst == x->stage_k) ng.nk = nd, ++found;
+      else if (dst == x->stage_v) ng.nv = nd, ++found;
+      else if (src == x->stage_out) ng.nout = nd, ++found;
+    }
+    cudaError_t ei = found == 4 ? cudaGraphInstantiate(&ng.exec, g, 0) : cudaErrorInvalidValue;
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    x->hgraphs.push_back(ng);
+    hg = &x->hgraphs.back();
+  } else {
+    SKV_CK(cudaGraphExecMemcpyNodeSetParams1D(hg->exec, hg->nq, x->stage_q, q, qb * L, cudaMemcpyHostToDevice));
+    SKV_CK(cudaGraphExecMemcpyNodeSetParams1D(hg->exec, hg->nk, x->stage_k, k, kb * L, cudaMemcpyHostToDevice));
+    SKV_CK(cudaGraphExecMemcpyNodeSetParams1D(hg->exec, hg->nv, x->stage_v, v, kb * L, cudaMemcpyHostToDevice));
+    SKV_CK(cudaGraphExecMemcpyNodeSetParams1D(hg->exec, hg->nout, out, x->stage_out, ob * L, cudaMemcpyDeviceToHost));
+  }
+  SKV_CK(cudaGraphLaunch(hg->exec, s_c));
+  x->restore(hg->post);
+  x->last_layer = hg->post_last_layer;
+  x->layers_chain = hg->post_chain;
+  x->launches += hg->launches;
+  return 1;
+}
+
 int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
                          void* stream) {
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
@@ -1023,6 +1145,14 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
   SKV_CK(cudaEventRecord(x->ev_entry, as_stream(stream)));
   SKV_CK(cudaStreamWaitEvent(s_in, x->ev_entry, 0));
   SKV_CK(cudaStreamWaitEvent(s_c, x->ev_entry, 0));
+  {
+    const int rc = host_step_graph(x, q, k, v, out, record, s_c, qb, kb, ob);
+    if (rc < 0) return rc;
+    if (rc == 1) {
+      SKV_CK(cudaStreamSynchronize(s_c));
+      return check_sticky(x);
+    }
+  }
   // Layers in (up to) four groups: one copy per tensor and group in, one out,
   // so the copies of group i+1 / i-1 overlap group i's kernels while the host
   // issues ~3x fewer runtime calls per token (batch-1 steps are host-bound).

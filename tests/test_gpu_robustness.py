@@ -299,3 +299,38 @@ def test_all_layer_persistent_decode_matches_oracle(G):
                 np.testing.assert_array_equal(eng.positions(s, layer), orc.kv[s][layer].pos[: orc.kv[s][layer].n])
     print(f"persistent G={G}: worst out {worst:.2e} rows {worst_row:.2e}")
     assert worst <= 2e-3 and worst_row <= 2e-3
+
+
+def test_host_step_graph_cache_over_periods():
+    """skv_decode_step_host runs each token as one CUDA graph cached per
+    engine state: over three eviction periods the states repeat (cache hits
+    rebind only the copy nodes to new pinned buffers).  Outputs every token,
+    kept sets every period, against the oracle."""
+    S, L, Hq, Hkv, D = 2, 3, 8, 2, 128
+    l, r, W, E = 32, 32, 8, 16
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = _eng(S, L, Hq, Hkv, D, l, r, W, B + E)
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    rng = np.random.default_rng(77)
+    _inject_both(eng, orc, rng, S, L, Hkv, D, B)
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    worst = 0.0
+    for period in range(3):
+        for t in range(E):
+            q = bf16_round(rng.standard_normal((L, S, Hq, D)).astype(F32))
+            k = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            hq, hk, hv = (torch.from_numpy(a).to(torch.bfloat16).pin_memory() for a in (q, k, v))
+            oh = torch.full((L, S, Hq, D), float("nan"), dtype=torch.float32).pin_memory()
+            eng.decode_step_host(hq, hk, hv, oh, record=t >= E - W)
+            worst = max(worst, rel_err(oh.numpy(), orc.step(q, k, v)))
+        eng.evict(-1, kept)
+        kc = kept.cpu().numpy()
+        for s in range(S):
+            for layer in range(L):
+                ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept, kc[s, layer],
+                                                B + E, cfg)
+                assert ok, (period, s, layer, nbad, gap)
+                orc.apply(s, layer, kc[s, layer].astype(np.int64))
+    assert worst <= 2e-3, worst
