@@ -54,3 +54,17 @@ def copies(i):
     q[0].copy_(qh[i], non_blocking=True); k[0].copy_(kh[i], non_blocking=True); v[0].copy_(vh[i], non_blocking=True)
     oh.copy_(out, non_blocking=True); torch.cuda.synchronize()
 run("copies only + sync", copies)
+
+# ---- where a host step's wall time goes (cfg0 shape)
+import ctypes
+if shape == "cfg0":
+    sh = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    def slices(i):
+        return qh[i % N], kh[i % N], vh[i % N]
+    run("python: three tensor slices", lambda i: slices(i))
+    run("ctypes skv_sync (stream sync)", lambda i: eng.lib.skv_sync(eng._h, sh))
+    args = [ctypes.c_void_p(t.data_ptr()) for t in (qh[0], kh[0], vh[0], oh)]
+    def raw(i):
+        evict_if_full()
+        eng.lib.skv_decode_step_host(eng._h, *args, 1, sh)
+    run("raw ctypes skv_decode_step_host", raw)
