@@ -645,10 +645,11 @@ def run_cfg2(args, rank: int, world: int):
     n0 = B  # every chunk starts from the evicted budget
     flops = 4 * D * (CI * n0 + CI * (CI + 1) / 2) * S * L * H  # useful QK^T + PV flops of the image chunk
     tflops = flops / L / (kern_us * 1e-6) / 1e12
-    peak_tf = 1394.7
+    # the kernel is timed alone (L launches back to back, ~7 ms): the burst peak
+    peak_tf, peak_kind = 1630.4, "fallback burst bf16"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peak_tf = float(json.load(f)["bf16_tflops_sustained"])
+            peak_tf, peak_kind = float(json.load(f)["bf16_tflops"]), "measured burst bf16 (kernel timed alone)"
     except Exception:
         pass
     tokens = S * (CI + CT) * world
@@ -662,7 +663,7 @@ def run_cfg2(args, rank: int, world: int):
                    "l2": "inputs larger than L2 (4 x 32 layers x 4.7K tokens of K/V, 10 GB)",
                    "parallelism": f"stream-partitioned x{world}, no hot-path collective"},
         "roofline": {"bound": "tensor", "kernel": "prefill_kernel (576-query image chunk, one layer, 4 streams x 32 heads)",
-                     "achieved": round(tflops, 1), "peak": peak_tf, "peak_kind": "measured sustained bf16",
+                     "achieved": round(tflops, 1), "peak": peak_tf, "peak_kind": peak_kind,
                      "unit": "TFLOP/s", "frac": round(tflops / peak_tf, 4), "traffic": None,
                      "avg_launch_us": round(kern_us, 1), "useful_tflop_per_launch": round(flops / L / 1e12, 4),
                      "image_chunk_ms": round(img_ms, 3), **phases,
