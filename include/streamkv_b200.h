@@ -297,6 +297,11 @@ int skv_attn_probs(const float* q_dev, const float* keys_dev, int n, int dim, fl
                    void* stream);
 /* weighted_sum (tensorops.py:105-111): out[dim] = probs[n] @ values[n][dim]. */
 int skv_weighted_sum(const float* probs_dev, const float* values_dev, int n, int dim, float* out_dev, void* stream);
+/* aggregate_heads (policies.py:259-265): probs [heads][n] -> out [n]; mode
+ * SKV_AGG_MEAN (sequential f32 head sum / heads) or SKV_AGG_MAX. */
+int skv_aggregate_heads(const float* probs_dev, int heads, int n, int mode, float* out_dev, void* stream);
+/* bias_vector (policies.py:150-162): out [n - recent_len] f32. */
+int skv_bias_vector(int n, int recent_len, float bias, float* out_dev, void* stream);
 /* rope_apply (tensorops.py:38-64): pairs rotated by position * base^(-2i/dim)
  * (angles in float64); synchronous. */
 int skv_rope_apply(const float* v_dev, int dim, int64_t position, double base, float* out_dev, void* stream);

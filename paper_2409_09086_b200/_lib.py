@@ -106,6 +106,8 @@ SIGNATURES = {
     "skv_attn_probs": (_I, [_P, _P, _I, _I, _F, _P, _P]),
     "skv_weighted_sum": (_I, [_P, _P, _I, _I, _P, _P]),
     "skv_rope_apply": (_I, [_P, _I, _I64, ctypes.c_double, _P, _P]),
+    "skv_aggregate_heads": (_I, [_P, _I, _I, _I, _P, _P]),
+    "skv_bias_vector": (_I, [_I, _I, _F, _P, _P]),
     "skv_window_view": (_I, [_P, _I, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I),
                              ctypes.POINTER(_I)]),
     "skv_positions_view": (_I, [_P, _I, _I, ctypes.POINTER(_P)]),

@@ -98,6 +98,27 @@ __global__ void rope_apply_kernel(const float* __restrict__ v, int half, const d
   out[2 * i + 1] = __fadd_rn(__fmul_rn(e, s), __fmul_rn(o, c));
 }
 
+// aggregate_heads (policies.py:259-265): mean = sequential f32 head sum / f32(H)
+// (numpy's axis-0 reduction order), max = elementwise max over heads.
+__global__ void aggregate_heads_kernel(const float* __restrict__ p, int H, int n, int mode, float* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float acc = p[j];
+  for (int h = 1; h < H; ++h) {
+    const float x = p[(int64_t)h * n + j];
+    acc = mode ? fmaxf(acc, x) : __fadd_rn(acc, x);
+  }
+  out[j] = mode ? acc : __fdiv_rn(acc, (float)H);
+}
+
+// bias_vector (policies.py:150-162): d = f32(b) / f32(cols), out[c] = (-d) * f32(cols - 1 - c).
+__global__ void bias_vector_kernel(int cols, float b, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const float d = __fdiv_rn(b, (float)cols);
+  out[c] = __fmul_rn(-d, (float)(cols - 1 - c));
+}
+
 }  // namespace skv
 
 using namespace skv;
@@ -130,6 +151,22 @@ int skv_weighted_sum(const float* probs_dev, const float* values_dev, int n, int
   weighted_sum_kernel<<<(dim + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(probs_dev, values_dev, n,
                                                                                               dim, out_dev);
   return cudaGetLastError() == cudaSuccess ? SKV_OK : tfail(SKV_ECUDA, "weighted_sum kernel launch");
+}
+
+int skv_aggregate_heads(const float* probs_dev, int heads, int n, int mode, float* out_dev, void* stream) {
+  if (heads < 1 || n < 1 || !probs_dev || !out_dev) return tfail(SKV_EINVAL, "per-head block must be non-empty");
+  if (mode != SKV_AGG_MEAN && mode != SKV_AGG_MAX) return tfail(SKV_EINVAL, "unknown head aggregation");
+  aggregate_heads_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(probs_dev, heads, n,
+                                                                                               mode, out_dev);
+  return cudaGetLastError() == cudaSuccess ? SKV_OK : tfail(SKV_ECUDA, "aggregate kernel launch");
+}
+
+int skv_bias_vector(int n, int recent_len, float bias, float* out_dev, void* stream) {
+  if (n <= recent_len) return tfail(SKV_EINVAL, "no scorable columns: n <= l");
+  if (!(bias >= 0.f)) return tfail(SKV_EINVAL, "bias must be >= 0");
+  const int cols = n - recent_len;
+  bias_vector_kernel<<<(cols + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(cols, bias, out_dev);
+  return cudaGetLastError() == cudaSuccess ? SKV_OK : tfail(SKV_ECUDA, "bias kernel launch");
 }
 
 int skv_rope_apply(const float* v_dev, int dim, int64_t position, double base, float* out_dev, void* stream) {

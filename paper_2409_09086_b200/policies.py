@@ -101,50 +101,83 @@ class EvictionDecision:
 
 
 class AttentionWindow:
-    """Rolling buffer of the last ``capacity`` rows (policies.py:87-127), rows on the GPU."""
+    """Rolling buffer of the last ``capacity`` rows (policies.py:87-127).
+
+    The rows live in one device buffer [capacity][width] (width grows with the
+    longest row) used as a ring, with their lengths: a push is one row copy,
+    ``remap`` one gather of every row through the kept set (row i keeps its
+    first #{kept < len_i} entries), and the policy kernels read the buffer
+    oldest-first."""
 
     def __init__(self, capacity: int):
         if capacity < 1:
             raise ValueError("window capacity must be >= 1")
         self.capacity = capacity
-        self._rows: List[torch.Tensor] = []
+        self._buf = None        # [capacity][width] f32 device ring
+        self._lens = []         # lengths, oldest first
+        self._head = 0          # ring slot of the oldest row
         self._host = True
 
     def __len__(self) -> int:
-        return len(self._rows)
+        return len(self._lens)
+
+    def _slot(self, i: int) -> int:
+        return (self._head + i) % self.capacity
 
     @property
     def rows(self):
-        return [r.cpu().numpy() for r in self._rows] if self._host else list(self._rows)
+        out = [self._buf[self._slot(i), :n] for i, n in enumerate(self._lens)]
+        return [r.cpu().numpy() for r in out] if self._host else [r.clone() for r in out]
 
     def push(self, row) -> None:
         r, host = _to_dev_f32(row)
         if r.ndim != 1 or r.numel() == 0:
             raise ValueError("row must be a non-empty vector")
-        if self._rows and r.numel() < self._rows[-1].numel():
+        n = r.numel()
+        if self._lens and n < self._lens[-1]:
             raise ValueError("row column count may not shrink between evictions")
         self._host = host
-        self._rows.append(r.clone())
-        if len(self._rows) > self.capacity:
-            del self._rows[0]
+        if self._buf is None or self._buf.shape[1] < n:
+            grown = torch.zeros((self.capacity, max(n, 2 * (self._buf.shape[1] if self._buf is not None else 0))),
+                                dtype=torch.float32, device="cuda")
+            if self._buf is not None:
+                grown[:, : self._buf.shape[1]] = self._buf
+            self._buf = grown
+        if len(self._lens) == self.capacity:  # drop the oldest
+            self._head = (self._head + 1) % self.capacity
+            self._lens.pop(0)
+        self._buf[self._slot(len(self._lens)), :n] = r
+        self._lens.append(n)
 
     def remap(self, kept) -> None:
+        if not self._lens:
+            return
         idx = torch.as_tensor(np.asarray(kept, dtype=np.int64) if not isinstance(kept, torch.Tensor) else kept)
-        idx = idx.to(device="cuda", dtype=torch.int64)
-        self._rows = [row[idx[idx < row.numel()]] for row in self._rows]
+        idx = idx.to(device="cuda", dtype=torch.int64).reshape(-1)
+        kh = idx.cpu().numpy()
+        new_lens = [int(np.searchsorted(kh, n)) for n in self._lens]  # #{kept < len}, kept ascending
+        width = self._buf.shape[1]
+        gathered = self._buf.index_select(1, idx.clamp(max=width - 1))
+        self._buf = torch.zeros_like(self._buf)
+        self._buf[:, : gathered.shape[1]] = gathered
+        self._lens = new_lens
 
     def clear(self) -> None:
-        self._rows = []
+        self._lens = []
+        self._head = 0
 
     def _packed(self, n: int):
-        m = len(self._rows)
-        width = max(max(r.numel() for r in self._rows), n)
-        buf = torch.zeros((m, width), dtype=torch.float32, device="cuda")
-        lens = torch.empty(m, dtype=torch.int32)
-        for i, r in enumerate(self._rows):
-            buf[i, : r.numel()] = r
-            lens[i] = r.numel()
-        return buf, lens.cuda(), width
+        """Oldest-first [m][width] view (one copy when the ring has wrapped) + lengths."""
+        m = len(self._lens)
+        if self._buf.shape[1] < n:
+            self._buf = torch.nn.functional.pad(self._buf, (0, n - self._buf.shape[1]))
+        order = [self._slot(i) for i in range(m)]
+        if order == list(range(m)):
+            buf = self._buf[:m]
+        else:
+            buf = self._buf.index_select(0, torch.tensor(order, dtype=torch.int64, device="cuda"))
+        lens = torch.tensor(self._lens, dtype=torch.int32, device="cuda")
+        return buf.contiguous(), lens, self._buf.shape[1]
 
 
 def window_mean_scores(window: AttentionWindow, n: int, l: int):
@@ -165,9 +198,10 @@ def bias_vector(n: int, l: int, b: float):
         raise ValueError(f"no scorable columns: n={n} <= l={l}")
     if b < 0:
         raise ValueError("bias must be >= 0")
-    cols = n - l
-    d = F32(b) / F32(cols)
-    return (-d) * np.arange(cols - 1, -1, -1, dtype=F32)
+    _lib.require_cuda()
+    out = torch.empty(n - l, dtype=torch.float32, device="cuda")
+    check(_lib.load().skv_bias_vector(n, l, ctypes.c_float(F32(b)), _p(out), _sh()))
+    return out.cpu().numpy()
 
 
 def top_k_indices(scores, k: int):
@@ -261,9 +295,10 @@ def aggregate_heads(per_head, how: str):
     if how not in (HEAD_AGG_MEAN, HEAD_AGG_MAX):
         raise ValueError(f"unknown head aggregation {how!r}")
     p, host = _to_dev_f32(per_head)
-    if how == HEAD_AGG_MAX:
-        return _out(p.max(dim=0).values, host)
-    acc = p[0].clone()
-    for h in range(1, p.shape[0]):
-        acc += p[h]
-    return _out(acc / F32(p.shape[0]), host)
+    if p.ndim != 2 or p.shape[0] == 0 or p.shape[1] == 0:
+        raise ValueError("per_head must be a non-empty (heads, n) block")
+    p = p.contiguous()
+    out = torch.empty(p.shape[1], dtype=torch.float32, device="cuda")
+    check(_lib.load().skv_aggregate_heads(_p(p), p.shape[0], p.shape[1], 1 if how == HEAD_AGG_MAX else 0, _p(out),
+                                          _sh()))
+    return _out(out, host)

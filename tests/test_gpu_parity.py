@@ -505,3 +505,42 @@ def test_decode_instantiations_vs_oracle(dt, D, G):
                 np.testing.assert_array_equal(eng.positions(s, 0), orc.kv[s][0].pos[: orc.kv[s][0].n])
     print(f"{dt} D={D} G={G}: worst output rel err {worst:.2e}")
     assert worst <= tol_for(dt)
+
+
+def test_dropin_aggregate_bias_and_window_ring():
+    """aggregate_heads / bias_vector on device bit-identical to the reference
+    arithmetic (numpy axis-0 mean with dtype f32, max; (-d) * f32 ages), and
+    the device AttentionWindow ring (wrap, remap) against the oracle window."""
+    from oracle.streamkv_oracle import age_bias, head_mean, window_scores
+    from paper_2409_09086_b200 import AttentionWindow, aggregate_heads, bias_vector, window_mean_scores
+
+    rng = np.random.default_rng(31)
+    for _ in range(20):
+        H, n = int(rng.integers(1, 40)), int(rng.integers(1, 3000))
+        p = rng.random((H, n)).astype(F32)
+        np.testing.assert_array_equal(aggregate_heads(p, "mean"), head_mean(p, "mean"))
+        np.testing.assert_array_equal(aggregate_heads(p, "max"), head_mean(p, "max"))
+        l = int(rng.integers(0, n)) if n > 1 else 0
+        if n > l:
+            b = float(rng.choice([0.0, 0.01, 0.5, 1.0]))
+            np.testing.assert_array_equal(bias_vector(n, l, b), age_bias(n, l, b))
+    for _ in range(10):
+        cap = int(rng.integers(1, 8))
+        w, ref = AttentionWindow(cap), RowWindow(cap)
+        n = int(rng.integers(4, 50))
+        for step in range(int(rng.integers(1, 25))):
+            n += int(rng.integers(0, 3))
+            row = rng.dirichlet(np.ones(n)).astype(F32)
+            w.push(row)
+            ref.push(row)
+            if rng.random() < 0.2 and n > 3:
+                kept = np.sort(rng.choice(n, size=int(rng.integers(1, n)), replace=False))
+                w.remap(kept)
+                ref.remap(kept)
+                n = kept.size
+        assert [a.size for a in w.rows] == [b.size for b in ref.rows]
+        for a, b_ in zip(w.rows, ref.rows):
+            np.testing.assert_array_equal(a, b_)
+        nn = max(r.size for r in ref.rows)
+        if nn > 1:
+            np.testing.assert_array_equal(window_mean_scores(w, nn, 1), window_scores(ref, nn, 1))
