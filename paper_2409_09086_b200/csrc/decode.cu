@@ -207,10 +207,28 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
       // then the last chunks (the short remainder chunk, and the one holding
       // the appended token, which waits for the previous launch): the launch
       // ends on the smallest work and no producer stalls on the release early.
-      const int nce = a.nc - 1, early = a.S * a.Hkv * nce;
+      // With a.late = DL > 0, segment sigma's last chunk is handed out right
+      // after segment sigma + DL's other chunks instead (DL segments ~ one
+      // ticket per CTA later: past the release), so most segments complete --
+      // and merge -- while later segments still stream, not all at the end.
+      const int nce = a.nc - 1, segs = a.S * a.Hkv, early = segs * nce;
+      const int DL = a.late > 0 && a.late < segs && nce > 0 ? a.late : 0;
       auto slot_of = [&](int t) {  // ticket -> chunk slot sigma * nc + j
         if (a.stat || t >= total) return t;
-        return t < early ? (t / nce) * a.nc + (t % nce) : (t - early) * a.nc + nce;
+        if (DL == 0) return t < early ? (t / nce) * a.nc + (t % nce) : (t - early) * a.nc + nce;
+        // blocks: sigma's nce early chunks, then (sigma >= DL) the last chunk of sigma - DL
+        const int bD = DL * nce;                         // start of block DL
+        const int bEnd = segs * nce + (segs - DL);       // after the last block
+        if (t >= bEnd) return (segs - DL + (t - bEnd)) * a.nc + nce;  // remaining last chunks
+        int sg, off;
+        if (t < bD) {
+          sg = t / nce;
+          off = t - sg * nce;
+        } else {
+          sg = DL + (t - bD) / (nce + 1);
+          off = (t - bD) - (sg - DL) * (nce + 1);
+        }
+        return off < nce ? sg * a.nc + off : (sg - DL) * a.nc + nce;
       };
       u = slot_of(u);
       while (u < total) {

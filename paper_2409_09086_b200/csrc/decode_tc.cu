@@ -109,6 +109,17 @@ struct Smem {
   static constexpr size_t bytes = tiles + slot_floats * 4 + 64 + 1024 + 8 * 1024;  // + bars, align, fold stats
 };
 
+// decode_tc_kernel's shared memory for chunks of MT tiles (2 MT consumer warps);
+// Hq query heads' fold stats
+template <int G, int MT>
+struct SmemT {
+  static constexpr int NWK = 2 * MT;
+  static constexpr int THREADS = NWK * 32 + 96;
+  static constexpr size_t tiles = (size_t)2 * MT * TILE;
+  static constexpr size_t slot_floats = 4 + 2 * NWK * G + NWK * G * D;
+  static size_t bytes(int Hq) { return tiles + slot_floats * 4 + 64 + 1024 + (size_t)Hq * 8; }
+};
+
 }  // namespace tcd
 
 namespace tcd {
@@ -204,17 +215,19 @@ __device__ __forceinline__ void warp_pv(const float (&p)[4][2], uint32_t vbase, 
 
 // One CTA = chunk blockIdx.x (static schedule): segment sigma = c / nc,
 // tiles [j*ch, min((j+1)*ch, nt)).
-template <int G>
-__global__ void __launch_bounds__(tcd::THREADS, 1)
+template <int G, int MT>
+__global__ void __launch_bounds__(tcd::SmemT<G, MT>::THREADS, (MT <= 2 ? 3 : 1))
     decode_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                      const AttnArgs a) {
   using namespace tcd;
+  constexpr int MAXT = MT, NW = 2 * MT, CT = NW * 32;  // chunk tiles, consumer warps / threads
+  using Smem = tcd::SmemT<G, MT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* ktiles = smem;
   unsigned char* vtiles = smem + MAXT * TILE;
-  float* slot = reinterpret_cast<float*>(smem + Smem<G>::tiles);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(slot + Smem<G>::slot_floats);
+  float* slot = reinterpret_cast<float*>(smem + Smem::tiles);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slot + Smem::slot_floats);
   uint64_t* full = bars;      // TMA of every tile
   uint64_t* row_ok = bars + 1;  // appended row written (chunks that hold it)
   float* fstats = reinterpret_cast<float*>(bars + 4);  // fold warp: [Hq][2]
@@ -340,7 +353,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       wl[warp * G + gid] = l;
     }
   }
-  consumers_sync();
+  bar_sync_n(1, CT);
   if (a.ctat && tid == 0) a.ctat[8 * c + 3] = gtimer();
   // ---- merge the warp partials in warp order and publish the chunk partial
   // KvCache.append: the segment's last chunk stores the new row and its
@@ -371,7 +384,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       part[h * PW + D + 1] = xs[0];
     }
   }
-  consumers_sync();
+  bar_sync_n(1, CT);
   if (tid == 0) {
     red_release_add(&a.counters[sigma], 1);
     if (a.tstamp) atomicMax(&a.tstamp[1], gtimer());
@@ -1037,36 +1050,35 @@ cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_
   const CUtensorMap& vmap = m->v;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(tcd::THREADS);
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  if (group == 4) {
-    static DevOnce attr;
+  static DevOnce attr_set[9][5];
+  auto run = [&](auto kern, int threads, size_t smem_bytes, DevOnce& attr) -> cudaError_t {
     if (!attr.here()) {
-      e = cudaFuncSetAttribute(decode_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)tcd::Smem<4>::bytes);
-      if (e != cudaSuccess) return e;
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+      if (r != cudaSuccess) return r;
       attr.here() = true;
     }
-    cfg.dynamicSmemBytes = tcd::Smem<4>::bytes;
-    e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<4>, kmap, vmap, a);
-  } else if (group == 8) {
-    static DevOnce attr;
-    if (!attr.here()) {
-      e = cudaFuncSetAttribute(decode_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)tcd::Smem<8>::bytes);
-      if (e != cudaSuccess) return e;
-      attr.here() = true;
-    }
-    cfg.dynamicSmemBytes = tcd::Smem<8>::bytes;
-    e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<8>, kmap, vmap, a);
-  } else {
-    return cudaErrorInvalidValue;
-  }
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    return cudaLaunchKernelEx(&cfg, kern, kmap, vmap, a);
+  };
+  const int mt = a.ch <= 2 ? 2 : 4;
+#define SKV_TC_CASE(GG, MM)                                                                                  \
+  if (group == GG && mt == MM)                                                                              \
+    e = run(decode_tc_kernel<GG, MM>, tcd::SmemT<GG, MM>::THREADS, tcd::SmemT<GG, MM>::bytes(MM == 4 ? 1024 : a.Hq), \
+            attr_set[GG][MM]);
+  e = cudaErrorInvalidValue;
+  SKV_TC_CASE(1, 2)
+  SKV_TC_CASE(2, 2)
+  SKV_TC_CASE(4, 2)
+  SKV_TC_CASE(4, 4)
+  SKV_TC_CASE(8, 4)
+#undef SKV_TC_CASE
   if (e != cudaSuccess) return e;
   return launch_merge(128, group, a, st);
 }

@@ -64,6 +64,25 @@ static int use_tc_decode() {  // SKV_TC_DECODE=0 keeps GQA small batches on the 
   }
   return env;
 }
+// Segments between a segment's early chunks and its last chunk in the dynamic
+// ticket order (SKV_LAST_DELAY: -1 automatic = one ticket per CTA later, 0 = all
+// last chunks at the end of the launch, > 0 explicit).
+static int last_delay_env() {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("SKV_LAST_DELAY");
+    env = e ? atoi(e) : 0;
+  }
+  return env;
+}
+static int use_tc_wide() {  // SKV_TC_WIDE=1: throughput launches on the tensor-core chunk kernel
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_TC_WIDE");
+    env = e ? atoi(e) : 0;
+  }
+  return env;
+}
 static int ctas_per_sm_override() {
   const char* e = getenv("SKV_CTAS_PER_SM");
   return e ? std::max(1, atoi(e)) : 0;
@@ -545,6 +564,8 @@ static void fold_target(skv_ctx* x, int layer, int slot, FoldArgs& f) {
   }
 }
 
+static int last_delay(const skv_ctx* x, int ctas, int nc);
+
 // A decode launch's schedule and arguments for one layer (no kernel of the
 // attention itself is launched here; RoPE rotation of q / new k is).
 struct DecodePlan {
@@ -581,8 +602,15 @@ static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, co
   const bool stat = (int64_t)segs * ((nt + ch - 1) / ch) <= x->max_ctas && (nt + ch - 1) / ch <= kMaxChunks &&
                     !chunk_tiles_forced();
   if (!stat) ch = std::max(chunk_tiles(x->G), (nt + kMaxChunks - 1) / kMaxChunks);
+  // Throughput launches on the tensor cores (SKV_TC_WIDE): one 2-tile chunk per
+  // CTA, three CTAs per SM, as many waves as chunks -- mma.sync does a tile's
+  // dot products and P.V in a fraction of the CUDA-core instructions, so the
+  // launch stays HBM-bound when the SM clock drops (power cap)
+  const bool wide = !stat && use_tc_wide() && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 &&
+                    (x->G == 1 || x->G == 2 || x->G == 4) && (nt + 1) / 2 <= kMaxChunks && !chunk_tiles_forced();
+  if (wide) ch = 2;
   const int nc = (nt + ch - 1) / ch;
-  const int ctas = std::min(segs * nc, x->max_ctas);
+  const int ctas = wide ? segs * nc : std::min(segs * nc, x->max_ctas);
   const void* kraw_in = nullptr;
   if (x->cfg.rope_mode != SKV_ROPE_NONE) {
     // rotate q and the new k at the token's position (engine.py:265-268)
@@ -616,9 +644,10 @@ static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, co
   a.nt = nt;
   a.ch = ch;
   a.qpf = q_prefetch();
+  a.late = last_delay(x, ctas, nc);
   a.nc = nc;
   a.S = x->S;
-  a.stat = stat;
+  a.stat = stat || wide;
   const int seq = x->launch_seq++;
   a.sched = x->sched + 4 * (seq % 64);
   a.prefetch = x->last_layer >= 0 && x->last_layer != layer;
@@ -691,8 +720,8 @@ static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, co
   plan.nc = nc;
   plan.ctas = ctas;
   plan.par = par;
-  plan.stat = stat;
-  plan.tc = stat && x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && ch <= 4 && use_tc_decode();
+  plan.stat = stat || wide;
+  plan.tc = wide || (stat && x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && ch <= 4 && use_tc_decode());
   if (plan.tc) {
     plan.a.L = x->L;
     plan.a.layer = layer;
@@ -705,6 +734,12 @@ static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, co
 }
 
 // Host mirror after a decode of `layer` (uniform over the streams).
+static int last_delay(const skv_ctx* x, int ctas, int nc) {
+  const int env = last_delay_env();
+  if (env >= 0) return env;
+  return nc > 1 ? (ctas + nc - 2) / (nc - 1) : 0;  // ~one ticket per CTA
+}
+
 static void commit_layer(skv_ctx* x, int layer, const DecodePlan& p) {
   x->pend_n[layer] = 0;
   if (p.record) {

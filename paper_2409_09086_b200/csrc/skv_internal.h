@@ -64,6 +64,7 @@ struct AttnArgs {
   int dctas;            // decode grid size (the merge waits for this many finished CTAs)
   int prefetch;         // producer may stream cached K/V before griddepcontrol.wait
   int qpf;              // consumers prefetch the next chunk's q
+  int late;             // dynamic schedule: hand out a segment's last chunk `late` segments later (0: all at the end)
   float scale;          // f32(1/sqrt(D)), engine.py:150
   void* kc;             // K store base (written for the appended row)
   void* vc;
