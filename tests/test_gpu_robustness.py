@@ -334,3 +334,72 @@ def test_host_step_graph_cache_over_periods():
                 assert ok, (period, s, layer, nbad, gap)
                 orc.apply(s, layer, kc[s, layer].astype(np.int64))
     assert worst <= 2e-3, worst
+
+
+def test_adversarial_kept_sets_dense_compaction_vs_torch_gather():
+    """K3's in-place stable compaction (skv_gather_rows / KvCache.gather_keep)
+    on adversarial kept sets -- everything but the first row, every other
+    row, only the last row, a single gap, runs of holes, random -- against a
+    torch gather of the same rows (stands in for compute-sanitizer, which the
+    GPU pool does not allow)."""
+    import ctypes
+
+    from paper_2409_09086_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(8)
+    H, n, D = 8, 3000, 128
+    for name, kept in [
+        ("drop-first", np.arange(1, n)),
+        ("every-other", np.arange(0, n, 2)),
+        ("last-only", np.array([n - 1])),
+        ("single-gap", np.delete(np.arange(n), n // 2)),
+        ("runs", np.concatenate([np.arange(i, i + 7) for i in range(0, n - 7, 19)])),
+        ("random", np.sort(rng.choice(n, size=n // 3, replace=False))),
+        ("identity", np.arange(n)),
+    ]:
+        for dt in (torch.bfloat16, torch.float32):
+            x = torch.randn((H, n, D), device="cuda").to(dt)
+            ref = x[:, torch.from_numpy(kept).cuda()].clone()
+            kd = torch.from_numpy(kept.astype(np.int64)).cuda()
+            row_bytes = D * x.element_size()
+            _lib.check(lib.skv_gather_rows(ctypes.c_void_p(x.data_ptr()), n * row_bytes, H, row_bytes,
+                                           ctypes.c_void_p(kd.data_ptr()), kept.size,
+                                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            assert torch.equal(x[:, : kept.size], ref), (name, dt)
+
+
+def test_full_size_config1_period_is_deterministic():
+    """Config 1 at full size: the same period replayed from the same state twice
+    gives bit-identical outputs, kept sets, slot maps and caches (the split-KV
+    merge combines chunk partials in chunk order, whatever the ticket order)."""
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    S, L, H, D, l, r, W, E = 8, 32, 32, 128, 1024, 1024, 32, 128
+    B = l + r
+    results = []
+    for rep in range(2):
+        eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, 0.01, W, B + E, torch.bfloat16))
+        g = torch.Generator(device="cuda").manual_seed(99)
+        for s in range(S):
+            for layer in range(L):
+                kf, vf = eng.kv_full(s, layer)
+                kf[:, :B] = torch.randn((H, B, D), generator=g, device="cuda").to(torch.bfloat16)
+                vf[:, :B] = torch.randn((H, B, D), generator=g, device="cuda").to(torch.bfloat16)
+                eng.lib.skv_state_inject(eng._h, s, layer, B, None, None, None, 0, None, None)
+        q = torch.randn((E, L, S, H, D), generator=g, device="cuda").to(torch.bfloat16)
+        k = torch.randn((E, L, S, H, D), generator=g, device="cuda").to(torch.bfloat16)
+        v = torch.randn((E, L, S, H, D), generator=g, device="cuda").to(torch.bfloat16)
+        out = torch.empty((L, S, H, D), dtype=torch.float32, device="cuda")
+        outs = []
+        for t in range(E):
+            eng.decode_step(q[t], k[t], v[t], out, record=t >= E - W)
+            outs.append(out[:, :2].clone())
+        kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+        eng.evict(-1, kept)
+        torch.cuda.synchronize()
+        results.append((torch.stack(outs).cpu(), kept.cpu(), eng.slot_map(3, 17).cpu(),
+                         eng.kv(5, 9)[0].cpu(), eng.kv(0, 31)[1].cpu()))
+        eng.close()
+    for a_, b_ in zip(*results):
+        assert torch.equal(a_, b_)
