@@ -124,88 +124,138 @@ struct SmemT {
 
 namespace tcd {
 
-// One consumer warp's 32 keys [wk0, wk0 + 32) of the chunk in shared memory:
-// S = Q K^T for 4 n-tiles of 8 keys (mma.m16n8k16, B fragments by ldmatrix
-// from the swizzled tile), then the softmax over the warp's keys (row gid =
-// query head): p = exp2((x - m) log2e), row max m and sum l.  Recorded steps
-// store the raw logits x = s * scale to lgrow (null: not recorded).
-__device__ __forceinline__ void warp_scores(const uint32_t (&qa)[8][2], uint32_t kbase, int wk0, int lane, int k0,
-                                            int kend, float scale, float* lgrow, float (&p)[4][2], float& m,
-                                            float& l) {
-  const int tig = lane & 3;
-  float sacc[4][4];
+// D = A(16x16) . B(16x8) + D, bf16 inputs, f32 accumulate (all four A registers)
+__device__ __forceinline__ void mma16816_a4(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                            uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Transpose of an 8x8 b16 matrix held in the accumulator layout (row lane/4,
+// columns 2(lane%4), +1) into the same layout.
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// One consumer warp's 32 keys [wk0, wk0 + 32) of the chunk in shared memory,
+// keys along the MMA's M dimension and the group's query heads along N (8
+// columns: G of them real), so no MMA row is padding:
+//   S^T (16 keys x 8 heads) = K (16 keys x 16 dims, ldmatrix from the swizzled
+//   tile) . Q^T (16 dims x 8 heads, the q fragments qb, fixed for the launch),
+// then the softmax over the warp's keys per head: p = exp2((x - m) log2e), head
+// max m and sum l.  Lane (gid, tig) holds keys wk0 + 16 mt + gid (+8) of heads
+// 2 tig, 2 tig + 1 (m[e], l[e] for head 2 tig + e).  Recorded steps store the
+// raw logits x = s * scale to lg + head * lg_hs (null: not recorded).
+__device__ __forceinline__ void warp_scores(const uint32_t (&qb)[8][2], uint32_t kbase, int wk0, int lane, int k0,
+                                            int kend, float scale, float* lg, int64_t lg_hs, int G, float (&p)[2][4],
+                                            float (&m)[2], float (&l)[2]) {
+  const int gid = lane >> 2, tig = lane & 3;
+  float sacc[2][4];
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-    const int kk = wk0 + nt * 8 + (lane & 7);  // key row this lane addresses
+  for (int mt = 0; mt < 2; ++mt) {
+    sacc[mt][0] = sacc[mt][1] = sacc[mt][2] = sacc[mt][3] = 0.f;
+    const int kk = wk0 + 16 * mt + (lane & 7) + 8 * ((lane >> 3) & 1);  // key row this lane addresses
     const int t = kk >> 6, r = kk & 63;
 #pragma unroll
-    for (int ks2 = 0; ks2 < 4; ++ks2) {  // two k-steps (32 dims) per ldmatrix.x4
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(kbase + t * TILE + swz(r, 4 * ks2 + (lane >> 3)), b0, b1, b2, b3);
-      mma16816(sacc[nt], qa[2 * ks2][0], qa[2 * ks2][1], b0, b1);
-      mma16816(sacc[nt], qa[2 * ks2 + 1][0], qa[2 * ks2 + 1][1], b2, b3);
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(kbase + t * TILE + swz(r, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+      mma16816_a4(sacc[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
     }
   }
-  // ---- softmax over the warp's 32 keys (row gid): logits x = s * scale
-  float x[4][2];
-  float mx = -INFINITY;
+  float x[2][4];
+  float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int key = k0 + wk0 + 16 * mt + gid + (c >> 1) * 8;
+      x[mt][c] = key < kend ? sacc[mt][c] * scale : -INFINITY;
+      mx[c & 1] = fmaxf(mx[c & 1], x[mt][c]);
+    }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+#pragma unroll
+    for (int sh = 4; sh < 32; sh <<= 1) mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], sh));
+    m[e] = mx[e];
+  }
+  float ls[2] = {0.f, 0.f};
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      p[mt][c] = m[c & 1] == -INFINITY ? 0.f : fast_exp2((x[mt][c] - m[c & 1]) * kLog2e);
+      ls[c & 1] += p[mt][c];
+    }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+#pragma unroll
+    for (int sh = 4; sh < 32; sh <<= 1) ls[e] += __shfl_xor_sync(0xffffffffu, ls[e], sh);
+    l[e] = ls[e];
+  }
+  if (lg) {  // recorded steps: raw f32 logits for the window fold
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
-      x[nt][e] = key < kend ? sacc[nt][e] * scale : -INFINITY;
-      mx = fmaxf(mx, x[nt][e]);
+      const int h = 2 * tig + e;
+      if (h >= G) continue;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          const int key = k0 + wk0 + 16 * mt + gid + 8 * hi;
+          if (key < kend) lg[h * lg_hs + key] = x[mt][2 * hi + e];
+        }
     }
-  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-  m = mx;
-  float ls = 0.f;
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      p[nt][e] = m == -INFINITY ? 0.f : fast_exp2((x[nt][e] - m) * kLog2e);
-      ls += p[nt][e];
-    }
-  ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-  ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-  l = ls;
-  if (lgrow) {  // recorded steps: raw f32 logits for the window fold
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int key = k0 + wk0 + nt * 8 + 2 * tig + e;
-        if (key < kend) lgrow[key] = x[nt][e];
-      }
   }
 }
 
-// O += P V over the warp's 32 keys: k-steps of 16 keys, P from the S
-// accumulators as two bf16 terms (hi + lo), V fragments by ldmatrix.trans.
-__device__ __forceinline__ void warp_pv(const float (&p)[4][2], uint32_t vbase, int wk0, int lane,
-                                        float (&o)[16][4]) {
+// O^T (16 dims x 8 heads) += V^T (16 dims x 16 keys, ldmatrix.trans) . P^T
+// (16 keys x 8 heads) over the warp's 32 keys: P^T fragments are the score
+// accumulators transposed in registers (movmatrix), as two bf16 terms (hi + lo).
+// Lane (gid, tig) holds o[md] = dims 16 md + gid (c 0, 1) and + 8 (c 2, 3) of
+// heads 2 tig + (c & 1).
+__device__ __forceinline__ void warp_pv(const float (&p)[2][4], uint32_t vbase, int wk0, int lane, float (&o)[8][4]) {
 #pragma unroll
   for (int kq = 0; kq < 2; ++kq) {
-    const uint32_t ah0 = pack_bf16(p[2 * kq][0], p[2 * kq][1]);
-    const uint32_t ah2 = pack_bf16(p[2 * kq + 1][0], p[2 * kq + 1][1]);
-    const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah0));
-    const float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ah2));
-    const uint32_t al0 = pack_bf16(p[2 * kq][0] - h0.x, p[2 * kq][1] - h0.y);
-    const uint32_t al2 = pack_bf16(p[2 * kq + 1][0] - h2.x, p[2 * kq + 1][1] - h2.y);
-    // lane's ldmatrix.trans row: key 16kq + 8*(matrix & 1) + (lane & 7), dim chunk nb/8 + (matrix >> 1)
-    const int kk = wk0 + 16 * kq + 8 * ((lane >> 3) & 1) + (lane & 7);
+    const uint32_t h0 = pack_bf16(p[kq][0], p[kq][1]), h1 = pack_bf16(p[kq][2], p[kq][3]);
+    const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h0));
+    const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h1));
+    const uint32_t l0 = pack_bf16(p[kq][0] - f0.x, p[kq][1] - f0.y), l1 = pack_bf16(p[kq][2] - f1.x, p[kq][3] - f1.y);
+    const uint32_t bh0 = movtrans(h0), bh1 = movtrans(h1), bl0 = movtrans(l0), bl1 = movtrans(l1);
+    // lane's ldmatrix.trans row: key 16 kq + (lane & 7) + 8 (lane >> 4), dim chunk 2 md + ((lane >> 3) & 1)
+    const int kk = wk0 + 16 * kq + (lane & 7) + 8 * (lane >> 4);
     const int t = kk >> 6, r = kk & 63;
 #pragma unroll
-    for (int np = 0; np < 8; ++np) {  // pairs of n-tiles (16 dims)
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(vbase + t * TILE + swz(r, 2 * np + (lane >> 4)), b0, b1, b2, b3);
-      mma16816(o[2 * np], ah0, ah2, b0, b1);
-      mma16816(o[2 * np], al0, al2, b0, b1);
-      mma16816(o[2 * np + 1], ah0, ah2, b2, b3);
-      mma16816(o[2 * np + 1], al0, al2, b2, b3);
+    for (int md = 0; md < 8; ++md) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4_t(vbase + t * TILE + swz(r, 2 * md + ((lane >> 3) & 1)), a0, a1, a2, a3);
+      mma16816_a4(o[md], a0, a1, a2, a3, bh0, bh1);
+      mma16816_a4(o[md], a0, a1, a2, a3, bl0, bl1);
+    }
+  }
+}
+
+// The warp's partial into shared memory: wo[h][D] (h < G), wm[h], wl[h].
+__device__ __forceinline__ void warp_stage(const float (&o)[8][4], const float (&m)[2], const float (&l)[2], int lane,
+                                           int G, float* wo, float* wm, float* wl) {
+  const int gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int h = 2 * tig + e;
+    if (h >= G) continue;
+#pragma unroll
+    for (int md = 0; md < 8; ++md) {
+      wo[h * D + 16 * md + gid] = o[md][e];
+      wo[h * D + 16 * md + gid + 8] = o[md][2 + e];
+    }
+    if (gid == 0) {
+      wm[h] = m[e];
+      wl[h] = l[e];
     }
   }
 }
@@ -223,7 +273,8 @@ __global__ void __launch_bounds__(tcd::SmemT<G, MT>::THREADS, (MT <= 2 ? 3 : 1))
   constexpr int MAXT = MT, NW = 2 * MT, CT = NW * 32;  // chunk tiles, consumer warps / threads
   using Smem = tcd::SmemT<G, MT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align up by offset from the array (keeps the shared state space: LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   unsigned char* ktiles = smem;
   unsigned char* vtiles = smem + MAXT * TILE;
   float* slot = reinterpret_cast<float*>(smem + Smem::tiles);
@@ -330,29 +381,21 @@ __global__ void __launch_bounds__(tcd::SmemT<G, MT>::THREADS, (MT <= 2 ? 3 : 1))
 
   const int wk0 = warp * 32;  // this warp's keys [wk0, wk0 + 32) of the chunk
   const uint32_t kbase = smem_u32(ktiles), vbase = smem_u32(vtiles);
-  float m = -INFINITY, l = 0.f;
-  float o[16][4];
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  float o[8][4];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float* lgrow = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs : nullptr;
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float* lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
   if (wk0 < ntile * TT) {
-    float p[4][2];
-    warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, real ? lgrow : nullptr, p, m, l);
+    float p[2][4];
+    warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, lg, a.l_hs, G, p, m, l);
     warp_pv(p, vbase, wk0, lane, o);
   }
   // ---- warp partials to the slot: wm[NW][G], wl[NW][G], wo[NW][G][D]
   float* wm = slot + 4;
   float* wl = wm + NW * G;
   float* wo = wl + NW * G;
-  if (real) {
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt)
-      *reinterpret_cast<float2*>(wo + (warp * G + gid) * D + 8 * nt + 2 * tig) = make_float2(o[nt][0], o[nt][1]);
-    if (tig == 0) {
-      wm[warp * G + gid] = m;
-      wl[warp * G + gid] = l;
-    }
-  }
+  warp_stage(o, m, l, lane, G, wo + warp * G * D, wm + warp * G, wl + warp * G);
   bar_sync_n(1, CT);
   if (a.ctat && tid == 0) a.ctat[8 * c + 3] = gtimer();
   // ---- merge the warp partials in warp order and publish the chunk partial
@@ -411,7 +454,8 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
                             const AttnArgs a, const LayerSteps ls) {
   using namespace tcd;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align up by offset from the array (keeps the shared state space: LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   unsigned char* ktiles = smem;
   unsigned char* vtiles = smem + MAXT * TILE;
   float* slot = reinterpret_cast<float*>(smem + Smem<G>::tiles);
@@ -522,7 +566,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
         }
       consumers_sync();
     }
-    unsigned long long* tl = ls.tl ? ls.tl + ((int64_t)l * gridDim.x + c) * 8 : nullptr;
+    unsigned long long* tl = ls.tl && c < 148 ? ls.tl + ((int64_t)l * 148 + c) * 8 : nullptr;
     if (tl && tid == 0) tl[0] = gtimer();  // released
     const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
     uint32_t qa[8][2];
@@ -551,15 +595,14 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
       }
       consumers_sync();
     }
-    float m = -INFINITY, lsum = 0.f;
-    float o[16][4];
+    float m[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
+    float o[8][4];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float* lgrow = a.logits ? a.logits + l * ls.lg_ls + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs
-                            : nullptr;
-    float p[4][2];
+    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float* lg = a.logits ? a.logits + l * ls.lg_ls + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+    float p[2][4];
     const bool active = wk0 < ntile * TT;
-    if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, real ? lgrow : nullptr, p, m, lsum);
+    if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, lg, a.l_hs, G, p, m, lsum);
     __syncwarp();
     if (lane == 0) mbar_arrive(kfree);
     mbar_wait(vfull, ph);
@@ -568,15 +611,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
     if (lane == 0) mbar_arrive(vfree);
     if (tl && tid == 0) tl[3] = gtimer();  // warp 0 math done
     // ---- warp partials -> chunk partial (decode_tc_kernel's order)
-    if (real) {
-#pragma unroll
-      for (int nt = 0; nt < 16; ++nt)
-        *reinterpret_cast<float2*>(wo + (warp * G + gid) * D + 8 * nt + 2 * tig) = make_float2(o[nt][0], o[nt][1]);
-      if (tig == 0) {
-        wm[warp * G + gid] = m;
-        wl[warp * G + gid] = lsum;
-      }
-    }
+    warp_stage(o, m, lsum, lane, G, wo + warp * G * D, wm + warp * G, wl + warp * G);
     consumers_sync();
     if (a.append && j == a.nc - 1) {
       AttnArgs al = a;  // layer l's cache rows and token metadata
@@ -708,12 +743,24 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
 template <int G, int MT>
 struct ClSmem {
   static constexpr int NWC = 2 * MT;                        // consumer warps (32 keys each)
-  static constexpr int THREADS = NWC * 32 + 96;             // + producer, fold, spare warps
+  static constexpr int THREADS = NWC * 32 + 64;             // + producer and fold warps
   static constexpr size_t tiles = (size_t)2 * MT * tcd::TILE;
-  static constexpr size_t slot_floats = 4 + 2 * NWC * G + NWC * G * tcd::D;
-  static constexpr size_t cpart_floats = 2 * G * tcd::PW;  // [parity][G][D + 2]
-  // + barriers, 1024-byte alignment slack and the fold warp's (M, 1/L) per query head
-  static size_t bytes(int Hq) { return tiles + (slot_floats + cpart_floats) * 4 + 128 + 1024 + (size_t)Hq * 8; }
+  // Each warp's partial (o [G][D], then m [G], l [G]) is staged in the K rows it
+  // alone has just scored (its 32 rows: 4 KB in each half of the swizzled tile),
+  // so no shared memory is set aside for it.
+  static_assert(G * tcd::D * 4 <= 4096, "warp partial must fit the warp's consumed K rows");
+  // receive buffer (one: layer l+1's pushes follow every rank's layer-l merge):
+  // [CS][per] chunk-partial values of the elements this rank owns, then
+  // [CS][G][2] every rank's (m, l) per head
+  __host__ __device__ static int per(int cs) { return ((G * tcd::D + cs - 1) / cs + 3) / 4 * 4; }
+  __host__ __device__ static int recv_floats(int cs) { return cs * per(cs) + 2 * G * cs; }
+  __device__ static uint32_t recv_bytes(int cs, int rank) {
+    const int cnt = max(0, min(per(cs), G * tcd::D - rank * per(cs)));
+    return (uint32_t)(cs * cnt + cs * G * 2) * 4;
+  }
+  // tiles + receive buffer + barriers + the fold warp's (M, 1/L) per query head;
+  // the launcher adds up to 1 KB of alignment slack where the SM has room
+  __host__ __device__ static size_t bytes(int Hq, int cs) { return tiles + (size_t)recv_floats(cs) * 4 + 128 + (size_t)Hq * 8; }
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -731,8 +778,17 @@ __device__ __forceinline__ float ld_cluster(uint32_t addr) {
   asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ void arrive_remote(uint32_t remote_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote_bar) : "memory");
+// Asynchronous stores into a cluster peer's shared memory, completing bytes
+// on that peer's mbarrier (visible to it once the barrier phase completes).
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(raddr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, float x, float y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr), "f"(x),
+               "f"(y), "r"(rbar)
+               : "memory");
 }
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -757,20 +813,28 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
   using Sm = ClSmem<G, MT>;
   constexpr int NWC = Sm::NWC, CTC = NWC * 32;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align up by offset from the array (keeps the shared state space: LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  const int CS = a.nc;  // cluster size == chunks per segment
   unsigned char* ktiles = smem;
   unsigned char* vtiles = smem + MT * TILE;
-  float* slot = reinterpret_cast<float*>(smem + Sm::tiles);
-  float* cpart = slot + Sm::slot_floats;  // [2][G][PW]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cpart + Sm::cpart_floats);
+  float* recv = reinterpret_cast<float*>(smem + Sm::tiles);  // [recv_floats(CS)]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(recv + Sm::recv_floats(CS));
   uint64_t* kfull = bars;
   uint64_t* vfull = bars + 1;
-  uint64_t* kfree = bars + 2;
+  uint64_t* kfree = bars + 2;  // K rows free: every warp's partial consumed by the chunk combine
   uint64_t* vfree = bars + 3;
-  uint64_t* ready = bars + 4;  // [2] by layer parity: one arrive per cluster rank
+  uint64_t* ready = bars + 4;  // own arrive + every rank's pushed bytes, one phase per layer
   float* fstats = reinterpret_cast<float*>(bars + 16);  // fold warp: [Hq][2]
+  {
+    uint32_t dyn;  // the tight layout needs the aligned base inside the allocation
+    asm("mov.u32 %0, %%dynamic_smem_size;\n" : "=r"(dyn));
+    if ((size_t)(smem - smem_raw) + Sm::bytes(a.Hq, CS) > dyn) {
+      if (threadIdx.x == 0 && a.err) atomicOr(a.err, 2);
+      return;  // same offset in every CTA of the launch: all leave, no barrier is left waiting
+    }
+  }
 
-  const int CS = a.nc;  // cluster size == chunks per segment
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j = (int)cluster_rank();
   const int sigma = blockIdx.x / CS;
@@ -789,9 +853,9 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
     mbar_init(vfull, 1);
     mbar_init(kfree, NWC);
     mbar_init(vfree, NWC);
-    mbar_init(&ready[0], CS);
-    mbar_init(&ready[1], CS);
+    mbar_init(ready, 1);
     mbar_fence_init();
+    mbar_arrive_expect_tx(ready, Sm::recv_bytes(CS, j));  // layer 0's pushes
   }
   cluster_sync_all();  // every rank's barriers exist before any remote arrive
 
@@ -801,19 +865,20 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
       if (!ls.prefetch0 || has_prev) griddep_wait();
       for (int l = 0; l < ls.L; ++l) {
         const int seg_row = (int)(((int64_t)s * a.L + a.layer + l) * a.Hkv + g) * a.cap;
-        if (l > 0) mbar_wait(kfree, (l - 1) & 1);
-        mbar_arrive_expect_tx(kfull, (uint32_t)ntile * TILE);
-        for (int t = 0; t < ntile; ++t) {
-          const int y = seg_row + (tt0 + t) * TT;
-          tma_load_2d(ktiles + t * TILE, &kmap, 0, y, kfull);
-          tma_load_2d(ktiles + t * TILE + REGION, &kmap, 64, y, kfull);
-        }
-        if (l > 0) mbar_wait(vfree, (l - 1) & 1);
-        mbar_arrive_expect_tx(vfull, (uint32_t)ntile * TILE);
-        for (int t = 0; t < ntile; ++t) {
-          const int y = seg_row + (tt0 + t) * TT;
-          tma_load_2d(vtiles + t * TILE, &vmap, 0, y, vfull);
-          tma_load_2d(vtiles + t * TILE + REGION, &vmap, 64, y, vfull);
+        // layer l > 0: V as soon as layer l-1's P V is done, K once the chunk
+        // combine has consumed the warp partials staged in the K rows
+        for (int kv = 0; kv < 2; ++kv) {
+          const bool isk = (kv == 0) == (l == 0);
+          if (l > 0) mbar_wait(isk ? kfree : vfree, (l - 1) & 1);
+          uint64_t* full = isk ? kfull : vfull;
+          unsigned char* dst = isk ? ktiles : vtiles;
+          const CUtensorMap* map = isk ? &kmap : &vmap;
+          mbar_arrive_expect_tx(full, (uint32_t)ntile * TILE);
+          for (int t = 0; t < ntile; ++t) {
+            const int y = seg_row + (tt0 + t) * TT;
+            tma_load_2d(dst + t * TILE, map, 0, y, full);
+            tma_load_2d(dst + t * TILE + REGION, map, 64, y, full);
+          }
         }
       }
     }
@@ -849,11 +914,10 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
     const bool real = gid < G;
     const uint32_t kbase = smem_u32(ktiles), vbase = smem_u32(vtiles);
     const int wk0 = warp * 32;
-    float* wm = slot + 4;
-    float* wl = wm + NWC * G;
-    float* wo = wl + NWC * G;
-    const int total_out = G * D;
-    const int per_rank = (total_out + CS - 1) / CS;  // output elements this rank merges
+    // warp w's partial lives in the 32 K rows it scored: o in the first half of
+    // the swizzled tile, (m, l) in the second
+    auto wpart = [&](int w) { return reinterpret_cast<float*>(ktiles + (w >> 1) * TILE + (w & 1) * 4096); };
+    constexpr int HALF = REGION / 4;  // floats
     for (int l = 0; l < ls.L; ++l) {
       if (l == 0) {
         griddep_wait();
@@ -864,7 +928,7 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
           }
         bar_sync_n(1, CTC);
       }
-      unsigned long long* tl = ls.tl ? ls.tl + ((int64_t)l * gridDim.x + blockIdx.x) * 8 : nullptr;
+      unsigned long long* tl = ls.tl && blockIdx.x < 148 ? ls.tl + ((int64_t)l * 148 + blockIdx.x) * 8 : nullptr;
       if (tl && tid == 0) tl[0] = gtimer();
       const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
       uint32_t qa[8][2];
@@ -892,32 +956,25 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
         }
         bar_sync_n(1, CTC);
       }
-      float m = -INFINITY, lsum = 0.f;
-      float o[16][4];
+      float m[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
+      float o[8][4];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-      float* lgrow = a.logits ? a.logits + l * ls.lg_ls + s * a.l_ss + (int64_t)(g * G + (real ? gid : 0)) * a.l_hs
-                              : nullptr;
-      float p[4][2];
+      for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      float* lg = a.logits ? a.logits + l * ls.lg_ls + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+      float p[2][4];
       const bool active = wk0 < ntile * TT;
-      if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, real ? lgrow : nullptr, p, m, lsum);
-      __syncwarp();
-      if (lane == 0 && any) mbar_arrive(kfree);
+      if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, lg, a.l_hs, G, p, m, lsum);
       if (any) mbar_wait(vfull, ph);
       if (active) warp_pv(p, vbase, wk0, lane, o);
       __syncwarp();
       if (lane == 0 && any) mbar_arrive(vfree);
       if (tl && tid == 0) tl[2] = gtimer();
-      if (real) {
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-          *reinterpret_cast<float2*>(wo + (warp * G + gid) * D + 8 * nt + 2 * tig) = make_float2(o[nt][0], o[nt][1]);
-        if (tig == 0) {
-          wm[warp * G + gid] = m;
-          wl[warp * G + gid] = lsum;
-        }
+      {  // into this warp's own K rows (every lane's ldmatrix reads are done)
+        float* wp = wpart(warp);
+        warp_stage(o, m, lsum, lane, G, wp, wp + HALF, wp + HALF + G);
       }
       bar_sync_n(1, CTC);
+      if (tl && tid == 0) tl[5] = gtimer();  // every warp's partial staged
       if (has_new) {
         AttnArgs al = a;  // layer l's cache rows and token metadata
         al.kc = static_cast<__nv_bfloat16*>(a.kc) + l * ls.kv_ls;
@@ -931,77 +988,76 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
         al.next_pos = a.next_pos + l;
         append_row<__nv_bfloat16, D>(al, sigma, n, tid, CTC);
       }
-      // ---- chunk partial (decode_tc_kernel's warp order) into this rank's buffer
-      float* cp = cpart + (l & 1) * G * PW;
-      for (int idx = tid; idx < G * D; idx += CTC) {
-        const int h = idx / D, d = idx - h * D;
+      // ---- chunk partial (decode_tc_kernel's warp order), pushed in 4-element
+      // groups straight into the owning rank's receive buffer (st.async with
+      // mbarrier byte accounting: no release fence, no pull round trip).  Rank r
+      // owns output elements [r*per, r*per + cnt_r) of the segment's G x D.
+      const int per = Sm::per(CS);
+      float* rv = recv;
+      const uint32_t rv_local = smem_u32(rv), rbar_local = smem_u32(ready);
+      for (int g4 = tid; g4 < G * D / 4; g4 += CTC) {
+        const int idx = g4 * 4, h = idx / D, d = idx - h * D;
         float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < NWC; ++w) M = fmaxf(M, wm[w * G + h]);
+        for (int w = 0; w < NWC; ++w) M = fmaxf(M, wpart(w)[HALF + h]);
         float f[NWC];
 #pragma unroll
-        for (int w = 0; w < NWC; ++w) f[w] = rescale(wm[w * G + h], M);
-        float acc = 0.f;
+        for (int w = 0; w < NWC; ++w) f[w] = rescale(wpart(w)[HALF + h], M);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int w = 0; w < NWC; ++w) acc = fmaf(f[w], wo[(w * G + h) * D + d], acc);
-        cp[h * PW + d] = acc;
+        for (int w = 0; w < NWC; ++w) {
+          const float4 o4 = *reinterpret_cast<const float4*>(wpart(w) + h * D + d);
+          acc.x = fmaf(f[w], o4.x, acc.x);
+          acc.y = fmaf(f[w], o4.y, acc.y);
+          acc.z = fmaf(f[w], o4.z, acc.z);
+          acc.w = fmaf(f[w], o4.w, acc.w);
+        }
+        const int owner = idx / per, e = idx - owner * per;
+        st_async_v4(map_rank(rv_local + (j * per + e) * 4, owner), acc, map_rank(rbar_local, owner));
         if (d == 0) {
           float xs = 0.f;  // warps in order (NWC need not be a power of two)
 #pragma unroll
-          for (int w = 0; w < NWC; ++w) xs += f[w] * wl[w * G + h];
-          cp[h * PW + D] = M;
-          cp[h * PW + D + 1] = xs;
+          for (int w = 0; w < NWC; ++w) xs += f[w] * wpart(w)[HALF + G + h];
+          const uint32_t so = rv_local + (CS * per + (j * G + h) * 2) * 4;
+          for (int r = 0; r < CS; ++r) st_async_v2(map_rank(so, r), M, xs, map_rank(rbar_local, r));
         }
       }
-      bar_sync_n(1, CTC);
-      // ---- publish to every rank of the cluster (release at cluster scope)
-      if (tid < CS) arrive_remote(map_rank(smem_u32(&ready[l & 1]), (uint32_t)tid));
+      __syncwarp();
+      if (lane == 0 && any) mbar_arrive(kfree);  // this warp's reads of the staged partials are done
       if (tl && tid == 0) tl[3] = gtimer();
-      wait_cluster(&ready[l & 1], (l >> 1) & 1);
-      // ---- merge this rank's slice of the segment's output elements: every
-      // rank's (m, l) per head staged once, then each element's CS partial
-      // values loaded together (distributed shared memory round trips overlap)
-      const uint32_t cp_local = smem_u32(cpart + (l & 1) * G * PW);
+      wait_cluster(ready, l & 1);
+      if (tl && tid == 0) tl[6] = gtimer();  // every rank's partial received
+      // ---- merge this rank's elements from local shared memory (merge_kernel's
+      // arithmetic: weights rescale(m_r, M), L = sum w_r l_r, out = sum_r w_r o_r / L)
       float* out = a.out + l * ls.o_ls + s * a.o_ss + (int64_t)(g * G) * D;
       float* stats = a.stats + l * ls.st_ls;
-      float* stg = wm;  // [G][16] m, [G][16] l, [G][16] weights, [G] L (warp partials consumed)
-      if (tid < G * CS) {
-        const int h = tid / CS, r = tid - (tid / CS) * CS;
-        stg[h * 16 + r] = ld_cluster(map_rank(cp_local + (h * PW + D) * 4, r));
-        stg[G * 16 + h * 16 + r] = ld_cluster(map_rank(cp_local + (h * PW + D + 1) * 4, r));
-      }
-      bar_sync_n(1, CTC);
-      if (tid < G) {
-        const int h = tid;
+      const int cnt = min(per, G * D - j * per);
+      for (int e4 = tid * 4; e4 < cnt; e4 += CTC * 4) {
+        const int idx = j * per + e4, h = idx / D;
+        const float* sm = rv + CS * per + h * 2;  // [src][G][2]
         float M = -INFINITY;
-        for (int r = 0; r < CS; ++r) M = fmaxf(M, stg[h * 16 + r]);
+        for (int r = 0; r < CS; ++r) M = fmaxf(M, sm[r * G * 2]);
         float L = 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int r = 0; r < CS; ++r) {
-          const float w = rescale(stg[h * 16 + r], M);
-          stg[2 * G * 16 + h * 16 + r] = w;
-          L += w * stg[G * 16 + h * 16 + r];
+          const float w = rescale(sm[r * G * 2], M);
+          L += w * sm[r * G * 2 + 1];
+          const float4 o4 = *reinterpret_cast<const float4*>(rv + r * per + e4);
+          acc.x = fmaf(w, o4.x, acc.x);
+          acc.y = fmaf(w, o4.y, acc.y);
+          acc.z = fmaf(w, o4.z, acc.z);
+          acc.w = fmaf(w, o4.w, acc.w);
         }
-        stg[3 * G * 16 + h] = L;
-        if (j == 0) {
+        *reinterpret_cast<float4*>(out + idx) = make_float4(acc.x / L, acc.y / L, acc.z / L, acc.w / L);
+        if (idx - h * D == 0) {
           stats[s * a.st_ss + (g * G + h) * 2] = M;
           stats[s * a.st_ss + (g * G + h) * 2 + 1] = L;
         }
       }
-      bar_sync_n(1, CTC);
-      for (int e = tid; e < per_rank; e += CTC) {
-        const int idx = j + e * CS;  // strided over ranks
-        if (idx >= total_out) break;
-        const int h = idx / D, d = idx - h * D;
-        float ov[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) ov[r] = r < CS ? ld_cluster(map_rank(cp_local + (h * PW + d) * 4, r)) : 0.f;
-        const float* w = stg + 2 * G * 16 + h * 16;
-        float acc = 0.f;
-#pragma unroll
-        for (int r = 0; r < 16; ++r)
-          if (r < CS) acc = fmaf(w[r], ov[r], acc);
-        out[idx] = acc / stg[3 * G * 16 + h];
-      }
+      if (tl && tid == 0) tl[7] = gtimer();  // thread 0's elements merged
+      // layer l+1's expected bytes (its pushes follow every rank's release of
+      // layer_done[l], hence this rank's merge above: one buffer suffices)
+      if (tid == 0) mbar_arrive_expect_tx(ready, Sm::recv_bytes(CS, j));
       bar_sync_n(1, CTC);
       if (tid == 0) {
         red_release_add(&ls.layer_done[l], 1);
@@ -1015,7 +1071,9 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
       }
     }
   }
-  cluster_sync_all();  // no rank leaves while another may still read its partials
+  // no rank leaves while a push into it may be in flight (every rank has
+  // received all its bytes before it arrives: no memory ordering needed)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;\n" ::: "memory");
 }
 
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
@@ -1059,7 +1117,7 @@ cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_
   static DevOnce attr_set[9][5];
   auto run = [&](auto kern, int threads, size_t smem_bytes, DevOnce& attr) -> cudaError_t {
     if (!attr.here()) {
-      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (r != cudaSuccess) return r;
       attr.here() = true;
     }
@@ -1067,7 +1125,7 @@ cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_
     cfg.dynamicSmemBytes = smem_bytes;
     return cudaLaunchKernelEx(&cfg, kern, kmap, vmap, a);
   };
-  const int mt = a.ch <= 2 ? 2 : 4;
+  const int mt = a.ch <= 2 && group <= 4 ? 2 : 4;  // (no 2-tile instantiation for groups of 8)
 #define SKV_TC_CASE(GG, MM)                                                                                  \
   if (group == GG && mt == MM)                                                                              \
     e = run(decode_tc_kernel<GG, MM>, tcd::SmemT<GG, MM>::THREADS, tcd::SmemT<GG, MM>::bytes(MM == 4 ? 1024 : a.Hq), \
@@ -1144,17 +1202,18 @@ cudaError_t launch_decode_tc_cluster(int group, int mt, const AttnArgs& a, const
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
   static DevOnce attrs_set[2][8];  // per instantiation (G, mt): kern has one type for all of them
-  auto run = [&](auto kern, int threads, size_t smem_bytes) -> cudaError_t {
+  constexpr size_t kMaxSmem = 227 * 1024;
+  auto run = [&](auto kern, int threads, size_t need) -> cudaError_t {
     DevOnce& attr = attrs_set[group == 8][mt & 7];
     if (!attr.here()) {
-      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
       if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (r != cudaSuccess) return r;
       attr.here() = true;
     }
+    if (need > kMaxSmem) return cudaErrorInvalidValue;
     cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem_bytes;
-    if (smem_bytes > 227 * 1024) return cudaErrorInvalidValue;
+    cfg.dynamicSmemBytes = std::min(need + 1024, kMaxSmem);  // + alignment slack where it fits (checked in-kernel)
     if (max_clusters) {  // co-residency check only
       cudaLaunchConfig_t q = cfg;
       q.numAttrs = 2;
@@ -1162,11 +1221,17 @@ cudaError_t launch_decode_tc_cluster(int group, int mt, const AttnArgs& a, const
     }
     return cudaLaunchKernelEx(&cfg, kern, kmap, vmap, a, ls);
   };
-  if (group == 4 && mt == 4) return run(decode_tc_cluster_kernel<4, 4>, ClSmem<4, 4>::THREADS, ClSmem<4, 4>::bytes(a.Hq));
-  if (group == 4 && mt == 5) return run(decode_tc_cluster_kernel<4, 5>, ClSmem<4, 5>::THREADS, ClSmem<4, 5>::bytes(a.Hq));
-  if (group == 4 && mt == 6) return run(decode_tc_cluster_kernel<4, 6>, ClSmem<4, 6>::THREADS, ClSmem<4, 6>::bytes(a.Hq));
-  if (group == 8 && mt == 4) return run(decode_tc_cluster_kernel<8, 4>, ClSmem<8, 4>::THREADS, ClSmem<8, 4>::bytes(a.Hq));
-  if (group == 8 && mt == 5) return run(decode_tc_cluster_kernel<8, 5>, ClSmem<8, 5>::THREADS, ClSmem<8, 5>::bytes(a.Hq));
+#define SKV_CL_CASE(GG, MM)       \
+  if (group == GG && mt == MM) \
+    return run(decode_tc_cluster_kernel<GG, MM>, ClSmem<GG, MM>::THREADS, ClSmem<GG, MM>::bytes(a.Hq, a.nc));
+  SKV_CL_CASE(4, 4)
+  SKV_CL_CASE(4, 5)
+  SKV_CL_CASE(4, 6)
+  SKV_CL_CASE(4, 7)
+  SKV_CL_CASE(8, 4)
+  SKV_CL_CASE(8, 5)
+  SKV_CL_CASE(8, 6)
+#undef SKV_CL_CASE
   return cudaErrorInvalidValue;
 }
 

@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
                    const __grid_constant__ CUtensorMap vmap, const PrefillArgs a) {
   using namespace pf;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align up by offset from the array (keeps the shared state space: LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SBAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;            // [KST]

@@ -272,6 +272,8 @@ static int check_sticky(skv_ctx* x) {
   const int32_t w = *x->err_host;
   if (w == 0) return SKV_OK;
   *x->err_host = 0;
+  if (w & 2)
+    return fail(SKV_ECUDA, "all-layer decode: dynamic shared memory base not 1024-byte aligned, launch skipped");
   return fail(SKV_EINVAL,
               "value overflow: a chunked prefill read |v| >= 65504, which its fp16 P.V cannot represent "
               "(outputs of that chunk are saturated)");
@@ -637,6 +639,7 @@ static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, co
   const int64_t SLstride = (int64_t)x->L;  // stream stride in (stream, layer) units
 
   AttnArgs a{};
+  a.err = x->err_word;
   a.Hq = x->Hq;
   a.Hkv = x->Hkv;
   a.n_old = n_old;
@@ -959,13 +962,13 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   if (rc) return rc;
   const int segs = x->S * x->Hkv;
   // cluster variant (default): one cluster of CS <= 16 CTAs per segment,
-  // chunks of mt = 4 or 5 tiles; all clusters must be co-resident
+  // chunks of mt = 4..7 tiles (4..6 at G = 8); all clusters must be co-resident
   // (the smallest chunk whose cluster of CS <= 16 CTAs per segment fits: a
   // GPC must hold a whole cluster, and not every GPC has 16 free SMs)
   int mt = 0, CS = 0;
   bool cluster = false;
 
-  for (int t = 4; t <= (x->G == 4 ? 6 : 5) && use_layers_kernel() == 1 && !cluster; ++t) {
+  for (int t = 4; t <= (x->G == 4 ? 7 : 6) && use_layers_kernel() == 1 && !cluster; ++t) {
     const int cs = (p.nt + t - 1) / t;
     if (cs > 16 || segs * cs > sms) continue;
     const int key = (x->G * 8 + t) * 32 + cs;

@@ -48,6 +48,7 @@ struct FoldArgs {
 };
 
 struct AttnArgs {
+  int32_t* err;         // sticky device error word (skv_ctx::err_word) or null
   int Hq, Hkv;          // group size G = Hq / Hkv is a template parameter
   int n_old;            // tokens cached before this step
   int append;           // 1: slot n_old is the new token taken from kin/vin

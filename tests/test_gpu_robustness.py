@@ -254,15 +254,18 @@ def test_slot_map_moves_only_the_survivors_of_the_period():
     assert dense.moved_rows() is None and dense.slot_map(0, 0) is None
 
 
-@pytest.mark.parametrize("G", [4, 8])
-def test_all_layer_persistent_decode_matches_oracle(G):
+@pytest.mark.parametrize("G,L,l,E,periods", [(4, 4, 512, 64, 3), (8, 4, 512, 64, 3), (4, 2, 2048, 256, 1)],
+                         ids=["G4", "G8", "G4-cfg3-budget"])
+def test_all_layer_persistent_decode_matches_oracle(G, L, l, E, periods):
     """decode_step of a latency-bound GQA engine runs all layers in one
-    persistent launch (decode_tc_layers_kernel: in-kernel segment merge,
-    layer l+1 released by layer l's outputs).  Against the oracle over three
-    periods: outputs, window rows, kept sets, compacted K/V."""
-    S, L, Hkv, D = 1, 4, 32 // G, 128
+    persistent launch (decode_tc_cluster_kernel: one cluster per segment,
+    segment merge over distributed shared memory, layer l+1 released by layer
+    l's outputs).  Against the oracle: outputs, window rows, kept sets,
+    compacted K/V.  The config-3 budget case (4096 + 256 tokens: 65-68 tiles per
+    segment) runs 7-tile chunks on clusters of 10."""
+    S, Hkv, D = 1, 32 // G, 128
     Hq = Hkv * G
-    l, r, W, E = 512, 512, 16, 64
+    r, W = l, 16
     B = l + r
     cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
     eng = _eng(S, L, Hq, Hkv, D, l, r, W, B + E)
@@ -271,7 +274,7 @@ def test_all_layer_persistent_decode_matches_oracle(G):
     _inject_both(eng, orc, rng, S, L, Hkv, D, B)
     kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
     worst = worst_row = 0.0
-    for period in range(3):
+    for period in range(periods):
         for t in range(E):
             q = bf16_round(rng.standard_normal((L, S, Hq, D)).astype(F32))
             k = bf16_round(rng.standard_normal((L, S, Hkv, D)).astype(F32))

@@ -27,12 +27,13 @@ torch.cuda.synchronize()
 a = tl.cpu().numpy()
 P = int((a[0, :, 0] > 0).sum())
 a = a[:, :P]
-names = ["released", "q+K in", "math done", "published", "merged", "-"]
+names = ["released", "q+K in", "math done", "staged", "published", "all pub", "merge0", "merged"]
+order = [0, 1, 2, 5, 3, 6, 7, 4]
 prev = None
 for l in range(L):
     r0 = a[l, :, 0].min()
     row = []
-    for i, nm in enumerate(names):
+    for nm, i in zip(names, order):
         col = a[l, :, i]
         col = col[col > 0]
         if col.size == 0:
