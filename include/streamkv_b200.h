@@ -212,7 +212,7 @@ int skv_timing_read(skv_ctx* ctx, uint64_t* out_host, int max_pairs);
 /* enable == 3 additionally records per-CTA [start, released, end] of the
  * launches in slots tcount % 64; skv_timing_cta copies one slot (max_ctas x 8). */
 int skv_timing_cta(skv_ctx* ctx, int slot, uint64_t* out_host);
-/* Instrumentation: a non-null device buffer of [L][148][8] u64 makes every
+/* Instrumentation: a non-null device buffer of [L][148][16] u64 makes every
  * later all-layer persistent decode record per-CTA, per-layer %globaltimer
  * stamps (released, q loaded, K in, math done, published, merged). */
 int skv_layers_timeline(skv_ctx* ctx, uint64_t* buf_dev);

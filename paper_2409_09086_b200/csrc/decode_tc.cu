@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
         }
       consumers_sync();
     }
-    unsigned long long* tl = ls.tl && c < 148 ? ls.tl + ((int64_t)l * 148 + c) * 8 : nullptr;
+    unsigned long long* tl = ls.tl && c < 148 ? ls.tl + ((int64_t)l * 148 + c) * 16 : nullptr;
     if (tl && tid == 0) tl[0] = gtimer();  // released
     const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
     uint32_t qa[8][2];
@@ -751,9 +751,10 @@ struct ClSmem {
   static_assert(G * tcd::D * 4 <= 4096, "warp partial must fit the warp's consumed K rows");
   // receive buffer (one: layer l+1's pushes follow every rank's layer-l merge):
   // [CS][per] chunk-partial values of the elements this rank owns, then
-  // [CS][G][2] every rank's (m, l) per head
+  // [CS][G][2] every rank's (m, l) per head, then the merge's [CS][G] chunk
+  // weights and [G] maxima
   __host__ __device__ static int per(int cs) { return ((G * tcd::D + cs - 1) / cs + 3) / 4 * 4; }
-  __host__ __device__ static int recv_floats(int cs) { return cs * per(cs) + 2 * G * cs; }
+  __host__ __device__ static int recv_floats(int cs) { return cs * per(cs) + 2 * G * cs + (cs + 1) * G; }
   __device__ static uint32_t recv_bytes(int cs, int rank) {
     const int cnt = max(0, min(per(cs), G * tcd::D - rank * per(cs)));
     return (uint32_t)(cs * cnt + cs * G * 2) * 4;
@@ -825,6 +826,8 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
   uint64_t* kfree = bars + 2;  // K rows free: every warp's partial consumed by the chunk combine
   uint64_t* vfree = bars + 3;
   uint64_t* ready = bars + 4;  // own arrive + every rank's pushed bytes, one phase per layer
+  uint64_t* mdone = bars + 5;  // (late_prefetch) this rank's merge of the layer is done
+  volatile int* relc = reinterpret_cast<volatile int*>(bars + 6);  // layers released to the consumers
   float* fstats = reinterpret_cast<float*>(bars + 16);  // fold warp: [Hq][2]
   {
     uint32_t dyn;  // the tight layout needs the aligned base inside the allocation
@@ -854,6 +857,8 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
     mbar_init(kfree, NWC);
     mbar_init(vfree, NWC);
     mbar_init(ready, 1);
+    mbar_init(mdone, 1);
+    *relc = 0;
     mbar_fence_init();
     mbar_arrive_expect_tx(ready, Sm::recv_bytes(CS, j));  // layer 0's pushes
   }
@@ -861,7 +866,9 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
 
   if (warp == NWC) {
     // ---------------------------------------------------------- producer
-    if (lane == 0 && ntile > 0) {
+    // (lane 0 streams the tiles; the whole warp appends the token's row once
+    // its layer is released, off the consumers' critical path)
+    if (ntile > 0) {
       if (!ls.prefetch0 || has_prev) griddep_wait();
       for (int l = 0; l < ls.L; ++l) {
         const int seg_row = (int)(((int64_t)s * a.L + a.layer + l) * a.Hkv + g) * a.cap;
@@ -869,16 +876,37 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
         // combine has consumed the warp partials staged in the K rows
         for (int kv = 0; kv < 2; ++kv) {
           const bool isk = (kv == 0) == (l == 0);
-          if (l > 0) mbar_wait(isk ? kfree : vfree, (l - 1) & 1);
-          uint64_t* full = isk ? kfull : vfull;
-          unsigned char* dst = isk ? ktiles : vtiles;
-          const CUtensorMap* map = isk ? &kmap : &vmap;
-          mbar_arrive_expect_tx(full, (uint32_t)ntile * TILE);
-          for (int t = 0; t < ntile; ++t) {
-            const int y = seg_row + (tt0 + t) * TT;
-            tma_load_2d(dst + t * TILE, map, 0, y, full);
-            tma_load_2d(dst + t * TILE + REGION, map, 64, y, full);
+          if (lane == 0) {
+            if (l > 0) {
+              const bool late = ls.late_prefetch == 1 || (ls.late_prefetch == 2 && isk);
+              mbar_wait(late ? mdone : isk ? kfree : vfree, (l - 1) & 1);
+            }
+            uint64_t* full = isk ? kfull : vfull;
+            unsigned char* dst = isk ? ktiles : vtiles;
+            const CUtensorMap* map = isk ? &kmap : &vmap;
+            mbar_arrive_expect_tx(full, (uint32_t)ntile * TILE);
+            for (int t = 0; t < ntile; ++t) {
+              const int y = seg_row + (tt0 + t) * TT;
+              tma_load_2d(dst + t * TILE, map, 0, y, full);
+              tma_load_2d(dst + t * TILE + REGION, map, 64, y, full);
+            }
           }
+          __syncwarp();
+        }
+        if (has_new) {  // KvCache.append of layer l's token, after layer l's release
+          while (*relc < l + 1) {
+          }
+          AttnArgs al = a;  // layer l's cache rows and token metadata
+          al.kc = static_cast<__nv_bfloat16*>(a.kc) + l * ls.kv_ls;
+          al.vc = static_cast<__nv_bfloat16*>(a.vc) + l * ls.kv_ls;
+          al.kin = static_cast<const __nv_bfloat16*>(a.kin) + l * ls.in_ls;
+          al.vin = static_cast<const __nv_bfloat16*>(a.vin) + l * ls.in_ls;
+          al.pos = a.pos + l * ls.m_ls;
+          al.modality = a.modality + l * ls.m_ls;
+          al.round_id = a.round_id + l * ls.m_ls;
+          al.len = a.len + l;
+          al.next_pos = a.next_pos + l;
+          append_row<__nv_bfloat16, D>(al, sigma, n, lane, 32);
         }
       }
     }
@@ -923,13 +951,27 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
         griddep_wait();
         if (tid == 0) griddep_launch();
       } else {
-        if (tid == 0)
-          while (ld_acquire(&ls.layer_done[l - 1]) < segs * CS) {
+        // layer l-1 released: four pollers (lane 0 of warps 0-3) staggered by a
+        // quarter of an L2 round trip, so some read reaches L2 soon after the
+        // last release lands; the first to see it tells the others
+        if (lane == 0 && warp < 4) {
+          if (warp) __nanosleep(160 * warp);
+          while (*relc < l + 1) {
+            if (ld_acquire(&ls.layer_done[l - 1]) >= segs * CS) {
+              *relc = l + 1;  // (also lets the producer warp append layer l's token)
+              break;
+            }
           }
+        }
         bar_sync_n(1, CTC);
       }
-      unsigned long long* tl = ls.tl && blockIdx.x < 148 ? ls.tl + ((int64_t)l * 148 + blockIdx.x) * 8 : nullptr;
-      if (tl && tid == 0) tl[0] = gtimer();
+      if (l == 0 && tid == 0) *relc = 1;  // the producer warp may append layer 0's token
+      unsigned long long* tl = ls.tl && blockIdx.x < 148 ? ls.tl + ((int64_t)l * 148 + blockIdx.x) * 16 : nullptr;
+      // instrumentation: release in %globaltimer ns, later stamps by SM cycles (ns at 1965 MHz)
+      const unsigned long long tg0 = tl && tid == 0 ? gtimer() : 0ull;
+      const long long tc0 = clock64();
+      auto stamp = [&](int i) { tl[i] = i == 0 ? tg0 : tg0 + (unsigned long long)((clock64() - tc0) * 1000 / 1965); };
+      if (tl && tid == 0) stamp(0);
       const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + l * ls.q_ls;
       uint32_t qa[8][2];
       {
@@ -944,7 +986,7 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
       const uint32_t ph = l & 1;
       const bool any = ntile > 0;
       if (any) mbar_wait(kfull, ph);
-      if (tl && tid == 0) tl[1] = gtimer();
+      if (tl && tid == 0) stamp(1);
       if (has_new) {
         if (warp == 0) {
           if (lane >= 16) mbar_wait(vfull, ph);
@@ -968,41 +1010,35 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
       if (active) warp_pv(p, vbase, wk0, lane, o);
       __syncwarp();
       if (lane == 0 && any) mbar_arrive(vfree);
-      if (tl && tid == 0) tl[2] = gtimer();
+      if (tl && tid == 0) stamp(2);
       {  // into this warp's own K rows (every lane's ldmatrix reads are done)
         float* wp = wpart(warp);
         warp_stage(o, m, lsum, lane, G, wp, wp + HALF, wp + HALF + G);
       }
       bar_sync_n(1, CTC);
-      if (tl && tid == 0) tl[5] = gtimer();  // every warp's partial staged
-      if (has_new) {
-        AttnArgs al = a;  // layer l's cache rows and token metadata
-        al.kc = static_cast<__nv_bfloat16*>(a.kc) + l * ls.kv_ls;
-        al.vc = static_cast<__nv_bfloat16*>(a.vc) + l * ls.kv_ls;
-        al.kin = static_cast<const __nv_bfloat16*>(a.kin) + l * ls.in_ls;
-        al.vin = static_cast<const __nv_bfloat16*>(a.vin) + l * ls.in_ls;
-        al.pos = a.pos + l * ls.m_ls;
-        al.modality = a.modality + l * ls.m_ls;
-        al.round_id = a.round_id + l * ls.m_ls;
-        al.len = a.len + l;
-        al.next_pos = a.next_pos + l;
-        append_row<__nv_bfloat16, D>(al, sigma, n, tid, CTC);
-      }
-      // ---- chunk partial (decode_tc_kernel's warp order), pushed in 4-element
-      // groups straight into the owning rank's receive buffer (st.async with
-      // mbarrier byte accounting: no release fence, no pull round trip).  Rank r
-      // owns output elements [r*per, r*per + cnt_r) of the segment's G x D.
+      if (tl && tid == 0) stamp(5);  // every warp's partial staged
+      if (tl && tid == 0) stamp(8);  // (append done)
       const int per = Sm::per(CS);
       float* rv = recv;
       const uint32_t rv_local = smem_u32(rv), rbar_local = smem_u32(ready);
-      for (int g4 = tid; g4 < G * D / 4; g4 += CTC) {
-        const int idx = g4 * 4, h = idx / D, d = idx - h * D;
+      // warp weights rescale(m_w, M) once per (warp, head), next to the warp's
+      // (m, l); the head maxima next to warp 0's
+      if (tid < NWC * G) {
+        const int w = tid / G, h = tid - (tid / G) * G;
         float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < NWC; ++w) M = fmaxf(M, wpart(w)[HALF + h]);
+        for (int w2 = 0; w2 < NWC; ++w2) M = fmaxf(M, wpart(w2)[HALF + h]);
+        wpart(w)[HALF + 2 * G + h] = rescale(wpart(w)[HALF + h], M);
+        if (w == 0) wpart(0)[HALF + 3 * G + h] = M;
+      }
+      bar_sync_n(1, CTC);
+      static_assert(G * D / 4 <= 2 * MT * 32, "one 4-element group per consumer thread");
+      if (tid < G * D / 4) {
+        const int idx = tid * 4, h = idx / D, d = idx - h * D;
+        const float M = wpart(0)[HALF + 3 * G + h];
         float f[NWC];
 #pragma unroll
-        for (int w = 0; w < NWC; ++w) f[w] = rescale(wpart(w)[HALF + h], M);
+        for (int w = 0; w < NWC; ++w) f[w] = wpart(w)[HALF + 2 * G + h];
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int w = 0; w < NWC; ++w) {
@@ -1014,33 +1050,45 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
         }
         const int owner = idx / per, e = idx - owner * per;
         st_async_v4(map_rank(rv_local + (j * per + e) * 4, owner), acc, map_rank(rbar_local, owner));
-        if (d == 0) {
-          float xs = 0.f;  // warps in order (NWC need not be a power of two)
+        // (every lane of this warp works on head h: G*D/4 groups fit the consumer
+        // threads, 32 groups per head) -- lane r sends (M, L) to rank r
+        float xs = 0.f;  // warps in order (NWC need not be a power of two)
 #pragma unroll
-          for (int w = 0; w < NWC; ++w) xs += f[w] * wpart(w)[HALF + G + h];
+        for (int w = 0; w < NWC; ++w) xs += f[w] * wpart(w)[HALF + G + h];
+        if (lane < CS) {
           const uint32_t so = rv_local + (CS * per + (j * G + h) * 2) * 4;
-          for (int r = 0; r < CS; ++r) st_async_v2(map_rank(so, r), M, xs, map_rank(rbar_local, r));
+          st_async_v2(map_rank(so, lane), M, xs, map_rank(rbar_local, lane));
         }
       }
+      if (tl && tid == 0) stamp(9);  // (combine + pushes issued)
       __syncwarp();
       if (lane == 0 && any) mbar_arrive(kfree);  // this warp's reads of the staged partials are done
-      if (tl && tid == 0) tl[3] = gtimer();
+      if (tl && tid == 0) stamp(3);
       wait_cluster(ready, l & 1);
-      if (tl && tid == 0) tl[6] = gtimer();  // every rank's partial received
+      if (tl && tid == 0) stamp(6);  // every rank's partial received
       // ---- merge this rank's elements from local shared memory (merge_kernel's
       // arithmetic: weights rescale(m_r, M), L = sum w_r l_r, out = sum_r w_r o_r / L)
       float* out = a.out + l * ls.o_ls + s * a.o_ss + (int64_t)(g * G) * D;
       float* stats = a.stats + l * ls.st_ls;
       const int cnt = min(per, G * D - j * per);
+      float* mw = rv + CS * per + 2 * G * CS;  // [CS][G] chunk weights, [G] maxima
+      if (tid < CS * G) {
+        const int r = tid / G, h = tid - (tid / G) * G;
+        const float* sm = rv + CS * per + h * 2;
+        float M = -INFINITY;
+        for (int r2 = 0; r2 < CS; ++r2) M = fmaxf(M, sm[r2 * G * 2]);
+        mw[r * G + h] = rescale(sm[r * G * 2], M);
+        if (r == 0) mw[CS * G + h] = M;
+      }
+      bar_sync_n(1, CTC);
       for (int e4 = tid * 4; e4 < cnt; e4 += CTC * 4) {
         const int idx = j * per + e4, h = idx / D;
         const float* sm = rv + CS * per + h * 2;  // [src][G][2]
-        float M = -INFINITY;
-        for (int r = 0; r < CS; ++r) M = fmaxf(M, sm[r * G * 2]);
+        const float M = mw[CS * G + h];
         float L = 0.f;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int r = 0; r < CS; ++r) {
-          const float w = rescale(sm[r * G * 2], M);
+          const float w = mw[r * G + h];
           L += w * sm[r * G * 2 + 1];
           const float4 o4 = *reinterpret_cast<const float4*>(rv + r * per + e4);
           acc.x = fmaf(w, o4.x, acc.x);
@@ -1054,14 +1102,15 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
           stats[s * a.st_ss + (g * G + h) * 2 + 1] = L;
         }
       }
-      if (tl && tid == 0) tl[7] = gtimer();  // thread 0's elements merged
+      if (tl && tid == 0) stamp(7);  // thread 0's elements merged
       // layer l+1's expected bytes (its pushes follow every rank's release of
       // layer_done[l], hence this rank's merge above: one buffer suffices)
       if (tid == 0) mbar_arrive_expect_tx(ready, Sm::recv_bytes(CS, j));
       bar_sync_n(1, CTC);
+      if (tid == 0 && any) mbar_arrive(mdone);
       if (tid == 0) {
         red_release_add(&ls.layer_done[l], 1);
-        if (tl) tl[4] = gtimer();
+        if (tl) stamp(4);
       }
     }
     if (tid == 0) {

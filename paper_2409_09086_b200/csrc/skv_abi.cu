@@ -1016,6 +1016,10 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   ls.exit_count = ls.layer_done + x->L;
   ls.prefetch0 = x->layers_chain ? 1 : 0;
   ls.tl = x->lay_tl;
+  {
+    static const int lp = getenv("SKV_LATE_PREFETCH") ? atoi(getenv("SKV_LATE_PREFETCH")) : 0;
+    ls.late_prefetch = lp;
+  }
   cudaError_t e;
   if (cluster) {
     AttnArgs ca = p.a;

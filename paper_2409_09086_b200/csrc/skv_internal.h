@@ -125,11 +125,12 @@ struct LayerSteps {
   int32_t* layer_done;        // [L] merged segments per layer (reset by the last CTA out)
   int32_t* exit_count;        // [1]
   int prefetch0;              // 1: layer 0's cached K/V may stream before griddepcontrol.wait
-  unsigned long long* tl;     // instrumentation (null: off): [L][grid][8] %globaltimer per CTA and layer
+  unsigned long long* tl;     // instrumentation (null: off): [L][148][16] %globaltimer per CTA and layer
+  int late_prefetch;          // cluster kernel: 0 V after P.V, K after the combine; 1 both after the merge; 2 K after the merge
 };
 cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st);
 // cluster variant: a.nc (<= 16) CTAs per segment form a cluster, chunks of up
-// to mt (4 or 5) tiles; with max_clusters set, only reports how many such
+// to mt (4..7) tiles; with max_clusters set, only reports how many such
 // clusters can be co-resident
 cudaError_t launch_decode_tc_cluster(int group, int mt, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st,
                                      int* max_clusters = nullptr);
