@@ -445,7 +445,7 @@ def run_gpu(args, rank: int, world: int):
         "config": workload_config(c, S=S, resident=resident, waves=waves, world=world, job_streams=job_streams,
                                   hq=hq, hkv=hkv, use_graph=use_graph, gathered=gathered, sharded=sharded,
                                   select=select),
-        "roofline": {"bound": "hbm", "kernel": f"decode_kernel<bf16,128,{G}> (+ merge_kernel)",
+        "roofline": {"bound": "hbm", "kernel": _kernel_label(eng.last_decode_kernel, G, c),
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
                      "traffic": _ncu_traffic() if args.workload == "cfg1" and not args.budget else None,
@@ -463,6 +463,19 @@ def run_gpu(args, rank: int, world: int):
     if e2e:
         res["e2e"] = e2e
     return res
+
+
+def _kernel_label(name: str, G: int, c: dict) -> str:
+    """The decode kernel the engine ran, as the roofline's `kernel` string."""
+    dt = c.get("dtype", "bf16")
+    if name == "decode_tc_cluster_kernel":
+        return (f"decode_tc_cluster_kernel<{G},mt> (all {c['layers']} layers of a token per launch, one thread-block "
+                "cluster per segment; per-layer figures = launch / layers)")
+    if name == "decode_tcd_kernel":
+        return f"decode_tcd_kernel<{G}> (+ merge_kernel)"
+    if name == "decode_tc_kernel":
+        return f"decode_tc_kernel<{G},mt> (+ merge_kernel)"
+    return f"decode_kernel<{dt},{c['head_dim']},{G}> (+ merge_kernel)"
 
 
 def run_cfg2(args, rank: int, world: int):

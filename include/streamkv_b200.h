@@ -216,6 +216,9 @@ int skv_timing_cta(skv_ctx* ctx, int slot, uint64_t* out_host);
  * later all-layer persistent decode record per-CTA, per-layer %globaltimer
  * stamps (released, q loaded, K in, math done, published, merged). */
 int skv_layers_timeline(skv_ctx* ctx, uint64_t* buf_dev);
+/* Name of the kernel the last decode launch of this context ran
+ * ("decode_tcd_kernel", "decode_tc_cluster_kernel", ...; "" before any). */
+const char* skv_last_decode_kernel(const skv_ctx* ctx);
 /* Instrumentation: a non-null device buffer of [CTAs][16] u64 makes every
  * later prefill launch accumulate per-CTA wait/busy cycle counters into it
  * (null turns it off). */

@@ -90,6 +90,7 @@ SIGNATURES = {
     "skv_timing_read": (_I, [_P, _P, _I]),
     "skv_timing_cta": (_I, [_P, _I, _P]),
     "skv_layers_timeline": (_I, [_P, _P]),
+    "skv_last_decode_kernel": (ctypes.c_char_p, [_P]),
     "skv_prefill_profile": (_I, [_P]),
     "skv_prefill_chunk": (_I, [_P, _I, _P, _P, _P, _I, _I, _P, _P]),
     "skv_prefill_attend": (_I, [_P, _I, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _P, _I64, _P, _P]),

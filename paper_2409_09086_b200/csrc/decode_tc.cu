@@ -1125,6 +1125,475 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;\n" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Throughput launches (many segments: dynamic chunk tickets) on the tensor
+// cores.  decode_kernel's schedule -- ticket producer with a 3-stage ring, the
+// epilogue warp merging each chunk's warp partials in the background, the fold
+// warp, merge_kernel after it -- with 2-D TMA tiles in the 128-byte swizzle and
+// the keys-as-M MMA math: 4 consumer warps take 16 keys of every 64-token tile
+// and keep a running (max, sum, O^T) per query head over the chunk.  The
+// segment's new token is appended to the cache by the producer warp before
+// the tile that holds it streams in (a proxy fence orders the row stores
+// before the tensor copy), so the tile arrives complete.
+namespace tcd {
+template <int G>
+struct DynSmem {
+  static constexpr int NWD = 4;                  // consumer warps
+  static constexpr int THREADS = NWD * 32 + 96;  // + producer, epilogue, fold warps
+  static constexpr int STAGES = 3;
+  static constexpr size_t tiles = (size_t)STAGES * 2 * TILE;
+  static constexpr size_t slot_floats = 4 + 2 * NWD * G + NWD * G * D;
+  static size_t bytes(int Hq) {
+    return tiles + 2 * slot_floats * 4 + (2 * STAGES + 4) * 8 + (2 * STAGES + 4) * 4 + (size_t)Hq * 8 + 1024;
+  }
+};
+
+// One warp's 16 keys [wk0, wk0 + 16) of a tile whose row 0 is cache index
+// key0: S^T = K Q^T, then the running softmax (m, l, O^T rescaled by
+// exp(m_old - m_new)) and O^T += V^T P^T; recorded steps store the logits.
+__device__ __forceinline__ void warp_tile16(const uint32_t (&qb)[8][2], uint32_t kbase, uint32_t vbase, int wk0,
+                                            int lane, int key0, int kend, float scale, float* lg, int64_t lg_hs,
+                                            int G, float (&m)[2], float (&l)[2], float (&o)[8][4]) {
+  const int gid = lane >> 2, tig = lane & 3;
+  float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+  {
+    const int kk = wk0 + (lane & 7) + 8 * ((lane >> 3) & 1);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(kbase + swz(kk, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+      mma16816_a4(sacc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+    }
+  }
+  float x[4], mx[2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int key = key0 + wk0 + gid + (c >> 1) * 8;
+    x[c] = key < kend ? sacc[c] * scale : -INFINITY;
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    mx[e] = fmaxf(x[e], x[2 + e]);
+#pragma unroll
+    for (int sh = 4; sh < 32; sh <<= 1) mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], sh));
+  }
+  float mn[2], alpha[2], p[4], ls[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    mn[e] = fmaxf(m[e], mx[e]);
+    alpha[e] = rescale(m[e], mn[e]);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) p[c] = mn[c & 1] == -INFINITY ? 0.f : fast_exp2((x[c] - mn[c & 1]) * kLog2e);
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    ls[e] = p[e] + p[2 + e];
+#pragma unroll
+    for (int sh = 4; sh < 32; sh <<= 1) ls[e] += __shfl_xor_sync(0xffffffffu, ls[e], sh);
+    l[e] = l[e] * alpha[e] + ls[e];
+    m[e] = mn[e];
+  }
+#pragma unroll
+  for (int md = 0; md < 8; ++md)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[md][c] *= alpha[c & 1];
+  if (lg) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int h = 2 * tig + e;
+      if (h >= G) continue;
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int key = key0 + wk0 + gid + 8 * hi;
+        if (key < kend) lg[h * lg_hs + key] = x[2 * hi + e];
+      }
+    }
+  }
+  const uint32_t h0 = pack_bf16(p[0], p[1]), h1 = pack_bf16(p[2], p[3]);
+  const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h0));
+  const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h1));
+  const uint32_t l0 = pack_bf16(p[0] - f0.x, p[1] - f0.y), l1 = pack_bf16(p[2] - f1.x, p[3] - f1.y);
+  const uint32_t bh0 = movtrans(h0), bh1 = movtrans(h1), bl0 = movtrans(l0), bl1 = movtrans(l1);
+  const int kk = wk0 + (lane & 7) + 8 * (lane >> 4);
+#pragma unroll
+  for (int md = 0; md < 8; ++md) {
+    uint32_t a0, a1, a2, a3;
+    ldsm_x4_t(vbase + swz(kk, 2 * md + ((lane >> 3) & 1)), a0, a1, a2, a3);
+    mma16816_a4(o[md], a0, a1, a2, a3, bh0, bh1);
+    mma16816_a4(o[md], a0, a1, a2, a3, bl0, bl1);
+  }
+}
+}  // namespace tcd
+
+template <int G>
+__global__ void __launch_bounds__(tcd::DynSmem<G>::THREADS, 2)
+    decode_tcd_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                      const AttnArgs a) {
+  using namespace tcd;
+  using Sm = DynSmem<G>;
+  constexpr int NWD = Sm::NWD, CTD = NWD * 32, STAGES = Sm::STAGES, SLOT = (int)Sm::slot_floats;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  unsigned char* tiles = smem;                                        // [STAGES][K tile, V tile]
+  float* slots = reinterpret_cast<float*>(smem + Sm::tiles);          // [2][SLOT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + 2 * SLOT);
+  uint64_t* empty = full + STAGES;
+  uint64_t* epi_full = empty + STAGES;  // [2]
+  uint64_t* epi_empty = epi_full + 2;   // [2]
+  int* tinfo = reinterpret_cast<int*>(epi_empty + 2);  // [STAGES][2]
+  int* cring = tinfo + 2 * STAGES;                     // [4] next chunk tickets
+  float* fstats = reinterpret_cast<float*>(cring + 4);  // [Hq][2]
+
+  const int c = blockIdx.x, P = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n_old + a.append;
+  const int total = a.S * a.Hkv * a.nc;
+  constexpr int PWD = D + 2;
+
+  if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], gtimer());
+  if (c == 0 && tid == 0 && a.done_self) {  // a stale flag from this slot's previous use must not leak
+    *a.done_self = 0;
+    __threadfence();
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NWD);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&epi_full[i], NWD);
+      mbar_init(&epi_empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto wait_prev = [&]() {
+    if (a.done_prev) {
+      while (ld_acquire(a.done_prev) == 0) __nanosleep(32);
+    } else {
+      griddep_wait();
+    }
+  };
+
+  if (warp == NWD) {
+    // ------------------------------------------------------------ producer
+    bool waited = false;
+    if (!a.prefetch) {
+      griddep_wait();
+      waited = true;
+    }
+    const int nce = a.nc - 1, segs = a.S * a.Hkv, early = segs * nce;
+    const int DL = a.late > 0 && a.late < segs && nce > 0 ? a.late : 0;
+    auto slot_of = [&](int t) {  // ticket -> chunk slot (decode_kernel's order)
+      if (t >= total) return t;
+      if (DL == 0) return t < early ? (t / nce) * a.nc + (t % nce) : (t - early) * a.nc + nce;
+      const int bD = DL * nce;
+      const int bEnd = segs * nce + (segs - DL);
+      if (t >= bEnd) return (segs - DL + (t - bEnd)) * a.nc + nce;
+      int sg, off;
+      if (t < bD) {
+        sg = t / nce;
+        off = t - sg * nce;
+      } else {
+        sg = DL + (t - bD) / (nce + 1);
+        off = (t - bD) - (sg - DL) * (nce + 1);
+      }
+      return off < nce ? sg * a.nc + off : (sg - DL) * a.nc + nce;
+    };
+    int u = 0, t1 = 0, t2 = 0;
+    if (lane == 0) {
+      u = slot_of(atomicAdd(&a.sched[0], 1));
+      t1 = atomicAdd(&a.sched[0], 1);
+      t2 = atomicAdd(&a.sched[0], 1);
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    int i = 0, kp = 0;
+    while (u < total) {
+      int u_next = 0;
+      if (lane == 0) {
+        u_next = slot_of(t1);
+        t1 = t2;
+        t2 = atomicAdd(&a.sched[0], 1);
+        cring[(kp + 1) & 3] = u_next < total ? u_next : -1;  // lets the consumers prefetch q
+      }
+      u_next = __shfl_sync(0xffffffffu, u_next, 0);
+      ++kp;
+      const int sigma = u / a.nc, j = u - sigma * a.nc;
+      const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+      const int tt0 = j * a.ch, tt1 = min(tt0 + a.ch, a.nt);
+      const int seg_row = (int)((((int64_t)s * a.L + a.layer) * a.Hkv + g) * a.cap);
+      for (int tt = tt0; tt < tt1; ++tt, ++i) {
+        const int ts = tt * TT;
+        const int st = i % STAGES;
+        if (a.append && a.n_old >= ts && a.n_old < ts + TT) {
+          // KvCache.append (the whole warp), then the tile holding the row
+          if (!waited) {
+            wait_prev();
+            waited = true;
+          }
+          append_row<__nv_bfloat16, D>(a, sigma, n, lane, 32);
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          __syncwarp();
+        }
+        if (lane == 0) {
+          mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
+          tinfo[2 * st] = u;
+          tinfo[2 * st + 1] = tt | ((tt == tt1 - 1) ? (1 << 30) : 0);
+          unsigned char* ks = tiles + (size_t)(2 * st) * TILE;
+          mbar_arrive_expect_tx(&full[st], 2u * TILE);
+          const int y = seg_row + ts;
+          tma_load_2d(ks, &kmap, 0, y, &full[st]);
+          tma_load_2d(ks + REGION, &kmap, 64, y, &full[st]);
+          tma_load_2d(ks + TILE, &vmap, 0, y, &full[st]);
+          tma_load_2d(ks + TILE + REGION, &vmap, 64, y, &full[st]);
+        }
+        __syncwarp();
+      }
+      u = u_next;
+    }
+    if (lane == 0) {  // end marker
+      const int st = i % STAGES;
+      mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
+      tinfo[2 * st] = -1;
+      mbar_arrive(&full[st]);
+    }
+    return;
+  }
+
+  if (warp == NWD + 2) {
+    // ------------------------------------------------- window-row fold warp
+    const FoldArgs& f = a.fold;
+    if (f.n <= 0) return;
+    if (!a.prefetch) griddep_wait();
+    const int ppc = (f.n + 63) / 64;
+    for (int piece = c; piece < a.S * ppc; piece += P) {
+      const int s = piece / ppc, col0 = (piece - s * ppc) * 64;
+      const float* stt = f.stats + s * f.st_ss;
+      for (int h = lane; h < a.Hq; h += 32) {
+        fstats[2 * h] = __ldg(stt + 2 * h);
+        fstats[2 * h + 1] = __frcp_rn(__ldg(stt + 2 * h + 1));  // staged as 1/L
+      }
+      __syncwarp();
+      fold_columns(f, s, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+      __syncwarp();
+      if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s * f.w_ss] = f.n;
+    }
+    return;
+  }
+
+  if (warp == NWD + 1) {
+    // ------------------------------------------------------ epilogue warp
+    for (int k = 0;; ++k) {
+      const int sl = k & 1;
+      mbar_wait(&epi_full[sl], (k >> 1) & 1);
+      const float* slot = slots + sl * SLOT;
+      const int u = reinterpret_cast<const int*>(slot)[0];
+      if (u < 0) break;
+      const float* wm = slot + 4;
+      const float* wl = wm + NWD * G;
+      const float* wo = wl + NWD * G;
+      const int sigma = u / a.nc, j = u - sigma * a.nc;
+      float* part = a.part + ((int64_t)sigma * a.nc + j) * G * PWD;
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const float mw = lane < NWD ? wm[lane * G + h] : -INFINITY;
+        float M = mw;
+#pragma unroll
+        for (int off = NWD / 2; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        const float f = lane < NWD ? rescale(mw, M) : 0.f;
+        float L = lane < NWD ? f * wl[lane * G + h] : 0.f;
+#pragma unroll
+        for (int off = NWD / 2; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+        float fw[NWD];
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) fw[w] = __shfl_sync(0xffffffffu, f, w);
+#pragma unroll
+        for (int d = lane; d < D; d += 32) {
+          float acc = 0.f;
+#pragma unroll
+          for (int w = 0; w < NWD; ++w) acc = fmaf(fw[w], wo[(w * G + h) * D + d], acc);
+          part[h * PWD + d] = acc;
+        }
+        if (lane == 0) {
+          part[h * PWD + D] = M;
+          part[h * PWD + D + 1] = L;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&epi_empty[sl]);
+      __syncwarp();
+      if (lane == 0) red_release_add(&a.counters[sigma], 1);  // the segment's merge counts it
+    }
+    __threadfence();
+    bar_sync_n(2, CTD + 32);
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  if (a.done_prev) {
+    if (tid == 0) wait_prev();
+    bar_sync_n(1, CTD);
+  } else {
+    griddep_wait();
+  }
+  if (tid == 0) griddep_launch();
+  const int gid = lane >> 2, tig = lane & 3;
+  const bool real = gid < G;
+  const int wk0 = warp * 16;
+  uint32_t qb[8][2], qn[8][2];
+  int qn_sigma = -1, cur = -1;
+  auto load_q = [&](uint32_t (&dst)[8][2], int sg) {
+    const int s2 = sg / a.Hkv, g2 = sg - s2 * a.Hkv;
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(a.q) + s2 * a.q_ss +
+                                                             (int64_t)(g2 * G + (real ? gid : 0)) * D);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      dst[ks][0] = real ? qrow[8 * ks + tig] : 0u;
+      dst[ks][1] = real ? qrow[8 * ks + 4 + tig] : 0u;
+    }
+  };
+  float m[2], l[2], o[8][4];
+  float* lg = nullptr;
+  int k = 0;
+  bool fresh = true;
+  for (int i = 0;; ++i) {
+    const int st = i % STAGES;
+    mbar_wait(&full[st], (i / STAGES) & 1);
+    const int u = tinfo[2 * st];
+    if (u < 0) break;
+    const int info = tinfo[2 * st + 1];
+    const int tt = info & 0xffff;
+    const bool chunk_end = (info >> 30) & 1;
+    const int sigma = u / a.nc;
+    if (fresh) {
+      if (sigma != cur) {
+        if (qn_sigma != sigma) load_q(qn, sigma);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          qb[ks][0] = qn[ks][0];
+          qb[ks][1] = qn[ks][1];
+        }
+        cur = sigma;
+        const int s = sigma / a.Hkv, g = sigma - s * a.Hkv;
+        lg = a.logits ? a.logits + s * a.l_ss + (int64_t)(g * G) * a.l_hs : nullptr;
+      }
+      const int un = a.qpf ? cring[(k + 1) & 3] : -1;
+      if (un >= 0 && un / a.nc != sigma) {
+        load_q(qn, un / a.nc);
+        qn_sigma = un / a.nc;
+      }
+      m[0] = m[1] = -INFINITY;
+      l[0] = l[1] = 0.f;
+#pragma unroll
+      for (int md = 0; md < 8; ++md) o[md][0] = o[md][1] = o[md][2] = o[md][3] = 0.f;
+      fresh = false;
+    }
+    const uint32_t kbase = smem_u32(tiles + (size_t)(2 * st) * TILE);
+    warp_tile16(qb, kbase, kbase + TILE, wk0, lane, tt * TT, n, a.scale, lg, a.l_hs, G, m, l, o);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (!chunk_end) continue;
+    // ---- chunk done: hand the warp partials to the epilogue warp
+    const int sl = k & 1;
+    mbar_wait(&epi_empty[sl], ((k >> 1) & 1) ^ 1);
+    float* slot = slots + sl * SLOT;
+    float* wm = slot + 4;
+    float* wl = wm + NWD * G;
+    float* wo = wl + NWD * G;
+    warp_stage(o, m, l, lane, G, wo + warp * G * D, wm + warp * G, wl + warp * G);
+    if (warp == 0 && lane == 0) reinterpret_cast<int*>(slot)[0] = u;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&epi_full[sl]);
+    ++k;
+    fresh = true;
+  }
+  {  // end marker for the epilogue warp
+    const int sl = k & 1;
+    mbar_wait(&epi_empty[sl], ((k >> 1) & 1) ^ 1);
+    if (warp == 0 && lane == 0) reinterpret_cast<int*>(slots + sl * SLOT)[0] = -1;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&epi_full[sl]);
+  }
+  bar_sync_n(2, CTD + 32);  // this CTA's epilogue warp has published its partials
+  if (a.tstamp && tid == 0) atomicMax(&a.tstamp[1], gtimer());
+  if (tid == 0) {
+    if (atomicAdd(&a.sched[2], 1) == P - 1) {  // the last CTA out resets the scheduler
+      a.sched[0] = 0;
+      a.sched[2] = 0;
+      if (a.done_prev) *const_cast<int32_t*>(a.done_prev) = 0;
+    }
+  }
+}
+
+
+// Tensor maps over the K/V stores, encoded once per store (base, rows).
+static cudaError_t kv_maps(const AttnArgs& a, const CUtensorMap** km, const CUtensorMap** vm) {
+  struct MapCache {
+    const void* kb = nullptr;
+    const void* vb = nullptr;
+    int64_t rows = 0;
+    CUtensorMap k, v;
+  };
+  static thread_local MapCache cache[4];
+  static thread_local int next = 0;
+  for (auto& e : cache)
+    if (e.kb == a.kc_base && e.vb == a.vc_base && e.rows == a.total_rows) {
+      *km = &e.k;
+      *vm = &e.v;
+      return cudaSuccess;
+    }
+  MapCache* m = &cache[next++ % 4];
+  cudaError_t e = make_kv_map(&m->k, a.kc_base, a.total_rows, tcd::TT);
+  if (e == cudaSuccess) e = make_kv_map(&m->v, a.vc_base, a.total_rows, tcd::TT);
+  if (e != cudaSuccess) {
+    m->kb = nullptr;
+    return e;
+  }
+  m->kb = a.kc_base;
+  m->vb = a.vc_base;
+  m->rows = a.total_rows;
+  *km = &m->k;
+  *vm = &m->v;
+  return cudaSuccess;
+}
+
+cudaError_t launch_decode_tcd(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
+  if (a.stat) return cudaErrorInvalidValue;
+  const CUtensorMap *km = nullptr, *vm = nullptr;
+  cudaError_t e = kv_maps(a, &km, &vm);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  static DevOnce attr_set[9];
+  auto run = [&](auto kern, int threads, size_t bytes) -> cudaError_t {
+    DevOnce& attr = attr_set[group];
+    if (!attr.here()) {
+      // (two CTAs per SM where the slots are small -- groups 1, 2; one otherwise)
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (r != cudaSuccess) return r;
+      attr.here() = true;
+    }
+    if (bytes > 227 * 1024) return cudaErrorInvalidValue;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = bytes;
+    return cudaLaunchKernelEx(&cfg, kern, *km, *vm, a);
+  };
+  e = cudaErrorInvalidValue;
+  if (group == 1) e = run(decode_tcd_kernel<1>, tcd::DynSmem<1>::THREADS, tcd::DynSmem<1>::bytes(a.Hq));
+  if (group == 2) e = run(decode_tcd_kernel<2>, tcd::DynSmem<2>::THREADS, tcd::DynSmem<2>::bytes(a.Hq));
+  if (group == 4) e = run(decode_tcd_kernel<4>, tcd::DynSmem<4>::THREADS, tcd::DynSmem<4>::bytes(a.Hq));
+  if (group == 8) e = run(decode_tcd_kernel<8>, tcd::DynSmem<8>::THREADS, tcd::DynSmem<8>::bytes(a.Hq));
+  if (e != cudaSuccess) return e;
+  return launch_merge(128, group, a, st);
+}
+
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st) {
   if (a.ch > tcd::MAXT || !a.stat) return cudaErrorInvalidValue;
   // tensor maps depend only on the store (base, rows): encode once per store

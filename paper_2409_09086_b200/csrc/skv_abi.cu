@@ -71,7 +71,7 @@ static int last_delay_env() {
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("SKV_LAST_DELAY");
-    env = e ? atoi(e) : 0;
+    env = e ? atoi(e) : -1;
   }
   return env;
 }
@@ -80,6 +80,14 @@ static int use_tc_wide() {  // SKV_TC_WIDE=1: throughput launches on the tensor-
   if (env < 0) {
     const char* e = getenv("SKV_TC_WIDE");
     env = e ? atoi(e) : 0;
+  }
+  return env;
+}
+static int use_tcd() {  // SKV_TCD=0: dynamic-schedule launches on the CUDA-core decode kernel
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_TCD");
+    env = e ? atoi(e) : 1;
   }
   return env;
 }
@@ -124,6 +132,7 @@ struct skv_ctx {
   unsigned long long* lay_tl = nullptr;  // instrumentation: persistent decode timeline (skv_layers_timeline)
   std::map<int, int> cluster_fit;  // (G, chunk tiles, cluster size) -> co-resident clusters
   int launch_seq = 0;   // decode launches (selects the scheduler slot)
+  const char* last_kernel = "";  // the last decode launch's kernel (skv_last_decode_kernel)
   int32_t* sched = nullptr;  // [64][4] per-launch ticket / barrier / exit counters
   int32_t* done = nullptr;   // [64] per-launch completion flags
   size_t part_floats = 0;    // one parity half of the double-buffered partials
@@ -484,6 +493,8 @@ int skv_timing(skv_ctx* x, int enable) {
   return SKV_OK;
 }
 
+const char* skv_last_decode_kernel(const skv_ctx* x) { return x ? x->last_kernel : ""; }
+
 int skv_layers_timeline(skv_ctx* x, uint64_t* buf_dev) {
   if (!x) return fail(SKV_EINVAL, "null argument");
   x->lay_tl = reinterpret_cast<unsigned long long*>(buf_dev);
@@ -573,7 +584,7 @@ static int last_delay(const skv_ctx* x, int ctas, int nc);
 struct DecodePlan {
   AttnArgs a;
   int record, n, nt, ch, nc, ctas, par;
-  bool stat, tc;
+  bool stat, tc, tcd;
 };
 
 static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, const void* v, const int64_t* pos_dev,
@@ -725,7 +736,10 @@ static int prepare_layer(skv_ctx* x, int layer, const void* q, const void* k, co
   plan.par = par;
   plan.stat = stat || wide;
   plan.tc = wide || (stat && x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && ch <= 4 && use_tc_decode());
-  if (plan.tc) {
+  // dynamic schedule on the tensor cores (decode_tcd_kernel)
+  plan.tcd = !plan.tc && !stat && use_tcd() && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 &&
+             (x->G == 1 || x->G == 2 || x->G == 4 || x->G == 8);
+  if (plan.tc || plan.tcd) {
     plan.a.L = x->L;
     plan.a.layer = layer;
     plan.a.cap = x->cap;
@@ -763,9 +777,12 @@ static int decode_layer_impl(skv_ctx* x, int layer, const void* q, const void* k
   DecodePlan p;
   int rc = prepare_layer(x, layer, q, k, v, pos_dev, out, record, st, p);
   if (rc) return rc;
-  cudaError_t e = p.tc ? launch_decode_tc(x->G, p.ctas, p.a, st) : launch_decode(x->cfg.dtype, x->D, x->G, p.ctas, p.a, st);
+  cudaError_t e = p.tc    ? launch_decode_tc(x->G, p.ctas, p.a, st)
+                  : p.tcd ? launch_decode_tcd(x->G, p.ctas, p.a, st)
+                          : launch_decode(x->cfg.dtype, x->D, x->G, p.ctas, p.a, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
   x->launches += 2;  // decode + segment merge
+  x->last_kernel = p.tc ? "decode_tc_kernel" : p.tcd ? "decode_tcd_kernel" : "decode_kernel";
   x->last_layer = layer;
   x->layers_chain = false;
   commit_layer(x, layer, p);
@@ -1031,6 +1048,7 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   }
   if (e != cudaSuccess) return cuda_fail(e, "decode (all layers) kernel launch");
   x->launches += 1;
+  x->last_kernel = cluster ? "decode_tc_cluster_kernel" : "decode_tc_layers_kernel";
   x->last_layer = -1;
   x->layers_chain = true;
   for (int l = 0; l < x->L; ++l) commit_layer(x, l, p);

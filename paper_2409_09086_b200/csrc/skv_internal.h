@@ -134,6 +134,8 @@ cudaError_t launch_decode_tc_layers(int group, int ctas, const AttnArgs& a, cons
 // clusters can be co-resident
 cudaError_t launch_decode_tc_cluster(int group, int mt, const AttnArgs& a, const LayerSteps& ls, cudaStream_t st,
                                      int* max_clusters = nullptr);
+// dynamic-schedule launches (bf16, D = 128, any group) on mma.sync: decode_tcd_kernel + merge
+cudaError_t launch_decode_tcd(int group, int ctas, const AttnArgs& a, cudaStream_t st);
 // static-schedule GQA launches (bf16, D = 128, group 4 or 8, chunks <= 4 tiles) on mma.sync
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st);
 // the segment merge alone (PDL), after a decode launch

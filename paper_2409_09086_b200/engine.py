@@ -128,6 +128,11 @@ class StreamEngine:
     def kernel_launches(self) -> int:
         return int(self.lib.skv_kernel_launches(self._h))
 
+    @property
+    def last_decode_kernel(self) -> str:
+        """The kernel the last decode launch ran (decode_tcd_kernel, decode_tc_cluster_kernel, ...)."""
+        return self.lib.skv_last_decode_kernel(self._h).decode()
+
     # -------------------------------------------------------------- decode --
     def _check_io(self, q, k, v, out, lead):
         c = self.cfg

@@ -98,6 +98,10 @@ class KvHeadEngine:
         o2 = None if out is None else out.view(*lead, S * Hkv, G, D)
         return q2, k2, v2, o2
 
+    @property
+    def last_decode_kernel(self) -> str:
+        return self.inner.last_decode_kernel
+
     def decode_step(self, q, k, v, out=None, record: bool = True):
         c = self.cfg
         if out is None:

@@ -5,6 +5,8 @@ state dump, and caches longer than the segment merge's chunk limit.
 Each case either compares against the CPU oracle (tests infrastructure) or
 asserts the reference's error behaviour (ValueError for domain errors)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -406,3 +408,33 @@ def test_full_size_config1_period_is_deterministic():
         eng.close()
     for a_, b_ in zip(*results):
         assert torch.equal(a_, b_)
+
+
+def test_dynamic_decode_kernels_both_match_oracle():
+    """Throughput launches (dynamic chunk tickets) run decode_tcd_kernel (tensor
+    cores) by default and decode_kernel (CUDA cores) with SKV_TCD=0: the
+    config-1 sampled-lane and baseline-shape parity tests, in a subprocess per
+    setting (the switch is read once per process), plus the kernel the engine
+    reports."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for flag, want in (("1", "decode_tcd_kernel"), ("0", "decode_kernel")):
+        env = dict(os.environ, SKV_TCD=flag)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                            os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                            "sampled_lanes or baseline_shapes or instantiations"],
+                           env=env, cwd=root, capture_output=True, text=True, timeout=1200)
+        assert r.returncode == 0, (flag, r.stdout[-3000:], r.stderr[-2000:])
+        probe = ("import torch; from paper_2409_09086_b200 import EngineConfig, StreamEngine\n"
+                 "e = StreamEngine(EngineConfig(8, 2, 32, 32, 128, 1024, 1024, 0.01, 32, 2200, torch.bfloat16))\n"
+                 "for s in range(8):\n"
+                 "    for l in range(2):\n"
+                 "        e.lib.skv_state_inject(e._h, s, l, 2048, None, None, None, 0, None, None)\n"
+                 "q = torch.randn((2, 8, 32, 128), device='cuda').bfloat16()\n"
+                 "e.decode_step(q, q, q)\nprint(e.last_decode_kernel)")
+        r = subprocess.run([sys.executable, "-c", probe], env=env, cwd=root, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert r.stdout.strip().splitlines()[-1] == want, (flag, r.stdout)
