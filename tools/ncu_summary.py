@@ -3,7 +3,7 @@
 usage: python tools/ncu_summary.py out.json report1.ncu-rep [report2.ncu-rep ...]
 Keeps, per profiled launch: duration, DRAM bytes read/written, DRAM and tensor
 pipe utilisation, issue activity, occupancy, registers and grid size.  The
-first decode_kernel launch's DRAM bytes become decode_traffic_bytes_per_launch
+first decode_tcd_kernel / decode_kernel launch's DRAM bytes become decode_traffic_bytes_per_launch
 (bench.py's roofline "traffic")."""
 import csv
 import io
@@ -47,7 +47,7 @@ def main():
                 if m in d:
                     k[m] = [d[m][0], d[m][1]]
             kernels.append(k)
-            if traffic is None and "decode_kernel" in k["kernel"]:
+            if traffic is None and ("decode_tcd_kernel" in k["kernel"] or "decode_kernel" in k["kernel"]):
                 b = 0.0
                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     x, u = d[m]
