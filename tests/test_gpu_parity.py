@@ -146,8 +146,15 @@ def _inject_random(eng, orc, rng, n0, c, dt_name):
         # BASELINE config 4's two largest budgets (l = r = B/2, E = 128)
         dict(S=1, L=1, Hq=32, Hkv=32, D=128, l=2048, r=2048, W=32, b=0.01, E=128, dtype="bf16", periods=2),
         dict(S=1, L=1, Hq=32, Hkv=32, D=128, l=4096, r=4096, W=32, b=0.01, E=128, dtype="bf16", periods=2),
+        # GQA groups 2 / 4 / 8 with enough segments for the dynamic (decode_tcd_kernel) schedule
+        dict(S=4, L=1, Hq=32, Hkv=16, D=128, l=2048, r=2048, W=32, b=0.01, E=64, dtype="bf16", periods=1,
+             kernel="decode_tcd_kernel"),
+        dict(S=4, L=1, Hq=32, Hkv=8, D=128, l=2048, r=2048, W=32, b=0.01, E=64, dtype="bf16", periods=1,
+             kernel="decode_tcd_kernel"),
+        dict(S=4, L=1, Hq=64, Hkv=8, D=128, l=2048, r=2048, W=32, b=0.01, E=64, dtype="bf16", periods=1,
+             kernel="decode_tcd_kernel"),
     ],
-    ids=["cfg1-shape", "cfg3-shape", "cfg4-B4096", "cfg4-B8192"],
+    ids=["cfg1-shape", "cfg3-shape", "cfg4-B4096", "cfg4-B8192", "gqa2-dynamic", "gqa4-dynamic", "gqa8-dynamic"],
 )
 def test_baseline_shapes_state_injection(shape):
     """State-injection parity at BASELINE per-layer shapes: inject a full cache,
@@ -173,6 +180,8 @@ def test_baseline_shapes_state_injection(shape):
             got = eng.decode_step(_dev(q, dt), _dev(k, dt), _dev(v, dt), record=True).cpu().numpy()
             want = orc.step(q, k, v)
             worst_out = max(worst_out, rel_err(got, want))
+            if "kernel" in c and os.environ.get("SKV_TCD", "1") != "0":
+                assert eng.last_decode_kernel == c["kernel"], eng.last_decode_kernel
         n = eng.length(0, 0)
         for s in range(c["S"]):
             for layer in range(c["L"]):
