@@ -377,6 +377,9 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
   // [4][S*Hkv]: per-launch slot (seq % 4) -- the merge of launch N+1 may be
   // resident (PDL) before launch N's merge has reset its counters
   chk(x->alloc(&x->counters, (size_t)4 * x->S * x->Hkv * sizeof(int32_t)));
+  // all-layer decode counters ([S*Hkv] segments, [L] layer_done, exit), here so
+  // that no allocation happens inside a caller's stream capture
+  chk(x->alloc(&x->lay_cnt, ((size_t)x->S * x->Hkv + x->L + 1) * sizeof(int32_t)));
   chk(x->alloc(&x->kept, SL * x->B * sizeof(int32_t)));
   chk(x->alloc(&x->first_moved, SL * sizeof(int32_t)));
   chk(x->alloc(&x->scores, SL * x->cap * sizeof(float)));
@@ -962,15 +965,28 @@ static int use_layers_kernel() {
 // when every layer is in the same state and its decode would run on the
 // static tensor-core schedule (latency-bound GQA steps, config 3).  Returns
 // 1 when launched, 0 to fall back to per-layer launches.
-static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
-                              cudaStream_t st) {
-  if (x->L < 2 || !use_layers_kernel() || x->cfg.rope_mode != SKV_ROPE_NONE || x->timing) return 0;
+// Whether a decode step of every layer may run as one all-layer launch (the
+// cluster fit is decided by decode_step_layers itself).
+static bool layers_eligible(const skv_ctx* x) {
+  if (x->L < 2 || !use_layers_kernel() || x->cfg.rope_mode != SKV_ROPE_NONE || x->timing) return false;
   for (int l = 0; l < x->L; ++l)
     if (x->ragged[l] || x->n[l] != x->n[0] || x->parity[l] != x->parity[0] || x->pend_n[l] != x->pend_n[0] ||
         x->pend_slot[l] != x->pend_slot[0] || x->pend_par[l] != x->pend_par[0] || x->whead[l] != x->whead[0] ||
         x->wcount[l] != x->wcount[0] || x->round_value[l] != x->round_value[0])
-      return 0;
-  if (!(x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && use_tc_decode())) return 0;
+      return false;
+  return x->G >= 4 && x->cfg.dtype == SKV_DTYPE_BF16 && x->D == 128 && use_tc_decode();
+}
+
+// The all-layer launch's counters (allocated outside any stream capture).
+static int ensure_layer_counters(skv_ctx* x) {
+  if (x->lay_cnt) return SKV_OK;
+  cudaError_t e = x->alloc(&x->lay_cnt, ((size_t)x->S * x->Hkv + x->L + 1) * sizeof(int32_t));
+  return e == cudaSuccess ? SKV_OK : cuda_fail(e, "layer counters");
+}
+
+static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
+                              cudaStream_t st) {
+  if (!layers_eligible(x)) return 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1013,10 +1029,7 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
   }
   if (!cluster && (!p.tc || p.ctas != segs * p.nc || p.ctas > sms || use_layers_kernel() != 2))
     return 0;  // per-layer launches
-  if (!x->lay_cnt) {
-    cudaError_t e = x->alloc(&x->lay_cnt, ((size_t)x->S * x->Hkv + x->L + 1) * sizeof(int32_t));
-    if (e != cudaSuccess) return cuda_fail(e, "layer counters");
-  }
+  if (!x->lay_cnt) return fail(SKV_ESTATE, "layer counters not allocated");
   LayerSteps ls{};
   ls.L = x->L;
   ls.q_ls = (int64_t)x->S * x->Hq * x->D;
@@ -1058,6 +1071,10 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
 int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record, void* stream) {
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
   cudaStream_t st = as_stream(stream);
+  if (layers_eligible(x)) {
+    const int ec = ensure_layer_counters(x);
+    if (ec) return ec;
+  }
   {
     const int rc = decode_step_layers(x, q, k, v, out, record, st);
     if (rc < 0) return rc;
@@ -1104,6 +1121,10 @@ static int host_step_graph(skv_ctx* x, const void* q, const void* k, const void*
   // 18.2 K vs 17.0 K tokens/s), the graph pays off for deep models (config 3)
   if (x->L < 4) return 0;
   if (!pinned_host(q) || !pinned_host(k) || !pinned_host(v) || !pinned_host(out)) return 0;
+  if (layers_eligible(x)) {
+    const int ec = ensure_layer_counters(x);
+    if (ec) return ec;
+  }
   const skv_ctx::Mirror pre = x->snap();
   skv_ctx::HostGraph* hg = nullptr;
   for (auto& e : x->hgraphs)
@@ -1134,10 +1155,14 @@ static int host_step_graph(skv_ctx* x, const void* q, const void* k, const void*
     ck(cudaMemcpyAsync(x->stage_q, q, qb * L, cudaMemcpyHostToDevice, s_c));
     ck(cudaMemcpyAsync(x->stage_k, k, kb * L, cudaMemcpyHostToDevice, s_c));
     ck(cudaMemcpyAsync(x->stage_v, v, kb * L, cudaMemcpyHostToDevice, s_c));
-    for (int l = 0; l < x->L && rc == SKV_OK; ++l)
-      rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb, static_cast<char*>(x->stage_k) + l * kb,
-                             static_cast<char*>(x->stage_v) + l * kb, nullptr, x->stage_out + l * (ob / sizeof(float)),
-                             record, s_c);
+    if (rc == SKV_OK) {  // every layer in one launch where the engine allows it (latency-bound GQA)
+      const int lr = decode_step_layers(x, x->stage_q, x->stage_k, x->stage_v, x->stage_out, record, s_c);
+      if (lr < 0) rc = lr;
+      for (int l = 0; lr == 0 && l < x->L && rc == SKV_OK; ++l)
+        rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb, static_cast<char*>(x->stage_k) + l * kb,
+                               static_cast<char*>(x->stage_v) + l * kb, nullptr,
+                               x->stage_out + l * (ob / sizeof(float)), record, s_c);
+    }
     ck(cudaMemcpyAsync(out, x->stage_out, ob * L, cudaMemcpyDeviceToHost, s_c));
     cudaGraph_t g = nullptr;
     cudaError_t ee = cudaStreamEndCapture(s_c, &g);
@@ -1235,6 +1260,25 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
       SKV_CK(cudaStreamSynchronize(s_c));
       return check_sticky(x);
     }
+  }
+  if (layers_eligible(x)) {
+    // all layers in one launch (decode_step_layers): whole-token copies around it
+    const int ec = ensure_layer_counters(x);
+    if (ec) return ec;
+    SKV_CK(cudaMemcpyAsync(x->stage_q, q, qb * x->L, cudaMemcpyHostToDevice, s_c));
+    SKV_CK(cudaMemcpyAsync(x->stage_k, k, kb * x->L, cudaMemcpyHostToDevice, s_c));
+    SKV_CK(cudaMemcpyAsync(x->stage_v, v, kb * x->L, cudaMemcpyHostToDevice, s_c));
+    const int lr = decode_step_layers(x, x->stage_q, x->stage_k, x->stage_v, x->stage_out, record, s_c);
+    if (lr < 0) return lr;
+    for (int l = 0; lr == 0 && l < x->L; ++l) {  // the clusters do not fit: per-layer launches
+      const int rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb,
+                                       static_cast<char*>(x->stage_k) + l * kb, static_cast<char*>(x->stage_v) + l * kb,
+                                       nullptr, x->stage_out + l * (ob / sizeof(float)), record, s_c);
+      if (rc) return rc;
+    }
+    SKV_CK(cudaMemcpyAsync(out, x->stage_out, ob * x->L, cudaMemcpyDeviceToHost, s_c));
+    SKV_CK(cudaStreamSynchronize(s_c));
+    return check_sticky(x);
   }
   // Layers in (up to) four groups: one copy per tensor and group in, one out,
   // so the copies of group i+1 / i-1 overlap group i's kernels while the host

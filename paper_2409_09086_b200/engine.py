@@ -33,7 +33,12 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_handle(stream: Optional[torch.cuda.Stream] = None):
+    if stream is None and _raw_stream is not None:  # (no Stream object per call: host steps are latency-bound)
+        return _raw_stream(torch.cuda.current_device())
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
 
@@ -192,14 +197,19 @@ class StreamEngine:
         Work already enqueued on the current torch stream (evictions, prefill
         chunks) is ordered before it."""
         c = self.cfg
-        lead = (c.layers, c.streams)
-        for name, t, heads in (("q", q, c.heads_q), ("k", k, c.heads_kv), ("v", v, c.heads_kv)):
-            if tuple(t.shape) != (*lead, heads, c.head_dim) or t.dtype != c.dtype or t.is_cuda:
-                raise ValueError(f"{name} must be a host {c.dtype} tensor of shape {(*lead, heads, c.head_dim)}")
+        shapes = self.__dict__.get("_host_shapes")
+        if shapes is None:
+            lead = (c.layers, c.streams)
+            shapes = self._host_shapes = ((*lead, c.heads_q, c.head_dim), (*lead, c.heads_kv, c.head_dim))
+        for name, t, shp in (("q", q, shapes[0]), ("k", k, shapes[1]), ("v", v, shapes[1])):
+            if t.shape != shp or t.dtype != c.dtype or t.is_cuda:
+                raise ValueError(f"{name} must be a host {c.dtype} tensor of shape {shp}")
         if out.is_cuda or out.dtype != torch.float32:
             raise ValueError("out must be a host float32 tensor")
-        check(self.lib.skv_decode_step_host(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), int(bool(record)),
-                                            _stream_handle()))
+        rc = self.lib.skv_decode_step_host(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                           1 if record else 0, _stream_handle())
+        if rc < 0:
+            check(rc)
         return out
 
     # --------------------------------------------------------------- evict --
