@@ -288,6 +288,12 @@ __global__ void __launch_bounds__(pf::THREADS, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align up by offset from the array (keeps the shared state space: LDS/STS, not generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  if (a.meta_len && blockIdx.x == 0 && threadIdx.x == 0) {  // the chunk's lengths / next positions
+    for (int s = 0; s < a.S; ++s) {
+      a.meta_len[s * a.meta_ss] = a.meta_n;
+      a.meta_next[s * a.meta_ss] += a.C;
+    }
+  }
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SBAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;            // [KST]
@@ -912,7 +918,8 @@ namespace skv {
 // Appends a C-token chunk's k/v ([S][C][Hkv][D] rows) to cache slots
 // [n0, n0+C) of every (stream, kv-head) segment with token metadata
 // (KvCache.append, cache.py:112-134, for C tokens at once).  Grid (C, S);
-// thread t copies 16 bytes of one head's row.
+// thread t copies 16 bytes of one head's row.  The streams' lengths and next
+// positions are stored by the prefill kernel that follows (PrefillArgs.meta_*).
 __global__ void append_chunk_kernel(const uint4* __restrict__ kin, const uint4* __restrict__ vin, uint4* kc, uint4* vc,
                                     int64_t c_ss, int64_t c_hs, int Hkv, int units, int n0, int C, int64_t* pos,
                                     int8_t* modality, int32_t* round_id, int64_t m_ss, const int64_t* next_pos,
@@ -1232,19 +1239,11 @@ cudaError_t launch_fold_rows(int streams, int rows, const FoldArgs& f, int Hq, i
   return cudaGetLastError();
 }
 
-// After the chunk: lengths and the next original position of every stream.
-__global__ void chunk_meta_kernel(int32_t* len, int64_t* next_pos, int64_t ss, int n, int C, int S) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < S) {
-    len[s * ss] = n;
-    next_pos[s * ss] += C;
-  }
-}
-
 cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
                                 int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,
                                 int8_t* modality, int32_t* round_id, int64_t m_ss, int64_t* next_pos, int32_t* len,
                                 int64_t ss, int mod, int rnd, cudaStream_t st, const void* kraw_in, void* kraw_c) {
+  (void)len;  // (stored by the prefill kernel after this one)
   dim3 grid(C, S);
   const int threads = std::min(1024, ((Hkv * units + 31) / 32) * 32);
   append_chunk_kernel<<<grid, threads, 0, st>>>(static_cast<const uint4*>(kin), static_cast<const uint4*>(vin),
@@ -1252,9 +1251,6 @@ cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void
                                                 c_hs_units, Hkv, units, n0, C, pos, modality, round_id, m_ss, next_pos,
                                                 ss, mod, rnd, static_cast<const uint4*>(kraw_in),
                                                 static_cast<uint4*>(kraw_c));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  chunk_meta_kernel<<<(S + 127) / 128, 128, 0, st>>>(len, next_pos, ss, n0 + C, C, S);
   return cudaGetLastError();
 }
 

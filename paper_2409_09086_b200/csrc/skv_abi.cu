@@ -895,6 +895,10 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
   a.lg_t = 1;
   a.st = wrec ? x->pstats : nullptr;
   a.ovf = x->err_word;  // |v| >= 65504 saturates the fp16 V: sticky error (skv_sync)
+  a.meta_len = x->len + layer;  // the chunk's lengths / next positions (after the append read them)
+  a.meta_next = x->next_pos + layer;
+  a.meta_ss = SLs;
+  a.meta_n = n0 + C;
   e = launch_prefill(q, x->S, x->k, x->v, (int64_t)x->S * x->L * x->Hkv * x->cap, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "prefill kernel launch");
   x->launches += 3;

@@ -269,6 +269,10 @@ struct PrefillArgs {
   int S;                // streams (CTA order 1)
   int lg_t;             // 1: lg is [S][Hq][lg_cap/4][W][4] raw q.k (unscaled; column quads outermost: the
                         // recorded rows of a warp store 512 contiguous bytes per quad); lg_cap % 128 == 0
+  int32_t* meta_len;    // optional (engine chunks): the streams' lengths := meta_n and next
+  int64_t* meta_next;   //   original positions += C (stride meta_ss), stored by CTA 0 -- after
+  int64_t meta_ss;      //   the chunk's append kernel, which read next_pos, in stream order
+  int meta_n;
 };
 
 #include <cuda.h>
@@ -287,8 +291,8 @@ cudaError_t launch_fold_rows_t(int streams, int rows, const FoldArgs& f, int Hq,
 cudaError_t launch_append_chunk(const void* kin, const void* vin, void* kc, void* vc, int64_t c_ss_units,
                                 int64_t c_hs_units, int S, int Hkv, int units, int n0, int C, int64_t* pos,
                                 int8_t* modality, int32_t* round_id, int64_t m_ss, int64_t* next_pos, int32_t* len,
-                                int64_t ss, int mod, int rnd, cudaStream_t st, const void* kraw_in = nullptr,
-                                void* kraw_c = nullptr);
+                                int64_t ss, int mod, int rnd, cudaStream_t st, const void* kraw_in,
+                                void* kraw_c);
 
 // ----------------------------------------------------------------------------
 // RoPE (RoPE-enabled engines): rotate q / new k, and raw -> rotated key rows
