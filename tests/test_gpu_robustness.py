@@ -306,12 +306,15 @@ def test_all_layer_persistent_decode_matches_oracle(G, L, l, E, periods):
     assert worst <= 2e-3 and worst_row <= 2e-3
 
 
-def test_host_step_graph_cache_over_periods():
-    """skv_decode_step_host runs each token as one CUDA graph cached per
-    engine state: over three eviction periods the states repeat (cache hits
-    rebind only the copy nodes to new pinned buffers).  Outputs every token,
-    kept sets every period, against the oracle."""
-    S, L, Hq, Hkv, D = 2, 3, 8, 2, 128
+@pytest.mark.parametrize("L", [3, 4], ids=["eager-L3", "graph-L4"])
+def test_host_step_graph_cache_over_periods(L):
+    """skv_decode_step_host (from the engine's very first call) over three
+    eviction periods: L = 4 runs each token as one CUDA graph cached per engine
+    state (cache hits rebind only the copy nodes to new pinned buffers; the
+    all-layer cluster launch and its fit query are captured), L = 3 the eager
+    whole-token path.  Outputs every token, kept sets every period, against
+    the oracle."""
+    S, Hq, Hkv, D = 2, 8, 2, 128
     l, r, W, E = 32, 32, 8, 16
     B = l + r
     cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
