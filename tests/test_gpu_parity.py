@@ -426,15 +426,19 @@ def test_baseline_policy_dropins_match_oracle():
         np.testing.assert_array_equal(got.relevant, want.relevant)
 
 
-@pytest.mark.parametrize("mode", ["cache_relative", "original"])
-def test_rope_bf16_engine_vs_oracle(mode):
+@pytest.mark.parametrize("mode,S,Hq,Hkv", [("cache_relative", 2, 8, 2), ("original", 2, 8, 2),
+                                            ("cache_relative", 40, 32, 8)],
+                         ids=["cache_relative", "original", "cache_relative-dynamic"])
+def test_rope_bf16_engine_vs_oracle(mode, S, Hq, Hkv):
     """bf16 RoPE engine (pre-rotation q/k in; raw keys cached; rotated keys
     attended; cache-relative re-rotation after each compaction) against the
     oracle restating the reference rotary helpers, with the bf16 rounding of
-    the rotated q / k a bf16 engine stores."""
+    the rotated q / k a bf16 engine stores.  The dynamic case has enough
+    segments for the throughput kernel (decode_tcd_kernel, raw keys appended
+    by its producer)."""
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
 
-    S, L, Hq, Hkv, D = 2, 2, 8, 2, 128
+    L, D = 2, 128
     l, r, W, E, T = 64, 64, 16, 32, 224
     cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
     eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, l + r + E, torch.bfloat16, rope=mode,
@@ -453,6 +457,8 @@ def test_rope_bf16_engine_vs_oracle(mode):
             eng.decode_layer(layer, _dev(q[layer], torch.bfloat16), _dev(k[layer], torch.bfloat16),
                              _dev(v[layer], torch.bfloat16), out, record=True)
             worst = max(worst, rel_err(out.cpu().numpy(), want))
+            if S * Hkv > 296 and os.environ.get("SKV_TCD", "1") != "0":
+                assert eng.last_decode_kernel == "decode_tcd_kernel", eng.last_decode_kernel
         orc.advance()
         if (t + 1) % E == 0:
             n = orc.length(0, 0)
