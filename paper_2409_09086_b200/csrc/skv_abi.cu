@@ -1251,6 +1251,23 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
     chk(cudaEventCreateWithFlags(&x->ev_entry, cudaEventDisableTiming));
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
   }
+  if (x->L <= 2) {
+    cudaStream_t sc = as_stream(stream);  // (ordered after the caller's work: no event)
+    // shallow models (config 0): the whole token on the caller's stream -- copies in,
+    // the layers' launches, the copy out, one synchronisation
+    SKV_CK(cudaMemcpyAsync(x->stage_q, q, qb * x->L, cudaMemcpyHostToDevice, sc));
+    SKV_CK(cudaMemcpyAsync(x->stage_k, k, kb * x->L, cudaMemcpyHostToDevice, sc));
+    SKV_CK(cudaMemcpyAsync(x->stage_v, v, kb * x->L, cudaMemcpyHostToDevice, sc));
+    for (int l = 0; l < x->L; ++l) {
+      const int rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb,
+                                       static_cast<char*>(x->stage_k) + l * kb, static_cast<char*>(x->stage_v) + l * kb,
+                                       nullptr, x->stage_out + l * (ob / sizeof(float)), record, sc);
+      if (rc) return rc;
+    }
+    SKV_CK(cudaMemcpyAsync(out, x->stage_out, ob * x->L, cudaMemcpyDeviceToHost, sc));
+    SKV_CK(cudaStreamSynchronize(sc));
+    return check_sticky(x);
+  }
   cudaStream_t s_in = x->hs[0], s_c = x->hs[1], s_out = x->hs[2];
   // work the caller enqueued before this call (an eviction, a prefill chunk,
   // a state injection) completes before the pipeline reads or writes the cache
