@@ -915,7 +915,8 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
     if (a.fold.n > 0) {
       griddep_wait();
       const int P = gridDim.x, c = blockIdx.x;
-      const int ppc = (a.fold.n + 63) / 64;
+      const int pw = 64 * fold_cols_per_pass(a.Hq);  // (wider pieces for few heads per stream)
+      const int ppc = (a.fold.n + pw - 1) / pw;
       for (int l = 0; l < ls.L; ++l) {
         FoldArgs f = a.fold;
         f.logits += l * ls.lg_ls;
@@ -923,14 +924,14 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
         f.rows += l * ls.fr_ls;
         if (f.wlen) f.wlen += l * ls.fw_ls;
         for (int piece = c; piece < a.S * ppc; piece += P) {
-          const int s2 = piece / ppc, col0 = (piece - s2 * ppc) * 64;
+          const int s2 = piece / ppc, col0 = (piece - s2 * ppc) * pw;
           const float* stt = f.stats + s2 * f.st_ss;
           for (int h = lane; h < a.Hq; h += 32) {
             fstats[2 * h] = __ldg(stt + 2 * h);
             fstats[2 * h + 1] = __frcp_rn(__ldg(stt + 2 * h + 1));  // staged as 1/L
           }
           __syncwarp();
-          fold_columns(f, s2, col0, min(col0 + 64, f.n), a.Hq, lane, 32, fstats);
+          fold_columns(f, s2, col0, min(col0 + pw, f.n), a.Hq, lane, 32, fstats);
           __syncwarp();
           if (col0 == 0 && lane == 0 && f.wlen) f.wlen[s2 * f.w_ss] = f.n;
         }

@@ -21,6 +21,51 @@ __device__ __forceinline__ float fold_prob(float x, float M, float rL) { return 
 // mode 2 may alias the logits as far as the compiler knows, so without the
 // explicit batch every load waited for the previous head's store (a 64-column
 // piece of 32 heads took ~30 us in a decode kernel's fold warp).
+// Few heads (a KV-head group as a stream): CB columns per thread per pass, all
+// their CB x Hq logit loads in flight together (same per-column arithmetic).
+template <int CB, int HMAX>
+__device__ __forceinline__ void fold_columns_few(const FoldArgs& f, int s, const float* lg, const float* stt,
+                                                 bool staged, float* row, int c0, int c1, int Hq, int tid,
+                                                 int nthreads) {
+  for (int jb = c0 + tid; jb < c1; jb += nthreads * CB) {
+    float x[CB][HMAX];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      const int j = jb + c * nthreads;
+#pragma unroll
+      for (int h = 0; h < HMAX; ++h) x[c][h] = (h < Hq && j < c1) ? __ldcs(lg + (int64_t)h * f.l_hs + j) : 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      const int j = jb + c * nthreads;
+      if (j >= c1) continue;
+      float acc = f.mode == 1 ? -INFINITY : 0.f;
+#pragma unroll
+      for (int h = 0; h < HMAX; ++h) {
+        if (h < Hq) {
+          const float M = stt[2 * h];
+          const float rL = staged ? stt[2 * h + 1] : __frcp_rn(stt[2 * h + 1]);
+          const float p = fold_prob(x[c][h], M, rL);
+          if (f.mode == 2) {
+            f.probs[s * f.p_ss + h * f.p_hs + j] = p;
+          } else if (f.mode == 1) {
+            acc = fmaxf(acc, p);
+          } else {
+            acc = __fadd_rn(acc, p);
+          }
+        }
+      }
+      if (f.mode != 2) {
+        const float v = f.mode == 0 ? __fdiv_rn(acc, (float)(f.agg_div ? f.agg_div : Hq)) : acc;
+        row[j] = (f.accum && j < f.n - 1) ? __fadd_rn(row[j], v) : v;
+      }
+    }
+  }
+}
+
+// columns one pass of fold_columns covers per thread (pieces of a fold warp)
+__host__ __device__ __forceinline__ int fold_cols_per_pass(int Hq) { return Hq <= 4 ? 4 : Hq <= 8 ? 2 : 1; }
+
 template <int HB = 16>
 __device__ __forceinline__ void fold_columns(const FoldArgs& f, int s, int c0, int c1, int Hq, int tid, int nthreads,
                                              const float* stt = nullptr) {
@@ -28,6 +73,8 @@ __device__ __forceinline__ void fold_columns(const FoldArgs& f, int s, int c0, i
   const float* lg = f.logits + s * f.l_ss;
   if (!stt) stt = f.stats + s * f.st_ss;
   float* row = f.rows ? f.rows + s * f.r_ss : nullptr;
+  if (Hq <= 4) return fold_columns_few<4, 4>(f, s, lg, stt, staged, row, c0, c1, Hq, tid, nthreads);
+  if (Hq <= 8) return fold_columns_few<2, 8>(f, s, lg, stt, staged, row, c0, c1, Hq, tid, nthreads);
   for (int j = c0 + tid; j < c1; j += nthreads) {
     float acc = f.mode == 1 ? -INFINITY : 0.f;
     for (int h0 = 0; h0 < Hq; h0 += HB) {
