@@ -19,10 +19,10 @@ k = torch.randn((8, L, S, Hkv, D), device="cuda").to(torch.bfloat16)
 v = torch.randn((8, L, S, Hkv, D), device="cuda").to(torch.bfloat16)
 tl = torch.zeros((L, 148, 16), dtype=torch.int64, device="cuda")
 for t in range(4):
-    eng.decode_step(q[t], k[t], v[t], record=False)
+    eng.decode_step(q[t], k[t], v[t], record=bool(int(os.environ.get("REC", "0"))))
 torch.cuda.synchronize()
 eng.lib.skv_layers_timeline(eng._h, tl.data_ptr())
-eng.decode_step(q[5], k[5], v[5], record=False)
+eng.decode_step(q[5], k[5], v[5], record=bool(int(os.environ.get("REC", "0"))))
 torch.cuda.synchronize()
 a = tl.cpu().numpy()
 P = int((a[0, :, 0] > 0).sum())
