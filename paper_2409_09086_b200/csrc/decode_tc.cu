@@ -729,17 +729,18 @@ __global__ void __launch_bounds__(tcd::THREADS, 1)
 // segment: cluster rank j owns chunk j (tiles [j ch, (j+1) ch)) in every layer,
 // so the cluster's CTAs are co-resident for the whole token and the segment
 // merge runs over distributed shared memory instead of a global round trip:
-//   * every rank writes its chunk partial (o, m, l per query head) into its own
-//     shared memory (double-buffered by layer parity) and arrives, with cluster
-//     release semantics, on every rank's `ready` mbarrier;
-//   * every rank waits on its own `ready`, then merges a slice of the segment's
-//     output elements reading all ranks' partials with ld.shared::cluster
-//     (merge_kernel's arithmetic: chunk weights rescale(m_j, M), L = sum w_j l_j,
+//   * every rank combines its warps' partials (staged in the K rows each warp
+//     scored) and pushes the chunk partial of each output element straight
+//     into the owning rank's receive buffer (st.async, completing bytes on that
+//     rank's `ready` mbarrier), and its (m, l) per head to every rank;
+//   * every rank waits on its own `ready` (its expected byte count), merges its
+//     slice of the segment's outputs from local shared memory (merge_kernel's
+//     arithmetic: chunk weights rescale(m_j, M), L = sum w_j l_j,
 //     out = sum_j w_j o_j / L in chunk order), stores them and releases
 //     layer_done[l] (target: segments x ranks);
 //   * layer l+1's consumers wait for layer_done[l] (the model's dependency),
 //     while the producer has already streamed layer l+1's K/V into the tiles
-//     freed by layer l.
+//     freed by layer l, and its warp appends layer l's token.
 template <int G, int MT>
 struct ClSmem {
   static constexpr int NWC = 2 * MT;                        // consumer warps (32 keys each)
@@ -773,11 +774,6 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
-}
-__device__ __forceinline__ float ld_cluster(uint32_t addr) {
-  float v;  // (ordered after the acquire wait by the barrier below it; no clobber so loads overlap)
-  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
-  return v;
 }
 // Asynchronous stores into a cluster peer's shared memory, completing bytes
 // on that peer's mbarrier (visible to it once the barrier phase completes).
