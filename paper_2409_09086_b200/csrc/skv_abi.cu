@@ -1301,17 +1301,32 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
     SKV_CK(cudaStreamSynchronize(s_c));
     return check_sticky(x);
   }
-  // Layers in (up to) four groups: one copy per tensor and group in, one out,
-  // so the copies of group i+1 / i-1 overlap group i's kernels while the host
-  // issues ~3x fewer runtime calls per token (batch-1 steps are host-bound).
+  // Layers in groups: one copy per tensor and group in, one out, so the copies
+  // of group i+1 / i-1 overlap group i's kernels while the host issues few
+  // runtime calls per token.  The first and the last group are one layer each:
+  // only layer 0's inputs and layer L-1's outputs cross PCIe unoverlapped.
   static int ngroups = -1;  // SKV_HOST_GROUPS overrides the group count
   if (ngroups < 0) {
     const char* e = getenv("SKV_HOST_GROUPS");
     ngroups = e ? std::max(1, atoi(e)) : 4;
   }
-  const int grp = std::max(1, (x->L + ngroups - 1) / ngroups);
-  for (int l0 = 0; l0 < x->L; l0 += grp) {
-    const int nl = std::min(grp, x->L - l0);
+  int bounds[66];
+  int nb = 0;
+  {
+    const int g = std::min(ngroups, std::min(x->L, 64));
+    bounds[nb++] = 0;
+    if (g >= 3) {
+      const int mid = x->L - 2, gm = g - 2;
+      bounds[nb++] = 1;
+      for (int i = 1; i <= gm; ++i) bounds[nb++] = 1 + (int)((int64_t)mid * i / gm);
+      bounds[nb++] = x->L;
+    } else {
+      for (int i = 1; i <= g; ++i) bounds[nb++] = (int)((int64_t)x->L * i / g);
+    }
+  }
+  for (int b = 0; b + 1 < nb; ++b) {
+    const int l0 = bounds[b], nl = bounds[b + 1] - l0;
+    if (nl <= 0) continue;
     SKV_CK(cudaMemcpyAsync(static_cast<char*>(x->stage_q) + l0 * qb, static_cast<const char*>(q) + l0 * qb, nl * qb,
                            cudaMemcpyHostToDevice, s_in));
     SKV_CK(cudaMemcpyAsync(static_cast<char*>(x->stage_k) + l0 * kb, static_cast<const char*>(k) + l0 * kb, nl * kb,
