@@ -982,18 +982,22 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
       }
       const uint32_t ph = l & 1;
       const bool any = ntile > 0;
+      // the token's new k/v row: loaded together with q by the one warp whose
+      // 32 keys hold slot n_old (lanes 0-15 k, 16-31 v) and written into its
+      // own tile rows -- no other warp reads them, so no CTA barrier
+      const int kk_new = a.n_old - k0;
+      const bool own_new = has_new && warp == (kk_new >> 5);
+      uint4 nrow = make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t nrow_off = own_new ? (uint32_t)((kk_new / TT) * TILE) + swz(kk_new % TT, lane & 15) : 0u;
+      if (own_new) {
+        const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(lane < 16 ? a.kin : a.vin) + l * ls.in_ls;
+        nrow = reinterpret_cast<const uint4*>(src + s * a.in_ss + (int64_t)g * D)[lane & 15];
+      }
       if (any) mbar_wait(kfull, ph);
       if (tl && tid == 0) stamp(1);
-      if (has_new) {
-        if (warp == 0) {
-          if (lane >= 16) mbar_wait(vfull, ph);
-          const int kk = a.n_old - k0, t = kk / TT, r = kk % TT;
-          const int cd = lane & 15;
-          const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(lane < 16 ? a.kin : a.vin) + l * ls.in_ls;
-          const uint4* in = reinterpret_cast<const uint4*>(src + s * a.in_ss + (int64_t)g * D);
-          *reinterpret_cast<uint4*>((lane < 16 ? ktiles : vtiles) + t * TILE + swz(r, cd)) = in[cd];
-        }
-        bar_sync_n(1, CTC);
+      if (own_new) {
+        if (lane < 16) *reinterpret_cast<uint4*>(ktiles + nrow_off) = nrow;
+        __syncwarp();
       }
       float m[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
       float o[8][4];
@@ -1004,6 +1008,12 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
       const bool active = wk0 < ntile * TT;
       if (active) warp_scores(qa, kbase, wk0, lane, k0, kend, a.scale, lg, a.l_hs, G, p, m, lsum);
       if (any) mbar_wait(vfull, ph);
+      if (own_new) {
+        if (lane >= 16) *reinterpret_cast<uint4*>(vtiles + nrow_off) = nrow;
+        // (generic writes into tiles the async proxy refills next layer)
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+      }
       if (active) warp_pv(p, vbase, wk0, lane, o);
       __syncwarp();
       if (lane == 0 && any) mbar_arrive(vfree);
