@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(ClSmem<G, MT>::THREADS, 1) decode_tc_cluster_k
     uint32_t dyn;  // the tight layout needs the aligned base inside the allocation
     asm("mov.u32 %0, %%dynamic_smem_size;\n" : "=r"(dyn));
     if ((size_t)(smem - smem_raw) + Sm::bytes(a.Hq, CS) > dyn) {
-      if (threadIdx.x == 0 && a.err) atomicOr(a.err, 2);
+      if (threadIdx.x == 0 && a.err) atomicOr(a.err, 1 << 30);
       return;  // same offset in every CTA of the launch: all leave, no barrier is left waiting
     }
   }

@@ -281,8 +281,8 @@ static int check_sticky(skv_ctx* x) {
   const int32_t w = *x->err_host;
   if (w == 0) return SKV_OK;
   *x->err_host = 0;
-  if (w & 2)
-    return fail(SKV_ECUDA, "all-layer decode: dynamic shared memory base not 1024-byte aligned, launch skipped");
+  if (w & (1 << 30))  // (the low bits count prefill V overflows)
+    return fail(SKV_ECUDA, "dynamic shared memory base not 1024-byte aligned: a kernel skipped its work");
   return fail(SKV_EINVAL,
               "value overflow: a chunked prefill read |v| >= 65504, which its fp16 P.V cannot represent "
               "(outputs of that chunk are saturated)");
