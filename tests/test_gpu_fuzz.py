@@ -1,0 +1,100 @@
+"""Seeded shape fuzz: random engine shapes through whichever decode path the
+engine picks for them (static / dynamic schedules, CUDA-core or tensor-core
+chunk math, the all-layer cluster launch) against the oracle over two
+eviction periods -- outputs every step, window rows, kept sets and the
+compacted K/V after each eviction (stands in for the sanitizers the GPU pool
+does not allow: any mis-indexed row or stale partial shows up as a mismatch).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match  # noqa: E402
+from tests.gpu_helpers import rel_err, tol_for  # noqa: E402
+
+F32 = np.float32
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _shape(seed):
+    rng = np.random.default_rng(1000 + seed)
+    if seed >= 12:  # many segments: the dynamic (ticket) schedule
+        G = int(rng.choice([1, 2, 4]))
+        Hkv = int(rng.choice([8, 16]))
+        l, r = int(rng.integers(256, 1025)), int(rng.integers(256, 1025))
+        return dict(S=int(rng.choice([16, 24, 32])), L=int(rng.choice([1, 2])), Hq=G * Hkv, Hkv=Hkv, D=128, l=l,
+                    r=r, W=int(rng.integers(4, 13)), E=int(rng.integers(12, 25)), dtype="bf16", seed=seed)
+    dtype = "bf16" if seed % 4 else "f32"
+    D = 128 if (dtype == "bf16" and seed % 3) else int(rng.choice([64, 128]))
+    G = int(rng.choice([1, 2, 4, 8]))
+    Hkv = int(rng.choice([1, 2, 4, 8] if G < 8 else [1, 2, 4]))
+    S = int(rng.choice([1, 2, 3, 5, 8, 12, 24]))
+    L = int(rng.choice([1, 2, 3, 4]))
+    l = int(rng.integers(16, 385))
+    r = int(rng.integers(16, 385))
+    W = int(rng.integers(2, min(40, l) + 1))
+    E = int(rng.integers(8, 65))
+    return dict(S=S, L=L, Hq=G * Hkv, Hkv=Hkv, D=D, l=l, r=r, W=W, E=E, dtype=dtype, seed=seed)
+
+
+@pytest.mark.parametrize("seed", list(range(20)))
+def test_random_shapes_vs_oracle(seed):
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    c = _shape(seed)
+    S, L, Hq, Hkv, D, l, r, W, E = (c[k] for k in ("S", "L", "Hq", "Hkv", "D", "l", "r", "W", "E"))
+    B = l + r
+    dt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    rnd = bf16_round if c["dtype"] == "bf16" else (lambda a: a)
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, B + E, dt))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    rng = np.random.default_rng(7 + seed)
+    for s in range(S):
+        for layer in range(L):
+            k = rnd(rng.standard_normal((Hkv, B, D)).astype(F32))
+            v = rnd(rng.standard_normal((Hkv, B, D)).astype(F32))
+            eng.inject(s, layer, k, v, np.arange(B, dtype=np.int64))
+            for t in range(B):
+                orc.kv[s][layer].append(k[:, t], v[:, t], t)
+    orc.pos = [B] * S
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    tol = tol_for(c["dtype"])
+    worst = worst_row = 0.0
+    kernels = set()
+    for period in range(2):
+        for t in range(E):
+            q = rnd(rng.standard_normal((L, S, Hq, D)).astype(F32))
+            k = rnd(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            v = rnd(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            got = eng.decode_step(*(torch.from_numpy(a).to("cuda", dt) for a in (q, k, v)),
+                                  record=t >= E - W).cpu().numpy()
+            kernels.add(eng.last_decode_kernel)
+            worst = max(worst, rel_err(got, orc.step(q, k, v)))
+        n = eng.length(0, 0)
+        for s in range(S):
+            for layer in range(L):
+                for a_, b_ in zip(eng.window_rows(s, layer), orc.win[s][layer].rows[-W:]):
+                    worst_row = max(worst_row, float(np.abs(a_ - b_).max() / np.abs(b_).max()))
+        eng.evict(-1, kept)
+        kc = kept.cpu().numpy()
+        for s in range(S):
+            for layer in range(L):
+                ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept, kc[s, layer], n,
+                                                cfg)
+                assert ok, (c, period, s, layer, nbad, gap)
+                orc.apply(s, layer, kc[s, layer].astype(np.int64))
+                kg, vg = eng.kv(s, layer)
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
+    print(f"fuzz {c}: kernels {sorted(kernels)} worst out {worst:.2e} rows {worst_row:.2e}")
+    assert worst <= tol and worst_row <= tol, (c, worst, worst_row)
