@@ -98,3 +98,69 @@ def test_random_shapes_vs_oracle(seed):
                 np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
     print(f"fuzz {c}: kernels {sorted(kernels)} worst out {worst:.2e} rows {worst_row:.2e}")
     assert worst <= tol and worst_row <= tol, (c, worst, worst_row)
+
+
+def _policy_shape(seed):
+    rng = np.random.default_rng(5000 + seed)
+    policy = ("window", "sink_recent", "heavy_hitter", "inf_mllm")[seed % 4]
+    G = int(rng.choice([1, 2, 4]))
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    l, r = int(rng.integers(16, 257)), int(rng.integers(16, 257))
+    return dict(policy=policy, head_agg="max" if policy == "inf_mllm" else "mean", sink=int(rng.integers(1, 9)),
+                S=int(rng.choice([1, 3, 8, 16])), L=int(rng.choice([1, 2, 3])), Hq=G * Hkv, Hkv=Hkv, D=128, l=l, r=r,
+                W=int(rng.integers(2, 17)), E=int(rng.integers(8, 33)), seed=seed)
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_random_policies_vs_oracle(seed):
+    """The Session policy switch (engine.py:296-307) under random shapes: window /
+    sink_recent keep sets are index arithmetic (bit-exact), heavy_hitter ranks the
+    accumulated attention mass, inf_mllm with head_agg="max" -- all vs the oracle
+    over two eviction periods, with the compacted K/V compared exactly."""
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    c = _policy_shape(seed)
+    S, L, Hq, Hkv, D, l, r, W, E = (c[k] for k in ("S", "L", "Hq", "Hkv", "D", "l", "r", "W", "E"))
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01, sink_count=c["sink"], head_agg=c["head_agg"])
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, B + E, torch.bfloat16, head_agg=c["head_agg"],
+                                    policy=c["policy"], sink_count=c["sink"]))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W, policy=c["policy"])
+    rng = np.random.default_rng(11 + seed)
+    for s in range(S):
+        for layer in range(L):
+            k = bf16_round(rng.standard_normal((Hkv, B, D)).astype(F32))
+            v = bf16_round(rng.standard_normal((Hkv, B, D)).astype(F32))
+            eng.inject(s, layer, k, v, np.arange(B, dtype=np.int64))
+            for t in range(B):
+                orc.kv[s][layer].append(k[:, t], v[:, t], t)
+    orc.pos = [B] * S
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    worst = 0.0
+    for period in range(2):
+        for t in range(E):
+            q, k, v = (bf16_round(rng.standard_normal(sh).astype(F32))
+                       for sh in ((L, S, Hq, D), (L, S, Hkv, D), (L, S, Hkv, D)))
+            got = eng.decode_step(*(torch.from_numpy(a).to("cuda", torch.bfloat16) for a in (q, k, v)),
+                                  record=t >= E - W).cpu().numpy()
+            worst = max(worst, rel_err(got, orc.step(q, k, v)))
+        n = eng.length(0, 0)
+        kept.fill_(-1)
+        eng.evict(-1, kept)
+        kc = kept.cpu().numpy()
+        for s in range(S):
+            for layer in range(L):
+                want = orc.decide(s, layer).kept
+                got_k = kc[s, layer, : want.size]
+                if c["policy"] in ("window", "sink_recent"):
+                    np.testing.assert_array_equal(got_k, want, err_msg=str((c, period, s, layer)))
+                else:
+                    sc = orc.acc[s][layer][: n - l] if c["policy"] == "heavy_hitter" else orc.scores(s, layer)
+                    ok, nbad, gap = kept_sets_match(sc, want, got_k, n, cfg, rel_tol=1e-4)
+                    assert ok, (c, period, s, layer, nbad, gap)
+                orc.apply(s, layer, got_k.astype(np.int64))
+                kg, vg = eng.kv(s, layer)
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
+    print(f"policy fuzz {c}: worst out {worst:.2e}")
+    assert worst <= tol_for("bf16"), (c, worst)
