@@ -190,6 +190,10 @@ def workload_config(c, S, resident, waves, world, job_streams, hq, hkv, use_grap
                             if sharded else f"stream-partitioned x{world}, no hot-path collective")}
 
 
+def _local_device() -> int:
+    return int(os.environ.get("SKV_BENCH_DEVICE", os.environ.get("LOCAL_RANK", 0)))
+
+
 def _max_over_ranks(x: float, world: int, device) -> float:
     if world == 1:
         return x
@@ -216,7 +220,7 @@ def run_gpu(args, rank: int, world: int):
     l, r, W, E = c["recent"], c["relevant"], c["window"], c["period"]
     B = l + r
     G = HQ // HKV
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", _local_device())
     torch.cuda.set_device(dev)
     select = args.select if c["shard"] == "heads" else "layer"
     sharded = c["shard"] == "heads" and world > 1 and select == "layer"
@@ -289,20 +293,22 @@ def run_gpu(args, rank: int, world: int):
     # one CUDA graph per period; head-sharded layer mode captures the NCCL
     # all-reduce of the window scores inside it too, and falls back to eager
     # launches if this NCCL / driver cannot capture it
-    use_graph = True
-    try:
-        with torch.cuda.stream(stream):
-            eng.capture_begin()
-            try:
-                period()
-            finally:
-                eng.capture_end()
-    except Exception as exc:  # noqa: BLE001
-        if not sharded:
-            raise
-        print(f"[bench] NCCL capture failed ({exc}); eager sharded periods", file=sys.stderr)
-        torch.cuda.synchronize()
-        use_graph = False
+    # (gloo collectives cannot be captured: eager periods, functional runs only)
+    use_graph = not (sharded and dist.get_backend() != "nccl")
+    if use_graph:
+        try:
+            with torch.cuda.stream(stream):
+                eng.capture_begin()
+                try:
+                    period()
+                finally:
+                    eng.capture_end()
+        except Exception as exc:  # noqa: BLE001
+            if not sharded:
+                raise
+            print(f"[bench] NCCL capture failed ({exc}); eager sharded periods", file=sys.stderr)
+            torch.cuda.synchronize()
+            use_graph = False
     if use_graph:
         launches_per_period = eng.kernel_launches - launches0
 
@@ -490,7 +496,7 @@ def run_cfg2(args, rank: int, world: int):
     L, H, D, S = c["layers"], c["heads_q"], c["head_dim"], c["streams"]
     l, r, W, CI, CT = c["recent"], c["relevant"], c["window"], c["image"], c["text"]
     B = l + r
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", _local_device())
     torch.cuda.set_device(dev)
     eng = StreamEngine(EngineConfig(S, L, H, H, D, l, r, c["bias"], W, B + CI + 64, torch.bfloat16))
     g = torch.Generator(device=dev).manual_seed(99 + rank)
@@ -888,9 +894,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        backend = "nccl" if args.impl == "ours" else "gloo"
+        # SKV_BENCH_BACKEND=gloo + SKV_BENCH_DEVICE=0: functional check of the
+        # multi-rank path on one GPU (tests/test_gpu_bench.py; not a measurement)
+        backend = os.environ.get("SKV_BENCH_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
         if backend == "nccl":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            torch.cuda.set_device(_local_device())
         dist.init_process_group(backend=backend)
     if args.impl == "reference":
         res = run_reference(args, rank, world)

@@ -222,9 +222,18 @@ class StreamEngine:
         return kept
 
     def evict_scores(self, layer: int = -1) -> torch.Tensor:
-        """This shard's unbiased window-mean scores, (S, L', capacity) f32 (first n-l valid)."""
+        """This shard's unbiased window-mean scores, (S, L', capacity) f32 (first n-l valid).
+
+        The tensor is the engine's persistent buffer for this shape: the next
+        call overwrites it."""
         nl = self.cfg.layers if layer < 0 else 1
-        scores = torch.zeros((self.cfg.streams, nl, self.cap), dtype=torch.float32, device="cuda")
+        # one persistent buffer per shape: a sharded period is captured in a CUDA
+        # graph, whose replays must write memory that outlives the capture
+        bufs = self.__dict__.setdefault("_score_bufs", {})
+        scores = bufs.get(nl)
+        if scores is None:
+            scores = bufs[nl] = torch.empty((self.cfg.streams, nl, self.cap), dtype=torch.float32, device="cuda")
+        scores.zero_()
         check(self.lib.skv_evict_scores(self._h, int(layer), _ptr(scores), _stream_handle()))
         return scores
 
