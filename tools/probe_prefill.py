@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 from paper_2409_09086_b200 import _lib
 
 lib = _lib.load()
-S, C, H, D, L, n0 = 4, int(os.environ.get("C", 576)), 32, 128, 1, int(os.environ.get("N0", 4096))
+S, C, H, D, L, n0 = int(os.environ.get("S", 4)), int(os.environ.get("C", 576)), 32, 128, 1, int(os.environ.get("N0", 4096))
 cap = n0 + C + 64
 g = torch.Generator(device="cuda").manual_seed(1)
 q = torch.randn((S, C, H, D), generator=g, device="cuda").to(torch.bfloat16)
