@@ -441,3 +441,34 @@ def test_dynamic_decode_kernels_both_match_oracle():
                            timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         assert r.stdout.strip().splitlines()[-1] == want, (flag, r.stdout)
+
+
+def test_project_row_matches_reference_projection():
+    """skv_project_row (the trace replay's per-row projection, replay.py:139-142):
+    probs[live] divided by their float64 total and rounded to f32 -- exact
+    against the same NumPy arithmetic; an all-zero projection stays unscaled;
+    m = 0 is a no-op."""
+    import ctypes
+
+    from paper_2409_09086_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for n, m, zero in ((5000, 3000, False), (64, 64, False), (300, 17, True), (10, 0, False)):
+        probs = rng.random(n).astype(np.float32) ** 4
+        if zero:
+            probs[:] = 0.0
+        live = np.sort(rng.choice(n, size=m, replace=False)).astype(np.int64)
+        out = torch.full((max(m, 1),), -7.0, dtype=torch.float32, device="cuda")
+        pd, ld = torch.from_numpy(probs).cuda(), torch.from_numpy(live).cuda() if m else torch.zeros(1, dtype=torch.int64,
+                                                                                                    device="cuda")
+        _lib.check(lib.skv_project_row(P(pd), n, P(ld), m, P(out), st))
+        got = out.cpu().numpy()[:m]
+        proj = probs[live]
+        total = proj.sum(dtype=np.float64)
+        want = (proj / total).astype(np.float32) if total > 0 else proj
+        np.testing.assert_array_equal(got, want)
+        if m == 0:
+            assert out.cpu().numpy()[0] == -7.0
