@@ -43,22 +43,44 @@ def _ref(q, kc, vc, n0, C, W):
 # not split (a row would see no key of the upper half's first tile)
 @pytest.mark.parametrize("S,C,Hq,Hkv,n0,W", [(1, 128, 2, 2, 0, 32), (2, 576, 4, 4, 1000, 32), (1, 32, 8, 2, 513, 32),
                                              (2, 200, 4, 1, 300, 16), (1, 32, 4, 4, 2016, 32),
-                                             (1, 64, 2, 2, 100, 32)])
+                                             (1, 64, 2, 2, 100, 32), (1, 1, 2, 2, 0, 1), (2, 1, 4, 1, 700, 1)])
 def test_prefill_matches_torch(S, C, Hq, Hkv, n0, W):
+    _check_prefill(S, C, Hq, Hkv, n0, W, 5)
+
+
+def _fuzz_shape(seed):
+    rng = np.random.default_rng(900 + seed)
+    Hkv = int(rng.choice([1, 2, 4]))
+    G = int(rng.choice([1, 2, 4, 8]))
+    C = int(rng.choice([1, 7, 31, 33, 127, 129, 255, 256, 300, 511, 577, 700]))
+    n0 = int(rng.choice([0, 1, 63, 128, 500, 1023, 2048, 2999]))
+    W = int(min(C, rng.choice([0, 1, 5, 32, 32, 64, 64])))
+    return int(rng.integers(1, 4)), C, G * Hkv, Hkv, n0, W
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_prefill_fuzz_matches_torch(seed):
+    """Seeded random chunk geometries (odd chunk lengths, lone and paired Q
+    tiles, empty and tile-boundary prefixes, 0..64 recorded rows, GQA groups up
+    to 8) against the float32 PyTorch prompt loop."""
+    _check_prefill(*_fuzz_shape(seed), seed)
+
+
+def _check_prefill(S, C, Hq, Hkv, n0, W, seed):
     from paper_2409_09086_b200 import _lib
 
     lib = _lib.load()
     D, L, layer = 128, 2, 1
     cap = ((n0 + C + 31) // 32) * 32 + 64
-    g = torch.Generator(device="cuda").manual_seed(5)
+    g = torch.Generator(device="cuda").manual_seed(seed)
     q = torch.randn((S, C, Hq, D), generator=g, device="cuda").to(torch.bfloat16)
     kc = torch.randn((S, L, Hkv, cap, D), generator=g, device="cuda").to(torch.bfloat16)
     vc = torch.randn((S, L, Hkv, cap, D), generator=g, device="cuda").to(torch.bfloat16)
     kc[:, :, :, ::97] *= 4  # key spikes
     out = torch.full((S, C, Hq, D), float("nan"), dtype=torch.float32, device="cuda")
     lg_cap = n0 + C
-    logits = torch.zeros((S, W, Hq, lg_cap), dtype=torch.float32, device="cuda")
-    stats = torch.zeros((S, W, Hq, 2), dtype=torch.float32, device="cuda")
+    logits = torch.zeros((S, max(W, 1), Hq, lg_cap), dtype=torch.float32, device="cuda")
+    stats = torch.zeros((S, max(W, 1), Hq, 2), dtype=torch.float32, device="cuda")
     P = lambda t: ctypes.c_void_p(t.data_ptr())
     rc = lib.skv_prefill_attend(P(q), S, C, Hq, Hkv, P(kc), P(vc), L, layer, cap, n0, P(out), W, P(logits), lg_cap,
                                 P(stats), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
@@ -205,4 +227,74 @@ def test_prefill_config2_full_shape():
             err = ((out[s, :, h] - ref).abs().amax(-1) / ref.abs().amax(-1)).max().item()
             worst = max(worst, err)
     print(f"config-2 full-shape prefill worst rel err {worst:.2e}")
+    assert worst <= 2e-3
+
+
+@pytest.mark.parametrize("seed", list(range(6)))
+def test_engine_chunks_and_decode_fuzz(seed):
+    """Random engines (1-2 streams and layers, GQA groups 1-4, budgets 64-300,
+    W 8-40) driven through a random mix of prefill chunks (1-600 tokens) and
+    decode steps, evicting after each phase, against the oracle's per-token
+    loop: chunk and step outputs, window rows, kept sets, compacted K/V."""
+    from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    rng = np.random.default_rng(4200 + seed)
+    S, L = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    Hkv, G = int(rng.choice([2, 4])), int(rng.choice([1, 2, 4]))
+    Hq, D = Hkv * G, 128
+    l, r, W = int(rng.integers(64, 301)), int(rng.integers(64, 301)), int(rng.choice([8, 32, 40]))
+    B = l + r
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, B + 640, torch.bfloat16))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    F32 = np.float32
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)
+    rnd = lambda *shape: bf16_round(rng.standard_normal(shape).astype(F32))
+    kept_buf = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    worst = 0.0
+    phases = []
+    for _ in range(4):
+        phases.append(("chunk", int(rng.choice([1, 17, 32, 129, 300, 576, 600]))))
+        phases.append(("decode", int(rng.integers(1, 12))))
+    for kind, count in phases:
+        if kind == "chunk":
+            q, k, v = rnd(L, S, count, Hq, D), rnd(L, S, count, Hkv, D), rnd(L, S, count, Hkv, D)
+            got = [eng.prefill_chunk(layer, dev(q[layer]), dev(k[layer]), dev(v[layer])).cpu().numpy()
+                   for layer in range(L)]
+            for i in range(count):
+                for layer in range(L):
+                    want, _ = orc.step_layer(layer, q[layer][:, i], k[layer][:, i], v[layer][:, i])
+                    g = got[layer][:, i].astype(np.float64)
+                    worst = max(worst, float((np.abs(g - want).max(-1) / np.abs(want).max(-1)).max()))
+                orc.advance()
+        else:
+            for _ in range(count):
+                q, k, v = rnd(L, S, Hq, D), rnd(L, S, Hkv, D), rnd(L, S, Hkv, D)
+                got = eng.decode_step(dev(q), dev(k), dev(v), record=True).cpu().numpy()
+                want = orc.step(q, k, v)
+                worst = max(worst, float((np.abs(got - want).max(-1) / np.abs(want).max(-1)).max()))
+        n = orc.length(0, 0)
+        for s in range(S):
+            for layer in range(L):
+                rows_g, rows_c = eng.window_rows(s, layer), orc.win[s][layer].rows
+                assert [a.size for a in rows_g] == [b.size for b in rows_c[-len(rows_g):]] if rows_g else True
+                for a_, b_ in zip(rows_g, rows_c[-len(rows_g):]):
+                    assert float(np.abs(a_ - b_).max() / np.abs(b_).max()) <= 1e-5, (kind, s, layer)
+        kept_buf.fill_(-1)
+        eng.evict(-1, kept_buf)
+        kc = kept_buf.cpu().numpy()
+        for s in range(S):
+            for layer in range(L):
+                if n > B:
+                    ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept, kc[s, layer], n,
+                                                    cfg)
+                    assert ok, (kind, count, s, layer, nbad, gap)
+                    orc.apply(s, layer, kc[s, layer].astype(np.int64))
+                else:
+                    np.testing.assert_array_equal(kc[s, layer, :n], np.arange(n))
+                kg, vg = eng.kv(s, layer)
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
+    print(f"chunk+decode fuzz seed {seed}: S={S} L={L} Hq={Hq} Hkv={Hkv} l={l} r={r} W={W}: worst {worst:.2e}")
     assert worst <= 2e-3
