@@ -230,12 +230,13 @@ def test_prefill_config2_full_shape():
     assert worst <= 2e-3
 
 
-@pytest.mark.parametrize("seed", list(range(6)))
+@pytest.mark.parametrize("seed", list(range(10)))
 def test_engine_chunks_and_decode_fuzz(seed):
     """Random engines (1-2 streams and layers, GQA groups 1-4, budgets 64-300,
-    W 8-40) driven through a random mix of prefill chunks (1-600 tokens) and
-    decode steps, evicting after each phase, against the oracle's per-token
-    loop: chunk and step outputs, window rows, kept sets, compacted K/V."""
+    W 8-40; seeds 6-9 with RoPE in both position modes) driven through a
+    random mix of prefill chunks (1-600 tokens) and decode steps, evicting
+    after each phase, against the oracle's per-token loop: chunk and step
+    outputs, window rows, kept sets, compacted (raw) K/V."""
     from oracle.streamkv_oracle import PolicyConfig, StreamOracle, bf16_round, kept_sets_match
     from paper_2409_09086_b200 import EngineConfig, StreamEngine
 
@@ -245,9 +246,10 @@ def test_engine_chunks_and_decode_fuzz(seed):
     Hq, D = Hkv * G, 128
     l, r, W = int(rng.integers(64, 301)), int(rng.integers(64, 301)), int(rng.choice([8, 32, 40]))
     B = l + r
+    rope = None if seed < 6 else ("cache_relative", "original")[seed % 2]
     cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
-    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, B + 640, torch.bfloat16))
-    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, B + 640, torch.bfloat16, rope=rope))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W, rope=rope, rope_round=bf16_round if rope else None)
     F32 = np.float32
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16)
     rnd = lambda *shape: bf16_round(rng.standard_normal(shape).astype(F32))
@@ -296,5 +298,6 @@ def test_engine_chunks_and_decode_fuzz(seed):
                 kg, vg = eng.kv(s, layer)
                 np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
                 np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
-    print(f"chunk+decode fuzz seed {seed}: S={S} L={L} Hq={Hq} Hkv={Hkv} l={l} r={r} W={W}: worst {worst:.2e}")
+    print(f"chunk+decode fuzz seed {seed}: S={S} L={L} Hq={Hq} Hkv={Hkv} l={l} r={r} W={W} rope={rope}: "
+          f"worst {worst:.2e}")
     assert worst <= 2e-3
