@@ -164,3 +164,59 @@ def test_random_policies_vs_oracle(seed):
                 np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
     print(f"policy fuzz {c}: worst out {worst:.2e}")
     assert worst <= tol_for("bf16"), (c, worst)
+
+
+@pytest.mark.parametrize("seed", list(range(6)))
+def test_random_host_steps_vs_oracle(seed):
+    """decode_step_host (the e2e entry point: pinned host q/k/v in, f32 outputs
+    out, per-state CUDA graphs, the all-layer cluster launch where eligible)
+    under random shapes over two eviction periods against the oracle."""
+    from paper_2409_09086_b200 import EngineConfig, StreamEngine
+
+    rng = np.random.default_rng(7000 + seed)
+    dtype = "f32" if seed == 5 else "bf16"
+    G = int(rng.choice([1, 4, 8]))
+    Hkv = int(rng.choice([1, 2, 4]))
+    S, L = int(rng.choice([1, 2, 8])), int(rng.choice([1, 2, 4, 6]))
+    Hq, D = G * Hkv, 128
+    l, r = int(rng.integers(32, 257)), int(rng.integers(32, 257))
+    W, E = int(rng.integers(2, 33)), int(rng.integers(8, 40))
+    B = l + r
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rnd = bf16_round if dtype == "bf16" else (lambda a: a)
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=0.01)
+    eng = StreamEngine(EngineConfig(S, L, Hq, Hkv, D, l, r, 0.01, W, B + E, dt))
+    orc = StreamOracle(S, L, Hq, Hkv, D, cfg, window=W)
+    for s in range(S):
+        for layer in range(L):
+            k = rnd(rng.standard_normal((Hkv, B, D)).astype(F32))
+            v = rnd(rng.standard_normal((Hkv, B, D)).astype(F32))
+            eng.inject(s, layer, k, v, np.arange(B, dtype=np.int64))
+            for t in range(B):
+                orc.kv[s][layer].append(k[:, t], v[:, t], t)
+    orc.pos = [B] * S
+    kept = torch.full((S, L, B), -1, dtype=torch.int32, device="cuda")
+    oh = torch.empty((L, S, Hq, D), dtype=torch.float32).pin_memory()
+    worst = 0.0
+    for period in range(2):
+        for t in range(E):
+            q = rnd(rng.standard_normal((L, S, Hq, D)).astype(F32))
+            k = rnd(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            v = rnd(rng.standard_normal((L, S, Hkv, D)).astype(F32))
+            qh, kh, vh = (torch.from_numpy(a).to(dt).pin_memory() for a in (q, k, v))
+            eng.decode_step_host(qh, kh, vh, oh, record=True)
+            worst = max(worst, rel_err(oh.numpy(), orc.step(q, k, v)))
+        n = eng.length(0, 0)
+        eng.evict(-1, kept)
+        kc = kept.cpu().numpy()
+        for s in range(S):
+            for layer in range(L):
+                ok, nbad, gap = kept_sets_match(orc.scores(s, layer), orc.decide(s, layer).kept, kc[s, layer], n, cfg)
+                assert ok, (seed, period, s, layer, nbad, gap)
+                orc.apply(s, layer, kc[s, layer].astype(np.int64))
+                kg, vg = eng.kv(s, layer)
+                np.testing.assert_array_equal(kg.float().cpu().numpy(), orc.kv[s][layer].keys())
+                np.testing.assert_array_equal(vg.float().cpu().numpy(), orc.kv[s][layer].values())
+    print(f"host-step fuzz seed {seed}: S={S} L={L} Hq={Hq} Hkv={Hkv} l={l} r={r} W={W} E={E} {dtype}: "
+          f"worst {worst:.2e}")
+    assert worst <= tol_for(dtype), (seed, worst)
