@@ -52,8 +52,11 @@ def test_reader_errors_name_the_offset():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fixture", ["ref_replay.npz", "ref_replay2.npz"])
 @pytest.mark.parametrize("policy", POLICIES)
-def test_device_replay_matches_reference(policy):
+def test_device_replay_matches_reference(policy, fixture):
+    """ref_replay2.npz: three layers, 8 heads, 40-token prompts, its own policy
+    config (stored in the fixture) -- the reference replay_trace's output."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -61,10 +64,12 @@ def test_device_replay_matches_reference(policy):
     from paper_2409_09086_b200.replay import replay_trace
     from paper_2409_09086_b200.traceio import read_trace
 
-    ref = dict(np.load(GOLD))
+    ref = dict(np.load(os.path.join(os.path.dirname(GOLD), fixture)))
+    l, r, sink, head_dim = (int(x) for x in ref["cfg"])
+    cfg = PolicyConfig(recent_len=l, relevant_budget=r, bias=float(ref["bias"][0]), sink_count=sink)
     key = policy.replace("-", "_")
     header, events = read_trace(io.BytesIO(ref["trace"].tobytes()))
-    res = replay_trace(header, list(events), policy, PolicyConfig(**CFG), head_dim=16)
+    res = replay_trace(header, list(events), policy, cfg, head_dim=head_dim)
     kept = [d.kept for rnd in res.decisions_per_round for d in rnd]
     off = ref[f"{key}_kept_off"]
     assert len(kept) == off.size - 1
