@@ -69,6 +69,14 @@ CASES = {
     "shadow_mini": dict(S=2, L=2, Hq=8, Hkv=2, D=64, T=384, l=32, r=32, W=16, b=0.01, E=64,
                         dtype="f32", seed=1013, saddles=4, saddle_gain=6.0, spike_prob=0.0,
                         spike_gain=1.0, out_every=64, shadow=True),
+    # eight query heads per KV head (the widest GQA group the kernels take), bf16
+    "gqa8_bf16": dict(S=2, L=2, Hq=16, Hkv=2, D=128, T=320, l=40, r=56, W=24, b=0.05, E=48,
+                      dtype="bf16", seed=1014, saddles=0, saddle_gain=1.0, spike_prob=0.01,
+                      spike_gain=4.0, out_every=48),
+    # a long run with a short period: ~100 evictions, a large age bias
+    "long_f32": dict(S=1, L=1, Hq=4, Hkv=4, D=64, T=1024, l=24, r=40, W=8, b=0.2, E=10,
+                     dtype="f32", seed=1015, saddles=5, saddle_gain=5.0, spike_prob=0.0,
+                     spike_gain=1.0, out_every=64),
 }
 
 
