@@ -559,3 +559,68 @@ def test_dropin_aggregate_bias_and_window_ring():
         nn = max(r.size for r in ref.rows)
         if nn > 1:
             np.testing.assert_array_equal(window_mean_scores(w, nn, 1), window_scores(ref, nn, 1))
+
+
+# bf16, head_dim 128 golden cases whose period is the prompt chunk: the same
+# reference run, fed to the engine as one tcgen05 prefill chunk per period
+CHUNK_CASES = [n for n, c in CASES.items() if c["dtype"] == "bf16" and c["D"] == 128 and not c.get("rope")
+               and c.get("policy", "inf_mllm") != "heavy_hitter"]
+
+
+@pytest.mark.parametrize("name", CHUNK_CASES)
+def test_engine_chunks_match_reference_golden(name):
+    """The reference's per-token loop with an eviction every E tokens is a
+    round of E prompt tokens (Session.start_round, engine.py:344-360): the
+    engine takes each period as ONE prefill chunk per layer (K4 + the chunk
+    fold) and must reproduce the reference's outputs, scores, kept sets and
+    final keys / positions."""
+    import hashlib
+
+    c = CASES[name]
+    ref = dict(np.load(os.path.join(GOLD, f"ref_{name}.npz")))
+    eng = _engine(c)
+    S, L, Hq, D, E = c["S"], c["L"], c["Hq"], c["D"], c["E"]
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"])
+    q_all, k_all, v_all = case_inputs(name)
+    kept_buf = torch.full((S, L, c["l"] + c["r"]), -1, dtype=torch.int32, device="cuda")
+    out_steps = list(ref["out_steps"])
+    worst_out = worst_score = 0.0
+    ei = 0
+    for t0 in range(0, c["T"], E):
+        C = min(E, c["T"] - t0)
+        outs = []
+        for layer in range(L):
+            chunk = lambda a: _dev(np.ascontiguousarray(a[t0:t0 + C, layer].transpose(1, 0, 2, 3)), torch.bfloat16)
+            outs.append(eng.prefill_chunk(layer, chunk(q_all), chunk(k_all), chunk(v_all)).cpu().numpy())
+        for oi, t in enumerate(out_steps):
+            if t0 <= t < t0 + C:
+                got = np.stack([outs[layer][:, t - t0] for layer in range(L)])
+                worst_out = max(worst_out, rel_err(got, ref["outs"][oi]))
+        if C == E:
+            n = eng.length(0, 0)
+            eng.evict(-1, kept_buf)
+            kc = kept_buf.cpu().numpy()
+            for s in range(S):
+                for layer in range(L):
+                    b = ei * S * L + s * L + layer
+                    want = ref["kept"][ref["kept_off"][b]: ref["kept_off"][b + 1]]
+                    sc = ref["scores"][ref["score_off"][b]: ref["score_off"][b + 1]]
+                    got = kc[s, layer, : want.size]
+                    if sc.size:
+                        gs = eng.last_scores(s, layer, sc.size)
+                        worst_score = max(worst_score, float(np.abs(gs - sc).max() / np.abs(sc).max()))
+                        ok, nbad, gap = kept_sets_match(sc, want, got, n, cfg)
+                        assert ok, f"{name} t0={t0} s={s} l={layer}: {nbad} kept mismatches, gap {gap:.2e}"
+                    else:
+                        np.testing.assert_array_equal(got, want)
+            ei += 1
+    print(f"[{name} chunks] worst output rel err {worst_out:.2e}, worst score rel err {worst_score:.2e}")
+    assert worst_out <= 2e-3
+    assert worst_score <= 2e-3
+    for s in range(S):
+        for layer in range(L):
+            np.testing.assert_array_equal(eng.positions(s, layer), ref["final_pos"][s, layer])
+    final_keys = np.stack([np.stack([eng.kv(s, layer)[0].float().cpu().numpy() for layer in range(L)])
+                           for s in range(S)]).astype(F32)
+    sha = np.frombuffer(hashlib.sha256(np.ascontiguousarray(final_keys).tobytes()).digest(), np.uint8)
+    np.testing.assert_array_equal(sha, ref["final_keys_sha"], err_msg=f"{name}: final keys differ")
