@@ -624,3 +624,51 @@ def test_engine_chunks_match_reference_golden(name):
                            for s in range(S)]).astype(F32)
     sha = np.frombuffer(hashlib.sha256(np.ascontiguousarray(final_keys).tobytes()).digest(), np.uint8)
     np.testing.assert_array_equal(sha, ref["final_keys_sha"], err_msg=f"{name}: final keys differ")
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_host_steps_match_reference_golden(name):
+    """Every golden case through decode_step_host (the e2e entry point: all
+    layers of a token from pinned host buffers, outputs back to the host)
+    against the reference's own outputs, kept sets and final keys."""
+    import hashlib
+
+    c = CASES[name]
+    ref = dict(np.load(os.path.join(GOLD, f"ref_{name}.npz")))
+    eng = _engine(c)
+    S, L, Hq, Hkv, D = c["S"], c["L"], c["Hq"], c["Hkv"], c["D"]
+    dt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    q_all, k_all, v_all = case_inputs(name)
+    kept_buf = torch.full((S, L, c["l"] + c["r"]), -1, dtype=torch.int32, device="cuda")
+    oh = torch.empty((L, S, Hq, D), dtype=torch.float32).pin_memory()
+    cfg = PolicyConfig(recent_len=c["l"], relevant_budget=c["r"], bias=c["b"])
+    oi = ei = 0
+    worst = 0.0
+    for t in range(c["T"]):
+        qh, kh, vh = (torch.from_numpy(np.ascontiguousarray(a[t])).to(dt).pin_memory() for a in (q_all, k_all, v_all))
+        eng.decode_step_host(qh, kh, vh, oh, record=True)
+        if oi < ref["out_steps"].size and ref["out_steps"][oi] == t:
+            worst = max(worst, rel_err(oh.numpy(), ref["outs"][oi]))
+            oi += 1
+        if (t + 1) % c["E"] == 0:
+            n = eng.length(0, 0)
+            eng.evict(-1, kept_buf)
+            kc = kept_buf.cpu().numpy()
+            for s in range(S):
+                for layer in range(L):
+                    b = ei * S * L + s * L + layer
+                    want = ref["kept"][ref["kept_off"][b]: ref["kept_off"][b + 1]]
+                    sc = ref["scores"][ref["score_off"][b]: ref["score_off"][b + 1]]
+                    got = kc[s, layer, : want.size]
+                    if sc.size:
+                        ok, nbad, gap = kept_sets_match(sc, want, got, n, cfg)
+                        assert ok, f"{name} t={t} s={s} l={layer}: {nbad} kept mismatches, gap {gap:.2e}"
+                    else:
+                        np.testing.assert_array_equal(got, want)
+            ei += 1
+    print(f"[{name} host steps] worst output rel err {worst:.2e}")
+    assert worst <= tol_for(c["dtype"])
+    final_keys = np.stack([np.stack([eng.kv(s, layer)[0].float().cpu().numpy() for layer in range(L)])
+                           for s in range(S)]).astype(F32)
+    sha = np.frombuffer(hashlib.sha256(np.ascontiguousarray(final_keys).tobytes()).digest(), np.uint8)
+    np.testing.assert_array_equal(sha, ref["final_keys_sha"], err_msg=f"{name}: final keys differ")
