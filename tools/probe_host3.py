@@ -48,3 +48,15 @@ timeit(lambda t, rec: eng.lib.skv_decode_step_host(eng._h, *args(t), int(rec), s
 timeit(lambda t, rec: eng.decode_step(qd[t % N], kd[t % N], vd[t % N], od, record=rec), "device decode_step, no sync")
 timeit(lambda t, rec: (eng.decode_step(qd[t % N], kd[t % N], vd[t % N], od, record=rec), torch.cuda.synchronize()),
        "device decode_step + sync")
+
+# order check and the wrapper's own cost
+timeit(lambda t, rec: eng.lib.skv_decode_step_host(eng._h, *args(t), int(rec), sh), "raw ctypes (again)")
+timeit(lambda t, rec: eng.decode_step_host(qh[t % N], kh[t % N], vh[t % N], oh, record=rec), "decode_step_host (again)")
+from paper_2409_09086_b200.engine import _stream_handle
+for tag, fn in (("_stream_handle()", lambda: _stream_handle()), ("qh[i] view x3", lambda: (qh[3], kh[3], vh[3])),
+                ("shape/dtype/is_cuda checks", lambda: [(t.shape != (L, S, Hq, D), t.dtype != torch.bfloat16, t.is_cuda)
+                                                        for t in (qh[0], kh[0], vh[0])])):
+    t0 = time.perf_counter()
+    for _ in range(10000):
+        fn()
+    print(f"{tag:45s} {(time.perf_counter() - t0) / 10000 * 1e6:8.2f} us")
