@@ -413,8 +413,10 @@ def run_gpu(args, rank: int, world: int):
             "h2d_bytes_per_step": int(steps * sum(t[0].numel() * t.element_size() for t in (qh, kh, vh))),
             "d2h_bytes_per_step": int(steps * oh.numel() * oh.element_size()),
             "tokens_per_step": steps,
-            "note": "one period through skv_decode_step_host (pinned host q/k/v in, f32 outputs out every token; "
-                    "one CUDA graph per token, cached per engine state) + the eviction, wall clock",
+            "note": "one period through skv_decode_step_host (pinned host q/k/v in, f32 outputs out every token -- "
+                    "copied, or read / written by the kernels through the mapped pinned buffers where the path "
+                    "allows (SKV_HOST_ZC); the layer-group copy pipeline, a per-state CUDA graph or the shallow "
+                    "path, as the engine picks) + the eviction, wall clock",
         }
 
     # the one collective outside the hot path: outputs and kept

@@ -1096,6 +1096,27 @@ int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, flo
   return SKV_OK;
 }
 
+// SKV_HOST_ZC=0: host steps always stage through device buffers and copies
+static bool use_host_zc() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SKV_HOST_ZC");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0;
+}
+
+// pinned host memory the kernels can address directly (UVA: the device
+// address of the mapping is the host address)
+static bool mapped_host(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost && at.devicePointer == p;
+}
+
 static bool pinned_host(const void* p) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -1131,21 +1152,9 @@ static int host_step_graph(skv_ctx* x, const void* q, const void* k, const void*
     if (ec) return ec;
   }
   // The kernels store the outputs through the caller's mapped pinned buffer
-  // (UVA: its device address is its host address) instead of a device
-  // staging buffer and a trailing copy node: the PCIe writes overlap the
-  // later layers (config 3: 283.6 -> 268.6 us per token).  SKV_HOST_ZC=0
-  // restores the copy node.
-  static int zc_env = -1;
-  if (zc_env < 0) {
-    const char* e = getenv("SKV_HOST_ZC");
-    zc_env = e ? atoi(e) : 1;
-  }
-  float* zc_out = nullptr;
-  if (zc_env) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, out) == cudaSuccess && at.devicePointer == out) zc_out = out;
-    cudaGetLastError();
-  }
+  // instead of a device staging buffer and a trailing copy node: the PCIe
+  // writes overlap the later layers (config 3: 283.6 -> 268.6 us per token).
+  float* zc_out = use_host_zc() && mapped_host(out) ? out : nullptr;
   float* dst = zc_out ? zc_out : x->stage_out;
   const skv_ctx::Mirror pre = x->snap();
   skv_ctx::HostGraph* hg = nullptr;
@@ -1274,18 +1283,26 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
   }
   if (x->L <= 2) {
     cudaStream_t sc = as_stream(stream);  // (ordered after the caller's work: no event)
-    // shallow models (config 0): the whole token on the caller's stream -- copies in,
-    // the layers' launches, the copy out, one synchronisation
-    SKV_CK(cudaMemcpyAsync(x->stage_q, q, qb * x->L, cudaMemcpyHostToDevice, sc));
-    SKV_CK(cudaMemcpyAsync(x->stage_k, k, kb * x->L, cudaMemcpyHostToDevice, sc));
-    SKV_CK(cudaMemcpyAsync(x->stage_v, v, kb * x->L, cudaMemcpyHostToDevice, sc));
+    // shallow models (config 0): the whole token on the caller's stream -- the
+    // layers' launches reading q/k/v and storing the outputs through the
+    // caller's mapped pinned buffers (a few KB: no copy operations), or copies
+    // in and out around them; one synchronisation
+    const bool zc = use_host_zc() && mapped_host(q) && mapped_host(k) && mapped_host(v) && mapped_host(out);
+    const char* qs = static_cast<const char*>(zc ? q : x->stage_q);
+    const char* ks = static_cast<const char*>(zc ? k : x->stage_k);
+    const char* vs = static_cast<const char*>(zc ? v : x->stage_v);
+    float* os = zc ? out : x->stage_out;
+    if (!zc) {
+      SKV_CK(cudaMemcpyAsync(x->stage_q, q, qb * x->L, cudaMemcpyHostToDevice, sc));
+      SKV_CK(cudaMemcpyAsync(x->stage_k, k, kb * x->L, cudaMemcpyHostToDevice, sc));
+      SKV_CK(cudaMemcpyAsync(x->stage_v, v, kb * x->L, cudaMemcpyHostToDevice, sc));
+    }
     for (int l = 0; l < x->L; ++l) {
-      const int rc = decode_layer_impl(x, l, static_cast<char*>(x->stage_q) + l * qb,
-                                       static_cast<char*>(x->stage_k) + l * kb, static_cast<char*>(x->stage_v) + l * kb,
-                                       nullptr, x->stage_out + l * (ob / sizeof(float)), record, sc);
+      const int rc = decode_layer_impl(x, l, qs + l * qb, ks + l * kb, vs + l * kb, nullptr,
+                                       os + l * (ob / sizeof(float)), record, sc);
       if (rc) return rc;
     }
-    SKV_CK(cudaMemcpyAsync(out, x->stage_out, ob * x->L, cudaMemcpyDeviceToHost, sc));
+    if (!zc) SKV_CK(cudaMemcpyAsync(out, x->stage_out, ob * x->L, cudaMemcpyDeviceToHost, sc));
     SKV_CK(cudaStreamSynchronize(sc));
     return check_sticky(x);
   }
