@@ -472,3 +472,19 @@ def test_project_row_matches_reference_projection():
         np.testing.assert_array_equal(got, want)
         if m == 0:
             assert out.cpu().numpy()[0] == -7.0
+
+
+def test_host_steps_with_staging_copies_match_reference():
+    """SKV_HOST_ZC=0 (staging buffers and copies instead of addressing the
+    caller's mapped pinned buffers): the golden host-step runs and the
+    host-step fuzz, in a subprocess (the switch is read once per process)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), os.path.join(root, "tests", "test_gpu_fuzz.py"),
+                        "-k", "host_steps"], env=dict(os.environ, SKV_HOST_ZC="0"), cwd=root, capture_output=True,
+                       text=True, timeout=1200)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])
+    assert " passed" in r.stdout and " failed" not in r.stdout
