@@ -392,6 +392,12 @@ def run_gpu(args, rank: int, world: int):
         torch.cuda.synchronize()
         steps = E  # one whole eviction period: the engine states (and their cached graphs) repeat
 
+        # shallow engines (config 0): speculative host steps -- each call also
+        # launches the next token behind a doorbell gate (skv_host_speculate)
+        spec = L <= 2 and not sharded and hasattr(eng, "host_speculation") and not args.no_host_spec
+        if spec:
+            eng.host_speculation(True, timeout_us=500)
+
         def host_period():
             for t in range(steps):
                 eng.decode_step_host(qh[t % T_in], kh[t % T_in], vh[t % T_in], oh, record=t >= steps - W)
@@ -413,10 +419,12 @@ def run_gpu(args, rank: int, world: int):
             "h2d_bytes_per_step": int(steps * sum(t[0].numel() * t.element_size() for t in (qh, kh, vh))),
             "d2h_bytes_per_step": int(steps * oh.numel() * oh.element_size()),
             "tokens_per_step": steps,
+            "host_speculation": bool(spec),
             "note": "one period through skv_decode_step_host (pinned host q/k/v in, f32 outputs out every token -- "
                     "copied, or read / written by the kernels through the mapped pinned buffers where the path "
                     "allows (SKV_HOST_ZC); the layer-group copy pipeline, a per-state CUDA graph or the shallow "
-                    "path, as the engine picks) + the eviction, wall clock",
+                    "path, as the engine picks; shallow engines: speculative steps, the next token launched behind a "
+                    "doorbell gate) + the eviction, wall clock",
         }
 
     # the one collective outside the hot path: outputs and kept
@@ -883,6 +891,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=128)
+    ap.add_argument("--no-host-spec", action="store_true", help="e2e leg without speculative host steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS))
     ap.add_argument("--budget", type=int, default=0, help="config 4 KV budget sweep (1024/2048/4096/8192)")

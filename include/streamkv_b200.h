@@ -118,6 +118,22 @@ int skv_decode_step(skv_ctx* ctx, const void* q_dev, const void* k_dev, const vo
 int skv_decode_step_host(skv_ctx* ctx, const void* q_host, const void* k_host, const void* v_host,
                          float* out_host, int record, void* stream);
 
+/* Speculative host steps for shallow (<= 2 layers, no RoPE) engines -- the
+ * batch-1 Session.decode_step loop (engine.py:250-289) driven token by token
+ * from the host.  With enable != 0, each skv_decode_step_host call also
+ * launches the NEXT token's kernels behind a device-side gate that waits (at
+ * most timeout_us) for the next call's doorbell in mapped pinned memory; the
+ * call copies q/k/v into the engine's mapped buffers, rings, and spins on a
+ * completion word instead of launching and synchronising.  Same kernels, same
+ * results.  Any other entry point, or a call with a different `record`,
+ * cancels the pending step first (its kernels exit without side effects);
+ * while a step is pending, a device-wide synchronisation can wait up to
+ * timeout_us.  Off by default.  No reference counterpart (a latency mode of
+ * the host-buffer step). */
+int skv_host_speculate(skv_ctx* ctx, int enable, int timeout_us);
+/* Steps served from a pending launch / pending steps cancelled or expired. */
+int skv_host_speculate_stats(skv_ctx* ctx, int64_t* hits, int64_t* misses);
+
 /* ---- eviction: Algorithm 1 + compaction -------------------------------------
  * Replaces Session._evict_layer (engine.py:310-337) for every stream:
  * inf_mllm_decide (policies.py:184-201: window_mean_scores 130-147, bias_vector

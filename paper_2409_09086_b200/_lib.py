@@ -69,6 +69,8 @@ SIGNATURES = {
     "skv_decode_layer": (_I, [_P, _I, _P, _P, _P, _P, _P, _I, _P]),
     "skv_decode_step": (_I, [_P, _P, _P, _P, _P, _I, _P]),
     "skv_decode_step_host": (_I, [_P, _P, _P, _P, _P, _I, _P]),
+    "skv_host_speculate": (_I, [_P, _I, _I]),
+    "skv_host_speculate_stats": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "skv_evict": (_I, [_P, _I, _P, _P]),
     "skv_evict_scores": (_I, [_P, _I, _P, _P]),
     "skv_evict_apply": (_I, [_P, _I, _P, _P, _P]),

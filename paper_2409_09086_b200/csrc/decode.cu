@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(Cw<G>::THREADS, (G >= 4 ? 1 : 2)) decode_kerne
   const int n = a.n_old + a.append;
   const int total = a.S * a.Hkv * a.nc;
 
+  if (a.gate) {  // speculative step: the gate grid ahead has completed and decided
+    griddep_wait();
+    if (*reinterpret_cast<const volatile int32_t*>(a.gate) != 1) return;
+  }
   if (a.tstamp && tid == 0) atomicMin(&a.tstamp[0], globaltimer());
   if (a.ctat && tid == 0) a.ctat[8 * c] = globaltimer();
   if (c == 0 && tid == 0 && a.done_self) {  // a stale flag from this slot's previous use must not leak
@@ -659,6 +663,9 @@ __global__ void __launch_bounds__(G * D) merge_kernel(const AttnArgs a) {
   constexpr int PW = D + 2;
   extern __shared__ __align__(16) float msm[];  // [G][nc] weights, [G] sums
   griddep_launch();
+  // speculative step: every decode CTA passed its griddepcontrol.wait on the
+  // gate grid before this grid could start, so the decision is final here
+  if (a.gate && *reinterpret_cast<const volatile int32_t*>(a.gate) != 1) return;
   const int sigma = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nc = a.nc;
   // wait until every chunk partial of this segment is published (decode CTAs
@@ -852,6 +859,93 @@ cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const At
     if (head_dim == 64) return dispatch_group<float, 64>(group, ctas, a, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// Gate of a speculative host step (launch_spec_gate).  The outputs of the
+// step ahead (device staging) go to the host's mapped buffer first, then the
+// completion word: the grids ahead happen-before this one and fence.sc.sys is
+// cumulative, so a host that reads `done` reads the outputs.  After the
+// decision, a GO copies the step's q/k/v from mapped host memory into device
+// staging with every thread's loads in flight at once (one PCIe round trip;
+// the decode kernels then read L2, not PCIe).
+__global__ void __launch_bounds__(256) spec_gate_kernel(SpecGate g) {
+  const int tid = threadIdx.x;
+  __shared__ int sd;
+  // launched early (programmatic dependent launch under the step ahead's
+  // merge): its outputs are complete and visible after this wait
+  griddep_wait();
+  if (g.signal_tick > 0) {
+    for (int i = tid; i < g.out_vec; i += blockDim.x) g.out_dst[i] = __ldcg(g.out_src + i);
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+      if (g.dbg) g.dbg[8 * (g.signal_tick & 63) + 2] = globaltimer();
+      g.hostw[1] = g.signal_tick;
+      __threadfence_system();
+    }
+  }
+  if (g.tick <= 0) return;  // signal only: the end of a speculation chain
+  // the gated decode grid may become resident now (its griddepcontrol.wait
+  // still waits for this grid to finish)
+  griddep_launch();
+  if (tid == 0) {
+    const unsigned long long t0 = globaltimer();
+    if (g.dbg) {
+      g.dbg[8 * (g.tick & 63) + 0] = t0;
+      g.dbg[8 * (g.tick & 63) + 4] = ~0ull;
+      g.dbg[8 * (g.tick & 63) + 5] = 0;
+    }
+    int d = 0;
+    for (;;) {
+      if (*reinterpret_cast<volatile int32_t*>(g.broken) == g.gen) { d = 2; break; }
+      const int b = g.hostw[0];
+      if (b == g.tick) { d = 1; break; }
+      if (b < 0 && -b <= g.tick) { d = 2; break; }
+      if ((long long)(globaltimer() - t0) > g.timeout_ns) { d = 3; break; }
+    }
+    *reinterpret_cast<volatile int32_t*>(g.gate) = d;
+    if (g.dbg) g.dbg[8 * (g.tick & 63) + 1] = globaltimer();
+    if (d == 3) {
+      *reinterpret_cast<volatile int32_t*>(g.broken) = g.gen;
+      __threadfence_system();
+      g.hostw[2] = g.tick;
+    }
+    sd = d;
+  }
+  __syncthreads();
+  if (sd == 1) {  // every load in flight before the first store: one PCIe round trip
+    constexpr int U = 8;
+    for (int i0 = 0; i0 < g.in_vec; i0 += U * 256) {
+      int4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * 256 + tid;
+        if (i < g.in_vec) r[u] = __ldcv(g.in_src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * 256 + tid;
+        if (i < g.in_vec) g.in_dst[i] = r[u];
+      }
+    }
+  }
+  if (g.dbg) {
+    __syncthreads();
+    if (tid == 0) g.dbg[8 * (g.tick & 63) + 3] = globaltimer();
+  }
+}
+
+cudaError_t launch_spec_gate(const SpecGate& g, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.stream = st;
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, spec_gate_kernel, g);
 }
 
 // One row per stream, four columns per thread (fold_vec4).

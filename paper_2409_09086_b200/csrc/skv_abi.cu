@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -239,6 +241,32 @@ struct skv_ctx {
     float* zc_out = nullptr;  // outputs stored straight into this mapped host buffer (no copy node)
   };
   std::vector<HostGraph> hgraphs;
+  // speculative host steps (skv_host_speculate): the next token's gate +
+  // decode + merge are launched on `st` before the host has its q/k/v; the
+  // gate waits for the host's doorbell, so a token costs a PCIe round trip
+  // instead of launches plus a stream synchronisation
+  struct Spec {
+    int on = 0;
+    long long timeout_ns = 0;
+    volatile int32_t* hostw = nullptr;  // mapped pinned: [0] bell, [1] done, [2] expired
+    int32_t* gate = nullptr;            // device [64] decisions, one per step
+    int32_t* broken = nullptr;          // device: generation whose chain expired
+    char* io = nullptr;                 // mapped pinned: two (q | k | v | out) sets, by tick parity
+    char* dio = nullptr;                // device staging: one (q | k | v | out) set
+    size_t set_bytes = 0, k_off = 0, v_off = 0, o_off = 0;
+    cudaStream_t st = nullptr;
+    int tick = 0, gen = 0;
+    // the pending (launched, not yet rung) step
+    bool pending = false;
+    int p_tick = 0, p_record = 0;
+    Mirror p_mirror;  // host state before the pending step (restored on cancel)
+    int p_launch_seq = 0, p_last_layer = -1, p_tcount = 0;
+    int64_t p_launches = 0;
+    const char* p_last_kernel = "";
+    bool p_chain = false;
+    unsigned long long* dbg = nullptr;  // probe (SKV_SPEC_PROF): gate start / go / signalled [64][4]
+    int64_t hits = 0, misses = 0;  // steps served from a pending launch / cancelled or expired
+  } spec;
 
   template <typename P>
   cudaError_t alloc(P** p, size_t bytes) {
@@ -290,6 +318,15 @@ static int check_sticky(skv_ctx* x) {
 }
 
 extern "C" {
+
+static int spec_cancel(skv_ctx* x);
+// every entry point but skv_decode_step_host first retires a pending
+// speculative step (its host state would otherwise show through)
+#define SPEC_CANCEL(x)                                          \
+  do {                                                          \
+    const int _src = spec_cancel(const_cast<skv_ctx*>(x));      \
+    if (_src) return _src;                                      \
+  } while (0)
 
 const char* skv_last_error(void) { return g_err.c_str(); }
 int skv_version(void) { return 1; }
@@ -452,7 +489,11 @@ int skv_create(const skv_config* cfg, skv_ctx** out) {
 
 int skv_destroy(skv_ctx* x) {
   if (!x) return SKV_OK;
+  spec_cancel(x);
   cudaDeviceSynchronize();
+  if (x->spec.st) cudaStreamDestroy(x->spec.st);
+  if (x->spec.hostw) cudaFreeHost(const_cast<int32_t*>(x->spec.hostw));
+  if (x->spec.io) cudaFreeHost(x->spec.io);
   for (auto& e : x->hgraphs) {
     cudaGraphExecDestroy(e.exec);
     cudaGraphDestroy(e.graph);
@@ -472,9 +513,14 @@ int skv_destroy(skv_ctx* x) {
 }
 
 int64_t skv_device_bytes(const skv_ctx* x) { return x ? x->device_bytes : 0; }
-int64_t skv_kernel_launches(const skv_ctx* x) { return x ? x->launches : 0; }
+int64_t skv_kernel_launches(const skv_ctx* x) {
+  if (!x) return 0;
+  spec_cancel(const_cast<skv_ctx*>(x));
+  return x->launches;
+}
 
 int skv_timing(skv_ctx* x, int enable) {
+  SPEC_CANCEL(x);
   if (!x) return fail(SKV_EINVAL, "null argument");
   if (enable) {
     if (!x->tbuf) {
@@ -497,15 +543,21 @@ int skv_timing(skv_ctx* x, int enable) {
   return SKV_OK;
 }
 
-const char* skv_last_decode_kernel(const skv_ctx* x) { return x ? x->last_kernel : ""; }
+const char* skv_last_decode_kernel(const skv_ctx* x) {
+  if (!x) return "";
+  spec_cancel(const_cast<skv_ctx*>(x));
+  return x->last_kernel;
+}
 
 int skv_layers_timeline(skv_ctx* x, uint64_t* buf_dev) {
+  SPEC_CANCEL(x);
   if (!x) return fail(SKV_EINVAL, "null argument");
   x->lay_tl = reinterpret_cast<unsigned long long*>(buf_dev);
   return SKV_OK;
 }
 
 int skv_timing_cta(skv_ctx* x, int slot, uint64_t* out) {
+  SPEC_CANCEL(x);
   if (!x || !out || !x->cbuf || slot < 0 || slot >= 64) return fail(SKV_EINVAL, "no per-CTA timing");
   SKV_CK(cudaDeviceSynchronize());
   SKV_CK(cudaMemcpy(out, x->cbuf + (size_t)slot * (x->max_ctas + 1) * 8, (size_t)(x->max_ctas + 1) * 8 * sizeof(uint64_t),
@@ -514,6 +566,7 @@ int skv_timing_cta(skv_ctx* x, int slot, uint64_t* out) {
 }
 
 int skv_timing_read(skv_ctx* x, uint64_t* out, int max_pairs) {
+  SPEC_CANCEL(x);
   if (!x || !out) return fail(SKV_EINVAL, "null argument");
   if (!x->tbuf) return 0;
   const int n = std::min(std::min(x->tcount, 8192), max_pairs);
@@ -819,6 +872,7 @@ static int flush_pending(skv_ctx* x, int layer, cudaStream_t st) {
 
 int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const void* v, int C, int modality,
                       float* out, void* stream) {
+  SPEC_CANCEL(x);
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
   if (layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
   if (x->cfg.dtype != SKV_DTYPE_BF16 || x->D != 128) return fail(SKV_EINVAL, "chunked prefill needs bf16, head_dim 128");
@@ -931,6 +985,7 @@ int skv_prefill_chunk(skv_ctx* x, int layer, const void* q, const void* k, const
 
 int skv_decode_layer(skv_ctx* x, int layer, const void* q, const void* k, const void* v,
                      const int64_t* positions_host, float* out, int record, void* stream) {
+  SPEC_CANCEL(x);
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
   if (layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "layer out of range");
   cudaStream_t st = as_stream(stream);
@@ -1074,6 +1129,7 @@ static int decode_step_layers(skv_ctx* x, const void* q, const void* k, const vo
 }
 
 int skv_decode_step(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record, void* stream) {
+  SPEC_CANCEL(x);
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
   cudaStream_t st = as_stream(stream);
   if (layers_eligible(x)) {
@@ -1255,6 +1311,306 @@ static int host_step_graph(skv_ctx* x, const void* q, const void* k, const void*
   return 1;
 }
 
+// ---------------------------------------------------------------------------
+// Speculative host steps (skv_host_speculate).  Shallow engines (config 0) at
+// batch 1 are bound by the host: two launches and a stream synchronisation
+// cost more than the step.  Instead, the next token's launches wait on the
+// device behind a one-thread gate kernel polling a doorbell in mapped pinned
+// memory; a call copies the caller's q/k/v into the engine's mapped input set,
+// rings the bell, launches the token after it (whose gate first reports this
+// one's completion), spins on the done word and copies the outputs out.  The
+// launches are planned with the host state advanced as if the call had come
+// with the same `record` flag; any other call (a different flag, or any other
+// entry point) cancels the pending step: its kernels exit before touching any
+// state and the host state goes back.  A gate that is not rung within the
+// timeout expires the same way, so nothing waits on the host for long.
+struct SpecSnap {
+  skv_ctx::Mirror m;
+  int launch_seq, last_layer, tcount;
+  int64_t launches;
+  const char* last_kernel;
+  bool chain;
+};
+static SpecSnap spec_snap(const skv_ctx* x) {
+  return SpecSnap{x->snap(), x->launch_seq, x->last_layer, x->tcount, x->launches, x->last_kernel, x->layers_chain};
+}
+static void spec_back(skv_ctx* x, const SpecSnap& s) {
+  x->restore(s.m);
+  x->launch_seq = s.launch_seq;
+  x->last_layer = s.last_layer;
+  x->tcount = s.tcount;
+  x->launches = s.launches;
+  x->last_kernel = s.last_kernel;
+  x->layers_chain = s.chain;
+}
+// host state before the pending step
+static void spec_set_before(skv_ctx* x, const SpecSnap& b) {
+  auto& p = x->spec;
+  p.p_mirror = b.m;
+  p.p_launch_seq = b.launch_seq;
+  p.p_last_layer = b.last_layer;
+  p.p_tcount = b.tcount;
+  p.p_launches = b.launches;
+  p.p_last_kernel = b.last_kernel;
+  p.p_chain = b.chain;
+}
+static SpecSnap spec_before(const skv_ctx* x) {
+  const auto& p = x->spec;
+  return SpecSnap{p.p_mirror, p.p_launch_seq, p.p_last_layer, p.p_tcount, p.p_launches, p.p_last_kernel, p.p_chain};
+}
+
+// the pending step's kernels are drained (they exit without side effects),
+// the bell is cleared for the next chain, the host state goes back
+static int spec_drain(skv_ctx* x, int bell) {
+  auto& p = x->spec;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  p.hostw[0] = bell;
+  p.pending = false;
+  p.misses++;
+  spec_back(x, spec_before(x));
+  SKV_CK(cudaStreamSynchronize(p.st));
+  p.hostw[0] = 0;
+  p.gen++;
+  return SKV_OK;
+}
+
+static int spec_cancel(skv_ctx* x) {
+  if (!x || !x->spec.pending) return SKV_OK;
+  return spec_drain(x, -x->spec.p_tick);
+}
+
+static bool spec_room(const skv_ctx* x) {
+  for (int l = 0; l < x->L; ++l)
+    if (x->ragged[l] || x->n[l] + 1 > x->cap) return false;
+  return true;
+}
+
+static SpecGate spec_gate_args(skv_ctx* x, int signal_tick, int tick, int32_t* gate) {
+  auto& p = x->spec;
+  SpecGate g{};
+  g.hostw = p.hostw;
+  g.gate = gate;
+  g.broken = p.broken;
+  g.signal_tick = signal_tick;
+  g.tick = tick;
+  g.gen = p.gen;
+  g.timeout_ns = p.timeout_ns;
+  g.in_src = reinterpret_cast<const int4*>(p.io + (size_t)(tick & 1) * p.set_bytes);
+  g.in_dst = reinterpret_cast<int4*>(p.dio);
+  g.in_vec = (int)(p.o_off / 16);
+  // (measured: the merge storing the outputs into mapped memory itself is
+  // slower -- 7.2 vs 4.7 us from the last decode CTA to the done word)
+  g.out_src = reinterpret_cast<const int4*>(p.dio + p.o_off);
+  g.out_dst = reinterpret_cast<int4*>(p.io + (size_t)(signal_tick & 1) * p.set_bytes + p.o_off);
+  g.out_vec = (int)((p.set_bytes - p.o_off) / 16);
+  g.dbg = p.dbg;
+  return g;
+}
+
+// Gate + every layer of step `tick` on spec.st, planned from the current host
+// state (advanced on success).  Returns 1 launched, 0 not eligible (nothing
+// left enqueued), < 0 error.
+static int spec_launch(skv_ctx* x, int record, int signal_tick) {
+  auto& p = x->spec;
+  const int64_t qb = (int64_t)x->S * x->Hq * x->D * x->elt;
+  const int64_t kb = (int64_t)x->S * x->Hkv * x->D * x->elt;
+  const int64_t ob = (int64_t)x->S * x->Hq * x->D;
+  const int tick = ++p.tick;
+  const SpecSnap before = spec_snap(x);
+  int32_t* gate = p.gate + (tick % 64);
+  cudaError_t e = launch_spec_gate(spec_gate_args(x, signal_tick, tick, gate), p.st);
+  if (e != cudaSuccess) return cuda_fail(e, "speculative gate launch");
+  x->launches++;
+  char* set = p.dio;
+  for (int l = 0; l < x->L; ++l) {
+    DecodePlan pl;
+    int rc = prepare_layer(x, l, set + l * qb, set + p.k_off + l * kb, set + p.v_off + l * kb, nullptr,
+                           reinterpret_cast<float*>(set + p.o_off) + l * ob, record, p.st, pl);
+    if (rc == SKV_OK && (pl.tc || pl.tcd)) {  // tensor-core plans are not gated: not eligible
+      p.on = 0;
+      rc = 1;
+    }
+    if (rc == SKV_OK) {
+      pl.a.gate = gate;
+      if (p.dbg) pl.a.tstamp = p.dbg + 8 * (tick & 63) + 4;
+      e = launch_decode(x->cfg.dtype, x->D, x->G, pl.ctas, pl.a, p.st);
+      if (e != cudaSuccess) rc = cuda_fail(e, "speculative decode launch");
+    }
+    if (rc != SKV_OK) {  // the launched part is cancelled and drained
+      spec_set_before(x, before);
+      p.pending = true;
+      p.p_tick = tick;
+      const int drc = spec_drain(x, -tick);
+      p.misses--;
+      if (drc) return drc;
+      return rc < 0 ? rc : 0;
+    }
+    x->launches += 2;
+    x->last_kernel = "decode_kernel";
+    x->last_layer = l;
+    x->layers_chain = false;
+    commit_layer(x, l, pl);
+  }
+  spec_set_before(x, before);
+  p.pending = true;
+  p.p_tick = tick;
+  p.p_record = record;
+  return 1;
+}
+
+// Returns 1 when the step was served (outputs in `out`), 0 when the caller
+// should run the regular path, < 0 on error.
+static int spec_step(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
+                     cudaStream_t caller) {
+  auto& p = x->spec;
+  const int64_t qb = (int64_t)x->S * x->Hq * x->D * x->elt * x->L;
+  const int64_t kb = (int64_t)x->S * x->Hkv * x->D * x->elt * x->L;
+  const int64_t ob = (int64_t)x->S * x->Hq * x->D * sizeof(float) * x->L;
+  if (p.pending && p.p_record != record) {
+    const int rc = spec_cancel(x);
+    if (rc) return rc;
+  }
+  if (!p.pending) {
+    if (!spec_room(x)) return 0;
+    // the first step of a chain is ordered after the caller's work
+    SKV_CK(cudaEventRecord(x->ev_entry, caller));
+    SKV_CK(cudaStreamWaitEvent(p.st, x->ev_entry, 0));
+    const int rc = spec_launch(x, record, 0);
+    if (rc <= 0) return rc;
+  }
+  static const bool prof = getenv("SKV_SPEC_PROF") != nullptr;  // probe: per-phase host times
+  static double acc[4] = {0, 0, 0, 0};
+  static int64_t cnt = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto p0 = now();
+  const int t = p.p_tick;
+  const SpecSnap before_t = spec_before(x);
+  char* set = p.io + (size_t)(t & 1) * p.set_bytes;
+  std::memcpy(set, q, qb);
+  std::memcpy(set + p.k_off, k, kb);
+  std::memcpy(set + p.v_off, v, kb);
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  p.hostw[0] = t;  // ring: the gate releases step t
+  p.pending = false;
+  const auto p1 = now();
+  // the next step goes in under this one's device time; its gate reports t
+  int rc = spec_room(x) ? spec_launch(x, record, t) : 0;
+  if (rc < 0) return rc;
+  if (rc == 0) {
+    cudaError_t e = launch_spec_gate(spec_gate_args(x, t, 0, p.gate + ((t + 1) % 64)), p.st);
+    if (e != cudaSuccess) return cuda_fail(e, "speculative gate launch");
+    x->launches++;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto p2 = t0;
+  for (uint32_t spin = 1;; ++spin) {
+    if (p.hostw[1] == t) break;
+    if ((spin & 4095) == 0) {
+      cudaError_t e = cudaStreamQuery(p.st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_fail(e, "speculative step");
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
+        return fail(SKV_ECUDA, "speculative step did not complete within 10 s");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  if (p.hostw[2] == t) {
+    // step t expired before the bell: nothing of it ran; the step after it
+    // (if launched) is cancelled by the broken chain
+    if (p.pending) {
+      const int drc = spec_drain(x, -p.p_tick);
+      if (drc) return drc;
+    } else {
+      SKV_CK(cudaStreamSynchronize(p.st));
+      p.hostw[0] = 0;
+      p.gen++;
+      p.misses++;
+    }
+    spec_back(x, before_t);
+    return 0;
+  }
+  std::memcpy(out, set + p.o_off, ob);
+  p.hits++;
+  if (prof) {
+    const auto p3 = now();
+    acc[0] += std::chrono::duration<double, std::micro>(p1 - p0).count();
+    acc[1] += std::chrono::duration<double, std::micro>(p2 - p1).count();
+    acc[2] += std::chrono::duration<double, std::micro>(p3 - p2).count();
+    if (p.dbg && cnt % 2048 == 2047) {  // the last 64 ticks' device timeline (device memory: no PCIe skew)
+      std::vector<unsigned long long> h(64 * 8);
+      cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+      double d[5] = {0, 0, 0, 0, 0};
+      int m = 0;
+      for (int i = 0; i < 64; ++i) {
+        const unsigned long long* d0 = h.data() + 8 * i;
+        if (!d0[2] || !d0[5] || d0[2] < d0[5] || d0[4] < d0[3]) continue;
+        d[0] += (double)(d0[3] - d0[1]) * 1e-3;  // go -> inputs staged
+        d[1] += (double)(d0[4] - d0[3]) * 1e-3;  // -> first decode CTA
+        d[2] += (double)(d0[5] - d0[4]) * 1e-3;  // decode span
+        d[3] += (double)(d0[2] - d0[5]) * 1e-3;  // last decode CTA -> signalled (merge, gate, copy out)
+        d[4] += (double)(d0[2] - d0[1]) * 1e-3;
+        ++m;
+      }
+      if (m)
+        fprintf(stderr, "device (%d ticks): go->staged %.2f, ->decode start %.2f, decode %.2f, ->signal %.2f, go->signal %.2f us\n",
+                m, d[0] / m, d[1] / m, d[2] / m, d[3] / m, d[4] / m);
+    }
+    if (++cnt % 2048 == 0)
+      fprintf(stderr, "spec step: copy+ring %.2f us, launch next %.2f us, wait+copy out %.2f us; device go->signal %.2f us\n",
+              acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt);
+  }
+  return 1;
+}
+
+int skv_host_speculate(skv_ctx* x, int enable, int timeout_us) {
+  if (!x) return fail(SKV_EINVAL, "null context");
+  SPEC_CANCEL(x);
+  auto& p = x->spec;
+  if (!enable) {
+    p.on = 0;
+    return SKV_OK;
+  }
+  if (timeout_us <= 0) return fail(SKV_EINVAL, "timeout_us must be > 0");
+  if (x->L > 2 || x->cfg.rope_mode != SKV_ROPE_NONE)
+    return fail(SKV_EINVAL, "speculative host steps serve shallow (<= 2 layers) engines without RoPE");
+  if (!p.hostw) {
+    void* hw = nullptr;
+    SKV_CK(cudaHostAlloc(&hw, 64, cudaHostAllocMapped));
+    std::memset(hw, 0, 64);
+    p.hostw = static_cast<volatile int32_t*>(hw);
+    cudaError_t e = x->alloc(&p.gate, 64 * sizeof(int32_t));
+    if (e == cudaSuccess) e = x->alloc(&p.broken, sizeof(int32_t));
+    if (e != cudaSuccess) return cuda_fail(e, "speculation state");
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t qb = (size_t)x->S * x->Hq * x->D * x->elt * x->L;
+    const size_t kb = (size_t)x->S * x->Hkv * x->D * x->elt * x->L;
+    const size_t ob = (size_t)x->S * x->Hq * x->D * sizeof(float) * x->L;
+    p.k_off = up(qb);
+    p.v_off = p.k_off + up(kb);
+    p.o_off = p.v_off + up(kb);
+    p.set_bytes = p.o_off + up(ob);
+    void* io = nullptr;
+    SKV_CK(cudaHostAlloc(&io, 2 * p.set_bytes, cudaHostAllocMapped));
+    std::memset(io, 0, 2 * p.set_bytes);
+    p.io = static_cast<char*>(io);
+    if (cudaError_t e2 = x->alloc(&p.dio, p.set_bytes)) return cuda_fail(e2, "speculation staging");
+    SKV_CK(cudaStreamCreateWithFlags(&p.st, cudaStreamNonBlocking));
+    p.gen = 1;
+    if (getenv("SKV_SPEC_PROF")) {
+      if (cudaError_t e3 = x->alloc(&p.dbg, 64 * 8 * sizeof(unsigned long long))) return cuda_fail(e3, "probe");
+    }
+  }
+  p.timeout_ns = (long long)timeout_us * 1000;
+  p.on = 1;
+  return SKV_OK;
+}
+
+int skv_host_speculate_stats(skv_ctx* x, int64_t* hits, int64_t* misses) {
+  if (!x) return fail(SKV_EINVAL, "null context");
+  if (hits) *hits = x->spec.hits;
+  if (misses) *misses = x->spec.misses;
+  return SKV_OK;
+}
+
 int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v, float* out, int record,
                          void* stream) {
   if (!x || !q || !k || !v || !out) return fail(SKV_EINVAL, "null argument");
@@ -1280,6 +1636,13 @@ int skv_decode_step_host(skv_ctx* x, const void* q, const void* k, const void* v
     chk(cudaEventCreateWithFlags(&x->ev_done, cudaEventDisableTiming));
     chk(cudaEventCreateWithFlags(&x->ev_entry, cudaEventDisableTiming));
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline setup");
+  }
+  if (x->spec.on && x->L <= 2 && !x->timing) {
+    const int rc = spec_step(x, q, k, v, out, record, as_stream(stream));
+    if (rc < 0) return rc;
+    if (rc == 1) return check_sticky(x);
+  } else {
+    SPEC_CANCEL(x);
   }
   if (x->L <= 2) {
     cudaStream_t sc = as_stream(stream);  // (ordered after the caller's work: no event)
@@ -1609,15 +1972,18 @@ static int evict_common(skv_ctx* x, int layer, int32_t* kept_dev, void* stream, 
 }
 
 int skv_evict(skv_ctx* x, int layer, int32_t* kept_dev, void* stream) {
+  SPEC_CANCEL(x);
   return evict_common(x, layer, kept_dev, stream, 0, nullptr);
 }
 
 int skv_evict_scores(skv_ctx* x, int layer, float* scores_dev, void* stream) {
+  SPEC_CANCEL(x);
   if (!scores_dev) return fail(SKV_EINVAL, "null argument");
   return evict_common(x, layer, nullptr, stream, 1, scores_dev);
 }
 
 int skv_evict_apply(skv_ctx* x, int layer, const float* scores_dev, int32_t* kept_dev, void* stream) {
+  SPEC_CANCEL(x);
   if (!scores_dev) return fail(SKV_EINVAL, "null argument");
   return evict_common(x, layer, kept_dev, stream, 2, const_cast<float*>(scores_dev));
 }
@@ -1625,11 +1991,13 @@ int skv_evict_apply(skv_ctx* x, int layer, const float* scores_dev, int32_t* kep
 // ------------------------------------------------------------ state access --
 
 int skv_length(const skv_ctx* x, int stream, int layer) {
+  SPEC_CANCEL(x);
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   return x->ragged[layer] ? std::max(0, x->sn[(size_t)stream * x->L + layer]) : x->n[layer];
 }
 
 int skv_kv_view(skv_ctx* x, int stream, int layer, void** k, void** v) {
+  SPEC_CANCEL(x);
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   const int64_t off = ((int64_t)stream * x->L + layer) * x->kv_layer_stride() * x->elt;
   // RoPE engines: the raw keys (KvCache.keys(), cache.py:93-96)
@@ -1667,6 +2035,7 @@ static int host_perm(const skv_ctx* x, int64_t sl, int n, std::vector<int32_t>& 
 }
 
 int skv_positions(skv_ctx* x, int stream, int layer, int64_t* out, int cap) {
+  SPEC_CANCEL(x);
   if (!x || !out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   int nn, mm, hh;
   int rc = stream_state(x, stream, layer, &nn, &mm, &hh);
@@ -1680,6 +2049,7 @@ int skv_positions(skv_ctx* x, int stream, int layer, int64_t* out, int cap) {
 }
 
 int skv_window_rows(skv_ctx* x, int stream, int layer, float* rows_host, int32_t* lens_host) {
+  SPEC_CANCEL(x);
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   int nn, count, head;
   int rc = stream_state(x, stream, layer, &nn, &count, &head);
@@ -1712,6 +2082,7 @@ int skv_window_rows(skv_ctx* x, int stream, int layer, float* rows_host, int32_t
 int skv_state_dump(skv_ctx* x, int stream, int layer, int* n_out, int* m_out, void* k_host, void* v_host,
                    int64_t* pos_host, int8_t* modality_host, int32_t* round_host, float* rows_host,
                    int32_t* lens_host) {
+  SPEC_CANCEL(x);
   if (!x || !n_out || !m_out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
     return fail(SKV_EINVAL, "out of range");
   int n, m, head;
@@ -1770,6 +2141,7 @@ int skv_state_dump(skv_ctx* x, int stream, int layer, int* n_out, int* m_out, vo
 
 int skv_window_view(skv_ctx* x, int stream, int layer, float** rows_dev, int32_t** lens_dev, int* ring_head,
                     int* count) {
+  SPEC_CANCEL(x);
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   int n, m, head;
   int rc = stream_state(x, stream, layer, &n, &m, &head);
@@ -1787,6 +2159,7 @@ int skv_window_view(skv_ctx* x, int stream, int layer, float** rows_dev, int32_t
 }
 
 int skv_positions_view(skv_ctx* x, int stream, int layer, int64_t** pos_dev) {
+  SPEC_CANCEL(x);
   if (!x || !pos_dev || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
     return fail(SKV_EINVAL, "out of range");
   *pos_dev = x->pos + ((int64_t)stream * x->L + layer) * x->cap;
@@ -1794,6 +2167,7 @@ int skv_positions_view(skv_ctx* x, int stream, int layer, int64_t** pos_dev) {
 }
 
 int skv_slot_map(skv_ctx* x, int stream, int layer, int32_t** perm_dev) {
+  SPEC_CANCEL(x);
   if (!x || !perm_dev || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L)
     return fail(SKV_EINVAL, "out of range");
   *perm_dev = x->perm ? x->perm + ((int64_t)stream * x->L + layer) * x->cap : nullptr;
@@ -1801,6 +2175,7 @@ int skv_slot_map(skv_ctx* x, int stream, int layer, int32_t** perm_dev) {
 }
 
 int skv_moved_rows(skv_ctx* x, int32_t* out_host) {
+  SPEC_CANCEL(x);
   if (!x || !out_host) return fail(SKV_EINVAL, "null argument");
   if (!x->mcount) return fail(SKV_ESTATE, "no slot map: this engine compacts densely");
   SKV_CK(cudaDeviceSynchronize());
@@ -1809,12 +2184,14 @@ int skv_moved_rows(skv_ctx* x, int32_t* out_host) {
 }
 
 int skv_sync(skv_ctx* x, void* stream) {
+  SPEC_CANCEL(x);
   if (!x) return fail(SKV_EINVAL, "null argument");
   SKV_CK(cudaStreamSynchronize(as_stream(stream)));
   return check_sticky(x);
 }
 
 int skv_last_scores(skv_ctx* x, int stream, int layer, float* out, int cap) {
+  SPEC_CANCEL(x);
   if (!x || !out || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   SKV_CK(cudaDeviceSynchronize());
   SKV_CK(cudaMemcpy(out, x->scores + ((int64_t)stream * x->L + layer) * x->cap,
@@ -1824,6 +2201,7 @@ int skv_last_scores(skv_ctx* x, int stream, int layer, float* out, int cap) {
 
 int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_host, const void* v_host,
                      const int64_t* pos_host, int m, const float* rows_host, const int32_t* lens_host) {
+  SPEC_CANCEL(x);
   if (!x || stream < 0 || stream >= x->S || layer < 0 || layer >= x->L) return fail(SKV_EINVAL, "out of range");
   if (n < 0 || n > x->cap) return fail(SKV_EINVAL, "n exceeds capacity");
   if (m < 0 || m > x->W) return fail(SKV_EINVAL, "too many window rows");
@@ -1893,6 +2271,7 @@ int skv_state_inject(skv_ctx* x, int stream, int layer, int n, const void* k_hos
 // ------------------------------------------------------------------ graphs --
 
 int skv_capture_begin(skv_ctx* x, void* stream) {
+  SPEC_CANCEL(x);
   if (!x) return fail(SKV_EINVAL, "null argument");
   // release the previous graph before capturing: destroying graph objects is not
   // permitted while a thread-local capture is active
@@ -1911,6 +2290,7 @@ int skv_capture_begin(skv_ctx* x, void* stream) {
 }
 
 int skv_capture_end(skv_ctx* x, void* stream) {
+  SPEC_CANCEL(x);
   if (!x) return fail(SKV_EINVAL, "null argument");
   x->gend = x->snap();
   x->restore(x->gbegin);  // nothing has executed yet
@@ -1920,6 +2300,7 @@ int skv_capture_end(skv_ctx* x, void* stream) {
 }
 
 int skv_graph_launch(skv_ctx* x, void* stream) {
+  SPEC_CANCEL(x);
   if (!x || !x->exec) return fail(SKV_ESTATE, "no captured graph");
   if (!(x->snap() == x->gbegin))
     return fail(SKV_ESTATE, "graph replay refused: engine state differs from the state at capture begin");

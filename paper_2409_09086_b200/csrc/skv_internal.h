@@ -104,6 +104,10 @@ struct AttnArgs {
   unsigned long long* tstamp;  // optional [2]: min CTA start / max CTA end (%globaltimer ns)
   unsigned long long* ctat;    // optional [P][8]: per-CTA timeline (instrumentation)
   unsigned long long* mstamp;  // optional [8]: merge timeline (instrumentation)
+  // speculative host steps (skv_host_speculate): this launch runs only if the
+  // gate kernel ahead of it on the stream wrote 1 here (else both kernels exit
+  // before touching any state)
+  const int32_t* gate;
 };
 
 cudaError_t launch_decode(int dtype, int head_dim, int group, int ctas, const AttnArgs& a, cudaStream_t st);
@@ -139,6 +143,28 @@ cudaError_t launch_decode_tcd(int group, int ctas, const AttnArgs& a, cudaStream
 // static-schedule GQA launches (bf16, D = 128, group 4 or 8, chunks <= 4 tiles) on mma.sync
 cudaError_t launch_decode_tc(int group, int ctas, const AttnArgs& a, cudaStream_t st);
 // the segment merge alone (PDL), after a decode launch
+// Speculative host steps (skv_host_speculate): the gate kernel first copies
+// the step ahead's outputs (out_src, device) to the host (out_dst, mapped) and
+// signals `signal_tick` as done, then one thread waits for the host to ring
+// `tick` (GO), cancel it, or `timeout_ns` to pass, and writes the decision to
+// *gate (1 go, 2 cancelled, 3 expired); a GO copies the step's inputs from
+// in_src (mapped) to in_dst (device).  hostw (mapped pinned): [0] bell,
+// [1] done, [2] expired; *broken (device) = generation whose chain expired.
+struct SpecGate {
+  volatile int32_t* hostw;
+  int32_t* gate;
+  int32_t* broken;
+  int signal_tick, tick, gen;
+  long long timeout_ns;
+  const int4* in_src;
+  int4* in_dst;
+  int in_vec;
+  const int4* out_src;
+  int4* out_dst;
+  int out_vec;
+  unsigned long long* dbg;  // probe: [64][4] gate start / go / signalled
+};
+cudaError_t launch_spec_gate(const SpecGate& g, cudaStream_t st);
 cudaError_t launch_merge(int head_dim, int group, const AttnArgs& a, cudaStream_t st);
 int decode_ctas_per_sm(int dtype, int head_dim, int group);
 int decode_tile_tokens();

@@ -212,6 +212,21 @@ class StreamEngine:
             check(rc)
         return out
 
+    def host_speculation(self, enable: bool = True, timeout_us: int = 500):
+        """Speculative host steps for shallow engines (<= 2 layers, no RoPE):
+        each decode_step_host call also launches the next token behind a
+        device-side doorbell gate, so the next call pays a PCIe round trip
+        instead of launches plus a synchronisation.  Same kernels and results;
+        any other engine call cancels the pending step.  While one is pending
+        a device-wide synchronisation may wait up to ``timeout_us``."""
+        check(self.lib.skv_host_speculate(self._h, 1 if enable else 0, int(timeout_us)))
+
+    def host_speculation_stats(self):
+        """(steps served from a pending launch, pending steps cancelled or expired)."""
+        h, m = ctypes.c_int64(0), ctypes.c_int64(0)
+        check(self.lib.skv_host_speculate_stats(self._h, ctypes.byref(h), ctypes.byref(m)))
+        return h.value, m.value
+
     # --------------------------------------------------------------- evict --
     def evict(self, layer: int = -1, kept: Optional[torch.Tensor] = None):
         """Algorithm 1 + compaction for every stream of ``layer`` (-1: all layers).

@@ -626,16 +626,24 @@ def test_engine_chunks_match_reference_golden(name):
     np.testing.assert_array_equal(sha, ref["final_keys_sha"], err_msg=f"{name}: final keys differ")
 
 
+@pytest.mark.parametrize("spec", [False, True], ids=["plain", "speculative"])
 @pytest.mark.parametrize("name", list(CASES))
-def test_host_steps_match_reference_golden(name):
+def test_host_steps_match_reference_golden(name, spec):
     """Every golden case through decode_step_host (the e2e entry point: all
     layers of a token from pinned host buffers, outputs back to the host)
-    against the reference's own outputs, kept sets and final keys."""
+    against the reference's own outputs, kept sets and final keys; shallow
+    cases also with speculative host steps (each call launches the next
+    token behind a doorbell gate; the length query and the eviction between
+    periods cancel it)."""
     import hashlib
 
     c = CASES[name]
     ref = dict(np.load(os.path.join(GOLD, f"ref_{name}.npz")))
     eng = _engine(c)
+    if spec:
+        if c["L"] > 2 or c.get("rope"):
+            pytest.skip("speculative host steps serve shallow engines without RoPE")
+        eng.host_speculation(True, timeout_us=2000)
     S, L, Hq, Hkv, D = c["S"], c["L"], c["Hq"], c["Hkv"], c["D"]
     dt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
     q_all, k_all, v_all = case_inputs(name)
@@ -667,6 +675,10 @@ def test_host_steps_match_reference_golden(name):
                         np.testing.assert_array_equal(got, want)
             ei += 1
     print(f"[{name} host steps] worst output rel err {worst:.2e}")
+    if spec:
+        hits, misses = eng.host_speculation_stats()
+        if c["dtype"] == "f32":  # (bf16 GQA plans may run on the tensor cores: not gated, regular path)
+            assert hits >= c["T"] // 2, (hits, misses)
     assert worst <= tol_for(c["dtype"])
     final_keys = np.stack([np.stack([eng.kv(s, layer)[0].float().cpu().numpy() for layer in range(L)])
                            for s in range(S)]).astype(F32)
