@@ -108,6 +108,13 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        # nvidia-smi needs a few hundred ms to its first sample: wait for it,
+        # so a timed region shorter than the 200 ms period (config 0) is still
+        # bracketed by samples (this one and the one stop() waits for)
+        deadline = time.time() + 5.0
+        while not self.lines and time.time() < deadline and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.n0 = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -116,6 +123,9 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        deadline = time.time() + 0.5  # one sample after the region too
+        while len(self.lines) <= getattr(self, "n0", 0) and time.time() < deadline and self.proc.poll() is None:
+            time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
